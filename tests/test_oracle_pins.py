@@ -1,0 +1,429 @@
+"""Pins for the CPU oracle (runs without a GPU).
+
+Each test checks the oracle against something other than itself: values the
+paper prints (tests/golden/, with citations), closed forms, the independent
+matrix-based route (oracle/fullmatrix.py, n <= 6), a library routine
+(numpy.fft) or invariants.  Chosen so that a dropped term, a wrong sign or
+index, or a transposed operand in oracle.c fails at least one of them.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import fullmatrix as FM
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+R2 = 1.0 / math.sqrt(2.0)
+
+ONEQ = ["H", "X", "Y", "Z", "S", "SDG", "T", "TDG", "RX", "RY", "RZ"]
+TWOQ = ["CNOT", "CZ", "CP", "SWAP", "CRY", "RXX", "RYY", "RZZ"]
+
+
+def rand_state(n, rng):
+    v = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    return (v / np.linalg.norm(v)).astype(np.complex128)
+
+
+def _read_state_golden(name):
+    rows, gate = [], None
+    for line in open(os.path.join(GOLD, name)):
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        if line.startswith("gate"):
+            gate = line.split()[1:]
+            continue
+        f = line.split()
+        val = lambda s: R2 if s == "r2" else float(s)
+        rows.append((int(f[0]), val(f[1]) + 1j * val(f[2]), val(f[3]) + 1j * val(f[4])))
+    N = len(rows)
+    psi_in = np.zeros(N, np.complex128)
+    psi_out = np.zeros(N, np.complex128)
+    for i, a, b in rows:
+        psi_in[i], psi_out[i] = a, b
+    return gate, psi_in, psi_out
+
+
+# ---------------------------------------------------------------- printed values
+
+def test_app_a_cnot(oracle):
+    gate, psi, expect = _read_state_golden("app_a_cnot.txt")
+    oracle.apply_gate(psi, gate[0], int(gate[1]), int(gate[2]))
+    np.testing.assert_array_equal(psi, expect)
+
+
+def test_app_b_toffoli(oracle):
+    gate, psi, expect = _read_state_golden("app_b_toffoli.txt")
+    oracle.apply_gate(psi, gate[0], int(gate[1]), int(gate[2]), q2=int(gate[3]))
+    np.testing.assert_array_equal(psi, expect)
+
+
+def _app_e_rows():
+    rows = []
+    for line in open(os.path.join(GOLD, "app_e_gradients.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, th, g, tol = [s.strip() for s in line.split("|")]
+        ev = lambda s: {"pi": math.pi, "pi/2": math.pi / 2}.get(s, None) or float(s)
+        rows.append((name, [ev(s) for s in th.split()], [float(s) for s in g.split()], float(tol)))
+    return rows
+
+
+@pytest.mark.parametrize("row", _app_e_rows(), ids=lambda r: r[0])
+def test_app_e_psr_table(oracle, row):
+    name, theta, expect, tol = row
+    gates = W.edge_case_circuit()
+    g = oracle.param_shift_grad(2, gates, np.array(theta), [(1.0, 0, 1)])
+    assert np.all(np.isfinite(g))
+    np.testing.assert_allclose(g, expect, rtol=0, atol=tol)
+
+
+# ---------------------------------------------------------------- matrix route
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 6])
+def test_every_1q_gate_vs_full_matrix(oracle, n):
+    rng = np.random.default_rng(100 + n)
+    for name in ONEQ:
+        for q in range(n):
+            ang = float(rng.uniform(0, 2 * np.pi))
+            psi = rand_state(n, rng)
+            ref = FM.gate_unitary(n, (name, q, -1, -1, ang)) @ psi
+            oracle.apply_gate(psi, name, q, -1, ang)
+            np.testing.assert_allclose(psi, ref, rtol=0, atol=1e-14, err_msg=f"{name} q{q}")
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 6])
+def test_every_2q_gate_vs_full_matrix(oracle, n):
+    rng = np.random.default_rng(200 + n)
+    for name in TWOQ:
+        for a in range(n):
+            for b in range(n):
+                if a == b:
+                    continue
+                ang = float(rng.uniform(0, 2 * np.pi))
+                psi = rand_state(n, rng)
+                ref = FM.gate_unitary(n, (name, a, b, -1, ang)) @ psi
+                oracle.apply_gate(psi, name, a, b, ang)
+                np.testing.assert_allclose(psi, ref, rtol=0, atol=1e-14,
+                                           err_msg=f"{name} ({a},{b})")
+
+
+@pytest.mark.parametrize("n", [2, 4, 6])
+def test_u1_u2_matrices_vs_full_matrix(oracle, n):
+    rng = np.random.default_rng(300 + n)
+    for _ in range(6):
+        A = rng.normal(size=(2, 2)) + 1j * rng.normal(size=(2, 2))
+        B = rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4))
+        q = int(rng.integers(n))
+        a, b = rng.choice(n, 2, replace=False)
+        psi = rand_state(n, rng)
+        ref = FM.gate_unitary(n, ("U1", q, -1, -1, 0.0, A)) @ psi
+        oracle.apply_gate(psi, "U1", q, mat=A)
+        np.testing.assert_allclose(psi, ref, atol=1e-13)
+        psi = rand_state(n, rng)
+        ref = FM.gate_unitary(n, ("U2", int(a), int(b), -1, 0.0, B)) @ psi
+        oracle.apply_gate(psi, "U2", int(a), int(b), mat=B)
+        np.testing.assert_allclose(psi, ref, atol=1e-13)
+
+
+def test_toffoli_all_positions_vs_full_matrix(oracle):
+    n = 4
+    rng = np.random.default_rng(7)
+    for a in range(n):
+        for b in range(n):
+            for c in range(n):
+                if len({a, b, c}) < 3:
+                    continue
+                psi = rand_state(n, rng)
+                ref = FM.gate_unitary(n, ("CCX", a, b, -1, 0.0, None, c)) @ psi
+                oracle.apply_gate(psi, "CCX", a, b, q2=c)
+                np.testing.assert_allclose(psi, ref, atol=1e-14)
+
+
+@pytest.mark.parametrize("n", [3, 5, 6])
+def test_random_circuit_vs_full_matrix(oracle, n):
+    rng = np.random.default_rng(400 + n)
+    gates = W.random_circuit(n, 120, rng, rng)
+    psi0 = oracle.init_random(n, 1234 + n)
+    ref = FM.circuit_unitary(n, gates) @ psi0
+    out = oracle.apply_circuit(psi0.copy(), gates)
+    np.testing.assert_allclose(out, ref, atol=1e-13)
+
+
+# ---------------------------------------------------------------- invariants
+
+def test_involutions_and_compositions(oracle):
+    n = 5
+    rng = np.random.default_rng(11)
+    psi0 = rand_state(n, rng)
+    for name in ["H", "X", "Y", "Z"]:
+        psi = psi0.copy()
+        oracle.apply_gate(psi, name, 2)
+        oracle.apply_gate(psi, name, 2)
+        np.testing.assert_allclose(psi, psi0, atol=1e-14)
+    for name in ["CNOT", "SWAP", "CZ"]:
+        psi = psi0.copy()
+        oracle.apply_gate(psi, name, 1, 3)
+        oracle.apply_gate(psi, name, 1, 3)
+        np.testing.assert_allclose(psi, psi0, atol=1e-14)
+    for a, b in [("S", "SDG"), ("T", "TDG")]:
+        psi = psi0.copy()
+        oracle.apply_gate(psi, a, 4)
+        oracle.apply_gate(psi, b, 4)
+        np.testing.assert_allclose(psi, psi0, atol=1e-14)
+    # S^2 = Z, T^2 = S, HXH = Z, Y = i X Z
+    for seq, single in [(["S", "S"], "Z"), (["T", "T"], "S"), (["H", "X", "H"], "Z")]:
+        p1, p2 = psi0.copy(), psi0.copy()
+        for g in seq:
+            oracle.apply_gate(p1, g, 0)
+        oracle.apply_gate(p2, single, 0)
+        np.testing.assert_allclose(p1, p2, atol=1e-14)
+    p1, p2 = psi0.copy(), psi0.copy()
+    oracle.apply_gate(p1, "Z", 3)
+    oracle.apply_gate(p1, "X", 3)
+    oracle.apply_gate(p2, "Y", 3)
+    np.testing.assert_allclose(1j * p1, p2, atol=1e-14)
+    # RZ(a) RZ(b) = RZ(a+b); same for RX, RY
+    for r in ["RX", "RY", "RZ"]:
+        p1, p2 = psi0.copy(), psi0.copy()
+        oracle.apply_gate(p1, r, 1, angle=0.7)
+        oracle.apply_gate(p1, r, 1, angle=1.9)
+        oracle.apply_gate(p2, r, 1, angle=2.6)
+        np.testing.assert_allclose(p1, p2, atol=1e-14)
+    # RX(pi) = -iX, RY(pi) = -iY, RZ(pi) = -iZ
+    for r, g in [("RX", "X"), ("RY", "Y"), ("RZ", "Z")]:
+        p1, p2 = psi0.copy(), psi0.copy()
+        oracle.apply_gate(p1, r, 2, angle=math.pi)
+        oracle.apply_gate(p2, g, 2)
+        np.testing.assert_allclose(p1, -1j * p2, atol=1e-15)
+
+
+def test_norm_preserved_by_random_circuit(oracle):
+    n = 12
+    rng = np.random.default_rng(3)
+    psi = oracle.init_random(n, 99)
+    oracle.apply_circuit(psi, W.random_circuit(n, 300, rng, rng))
+    assert abs(oracle.norm2(psi) - 1.0) < 1e-12
+
+
+def test_rotation_sign_closed_forms(oracle):
+    """Reading A3: RX(t)|0> has <Y> = -sin t; RY(t)|0> has <X> = +sin t;
+    RZ(t)|+> has <X> = cos t, <Y> = sin t.  (Direct consequence of
+    e^{-i t G/2}.)"""
+    for t in [0.0, 0.3, 1.1, math.pi / 2, 2.0, 4.5]:
+        psi = oracle.zeros(1)
+        oracle.apply_gate(psi, "RX", 0, angle=t)
+        assert oracle.expval(psi, [(1.0, 1, 1)]) == pytest.approx(-math.sin(t), abs=1e-15)
+        assert oracle.expval(psi, [(1.0, 0, 1)]) == pytest.approx(math.cos(t), abs=1e-15)
+        psi = oracle.zeros(1)
+        oracle.apply_gate(psi, "RY", 0, angle=t)
+        assert oracle.expval(psi, [(1.0, 1, 0)]) == pytest.approx(math.sin(t), abs=1e-15)
+        psi = oracle.zeros(1)
+        oracle.apply_gate(psi, "H", 0)
+        oracle.apply_gate(psi, "RZ", 0, angle=t)
+        assert oracle.expval(psi, [(1.0, 1, 0)]) == pytest.approx(math.cos(t), abs=1e-15)
+        assert oracle.expval(psi, [(1.0, 1, 1)]) == pytest.approx(math.sin(t), abs=1e-15)
+
+
+# ---------------------------------------------------------------- init
+
+def test_init_basis(oracle):
+    psi = oracle.init_basis(3, 6)
+    expect = np.zeros(8, np.complex128)
+    expect[6] = 1
+    np.testing.assert_array_equal(psi, expect)
+
+
+def test_init_random_gaussian_and_normalised(oracle):
+    n = 16
+    a = oracle.init_random(n, 2024)
+    b = oracle.init_random(n, 2024)
+    c = oracle.init_random(n, 2025)
+    np.testing.assert_array_equal(a, b)
+    assert np.abs(a - c).max() > 1e-3
+    assert abs(oracle.norm2(a) - 1.0) < 1e-13
+    N = 1 << n
+    z = a * math.sqrt(N)             # components ~ N(0, 1/2) each
+    assert abs(z.real.mean()) < 5 * math.sqrt(0.5 / N)
+    assert abs(z.imag.mean()) < 5 * math.sqrt(0.5 / N)
+    assert abs(z.real.var() - 0.5) < 0.02 and abs(z.imag.var() - 0.5) < 0.02
+    assert abs(np.mean(z.real * z.imag)) < 0.01
+    # |z|^2 ~ Exp(1): P(|z|^2 < 1) = 1 - 1/e
+    assert abs(np.mean(np.abs(z) ** 2 < 1.0) - (1 - math.exp(-1))) < 0.01
+    # Gaussian kurtosis of each component is 3
+    k = np.mean(z.real ** 4) / np.mean(z.real ** 2) ** 2
+    assert abs(k - 3.0) < 0.1
+
+
+# ---------------------------------------------------------------- QFT
+
+def alg3_gates(n):
+    g = []
+    for i in range(n):
+        g.append(("H", i, -1, -1, 0.0))
+        for j in range(i + 1, n):
+            g.append(("CP", i, j, -1, math.pi / 2 ** (j - i)))
+    for i in range(n // 2):
+        g.append(("SWAP", i, n - 1 - i, -1, 0.0))
+    return g
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6])
+def test_alg3_equals_qft_definition_matrix(n):
+    """Reading A5: Alg. 3 under MSB-first equals the closed form of P:601
+    (numerically via the independent matrix route)."""
+    assert len(alg3_gates(n)) == W.qft_gate_count(n)
+    np.testing.assert_allclose(FM.circuit_unitary(n, alg3_gates(n)), FM.qft_matrix(n), atol=1e-14)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 10])
+def test_qft_basis_states_closed_form(oracle, n):
+    N = 1 << n
+    j = np.arange(N, dtype=np.int64)
+    for k in sorted({0, 1, N - 1, N // 3, (5 * N) // 7} & set(range(N))):
+        psi = oracle.init_basis(n, k)
+        oracle.qft(psi)
+        expect = np.exp(2j * np.pi * ((j * k) % N) / N) / math.sqrt(N)
+        np.testing.assert_allclose(psi, expect, atol=1e-13)
+
+
+@pytest.mark.parametrize("n", [4, 9, 12])
+def test_qft_random_state_vs_numpy_ifft(oracle, n):
+    psi = oracle.init_random(n, 77 + n)
+    ref = np.fft.ifft(psi) * math.sqrt(1 << n)
+    oracle.qft(psi)
+    np.testing.assert_allclose(psi, ref, atol=1e-13)
+
+
+def test_qft_vs_dft_matrix_and_roundtrip(oracle):
+    n = 7
+    psi0 = oracle.init_random(n, 5)
+    psi = psi0.copy()
+    oracle.qft(psi)
+    np.testing.assert_allclose(psi, FM.qft_matrix(n) @ psi0, atol=1e-13)
+    oracle.qft(psi, inverse=True)
+    np.testing.assert_allclose(psi, psi0, atol=1e-13)
+
+
+# ---------------------------------------------------------------- expectation
+
+def test_expectation_small_closed_forms(oracle):
+    psi = oracle.zeros(1)
+    assert oracle.expval(psi, [(1.0, 0, 1)]) == 1.0          # <Z> on |0>
+    bell = np.array([R2, 0, 0, R2], np.complex128)
+    assert oracle.expval(bell, [(1.0, 3, 0)]) == pytest.approx(1.0, abs=1e-15)   # XX
+    assert oracle.expval(bell, [(1.0, 3, 3)]) == pytest.approx(-1.0, abs=1e-15)  # YY
+    assert oracle.expval(bell, [(1.0, 0, 3)]) == pytest.approx(1.0, abs=1e-15)   # ZZ
+    assert oracle.expval(bell, [(1.0, 1, 0)]) == pytest.approx(0.0, abs=1e-15)   # X on q0
+
+
+@pytest.mark.parametrize("n", [2, 4, 6])
+def test_expectation_vs_hamiltonian_matrix(oracle, n):
+    rng = np.random.default_rng(500 + n)
+    terms = W.random_pauli_sum(n, min(15, 4 ** n - 1), rng)
+    psi = rand_state(n, rng)
+    Hm = FM.hamiltonian_matrix(n, terms)
+    ref = float(np.real(np.vdot(psi, Hm @ psi)))
+    assert oracle.expval(psi, terms) == pytest.approx(ref, abs=1e-13)
+
+
+@pytest.mark.parametrize("n", [6, 8, 10])
+def test_xyz_energy_at_theta_zero(oracle, n):
+    """SURVEY c.4: ring ansatz at theta = 0 leaves |0...0> (CNOTs act on
+    controls = 0), so E = Jz (n-1) + hz n exactly."""
+    gates = W.hea_ansatz(n, 2, "ring")
+    e = oracle.energy(n, gates, np.zeros(4 * n), W.xyz_terms(n))
+    assert e == pytest.approx(0.4 * (n - 1) + 0.3 * n, abs=1e-13)
+
+
+# ---------------------------------------------------------------- PSR
+
+def test_psr_single_ry_closed_form(oracle):
+    """North star: <Z> after RY(t)|0> is cos t; its PSR derivative is -sin t."""
+    gates = [("RY", 0, -1, 0, 0.0)]
+    for t in [0.0, 0.3, math.pi / 2, 2.0, 5.5]:
+        assert oracle.energy(1, gates, [t], [(1.0, 0, 1)]) == pytest.approx(math.cos(t), abs=1e-15)
+        g = oracle.param_shift_grad(1, gates, np.array([t]), [(1.0, 0, 1)])
+        assert g[0] == pytest.approx(-math.sin(t), abs=1e-15)
+
+
+def product_energy_and_grad(n, theta, terms_j=(1.0, 0.7, 0.4), hz=0.3):
+    """Closed form for the product ansatz RY(t_q) then RZ(p_q): Bloch vector
+    b_q = (sin t cos p, sin t sin p, cos t); E = sum_i sum_a J_a b^a_i b^a_{i+1}
+    + hz sum_q b^z_q; gradient by the product rule (SURVEY c.4)."""
+    t, p = theta[:n], theta[n:]
+    b = np.stack([np.sin(t) * np.cos(p), np.sin(t) * np.sin(p), np.cos(t)], 1)
+    db_dt = np.stack([np.cos(t) * np.cos(p), np.cos(t) * np.sin(p), -np.sin(t)], 1)
+    db_dp = np.stack([-np.sin(t) * np.sin(p), np.sin(t) * np.cos(p), 0 * t], 1)
+    J = np.array(terms_j)
+    E = sum(float(np.sum(J * b[i] * b[i + 1])) for i in range(n - 1)) + hz * float(b[:, 2].sum())
+    gt, gp = np.zeros(n), np.zeros(n)
+    for q in range(n):
+        for nb in (q - 1, q + 1):
+            if 0 <= nb < n:
+                gt[q] += np.sum(J * db_dt[q] * b[nb])
+                gp[q] += np.sum(J * db_dp[q] * b[nb])
+        gt[q] += hz * db_dt[q, 2]
+    return E, np.concatenate([gt, gp])
+
+
+@pytest.mark.parametrize("n", [3, 6, 8])
+def test_psr_product_ansatz_closed_form(oracle, n):
+    rng = np.random.default_rng(600 + n)
+    gates, theta = W.product_ansatz(n, rng)
+    terms = W.xyz_terms(n)
+    E, g = product_energy_and_grad(n, theta)
+    assert oracle.energy(n, gates, theta, terms) == pytest.approx(E, abs=1e-13)
+    np.testing.assert_allclose(oracle.param_shift_grad(n, gates, theta, terms, threads=4), g,
+                               atol=1e-13)
+
+
+def test_psr_matches_central_difference_cfg3(oracle):
+    """PSR vs central finite difference on config 3."""
+    w = W.config3()
+    g = oracle.param_shift_grad(w.n, w.gates, w.theta, w.terms)
+    h = 1e-5
+    fd = np.zeros_like(g)
+    for p in range(w.theta.size):
+        tp, tm = w.theta.copy(), w.theta.copy()
+        tp[p] += h
+        tm[p] -= h
+        fd[p] = (oracle.energy(w.n, w.gates, tp, w.terms) - oracle.energy(w.n, w.gates, tm, w.terms)) / (2 * h)
+    np.testing.assert_allclose(g, fd, atol=1e-8)
+
+
+def test_psr_vs_matrix_route_gradient(oracle):
+    """Exact derivative through the matrix route: d/dt <0|U(t)^+ H U(t)|0>
+    with dU from the generator, n = 3 ring ansatz."""
+    n = 3
+    rng = np.random.default_rng(9)
+    gates = W.hea_ansatz(n, 2, "ring")
+    theta = rng.uniform(0, 2 * np.pi, 4 * n)
+    terms = W.random_pauli_sum(n, 10, rng)
+    Hm = FM.hamiltonian_matrix(n, terms)
+    gens = {"RX": FM.X, "RY": FM.Y, "RZ": FM.Z}
+    psi0 = np.zeros(1 << n, np.complex128)
+    psi0[0] = 1
+    exact = np.zeros(theta.size)
+    for k, (name, a, b, p, _) in enumerate(gates):
+        if p < 0:
+            continue
+        pre = FM.circuit_unitary(n, gates[:k + 1], theta)
+        post = FM.circuit_unitary(n, gates[k + 1:], theta)
+        G = FM.embed(n, {a: gens[name]})
+        dpsi = post @ (-0.5j * G) @ pre @ psi0
+        psi = post @ pre @ psi0
+        exact[p] = 2 * np.real(np.vdot(psi, Hm @ dpsi))
+    g = oracle.param_shift_grad(n, gates, theta, terms)
+    np.testing.assert_allclose(g, exact, atol=1e-13)
+
+
+def test_expval_rejects_non_hermitian_imag(oracle):
+    """a non-real <P> is an error, never silent.  A Pauli
+    product is Hermitian, so this only fires on a corrupted state buffer."""
+    psi = np.array([1, 1j], np.complex128) / math.sqrt(2)
+    # <Y> on (|0> + i|1>)/sqrt2 = 1 (real) -- must pass
+    assert oracle.expval(psi, [(1.0, 1, 1)]) == pytest.approx(1.0)
