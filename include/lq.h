@@ -1,0 +1,224 @@
+/*
+ * lq.h -- C ABI of liblq.so: B200-native dense complex128 state-vector
+ * simulation of parameterised circuits (the data-parallel hot path of
+ * LogosQ, arXiv 2512.23183; /root/reference/PAPER.md).
+ *
+ * Conventions (all entry points)
+ *   - A state on n qubits holds N = 2^n complex128 amplitudes (interleaved
+ *     re, im doubles), the paper's DenseState of Complex64.
+ *   - Qubit q <-> logical index bit n-1-q (MSB first; Alg. 1).
+ *     The library may keep amplitudes in a permuted physical layout (a qubit
+ *     map); every call that takes or returns indices uses LOGICAL indices.
+ *   - Rotations R_G(theta) = exp(-i theta G / 2).
+ *   - 2-qubit matrices act on the sub-index 2*bit(q0) + bit(q1) (q0 is the
+ *     high bit).  Controlled gates list the control first.
+ *   - Every call validates all arguments before any device work: a rejected
+ *     call returns a negative lq_status, sets lq_last_error() and leaves the
+ *     state untouched.  No exception or abort crosses this ABI.
+ *   - Device work is enqueued on the handle's CUDA stream (cudaStream_t passed
+ *     as void*; NULL = legacy default stream).  Calls documented "syncs"
+ *     block until their results are on the host.
+ *   - Handles are single-writer: do not call into one handle
+ *     from two threads at once.
+ *   - No CPU fallback: if no CUDA device is present every call that needs one
+ *     fails with LQ_ERR_CUDA.
+ */
+#ifndef LQ_C_ABI_H_
+#define LQ_C_ABI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LQ_VERSION 1
+
+typedef enum {
+    LQ_OK = 0,
+    LQ_ERR_ARG = -1,        /* bad argument (qubit range, duplicate qubits, angle on a fixed gate, ...) */
+    LQ_ERR_OOM = -2,        /* device allocation failed / state too large */
+    LQ_ERR_CUDA = -3,       /* CUDA runtime error (incl. no device) */
+    LQ_ERR_NCCL = -4,       /* reserved: collective failure */
+    LQ_ERR_DIM = -5,        /* size mismatch (wrapped buffer too small, count out of range) */
+    LQ_ERR_NONFINITE = -6,  /* NaN/Inf angle, parameter or coefficient */
+    LQ_ERR_STATE = -7       /* handle unusable after an earlier asynchronous failure */
+} lq_status;
+
+/* Gate kinds.  Fixed gates take no angle; rotation
+ * kinds take exactly one angle (literal or theta[param_idx]). */
+typedef enum {
+    LQ_H = 0, LQ_X, LQ_Y, LQ_Z, LQ_S, LQ_SDG, LQ_T, LQ_TDG,
+    LQ_RX, LQ_RY, LQ_RZ,          /* exp(-i theta {X,Y,Z} / 2) */
+    LQ_CNOT,                      /* q0 control, q1 target (Alg. 1) */
+    LQ_CZ,                        /* diag(1,1,1,-1) */
+    LQ_CP,                        /* diag(1,1,1,e^{i theta}) (Alg. 3 CP) */
+    LQ_SWAP,
+    LQ_U1,                        /* arbitrary 2x2, row-major complex128 in .mat (8 doubles) */
+    LQ_U2,                        /* arbitrary 4x4 on (q0 high, q1 low), .mat (32 doubles) */
+    LQ_CRY,                       /* RY(theta) on q1 when q0 = |1> (App. E circuit) */
+    LQ_CCX,                       /* Toffoli: q0, q1 controls, q2 target (App. B) */
+    LQ_RXX, LQ_RYY, LQ_RZZ,       /* exp(-i theta P(x)P / 2) (Trotter gates) */
+    LQ_NUM_KINDS
+} lq_kind;
+
+/* One circuit operation ("Operation").  Unused qubit slots
+ * are -1.  angle source: param_idx >= 0 -> theta[param_idx] (an ansatz
+ * parameter); param_idx == -1 -> .angle.  Fixed gates
+ * must have param_idx == -1 and angle == 0.  mat is read only for
+ * LQ_U1/LQ_U2 and is borrowed for the call. */
+typedef struct lq_gate {
+    int32_t kind;
+    int32_t q0, q1, q2;
+    int32_t param_idx;
+    int32_t reserved;             /* must be 0 */
+    double angle;
+    const double *mat;
+} lq_gate;
+
+/* Real-weighted Pauli string coeff * P, P = prod_q sigma_q:
+ * bit q of x_mask / z_mask = qubit q; X: x only, Z: z only, Y: both. */
+typedef struct lq_pauli_term {
+    double coeff;
+    uint64_t x_mask;
+    uint64_t z_mask;
+} lq_pauli_term;
+
+typedef struct lq_sv lq_sv;       /* opaque state-vector handle */
+typedef struct lq_psr lq_psr;     /* opaque parameter-shift gradient plan */
+
+/* Thread-local message for the last failing call on this thread. */
+const char *lq_last_error(void);
+int lq_version(void);
+
+/* Number of CUDA devices visible (0 on a host without a GPU; never fails). */
+int lq_device_count(void);
+
+/* ---- state vectors (DenseState) ---------------------- */
+
+/* Allocate 2^n_qubits amplitudes on the current CUDA device; the library
+ * owns the memory.  Contents are undefined until an init call.
+ * n_qubits in [1, 40]; LQ_ERR_OOM if the device cannot hold the state. */
+lq_status lq_sv_alloc(int n_qubits, void *cuda_stream, lq_sv **out);
+
+/* Wrap caller-owned device memory (e.g. a torch complex128 tensor the
+ * caller keeps alive).  bytes >= 16 * 2^n_qubits; dev_ptr 16-byte aligned.
+ * The library never frees wrapped memory. */
+lq_status lq_sv_wrap(int n_qubits, void *cuda_stream, void *dev_ptr, size_t bytes, lq_sv **out);
+
+/* Free the handle (and its memory unless wrapped).  NULL is a no-op. */
+lq_status lq_sv_free(lq_sv *sv);
+
+/* Change the stream later calls enqueue on. */
+lq_status lq_sv_set_stream(lq_sv *sv, void *cuda_stream);
+
+int lq_sv_num_qubits(const lq_sv *sv);
+
+/* Raw device pointer of the amplitudes in the current PHYSICAL layout. */
+void *lq_sv_device_ptr(const lq_sv *sv);
+
+/* Physical bit of each qubit: map_out[q] for q < n (identity = n-1-q). */
+lq_status lq_sv_qubit_map(const lq_sv *sv, int32_t *map_out);
+
+/* |k>.  k < 2^n (logical index). Resets the qubit map. */
+lq_status lq_sv_init_basis(lq_sv *sv, uint64_t k);
+
+/* Seeded random normalised state: for logical index i,
+ *   x0 = splitmix64(seed ^ 2i), x1 = splitmix64(seed ^ (2i+1)),
+ *   u_j = ((x_j >> 11) + 0.5) 2^-53,
+ *   a_i = sqrt(-2 ln u0) (cos 2 pi u1 + i sin 2 pi u1),
+ * then a /= sqrt(sum |a|^2).  splitmix64(x): z = x + 0x9E3779B97F4A7C15;
+ * z = (z ^ z>>30) * 0xBF58476D1CE4E5B9; z = (z ^ z>>27) * 0x94D049BB133111EB;
+ * return z ^ z>>31.  Resets the qubit map. */
+lq_status lq_sv_init_random(lq_sv *sv, uint64_t seed);
+
+/* Copy amplitudes from/to host memory in LOGICAL order (syncs).
+ * host buffers hold 2*count doubles (re, im).  offset + count <= 2^n. */
+lq_status lq_sv_read(lq_sv *sv, uint64_t offset, uint64_t count, double *host_out);
+lq_status lq_sv_write(lq_sv *sv, uint64_t offset, uint64_t count, const double *host_in);
+
+/* Amplitudes at arbitrary logical indices (syncs); host_out: 2*count doubles. */
+lq_status lq_sv_gather(lq_sv *sv, const uint64_t *idx, size_t count, double *host_out);
+
+/* sum_i |a_i|^2 with a deterministic fixed-order reduction (syncs). */
+lq_status lq_sv_norm2(lq_sv *sv, double *out);
+
+/* Physically permute amplitudes so the qubit map is the identity
+ * (natural MSB-first order in device memory). */
+lq_status lq_sv_canonicalize(lq_sv *sv);
+
+/* ---- circuits (Circuit::execute) ----------------------- */
+
+/* Apply gates[0..n_gates) in order (Circuit::execute semantics).  theta
+ * (host, n_theta doubles) supplies angles for gates with param_idx >= 0;
+ * it may be NULL when no gate uses a parameter.  The library fuses gates
+ * into shared-memory tile passes; the result equals sequential application
+ * up to floating-point rounding.  SWAP gates are applied as qubit-map
+ * relabels (no data movement). */
+lq_status lq_apply_circuit(lq_sv *sv, const lq_gate *gates, size_t n_gates,
+                           const double *theta, size_t n_theta);
+
+/* QFT|x> = N^-1/2 sum_k e^{2 pi i x k / N}|k>, i.e.
+ * Alg. 2's InverseFFT / sqrt(N) and Alg. 3's gate
+ * sequence.  inverse != 0 applies QFT^-1.  Computed as
+ * fused radix-2 butterfly tiles; the final bit reversal is a qubit-map
+ * relabel (call lq_sv_canonicalize to materialise natural order). */
+lq_status lq_qft(lq_sv *sv, int inverse);
+
+/* ---- observables ---------------------------- */
+
+/* E = sum_t coeff_t <psi|P_t|psi> (syncs).  Deterministic reduction. */
+lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_terms,
+                              double *out_energy);
+
+/* ---- parameter-shift gradients -------------- */
+
+/* g_p = ( E(theta + (pi/2) e_p) - E(theta - (pi/2) e_p) ) / 2 for the ansatz
+ * ansatz[0..n_gates) run from |0...0> and the Pauli sum
+ * terms.  Each parameter must be used by exactly one rotation gate
+ * (reading A7); all 2*n_params shifted circuits are independent and are
+ * batched.  shard_rank/shard_world: compute only parameters with
+ * p % shard_world == shard_rank (others are written as 0); the caller sums
+ * the shards (e.g. torch.distributed.all_reduce).  energy_out (nullable)
+ * receives E(theta) on shard 0 (0 elsewhere).  Host in/out (syncs). */
+lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gates,
+                              const double *theta, size_t n_params,
+                              const lq_pauli_term *terms, size_t n_terms,
+                              int shard_rank, int shard_world, void *cuda_stream,
+                              double *grad_out, double *energy_out);
+
+/* Same computation split into a reusable plan and an asynchronous run on
+ * DEVICE pointers (theta_dev: n_params doubles; grad_dev: n_params doubles;
+ * energy_dev: 1 double or NULL).  lq_psr_run does not sync. */
+lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, size_t n_params,
+                        const lq_pauli_term *terms, size_t n_terms, int shard_rank,
+                        int shard_world, void *cuda_stream, lq_psr **out);
+lq_status lq_psr_run(lq_psr *plan, const double *theta_dev, double *grad_dev, double *energy_dev);
+lq_status lq_psr_free(lq_psr *plan);
+/* Number of circuits one lq_psr_run evaluates on this shard and the kernel
+ * launches it issues (for throughput accounting). */
+lq_status lq_psr_stats(const lq_psr *plan, uint64_t *n_circuits, uint64_t *n_launches);
+
+/* ---- execution options (testing / measurement) -------------------------- */
+typedef enum {
+    LQ_OPT_FUSION = 0,     /* 1 (default): tile-fused passes; 0: one pass per gate (pair/diag kernels) */
+    LQ_OPT_TILE_BITS = 1,  /* tile size K in bits (default 0 = automatic) */
+    LQ_OPT_COALESCE_BITS = 2 /* low physical bits every strided tile includes (default 3) */
+} lq_option;
+lq_status lq_set_option(int option, int64_t value);
+int64_t lq_get_option(int option);
+
+/* Host-only planning diagnostics (no device needed): plan `gates` on
+ * n_qubits with the current options; report the number of passes, of tile
+ * passes, and a text description (truncated to buf_len). */
+lq_status lq_plan_describe(int n_qubits, const lq_gate *gates, size_t n_gates, uint64_t *n_passes,
+                           uint64_t *n_tile, char *buf, size_t buf_len);
+
+/* Kernel launches issued by this process so far (all entry points). */
+uint64_t lq_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LQ_C_ABI_H_ */

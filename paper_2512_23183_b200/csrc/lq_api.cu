@@ -1,0 +1,884 @@
+// lq_api.cu -- C ABI of liblq.so (include/lq.h): handles, validation,
+// launch orchestration, the batched parameter-shift driver.
+//
+// Every numerical step runs in the kernels of kernels.cuh; this file only
+// validates arguments, plans (planner.cpp), uploads plans and launches.
+// There is no CPU fallback: without a CUDA device every call that needs one
+// returns LQ_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "planner.h"
+
+using namespace lq;
+
+struct lq_sv;
+struct lq_psr;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int64_t> g_opt_fusion{1};
+std::atomic<int64_t> g_opt_K{0};
+std::atomic<int64_t> g_opt_coalesce{3};
+const double PI = 3.14159265358979323846264338327950288;
+
+lq_status fail(lq_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+
+#define CUDA_TRY(x)                                                                         \
+    do {                                                                                    \
+        cudaError_t e_ = (x);                                                               \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(LQ_ERR_CUDA, std::string(#x) + " failed: " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define LQ_TRY(x)                          \
+    do {                                   \
+        lq_status s_ = (x);                \
+        if (s_ != LQ_OK) return s_;        \
+    } while (0)
+
+lq_status check_launch(const char *what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(LQ_ERR_CUDA, std::string(what) + " launch failed: " + cudaGetErrorString(e));
+    return LQ_OK;
+}
+
+lq_status have_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(LQ_ERR_CUDA, "no CUDA device available (liblq has no CPU fallback)");
+    }
+    return LQ_OK;
+}
+
+PlanOptions options() {
+    PlanOptions o;
+    o.K = (int)g_opt_K.load();
+    o.coalesce = (int)g_opt_coalesce.load();
+    o.fusion = g_opt_fusion.load() != 0;
+    return o;
+}
+
+// Stream-ordered growable device buffer.
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    lq_status reserve(size_t bytes, cudaStream_t s) {
+        if (bytes <= cap && p) return LQ_OK;
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        size_t nb = std::max<size_t>(bytes, std::max<size_t>(cap * 2, 4096));
+        cudaError_t e = cudaMallocAsync(&p, nb, s);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            cap = 0;
+            return fail(e == cudaErrorMemoryAllocation ? LQ_ERR_OOM : LQ_ERR_CUDA,
+                        std::string("device allocation of ") + std::to_string(nb) + " bytes failed: " +
+                            cudaGetErrorString(e));
+        }
+        cap = nb;
+        return LQ_OK;
+    }
+    void release(cudaStream_t s) {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T> T *at(size_t off) const { return reinterpret_cast<T *>(static_cast<char *>(p) + off); }
+};
+
+// Host staging of several arrays uploaded with one copy.
+struct Blob {
+    std::vector<char> h;
+    template <class T> size_t add(const std::vector<T> &v) { return add(v.data(), v.size() * sizeof(T)); }
+    size_t add(const void *d, size_t bytes) {
+        size_t off = (h.size() + 255) & ~size_t(255);
+        h.resize(off + std::max<size_t>(bytes, 1));
+        if (bytes) memcpy(h.data() + off, d, bytes);
+        return off;
+    }
+    lq_status upload(DevBuf &b, cudaStream_t s) {
+        LQ_TRY(b.reserve(h.size(), s));
+        CUDA_TRY(cudaMemcpyAsync(b.p, h.data(), h.size(), cudaMemcpyHostToDevice, s));
+        return LQ_OK;
+    }
+};
+
+bool is_rotation(int k) {
+    return k == LQ_RX || k == LQ_RY || k == LQ_RZ || k == LQ_CP || k == LQ_CRY || k == LQ_RXX || k == LQ_RYY ||
+           k == LQ_RZZ;
+}
+int arity(int k) {
+    if (k <= LQ_RZ || k == LQ_U1) return 1;
+    if (k == LQ_CCX) return 3;
+    return 2;
+}
+
+// Boundary validation: the runtime form of the paper's
+// compile-time parameter/gate distinction.
+lq_status validate_gates(int n, const lq_gate *g, size_t ng, const double *theta, size_t n_theta,
+                         bool theta_known, std::vector<int> *uses) {
+    if (ng && !g) return fail(LQ_ERR_ARG, "gates is NULL");
+    for (size_t i = 0; i < ng; i++) {
+        const lq_gate &G = g[i];
+        std::string at = "gate " + std::to_string(i) + ": ";
+        if (G.kind < 0 || G.kind >= LQ_NUM_KINDS) return fail(LQ_ERR_ARG, at + "unknown kind");
+        if (G.reserved != 0) return fail(LQ_ERR_ARG, at + "reserved field must be 0");
+        int a = arity(G.kind);
+        int qs[3] = {G.q0, G.q1, G.q2};
+        for (int k = 0; k < 3; k++) {
+            if (k < a) {
+                if (qs[k] < 0 || qs[k] >= n) return fail(LQ_ERR_ARG, at + "qubit out of range");
+            } else if (qs[k] != -1) {
+                return fail(LQ_ERR_ARG, at + "unused qubit slot must be -1");
+            }
+        }
+        if ((a >= 2 && G.q0 == G.q1) || (a == 3 && (G.q2 == G.q0 || G.q2 == G.q1)))
+            return fail(LQ_ERR_ARG, at + "duplicate qubits");
+        if (is_rotation(G.kind)) {
+            if (G.param_idx >= 0) {
+                if (G.param_idx >= (int64_t)n_theta) return fail(LQ_ERR_ARG, at + "param_idx >= n_params");
+                if (G.angle != 0.0) return fail(LQ_ERR_ARG, at + "angle must be 0 when param_idx is used");
+                if (theta_known) {
+                    if (!theta) return fail(LQ_ERR_ARG, at + "theta is NULL");
+                    if (!std::isfinite(theta[G.param_idx])) return fail(LQ_ERR_NONFINITE, at + "non-finite theta");
+                }
+                if (uses) (*uses)[G.param_idx]++;
+            } else if (G.param_idx == -1) {
+                if (!std::isfinite(G.angle)) return fail(LQ_ERR_NONFINITE, at + "non-finite angle");
+            } else {
+                return fail(LQ_ERR_ARG, at + "param_idx must be >= 0 or -1");
+            }
+        } else {
+            if (G.param_idx != -1 || G.angle != 0.0)
+                return fail(LQ_ERR_ARG, at + "fixed gate takes no angle or parameter");
+        }
+        if (G.kind == LQ_U1 || G.kind == LQ_U2) {
+            if (!G.mat) return fail(LQ_ERR_ARG, at + "matrix is NULL");
+            int cnt = G.kind == LQ_U1 ? 8 : 32;
+            for (int k = 0; k < cnt; k++)
+                if (!std::isfinite(G.mat[k])) return fail(LQ_ERR_NONFINITE, at + "non-finite matrix entry");
+        }
+    }
+    if (uses)
+        for (size_t p = 0; p < uses->size(); p++)
+            if ((*uses)[p] > 1)
+                return fail(LQ_ERR_ARG, "parameter " + std::to_string(p) +
+                                            " is used by more than one gate (not supported, reading A7)");
+    return LQ_OK;
+}
+
+lq_status validate_terms(int n, const lq_pauli_term *t, size_t nt) {
+    if (nt && !t) return fail(LQ_ERR_ARG, "terms is NULL");
+    uint64_t lim = n >= 64 ? ~0ull : ((1ull << n) - 1);
+    for (size_t i = 0; i < nt; i++) {
+        if ((t[i].x_mask & ~lim) || (t[i].z_mask & ~lim))
+            return fail(LQ_ERR_ARG, "term " + std::to_string(i) + ": mask has bits beyond n qubits");
+        if (!std::isfinite(t[i].coeff)) return fail(LQ_ERR_NONFINITE, "term " + std::to_string(i) + ": non-finite coeff");
+    }
+    return LQ_OK;
+}
+
+// ---------------------------------------------------------------- launches
+template <int RR>
+lq_status launch_tile_rr(const KPass &kp, const KSub *subs, const KOp *kops, const double2 *mats,
+                         uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride,
+                         int n_circ, cudaStream_t st) {
+    static bool attr = false;
+    static int n_sm = 0;
+    const size_t smem = ((size_t)32 << kp.K) + (size_t)kp.smat * sizeof(double2) +
+                        (size_t)(kp.op_end - kp.op_begin) * sizeof(KOp);
+    if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(k_tile<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+        attr = true;
+    }
+    if (smem > 227 * 1024) return fail(LQ_ERR_STATE, "tile pass exceeds shared memory (planner bug)");
+    const uint32_t tiles_log2 = (uint32_t)(kp.n - kp.K);
+    const uint64_t total = (uint64_t)n_circ << tiles_log2;
+    if (total >= (1ull << 32)) return fail(LQ_ERR_DIM, "too many tiles in one launch");
+    const unsigned grid = (unsigned)std::min<uint64_t>(total, (uint64_t)n_sm);
+    k_tile<RR><<<grid, 1u << (kp.K - RR), smem, st>>>(kp, subs, kops, mats, mat_stride, cst, state, state_stride,
+                                                      tiles_log2, (uint32_t)total);
+    return check_launch("k_tile");
+}
+
+lq_status launch_tile(const KPass &kp, const KSub *subs, const KOp *kops, const double2 *mats, uint64_t mat_stride,
+                      const double2 *cst, double2 *state, uint64_t state_stride, int n_circ, cudaStream_t st) {
+    switch (std::min(R, kp.K)) {
+    case 1: return launch_tile_rr<1>(kp, subs, kops, mats, mat_stride, cst, state, state_stride, n_circ, st);
+    case 2: return launch_tile_rr<2>(kp, subs, kops, mats, mat_stride, cst, state, state_stride, n_circ, st);
+    case 3: return launch_tile_rr<3>(kp, subs, kops, mats, mat_stride, cst, state, state_stride, n_circ, st);
+    default: return launch_tile_rr<4>(kp, subs, kops, mats, mat_stride, cst, state, state_stride, n_circ, st);
+    }
+}
+
+unsigned grid_for(uint64_t work, unsigned per_block = 256) {
+    uint64_t b = (work + per_block - 1) / per_block;
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, 148ull * 16));
+}
+
+struct DevPlan {
+    const KSub *subs = nullptr;
+    const KOp *kops = nullptr;
+    const MSpec *specs = nullptr;
+    const MFactor *factors = nullptr;
+    const double2 *cst = nullptr;
+};
+
+lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uint64_t state_stride, int n_circ,
+                        const double2 *mats, uint64_t mat_stride, cudaStream_t st, bool zero_first) {
+    const int n = plan.n;
+    if (zero_first && (plan.passes.empty() || plan.passes[0].kind != PASS_TILE)) {
+        dim3 grid(grid_for(1ull << n), n_circ);
+        k_fill_basis<<<grid, 256, 0, st>>>(1ull << n, 0, state, state_stride);
+        LQ_TRY(check_launch("k_fill_basis"));
+    }
+    for (size_t i = 0; i < plan.passes.size(); i++) {
+        const PlanPass &p = plan.passes[i];
+        if (p.kind == PASS_TILE) {
+            KPass kp = p.kp;
+            if (zero_first && i == 0) kp.flags |= PF_LOAD_ZERO;
+            LQ_TRY(launch_tile(kp, dp.subs, dp.kops, mats, mat_stride, dp.cst, state, state_stride, n_circ, st));
+        } else if (p.kind == PASS_PAIR) {
+            const KOp op = plan.kops[p.op_begin];
+            uint64_t work = (op.type == K_U1 || op.type == K_X) ? (1ull << (n - 1)) : (1ull << (n - 2));
+            dim3 grid(grid_for(work), n_circ);
+            k_pair<<<grid, 256, 0, st>>>(n, op, mats, mat_stride, state, state_stride);
+            LQ_TRY(check_launch("k_pair"));
+        } else {
+            for (uint32_t b = p.op_begin; b < p.op_end; b += DIAG_MAX_OPS) {
+                int cnt = (int)std::min<uint32_t>(DIAG_MAX_OPS, p.op_end - b);
+                dim3 grid(grid_for(1ull << n), n_circ);
+                k_diag<<<grid, 256, 0, st>>>(n, dp.kops + b, cnt, mats, mat_stride, state, state_stride);
+                LQ_TRY(check_launch("k_diag"));
+            }
+        }
+    }
+    return LQ_OK;
+}
+
+size_t pauli_smem(int K) {
+    return ((size_t)16 << K) + PAULI_MAX_TERMS * (8 + 3 * 4);
+}
+
+template <int RR>
+lq_status launch_pauli_rr(const KPauliPass &P, const PTerm *terms, const double2 *state, uint64_t state_stride,
+                          int n_circ, double *partial, uint64_t slot_stride, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(k_pauli_tile<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)pauli_smem(13)));
+        attr = true;
+    }
+    dim3 grid((unsigned)(1ull << (P.n - P.K)), (unsigned)n_circ);
+    k_pauli_tile<RR><<<grid, 1u << (P.K - RR), pauli_smem(P.K), st>>>(P, terms, state, state_stride, partial,
+                                                                        slot_stride);
+    return check_launch("k_pauli_tile");
+}
+
+lq_status launch_pauli(const PauliPlan &pp, const PTerm *dterms, const double2 *state, uint64_t state_stride,
+                       int n_circ, double *partial, uint64_t slot_stride, double *E, cudaStream_t st) {
+    for (const KPauliPass &P : pp.passes) {
+        switch (std::min(R, P.K)) {
+        case 1: LQ_TRY(launch_pauli_rr<1>(P, dterms, state, state_stride, n_circ, partial, slot_stride, st)); break;
+        case 2: LQ_TRY(launch_pauli_rr<2>(P, dterms, state, state_stride, n_circ, partial, slot_stride, st)); break;
+        case 3: LQ_TRY(launch_pauli_rr<3>(P, dterms, state, state_stride, n_circ, partial, slot_stride, st)); break;
+        default: LQ_TRY(launch_pauli_rr<4>(P, dterms, state, state_stride, n_circ, partial, slot_stride, st)); break;
+        }
+    }
+    for (const auto &D : pp.direct) {
+        dim3 grid(D.n_blocks, n_circ);
+        k_pauli_direct<<<grid, 256, 0, st>>>(pp.n, D.x, dterms + D.term_begin, D.term_end - D.term_begin, state,
+                                             state_stride, partial, slot_stride, D.slot);
+        LQ_TRY(check_launch("k_pauli_direct"));
+    }
+    if (pp.n_slots == 0) {
+        CUDA_TRY(cudaMemsetAsync(E, 0, sizeof(double) * n_circ, st));
+        return LQ_OK;
+    }
+    k_sum_partials<<<n_circ, 256, 0, st>>>(partial, slot_stride, pp.n_slots, E);
+    return check_launch("k_sum_partials");
+}
+
+bool qmap_identity(int n, const int32_t *qm) {
+    for (int q = 0; q < n; q++)
+        if (qm[q] != n - 1 - q) return false;
+    return true;
+}
+
+QMap to_qmap(int n, const int32_t *qm) {
+    QMap m;
+    memset(&m, 0, sizeof(m));
+    for (int q = 0; q < n; q++) m.q[q] = (int8_t)qm[q];
+    return m;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- handles
+struct lq_sv {
+    int n = 0;
+    double2 *d = nullptr;
+    bool owned = false;
+    cudaStream_t stream = nullptr;
+    int32_t qmap[64];
+    DevBuf plan_buf, work_buf;
+    void reset_map() {
+        for (int q = 0; q < n; q++) qmap[q] = n - 1 - q;
+    }
+};
+
+namespace {
+lq_status check_sv(const lq_sv *sv) {
+    if (!sv || !sv->d) return fail(LQ_ERR_ARG, "invalid state handle");
+    return LQ_OK;
+}
+
+// Run a circuit-level plan on one state (apply_circuit / canonicalize / qft).
+lq_status run_single(lq_sv *sv, const Plan &plan, const MatBuilder &mb, const double *theta, size_t n_theta) {
+    if (plan.passes.empty()) return LQ_OK;
+    Blob blob;
+    size_t o_sub = blob.add(plan.subs), o_kop = blob.add(plan.kops), o_spec = blob.add(mb.specs),
+           o_fac = blob.add(mb.factors), o_cst = blob.add(mb.cst);
+    size_t o_th = blob.add(theta, theta ? n_theta * sizeof(double) : 0);
+    LQ_TRY(blob.upload(sv->plan_buf, sv->stream));
+    DevPlan dp;
+    dp.subs = sv->plan_buf.at<KSub>(o_sub);
+    dp.kops = sv->plan_buf.at<KOp>(o_kop);
+    dp.specs = sv->plan_buf.at<MSpec>(o_spec);
+    dp.factors = sv->plan_buf.at<MFactor>(o_fac);
+    dp.cst = sv->plan_buf.at<double2>(o_cst);
+    double2 *mats = nullptr;
+    if (mb.mat_size) {
+        LQ_TRY(sv->work_buf.reserve((size_t)mb.mat_size * sizeof(double2), sv->stream));
+        mats = sv->work_buf.at<double2>(0);
+        k_build_mats<<<grid_for(mb.specs.size()), 256, 0, sv->stream>>>(
+            dp.specs, (int)mb.specs.size(), dp.factors, theta ? sv->plan_buf.at<double>(o_th) : nullptr, nullptr,
+            dp.cst, mats, mb.mat_size, 1);
+        LQ_TRY(check_launch("k_build_mats"));
+    }
+    return launch_passes(plan, dp, sv->d, 0, 1, mats, 0, sv->stream, false);
+}
+
+lq_status canonicalize(lq_sv *sv) {
+    if (qmap_identity(sv->n, sv->qmap)) return LQ_OK;
+    std::vector<POp> ops;
+    int32_t qm[64];
+    memcpy(qm, sv->qmap, sizeof(qm));
+    canonicalize_ops(sv->n, qm, ops);
+    Plan plan;
+    MatBuilder mb;
+    plan_circuit(sv->n, ops, options(), mb, plan);
+    LQ_TRY(run_single(sv, plan, mb, nullptr, 0));
+    memcpy(sv->qmap, qm, sizeof(qm));
+    return LQ_OK;
+}
+
+lq_status sync(cudaStream_t s) {
+    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(cudaGetLastError());
+    return LQ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+const char *lq_last_error(void) { return g_err.c_str(); }
+int lq_version(void) { return LQ_VERSION; }
+
+int lq_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+uint64_t lq_launch_count(void) { return g_launches.load(); }
+
+lq_status lq_set_option(int option, int64_t value) {
+    switch (option) {
+    case LQ_OPT_FUSION: g_opt_fusion = value ? 1 : 0; return LQ_OK;
+    case LQ_OPT_TILE_BITS:
+        if (value != 0 && (value < 1 || value > 12)) return fail(LQ_ERR_ARG, "tile bits must be 0 or 1..12");
+        g_opt_K = value;
+        return LQ_OK;
+    case LQ_OPT_COALESCE_BITS:
+        if (value < 0 || value > 6) return fail(LQ_ERR_ARG, "coalesce bits must be 0..6");
+        g_opt_coalesce = value;
+        return LQ_OK;
+    default: return fail(LQ_ERR_ARG, "unknown option");
+    }
+}
+
+int64_t lq_get_option(int option) {
+    switch (option) {
+    case LQ_OPT_FUSION: return g_opt_fusion.load();
+    case LQ_OPT_TILE_BITS: return g_opt_K.load();
+    case LQ_OPT_COALESCE_BITS: return g_opt_coalesce.load();
+    default: return -1;
+    }
+}
+
+lq_status lq_sv_alloc(int n_qubits, void *cuda_stream, lq_sv **out) {
+    if (!out) return fail(LQ_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (n_qubits < 1 || n_qubits > 40) return fail(LQ_ERR_ARG, "n_qubits must be in [1, 40]");
+    LQ_TRY(have_device());
+    size_t bytes = (size_t)16 << n_qubits;
+    size_t fr = 0, tot = 0;
+    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+    if (bytes > fr) return fail(LQ_ERR_OOM, "state of " + std::to_string(bytes) + " bytes exceeds free device memory");
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LQ_ERR_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    }
+    lq_sv *sv = new lq_sv();
+    sv->n = n_qubits;
+    sv->d = (double2 *)p;
+    sv->owned = true;
+    sv->stream = (cudaStream_t)cuda_stream;
+    sv->reset_map();
+    *out = sv;
+    return LQ_OK;
+}
+
+lq_status lq_sv_wrap(int n_qubits, void *cuda_stream, void *dev_ptr, size_t bytes, lq_sv **out) {
+    if (!out) return fail(LQ_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (n_qubits < 1 || n_qubits > 40) return fail(LQ_ERR_ARG, "n_qubits must be in [1, 40]");
+    if (!dev_ptr || ((uintptr_t)dev_ptr & 15)) return fail(LQ_ERR_ARG, "dev_ptr must be non-NULL and 16-byte aligned");
+    if (bytes < ((size_t)16 << n_qubits)) return fail(LQ_ERR_DIM, "wrapped buffer smaller than 16 * 2^n bytes");
+    LQ_TRY(have_device());
+    lq_sv *sv = new lq_sv();
+    sv->n = n_qubits;
+    sv->d = (double2 *)dev_ptr;
+    sv->owned = false;
+    sv->stream = (cudaStream_t)cuda_stream;
+    sv->reset_map();
+    *out = sv;
+    return LQ_OK;
+}
+
+lq_status lq_sv_free(lq_sv *sv) {
+    if (!sv) return LQ_OK;
+    sv->plan_buf.release(sv->stream);
+    sv->work_buf.release(sv->stream);
+    cudaError_t e = cudaSuccess;
+    if (sv->owned && sv->d) {
+        cudaStreamSynchronize(sv->stream);
+        e = cudaFree(sv->d);
+    }
+    delete sv;
+    if (e != cudaSuccess) return fail(LQ_ERR_CUDA, std::string("cudaFree failed: ") + cudaGetErrorString(e));
+    return LQ_OK;
+}
+
+lq_status lq_sv_set_stream(lq_sv *sv, void *cuda_stream) {
+    LQ_TRY(check_sv(sv));
+    // order the old stream's pending work (and buffer frees) before the new one
+    CUDA_TRY(cudaStreamSynchronize(sv->stream));
+    sv->stream = (cudaStream_t)cuda_stream;
+    return LQ_OK;
+}
+
+int lq_sv_num_qubits(const lq_sv *sv) { return sv ? sv->n : -1; }
+void *lq_sv_device_ptr(const lq_sv *sv) { return sv ? (void *)sv->d : nullptr; }
+
+lq_status lq_sv_qubit_map(const lq_sv *sv, int32_t *map_out) {
+    LQ_TRY(check_sv(sv));
+    if (!map_out) return fail(LQ_ERR_ARG, "map_out is NULL");
+    for (int q = 0; q < sv->n; q++) map_out[q] = sv->qmap[q];
+    return LQ_OK;
+}
+
+lq_status lq_sv_init_basis(lq_sv *sv, uint64_t k) {
+    LQ_TRY(check_sv(sv));
+    if (k >= (1ull << sv->n)) return fail(LQ_ERR_ARG, "basis index out of range");
+    sv->reset_map();
+    const uint64_t N = 1ull << sv->n;
+    k_fill_basis<<<dim3(grid_for(N), 1), 256, 0, sv->stream>>>(N, k, sv->d, 0);
+    return check_launch("k_fill_basis");
+}
+
+lq_status lq_sv_init_random(lq_sv *sv, uint64_t seed) {
+    LQ_TRY(check_sv(sv));
+    sv->reset_map();
+    const uint64_t N = 1ull << sv->n;
+    LQ_TRY(sv->work_buf.reserve(sizeof(double) * (RED_BLOCKS + 1), sv->stream));
+    double *part = sv->work_buf.at<double>(0);
+    k_random_norm<<<RED_BLOCKS, 256, 0, sv->stream>>>(N, seed, part);
+    LQ_TRY(check_launch("k_random_norm"));
+    k_sum_partials<<<1, 256, 0, sv->stream>>>(part, 0, RED_BLOCKS, part + RED_BLOCKS);
+    LQ_TRY(check_launch("k_sum_partials"));
+    k_random_write<<<grid_for(N), 256, 0, sv->stream>>>(N, seed, part + RED_BLOCKS, sv->d);
+    return check_launch("k_random_write");
+}
+
+lq_status lq_sv_norm2(lq_sv *sv, double *out) {
+    LQ_TRY(check_sv(sv));
+    if (!out) return fail(LQ_ERR_ARG, "out is NULL");
+    const uint64_t N = 1ull << sv->n;
+    LQ_TRY(sv->work_buf.reserve(sizeof(double) * (RED_BLOCKS + 1), sv->stream));
+    double *part = sv->work_buf.at<double>(0);
+    k_norm2<<<RED_BLOCKS, 256, 0, sv->stream>>>(N, sv->d, part);
+    LQ_TRY(check_launch("k_norm2"));
+    k_sum_partials<<<1, 256, 0, sv->stream>>>(part, 0, RED_BLOCKS, part + RED_BLOCKS);
+    LQ_TRY(check_launch("k_sum_partials"));
+    CUDA_TRY(cudaMemcpyAsync(out, part + RED_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, sv->stream));
+    return sync(sv->stream);
+}
+
+static lq_status read_impl(lq_sv *sv, const uint64_t *idx, uint64_t offset, uint64_t count, double *host_out) {
+    const uint64_t CH = 1ull << 22;   // 64 MiB chunks
+    size_t need = (size_t)std::min(count, CH) * (sizeof(double2) + (idx ? sizeof(uint64_t) : 0));
+    LQ_TRY(sv->work_buf.reserve(std::max<size_t>(need, 16), sv->stream));
+    QMap m = to_qmap(sv->n, sv->qmap);
+    for (uint64_t c0 = 0; c0 < count; c0 += CH) {
+        uint64_t cnt = std::min(CH, count - c0);
+        double2 *tmp = sv->work_buf.at<double2>(0);
+        uint64_t *didx = nullptr;
+        if (idx) {
+            didx = reinterpret_cast<uint64_t *>(tmp + std::min(count, CH));
+            CUDA_TRY(cudaMemcpyAsync(didx, idx + c0, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice, sv->stream));
+        }
+        k_gather<<<grid_for(cnt), 256, 0, sv->stream>>>(sv->n, m, sv->d, didx, offset + c0, cnt, tmp);
+        LQ_TRY(check_launch("k_gather"));
+        CUDA_TRY(cudaMemcpyAsync(host_out + 2 * c0, tmp, cnt * sizeof(double2), cudaMemcpyDeviceToHost, sv->stream));
+        LQ_TRY(sync(sv->stream));
+    }
+    return LQ_OK;
+}
+
+lq_status lq_sv_read(lq_sv *sv, uint64_t offset, uint64_t count, double *host_out) {
+    LQ_TRY(check_sv(sv));
+    if (!host_out && count) return fail(LQ_ERR_ARG, "host_out is NULL");
+    uint64_t N = 1ull << sv->n;
+    if (offset > N || count > N - offset) return fail(LQ_ERR_DIM, "read range out of bounds");
+    if (!count) return LQ_OK;
+    return read_impl(sv, nullptr, offset, count, host_out);
+}
+
+lq_status lq_sv_gather(lq_sv *sv, const uint64_t *idx, size_t count, double *host_out) {
+    LQ_TRY(check_sv(sv));
+    if (count && (!idx || !host_out)) return fail(LQ_ERR_ARG, "NULL buffer");
+    uint64_t N = 1ull << sv->n;
+    for (size_t i = 0; i < count; i++)
+        if (idx[i] >= N) return fail(LQ_ERR_DIM, "gather index out of range");
+    if (!count) return LQ_OK;
+    return read_impl(sv, idx, 0, count, host_out);
+}
+
+lq_status lq_sv_write(lq_sv *sv, uint64_t offset, uint64_t count, const double *host_in) {
+    LQ_TRY(check_sv(sv));
+    if (!host_in && count) return fail(LQ_ERR_ARG, "host_in is NULL");
+    uint64_t N = 1ull << sv->n;
+    if (offset > N || count > N - offset) return fail(LQ_ERR_DIM, "write range out of bounds");
+    for (uint64_t i = 0; i < 2 * count; i++)
+        if (!std::isfinite(host_in[i])) return fail(LQ_ERR_NONFINITE, "non-finite amplitude");
+    const uint64_t CH = 1ull << 22;
+    LQ_TRY(sv->work_buf.reserve((size_t)std::min(count, CH) * sizeof(double2) + 16, sv->stream));
+    QMap m = to_qmap(sv->n, sv->qmap);
+    for (uint64_t c0 = 0; c0 < count; c0 += CH) {
+        uint64_t cnt = std::min(CH, count - c0);
+        double2 *tmp = sv->work_buf.at<double2>(0);
+        CUDA_TRY(cudaMemcpyAsync(tmp, host_in + 2 * c0, cnt * sizeof(double2), cudaMemcpyHostToDevice, sv->stream));
+        k_scatter<<<grid_for(cnt), 256, 0, sv->stream>>>(sv->n, m, sv->d, offset + c0, cnt, tmp);
+        LQ_TRY(check_launch("k_scatter"));
+        LQ_TRY(sync(sv->stream));
+    }
+    return LQ_OK;
+}
+
+lq_status lq_sv_canonicalize(lq_sv *sv) {
+    LQ_TRY(check_sv(sv));
+    return canonicalize(sv);
+}
+
+lq_status lq_apply_circuit(lq_sv *sv, const lq_gate *gates, size_t n_gates, const double *theta, size_t n_theta) {
+    LQ_TRY(check_sv(sv));
+    LQ_TRY(validate_gates(sv->n, gates, n_gates, theta, n_theta, true, nullptr));
+    if (!n_gates) return LQ_OK;
+    int32_t qm[64];
+    memcpy(qm, sv->qmap, sizeof(qm));
+    std::vector<POp> ops;
+    MatBuilder mb;
+    lower_gates(sv->n, gates, n_gates, qm, ops, mb);
+    Plan plan;
+    plan_circuit(sv->n, ops, options(), mb, plan);
+    LQ_TRY(run_single(sv, plan, mb, theta, n_theta));
+    memcpy(sv->qmap, qm, sizeof(qm));
+    return LQ_OK;
+}
+
+lq_status lq_qft(lq_sv *sv, int inverse) {
+    LQ_TRY(check_sv(sv));
+    int32_t qm[64];
+    memcpy(qm, sv->qmap, sizeof(qm));
+    bool ident = true, rev = true;
+    for (int q = 0; q < sv->n; q++) {
+        ident &= qm[q] == sv->n - 1 - q;
+        rev &= qm[q] == q;
+    }
+    if (!ident && !rev) {
+        LQ_TRY(canonicalize(sv));
+        memcpy(qm, sv->qmap, sizeof(qm));
+    }
+    Plan plan;
+    MatBuilder mb;
+    if (!plan_qft(sv->n, qm, inverse != 0, options(), plan, mb)) return fail(LQ_ERR_STATE, "qft planning failed");
+    LQ_TRY(run_single(sv, plan, mb, nullptr, 0));
+    memcpy(sv->qmap, qm, sizeof(qm));
+    return LQ_OK;
+}
+
+lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_terms, double *out_energy) {
+    LQ_TRY(check_sv(sv));
+    if (!out_energy) return fail(LQ_ERR_ARG, "out_energy is NULL");
+    LQ_TRY(validate_terms(sv->n, terms, n_terms));
+    PauliPlan pp;
+    plan_pauli(sv->n, sv->qmap, terms, n_terms, options(), pp);
+    Blob blob;
+    size_t o_t = blob.add(pp.terms);
+    LQ_TRY(blob.upload(sv->plan_buf, sv->stream));
+    LQ_TRY(sv->work_buf.reserve(sizeof(double) * (pp.n_slots + 2), sv->stream));
+    double *part = sv->work_buf.at<double>(0);
+    double *E = part + pp.n_slots + 1;
+    LQ_TRY(launch_pauli(pp, sv->plan_buf.at<PTerm>(o_t), sv->d, 0, 1, part, pp.n_slots, E, sv->stream));
+    CUDA_TRY(cudaMemcpyAsync(out_energy, E, sizeof(double), cudaMemcpyDeviceToHost, sv->stream));
+    return sync(sv->stream);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- PSR driver (a8)
+struct lq_psr {
+    int n = 0;
+    size_t n_params = 0;
+    int rank = 0, world = 1;
+    cudaStream_t stream = nullptr;
+    Plan plan;
+    MatBuilder mb;
+    PauliPlan pp;
+    std::vector<Shift> shifts;
+    std::vector<PsrPair> pairs;
+    int base_idx = -1;
+    int B = 1;
+    DevBuf blob_buf, states, mats, partials, E;
+    DevPlan dp;
+    const Shift *d_shifts = nullptr;
+    const PsrPair *d_pairs = nullptr;
+    const PTerm *d_terms = nullptr;
+    uint64_t launches_per_run = 0;
+};
+
+extern "C" {
+
+lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, size_t n_params,
+                        const lq_pauli_term *terms, size_t n_terms, int shard_rank, int shard_world,
+                        void *cuda_stream, lq_psr **out) {
+    if (!out) return fail(LQ_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (n_qubits < 1 || n_qubits > 36) return fail(LQ_ERR_ARG, "n_qubits must be in [1, 36]");
+    if (shard_world < 1 || shard_rank < 0 || shard_rank >= shard_world) return fail(LQ_ERR_ARG, "bad shard rank/world");
+    std::vector<int> uses(n_params, 0);
+    LQ_TRY(validate_gates(n_qubits, ansatz, n_gates, nullptr, n_params, false, &uses));
+    LQ_TRY(validate_terms(n_qubits, terms, n_terms));
+    LQ_TRY(have_device());
+    lq_psr *P = new lq_psr();
+    P->n = n_qubits;
+    P->n_params = n_params;
+    P->rank = shard_rank;
+    P->world = shard_world;
+    P->stream = (cudaStream_t)cuda_stream;
+    int32_t qm[64];
+    for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
+    std::vector<POp> ops;
+    lower_gates(n_qubits, ansatz, n_gates, qm, ops, P->mb);
+    plan_circuit(n_qubits, ops, options(), P->mb, P->plan);
+    plan_pauli(n_qubits, qm, terms, n_terms, options(), P->pp);
+    // circuits of this shard: (p, +pi/2), (p, -pi/2) for owned p; base on shard 0.
+    // Parameters used by no gate have E+ == E- identically: g_p = 0 (written by combine).
+    for (size_t p = 0; p < n_params; p++) {
+        if ((int)(p % shard_world) != shard_rank || uses[p] == 0) continue;
+        PsrPair pr;
+        pr.p = (int)p;
+        pr.plus = (int)P->shifts.size();
+        P->shifts.push_back({(int)p, 0, PI / 2});
+        pr.minus = (int)P->shifts.size();
+        P->shifts.push_back({(int)p, 0, -PI / 2});
+        pr.pad = 0;
+        P->pairs.push_back(pr);
+    }
+    if (shard_rank == 0) {
+        P->base_idx = (int)P->shifts.size();
+        P->shifts.push_back({-1, 0, 0.0});
+    }
+    const int n_circ = (int)P->shifts.size();
+    const uint64_t N = 1ull << n_qubits;
+    // batch: >= 2^25 amplitudes per launch when possible, <= 4 GiB of states
+    uint64_t B = std::max<uint64_t>(1, (1ull << 25) / N);
+    B = std::min<uint64_t>(B, std::max<uint64_t>(1, (1ull << 28) / N));
+    B = std::min<uint64_t>(B, std::max(1, n_circ));
+    B = std::min<uint64_t>(B, 65535);
+    P->B = (int)B;
+    cudaStream_t st = P->stream;
+    Blob blob;
+    size_t o_sub = blob.add(P->plan.subs), o_kop = blob.add(P->plan.kops), o_spec = blob.add(P->mb.specs),
+           o_fac = blob.add(P->mb.factors), o_cst = blob.add(P->mb.cst), o_sh = blob.add(P->shifts),
+           o_pr = blob.add(P->pairs), o_t = blob.add(P->pp.terms);
+    lq_status s = blob.upload(P->blob_buf, st);
+    if (s == LQ_OK) s = P->states.reserve((size_t)B * N * sizeof(double2), st);
+    if (s == LQ_OK) s = P->mats.reserve((size_t)B * std::max<uint32_t>(P->mb.mat_size, 1) * sizeof(double2), st);
+    if (s == LQ_OK) s = P->partials.reserve((size_t)B * std::max<uint32_t>(P->pp.n_slots, 1) * sizeof(double), st);
+    if (s == LQ_OK) s = P->E.reserve(sizeof(double) * std::max(n_circ, 1), st);
+    if (s != LQ_OK) {
+        std::string keep = g_err;
+        lq_psr_free(P);
+        g_err = keep;
+        return s;
+    }
+    P->dp.subs = P->blob_buf.at<KSub>(o_sub);
+    P->dp.kops = P->blob_buf.at<KOp>(o_kop);
+    P->dp.specs = P->blob_buf.at<MSpec>(o_spec);
+    P->dp.factors = P->blob_buf.at<MFactor>(o_fac);
+    P->dp.cst = P->blob_buf.at<double2>(o_cst);
+    P->d_shifts = P->blob_buf.at<Shift>(o_sh);
+    P->d_pairs = P->blob_buf.at<PsrPair>(o_pr);
+    P->d_terms = P->blob_buf.at<PTerm>(o_t);
+    *out = P;
+    return LQ_OK;
+}
+
+lq_status lq_psr_run(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev) {
+    if (!P) return fail(LQ_ERR_ARG, "invalid plan");
+    if ((!theta_dev && P->n_params) || (!grad_dev && P->n_params)) return fail(LQ_ERR_ARG, "NULL device pointer");
+    const uint64_t N = 1ull << P->n;
+    const int n_circ = (int)P->shifts.size();
+    cudaStream_t st = P->stream;
+    uint64_t l0 = g_launches.load();
+    double2 *states = P->states.at<double2>(0);
+    double2 *mats = P->mats.at<double2>(0);
+    double *part = P->partials.at<double>(0);
+    double *E = P->E.at<double>(0);
+    const uint32_t ms = std::max<uint32_t>(P->mb.mat_size, 1);
+    for (int c0 = 0; c0 < n_circ; c0 += P->B) {
+        const int nb = std::min(P->B, n_circ - c0);
+        if (P->mb.mat_size) {
+            k_build_mats<<<grid_for((uint64_t)P->mb.specs.size() * nb), 256, 0, st>>>(
+                P->dp.specs, (int)P->mb.specs.size(), P->dp.factors, theta_dev, P->d_shifts + c0, P->dp.cst, mats,
+                ms, nb);
+            LQ_TRY(check_launch("k_build_mats"));
+        }
+        LQ_TRY(launch_passes(P->plan, P->dp, states, N, nb, mats, ms, st, true));
+        LQ_TRY(launch_pauli(P->pp, P->d_terms, states, N, nb, part, std::max<uint32_t>(P->pp.n_slots, 1), E + c0, st));
+    }
+    k_psr_combine<<<1, 256, 0, st>>>(E, P->d_pairs, (int)P->pairs.size(), P->base_idx, grad_dev, (int)P->n_params,
+                                     energy_dev);
+    LQ_TRY(check_launch("k_psr_combine"));
+    P->launches_per_run = g_launches.load() - l0;
+    return LQ_OK;
+}
+
+lq_status lq_psr_stats(const lq_psr *P, uint64_t *n_circuits, uint64_t *n_launches) {
+    if (!P) return fail(LQ_ERR_ARG, "invalid plan");
+    if (n_circuits) *n_circuits = P->shifts.size();
+    if (n_launches) *n_launches = P->launches_per_run;
+    return LQ_OK;
+}
+
+lq_status lq_psr_free(lq_psr *P) {
+    if (!P) return LQ_OK;
+    P->blob_buf.release(P->stream);
+    P->states.release(P->stream);
+    P->mats.release(P->stream);
+    P->partials.release(P->stream);
+    P->E.release(P->stream);
+    delete P;
+    return LQ_OK;
+}
+
+lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gates, const double *theta,
+                              size_t n_params, const lq_pauli_term *terms, size_t n_terms, int shard_rank,
+                              int shard_world, void *cuda_stream, double *grad_out, double *energy_out) {
+    if (n_params && (!theta || !grad_out)) return fail(LQ_ERR_ARG, "theta/grad_out is NULL");
+    for (size_t p = 0; p < n_params; p++)
+        if (!std::isfinite(theta[p])) return fail(LQ_ERR_NONFINITE, "non-finite theta[" + std::to_string(p) + "]");
+    lq_psr *P = nullptr;
+    LQ_TRY(lq_psr_create(n_qubits, ansatz, n_gates, n_params, terms, n_terms, shard_rank, shard_world, cuda_stream,
+                         &P));
+    cudaStream_t st = P->stream;
+    DevBuf io;
+    lq_status s = io.reserve(sizeof(double) * (2 * n_params + 2), st);
+    double *d_theta = io.at<double>(0), *d_grad = d_theta + n_params, *d_e = d_grad + n_params;
+    if (s == LQ_OK && n_params) {
+        cudaError_t e = cudaMemcpyAsync(d_theta, theta, n_params * sizeof(double), cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, cudaGetErrorString(e));
+    }
+    if (s == LQ_OK) s = lq_psr_run(P, d_theta, d_grad, d_e);
+    if (s == LQ_OK && n_params) {
+        cudaError_t e = cudaMemcpyAsync(grad_out, d_grad, n_params * sizeof(double), cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, cudaGetErrorString(e));
+    }
+    if (s == LQ_OK && energy_out) {
+        cudaError_t e = cudaMemcpyAsync(energy_out, d_e, sizeof(double), cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, cudaGetErrorString(e));
+    }
+    if (s == LQ_OK) s = sync(st);
+    std::string keep = g_err;
+    io.release(st);
+    lq_psr_free(P);
+    if (s != LQ_OK) g_err = keep;
+    return s;
+}
+
+// Host-only planning diagnostics (no device needed): plan `gates` on n
+// qubits with the current options and report pass counts and a text dump.
+lq_status lq_plan_describe(int n_qubits, const lq_gate *gates, size_t n_gates, uint64_t *n_passes,
+                           uint64_t *n_tile, char *buf, size_t buf_len) {
+    if (n_qubits < 1 || n_qubits > 40) return fail(LQ_ERR_ARG, "n_qubits must be in [1, 40]");
+    std::vector<int> uses(1 << 16, 0);
+    // parameters are not bound here; validate structure with a permissive theta count
+    LQ_TRY(validate_gates(n_qubits, gates, n_gates, nullptr, 1 << 16, false, nullptr));
+    int32_t qm[64];
+    for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
+    std::vector<POp> ops;
+    MatBuilder mb;
+    lower_gates(n_qubits, gates, n_gates, qm, ops, mb);
+    Plan plan;
+    plan_circuit(n_qubits, ops, options(), mb, plan);
+    if (n_passes) *n_passes = plan.passes.size();
+    if (n_tile) *n_tile = plan.n_tile;
+    if (buf && buf_len) {
+        std::string d = "ops=" + std::to_string(ops.size()) + " " + describe(plan);
+        size_t k = std::min(buf_len - 1, d.size());
+        memcpy(buf, d.data(), k);
+        buf[k] = 0;
+    }
+    return LQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,176 @@
+// lq_internal.h -- data structures shared by the host planner (planner.cpp)
+// and the sm_100a kernels (kernels.cuh).  Product code; shares nothing with
+// oracle/.
+//
+// Execution model.  A state of n qubits is 2^n complex128
+// amplitudes in HBM.  Work is a list of PASSES; each pass streams the whole
+// state through the SMs exactly once (32 B/amp of HBM traffic) and applies
+// many gates on the way:
+//
+//   TILE pass  : a CTA owns one tile = the 2^K amplitudes whose index bits
+//                outside the tile-bit set T are fixed.  Each thread keeps
+//                2^R amplitudes in registers (the "register bits" S of the
+//                current sub-block); gates whose target bits lie in S are
+//                applied in registers; sub-blocks with different S exchange
+//                amplitudes through shared memory.  Controls and diagonal
+//                factors on bits outside S are thread constants, so they
+//                never constrain T.
+//   PAIR pass  : one 1q/2q gate on arbitrary bits, strided pairs/quads with
+//                16-byte loads (a4).
+//   DIAG pass  : any number of diagonal/phase gates on any bits (a3).
+//
+// Physical bit p of an amplitude index holds logical qubit q with
+// qmap[q] = p (identity: p = n-1-q).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define LQ_HD __host__ __device__
+#else
+#define LQ_HD
+#endif
+
+namespace lq {
+
+constexpr int R = 4;          // register bits per thread: 16 amplitudes in registers
+constexpr int NREG = 1 << R;
+constexpr int MAXK = 14;      // max tile bits (2^14 * 16 B = 256 KiB > smem; 13 is the practical max)
+constexpr uint8_t NOREG = 0xFF;
+
+enum KOpType : uint8_t {
+    K_U1 = 0,   // general 2x2 on register bit r0 (mat: U00 U01 U10 U11)
+    K_D1 = 1,   // diagonal (d0, d1) on one bit: register r0, or thread-constant physical bit b0
+    K_X = 2,    // X-type permutation on register bit r0 (CNOT/CCX/X)
+    K_U2 = 3,   // general 4x4 on register bits (r0 high, r1 low)
+    K_D2 = 4,   // diagonal on two bits (r0|b0 high, r1|b1 low): mat d[4]
+    K_SWAP = 5, // exchange register bits r0, r1
+    K_QFT = 6,  // QFT stage on register bit r0 (logical bit qj); aux = twiddle table
+    K_SCALE = 7 // multiply every amplitude by `scale`
+};
+
+enum KOpFlags : uint8_t {
+    QF_INVERSE = 1,   // inverse stage (conj twiddle before the butterfly)
+    QF_REVERSED = 2,  // layout is bit-reversed (logical index = brev(physical))
+    QF_HEAD = 4       // first QFT op of its sub-block: compute the thread twiddle for j = b1
+};
+
+// One op inside a sub-block.  Controls on register bits are the register
+// mask rcm (all must be 1); controls on other bits are the physical mask
+// cmask, a thread constant.  `code` selects a specialised code path in the
+// tile kernel (CodeTile); C_GENERIC falls back to a switch on `type`.
+struct KOp {
+    uint8_t type;
+    uint8_t code;
+    uint8_t r0, r1;      // register positions (NOREG if not a register bit)
+    uint8_t rcm;         // register-position control mask
+    uint8_t b0, b1;      // physical bits for thread-constant diagonal bits (QFT: b1 = largest j of the sub-block)
+    uint8_t flags;       // QF_*
+    uint64_t cmask;      // physical non-register control mask
+    uint32_t mat;        // source of the op's table (double2 units): per-circuit matrix block, or cst
+    uint32_t aux;        // where the kernel stages that table in shared memory (pass-local, double2 units)
+    uint8_t qj;          // QFT: logical bit j of the stage
+    uint8_t pad[7];
+};
+static_assert(sizeof(KOp) == 32, "KOp layout");
+
+// Specialised tile-kernel code paths.
+enum CodeTile : uint8_t {
+    C_U1 = 0,        // + r0 (0..3): general 2x2, no register control
+    C_X = 4,         // + r0: X, no register control
+    C_CX = 8,        // + 4*c + t: X on register t controlled by register c
+    C_D1R = 24,      // + r0: diagonal on a register bit, no register control
+    C_D1T = 28,      // diagonal on a thread-constant bit, no register control
+    C_QFT = 29,      // + r0
+    C_SCALE = 33,
+    C_GENERIC = 34
+};
+
+struct KSub {
+    uint8_t S[R];        // local bit positions held in registers (ascending)
+    uint32_t op_begin, op_end;
+};
+
+enum PassFlags : uint32_t {
+    PF_LOAD_ZERO = 1     // synthesise |0...0> instead of loading (fused init_basis(0))
+};
+
+// Tile pass descriptor, passed by value to the kernel.
+constexpr int MAX_PASS_OPS = 96;   // ops staged in shared memory per tile pass
+
+// table size (double2) an op stages in shared memory
+LQ_HD inline int op_table_size(uint8_t type) {
+    switch (type) {
+    case K_U1: return 4;
+    case K_D1: return 2;
+    case K_U2: return 16;
+    case K_D2: return 4;
+    case K_QFT: return 16;
+    case K_SCALE: return 1;
+    default: return 0;
+    }
+}
+
+struct KPass {
+    int32_t n;           // index bits of one state
+    int32_t K;           // tile bits
+    uint32_t sub_begin, sub_end;
+    uint32_t op_begin, op_end;   // contiguous op range of the pass
+    uint32_t smat;       // staged table size (double2)
+    uint32_t flags;
+    uint8_t T[MAXK];     // physical bit of each local bit, ascending
+    uint8_t Sload[R];    // local bits of the register mapping used for the HBM load
+    uint8_t Sstore[R];   // ... and for the HBM store
+    uint8_t pad[2];
+};
+
+// Matrix construction (device-side, per circuit): every fused op has a
+// MSpec that multiplies its factor gates (later factors on the left).
+enum MForm : uint8_t { MF_U2x2 = 0, MF_DIAG2 = 1, MF_U4x4 = 2, MF_DIAG4 = 3 };
+
+// Factor kinds use lq_kind numbering for gates; the angle is theta[pidx]
+// (+ the circuit's shift if pidx is the shifted parameter) or `angle`.
+struct MFactor {
+    int32_t kind;
+    int32_t pidx;
+    double angle;
+    int32_t cst;         // offset of a constant matrix (U1: 4, U2: 16 double2) in cst, else -1
+    int32_t pad;
+};
+
+struct MSpec {
+    uint32_t out;        // output offset (double2 units) in the circuit's matrix block
+    uint32_t f_begin, f_end;
+    uint32_t form;       // MForm
+};
+
+// Per-circuit parameter shift (PSR): theta[pidx] += delta.
+struct Shift {
+    int32_t pidx;        // -1: unshifted
+    int32_t pad;
+    double delta;
+};
+
+// Pauli expectation tile pass.
+struct PTerm {
+    double coeff;
+    uint64_t zfull;      // physical z mask (all bits)
+    uint32_t zloc;       // z mask restricted to the tile, in local bit positions
+    uint32_t xloc;       // x mask in local bit positions (all x bits lie in the tile)
+    uint32_t yph;        // i^{yph}: number of Y factors mod 4
+    uint32_t pad;
+};
+
+constexpr uint32_t PAULI_MAX_TERMS_PLAN = 256;   // == PAULI_MAX_TERMS in kernels.cuh
+
+struct KPauliPass {
+    int32_t n;
+    int32_t K;
+    uint32_t term_begin, term_end;
+    uint32_t slot;       // first partial-sum slot of this pass (one per tile)
+    uint32_t pad;
+    uint8_t T[MAXK];
+    uint8_t pad2[2];
+};
+
+}  // namespace lq

@@ -1,0 +1,701 @@
+// planner.cpp -- host gate-fusion planner.  See planner.h.
+#include "planner.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+
+namespace lq {
+
+static inline int popc(uint64_t x) { return __builtin_popcountll(x); }
+static inline uint64_t bit(int b) { return 1ull << b; }
+
+uint64_t POp::full() const {
+    switch (type) {
+    case K_U1: case K_X: case K_QFT: return bit(t0);
+    case K_U2: case K_SWAP: return bit(t0) | bit(t1);
+    default: return 0;
+    }
+}
+
+uint64_t POp::touch() const {
+    uint64_t m = ctrl | full();
+    if (type == K_D1) m |= bit(t0);
+    if (type == K_D2) m |= bit(t0) | bit(t1);
+    return m;
+}
+
+// Two ops commute if every bit they share is acted on diagonally (as a
+// control or a diagonal factor) by both.
+bool commute(const POp &a, const POp &b) {
+    return (a.full() & b.touch()) == 0 && (b.full() & a.touch()) == 0;
+}
+
+int MatBuilder::add_spec(MForm form, const std::vector<MFactor> &f) {
+    MSpec s;
+    s.out = mat_size;
+    s.f_begin = (uint32_t)factors.size();
+    factors.insert(factors.end(), f.begin(), f.end());
+    s.f_end = (uint32_t)factors.size();
+    s.form = form;
+    static const uint32_t sz[4] = {4, 2, 16, 4};
+    mat_size += sz[form];
+    specs.push_back(s);
+    return (int)specs.size() - 1;
+}
+
+int MatBuilder::add_const(const double *v, int n_complex) {
+    int off = (int)(cst.size() / 2);
+    cst.insert(cst.end(), v, v + 2 * n_complex);
+    return off;
+}
+
+int auto_tile_bits(int n) { return n < 12 ? n : 12; }
+
+// --------------------------------------------------------------------------
+// Lowering of user gates (PAPER.md:77-139 operations) to physical-bit ops.
+// --------------------------------------------------------------------------
+static bool is_1q(int k) { return k <= LQ_RZ || k == LQ_U1; }
+static bool is_diag_1q(int k) {
+    return k == LQ_Z || k == LQ_S || k == LQ_SDG || k == LQ_T || k == LQ_TDG || k == LQ_RZ;
+}
+
+void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
+                 std::vector<POp> &ops, MatBuilder &mb) {
+    std::vector<std::vector<MFactor>> fl;   // factor list per op
+    std::vector<int> last(64, -1);          // last op touching each physical bit
+    std::vector<char> fusable;              // op is an uncontrolled 1q op
+    size_t base = ops.size();
+    auto touch_all = [&](int idx) {
+        uint64_t m = ops[idx].touch();
+        while (m) { int b = __builtin_ctzll(m); last[b] = idx; m &= m - 1; }
+    };
+    for (size_t g = 0; g < n_gates; g++) {
+        const lq_gate &G = gates[g];
+        MFactor f{G.kind, G.param_idx, G.angle, -1, 0};
+        int k = G.kind;
+        if (k == LQ_SWAP) {
+            std::swap(qmap[G.q0], qmap[G.q1]);
+            continue;
+        }
+        if (is_1q(k)) {
+            if (k == LQ_U1) f.cst = mb.add_const(G.mat, 4);
+            int b = qmap[G.q0];
+            int prev = last[b];
+            if (prev >= (int)base && fusable[prev - base] && ops[prev].t0 == b) {
+                // no op touched bit b since `prev`: this gate commutes with
+                // everything in between, so it can join `prev`.
+                POp &P = ops[prev];
+                fl[prev - base].push_back(f);
+                bool d = (P.type == K_D1) && is_diag_1q(k);
+                P.type = d ? K_D1 : K_U1;
+                continue;
+            }
+            POp op;
+            op.type = is_diag_1q(k) ? K_D1 : (k == LQ_X ? K_X : K_U1);
+            op.t0 = b;
+            ops.push_back(op);
+            fl.push_back({f});
+            fusable.push_back(1);
+            touch_all((int)ops.size() - 1);
+            continue;
+        }
+        POp op;
+        switch (k) {
+        case LQ_CNOT: op.type = K_X; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); break;
+        case LQ_CCX:  op.type = K_X; op.t0 = qmap[G.q2]; op.ctrl = bit(qmap[G.q0]) | bit(qmap[G.q1]); break;
+        case LQ_CZ:   op.type = K_D1; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); f.kind = LQ_Z; break;
+        case LQ_CP:   op.type = K_D1; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); break;
+        case LQ_CRY:  op.type = K_U1; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); f.kind = LQ_RY; break;
+        case LQ_U2:   op.type = K_U2; op.t0 = qmap[G.q0]; op.t1 = qmap[G.q1]; f.cst = mb.add_const(G.mat, 16); break;
+        case LQ_RXX: case LQ_RYY:
+                      op.type = K_U2; op.t0 = qmap[G.q0]; op.t1 = qmap[G.q1]; break;
+        case LQ_RZZ:  op.type = K_D2; op.t0 = qmap[G.q0]; op.t1 = qmap[G.q1]; break;
+        default: break;
+        }
+        ops.push_back(op);
+        fl.push_back(op.type == K_X ? std::vector<MFactor>{} : std::vector<MFactor>{f});
+        fusable.push_back(0);
+        touch_all((int)ops.size() - 1);
+    }
+    for (size_t i = base; i < ops.size(); i++) {
+        POp &P = ops[i];
+        auto &F = fl[i - base];
+        if (P.type == K_X && F.size() <= 1) { P.spec = -1; continue; }
+        if (P.type == K_X) P.type = K_U1;
+        MForm form = P.type == K_D1 ? MF_DIAG2 : P.type == K_U1 ? MF_U2x2
+                   : P.type == K_U2 ? MF_U4x4 : MF_DIAG4;
+        P.spec = mb.add_spec(form, F);
+    }
+}
+
+void canonicalize_ops(int n, int32_t *qmap, std::vector<POp> &ops) {
+    for (int q = 0; q < n; q++) {
+        int target = n - 1 - q;
+        if (qmap[q] == target) continue;
+        int q2 = -1;
+        for (int r = 0; r < n; r++) if (qmap[r] == target) q2 = r;
+        POp op;
+        op.type = K_SWAP;
+        op.t0 = std::max(qmap[q], target);
+        op.t1 = std::min(qmap[q], target);
+        ops.push_back(op);
+        std::swap(qmap[q], qmap[q2]);
+    }
+}
+
+// --------------------------------------------------------------------------
+// Tile / sub-block planning
+// --------------------------------------------------------------------------
+namespace {
+
+struct Blocker {
+    uint64_t bF = 0, bT = 0;
+    bool blocked(const POp &o) const { return (o.full() & bT) || (o.touch() & bF); }
+    void add(const POp &o) { bF |= o.full(); bT |= o.touch(); }
+};
+
+// first-fit absorption of `rem` into a tile whose bit set starts at Tm.
+static void first_fit(const std::vector<POp> &ops, const std::vector<int> &rem, int K,
+                      uint64_t &Tm, std::vector<int> &absorbed) {
+    Blocker blk;
+    for (int i : rem) {
+        const POp &o = ops[i];
+        if (blk.blocked(o)) { blk.add(o); continue; }
+        uint64_t need = o.full() & ~Tm;
+        if (popc(Tm | need) <= K) { Tm |= need; absorbed.push_back(i); }
+        else blk.add(o);
+    }
+}
+
+static int score(const std::vector<POp> &ops, const std::vector<int> &absorbed) {
+    int s = 0;
+    for (int i : absorbed) s += ops[i].diag() ? 1 : 4;
+    return s;
+}
+
+// Count ops absorbable with a FIXED tile bit set Tm.
+static void absorb_fixed(const std::vector<POp> &ops, const std::vector<int> &rem, uint64_t Tm,
+                         std::vector<int> &absorbed) {
+    Blocker blk;
+    for (int i : rem) {
+        const POp &o = ops[i];
+        if (blk.blocked(o) || (o.full() & ~Tm)) { blk.add(o); continue; }
+        absorbed.push_back(i);
+    }
+}
+
+struct LocalMap {
+    int K;
+    uint8_t T[MAXK];
+    int loc[64];
+    LocalMap(uint64_t Tm) {
+        K = 0;
+        for (int b = 0; b < 64; b++) loc[b] = -1;
+        for (int b = 0; b < 64; b++)
+            if (Tm & bit(b)) { loc[b] = K; T[K++] = (uint8_t)b; }
+    }
+    uint32_t local(uint64_t phys) const {
+        uint32_t m = 0;
+        while (phys) { int b = __builtin_ctzll(phys); if (loc[b] >= 0) m |= 1u << loc[b]; phys &= phys - 1; }
+        return m;
+    }
+};
+
+static int lowrun_of(const LocalMap &L) {
+    int r = 0;
+    while (r < L.K && L.T[r] == r) r++;
+    return r;
+}
+
+// fill a local register mask up to Rr bits
+static uint32_t fill_S(uint32_t Sm, int K, int Rr, int lowrun) {
+    for (int b = K - 1; b >= 0 && popc(Sm) < Rr; b--)
+        if (b >= std::min(lowrun, 3) && !(Sm & (1u << b))) Sm |= 1u << b;
+    for (int b = 0; b < K && popc(Sm) < Rr; b++)
+        if (!(Sm & (1u << b))) Sm |= 1u << b;
+    return Sm;
+}
+
+static void mask_to_S(uint32_t Sm, uint8_t *S) {
+    int i = 0;
+    for (int b = 0; b < 32 && i < R; b++) if (Sm & (1u << b)) S[i++] = (uint8_t)b;
+    for (; i < R; i++) S[i] = 0;
+}
+
+static KOp lower_tile_op(const POp &o, const LocalMap &L, const uint8_t *S, int Rr,
+                         const std::vector<uint32_t> &mat_off) {
+    KOp k{};
+    k.type = o.type;
+    k.r0 = k.r1 = NOREG;
+    auto reg = [&](int p) -> uint8_t {
+        if (p < 0 || L.loc[p] < 0) return NOREG;
+        for (int i = 0; i < Rr; i++) if (S[i] == L.loc[p]) return (uint8_t)i;
+        return NOREG;
+    };
+    k.r0 = reg(o.t0);
+    if (o.t1 >= 0) k.r1 = reg(o.t1);
+    k.b0 = (uint8_t)(o.t0 >= 0 ? o.t0 : 0);
+    k.b1 = (uint8_t)(o.t1 >= 0 ? o.t1 : 0);
+    uint64_t c = o.ctrl;
+    while (c) {
+        int b = __builtin_ctzll(c);
+        uint8_t r = reg(b);
+        if (r != NOREG) k.rcm |= (uint8_t)(1u << r); else k.cmask |= bit(b);
+        c &= c - 1;
+    }
+    k.flags = o.qflags;
+    k.qj = o.qj;
+    k.mat = o.spec >= 0 ? mat_off[o.spec] : 0;
+    return k;
+}
+
+static KOp lower_flat_op(const POp &o, const std::vector<uint32_t> &mat_off) {
+    KOp k{};
+    k.type = o.type;
+    k.r0 = k.r1 = NOREG;
+    k.b0 = (uint8_t)(o.t0 >= 0 ? o.t0 : 0);
+    k.b1 = (uint8_t)(o.t1 >= 0 ? o.t1 : 0);
+    k.cmask = o.ctrl;
+    k.mat = o.spec >= 0 ? mat_off[o.spec] : 0;
+    k.code = C_GENERIC;
+    return k;
+}
+
+// Pick the specialised tile-kernel path of a lowered op.
+static uint8_t tile_code(const KOp &k) {
+    switch (k.type) {
+    case K_U1:
+        if (k.rcm == 0 && k.r0 < R) return (uint8_t)(C_U1 + k.r0);
+        break;
+    case K_X:
+        if (k.rcm == 0 && k.r0 < R) return (uint8_t)(C_X + k.r0);
+        if (__builtin_popcount(k.rcm) == 1 && k.r0 < R) return (uint8_t)(C_CX + 4 * __builtin_ctz(k.rcm) + k.r0);
+        break;
+    case K_D1:
+        if (k.rcm == 0) return k.r0 < R ? (uint8_t)(C_D1R + k.r0) : (uint8_t)C_D1T;
+        break;
+    case K_QFT:
+        if (k.r0 < R) return (uint8_t)(C_QFT + k.r0);
+        break;
+    case K_SCALE:
+        return C_SCALE;
+    default:
+        break;
+    }
+    return C_GENERIC;
+}
+
+// Assign shared-memory staging offsets to the ops of a tile pass.
+static void finalize_pass_tables(PlanPass &pp, Plan &plan) {
+    pp.kp.op_begin = plan.subs[pp.kp.sub_begin].op_begin;
+    pp.kp.op_end = plan.subs[pp.kp.sub_end - 1].op_end;
+    uint32_t off = 0;
+    for (uint32_t i = pp.kp.op_begin; i < pp.kp.op_end; i++) {
+        plan.kops[i].code = tile_code(plan.kops[i]);
+        plan.kops[i].aux = off;
+        off += (uint32_t)op_table_size(plan.kops[i].type);
+    }
+    pp.kp.smat = off;
+}
+
+// Build a TILE pass from absorbed ops (execution order) and tile mask Tm.
+static void emit_tile(int n, int K, int Rr, uint64_t Tm, const std::vector<POp> &ops,
+                      const std::vector<int> &absorbed, const std::vector<uint32_t> &mat_off,
+                      Plan &plan) {
+    LocalMap L(Tm);
+    int lowrun = (n > K) ? lowrun_of(L) : 0;
+    PlanPass pp;
+    pp.kind = PASS_TILE;
+    pp.kp.n = n;
+    pp.kp.K = K;
+    pp.kp.flags = 0;
+    memcpy(pp.kp.T, L.T, MAXK);
+    pp.kp.sub_begin = (uint32_t)plan.subs.size();
+    pp.n_ops = (int)absorbed.size();
+
+    std::vector<int> rem = absorbed;
+    std::vector<std::pair<uint32_t, std::vector<int>>> blocks;
+    while (!rem.empty()) {
+        uint32_t Sm = 0;
+        Blocker blk;
+        std::vector<int> taken, left;
+        for (int i : rem) {
+            const POp &o = ops[i];
+            if (blk.blocked(o)) { blk.add(o); left.push_back(i); continue; }
+            uint32_t need = L.local(o.full()) & ~Sm;
+            if (popc(Sm | need) <= Rr) { Sm |= need; taken.push_back(i); }
+            else { blk.add(o); left.push_back(i); }
+        }
+        blocks.push_back({Sm, taken});
+        rem.swap(left);
+    }
+    // fill the register sets; the first and last prefer non-lane high bits
+    for (auto &b : blocks) b.first = fill_S(b.first, K, Rr, lowrun);
+    uint32_t lane_forbid = (uint32_t)((1u << std::min(lowrun, 3)) - 1);
+    uint32_t top = 0;
+    for (int b = K - 1; b >= 0 && popc(top) < Rr; b--) top |= 1u << b;
+    uint32_t Sl = blocks.front().first, Ss = blocks.back().first;
+    if (Sl & lane_forbid) Sl = top;
+    if (Ss & lane_forbid) Ss = top;
+    mask_to_S(Sl, pp.kp.Sload);
+    mask_to_S(Ss, pp.kp.Sstore);
+    for (auto &b : blocks) {
+        KSub s{};
+        mask_to_S(b.first, s.S);
+        s.op_begin = (uint32_t)plan.kops.size();
+        for (int i : b.second) plan.kops.push_back(lower_tile_op(ops[i], L, s.S, Rr, mat_off));
+        s.op_end = (uint32_t)plan.kops.size();
+        plan.subs.push_back(s);
+    }
+    pp.kp.sub_end = (uint32_t)plan.subs.size();
+    finalize_pass_tables(pp, plan);
+    plan.passes.push_back(pp);
+    plan.n_tile++;
+}
+
+}  // namespace
+
+void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, const MatBuilder &mb,
+                  Plan &plan) {
+    std::vector<uint32_t> mat_off;
+    for (auto &sp : mb.specs) mat_off.push_back(sp.out);
+    int K = opt.K > 0 ? std::min(opt.K, n) : auto_tile_bits(n);
+    if (K > 12) K = 12;   // two 2^K buffers must fit in shared memory
+    if (n <= K) K = n;
+    int Rr = std::min(R, K);
+    plan.n = n;
+    plan.K = K;
+    if (!opt.fusion) {
+        for (const POp &o : ops) {
+            PlanPass pp;
+            pp.kind = o.diag() ? PASS_DIAG : PASS_PAIR;
+            pp.op_begin = (uint32_t)plan.kops.size();
+            plan.kops.push_back(lower_flat_op(o, mat_off));
+            pp.op_end = (uint32_t)plan.kops.size();
+            pp.n_ops = 1;
+            plan.passes.push_back(pp);
+            (o.diag() ? plan.n_diag : plan.n_pair)++;
+        }
+        return;
+    }
+    // the coalescing run must leave room for a 2-qubit gate's two target bits
+    int c = std::max(0, std::min(opt.coalesce, K - 2));
+    uint64_t mand = (n > K) ? ((1ull << c) - 1) : ((n >= 64) ? ~0ull : ((1ull << n) - 1));
+    std::vector<int> rem(ops.size());
+    for (size_t i = 0; i < ops.size(); i++) rem[i] = (int)i;
+    while (!rem.empty()) {
+        uint64_t Tm = mand;
+        std::vector<int> absorbed, absorbed_w;
+        first_fit(ops, rem, K, Tm, absorbed);
+        // local search works on a window of the next ops (bounded cost)
+        std::vector<int> window(rem.begin(), rem.begin() + std::min<size_t>(rem.size(), 384));
+        {
+            std::vector<int> a0;
+            absorb_fixed(ops, window, Tm, a0);
+            absorbed_w.swap(a0);
+        }
+        int best = score(ops, absorbed_w);
+        uint64_t Tm0 = Tm;
+        // local search: swap one free tile bit for another if it absorbs more
+        if (n > K) {
+            for (int iter = 0; iter < 2; iter++) {
+                bool improved = false;
+                // fill Tm to K bits first with the bits most used by blocked ops
+                for (int out = 0; out < n; out++) {
+                    if (!(Tm & bit(out)) || (mand & bit(out))) continue;
+                    for (int in = 0; in < n; in++) {
+                        if (Tm & bit(in)) continue;
+                        uint64_t T2 = (Tm & ~bit(out)) | bit(in);
+                        std::vector<int> a2;
+                        absorb_fixed(ops, window, T2, a2);
+                        int s2 = score(ops, a2);
+                        if (s2 > best) { best = s2; Tm = T2; improved = true; break; }
+                    }
+                }
+                if (popc(Tm) < K) {
+                    for (int in = 0; in < n && popc(Tm) < K; in++) {
+                        if (Tm & bit(in)) continue;
+                        std::vector<int> a2;
+                        absorb_fixed(ops, window, Tm | bit(in), a2);
+                        int s2 = score(ops, a2);
+                        if (s2 > best) { best = s2; Tm |= bit(in); improved = true; }
+                    }
+                }
+                if (!improved) break;
+            }
+            if (Tm != Tm0) {
+                absorbed.clear();
+                absorb_fixed(ops, rem, Tm, absorbed);
+            }
+        }
+        if (absorbed.empty()) absorbed.push_back(rem[0]);   // progress guarantee
+        if (absorbed.size() > (size_t)MAX_PASS_OPS) absorbed.resize(MAX_PASS_OPS);   // a valid prefix
+        int n_full = 0;
+        for (int i : absorbed) n_full += ops[i].diag() ? 0 : 1;
+        if (n_full == 0) {
+            PlanPass pp;
+            pp.kind = PASS_DIAG;
+            pp.op_begin = (uint32_t)plan.kops.size();
+            for (int i : absorbed) plan.kops.push_back(lower_flat_op(ops[i], mat_off));
+            pp.op_end = (uint32_t)plan.kops.size();
+            pp.n_ops = (int)absorbed.size();
+            plan.passes.push_back(pp);
+            plan.n_diag++;
+        } else if (absorbed.size() == 1 && (n > K || popc(ops[absorbed[0]].full()) > K)) {
+            PlanPass pp;
+            pp.kind = PASS_PAIR;
+            pp.op_begin = (uint32_t)plan.kops.size();
+            plan.kops.push_back(lower_flat_op(ops[absorbed[0]], mat_off));
+            pp.op_end = (uint32_t)plan.kops.size();
+            pp.n_ops = 1;
+            plan.passes.push_back(pp);
+            plan.n_pair++;
+        } else {
+            // fill the tile to exactly K bits, lowest free bits first (longer
+            // contiguous runs for coalescing)
+            for (int b = 0; b < n && popc(Tm) < K; b++) Tm |= bit(b);
+            emit_tile(n, K, Rr, Tm, ops, absorbed, mat_off, plan);
+        }
+        // remove absorbed from rem (absorbed is a subsequence of rem)
+        std::vector<int> left;
+        size_t j = 0;
+        for (int i : rem) {
+            if (j < absorbed.size() && absorbed[j] == i) { j++; continue; }
+            left.push_back(i);
+        }
+        rem.swap(left);
+    }
+}
+
+// --------------------------------------------------------------------------
+// QFT.  Stage for logical bit j (qubit n-1-j): butterfly
+// (u, w) -> (u + w, u - w) then multiply the bit-j-set output by
+// exp(i pi (x mod 2^j) / 2^j), x the logical index -- Alg. 3's H(i) followed
+// by all CP(pi/2^{k-i}) controlled by qubit i.  The 1/sqrt2 of each H is
+// applied once per pass (K_SCALE).  The closing SWAP layer is the layout
+// relabel.
+// --------------------------------------------------------------------------
+static uint64_t brev_n(uint64_t x, int n) {
+    uint64_t r = 0;
+    for (int i = 0; i < n; i++) if (x & bit(i)) r |= bit(n - 1 - i);
+    return r;
+}
+
+bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &plan,
+              MatBuilder &mb) {
+    bool ident = true, rev = true;
+    for (int q = 0; q < n; q++) {
+        if (qmap[q] != n - 1 - q) ident = false;
+        if (qmap[q] != q) rev = false;
+    }
+    if (!ident && !rev) return false;
+    bool layout_rev = ident ? false : true;
+    if (inverse) layout_rev = !layout_rev;
+    std::vector<int> js;
+    if (!inverse) for (int j = n - 1; j >= 0; j--) js.push_back(j);
+    else for (int j = 0; j < n; j++) js.push_back(j);
+    auto phys = [&](int j) { return layout_rev ? n - 1 - j : j; };
+
+    int K = opt.K > 0 ? std::min(opt.K, n) : auto_tile_bits(n);
+    if (K > 12) K = 12;
+    if (n <= K) K = n;
+    int Rr = std::min(R, K);
+    int c = std::max(0, std::min(opt.coalesce, K - 1));   // room for at least one stage bit
+    uint64_t mand = (n > K) ? ((1ull << c) - 1) : ((1ull << n) - 1);
+    plan.n = n;
+    plan.K = K;
+    size_t s = 0;
+    while (s < js.size()) {
+        uint64_t Tm = mand;
+        std::vector<int> st;
+        while (s < js.size() && popc(Tm | bit(phys(js[s]))) <= K) {
+            Tm |= bit(phys(js[s]));
+            st.push_back(js[s]);
+            s++;
+        }
+        for (int b = 0; b < n && popc(Tm) < K; b++) Tm |= bit(b);
+        LocalMap L(Tm);
+        int lowrun = (n > K) ? lowrun_of(L) : 0;
+        PlanPass pp;
+        pp.kind = PASS_TILE;
+        pp.kp.n = n;
+        pp.kp.K = K;
+        memcpy(pp.kp.T, L.T, MAXK);
+        pp.kp.sub_begin = (uint32_t)plan.subs.size();
+        pp.n_ops = (int)st.size();
+        std::vector<uint32_t> Sms;
+        for (size_t a = 0; a < st.size(); a += Rr) {
+            uint32_t Sm = 0;
+            for (size_t b = a; b < std::min(st.size(), a + Rr); b++) Sm |= 1u << L.loc[phys(st[b])];
+            Sms.push_back(fill_S(Sm, K, Rr, lowrun));
+        }
+        uint32_t lane_forbid = (uint32_t)((1u << std::min(lowrun, 3)) - 1);
+        uint32_t top = 0;
+        for (int b = K - 1; b >= 0 && popc(top) < Rr; b--) top |= 1u << b;
+        uint32_t Sl = Sms.front(), Ss = Sms.back();
+        if (Sl & lane_forbid) Sl = top;
+        if (Ss & lane_forbid) Ss = top;
+        mask_to_S(Sl, pp.kp.Sload);
+        mask_to_S(Ss, pp.kp.Sstore);
+        for (size_t a = 0, blk = 0; a < st.size(); a += Rr, blk++) {
+            KSub sb{};
+            mask_to_S(Sms[blk], sb.S);
+            sb.op_begin = (uint32_t)plan.kops.size();
+            for (size_t b = a; b < std::min(st.size(), a + Rr); b++) {
+                int j = st[b], p = phys(j);
+                KOp k{};
+                k.type = K_QFT;
+                k.r0 = NOREG;
+                k.r1 = NOREG;
+                for (int i = 0; i < Rr; i++) if (sb.S[i] == L.loc[p]) k.r0 = (uint8_t)i;
+                k.b0 = (uint8_t)p;
+                k.qj = (uint8_t)j;
+                k.flags = (inverse ? QF_INVERSE : 0) | (layout_rev ? QF_REVERSED : 0);
+                // register twiddle table: exp(+-i pi (logical(goff_v) mod 2^j) / 2^j)
+                double tab[2 * NREG];
+                for (int v = 0; v < NREG; v++) {
+                    uint64_t goff = 0;
+                    for (int i = 0; i < Rr; i++) if (v & (1 << i)) goff |= bit(L.T[sb.S[i]]);
+                    uint64_t lg = layout_rev ? brev_n(goff, n) : goff;
+                    uint64_t Lm = (j == 0) ? 0 : (lg & (bit(j) - 1));
+                    long double ang = (long double)3.141592653589793238462643383279502884L *
+                                      (long double)Lm / ldexpl(1.0L, j);
+                    double sgn = inverse ? -1.0 : 1.0;
+                    tab[2 * v] = (double)cosl(ang);
+                    tab[2 * v + 1] = sgn * (double)sinl(ang);
+                }
+                k.mat = (uint32_t)mb.add_const(tab, NREG);
+                if (b == a) k.flags |= QF_HEAD;
+                int jmax = 0;
+                for (size_t b2 = a; b2 < std::min(st.size(), a + Rr); b2++) jmax = std::max(jmax, st[b2]);
+                k.b1 = (uint8_t)jmax;
+                plan.kops.push_back(k);
+            }
+            if (a + Rr >= st.size()) {
+                KOp k{};
+                k.type = K_SCALE;
+                k.r0 = k.r1 = NOREG;
+                double sc[2] = {std::pow(0.5, 0.5 * (double)st.size()), 0.0};
+                k.mat = (uint32_t)mb.add_const(sc, 1);
+                plan.kops.push_back(k);
+            }
+            sb.op_end = (uint32_t)plan.kops.size();
+            plan.subs.push_back(sb);
+        }
+        pp.kp.sub_end = (uint32_t)plan.subs.size();
+        finalize_pass_tables(pp, plan);
+        plan.passes.push_back(pp);
+        plan.n_tile++;
+    }
+    // new layout
+    bool final_rev = ident;   // the layout flips
+    for (int q = 0; q < n; q++) qmap[q] = final_rev ? q : n - 1 - q;
+    return true;
+}
+
+// --------------------------------------------------------------------------
+// Pauli-sum expectation planning.
+// --------------------------------------------------------------------------
+void plan_pauli(int n, const int32_t *qmap, const lq_pauli_term *terms, size_t n_terms,
+                const PlanOptions &opt, PauliPlan &pp) {
+    int K = opt.K > 0 ? std::min(opt.K, n) : auto_tile_bits(n);
+    if (K > 13) K = 13;
+    if (n <= K) K = n;
+    pp.n = n;
+    pp.K = K;
+    struct T { double c; uint64_t x, z; uint32_t y; };
+    std::vector<uint64_t> gx;
+    std::vector<std::vector<T>> gt;
+    for (size_t t = 0; t < n_terms; t++) {
+        uint64_t x = 0, z = 0;
+        for (int q = 0; q < n; q++) {
+            if (terms[t].x_mask & bit(q)) x |= bit(qmap[q]);
+            if (terms[t].z_mask & bit(q)) z |= bit(qmap[q]);
+        }
+        uint32_t y = (uint32_t)(popc(terms[t].x_mask & terms[t].z_mask) & 3);
+        size_t g = 0;
+        while (g < gx.size() && gx[g] != x) g++;
+        if (g == gx.size()) { gx.push_back(x); gt.push_back({}); }
+        gt[g].push_back({terms[t].coeff, x, z, y});
+    }
+    int c = std::max(0, std::min(opt.coalesce, K - 2));
+    uint64_t mand = (n > K) ? ((1ull << c) - 1) : ((1ull << n) - 1);
+    std::vector<char> done(gx.size(), 0);
+    uint32_t tiles = (uint32_t)(1ull << (n - K));
+    for (size_t g = 0; g < gx.size(); g++)
+        if (popc(mand | gx[g]) > K) {
+            done[g] = 1;
+            PauliPlan::Direct d;
+            d.x = gx[g];
+            d.term_begin = (uint32_t)pp.terms.size();
+            for (auto &t : gt[g]) {
+                PTerm p{};
+                p.coeff = t.c; p.zfull = t.z; p.yph = t.y;
+                pp.terms.push_back(p);
+            }
+            d.term_end = (uint32_t)pp.terms.size();
+            uint64_t pairs = 1ull << (n - 1);
+            uint64_t blocks = (pairs + 1023) / 1024;
+            d.n_blocks = (uint32_t)std::min<uint64_t>(blocks, 148 * 16);
+            d.slot = pp.n_slots;
+            pp.n_slots += d.n_blocks;
+            pp.direct.push_back(d);
+        }
+    for (;;) {
+        uint64_t Tm = mand;
+        std::vector<size_t> sel;
+        for (size_t g = 0; g < gx.size(); g++) {
+            if (done[g]) continue;
+            if (popc(Tm | gx[g]) <= K) { Tm |= gx[g]; sel.push_back(g); done[g] = 1; }
+        }
+        if (sel.empty()) break;
+        for (int b = 0; b < n && popc(Tm) < K; b++) Tm |= bit(b);
+        LocalMap L(Tm);
+        uint32_t tb = (uint32_t)pp.terms.size();
+        for (size_t g : sel)
+            for (auto &t : gt[g]) {
+                PTerm p{};
+                p.coeff = t.c;
+                p.zfull = t.z;
+                p.zloc = L.local(t.z);
+                p.xloc = L.local(t.x);
+                p.yph = t.y;
+                pp.terms.push_back(p);
+            }
+        uint32_t te = (uint32_t)pp.terms.size();
+        // the kernel stages at most PAULI_MAX_TERMS terms in shared memory
+        for (uint32_t b = tb; b < te; b += PAULI_MAX_TERMS_PLAN) {
+            KPauliPass P{};
+            P.n = n;
+            P.K = K;
+            memcpy(P.T, L.T, MAXK);
+            P.term_begin = b;
+            P.term_end = std::min<uint32_t>(te, b + PAULI_MAX_TERMS_PLAN);
+            P.slot = pp.n_slots;
+            pp.n_slots += tiles;
+            pp.passes.push_back(P);
+        }
+    }
+}
+
+std::string describe(const Plan &plan) {
+    std::ostringstream os;
+    os << "n=" << plan.n << " K=" << plan.K << " passes=" << plan.passes.size()
+       << " (tile " << plan.n_tile << ", pair " << plan.n_pair << ", diag " << plan.n_diag << ")\n";
+    for (size_t i = 0; i < plan.passes.size(); i++) {
+        const PlanPass &p = plan.passes[i];
+        if (p.kind == PASS_TILE) {
+            os << "  [" << i << "] TILE ops=" << p.n_ops << " subs=" << (p.kp.sub_end - p.kp.sub_begin) << " T={";
+            for (int k = 0; k < p.kp.K; k++) os << (int)p.kp.T[k] << (k + 1 < p.kp.K ? "," : "");
+            os << "}\n";
+        } else {
+            os << "  [" << i << "] " << (p.kind == PASS_PAIR ? "PAIR" : "DIAG") << " ops=" << p.n_ops << "\n";
+        }
+    }
+    return os.str();
+}
+
+}  // namespace lq

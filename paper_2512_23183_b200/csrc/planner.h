@@ -1,0 +1,102 @@
+// planner.h -- host-side gate-fusion planner.
+//
+// Turns a circuit (an ordered gate list) into passes over
+// the state: commutation-aware first-fit tile selection, register sub-blocks
+// inside each tile, 1q gate fusion, and lowering of every op into the
+// register-position form the kernels execute.  Also plans the QFT stage
+// passes and the Pauli-expectation tile passes
+// (PAPER.md:733-734).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "lq_internal.h"
+#include "../../include/lq.h"
+
+namespace lq {
+
+// Abstract op on physical bits, before tiling.
+struct POp {
+    uint8_t type = K_U1;      // KOpType
+    int t0 = -1, t1 = -1;     // target bits (U1/X/QFT: t0; U2/SWAP: t0 high, t1 low; D1: t0; D2: t0 high, t1 low)
+    uint64_t ctrl = 0;        // control bits (DIAG role)
+    int spec = -1;            // MSpec index (matrix), -1 if none
+    uint8_t qflags = 0, qj = 0;
+    double scale = 1.0;
+    uint64_t full() const;    // bits on which the op is not diagonal
+    uint64_t touch() const;   // every bit the op reads
+    bool diag() const { return type == K_D1 || type == K_D2 || type == K_SCALE; }
+};
+
+bool commute(const POp &a, const POp &b);
+
+enum PassKind { PASS_TILE = 0, PASS_PAIR = 1, PASS_DIAG = 2 };
+
+struct PlanPass {
+    PassKind kind = PASS_TILE;
+    KPass kp{};               // TILE: descriptor (sub range into Plan::subs)
+    uint32_t op_begin = 0, op_end = 0;   // PAIR/DIAG: range into Plan::kops (physical-bit form)
+    int n_ops = 0;            // user-level ops fused into this pass (for stats)
+};
+
+struct Plan {
+    int n = 0;
+    int K = 0;
+    std::vector<PlanPass> passes;
+    std::vector<KSub> subs;
+    std::vector<KOp> kops;
+    size_t n_tile = 0, n_pair = 0, n_diag = 0;
+};
+
+struct MatBuilder {
+    std::vector<MSpec> specs;
+    std::vector<MFactor> factors;
+    std::vector<double> cst;      // constant complex entries (re, im) -- U1/U2 user matrices, QFT twiddles
+    uint32_t mat_size = 0;        // per-circuit matrix block size (double2 units)
+    int add_spec(MForm form, const std::vector<MFactor> &f);
+    int add_const(const double *re_im_pairs, int n_complex);
+};
+
+struct PlanOptions {
+    int K = 0;               // tile bits (0 = automatic)
+    int coalesce = 3;        // low physical bits a strided tile always holds
+    bool fusion = true;      // false: one PAIR/DIAG pass per op
+};
+
+// Lower user gates (already validated) to POps on physical bits.  SWAP
+// gates update qmap (relabel) and emit nothing.  Adjacent 1q gates on the
+// same qubit are fused into one op (product of factors).
+void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
+                 std::vector<POp> &ops, MatBuilder &mb);
+
+// Physical SWAP ops that permute the layout `qmap` into the identity.
+void canonicalize_ops(int n, int32_t *qmap, std::vector<POp> &ops);
+
+// Plan generic passes for `ops`.
+void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, const MatBuilder &mb,
+                  Plan &plan);
+
+// Plan the QFT (forward or inverse) as tile passes; updates qmap (layout
+// flips between identity and reversed).  Requires qmap identity or reversed.
+bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &plan,
+              MatBuilder &mb);
+
+// Pauli expectation planning.
+struct PauliPlan {
+    int n = 0, K = 0;
+    std::vector<KPauliPass> passes;     // tiled passes
+    std::vector<PTerm> terms;
+    uint32_t n_slots = 0;               // partial sums per circuit
+    // groups whose x mask does not fit in a tile: direct pair passes
+    struct Direct { uint64_t x; uint32_t term_begin, term_end; uint32_t slot; uint32_t n_blocks; };
+    std::vector<Direct> direct;
+};
+void plan_pauli(int n, const int32_t *qmap, const lq_pauli_term *terms, size_t n_terms,
+                const PlanOptions &opt, PauliPlan &pp);
+
+int auto_tile_bits(int n);
+
+std::string describe(const Plan &plan);
+
+}  // namespace lq

@@ -1,0 +1,389 @@
+"""Thin ctypes binding of liblq.so (include/lq.h), same names as the C ABI.
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels of liblq.so.  There is no CPU fallback -- importing this module
+fails loudly if liblq.so is missing, and every call that needs a GPU raises
+LQError(LQ_ERR_CUDA) without one.
+
+PyTorch is used for device memory (``StateVector`` wraps a torch complex128
+tensor through ``lq_sv_wrap``) and for CUDA streams.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from typing import Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblq.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ---- enums (include/lq.h) -------------------------------------------------
+LQ_OK, LQ_ERR_ARG, LQ_ERR_OOM, LQ_ERR_CUDA, LQ_ERR_NCCL, LQ_ERR_DIM, LQ_ERR_NONFINITE, LQ_ERR_STATE = \
+    0, -1, -2, -3, -4, -5, -6, -7
+STATUS_NAMES = {0: "LQ_OK", -1: "LQ_ERR_ARG", -2: "LQ_ERR_OOM", -3: "LQ_ERR_CUDA", -4: "LQ_ERR_NCCL",
+                -5: "LQ_ERR_DIM", -6: "LQ_ERR_NONFINITE", -7: "LQ_ERR_STATE"}
+KIND_NAMES = ["H", "X", "Y", "Z", "S", "SDG", "T", "TDG", "RX", "RY", "RZ", "CNOT", "CZ", "CP",
+              "SWAP", "U1", "U2", "CRY", "CCX", "RXX", "RYY", "RZZ"]
+KINDS = {k: i for i, k in enumerate(KIND_NAMES)}
+LQ_OPT_FUSION, LQ_OPT_TILE_BITS, LQ_OPT_COALESCE_BITS = 0, 1, 2
+
+
+class lq_gate(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("q0", ctypes.c_int32), ("q1", ctypes.c_int32),
+                ("q2", ctypes.c_int32), ("param_idx", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("angle", ctypes.c_double), ("mat", ctypes.POINTER(ctypes.c_double))]
+
+
+class lq_pauli_term(ctypes.Structure):
+    _fields_ = [("coeff", ctypes.c_double), ("x_mask", ctypes.c_uint64), ("z_mask", ctypes.c_uint64)]
+
+
+class LQError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_P = ctypes.c_void_p
+_i32, _i64, _u64, _sz, _dbl = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_double
+_GP = ctypes.POINTER(lq_gate)
+_TP = ctypes.POINTER(lq_pauli_term)
+_DP = ctypes.POINTER(ctypes.c_double)
+
+_SIGS = {
+    "lq_last_error": ([], ctypes.c_char_p),
+    "lq_version": ([], _i32),
+    "lq_device_count": ([], _i32),
+    "lq_sv_alloc": ([_i32, _P, ctypes.POINTER(_P)], _i32),
+    "lq_sv_wrap": ([_i32, _P, _P, _sz, ctypes.POINTER(_P)], _i32),
+    "lq_sv_free": ([_P], _i32),
+    "lq_sv_set_stream": ([_P, _P], _i32),
+    "lq_sv_num_qubits": ([_P], _i32),
+    "lq_sv_device_ptr": ([_P], _P),
+    "lq_sv_qubit_map": ([_P, ctypes.POINTER(ctypes.c_int32)], _i32),
+    "lq_sv_init_basis": ([_P, _u64], _i32),
+    "lq_sv_init_random": ([_P, _u64], _i32),
+    "lq_sv_read": ([_P, _u64, _u64, _DP], _i32),
+    "lq_sv_write": ([_P, _u64, _u64, _DP], _i32),
+    "lq_sv_gather": ([_P, ctypes.POINTER(ctypes.c_uint64), _sz, _DP], _i32),
+    "lq_sv_norm2": ([_P, _DP], _i32),
+    "lq_sv_canonicalize": ([_P], _i32),
+    "lq_apply_circuit": ([_P, _GP, _sz, _DP, _sz], _i32),
+    "lq_qft": ([_P, _i32], _i32),
+    "lq_expval_pauli_sum": ([_P, _TP, _sz, _DP], _i32),
+    "lq_param_shift_grad": ([_i32, _GP, _sz, _DP, _sz, _TP, _sz, _i32, _i32, _P, _DP, _DP], _i32),
+    "lq_psr_create": ([_i32, _GP, _sz, _sz, _TP, _sz, _i32, _i32, _P, ctypes.POINTER(_P)], _i32),
+    "lq_psr_run": ([_P, _P, _P, _P], _i32),
+    "lq_psr_free": ([_P], _i32),
+    "lq_psr_stats": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i32),
+    "lq_set_option": ([_i32, _i64], _i32),
+    "lq_get_option": ([_i32], _i64),
+    "lq_plan_describe": ([_i32, _GP, _sz, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.c_char_p, _sz], _i32),
+    "lq_launch_count": ([], _u64),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = tuple(_SIGS)
+
+
+def _chk(status: int):
+    if status != LQ_OK:
+        raise LQError(status, _lib.lq_last_error().decode())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_DP)
+
+
+# ---- marshalling ------------------------------------------------------------
+class GateArray:
+    """Gate tuples ``(name, q0, q1, param_idx, angle[, mat][, q2])`` (the
+    workloads format) as a contiguous ``lq_gate[]`` plus owned matrices."""
+
+    def __init__(self, gates: Sequence[tuple]):
+        self.n = len(gates)
+        self.arr = (lq_gate * max(self.n, 1))()
+        self._mats: List[np.ndarray] = []
+        for i, g in enumerate(gates):
+            name, a, b, p, ang = g[:5]
+            G = self.arr[i]
+            G.kind = KINDS[name] if isinstance(name, str) else int(name)
+            G.q0, G.q1 = int(a), int(b)
+            G.q2 = int(g[6]) if len(g) > 6 else -1
+            G.param_idx = int(p)
+            G.reserved = 0
+            G.angle = float(ang)
+            if len(g) > 5 and g[5] is not None:
+                m = np.asarray(g[5], np.complex128).reshape(-1)
+                buf = np.ascontiguousarray(np.stack([m.real, m.imag], -1).reshape(-1))
+                self._mats.append(buf)
+                G.mat = _dptr(buf)
+            else:
+                G.mat = None
+
+    @property
+    def ptr(self):
+        return ctypes.cast(self.arr, _GP)
+
+
+class TermArray:
+    def __init__(self, terms: Sequence[tuple]):
+        self.n = len(terms)
+        self.arr = (lq_pauli_term * max(self.n, 1))()
+        for i, (c, x, z) in enumerate(terms):
+            self.arr[i].coeff = float(c)
+            self.arr[i].x_mask = int(x)
+            self.arr[i].z_mask = int(z)
+
+    @property
+    def ptr(self):
+        return ctypes.cast(self.arr, _TP)
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ---- C ABI, same names --------------------------------------------------------
+def lq_last_error() -> str:
+    return _lib.lq_last_error().decode()
+
+
+def lq_version() -> int:
+    return _lib.lq_version()
+
+
+def lq_device_count() -> int:
+    return _lib.lq_device_count()
+
+
+def lq_launch_count() -> int:
+    return _lib.lq_launch_count()
+
+
+def lq_set_option(option: int, value: int):
+    _chk(_lib.lq_set_option(option, int(value)))
+
+
+def lq_get_option(option: int) -> int:
+    return _lib.lq_get_option(option)
+
+
+def lq_sv_alloc(n_qubits: int, stream=None):
+    h = _P()
+    _chk(_lib.lq_sv_alloc(n_qubits, _stream_ptr(stream), ctypes.byref(h)))
+    return h
+
+
+def lq_sv_wrap(n_qubits: int, dev_ptr: int, nbytes: int, stream=None):
+    h = _P()
+    _chk(_lib.lq_sv_wrap(n_qubits, _stream_ptr(stream), dev_ptr, nbytes, ctypes.byref(h)))
+    return h
+
+
+def lq_sv_free(h):
+    _chk(_lib.lq_sv_free(h))
+
+
+def lq_sv_set_stream(h, stream):
+    _chk(_lib.lq_sv_set_stream(h, _stream_ptr(stream)))
+
+
+def lq_sv_num_qubits(h) -> int:
+    return _lib.lq_sv_num_qubits(h)
+
+
+def lq_sv_device_ptr(h) -> int:
+    return _lib.lq_sv_device_ptr(h)
+
+
+def lq_sv_qubit_map(h) -> List[int]:
+    n = lq_sv_num_qubits(h)
+    out = (ctypes.c_int32 * 64)()
+    _chk(_lib.lq_sv_qubit_map(h, out))
+    return list(out[:n])
+
+
+def lq_sv_init_basis(h, k: int):
+    _chk(_lib.lq_sv_init_basis(h, int(k)))
+
+
+def lq_sv_init_random(h, seed: int):
+    _chk(_lib.lq_sv_init_random(h, int(seed) & (2**64 - 1)))
+
+
+def lq_sv_read(h, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
+    n = lq_sv_num_qubits(h)
+    if count is None:
+        count = (1 << n) - offset
+    out = np.empty(count, np.complex128)
+    _chk(_lib.lq_sv_read(h, offset, count, out.ctypes.data_as(_DP)))
+    return out
+
+
+def lq_sv_write(h, amps: np.ndarray, offset: int = 0):
+    a = np.ascontiguousarray(amps, np.complex128)
+    _chk(_lib.lq_sv_write(h, offset, a.size, a.ctypes.data_as(_DP)))
+
+
+def lq_sv_gather(h, idx: Iterable[int]) -> np.ndarray:
+    ix = np.ascontiguousarray(np.asarray(list(idx) if not isinstance(idx, np.ndarray) else idx, np.uint64))
+    out = np.empty(ix.size, np.complex128)
+    _chk(_lib.lq_sv_gather(h, ix.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ix.size,
+                           out.ctypes.data_as(_DP)))
+    return out
+
+
+def lq_sv_norm2(h) -> float:
+    out = ctypes.c_double()
+    _chk(_lib.lq_sv_norm2(h, ctypes.byref(out)))
+    return out.value
+
+
+def lq_sv_canonicalize(h):
+    _chk(_lib.lq_sv_canonicalize(h))
+
+
+def lq_apply_circuit(h, gates, theta=None):
+    ga = gates if isinstance(gates, GateArray) else GateArray(gates)
+    th = None if theta is None else np.ascontiguousarray(theta, np.float64)
+    _chk(_lib.lq_apply_circuit(h, ga.ptr, ga.n, None if th is None else _dptr(th),
+                               0 if th is None else th.size))
+
+
+def lq_qft(h, inverse: bool = False):
+    _chk(_lib.lq_qft(h, int(bool(inverse))))
+
+
+def lq_expval_pauli_sum(h, terms) -> float:
+    ta = terms if isinstance(terms, TermArray) else TermArray(terms)
+    out = ctypes.c_double()
+    _chk(_lib.lq_expval_pauli_sum(h, ta.ptr, ta.n, ctypes.byref(out)))
+    return out.value
+
+
+def lq_param_shift_grad(n_qubits: int, ansatz, theta, terms, shard_rank: int = 0, shard_world: int = 1,
+                        stream=None, with_energy: bool = True) -> Tuple[np.ndarray, Optional[float]]:
+    ga = ansatz if isinstance(ansatz, GateArray) else GateArray(ansatz)
+    ta = terms if isinstance(terms, TermArray) else TermArray(terms)
+    th = np.ascontiguousarray(theta, np.float64)
+    grad = np.zeros(th.size, np.float64)
+    e = ctypes.c_double()
+    _chk(_lib.lq_param_shift_grad(n_qubits, ga.ptr, ga.n, _dptr(th), th.size, ta.ptr, ta.n, shard_rank,
+                                  shard_world, _stream_ptr(stream), _dptr(grad),
+                                  ctypes.byref(e) if with_energy else None))
+    return grad, (e.value if with_energy else None)
+
+
+def lq_psr_create(n_qubits: int, ansatz, n_params: int, terms, shard_rank: int = 0, shard_world: int = 1,
+                  stream=None):
+    ga = ansatz if isinstance(ansatz, GateArray) else GateArray(ansatz)
+    ta = terms if isinstance(terms, TermArray) else TermArray(terms)
+    h = _P()
+    _chk(_lib.lq_psr_create(n_qubits, ga.ptr, ga.n, n_params, ta.ptr, ta.n, shard_rank, shard_world,
+                            _stream_ptr(stream), ctypes.byref(h)))
+    return h
+
+
+def lq_psr_run(plan, theta_dev: int, grad_dev: int, energy_dev: Optional[int] = None):
+    _chk(_lib.lq_psr_run(plan, theta_dev, grad_dev, energy_dev))
+
+
+def lq_psr_free(plan):
+    _chk(_lib.lq_psr_free(plan))
+
+
+def lq_psr_stats(plan) -> Tuple[int, int]:
+    c, l = ctypes.c_uint64(), ctypes.c_uint64()
+    _chk(_lib.lq_psr_stats(plan, ctypes.byref(c), ctypes.byref(l)))
+    return c.value, l.value
+
+
+def lq_plan_describe(n_qubits: int, gates) -> Tuple[int, int, str]:
+    ga = gates if isinstance(gates, GateArray) else GateArray(gates)
+    np_, nt = ctypes.c_uint64(), ctypes.c_uint64()
+    buf = ctypes.create_string_buffer(1 << 16)
+    _chk(_lib.lq_plan_describe(n_qubits, ga.ptr, ga.n, ctypes.byref(np_), ctypes.byref(nt), buf, len(buf)))
+    return np_.value, nt.value, buf.value.decode()
+
+
+# ---- convenience: a torch-owned state ---------------------------------------
+class StateVector:
+    """A state whose amplitudes live in a torch complex128 CUDA tensor
+    (``self.tensor``, physical layout) wrapped by an lq_sv handle."""
+
+    def __init__(self, n_qubits: int, stream=None, device=None):
+        import torch
+        self.n = n_qubits
+        self.tensor = torch.empty(1 << n_qubits, dtype=torch.complex128,
+                                  device=device if device is not None else "cuda")
+        self.h = lq_sv_wrap(n_qubits, self.tensor.data_ptr(), self.tensor.numel() * 16, stream)
+
+    def free(self):
+        if self.h is not None:
+            lq_sv_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def init_basis(self, k: int):
+        lq_sv_init_basis(self.h, k)
+        return self
+
+    def init_random(self, seed: int):
+        lq_sv_init_random(self.h, seed)
+        return self
+
+    def apply(self, gates, theta=None):
+        lq_apply_circuit(self.h, gates, theta)
+        return self
+
+    def qft(self, inverse: bool = False):
+        lq_qft(self.h, inverse)
+        return self
+
+    def expval(self, terms) -> float:
+        return lq_expval_pauli_sum(self.h, terms)
+
+    def read(self, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
+        return lq_sv_read(self.h, offset, count)
+
+    def gather(self, idx) -> np.ndarray:
+        return lq_sv_gather(self.h, idx)
+
+    def norm2(self) -> float:
+        return lq_sv_norm2(self.h)
+
+    def canonicalize(self):
+        lq_sv_canonicalize(self.h)
+        return self
+
+    def qubit_map(self) -> List[int]:
+        return lq_sv_qubit_map(self.h)

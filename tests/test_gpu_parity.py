@@ -1,0 +1,435 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Tolerances (BASELINE.json north_star; reading A16): amplitudes max-abs
+<= 1e-10; expectations |E - E_o| <= 1e-10 max(|E_o|, 1); gradients
+|g_i - g_o,i| <= 1e-10 max(|g_o,i|, ||g_o||_inf).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+AMP_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def lq():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2512_23183_b200 import lq as _lq
+    assert _lq.lq_device_count() >= 1
+    return _lq
+
+
+@pytest.fixture(autouse=True)
+def _restore_options(lq):
+    yield
+    lq.lq_set_option(lq.LQ_OPT_FUSION, 1)
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 0)
+    lq.lq_set_option(lq.LQ_OPT_COALESCE_BITS, 3)
+
+
+def grad_close(g, go):
+    scale = max(float(np.abs(go).max()), 1e-300)
+    tol = 1e-10 * np.maximum(np.abs(go), scale)
+    assert np.all(np.abs(g - go) <= tol), f"max grad err {np.abs(g - go).max():.3e} (scale {scale:.3e})"
+
+
+ALL_KINDS = ("H", "X", "Y", "Z", "S", "SDG", "T", "TDG", "RX", "RY", "RZ", "CNOT", "CZ", "CP",
+             "SWAP", "CRY", "RXX", "RYY", "RZZ", "U1", "U2", "CCX")
+
+
+def rich_circuit(n, n_gates, rng):
+    """Every gate kind the ABI accepts, on uniformly random qubits."""
+    kinds = [k for k in ALL_KINDS if (k != "CCX" or n >= 3) and (k not in
+             ("CNOT", "CZ", "CP", "SWAP", "CRY", "RXX", "RYY", "RZZ", "U2") or n >= 2)]
+    gates = []
+    for _ in range(n_gates):
+        k = kinds[int(rng.integers(len(kinds)))]
+        qs = [int(q) for q in rng.choice(n, size=3 if n >= 3 else n, replace=False)]
+        ang = float(rng.uniform(0, 2 * np.pi)) if k in W.PARAMETRIC else 0.0
+        if k in ("RX", "RY", "RZ", "H", "X", "Y", "Z", "S", "SDG", "T", "TDG"):
+            gates.append((k, qs[0], -1, -1, ang))
+        elif k == "U1":
+            A = rng.normal(size=(2, 2)) + 1j * rng.normal(size=(2, 2))
+            Q, _ = np.linalg.qr(A)
+            gates.append(("U1", qs[0], -1, -1, 0.0, Q))
+        elif k == "U2":
+            A = rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4))
+            Q, _ = np.linalg.qr(A)
+            gates.append(("U2", qs[0], qs[1], -1, 0.0, Q))
+        elif k == "CCX":
+            gates.append(("CCX", qs[0], qs[1], -1, 0.0, None, qs[2]))
+        else:
+            gates.append((k, qs[0], qs[1], -1, ang))
+    return gates
+
+
+def run_gpu(lq, n, seed, gates, theta=None, qft=None):
+    sv = lq.StateVector(n)
+    sv.init_random(seed)
+    if gates:
+        sv.apply(gates, theta)
+    if qft is not None:
+        sv.qft(inverse=qft == "inverse")
+    out = sv.read()
+    sv.free()
+    return out
+
+
+def run_oracle(oracle, n, seed, gates, theta=None, qft=None):
+    psi = oracle.init_random(n, seed)
+    if gates:
+        oracle.apply_circuit(psi, gates, theta)
+    if qft is not None:
+        oracle.qft(psi, inverse=qft == "inverse")
+    return psi
+
+
+# ---------------------------------------------------------------- init / io
+
+def test_init_random_matches_oracle(lq, oracle):
+    for n in (1, 3, 10, 17):
+        got = run_gpu(lq, n, 1234 + n, [])
+        np.testing.assert_allclose(got, oracle.init_random(n, 1234 + n), rtol=0, atol=1e-13)
+
+
+def test_init_basis_norm_gather_write(lq):
+    n = 12
+    sv = lq.StateVector(n)
+    sv.init_basis(3000)
+    a = sv.read()
+    assert a[3000] == 1 and np.count_nonzero(a) == 1
+    assert sv.norm2() == 1.0
+    amps = (np.arange(1 << n) + 1j * np.arange(1 << n)[::-1]).astype(np.complex128)
+    lq.lq_sv_write(sv.h, amps)
+    idx = [0, 5, 4095, 77, 1234]
+    np.testing.assert_array_equal(sv.gather(idx), amps[idx])
+    np.testing.assert_array_equal(sv.read(100, 50), amps[100:150])
+    sv.free()
+
+
+# ---------------------------------------------------------------- circuits
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 10, 13, 14, 17, 20])
+def test_rich_random_circuit(lq, oracle, n):
+    rng = np.random.default_rng(1000 + n)
+    gates = rich_circuit(n, 160, rng)
+    ref = run_oracle(oracle, n, 55 + n, gates)
+    got = run_gpu(lq, n, 55 + n, gates)
+    assert np.abs(got - ref).max() <= AMP_TOL
+
+
+@pytest.mark.parametrize("K", [2, 3, 5, 8, 12])
+@pytest.mark.parametrize("n", [9, 15])
+def test_tile_sizes_and_multi_tile(lq, oracle, n, K):
+    """Small tiles force many tiles / ragged register sets at small n."""
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
+    rng = np.random.default_rng(2000 + n * 16 + K)
+    gates = rich_circuit(n, 120, rng)
+    ref = run_oracle(oracle, n, 7, gates)
+    got = run_gpu(lq, n, 7, gates)
+    assert np.abs(got - ref).max() <= AMP_TOL
+
+
+@pytest.mark.parametrize("coalesce", [0, 1, 3])
+def test_coalesce_bits(lq, oracle, coalesce):
+    lq.lq_set_option(lq.LQ_OPT_COALESCE_BITS, coalesce)
+    n = 16
+    rng = np.random.default_rng(31 + coalesce)
+    gates = rich_circuit(n, 150, rng)
+    ref = run_oracle(oracle, n, 9, gates)
+    assert np.abs(run_gpu(lq, n, 9, gates) - ref).max() <= AMP_TOL
+
+
+@pytest.mark.parametrize("n", [3, 11, 16])
+def test_unfused_pair_and_diag_kernels(lq, oracle, n):
+    """LQ_OPT_FUSION=0: one pair (a4) or diagonal (a3) pass per gate."""
+    lq.lq_set_option(lq.LQ_OPT_FUSION, 0)
+    rng = np.random.default_rng(3000 + n)
+    gates = rich_circuit(n, 100, rng)
+    ref = run_oracle(oracle, n, 11, gates)
+    assert np.abs(run_gpu(lq, n, 11, gates) - ref).max() <= AMP_TOL
+
+
+def test_diagonal_runs(lq, oracle):
+    """Runs of diagonal gates on many qubits (diag pass path)."""
+    n = 18
+    rng = np.random.default_rng(4)
+    gates = []
+    for _ in range(200):
+        k = ["Z", "S", "T", "SDG", "TDG", "RZ", "CZ", "CP", "RZZ"][int(rng.integers(9))]
+        a, b = (int(q) for q in rng.choice(n, 2, replace=False))
+        ang = float(rng.uniform(0, 2 * np.pi)) if k in W.PARAMETRIC else 0.0
+        gates.append((k, a, -1 if k in ("Z", "S", "T", "SDG", "TDG", "RZ") else b, -1, ang))
+    ref = run_oracle(oracle, n, 3, gates)
+    assert np.abs(run_gpu(lq, n, 3, gates) - ref).max() <= AMP_TOL
+
+
+def test_parameterised_gates_with_theta(lq, oracle):
+    n = 12
+    gates = W.hea_ansatz(n, 3, "ring")
+    theta = np.random.default_rng(8).uniform(0, 2 * np.pi, 6 * n)
+    ref = run_oracle(oracle, n, 21, gates, theta)
+    assert np.abs(run_gpu(lq, n, 21, gates, theta) - ref).max() <= AMP_TOL
+
+
+def test_app_a_cnot_on_gpu(lq):
+    """PAPER.md App. A on the GPU."""
+    r2 = 1 / math.sqrt(2)
+    sv = lq.StateVector(2)
+    lq.lq_sv_write(sv.h, np.array([r2, 0, 0, r2], np.complex128))
+    sv.apply([("CNOT", 0, 1, -1, 0.0)])
+    np.testing.assert_allclose(sv.read(), [r2, 0, r2, 0], atol=1e-16)
+
+
+def test_app_b_toffoli_on_gpu(lq):
+    """PAPER.md App. B on the GPU."""
+    r2 = 1 / math.sqrt(2)
+    sv = lq.StateVector(3)
+    lq.lq_sv_write(sv.h, np.array([0, 0, 0, 0, 0, r2, r2, 0], np.complex128))
+    sv.apply([("CCX", 0, 1, -1, 0.0, None, 2)])
+    np.testing.assert_allclose(sv.read(), [0, 0, 0, 0, 0, r2, 0, r2], atol=1e-16)
+
+
+# ---------------------------------------------------------------- config 1
+
+def test_config1_exact(lq, oracle):
+    """BASELINE configs[0]: n=10 seeded state, 200 random gates, full QFT."""
+    w = W.config1()
+    ref = run_oracle(oracle, w.n, w.seed, w.gates, qft="forward")
+    got = run_gpu(lq, w.n, w.seed, w.gates, qft="forward")
+    assert np.abs(got - ref).max() <= AMP_TOL
+    assert abs(np.vdot(got, got).real - 1) < 1e-12
+
+
+# ---------------------------------------------------------------- QFT
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8, 11, 12, 13, 16, 19])
+def test_qft_random_state(lq, oracle, n):
+    ref = run_oracle(oracle, n, 40 + n, [], qft="forward")
+    got = run_gpu(lq, n, 40 + n, [], qft="forward")
+    assert np.abs(got - ref).max() <= AMP_TOL
+
+
+@pytest.mark.parametrize("n", [3, 10, 15])
+def test_qft_inverse_and_roundtrip(lq, oracle, n):
+    ref = run_oracle(oracle, n, 60 + n, [], qft="inverse")
+    assert np.abs(run_gpu(lq, n, 60 + n, [], qft="inverse") - ref).max() <= AMP_TOL
+    sv = lq.StateVector(n).init_random(60 + n)
+    sv.qft().qft(inverse=True)
+    assert np.abs(sv.read() - oracle.init_random(n, 60 + n)).max() <= AMP_TOL
+    # inverse first, then forward (layout reversed <-> identity both ways)
+    sv.init_random(60 + n).qft(inverse=True).qft()
+    assert np.abs(sv.read() - oracle.init_random(n, 60 + n)).max() <= AMP_TOL
+    sv.free()
+
+
+@pytest.mark.parametrize("K", [3, 6])
+def test_qft_small_tiles(lq, oracle, K):
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
+    n = 14
+    ref = run_oracle(oracle, n, 5, [], qft="forward")
+    assert np.abs(run_gpu(lq, n, 5, [], qft="forward") - ref).max() <= AMP_TOL
+
+
+def test_qft_then_gates_then_canonicalize(lq, oracle):
+    """Gates after a QFT act through the qubit map; canonicalize
+    materialises natural order."""
+    n = 13
+    rng = np.random.default_rng(17)
+    gates = rich_circuit(n, 80, rng)
+    psi = oracle.init_random(n, 2)
+    oracle.qft(psi)
+    oracle.apply_circuit(psi, gates)
+    oracle.qft(psi)
+    sv = lq.StateVector(n).init_random(2).qft().apply(gates).qft()
+    assert np.abs(sv.read() - psi).max() <= AMP_TOL
+    sv.canonicalize()
+    assert sv.qubit_map() == [n - 1 - q for q in range(n)]
+    import torch
+    torch.cuda.synchronize()
+    raw = sv.tensor.cpu().numpy()
+    assert np.abs(raw - psi).max() <= AMP_TOL
+    sv.free()
+
+
+def test_config2_qft_n20_closed_form(lq, oracle):
+    """BASELINE configs[1]: QFT(20) on 16 seeded basis states against the
+    closed form N^-1/2 e^{2 pi i j k / N}, every amplitude, and
+    on the seeded random state against the oracle's independent numpy ifft
+    route (numpy.fft.ifft * sqrt(N))."""
+    w = W.config2()
+    n, N = w.n, 1 << w.n
+    j = np.arange(N, dtype=np.int64)
+    sv = lq.StateVector(n)
+    for k in w.basis:
+        sv.init_basis(k).qft()
+        expect = np.exp(2j * np.pi * ((j * k) % N) / N) / math.sqrt(N)
+        assert np.abs(sv.read() - expect).max() <= AMP_TOL
+    sv.init_random(w.seed).qft()
+    ref = np.fft.ifft(oracle.init_random(n, w.seed)) * math.sqrt(N)
+    assert np.abs(sv.read() - ref).max() <= AMP_TOL
+    sv.free()
+
+
+# ---------------------------------------------------------------- expectation
+
+@pytest.mark.parametrize("n", [1, 2, 4, 9, 14])
+def test_expval_random_pauli_sums(lq, oracle, n):
+    rng = np.random.default_rng(70 + n)
+    terms = W.random_pauli_sum(n, min(40, 4 ** n), rng)
+    psi = oracle.init_random(n, 70 + n)
+    eo = oracle.expval(psi, terms)
+    sv = lq.StateVector(n).init_random(70 + n)
+    e = sv.expval(terms)
+    assert abs(e - eo) <= 1e-10 * max(abs(eo), 1.0)
+    sv.free()
+
+
+def test_expval_wide_x_masks_direct_path(lq, oracle):
+    """x masks wider than a tile take the direct pair kernel."""
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 5)
+    n = 13
+    full = (1 << n) - 1
+    terms = [(0.7, full, 0), (-0.3, full, full), (0.2, full & 0x5555, full & 0x0F0F), (1.1, 0, full)]
+    psi = oracle.init_random(n, 3)
+    eo = oracle.expval(psi, terms)
+    sv = lq.StateVector(n).init_random(3)
+    assert abs(sv.expval(terms) - eo) <= 1e-10 * max(abs(eo), 1.0)
+    sv.free()
+
+
+def test_expval_after_qft_uses_qubit_map(lq, oracle):
+    n = 12
+    rng = np.random.default_rng(12)
+    terms = W.random_pauli_sum(n, 30, rng)
+    psi = oracle.init_random(n, 4)
+    oracle.qft(psi)
+    sv = lq.StateVector(n).init_random(4).qft()
+    assert sv.qubit_map() != [n - 1 - q for q in range(n)]
+    eo = oracle.expval(psi, terms)
+    assert abs(sv.expval(terms) - eo) <= 1e-10 * max(abs(eo), 1.0)
+    sv.free()
+
+
+# ---------------------------------------------------------------- parameter shift
+
+def test_psr_single_ry_closed_form(lq):
+    for t in [0.0, 0.3, math.pi / 2, 2.0]:
+        g, e = lq.lq_param_shift_grad(1, [("RY", 0, -1, 0, 0.0)], [t], [(1.0, 0, 1)])
+        assert abs(e - math.cos(t)) <= 1e-15 and abs(g[0] + math.sin(t)) <= 1e-15
+
+
+def test_psr_app_e_table(lq, oracle):
+    """PAPER.md App. E circuit (CRY included) on the GPU vs the oracle."""
+    gates = W.edge_case_circuit()
+    for th in ([0.5, 0.3, 0.2, 0.1], [10.0, 5.0, 3.0, 2.0], [1e-8, 1e-7, 1e-6, 1e-5],
+               [math.pi / 2] * 4, [math.pi] * 4):
+        g, _ = lq.lq_param_shift_grad(2, gates, th, [(1.0, 0, 1)])
+        go = oracle.param_shift_grad(2, gates, np.array(th), [(1.0, 0, 1)])
+        assert np.all(np.isfinite(g))
+        np.testing.assert_allclose(g, go, rtol=0, atol=1e-15)
+
+
+def test_config3_gradient(lq, oracle):
+    """BASELINE configs[2]: n=4 HEA, 48 params, 15-term H, 96 shifted circuits."""
+    w = W.config3()
+    g, e = lq.lq_param_shift_grad(w.n, w.gates, w.theta, w.terms)
+    go = oracle.param_shift_grad(w.n, w.gates, w.theta, w.terms)
+    eo = oracle.energy(w.n, w.gates, w.theta, w.terms)
+    grad_close(g, go)
+    assert abs(e - eo) <= 1e-10 * max(abs(eo), 1)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_psr_shards_partition_components(lq, oracle, world):
+    w = W.config3()
+    full, e0 = lq.lq_param_shift_grad(w.n, w.gates, w.theta, w.terms)
+    acc = np.zeros_like(full)
+    for r in range(world):
+        g, e = lq.lq_param_shift_grad(w.n, w.gates, w.theta, w.terms, shard_rank=r, shard_world=world)
+        owned = np.arange(full.size) % world == r
+        assert np.all(g[~owned] == 0.0)
+        acc += g
+        assert e == (e0 if r == 0 else 0.0)
+    np.testing.assert_array_equal(acc, full)   # bit-identical
+
+
+@pytest.mark.parametrize("n", [10, 16])
+def test_xyz_ring_gradient_small(lq, oracle, n):
+    """Config-4 structure at n where the oracle runs every component."""
+    gates = W.hea_ansatz(n, 2, "ring")
+    theta = np.random.default_rng(n).uniform(0, 2 * np.pi, 4 * n)
+    terms = W.xyz_terms(n)
+    g, e = lq.lq_param_shift_grad(n, gates, theta, terms)
+    go = oracle.param_shift_grad(n, gates, theta, terms, threads=8)
+    grad_close(g, go)
+    eo = oracle.energy(n, gates, theta, terms)
+    assert abs(e - eo) <= 1e-10 * max(abs(eo), 1)
+
+
+def test_config4_full_size_closed_forms(lq):
+    """n=24 (configs[3] size): theta = 0 gives E = 0.4*23 + 0.3*24 = 16.4
+    exactly; the product ansatz has a closed-form energy and gradient."""
+    from closed_forms import product_energy_and_grad
+    n = 24
+    w = W.config4()
+    g, e = lq.lq_param_shift_grad(n, w.gates[:3 * n], np.zeros(2 * n), w.terms)
+    assert abs(e - 16.4) <= 1e-10 * 16.4
+    gates, theta = W.product_ansatz(n, np.random.default_rng(24))
+    g, e = lq.lq_param_shift_grad(n, gates, theta, W.xyz_terms(n))
+    E, gref = product_energy_and_grad(n, theta)
+    assert abs(e - E) <= 1e-10 * max(abs(E), 1)
+    grad_close(g, gref)
+
+
+def test_config4_full_size_sampled_vs_oracle(lq, oracle):
+    """configs[3] in full (n=24, 480 params, 961 circuits) through the same
+    call bench.py times; E(theta) and two seeded gradient components are
+    recomputed by the oracle (4 circuits of 720 gates on 2^24 amplitudes)."""
+    import os
+    w = W.config4()
+    g, e = lq.lq_param_shift_grad(w.n, w.gates, w.theta, w.terms)
+    assert np.all(np.isfinite(g))
+    sample = w.meta["oracle_params"][:2]
+    go = oracle.param_shift_grad(w.n, w.gates, w.theta, w.terms, which=sample,
+                                 threads=min(4, os.cpu_count() or 1))
+    scale = float(np.abs(g).max())
+    for p, v in zip(sample, go):
+        assert abs(g[p] - v) <= 1e-10 * max(abs(v), scale), (p, g[p], v)
+
+
+# ---------------------------------------------------------------- boundary errors
+
+def test_boundary_rejections_leave_state_untouched(lq):
+    n = 6
+    sv = lq.StateVector(n).init_random(5)
+    before = sv.read()
+    bad = [
+        [("H", 6, -1, -1, 0.0)],                 # qubit out of range
+        [("CNOT", 2, 2, -1, 0.0)],               # duplicate qubits
+        [("H", 0, -1, -1, 0.3)],                 # angle on a fixed gate
+        [("RX", 0, -1, 3, 0.0)],                 # param_idx without theta
+    ]
+    for gates in bad:
+        with pytest.raises(lq.LQError) as ei:
+            sv.apply(gates)
+        assert ei.value.status == lq.LQ_ERR_ARG
+    with pytest.raises(lq.LQError) as ei:
+        sv.apply([("RX", 0, -1, -1, float("nan"))])
+    assert ei.value.status == lq.LQ_ERR_NONFINITE
+    with pytest.raises(lq.LQError) as ei:
+        sv.apply([("RX", 0, -1, 0, 0.0)], [float("inf")])
+    assert ei.value.status == lq.LQ_ERR_NONFINITE
+    np.testing.assert_array_equal(sv.read(), before)
+    with pytest.raises(lq.LQError):
+        lq.lq_param_shift_grad(2, [("RX", 0, -1, 0, 0.0), ("RY", 1, -1, 0, 0.0)], [0.1], [(1.0, 0, 1)])
+    with pytest.raises(lq.LQError):
+        sv.expval([(1.0, 1 << 6, 0)])
+    sv.free()
