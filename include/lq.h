@@ -196,15 +196,19 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
                         int shard_world, void *cuda_stream, lq_psr **out);
 lq_status lq_psr_run(lq_psr *plan, const double *theta_dev, double *grad_dev, double *energy_dev);
 lq_status lq_psr_free(lq_psr *plan);
-/* Number of circuits one lq_psr_run evaluates on this shard and the kernel
- * launches it issues (for throughput accounting). */
-lq_status lq_psr_stats(const lq_psr *plan, uint64_t *n_circuits, uint64_t *n_launches);
+/* Accounting for one lq_psr_run on this shard: circuits evaluated, kernel
+ * launches issued (by the last run), bytes of the uploaded plan, tile passes
+ * per circuit.  Any output pointer may be NULL. */
+lq_status lq_psr_stats(const lq_psr *plan, uint64_t *n_circuits, uint64_t *n_launches, uint64_t *plan_bytes,
+                       uint64_t *tile_passes);
 
 /* ---- execution options (testing / measurement) -------------------------- */
 typedef enum {
     LQ_OPT_FUSION = 0,     /* 1 (default): tile-fused passes; 0: one pass per gate (pair/diag kernels) */
     LQ_OPT_TILE_BITS = 1,  /* tile size K in bits (default 0 = automatic) */
-    LQ_OPT_COALESCE_BITS = 2 /* low physical bits every strided tile includes (default 3) */
+    LQ_OPT_COALESCE_BITS = 2, /* low physical bits every strided tile includes (default 3) */
+    LQ_OPT_REG_BITS = 3,      /* amplitudes per thread in tile passes = 2^value, 3 or 4 (default 4) */
+    LQ_OPT_KERNEL_TIMING = 4  /* 1: bracket every launch with CUDA events on its stream (lq_kernel_timing) */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);
@@ -214,6 +218,12 @@ int64_t lq_get_option(int option);
  * passes, and a text description (truncated to buf_len). */
 lq_status lq_plan_describe(int n_qubits, const lq_gate *gates, size_t n_gates, uint64_t *n_passes,
                            uint64_t *n_tile, char *buf, size_t buf_len);
+
+/* Accumulated device time of launches made while LQ_OPT_KERNEL_TIMING was
+ * on, per kernel class: 0 tile pass, 1 pair pass, 2 diagonal pass,
+ * 3 Pauli expectation, 4 other.  Synchronises on the recorded events. */
+lq_status lq_kernel_timing(int kernel_class, double *total_ms, uint64_t *count);
+lq_status lq_kernel_timing_reset(void);
 
 /* Kernel launches issued by this process so far (all entry points). */
 uint64_t lq_launch_count(void);

@@ -29,6 +29,14 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
 }
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 
+// In-place register swap the compiler cannot turn into a renaming (a
+// renaming would force loop-carried copies of the whole register tile).
+__device__ __forceinline__ void swap_inplace(double2 &x, double2 &y) {
+    asm volatile("{\n\t.reg .f64 t;\n\tmov.f64 t, %0;\n\tmov.f64 %0, %2;\n\tmov.f64 %2, t;\n\t"
+                 "mov.f64 t, %1;\n\tmov.f64 %1, %3;\n\tmov.f64 %3, t;\n\t}"
+                 : "+d"(x.x), "+d"(x.y), "+d"(y.x), "+d"(y.y));
+}
+
 __device__ __forceinline__ uint64_t insert_zero64(uint64_t x, int b) {
     uint64_t lo = x & ((1ull << b) - 1);
     return ((x ^ lo) << 1) | lo;
@@ -54,38 +62,73 @@ __device__ __forceinline__ uint32_t swz(uint32_t x) {
 // are swizzled: slot = swz(lt) ^ swz(loff(v)).
 template <int RR>
 struct Mapping {
-    uint32_t slt;        // swizzled shared-memory slot of v = 0
-    uint32_t spos;       // S[0..RR-1] packed one byte each
+    uint32_t lt;         // local index of v = 0
+    uint32_t slt;        // shared-memory slot of v = 0 (plain, used for writes)
+    uint32_t slm[RR];    // slot offsets (XOR) of the register bits
     uint64_t gt;         // global index of v = 0
-    __device__ __forceinline__ void make(uint32_t t, const uint8_t *S, const uint8_t *T, int K, uint64_t tb) {
-        uint32_t l = t, sp = 0;
+    uint64_t gm[RR];     // global offsets of the register bits
+    // dep: deposit tables of the local->global bit map (dep[0][l & 255] |
+    // dep[1][l >> 8] = the global bits of local index l)
+    __device__ __forceinline__ void make(uint32_t t, const uint8_t *S, const uint64_t *dlo, const uint64_t *dhi,
+                                         uint64_t tb) {
+        uint32_t l = t;
+#pragma unroll
+        for (int i = 0; i < RR; i++) l = insert_zero32(l, S[i]);
+        lt = l;
+        gt = tb | dlo[l & 255] | dhi[l >> 8];
+        slt = swz(l);
 #pragma unroll
         for (int i = 0; i < RR; i++) {
-            l = insert_zero32(l, S[i]);
-            sp |= (uint32_t)S[i] << (8 * i);
+            slm[i] = swz(1u << S[i]);
+            gm[i] = S[i] < 8 ? dlo[1u << S[i]] : dhi[1u << (S[i] - 8)];
         }
-        spos = sp;
-        slt = swz(l);
-        uint64_t g = tb;
-        for (int i = 0; i < K; i++)
-            if ((l >> i) & 1) g |= 1ull << T[i];
-        gt = g;
     }
-    __device__ __forceinline__ int s(int i) const { return (spos >> (8 * i)) & 0xFF; }
     template <int V>
     __device__ __forceinline__ uint32_t sidx() const {
         uint32_t o = slt;
 #pragma unroll
         for (int i = 0; i < RR; i++)
-            if (V & (1 << i)) o ^= swz(1u << s(i));
+            if (V & (1 << i)) o ^= slm[i];
+        return o;
+    }
+    // slot offset of a runtime register index u (folds the flip mask)
+    __device__ __forceinline__ uint32_t soff_dyn(uint32_t u) const {
+        uint32_t o = 0;
+#pragma unroll
+        for (int i = 0; i < RR; i++)
+            if ((u >> i) & 1) o ^= slm[i];
         return o;
     }
     template <int V>
-    __device__ __forceinline__ uint64_t goff(const uint8_t *T) const {
+    __device__ __forceinline__ uint64_t goff() const {
         uint64_t o = 0;
 #pragma unroll
         for (int i = 0; i < RR; i++)
-            if (V & (1 << i)) o |= 1ull << T[s(i)];
+            if (V & (1 << i)) o |= gm[i];
+        return o;
+    }
+};
+
+// Read slots of a mapping through an entry permutation: register slot l
+// reads position P^-1(l) = Ainv l + binv.
+template <int RR>
+struct PermSlots {
+    uint32_t slt, slm[RR];
+    __device__ __forceinline__ void make(const Mapping<RR> &m, const uint8_t *S, int K, const KPerm &pm,
+                                         uint32_t binv) {
+        uint32_t lp = binv;
+        for (int i = 0; i < K; i++)
+            if ((m.lt >> i) & 1) lp ^= pm.col[i];
+        slt = swz(lp);
+#pragma unroll
+        for (int i = 0; i < RR; i++) slm[i] = swz(pm.col[S[i]]);
+    }
+    template <int V>
+    __device__ __forceinline__ uint32_t sidx() const {
+        uint32_t o = slt;
+#pragma unroll
+        for (int i = 0; i < RR; i++)
+            if (V & (1 << i)) o ^= slm[i];
         return o;
     }
 };
@@ -125,9 +168,7 @@ __device__ __forceinline__ void ap_x(double2 (&a)[1 << RR], uint32_t rcm) {
         if (v & (1 << P)) continue;
         if ((v & rcm) != rcm) continue;
         const int w = v | (1 << P);
-        double2 x = a[v];
-        a[v] = a[w];
-        a[w] = x;
+        swap_inplace(a[v], a[w]);
     }
 }
 
@@ -153,9 +194,7 @@ __device__ __forceinline__ void ap_swap(double2 (&a)[1 << RR], uint32_t rcm) {
         if (v & ((1 << P0) | (1 << P1))) continue;
         if ((v & rcm) != rcm) continue;
         const int i1 = v | (1 << P1), i2 = v | (1 << P0);
-        double2 x = a[i1];
-        a[i1] = a[i2];
-        a[i2] = x;
+        swap_inplace(a[i1], a[i2]);
     }
 }
 
@@ -217,10 +256,32 @@ __device__ __forceinline__ void ap_cx(double2 (&a)[1 << RR]) {
     for (int v = 0; v < (1 << RR); v++) {
         if ((v & (1 << T)) || !(v & (1 << C))) continue;
         const int w = v | (1 << T);
-        double2 x = a[v];
-        a[v] = a[w];
-        a[w] = x;
+        swap_inplace(a[v], a[w]);
     }
+}
+
+template <int RR, int C, int T>
+__device__ __forceinline__ void ap_cx_n(double2 (&a)[1 << RR]) {   // control bit sense inverted
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++) {
+        if ((v & (1 << T)) || (v & (1 << C))) continue;
+        const int w = v | (1 << T);
+        swap_inplace(a[v], a[w]);
+    }
+}
+
+// Materialise a pending register flip mask (see apply_ops).
+template <int RR>
+__device__ __forceinline__ void flush_flips(double2 (&a)[1 << RR], uint32_t &fb) {
+    if (fb == 0) return;
+#pragma unroll
+    for (int p = 0; p < RR; p++)
+        if ((fb >> p) & 1) {
+#pragma unroll
+            for (int v = 0; v < (1 << RR); v++)
+                if (!(v & (1 << p))) swap_inplace(a[v], a[v | (1 << p)]);
+        }
+    fb = 0;
 }
 
 // Rare op shapes (register-controlled U1/D1, multi-register controls, U2,
@@ -304,9 +365,15 @@ __device__ __forceinline__ void apply_generic(double2 (&a)[1 << RR], const KOp &
     }
 }
 
+// Apply the ops [ob, oe) of a sub-block to the register tile.
+// fb is a pending flip mask over register positions: register v holds the
+// amplitude of logical register index v ^ fb.  X, and CNOT/CCX whose
+// controls are thread constants, only toggle fb (no data movement); the
+// mask is absorbed into the next shared-memory write or global store
+// address.  Other ops read logical bit values through fb.
 template <int RR>
 __device__ __forceinline__ void apply_ops(double2 (&a)[1 << RR], const KOp *ops, uint32_t ob, uint32_t oe,
-                                          uint64_t gbase, int n, const double2 *tab) {
+                                          uint64_t gbase, int n, const double2 *tab, uint32_t &fb) {
     double2 ttmax = make_double2(1.0, 0.0);
     uint64_t lg = 0;
     for (uint32_t oi = ob; oi < oe; oi++) {
@@ -315,20 +382,35 @@ __device__ __forceinline__ void apply_ops(double2 (&a)[1 << RR], const KOp *ops,
         const double2 *M = tab + op.aux;
         const int code = op.code;
         switch (code) {
-#define U1C(P) case C_U1 + P: if (RR > P) ap_u1<RR, (RR > P ? P : 0)>(a, M[0], M[1], M[2], M[3], 0u); break;
+#define U1C(P)                                                                         \
+        case C_U1 + P:                                                                 \
+            if (RR > P) {                                                              \
+                const bool f = (fb >> P) & 1;                                          \
+                const double2 m00 = M[0], m01 = M[1], m10 = M[2], m11 = M[3];          \
+                ap_u1<RR, (RR > P ? P : 0)>(a, f ? m11 : m00, f ? m10 : m01,            \
+                                            f ? m01 : m10, f ? m00 : m11, 0u);          \
+            }                                                                          \
+            break;
         U1C(0) U1C(1) U1C(2) U1C(3)
 #undef U1C
-#define XC(P) case C_X + P: if (RR > P) ap_x<RR, (RR > P ? P : 0)>(a, 0u); break;
+#define XC(P) case C_X + P: fb ^= 1u << P; break;
         XC(0) XC(1) XC(2) XC(3)
 #undef XC
-#define CXC(C, T) case C_CX + 4 * C + T: if (RR > C && RR > T) ap_cx<RR, (RR > C ? C : 0), (RR > T ? T : 1)>(a); break;
+#define CXC(C, T)                                                                      \
+        case C_CX + 4 * C + T:                                                         \
+            if (RR > C && RR > T) {                                                    \
+                if ((fb >> C) & 1) ap_cx_n<RR, (RR > C ? C : 0), (RR > T ? T : 1)>(a);  \
+                else ap_cx<RR, (RR > C ? C : 0), (RR > T ? T : 1)>(a);                  \
+            }                                                                          \
+            break;
         CXC(0, 1) CXC(0, 2) CXC(0, 3) CXC(1, 0) CXC(1, 2) CXC(1, 3)
         CXC(2, 0) CXC(2, 1) CXC(2, 3) CXC(3, 0) CXC(3, 1) CXC(3, 2)
 #undef CXC
 #define D1C(P)                                                                      \
         case C_D1R + P:                                                             \
             if (RR > P) {                                                           \
-                const double2 d0 = M[0], d1 = M[1];                                 \
+                const bool f = (fb >> P) & 1;                                       \
+                const double2 d0 = f ? M[1] : M[0], d1 = f ? M[0] : M[1];           \
                 _Pragma("unroll") for (int v = 0; v < (1 << RR); v++)              \
                     a[v] = cmul(a[v], ((v >> (RR > P ? P : 0)) & 1) ? d1 : d0);     \
             }                                                                       \
@@ -346,6 +428,7 @@ __device__ __forceinline__ void apply_ops(double2 (&a)[1 << RR], const KOp *ops,
 #define QC(P)                                                                          \
         case C_QFT + P:                                                                \
             if (RR > P) {                                                              \
+                flush_flips<RR>(a, fb);                                                \
                 const double2 tt = qft_thread_twiddle(op, gbase, n, ttmax, lg);         \
                 ap_qft<RR, (RR > P ? P : 0)>(a, tt, M, op.flags & QF_INVERSE);          \
             }                                                                          \
@@ -359,6 +442,7 @@ __device__ __forceinline__ void apply_ops(double2 (&a)[1 << RR], const KOp *ops,
             break;
         }
         default:
+            flush_flips<RR>(a, fb);
             apply_generic<RR>(a, op, M, gbase);
             break;
         }
@@ -387,8 +471,9 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // FP64 work; results go back to HBM with plain 16-byte stores.
 // Shared memory: [buf0 2^K][buf1 2^K][staged op tables][ops].
 template <int RR>
-__global__ void __launch_bounds__(256, 1) k_tile(const __grid_constant__ KPass P, const KSub *__restrict__ subs,
-                                                 const KOp *__restrict__ ops, const double2 *__restrict__ mats,
+__global__ void __launch_bounds__(RR >= 4 ? 256 : 512, 1) k_tile(const __grid_constant__ KPass P, const KSub *__restrict__ subs,
+                                                 const KOp *__restrict__ ops, const KPerm *__restrict__ perms,
+                                                 const KPermTerm *__restrict__ pterms, const double2 *__restrict__ mats,
                                                  uint64_t mat_stride, const double2 *__restrict__ cst,
                                                  double2 *__restrict__ state, uint64_t state_stride,
                                                  uint32_t tiles_log2, uint32_t total_tiles) {
@@ -401,7 +486,33 @@ __global__ void __launch_bounds__(256, 1) k_tile(const __grid_constant__ KPass P
     double2 *s_tab = sm + 2 * TS;
     KOp *s_ops = reinterpret_cast<KOp *>(s_tab + P.smat);
     const uint32_t nops = P.op_end - P.op_begin;
+    const uint32_t nperm = P.perm_end - P.perm_begin;
+    KPerm *s_perm = reinterpret_cast<KPerm *>(s_ops + nops);
+    const uint32_t pt0 = nperm ? perms[P.perm_begin].term_begin : 0;
+    const uint32_t npt = nperm ? perms[P.perm_end - 1].term_end - pt0 : 0;
+    KPermTerm *s_pt = reinterpret_cast<KPermTerm *>(s_perm + nperm);
+    uint64_t *s_dlo = reinterpret_cast<uint64_t *>(s_pt + npt);
+    uint64_t *s_dhi = s_dlo + 256;
+    KSub *s_sub = reinterpret_cast<KSub *>(s_dhi + 32);
     const bool zero = P.flags & PF_LOAD_ZERO;
+    for (uint32_t k = threadIdx.x; k < 256 + 32; k += blockDim.x) {
+        uint64_t g = 0;
+        const uint32_t l = k < 256 ? k : (k - 256) << 8;
+        for (int i = 0; i < K; i++)
+            if ((l >> i) & 1) g |= 1ull << P.T[i];
+        s_dlo[k] = g;   // s_dhi = s_dlo + 256
+    }
+    for (uint32_t k = threadIdx.x; k < P.sub_end - P.sub_begin; k += blockDim.x) s_sub[k] = subs[P.sub_begin + k];
+    for (uint32_t k = threadIdx.x; k < nperm; k += blockDim.x) s_perm[k] = perms[P.perm_begin + k];
+    for (uint32_t k = threadIdx.x; k < npt; k += blockDim.x) s_pt[k] = pterms[pt0 + k];
+    // translation of an entry permutation for this tile
+    auto binv_of = [&](int pi, uint64_t tb) {
+        uint32_t b = 0;
+        const KPerm &pm = s_perm[pi];
+        for (uint32_t k = pm.term_begin - pt0; k < pm.term_end - pt0; k++)
+            if ((tb & s_pt[k].cmask) == s_pt[k].cmask) b ^= s_pt[k].vec;
+        return b;
+    };
 
     // this thread's copy slots: local index l = t + v * NT (top RR bits = v)
     uint64_t dep_t = 0;
@@ -454,43 +565,66 @@ __global__ void __launch_bounds__(256, 1) k_tile(const __grid_constant__ KPass P
         const uint64_t tb = tile_base(g);
         double2 a[NV];
         Mapping<RR> cur;
-        KSub sb = subs[P.sub_begin];
-        cur.make(t, sb.S, P.T, K, tb);
+        KSub sb = s_sub[0];
+        cur.make(t, sb.S, s_dlo, s_dhi, tb);
         uint32_t cur_m = smask<RR>(sb.S);
-        if (zero) {
-            Unroll<RR>::run([&](auto V) {
-                const uint64_t gi = cur.gt + cur.template goff<decltype(V)::value>(P.T);
-                a[decltype(V)::value] = make_double2(gi == 0 ? 1.0 : 0.0, 0.0);
-            });
+        // registers <- buffer (through the entry permutation, if any)
+        auto load_regs = [&](int perm, const uint8_t *S) {
+            if (perm >= 0) {
+                PermSlots<RR> ps;
+                ps.make(cur, S, K, s_perm[perm], binv_of(perm, tb));
+                Unroll<RR>::run([&](auto V) { a[decltype(V)::value] = b[ps.template sidx<decltype(V)::value>()]; });
+            } else {
+                Unroll<RR>::run([&](auto V) { a[decltype(V)::value] = b[cur.template sidx<decltype(V)::value>()]; });
+            }
+        };
+        if (zero) {   // |0...0>: amplitude 1 where the source position is local 0 of tile 0
+            if (sb.perm >= 0) {
+                PermSlots<RR> ps;
+                ps.make(cur, sb.S, K, s_perm[sb.perm], binv_of(sb.perm, tb));
+                Unroll<RR>::run([&](auto V) {
+                    a[decltype(V)::value] = make_double2((tb == 0 && ps.template sidx<decltype(V)::value>() == 0) ? 1.0 : 0.0, 0.0);
+                });
+            } else {
+                Unroll<RR>::run([&](auto V) {
+                    a[decltype(V)::value] = make_double2((tb == 0 && cur.template sidx<decltype(V)::value>() == 0) ? 1.0 : 0.0, 0.0);
+                });
+            }
         } else {
-            Unroll<RR>::run([&](auto V) { a[decltype(V)::value] = b[cur.template sidx<decltype(V)::value>()]; });
+            load_regs(sb.perm, sb.S);
         }
+        uint32_t fb = 0;   // pending register flip mask (apply_ops)
         for (uint32_t s = P.sub_begin; s < P.sub_end; s++) {
             if (s != P.sub_begin) {
-                sb = subs[s];
+                sb = s_sub[s - P.sub_begin];
                 const uint32_t m = smask<RR>(sb.S);
-                if (m != cur_m) {
+                if (m != cur_m || sb.perm >= 0) {
                     __syncthreads();   // everyone has read the previous mapping's slots
-                    Unroll<RR>::run([&](auto V) { b[cur.template sidx<decltype(V)::value>()] = a[decltype(V)::value]; });
+                    const uint32_t adj = cur.soff_dyn(fb);
+                    Unroll<RR>::run([&](auto V) { b[cur.template sidx<decltype(V)::value>() ^ adj] = a[decltype(V)::value]; });
+                    fb = 0;
                     __syncthreads();
-                    cur.make(t, sb.S, P.T, K, tb);
+                    cur.make(t, sb.S, s_dlo, s_dhi, tb);
                     cur_m = m;
-                    Unroll<RR>::run([&](auto V) { a[decltype(V)::value] = b[cur.template sidx<decltype(V)::value>()]; });
+                    load_regs(sb.perm, sb.S);
                 }
             }
-            apply_ops<RR>(a, s_ops, sb.op_begin - P.op_begin, sb.op_end - P.op_begin, cur.gt, P.n, s_tab);
+            apply_ops<RR>(a, s_ops, sb.op_begin - P.op_begin, sb.op_end - P.op_begin, cur.gt, P.n, s_tab, fb);
         }
         double2 *psi = state + (uint64_t)circ * state_stride;
         const uint32_t ms = smask<RR>(P.Sstore);
-        if (ms != cur_m) {
+        // a non-zero flip mask would scatter the lanes of each store: go
+        // through shared memory (collective decision: the exchange syncs)
+        if (__syncthreads_or(ms != cur_m || fb != 0 || P.store_perm >= 0)) {
+            const uint32_t adj = cur.soff_dyn(fb);
+            Unroll<RR>::run([&](auto V) { b[cur.template sidx<decltype(V)::value>() ^ adj] = a[decltype(V)::value]; });
+            fb = 0;
             __syncthreads();
-            Unroll<RR>::run([&](auto V) { b[cur.template sidx<decltype(V)::value>()] = a[decltype(V)::value]; });
-            __syncthreads();
-            cur.make(t, P.Sstore, P.T, K, tb);
-            Unroll<RR>::run([&](auto V) { a[decltype(V)::value] = b[cur.template sidx<decltype(V)::value>()]; });
+            cur.make(t, P.Sstore, s_dlo, s_dhi, tb);
+            load_regs(P.store_perm, P.Sstore);
         }
         Unroll<RR>::run([&](auto V) {
-            psi[cur.gt + cur.template goff<decltype(V)::value>(P.T)] = a[decltype(V)::value];
+            psi[cur.gt + cur.template goff<decltype(V)::value>()] = a[decltype(V)::value];
         });
         __syncthreads();   // buffer b is refilled by the next iteration's prefetch
     }

@@ -30,6 +30,7 @@ std::atomic<uint64_t> g_launches{0};
 std::atomic<int64_t> g_opt_fusion{1};
 std::atomic<int64_t> g_opt_K{0};
 std::atomic<int64_t> g_opt_coalesce{3};
+std::atomic<int64_t> g_opt_regbits{4};
 const double PI = 3.14159265358979323846264338327950288;
 
 lq_status fail(lq_status s, const std::string &msg) {
@@ -49,6 +50,54 @@ lq_status fail(lq_status s, const std::string &msg) {
         lq_status s_ = (x);                \
         if (s_ != LQ_OK) return s_;        \
     } while (0)
+
+// ---- optional per-launch CUDA-event timing (LQ_OPT_KERNEL_TIMING) ----
+enum KClass { KC_TILE = 0, KC_PAIR = 1, KC_DIAG = 2, KC_PAULI = 3, KC_OTHER = 4, KC_N = 5 };
+std::atomic<int64_t> g_opt_timing{0};
+struct TimedLaunch { int cls; cudaEvent_t a, b; };
+std::vector<TimedLaunch> g_timed;
+std::vector<cudaEvent_t> g_event_pool;
+double g_time_ms[KC_N] = {0, 0, 0, 0, 0};
+uint64_t g_time_cnt[KC_N] = {0, 0, 0, 0, 0};
+
+cudaEvent_t pool_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+struct LaunchTimer {
+    int cls;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    LaunchTimer(int c, cudaStream_t s) : cls(c), st(s) {
+        if (g_opt_timing.load()) { a = pool_event(); cudaEventRecord(a, st); }
+    }
+    ~LaunchTimer() {
+        if (a) {
+            cudaEvent_t b = pool_event();
+            cudaEventRecord(b, st);
+            g_timed.push_back({cls, a, b});
+        }
+    }
+};
+void harvest_timing() {
+    for (auto &t : g_timed) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(t.b) == cudaSuccess && cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) {
+            g_time_ms[t.cls] += ms;
+            g_time_cnt[t.cls] += 1;
+        }
+        g_event_pool.push_back(t.a);
+        g_event_pool.push_back(t.b);
+    }
+    g_timed.clear();
+    cudaGetLastError();
+}
 
 lq_status check_launch(const char *what) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -72,6 +121,7 @@ PlanOptions options() {
     o.K = (int)g_opt_K.load();
     o.coalesce = (int)g_opt_coalesce.load();
     o.fusion = g_opt_fusion.load() != 0;
+    o.reg_bits = (int)g_opt_regbits.load();
     return o;
 }
 
@@ -198,13 +248,16 @@ lq_status validate_terms(int n, const lq_pauli_term *t, size_t nt) {
 
 // ---------------------------------------------------------------- launches
 template <int RR>
-lq_status launch_tile_rr(const KPass &kp, const KSub *subs, const KOp *kops, const double2 *mats,
+lq_status launch_tile_rr(const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
+                         const KPermTerm *pterms, uint32_t n_pterms, const double2 *mats,
                          uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride,
                          int n_circ, cudaStream_t st) {
     static bool attr = false;
     static int n_sm = 0;
     const size_t smem = ((size_t)32 << kp.K) + (size_t)kp.smat * sizeof(double2) +
-                        (size_t)(kp.op_end - kp.op_begin) * sizeof(KOp);
+                        (size_t)(kp.op_end - kp.op_begin) * sizeof(KOp) +
+                        (size_t)(kp.perm_end - kp.perm_begin) * sizeof(KPerm) + (size_t)n_pterms * sizeof(KPermTerm) +
+                        (256 + 32) * sizeof(uint64_t) + (size_t)(kp.sub_end - kp.sub_begin) * sizeof(KSub);
     if (!attr) {
         CUDA_TRY(cudaFuncSetAttribute(k_tile<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         int dev = 0;
@@ -217,18 +270,20 @@ lq_status launch_tile_rr(const KPass &kp, const KSub *subs, const KOp *kops, con
     const uint64_t total = (uint64_t)n_circ << tiles_log2;
     if (total >= (1ull << 32)) return fail(LQ_ERR_DIM, "too many tiles in one launch");
     const unsigned grid = (unsigned)std::min<uint64_t>(total, (uint64_t)n_sm);
-    k_tile<RR><<<grid, 1u << (kp.K - RR), smem, st>>>(kp, subs, kops, mats, mat_stride, cst, state, state_stride,
-                                                      tiles_log2, (uint32_t)total);
+    LaunchTimer lt_(KC_TILE, st);
+    k_tile<RR><<<grid, 1u << (kp.K - RR), smem, st>>>(kp, subs, kops, perms, pterms, mats, mat_stride, cst, state,
+                                                      state_stride, tiles_log2, (uint32_t)total);
     return check_launch("k_tile");
 }
 
-lq_status launch_tile(const KPass &kp, const KSub *subs, const KOp *kops, const double2 *mats, uint64_t mat_stride,
-                      const double2 *cst, double2 *state, uint64_t state_stride, int n_circ, cudaStream_t st) {
-    switch (std::min(R, kp.K)) {
-    case 1: return launch_tile_rr<1>(kp, subs, kops, mats, mat_stride, cst, state, state_stride, n_circ, st);
-    case 2: return launch_tile_rr<2>(kp, subs, kops, mats, mat_stride, cst, state, state_stride, n_circ, st);
-    case 3: return launch_tile_rr<3>(kp, subs, kops, mats, mat_stride, cst, state, state_stride, n_circ, st);
-    default: return launch_tile_rr<4>(kp, subs, kops, mats, mat_stride, cst, state, state_stride, n_circ, st);
+lq_status launch_tile(int Rr, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms, const KPermTerm *pterms,
+                      uint32_t n_pterms, const double2 *mats, uint64_t mat_stride, const double2 *cst, double2 *state,
+                      uint64_t state_stride, int n_circ, cudaStream_t st) {
+    switch (Rr) {
+    case 1: return launch_tile_rr<1>(kp, subs, kops, perms, pterms, n_pterms, mats, mat_stride, cst, state, state_stride, n_circ, st);
+    case 2: return launch_tile_rr<2>(kp, subs, kops, perms, pterms, n_pterms, mats, mat_stride, cst, state, state_stride, n_circ, st);
+    case 3: return launch_tile_rr<3>(kp, subs, kops, perms, pterms, n_pterms, mats, mat_stride, cst, state, state_stride, n_circ, st);
+    default: return launch_tile_rr<4>(kp, subs, kops, perms, pterms, n_pterms, mats, mat_stride, cst, state, state_stride, n_circ, st);
     }
 }
 
@@ -240,6 +295,8 @@ unsigned grid_for(uint64_t work, unsigned per_block = 256) {
 struct DevPlan {
     const KSub *subs = nullptr;
     const KOp *kops = nullptr;
+    const KPerm *perms = nullptr;
+    const KPermTerm *pterms = nullptr;
     const MSpec *specs = nullptr;
     const MFactor *factors = nullptr;
     const double2 *cst = nullptr;
@@ -258,17 +315,23 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
         if (p.kind == PASS_TILE) {
             KPass kp = p.kp;
             if (zero_first && i == 0) kp.flags |= PF_LOAD_ZERO;
-            LQ_TRY(launch_tile(kp, dp.subs, dp.kops, mats, mat_stride, dp.cst, state, state_stride, n_circ, st));
+            uint32_t npt = 0;
+            if (kp.perm_end > kp.perm_begin)
+                npt = plan.perms[kp.perm_end - 1].term_end - plan.perms[kp.perm_begin].term_begin;
+            LQ_TRY(launch_tile(plan.Rr, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, mats, mat_stride, dp.cst, state,
+                               state_stride, n_circ, st));
         } else if (p.kind == PASS_PAIR) {
             const KOp op = plan.kops[p.op_begin];
             uint64_t work = (op.type == K_U1 || op.type == K_X) ? (1ull << (n - 1)) : (1ull << (n - 2));
             dim3 grid(grid_for(work), n_circ);
+            LaunchTimer lt_(KC_PAIR, st);
             k_pair<<<grid, 256, 0, st>>>(n, op, mats, mat_stride, state, state_stride);
             LQ_TRY(check_launch("k_pair"));
         } else {
             for (uint32_t b = p.op_begin; b < p.op_end; b += DIAG_MAX_OPS) {
                 int cnt = (int)std::min<uint32_t>(DIAG_MAX_OPS, p.op_end - b);
                 dim3 grid(grid_for(1ull << n), n_circ);
+                LaunchTimer lt_(KC_DIAG, st);
                 k_diag<<<grid, 256, 0, st>>>(n, dp.kops + b, cnt, mats, mat_stride, state, state_stride);
                 LQ_TRY(check_launch("k_diag"));
             }
@@ -291,6 +354,7 @@ lq_status launch_pauli_rr(const KPauliPass &P, const PTerm *terms, const double2
         attr = true;
     }
     dim3 grid((unsigned)(1ull << (P.n - P.K)), (unsigned)n_circ);
+    LaunchTimer lt_(KC_PAULI, st);
     k_pauli_tile<RR><<<grid, 1u << (P.K - RR), pauli_smem(P.K), st>>>(P, terms, state, state_stride, partial,
                                                                         slot_stride);
     return check_launch("k_pauli_tile");
@@ -308,6 +372,7 @@ lq_status launch_pauli(const PauliPlan &pp, const PTerm *dterms, const double2 *
     }
     for (const auto &D : pp.direct) {
         dim3 grid(D.n_blocks, n_circ);
+        LaunchTimer lt_(KC_PAULI, st);
         k_pauli_direct<<<grid, 256, 0, st>>>(pp.n, D.x, dterms + D.term_begin, D.term_end - D.term_begin, state,
                                              state_stride, partial, slot_stride, D.slot);
         LQ_TRY(check_launch("k_pauli_direct"));
@@ -359,7 +424,8 @@ lq_status run_single(lq_sv *sv, const Plan &plan, const MatBuilder &mb, const do
     if (plan.passes.empty()) return LQ_OK;
     Blob blob;
     size_t o_sub = blob.add(plan.subs), o_kop = blob.add(plan.kops), o_spec = blob.add(mb.specs),
-           o_fac = blob.add(mb.factors), o_cst = blob.add(mb.cst);
+           o_fac = blob.add(mb.factors), o_cst = blob.add(mb.cst), o_perm = blob.add(plan.perms),
+           o_pt = blob.add(plan.perm_terms);
     size_t o_th = blob.add(theta, theta ? n_theta * sizeof(double) : 0);
     LQ_TRY(blob.upload(sv->plan_buf, sv->stream));
     DevPlan dp;
@@ -368,6 +434,8 @@ lq_status run_single(lq_sv *sv, const Plan &plan, const MatBuilder &mb, const do
     dp.specs = sv->plan_buf.at<MSpec>(o_spec);
     dp.factors = sv->plan_buf.at<MFactor>(o_fac);
     dp.cst = sv->plan_buf.at<double2>(o_cst);
+    dp.perms = sv->plan_buf.at<KPerm>(o_perm);
+    dp.pterms = sv->plan_buf.at<KPermTerm>(o_pt);
     double2 *mats = nullptr;
     if (mb.mat_size) {
         LQ_TRY(sv->work_buf.reserve((size_t)mb.mat_size * sizeof(double2), sv->stream));
@@ -417,6 +485,20 @@ int lq_device_count(void) {
 
 uint64_t lq_launch_count(void) { return g_launches.load(); }
 
+lq_status lq_kernel_timing(int kernel_class, double *total_ms, uint64_t *count) {
+    if (kernel_class < 0 || kernel_class >= KC_N) return fail(LQ_ERR_ARG, "bad kernel class");
+    harvest_timing();
+    if (total_ms) *total_ms = g_time_ms[kernel_class];
+    if (count) *count = g_time_cnt[kernel_class];
+    return LQ_OK;
+}
+
+lq_status lq_kernel_timing_reset(void) {
+    harvest_timing();
+    for (int k = 0; k < KC_N; k++) { g_time_ms[k] = 0; g_time_cnt[k] = 0; }
+    return LQ_OK;
+}
+
 lq_status lq_set_option(int option, int64_t value) {
     switch (option) {
     case LQ_OPT_FUSION: g_opt_fusion = value ? 1 : 0; return LQ_OK;
@@ -428,6 +510,13 @@ lq_status lq_set_option(int option, int64_t value) {
         if (value < 0 || value > 6) return fail(LQ_ERR_ARG, "coalesce bits must be 0..6");
         g_opt_coalesce = value;
         return LQ_OK;
+    case LQ_OPT_REG_BITS:
+        if (value != 3 && value != 4) return fail(LQ_ERR_ARG, "register bits must be 3 or 4");
+        g_opt_regbits = value;
+        return LQ_OK;
+    case LQ_OPT_KERNEL_TIMING:
+        g_opt_timing = value ? 1 : 0;
+        return LQ_OK;
     default: return fail(LQ_ERR_ARG, "unknown option");
     }
 }
@@ -437,6 +526,8 @@ int64_t lq_get_option(int option) {
     case LQ_OPT_FUSION: return g_opt_fusion.load();
     case LQ_OPT_TILE_BITS: return g_opt_K.load();
     case LQ_OPT_COALESCE_BITS: return g_opt_coalesce.load();
+    case LQ_OPT_REG_BITS: return g_opt_regbits.load();
+    case LQ_OPT_KERNEL_TIMING: return g_opt_timing.load();
     default: return -1;
     }
 }
@@ -693,6 +784,7 @@ struct lq_psr {
     const PsrPair *d_pairs = nullptr;
     const PTerm *d_terms = nullptr;
     uint64_t launches_per_run = 0;
+    uint64_t blob_bytes = 0;
 };
 
 extern "C" {
@@ -748,8 +840,10 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     cudaStream_t st = P->stream;
     Blob blob;
     size_t o_sub = blob.add(P->plan.subs), o_kop = blob.add(P->plan.kops), o_spec = blob.add(P->mb.specs),
-           o_fac = blob.add(P->mb.factors), o_cst = blob.add(P->mb.cst), o_sh = blob.add(P->shifts),
+           o_fac = blob.add(P->mb.factors), o_cst = blob.add(P->mb.cst), o_perm = blob.add(P->plan.perms),
+           o_pt = blob.add(P->plan.perm_terms), o_sh = blob.add(P->shifts),
            o_pr = blob.add(P->pairs), o_t = blob.add(P->pp.terms);
+    P->blob_bytes = blob.h.size();
     lq_status s = blob.upload(P->blob_buf, st);
     if (s == LQ_OK) s = P->states.reserve((size_t)B * N * sizeof(double2), st);
     if (s == LQ_OK) s = P->mats.reserve((size_t)B * std::max<uint32_t>(P->mb.mat_size, 1) * sizeof(double2), st);
@@ -766,6 +860,8 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     P->dp.specs = P->blob_buf.at<MSpec>(o_spec);
     P->dp.factors = P->blob_buf.at<MFactor>(o_fac);
     P->dp.cst = P->blob_buf.at<double2>(o_cst);
+    P->dp.perms = P->blob_buf.at<KPerm>(o_perm);
+    P->dp.pterms = P->blob_buf.at<KPermTerm>(o_pt);
     P->d_shifts = P->blob_buf.at<Shift>(o_sh);
     P->d_pairs = P->blob_buf.at<PsrPair>(o_pr);
     P->d_terms = P->blob_buf.at<PTerm>(o_t);
@@ -803,10 +899,13 @@ lq_status lq_psr_run(lq_psr *P, const double *theta_dev, double *grad_dev, doubl
     return LQ_OK;
 }
 
-lq_status lq_psr_stats(const lq_psr *P, uint64_t *n_circuits, uint64_t *n_launches) {
+lq_status lq_psr_stats(const lq_psr *P, uint64_t *n_circuits, uint64_t *n_launches, uint64_t *plan_bytes,
+                       uint64_t *tile_passes) {
     if (!P) return fail(LQ_ERR_ARG, "invalid plan");
     if (n_circuits) *n_circuits = P->shifts.size();
     if (n_launches) *n_launches = P->launches_per_run;
+    if (plan_bytes) *plan_bytes = P->blob_bytes;
+    if (tile_passes) *tile_passes = P->plan.n_tile;
     return LQ_OK;
 }
 

@@ -89,6 +89,26 @@ enum CodeTile : uint8_t {
 struct KSub {
     uint8_t S[R];        // local bit positions held in registers (ascending)
     uint32_t op_begin, op_end;
+    int32_t perm;        // entry permutation (pass-local index into the KPerm list), -1: none
+};
+
+// An affine permutation of the tile's local index, folded into a shared
+// memory exchange: gates X, CNOT, SWAP, and multi-controlled X whose
+// controls are tile constants map basis state |l> to |A l + b> over GF(2).
+// The kernel reads register slot l' of the next mapping from position
+// P^-1(l') = Ainv l' + binv, binv = sum over terms with (tile & cmask) ==
+// cmask of vec.  Permutation gates folded this way cost no instructions
+// beyond the exchange itself.
+struct KPerm {
+    uint16_t col[MAXK];  // columns of Ainv (local bit masks)
+    uint32_t term_begin, term_end;
+    uint32_t pad;        // keeps sizeof a multiple of 8 (KPermTerm follows in shared memory)
+};
+static_assert(sizeof(KPerm) % 8 == 0, "KPerm alignment");
+struct KPermTerm {
+    uint64_t cmask;      // physical tile-constant condition bits (0 = always)
+    uint32_t vec;        // local translation (already multiplied by Ainv)
+    uint32_t pad;
 };
 
 enum PassFlags : uint32_t {
@@ -117,10 +137,12 @@ struct KPass {
     uint32_t sub_begin, sub_end;
     uint32_t op_begin, op_end;   // contiguous op range of the pass
     uint32_t smat;       // staged table size (double2)
+    uint32_t perm_begin, perm_end;   // KPerm range of the pass (global indices)
+    int32_t store_perm;  // permutation applied before the store (pass-local), -1: none
     uint32_t flags;
     uint8_t T[MAXK];     // physical bit of each local bit, ascending
-    uint8_t Sload[R];    // local bits of the register mapping used for the HBM load
-    uint8_t Sstore[R];   // ... and for the HBM store
+    uint8_t Sload[R];    // (unused by the persistent kernel; kept for layout)
+    uint8_t Sstore[R];   // local bits of the register mapping used for the HBM store
     uint8_t pad[2];
 };
 

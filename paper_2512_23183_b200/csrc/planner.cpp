@@ -292,6 +292,7 @@ static uint8_t tile_code(const KOp &k) {
 static void finalize_pass_tables(PlanPass &pp, Plan &plan) {
     pp.kp.op_begin = plan.subs[pp.kp.sub_begin].op_begin;
     pp.kp.op_end = plan.subs[pp.kp.sub_end - 1].op_end;
+    if (pp.kp.perm_end < pp.kp.perm_begin) pp.kp.perm_end = pp.kp.perm_begin;
     uint32_t off = 0;
     for (uint32_t i = pp.kp.op_begin; i < pp.kp.op_end; i++) {
         plan.kops[i].code = tile_code(plan.kops[i]);
@@ -301,7 +302,103 @@ static void finalize_pass_tables(PlanPass &pp, Plan &plan) {
     pp.kp.smat = off;
 }
 
-// Build a TILE pass from absorbed ops (execution order) and tile mask Tm.
+// An X-type op (X, CNOT, CCX) or SWAP is an affine permutation of the
+// tile's local index when at most one control lies in the tile and, in that
+// case, none lies outside (a tile-constant control makes it a conditional
+// translation).
+static bool foldable(const POp &o, const LocalMap &L) {
+    if (o.type == K_SWAP) return o.ctrl == 0;
+    if (o.type != K_X) return false;
+    int in_t = 0;
+    uint64_t out = 0, c = o.ctrl;
+    while (c) {
+        int b = __builtin_ctzll(c);
+        if (L.loc[b] >= 0) in_t++; else out |= bit(b);
+        c &= c - 1;
+    }
+    return in_t == 0 || (in_t == 1 && out == 0);
+}
+
+// Affine map l -> A l + sum_i [tile & cm_i == cm_i] v_i over GF(2)^K.
+struct Affine {
+    int K;
+    uint32_t A[MAXK];                 // columns A e_j
+    std::vector<std::pair<uint64_t, uint32_t>> terms;
+    explicit Affine(int k) : K(k) { for (int j = 0; j < K; j++) A[j] = 1u << j; }
+    template <class F> void linear(F M) {
+        for (int j = 0; j < K; j++) A[j] = M(A[j]);
+        for (auto &t : terms) t.second = M(t.second);
+    }
+    void add(const POp &o, const LocalMap &L) {
+        if (o.type == K_SWAP) {
+            int a = L.loc[o.t0], b = L.loc[o.t1];
+            linear([&](uint32_t v) {
+                uint32_t x = ((v >> a) ^ (v >> b)) & 1u;
+                return v ^ (x << a) ^ (x << b);
+            });
+            return;
+        }
+        int t = L.loc[o.t0];
+        int cin = -1;
+        uint64_t out = 0, c = o.ctrl;
+        while (c) {
+            int b = __builtin_ctzll(c);
+            if (L.loc[b] >= 0) cin = L.loc[b]; else out |= bit(b);
+            c &= c - 1;
+        }
+        if (cin >= 0) linear([&](uint32_t v) { return v ^ (((v >> cin) & 1u) << t); });
+        else terms.push_back({out, 1u << t});
+    }
+    // columns of A^-1 (Gauss-Jordan on [A | I])
+    void inverse(uint32_t *inv) const {
+        uint32_t rowsA[MAXK], rowsI[MAXK];
+        for (int i = 0; i < K; i++) {
+            rowsA[i] = 0;
+            for (int j = 0; j < K; j++) if ((A[j] >> i) & 1) rowsA[i] |= 1u << j;
+            rowsI[i] = 1u << i;
+        }
+        for (int col = 0; col < K; col++) {
+            int piv = col;
+            while (!((rowsA[piv] >> col) & 1)) piv++;
+            std::swap(rowsA[piv], rowsA[col]);
+            std::swap(rowsI[piv], rowsI[col]);
+            for (int r = 0; r < K; r++)
+                if (r != col && ((rowsA[r] >> col) & 1)) { rowsA[r] ^= rowsA[col]; rowsI[r] ^= rowsI[col]; }
+        }
+        for (int j = 0; j < K; j++) {   // column j of inverse = bits (row i, col j) of rowsI
+            inv[j] = 0;
+            for (int i = 0; i < K; i++) if ((rowsI[i] >> j) & 1) inv[j] |= 1u << i;
+        }
+    }
+};
+
+static int32_t build_perm(const std::vector<POp> &ops, const std::vector<int> &group, const LocalMap &L,
+                          const PlanPass &pp, Plan &plan) {
+    if (group.empty()) return -1;
+    Affine F(L.K);
+    for (int i : group) F.add(ops[i], L);
+    uint32_t inv[MAXK];
+    F.inverse(inv);
+    KPerm P{};
+    for (int j = 0; j < L.K; j++) P.col[j] = (uint16_t)inv[j];
+    P.term_begin = (uint32_t)plan.perm_terms.size();
+    for (auto &t : F.terms) {
+        uint32_t v = 0;
+        for (int j = 0; j < L.K; j++) if ((t.second >> j) & 1) v ^= inv[j];
+        KPermTerm kt{};
+        kt.cmask = t.first;
+        kt.vec = v;
+        plan.perm_terms.push_back(kt);
+    }
+    P.term_end = (uint32_t)plan.perm_terms.size();
+    plan.perms.push_back(P);
+    plan.n_folded += group.size();
+    return (int32_t)(plan.perms.size() - 1 - pp.kp.perm_begin);
+}
+
+// Build a TILE pass from absorbed ops (execution order) and tile mask Tm:
+// segments = [entry permutation group][register sub-block], the entry
+// permutations being folded into the exchange that starts the sub-block.
 static void emit_tile(int n, int K, int Rr, uint64_t Tm, const std::vector<POp> &ops,
                       const std::vector<int> &absorbed, const std::vector<uint32_t> &mat_off,
                       Plan &plan) {
@@ -314,10 +411,25 @@ static void emit_tile(int n, int K, int Rr, uint64_t Tm, const std::vector<POp> 
     pp.kp.flags = 0;
     memcpy(pp.kp.T, L.T, MAXK);
     pp.kp.sub_begin = (uint32_t)plan.subs.size();
+    pp.kp.perm_begin = (uint32_t)plan.perms.size();
     pp.n_ops = (int)absorbed.size();
 
     std::vector<int> rem = absorbed;
-    std::vector<std::pair<uint32_t, std::vector<int>>> blocks;
+    auto collect_perm = [&](std::vector<int> &group) {
+        Blocker blk;
+        std::vector<int> left;
+        for (int i : rem) {
+            const POp &o = ops[i];
+            if (!blk.blocked(o) && foldable(o, L)) { group.push_back(i); continue; }
+            blk.add(o);
+            left.push_back(i);
+        }
+        rem.swap(left);
+    };
+    struct Seg { std::vector<int> entry; uint32_t Sm; std::vector<int> taken; };
+    std::vector<Seg> segs;
+    std::vector<int> entry;
+    collect_perm(entry);
     while (!rem.empty()) {
         uint32_t Sm = 0;
         Blocker blk;
@@ -325,32 +437,49 @@ static void emit_tile(int n, int K, int Rr, uint64_t Tm, const std::vector<POp> 
         for (int i : rem) {
             const POp &o = ops[i];
             if (blk.blocked(o)) { blk.add(o); left.push_back(i); continue; }
+            if (foldable(o, L)) {
+                // X / CNOT with a register target and thread-constant controls is
+                // free inside the sub-block (flip mask); otherwise defer it to the
+                // next exchange
+                bool inl = o.type == K_X && (Sm & (1u << L.loc[o.t0])) && !(L.local(o.ctrl) & Sm);
+                if (inl) taken.push_back(i);
+                else { blk.add(o); left.push_back(i); }
+                continue;
+            }
             uint32_t need = L.local(o.full()) & ~Sm;
             if (popc(Sm | need) <= Rr) { Sm |= need; taken.push_back(i); }
             else { blk.add(o); left.push_back(i); }
         }
-        blocks.push_back({Sm, taken});
         rem.swap(left);
+        segs.push_back({entry, Sm, taken});
+        entry.clear();
+        collect_perm(entry);
     }
-    // fill the register sets; the first and last prefer non-lane high bits
-    for (auto &b : blocks) b.first = fill_S(b.first, K, Rr, lowrun);
+    if (segs.empty()) segs.push_back({std::vector<int>(), 0u, std::vector<int>()});   // pure permutation pass
+    std::vector<int> store_group = entry;
+    if (segs.size() == 1 && segs[0].taken.empty() && !segs[0].entry.empty() && store_group.empty()) {
+        store_group.swap(segs[0].entry);   // a lone permutation group: apply it at the store
+    }
+    for (auto &sg : segs) sg.Sm = fill_S(sg.Sm, K, Rr, lowrun);
     uint32_t lane_forbid = (uint32_t)((1u << std::min(lowrun, 3)) - 1);
     uint32_t top = 0;
     for (int b = K - 1; b >= 0 && popc(top) < Rr; b--) top |= 1u << b;
-    uint32_t Sl = blocks.front().first, Ss = blocks.back().first;
-    if (Sl & lane_forbid) Sl = top;
+    uint32_t Ss = segs.back().Sm;
     if (Ss & lane_forbid) Ss = top;
-    mask_to_S(Sl, pp.kp.Sload);
+    mask_to_S(segs.front().Sm, pp.kp.Sload);
     mask_to_S(Ss, pp.kp.Sstore);
-    for (auto &b : blocks) {
-        KSub s{};
-        mask_to_S(b.first, s.S);
-        s.op_begin = (uint32_t)plan.kops.size();
-        for (int i : b.second) plan.kops.push_back(lower_tile_op(ops[i], L, s.S, Rr, mat_off));
-        s.op_end = (uint32_t)plan.kops.size();
-        plan.subs.push_back(s);
+    for (auto &sg : segs) {
+        KSub sb{};
+        mask_to_S(sg.Sm, sb.S);
+        sb.perm = build_perm(ops, sg.entry, L, pp, plan);
+        sb.op_begin = (uint32_t)plan.kops.size();
+        for (int i : sg.taken) plan.kops.push_back(lower_tile_op(ops[i], L, sb.S, Rr, mat_off));
+        sb.op_end = (uint32_t)plan.kops.size();
+        plan.subs.push_back(sb);
     }
+    pp.kp.store_perm = build_perm(ops, store_group, L, pp, plan);
     pp.kp.sub_end = (uint32_t)plan.subs.size();
+    pp.kp.perm_end = (uint32_t)plan.perms.size();
     finalize_pass_tables(pp, plan);
     plan.passes.push_back(pp);
     plan.n_tile++;
@@ -365,7 +494,8 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
     int K = opt.K > 0 ? std::min(opt.K, n) : auto_tile_bits(n);
     if (K > 12) K = 12;   // two 2^K buffers must fit in shared memory
     if (n <= K) K = n;
-    int Rr = std::min(R, K);
+    int Rr = std::min(std::max(1, std::min(opt.reg_bits, R)), K);
+    plan.Rr = Rr;
     plan.n = n;
     plan.K = K;
     if (!opt.fusion) {
@@ -502,7 +632,8 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
     int K = opt.K > 0 ? std::min(opt.K, n) : auto_tile_bits(n);
     if (K > 12) K = 12;
     if (n <= K) K = n;
-    int Rr = std::min(R, K);
+    int Rr = std::min(std::max(1, std::min(opt.reg_bits, R)), K);
+    plan.Rr = Rr;
     int c = std::max(0, std::min(opt.coalesce, K - 1));   // room for at least one stage bit
     uint64_t mand = (n > K) ? ((1ull << c) - 1) : ((1ull << n) - 1);
     plan.n = n;
@@ -525,6 +656,8 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
         pp.kp.K = K;
         memcpy(pp.kp.T, L.T, MAXK);
         pp.kp.sub_begin = (uint32_t)plan.subs.size();
+        pp.kp.perm_begin = pp.kp.perm_end = (uint32_t)plan.perms.size();
+        pp.kp.store_perm = -1;
         pp.n_ops = (int)st.size();
         std::vector<uint32_t> Sms;
         for (size_t a = 0; a < st.size(); a += Rr) {
@@ -543,6 +676,7 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
         for (size_t a = 0, blk = 0; a < st.size(); a += Rr, blk++) {
             KSub sb{};
             mask_to_S(Sms[blk], sb.S);
+            sb.perm = -1;
             sb.op_begin = (uint32_t)plan.kops.size();
             for (size_t b = a; b < std::min(st.size(), a + Rr); b++) {
                 int j = st[b], p = phys(j);
@@ -684,7 +818,8 @@ void plan_pauli(int n, const int32_t *qmap, const lq_pauli_term *terms, size_t n
 std::string describe(const Plan &plan) {
     std::ostringstream os;
     os << "n=" << plan.n << " K=" << plan.K << " passes=" << plan.passes.size()
-       << " (tile " << plan.n_tile << ", pair " << plan.n_pair << ", diag " << plan.n_diag << ")\n";
+       << " (tile " << plan.n_tile << ", pair " << plan.n_pair << ", diag " << plan.n_diag
+       << ") folded_perm_gates=" << plan.n_folded << "\n";
     for (size_t i = 0; i < plan.passes.size(); i++) {
         const PlanPass &p = plan.passes[i];
         if (p.kind == PASS_TILE) {

@@ -43,10 +43,14 @@ struct PlanPass {
 struct Plan {
     int n = 0;
     int K = 0;
+    int Rr = 0;               // register bits of the tile passes
     std::vector<PlanPass> passes;
     std::vector<KSub> subs;
     std::vector<KOp> kops;
+    std::vector<KPerm> perms;
+    std::vector<KPermTerm> perm_terms;
     size_t n_tile = 0, n_pair = 0, n_diag = 0;
+    size_t n_folded = 0;      // permutation gates folded into exchanges
 };
 
 struct MatBuilder {
@@ -62,6 +66,7 @@ struct PlanOptions {
     int K = 0;               // tile bits (0 = automatic)
     int coalesce = 3;        // low physical bits a strided tile always holds
     bool fusion = true;      // false: one PAIR/DIAG pass per op
+    int reg_bits = 4;        // register bits per thread (R); tile kernels run 2^(K-R) threads
 };
 
 // Lower user gates (already validated) to POps on physical bits.  SWAP

@@ -35,7 +35,8 @@ STATUS_NAMES = {0: "LQ_OK", -1: "LQ_ERR_ARG", -2: "LQ_ERR_OOM", -3: "LQ_ERR_CUDA
 KIND_NAMES = ["H", "X", "Y", "Z", "S", "SDG", "T", "TDG", "RX", "RY", "RZ", "CNOT", "CZ", "CP",
               "SWAP", "U1", "U2", "CRY", "CCX", "RXX", "RYY", "RZZ"]
 KINDS = {k: i for i, k in enumerate(KIND_NAMES)}
-LQ_OPT_FUSION, LQ_OPT_TILE_BITS, LQ_OPT_COALESCE_BITS = 0, 1, 2
+LQ_OPT_FUSION, LQ_OPT_TILE_BITS, LQ_OPT_COALESCE_BITS, LQ_OPT_REG_BITS, LQ_OPT_KERNEL_TIMING = 0, 1, 2, 3, 4
+KC_TILE, KC_PAIR, KC_DIAG, KC_PAULI, KC_OTHER = 0, 1, 2, 3, 4
 
 
 class lq_gate(ctypes.Structure):
@@ -85,7 +86,10 @@ _SIGS = {
     "lq_psr_create": ([_i32, _GP, _sz, _sz, _TP, _sz, _i32, _i32, _P, ctypes.POINTER(_P)], _i32),
     "lq_psr_run": ([_P, _P, _P, _P], _i32),
     "lq_psr_free": ([_P], _i32),
-    "lq_psr_stats": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i32),
+    "lq_psr_stats": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_u64),
+                      ctypes.POINTER(_u64)], _i32),
+    "lq_kernel_timing": ([_i32, ctypes.POINTER(_dbl), ctypes.POINTER(_u64)], _i32),
+    "lq_kernel_timing_reset": ([], _i32),
     "lq_set_option": ([_i32, _i64], _i32),
     "lq_get_option": ([_i32], _i64),
     "lq_plan_describe": ([_i32, _GP, _sz, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.c_char_p, _sz], _i32),
@@ -316,10 +320,21 @@ def lq_psr_free(plan):
     _chk(_lib.lq_psr_free(plan))
 
 
-def lq_psr_stats(plan) -> Tuple[int, int]:
-    c, l = ctypes.c_uint64(), ctypes.c_uint64()
-    _chk(_lib.lq_psr_stats(plan, ctypes.byref(c), ctypes.byref(l)))
-    return c.value, l.value
+def lq_psr_stats(plan) -> Tuple[int, int, int, int]:
+    """(circuits, launches of the last run, plan bytes uploaded, tile passes per circuit)"""
+    c, l, b, t = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    _chk(_lib.lq_psr_stats(plan, ctypes.byref(c), ctypes.byref(l), ctypes.byref(b), ctypes.byref(t)))
+    return c.value, l.value, b.value, t.value
+
+
+def lq_kernel_timing(kernel_class: int) -> Tuple[float, int]:
+    ms, n = ctypes.c_double(), ctypes.c_uint64()
+    _chk(_lib.lq_kernel_timing(kernel_class, ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value
+
+
+def lq_kernel_timing_reset():
+    _chk(_lib.lq_kernel_timing_reset())
 
 
 def lq_plan_describe(n_qubits: int, gates) -> Tuple[int, int, str]:

@@ -32,6 +32,7 @@ def _restore_options(lq):
     lq.lq_set_option(lq.LQ_OPT_FUSION, 1)
     lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 0)
     lq.lq_set_option(lq.LQ_OPT_COALESCE_BITS, 3)
+    lq.lq_set_option(lq.LQ_OPT_REG_BITS, 4)
 
 
 def grad_close(g, go):
@@ -125,11 +126,14 @@ def test_rich_random_circuit(lq, oracle, n):
     assert np.abs(got - ref).max() <= AMP_TOL
 
 
+@pytest.mark.parametrize("rb", [3, 4])
 @pytest.mark.parametrize("K", [2, 3, 5, 8, 12])
 @pytest.mark.parametrize("n", [9, 15])
-def test_tile_sizes_and_multi_tile(lq, oracle, n, K):
-    """Small tiles force many tiles / ragged register sets at small n."""
+def test_tile_sizes_and_multi_tile(lq, oracle, n, K, rb):
+    """Small tiles force many tiles / ragged register sets at small n;
+    both register-block sizes (8 or 16 amplitudes per thread)."""
     lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
+    lq.lq_set_option(lq.LQ_OPT_REG_BITS, rb)
     rng = np.random.default_rng(2000 + n * 16 + K)
     gates = rich_circuit(n, 120, rng)
     ref = run_oracle(oracle, n, 7, gates)
@@ -230,9 +234,11 @@ def test_qft_inverse_and_roundtrip(lq, oracle, n):
     sv.free()
 
 
-@pytest.mark.parametrize("K", [3, 6])
-def test_qft_small_tiles(lq, oracle, K):
+@pytest.mark.parametrize("rb", [3, 4])
+@pytest.mark.parametrize("K", [3, 6, 12])
+def test_qft_small_tiles(lq, oracle, K, rb):
     lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
+    lq.lq_set_option(lq.LQ_OPT_REG_BITS, rb)
     n = 14
     ref = run_oracle(oracle, n, 5, [], qft="forward")
     assert np.abs(run_gpu(lq, n, 5, [], qft="forward") - ref).max() <= AMP_TOL
@@ -361,9 +367,11 @@ def test_psr_shards_partition_components(lq, oracle, world):
     np.testing.assert_array_equal(acc, full)   # bit-identical
 
 
+@pytest.mark.parametrize("rb", [3, 4])
 @pytest.mark.parametrize("n", [10, 16])
-def test_xyz_ring_gradient_small(lq, oracle, n):
+def test_xyz_ring_gradient_small(lq, oracle, n, rb):
     """Config-4 structure at n where the oracle runs every component."""
+    lq.lq_set_option(lq.LQ_OPT_REG_BITS, rb)
     gates = W.hea_ansatz(n, 2, "ring")
     theta = np.random.default_rng(n).uniform(0, 2 * np.pi, 4 * n)
     terms = W.xyz_terms(n)
