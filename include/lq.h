@@ -219,6 +219,13 @@ int64_t lq_get_option(int option);
 lq_status lq_plan_describe(int n_qubits, const lq_gate *gates, size_t n_gates, uint64_t *n_passes,
                            uint64_t *n_tile, char *buf, size_t buf_len);
 
+/* Host-only: the full plan (passes, sub-blocks, lowered ops, folded
+ * permutations, Pauli-group terms, matrix specs) of `gates` followed by the
+ * Pauli sum `terms` (may be empty), as JSON text.  *needed receives the
+ * buffer size required (including the terminating NUL). */
+lq_status lq_plan_export_json(int n_qubits, const lq_gate *gates, size_t n_gates, const lq_pauli_term *terms,
+                              size_t n_terms, char *buf, size_t buf_len, size_t *needed);
+
 /* Accumulated device time of launches made while LQ_OPT_KERNEL_TIMING was
  * on, per kernel class: 0 tile pass, 1 pair pass, 2 diagonal pass,
  * 3 Pauli expectation, 4 other.  Synchronises on the recorded events. */

@@ -29,6 +29,37 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
 }
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 
+// Deterministic block reduction (fixed shuffle tree + fixed smem tree).
+// red: >= max(32, blockDim.x) doubles of shared memory.  blockDim.x must be
+// a power of two.  Result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double *red) {
+    const int nt = blockDim.x, t = threadIdx.x;
+    if (nt >= 32) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        const int w = t >> 5, l = t & 31;
+        if (l == 0) red[w] = v;
+        __syncthreads();
+        double r = 0.0;
+        if (w == 0) {
+            r = (l < (nt >> 5)) ? red[l] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+        }
+        __syncthreads();
+        return r;
+    }
+    red[t] = v;
+    __syncthreads();
+    for (int s = nt >> 1; s > 0; s >>= 1) {
+        if (t < s) red[t] += red[t + s];
+        __syncthreads();
+    }
+    double r = red[0];
+    __syncthreads();
+    return r;
+}
+
 // In-place register swap the compiler cannot turn into a renaming (a
 // renaming would force loop-carried copies of the whole register tile).
 __device__ __forceinline__ void swap_inplace(double2 &x, double2 &y) {
@@ -365,6 +396,96 @@ __device__ __forceinline__ void apply_generic(double2 (&a)[1 << RR], const KOp &
     }
 }
 
+// Pauli-group expectation on the register tile (SURVEY
+// §8(a) a7).  For the group's x mask X (register positions) and register
+// index v: w_v = conj(a[v ^ X]) a[v]; a term (c, z, y) contributes
+//   c (-1)^{popcount(gbase & znr)} Re[ i^y sum_v chi_zreg(v) w_v ].
+// sum_v chi_p(v) w_v for all 16 patterns p is one Walsh-Hadamard transform
+// of w.  Pairs (v, v ^ X) give conjugate w, so only half are formed.
+template <int RR, int X, bool IM>
+__device__ __forceinline__ void expv_w(const double2 (&a)[1 << RR], double (&w)[1 << RR]) {
+    if constexpr (X == 0) {
+#pragma unroll
+        for (int v = 0; v < (1 << RR); v++) w[v] = IM ? 0.0 : fma(a[v].x, a[v].x, a[v].y * a[v].y);
+    } else {
+        constexpr int lowb = X & -X;
+#pragma unroll
+        for (int v = 0; v < (1 << RR); v++) {
+            if (v & lowb) continue;
+            const double2 p = a[v ^ X], q = a[v];
+            if constexpr (IM) {
+                const double im = fma(p.x, q.y, -p.y * q.x);
+                w[v] = im;
+                w[v ^ X] = -im;
+            } else {
+                const double r = fma(p.x, q.x, p.y * q.y);
+                w[v] = r;
+                w[v ^ X] = r;
+            }
+        }
+    }
+}
+
+template <int RR>
+__device__ __forceinline__ void wht(double (&w)[1 << RR]) {
+#pragma unroll
+    for (int b = 0; b < RR; b++)
+#pragma unroll
+        for (int v = 0; v < (1 << RR); v++) {
+            if (v & (1 << b)) continue;
+            const double x = w[v], y = w[v | (1 << b)];
+            w[v] = x + y;
+            w[v | (1 << b)] = x - y;
+        }
+}
+
+template <int RR>
+__device__ __forceinline__ double pick(const double (&w)[1 << RR], uint32_t p) {
+    double r = 0.0;
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++)
+        if (p == (uint32_t)v) r = w[v];
+    return r;
+}
+
+template <int RR, bool IM>
+__device__ __forceinline__ double expv_part(const double2 (&a)[1 << RR], uint32_t xreg, const ETerm *et, uint32_t nt,
+                                            uint64_t gbase) {
+    double w[1 << RR];
+    switch (xreg) {
+#define EW(X) case X: if constexpr (X < (1 << RR)) expv_w<RR, (X < (1 << RR) ? X : 0), IM>(a, w); break;
+    EW(0) EW(1) EW(2) EW(3) EW(4) EW(5) EW(6) EW(7) EW(8) EW(9) EW(10) EW(11) EW(12) EW(13) EW(14) EW(15)
+#undef EW
+    default: break;
+    }
+    wht<RR>(w);
+    double e = 0.0;
+    uint32_t k = 0;
+    while (k < nt) {
+        const uint32_t z = et[k].zreg;
+        double cz = 0.0;
+        for (; k < nt && et[k].zreg == z; k++) {
+            const ETerm t = et[k];
+            if ((bool)(t.y & 1) != IM) continue;
+            double c = (__popcll(gbase & t.znr) & 1) ? -t.c : t.c;
+            if (t.y & 2) c = -c;
+            cz += IM ? -c : c;   // Re[i w] = -Im w, Re[-i w] = Im w
+        }
+        if (cz != 0.0) e = fma(cz, pick<RR>(w, z), e);
+    }
+    return e;
+}
+
+template <int RR>
+__device__ __forceinline__ double expv_group(const double2 (&a)[1 << RR], uint32_t xreg, const ETerm *et, uint32_t nt,
+                                             uint64_t gbase) {
+    double e = expv_part<RR, false>(a, xreg, et, nt, gbase);
+    bool need_im = false;
+    for (uint32_t k = 0; k < nt; k++) need_im |= (et[k].y & 1);
+    if (need_im) e += expv_part<RR, true>(a, xreg, et, nt, gbase);
+    return e;
+}
+
 // Apply the ops [ob, oe) of a sub-block to the register tile.
 // fb is a pending flip mask over register positions: register v holds the
 // amplitude of logical register index v ^ fb.  X, and CNOT/CCX whose
@@ -373,7 +494,8 @@ __device__ __forceinline__ void apply_generic(double2 (&a)[1 << RR], const KOp &
 // address.  Other ops read logical bit values through fb.
 template <int RR>
 __device__ __forceinline__ void apply_ops(double2 (&a)[1 << RR], const KOp *ops, uint32_t ob, uint32_t oe,
-                                          uint64_t gbase, int n, const double2 *tab, uint32_t &fb) {
+                                          uint64_t gbase, int n, const double2 *tab, uint32_t &fb,
+                                          const ETerm *et, double &eacc) {
     double2 ttmax = make_double2(1.0, 0.0);
     uint64_t lg = 0;
     for (uint32_t oi = ob; oi < oe; oi++) {
@@ -441,6 +563,10 @@ __device__ __forceinline__ void apply_ops(double2 (&a)[1 << RR], const KOp *ops,
             for (int v = 0; v < (1 << RR); v++) a[v] = cscale(a[v], sc);
             break;
         }
+        case C_EXPV:
+            flush_flips<RR>(a, fb);
+            eacc += expv_group<RR>(a, op.rcm, et + op.mat, op.aux, gbase);
+            break;
         default:
             flush_flips<RR>(a, fb);
             apply_generic<RR>(a, op, M, gbase);
@@ -473,10 +599,12 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 template <int RR>
 __global__ void __launch_bounds__(RR >= 4 ? 256 : 512, 1) k_tile(const __grid_constant__ KPass P, const KSub *__restrict__ subs,
                                                  const KOp *__restrict__ ops, const KPerm *__restrict__ perms,
-                                                 const KPermTerm *__restrict__ pterms, const double2 *__restrict__ mats,
+                                                 const KPermTerm *__restrict__ pterms, const ETerm *__restrict__ eterms,
+                                                 const double2 *__restrict__ mats,
                                                  uint64_t mat_stride, const double2 *__restrict__ cst,
                                                  double2 *__restrict__ state, uint64_t state_stride,
-                                                 uint32_t tiles_log2, uint32_t total_tiles) {
+                                                 uint32_t tiles_log2, uint32_t total_tiles,
+                                                 double *__restrict__ partials, uint64_t slot_stride) {
     extern __shared__ double2 sm[];
     constexpr int NV = 1 << RR;
     const int K = P.K;
@@ -494,6 +622,10 @@ __global__ void __launch_bounds__(RR >= 4 ? 256 : 512, 1) k_tile(const __grid_co
     uint64_t *s_dlo = reinterpret_cast<uint64_t *>(s_pt + npt);
     uint64_t *s_dhi = s_dlo + 256;
     KSub *s_sub = reinterpret_cast<KSub *>(s_dhi + 32);
+    const uint32_t nsub = P.sub_end - P.sub_begin;
+    const uint32_t net = P.eterm_end - P.eterm_begin;
+    ETerm *s_et = reinterpret_cast<ETerm *>(s_sub + nsub + (nsub & 1));   // 8-byte aligned
+    for (uint32_t k = threadIdx.x; k < net; k += blockDim.x) s_et[k] = eterms[P.eterm_begin + k];
     const bool zero = P.flags & PF_LOAD_ZERO;
     for (uint32_t k = threadIdx.x; k < 256 + 32; k += blockDim.x) {
         uint64_t g = 0;
@@ -594,6 +726,7 @@ __global__ void __launch_bounds__(RR >= 4 ? 256 : 512, 1) k_tile(const __grid_co
             load_regs(sb.perm, sb.S);
         }
         uint32_t fb = 0;   // pending register flip mask (apply_ops)
+        double eacc = 0.0; // Pauli-group contributions of this thread
         for (uint32_t s = P.sub_begin; s < P.sub_end; s++) {
             if (s != P.sub_begin) {
                 sb = s_sub[s - P.sub_begin];
@@ -609,9 +742,19 @@ __global__ void __launch_bounds__(RR >= 4 ? 256 : 512, 1) k_tile(const __grid_co
                     load_regs(sb.perm, sb.S);
                 }
             }
-            apply_ops<RR>(a, s_ops, sb.op_begin - P.op_begin, sb.op_end - P.op_begin, cur.gt, P.n, s_tab, fb);
+            apply_ops<RR>(a, s_ops, sb.op_begin - P.op_begin, sb.op_end - P.op_begin, cur.gt, P.n, s_tab, fb, s_et,
+                          eacc);
         }
         double2 *psi = state + (uint64_t)circ * state_stride;
+        if (P.flags & PF_EXPV) {   // one deterministic partial per tile
+            __syncthreads();       // all reads of b done: reuse it as reduction scratch
+            const double r = block_sum(eacc, reinterpret_cast<double *>(b));
+            if (t == 0) partials[(uint64_t)circ * slot_stride + P.eslot + (g & ((1u << tiles_log2) - 1))] = r;
+        }
+        if (P.flags & PF_NO_STORE) {
+            __syncthreads();
+            continue;
+        }
         const uint32_t ms = smask<RR>(P.Sstore);
         // a non-zero flip mask would scatter the lanes of each store: go
         // through shared memory (collective decision: the exchange syncs)
@@ -821,37 +964,6 @@ __device__ __forceinline__ double2 gauss_amp(uint64_t seed, uint64_t i) {
     return make_double2(r * c, r * s);
 }
 
-// Deterministic block reduction (fixed shuffle tree + fixed smem tree).
-// red: >= max(32, blockDim.x) doubles of shared memory.  blockDim.x must be
-// a power of two.  Result valid in thread 0.
-__device__ __forceinline__ double block_sum(double v, double *red) {
-    const int nt = blockDim.x, t = threadIdx.x;
-    if (nt >= 32) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-        const int w = t >> 5, l = t & 31;
-        if (l == 0) red[w] = v;
-        __syncthreads();
-        double r = 0.0;
-        if (w == 0) {
-            r = (l < (nt >> 5)) ? red[l] : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
-        }
-        __syncthreads();
-        return r;
-    }
-    red[t] = v;
-    __syncthreads();
-    for (int s = nt >> 1; s > 0; s >>= 1) {
-        if (t < s) red[t] += red[t + s];
-        __syncthreads();
-    }
-    double r = red[0];
-    __syncthreads();
-    return r;
-}
-
 constexpr int RED_BLOCKS = 1184;   // 8 x 148 SMs; fixed => deterministic reduction order
 
 __global__ void __launch_bounds__(256) k_random_norm(uint64_t N, uint64_t seed, double *partial) {
@@ -931,7 +1043,6 @@ __global__ void k_scatter(int n, QMap m, double2 *__restrict__ psi, uint64_t off
 // E = sum_t c_t Re <psi|P_t|psi>,  P|j> = i^{y} (-1)^{popcount(j & z)} |j ^ x>
 // (PAPER.md:733-734).  One CTA per tile: the tile holds every pair (j, j^x)
 // of the pass's x masks; per-CTA partial sums are reduced in fixed order.
-constexpr int PAULI_MAX_TERMS = (int)PAULI_MAX_TERMS_PLAN;
 
 __device__ __forceinline__ double re_iy(double2 w, uint32_t y) {
     switch (y & 3) {
@@ -940,68 +1051,6 @@ __device__ __forceinline__ double re_iy(double2 w, uint32_t y) {
     case 2: return -w.x;
     default: return w.y;
     }
-}
-
-template <int RR>
-__global__ void __launch_bounds__(512) k_pauli_tile(const __grid_constant__ KPauliPass P, const PTerm *__restrict__ terms,
-                                                    const double2 *__restrict__ state, uint64_t state_stride,
-                                                    double *__restrict__ partial, uint64_t slot_stride) {
-    extern __shared__ double2 sm[];
-    constexpr int NV = 1 << RR;
-    const int K = P.K;
-    const int NT = 1 << (K - RR);
-    const uint32_t nterm = P.term_end - P.term_begin;
-    double *cs = reinterpret_cast<double *>(sm + (1u << K));
-    uint32_t *xl = reinterpret_cast<uint32_t *>(cs + PAULI_MAX_TERMS);
-    uint32_t *zl = xl + PAULI_MAX_TERMS;
-    uint32_t *yl = zl + PAULI_MAX_TERMS;
-    const double2 *__restrict__ psi = state + (uint64_t)blockIdx.y * state_stride;
-    const uint32_t t = threadIdx.x;
-
-    uint64_t tb = blockIdx.x;
-    for (int i = 0; i < K; i++) tb = insert_zero64(tb, P.T[i]);
-    for (uint32_t k = t; k < nterm; k += blockDim.x) {
-        const PTerm pt = terms[P.term_begin + k];
-        cs[k] = (__popcll(tb & pt.zfull) & 1) ? -pt.coeff : pt.coeff;
-        xl[k] = pt.xloc;
-        zl[k] = pt.zloc;
-        yl[k] = pt.yph;
-    }
-    // load: thread t holds local indices t + v * NT (top RR bits in registers)
-    uint64_t gt = tb;
-    for (int i = 0; i < K - RR; i++)
-        if ((t >> i) & 1) gt |= 1ull << P.T[i];
-    double2 a[NV];
-#pragma unroll
-    for (int v = 0; v < NV; v++) {
-        uint64_t g = gt;
-#pragma unroll
-        for (int i = 0; i < RR; i++)
-            if (v & (1 << i)) g |= 1ull << P.T[K - RR + i];
-        a[v] = psi[g];
-        sm[t + v * NT] = a[v];
-    }
-    __syncthreads();
-    double acc = 0.0;
-#pragma unroll
-    for (int v = 0; v < NV; v++) {
-        const uint32_t l = t + v * NT;
-        uint32_t px = 0xFFFFFFFFu;
-        double2 w = make_double2(0, 0);
-        for (uint32_t k = 0; k < nterm; k++) {
-            const uint32_t x = xl[k];
-            if (x != px) {
-                const double2 p = (x == 0) ? a[v] : sm[l ^ x];
-                w = make_double2(fma(p.x, a[v].x, p.y * a[v].y), fma(p.x, a[v].y, -p.y * a[v].x));
-                px = x;
-            }
-            const double c = (__popc(l & zl[k]) & 1) ? -cs[k] : cs[k];
-            acc = fma(c, re_iy(w, yl[k]), acc);
-        }
-    }
-    __syncthreads();   // tile reads done: reuse the tile's shared memory
-    double r = block_sum(acc, reinterpret_cast<double *>(sm));
-    if (t == 0) partial[(uint64_t)blockIdx.y * slot_stride + P.slot + blockIdx.x] = r;
 }
 
 // Direct (non-tiled) pass for x masks wider than a tile.

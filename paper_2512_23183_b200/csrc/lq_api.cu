@@ -249,15 +249,16 @@ lq_status validate_terms(int n, const lq_pauli_term *t, size_t nt) {
 // ---------------------------------------------------------------- launches
 template <int RR>
 lq_status launch_tile_rr(const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
-                         const KPermTerm *pterms, uint32_t n_pterms, const double2 *mats,
+                         const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                          uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride,
-                         int n_circ, cudaStream_t st) {
+                         int n_circ, double *partials, uint64_t slot_stride, cudaStream_t st) {
     static bool attr = false;
     static int n_sm = 0;
     const size_t smem = ((size_t)32 << kp.K) + (size_t)kp.smat * sizeof(double2) +
                         (size_t)(kp.op_end - kp.op_begin) * sizeof(KOp) +
                         (size_t)(kp.perm_end - kp.perm_begin) * sizeof(KPerm) + (size_t)n_pterms * sizeof(KPermTerm) +
-                        (256 + 32) * sizeof(uint64_t) + (size_t)(kp.sub_end - kp.sub_begin) * sizeof(KSub);
+                        (256 + 32) * sizeof(uint64_t) + (size_t)(kp.sub_end - kp.sub_begin + 1) * sizeof(KSub) +
+                        (size_t)(kp.eterm_end - kp.eterm_begin) * sizeof(ETerm);
     if (!attr) {
         CUDA_TRY(cudaFuncSetAttribute(k_tile<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         int dev = 0;
@@ -271,20 +272,26 @@ lq_status launch_tile_rr(const KPass &kp, const KSub *subs, const KOp *kops, con
     if (total >= (1ull << 32)) return fail(LQ_ERR_DIM, "too many tiles in one launch");
     const unsigned grid = (unsigned)std::min<uint64_t>(total, (uint64_t)n_sm);
     LaunchTimer lt_(KC_TILE, st);
-    k_tile<RR><<<grid, 1u << (kp.K - RR), smem, st>>>(kp, subs, kops, perms, pterms, mats, mat_stride, cst, state,
-                                                      state_stride, tiles_log2, (uint32_t)total);
+    if ((kp.flags & PF_EXPV) && !partials) return fail(LQ_ERR_STATE, "expectation pass without partial buffer");
+    k_tile<RR><<<grid, 1u << (kp.K - RR), smem, st>>>(kp, subs, kops, perms, pterms, eterms, mats, mat_stride, cst,
+                                                      state, state_stride, tiles_log2, (uint32_t)total, partials,
+                                                      slot_stride);
     return check_launch("k_tile");
 }
 
-lq_status launch_tile(int Rr, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms, const KPermTerm *pterms,
-                      uint32_t n_pterms, const double2 *mats, uint64_t mat_stride, const double2 *cst, double2 *state,
-                      uint64_t state_stride, int n_circ, cudaStream_t st) {
+lq_status launch_tile(int Rr, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
+                      const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
+                      uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride, int n_circ,
+                      double *partials, uint64_t slot_stride, cudaStream_t st) {
+#define LT(RRV) launch_tile_rr<RRV>(kp, subs, kops, perms, pterms, n_pterms, eterms, mats, mat_stride, cst, state, \
+                                    state_stride, n_circ, partials, slot_stride, st)
     switch (Rr) {
-    case 1: return launch_tile_rr<1>(kp, subs, kops, perms, pterms, n_pterms, mats, mat_stride, cst, state, state_stride, n_circ, st);
-    case 2: return launch_tile_rr<2>(kp, subs, kops, perms, pterms, n_pterms, mats, mat_stride, cst, state, state_stride, n_circ, st);
-    case 3: return launch_tile_rr<3>(kp, subs, kops, perms, pterms, n_pterms, mats, mat_stride, cst, state, state_stride, n_circ, st);
-    default: return launch_tile_rr<4>(kp, subs, kops, perms, pterms, n_pterms, mats, mat_stride, cst, state, state_stride, n_circ, st);
+    case 1: return LT(1);
+    case 2: return LT(2);
+    case 3: return LT(3);
+    default: return LT(4);
     }
+#undef LT
 }
 
 unsigned grid_for(uint64_t work, unsigned per_block = 256) {
@@ -297,13 +304,15 @@ struct DevPlan {
     const KOp *kops = nullptr;
     const KPerm *perms = nullptr;
     const KPermTerm *pterms = nullptr;
+    const ETerm *eterms = nullptr;
     const MSpec *specs = nullptr;
     const MFactor *factors = nullptr;
     const double2 *cst = nullptr;
 };
 
 lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uint64_t state_stride, int n_circ,
-                        const double2 *mats, uint64_t mat_stride, cudaStream_t st, bool zero_first) {
+                        const double2 *mats, uint64_t mat_stride, cudaStream_t st, bool zero_first,
+                        double *partials = nullptr, uint64_t slot_stride = 0, bool no_final_store = false) {
     const int n = plan.n;
     if (zero_first && (plan.passes.empty() || plan.passes[0].kind != PASS_TILE)) {
         dim3 grid(grid_for(1ull << n), n_circ);
@@ -315,11 +324,12 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
         if (p.kind == PASS_TILE) {
             KPass kp = p.kp;
             if (zero_first && i == 0) kp.flags |= PF_LOAD_ZERO;
+            if (no_final_store && i + 1 == plan.passes.size()) kp.flags |= PF_NO_STORE;
             uint32_t npt = 0;
             if (kp.perm_end > kp.perm_begin)
                 npt = plan.perms[kp.perm_end - 1].term_end - plan.perms[kp.perm_begin].term_begin;
-            LQ_TRY(launch_tile(plan.Rr, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, mats, mat_stride, dp.cst, state,
-                               state_stride, n_circ, st));
+            LQ_TRY(launch_tile(plan.Rr, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, dp.eterms, mats, mat_stride,
+                               dp.cst, state, state_stride, n_circ, partials, slot_stride, st));
         } else if (p.kind == PASS_PAIR) {
             const KOp op = plan.kops[p.op_begin];
             uint64_t work = (op.type == K_U1 || op.type == K_X) ? (1ull << (n - 1)) : (1ull << (n - 2));
@@ -340,48 +350,51 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
     return LQ_OK;
 }
 
-size_t pauli_smem(int K) {
-    return ((size_t)16 << K) + PAULI_MAX_TERMS * (8 + 3 * 4);
-}
-
-template <int RR>
-lq_status launch_pauli_rr(const KPauliPass &P, const PTerm *terms, const double2 *state, uint64_t state_stride,
-                          int n_circ, double *partial, uint64_t slot_stride, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        CUDA_TRY(cudaFuncSetAttribute(k_pauli_tile<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)pauli_smem(13)));
-        attr = true;
-    }
-    dim3 grid((unsigned)(1ull << (P.n - P.K)), (unsigned)n_circ);
-    LaunchTimer lt_(KC_PAULI, st);
-    k_pauli_tile<RR><<<grid, 1u << (P.K - RR), pauli_smem(P.K), st>>>(P, terms, state, state_stride, partial,
-                                                                        slot_stride);
-    return check_launch("k_pauli_tile");
-}
-
-lq_status launch_pauli(const PauliPlan &pp, const PTerm *dterms, const double2 *state, uint64_t state_stride,
-                       int n_circ, double *partial, uint64_t slot_stride, double *E, cudaStream_t st) {
-    for (const KPauliPass &P : pp.passes) {
-        switch (std::min(R, P.K)) {
-        case 1: LQ_TRY(launch_pauli_rr<1>(P, dterms, state, state_stride, n_circ, partial, slot_stride, st)); break;
-        case 2: LQ_TRY(launch_pauli_rr<2>(P, dterms, state, state_stride, n_circ, partial, slot_stride, st)); break;
-        case 3: LQ_TRY(launch_pauli_rr<3>(P, dterms, state, state_stride, n_circ, partial, slot_stride, st)); break;
-        default: LQ_TRY(launch_pauli_rr<4>(P, dterms, state, state_stride, n_circ, partial, slot_stride, st)); break;
+// Pauli groups whose x mask is wider than a tile: the direct pair kernel.
+struct DirectSet {
+    std::vector<PTerm> terms;
+    struct D { uint64_t x; uint32_t tb, te, slot, nblocks; };
+    std::vector<D> ds;
+    uint32_t slots = 0;          // total partial slots (tile passes + direct)
+    void build(const Plan &plan) {
+        slots = plan.n_slots;
+        for (uint32_t g : plan.wide_groups) {
+            D d;
+            d.x = plan.groups[g].x;
+            d.tb = (uint32_t)terms.size();
+            for (auto &t : plan.groups[g].terms) {
+                PTerm p{};
+                p.coeff = t.c;
+                p.zfull = t.z;
+                p.yph = t.y;
+                terms.push_back(p);
+            }
+            d.te = (uint32_t)terms.size();
+            uint64_t blocks = ((1ull << plan.n) + 255) / 256;
+            d.nblocks = (uint32_t)std::min<uint64_t>(blocks, 148ull * 8);
+            d.slot = slots;
+            slots += d.nblocks;
+            ds.push_back(d);
         }
     }
-    for (const auto &D : pp.direct) {
-        dim3 grid(D.n_blocks, n_circ);
+};
+
+// Direct groups, then E[c] = fixed-order sum of the circuit's partials.
+lq_status finish_expv(const Plan &plan, const DirectSet &dset, const PTerm *dterms, const double2 *state,
+                      uint64_t state_stride, int n_circ, double *partial, uint64_t slot_stride, double *E,
+                      cudaStream_t st) {
+    for (const auto &D : dset.ds) {
+        dim3 grid(D.nblocks, n_circ);
         LaunchTimer lt_(KC_PAULI, st);
-        k_pauli_direct<<<grid, 256, 0, st>>>(pp.n, D.x, dterms + D.term_begin, D.term_end - D.term_begin, state,
-                                             state_stride, partial, slot_stride, D.slot);
+        k_pauli_direct<<<grid, 256, 0, st>>>(plan.n, D.x, dterms + D.tb, D.te - D.tb, state, state_stride, partial,
+                                             slot_stride, D.slot);
         LQ_TRY(check_launch("k_pauli_direct"));
     }
-    if (pp.n_slots == 0) {
+    if (dset.slots == 0) {
         CUDA_TRY(cudaMemsetAsync(E, 0, sizeof(double) * n_circ, st));
         return LQ_OK;
     }
-    k_sum_partials<<<n_circ, 256, 0, st>>>(partial, slot_stride, pp.n_slots, E);
+    k_sum_partials<<<n_circ, 256, 0, st>>>(partial, slot_stride, dset.slots, E);
     return check_launch("k_sum_partials");
 }
 
@@ -750,17 +763,56 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
     LQ_TRY(check_sv(sv));
     if (!out_energy) return fail(LQ_ERR_ARG, "out_energy is NULL");
     LQ_TRY(validate_terms(sv->n, terms, n_terms));
-    PauliPlan pp;
-    plan_pauli(sv->n, sv->qmap, terms, n_terms, options(), pp);
+    Plan plan;
+    MatBuilder mb;
+    std::vector<POp> ops;
+    lower_pauli(sv->n, sv->qmap, terms, n_terms, ops, plan);
+    plan_circuit(sv->n, ops, options(), mb, plan);
+    DirectSet dset;
+    dset.build(plan);
     Blob blob;
-    size_t o_t = blob.add(pp.terms);
+    size_t o_sub = blob.add(plan.subs), o_kop = blob.add(plan.kops), o_perm = blob.add(plan.perms),
+           o_pt = blob.add(plan.perm_terms), o_et = blob.add(plan.eterms), o_dt = blob.add(dset.terms);
     LQ_TRY(blob.upload(sv->plan_buf, sv->stream));
-    LQ_TRY(sv->work_buf.reserve(sizeof(double) * (pp.n_slots + 2), sv->stream));
+    DevPlan dp;
+    dp.subs = sv->plan_buf.at<KSub>(o_sub);
+    dp.kops = sv->plan_buf.at<KOp>(o_kop);
+    dp.perms = sv->plan_buf.at<KPerm>(o_perm);
+    dp.pterms = sv->plan_buf.at<KPermTerm>(o_pt);
+    dp.eterms = sv->plan_buf.at<ETerm>(o_et);
+    LQ_TRY(sv->work_buf.reserve(sizeof(double) * (dset.slots + 2), sv->stream));
     double *part = sv->work_buf.at<double>(0);
-    double *E = part + pp.n_slots + 1;
-    LQ_TRY(launch_pauli(pp, sv->plan_buf.at<PTerm>(o_t), sv->d, 0, 1, part, pp.n_slots, E, sv->stream));
+    double *E = part + dset.slots + 1;
+    LQ_TRY(launch_passes(plan, dp, sv->d, 0, 1, nullptr, 0, sv->stream, false, part, dset.slots, false));
+    LQ_TRY(finish_expv(plan, dset, sv->plan_buf.at<PTerm>(o_dt), sv->d, 0, 1, part, dset.slots, E, sv->stream));
     CUDA_TRY(cudaMemcpyAsync(out_energy, E, sizeof(double), cudaMemcpyDeviceToHost, sv->stream));
     return sync(sv->stream);
+}
+
+// Plan export (JSON) for host-side inspection and the test-suite's plan
+// emulator: the gates (and an optional Pauli sum, planned as the PSR driver
+// does) with the current options.
+lq_status lq_plan_export_json(int n_qubits, const lq_gate *gates, size_t n_gates, const lq_pauli_term *terms,
+                              size_t n_terms, char *buf, size_t buf_len, size_t *needed) {
+    if (n_qubits < 1 || n_qubits > 40) return fail(LQ_ERR_ARG, "n_qubits must be in [1, 40]");
+    LQ_TRY(validate_gates(n_qubits, gates, n_gates, nullptr, 1 << 16, false, nullptr));
+    LQ_TRY(validate_terms(n_qubits, terms, n_terms));
+    int32_t qm[64];
+    for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
+    std::vector<POp> ops;
+    MatBuilder mb;
+    Plan plan;
+    lower_gates(n_qubits, gates, n_gates, qm, ops, mb);
+    if (n_terms) lower_pauli(n_qubits, qm, terms, n_terms, ops, plan);
+    plan_circuit(n_qubits, ops, options(), mb, plan);
+    std::string j = export_json(plan, mb, qm);
+    if (needed) *needed = j.size() + 1;
+    if (buf && buf_len) {
+        size_t k = std::min(buf_len - 1, j.size());
+        memcpy(buf, j.data(), k);
+        buf[k] = 0;
+    }
+    return LQ_OK;
 }
 
 }  // extern "C"
@@ -773,7 +825,7 @@ struct lq_psr {
     cudaStream_t stream = nullptr;
     Plan plan;
     MatBuilder mb;
-    PauliPlan pp;
+    DirectSet dset;
     std::vector<Shift> shifts;
     std::vector<PsrPair> pairs;
     int base_idx = -1;
@@ -810,8 +862,11 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
     std::vector<POp> ops;
     lower_gates(n_qubits, ansatz, n_gates, qm, ops, P->mb);
+    // the Pauli groups ride on the circuit's own tile passes (read after the
+    // last gate that touches their qubits)
+    lower_pauli(n_qubits, qm, terms, n_terms, ops, P->plan);
     plan_circuit(n_qubits, ops, options(), P->mb, P->plan);
-    plan_pauli(n_qubits, qm, terms, n_terms, options(), P->pp);
+    P->dset.build(P->plan);
     // circuits of this shard: (p, +pi/2), (p, -pi/2) for owned p; base on shard 0.
     // Parameters used by no gate have E+ == E- identically: g_p = 0 (written by combine).
     for (size_t p = 0; p < n_params; p++) {
@@ -842,12 +897,12 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     size_t o_sub = blob.add(P->plan.subs), o_kop = blob.add(P->plan.kops), o_spec = blob.add(P->mb.specs),
            o_fac = blob.add(P->mb.factors), o_cst = blob.add(P->mb.cst), o_perm = blob.add(P->plan.perms),
            o_pt = blob.add(P->plan.perm_terms), o_sh = blob.add(P->shifts),
-           o_pr = blob.add(P->pairs), o_t = blob.add(P->pp.terms);
+           o_pr = blob.add(P->pairs), o_t = blob.add(P->dset.terms), o_et = blob.add(P->plan.eterms);
     P->blob_bytes = blob.h.size();
     lq_status s = blob.upload(P->blob_buf, st);
     if (s == LQ_OK) s = P->states.reserve((size_t)B * N * sizeof(double2), st);
     if (s == LQ_OK) s = P->mats.reserve((size_t)B * std::max<uint32_t>(P->mb.mat_size, 1) * sizeof(double2), st);
-    if (s == LQ_OK) s = P->partials.reserve((size_t)B * std::max<uint32_t>(P->pp.n_slots, 1) * sizeof(double), st);
+    if (s == LQ_OK) s = P->partials.reserve((size_t)B * std::max<uint32_t>(P->dset.slots, 1) * sizeof(double), st);
     if (s == LQ_OK) s = P->E.reserve(sizeof(double) * std::max(n_circ, 1), st);
     if (s != LQ_OK) {
         std::string keep = g_err;
@@ -862,6 +917,7 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     P->dp.cst = P->blob_buf.at<double2>(o_cst);
     P->dp.perms = P->blob_buf.at<KPerm>(o_perm);
     P->dp.pterms = P->blob_buf.at<KPermTerm>(o_pt);
+    P->dp.eterms = P->blob_buf.at<ETerm>(o_et);
     P->d_shifts = P->blob_buf.at<Shift>(o_sh);
     P->d_pairs = P->blob_buf.at<PsrPair>(o_pr);
     P->d_terms = P->blob_buf.at<PTerm>(o_t);
@@ -889,8 +945,11 @@ lq_status lq_psr_run(lq_psr *P, const double *theta_dev, double *grad_dev, doubl
                 ms, nb);
             LQ_TRY(check_launch("k_build_mats"));
         }
-        LQ_TRY(launch_passes(P->plan, P->dp, states, N, nb, mats, ms, st, true));
-        LQ_TRY(launch_pauli(P->pp, P->d_terms, states, N, nb, part, std::max<uint32_t>(P->pp.n_slots, 1), E + c0, st));
+        const uint32_t ss = std::max<uint32_t>(P->dset.slots, 1);
+        // the state after the last pass is only read by the Pauli groups of
+        // that pass: no store (unless a wide group still has to read it)
+        LQ_TRY(launch_passes(P->plan, P->dp, states, N, nb, mats, ms, st, true, part, ss, P->dset.ds.empty()));
+        LQ_TRY(finish_expv(P->plan, P->dset, P->d_terms, states, N, nb, part, ss, E + c0, st));
     }
     k_psr_combine<<<1, 256, 0, st>>>(E, P->d_pairs, (int)P->pairs.size(), P->base_idx, grad_dev, (int)P->n_params,
                                      energy_dev);

@@ -46,7 +46,8 @@ enum KOpType : uint8_t {
     K_D2 = 4,   // diagonal on two bits (r0|b0 high, r1|b1 low): mat d[4]
     K_SWAP = 5, // exchange register bits r0, r1
     K_QFT = 6,  // QFT stage on register bit r0 (logical bit qj); aux = twiddle table
-    K_SCALE = 7 // multiply every amplitude by `scale`
+    K_SCALE = 7, // multiply every amplitude by `scale`
+    K_EXPV = 8   // Pauli-group expectation contribution (read-only; see ETerm)
 };
 
 enum KOpFlags : uint8_t {
@@ -83,7 +84,18 @@ enum CodeTile : uint8_t {
     C_D1T = 28,      // diagonal on a thread-constant bit, no register control
     C_QFT = 29,      // + r0
     C_SCALE = 33,
-    C_GENERIC = 34
+    C_GENERIC = 34,
+    C_EXPV = 35      // Pauli group: rcm = x mask in register positions, mat/aux = ETerm range
+};
+
+// One Pauli term of a group lowered to a sub-block:
+// contribution c * Re[ i^y sum_v chi_zreg(v) conj(a[v ^ x]) a[v] ]
+// times the thread-constant sign (-1)^{popcount(gbase & znr)}.
+struct ETerm {
+    double c;
+    uint64_t znr;        // z bits that are not register bits (physical)
+    uint32_t zreg;       // z bits in register positions
+    uint32_t y;          // number of Y factors mod 4
 };
 
 struct KSub {
@@ -112,7 +124,9 @@ struct KPermTerm {
 };
 
 enum PassFlags : uint32_t {
-    PF_LOAD_ZERO = 1     // synthesise |0...0> instead of loading (fused init_basis(0))
+    PF_LOAD_ZERO = 1,    // synthesise |0...0> instead of loading (fused init_basis(0))
+    PF_EXPV = 2,         // the pass evaluates Pauli groups: write one partial sum per tile
+    PF_NO_STORE = 4      // the state after the pass is not needed (read-only pass / final PSR pass)
 };
 
 // Tile pass descriptor, passed by value to the kernel.
@@ -139,6 +153,8 @@ struct KPass {
     uint32_t smat;       // staged table size (double2)
     uint32_t perm_begin, perm_end;   // KPerm range of the pass (global indices)
     int32_t store_perm;  // permutation applied before the store (pass-local), -1: none
+    uint32_t eterm_begin, eterm_end;   // ETerm range of the pass (global indices)
+    uint32_t eslot;      // first partial-sum slot of the pass (one per tile)
     uint32_t flags;
     uint8_t T[MAXK];     // physical bit of each local bit, ascending
     uint8_t Sload[R];    // (unused by the persistent kernel; kept for layout)
@@ -173,26 +189,13 @@ struct Shift {
     double delta;
 };
 
-// Pauli expectation tile pass.
+// Pauli term of a wide group (direct kernel): coeff * i^yph (-1)^{popcount(j & zfull)}.
 struct PTerm {
     double coeff;
-    uint64_t zfull;      // physical z mask (all bits)
-    uint32_t zloc;       // z mask restricted to the tile, in local bit positions
-    uint32_t xloc;       // x mask in local bit positions (all x bits lie in the tile)
-    uint32_t yph;        // i^{yph}: number of Y factors mod 4
+    uint64_t zfull;      // physical z mask
+    uint32_t zloc, xloc; // (unused)
+    uint32_t yph;        // number of Y factors mod 4
     uint32_t pad;
-};
-
-constexpr uint32_t PAULI_MAX_TERMS_PLAN = 256;   // == PAULI_MAX_TERMS in kernels.cuh
-
-struct KPauliPass {
-    int32_t n;
-    int32_t K;
-    uint32_t term_begin, term_end;
-    uint32_t slot;       // first partial-sum slot of this pass (one per tile)
-    uint32_t pad;
-    uint8_t T[MAXK];
-    uint8_t pad2[2];
 };
 
 }  // namespace lq

@@ -16,12 +16,14 @@ uint64_t POp::full() const {
     switch (type) {
     case K_U1: case K_X: case K_QFT: return bit(t0);
     case K_U2: case K_SWAP: return bit(t0) | bit(t1);
+    case K_EXPV: return xm;
     default: return 0;
     }
 }
 
 uint64_t POp::touch() const {
     uint64_t m = ctrl | full();
+    if (type == K_EXPV) m |= zm;
     if (type == K_D1) m |= bit(t0);
     if (type == K_D2) m |= bit(t0) | bit(t1);
     return m;
@@ -143,6 +145,35 @@ void canonicalize_ops(int n, int32_t *qmap, std::vector<POp> &ops) {
         op.t1 = std::min(qmap[q], target);
         ops.push_back(op);
         std::swap(qmap[q], qmap[q2]);
+    }
+}
+
+// Pauli sum -> one K_EXPV op per x mask (E = sum_t c_t <P_t>).
+void lower_pauli(int n, const int32_t *qmap, const lq_pauli_term *terms, size_t n_terms,
+                 std::vector<POp> &ops, Plan &plan) {
+    size_t g0 = plan.groups.size();
+    for (size_t t = 0; t < n_terms; t++) {
+        uint64_t x = 0, z = 0;
+        for (int q = 0; q < n; q++) {
+            if (terms[t].x_mask & bit(q)) x |= bit(qmap[q]);
+            if (terms[t].z_mask & bit(q)) z |= bit(qmap[q]);
+        }
+        uint32_t y = (uint32_t)(popc(terms[t].x_mask & terms[t].z_mask) & 3);
+        size_t g = g0;
+        while (g < plan.groups.size() && plan.groups[g].x != x) g++;
+        if (g == plan.groups.size()) {
+            plan.groups.push_back(PGroup());
+            plan.groups.back().x = x;
+        }
+        plan.groups[g].terms.push_back({terms[t].coeff, z, y});
+    }
+    for (size_t g = g0; g < plan.groups.size(); g++) {
+        POp op;
+        op.type = K_EXPV;
+        op.xm = plan.groups[g].x;
+        for (auto &t : plan.groups[g].terms) op.zm |= t.z;
+        op.group = (int)g;
+        ops.push_back(op);
     }
 }
 
@@ -282,6 +313,8 @@ static uint8_t tile_code(const KOp &k) {
         break;
     case K_SCALE:
         return C_SCALE;
+    case K_EXPV:
+        return C_EXPV;
     default:
         break;
     }
@@ -296,6 +329,7 @@ static void finalize_pass_tables(PlanPass &pp, Plan &plan) {
     uint32_t off = 0;
     for (uint32_t i = pp.kp.op_begin; i < pp.kp.op_end; i++) {
         plan.kops[i].code = tile_code(plan.kops[i]);
+        if (plan.kops[i].type == K_EXPV) continue;   // mat/aux hold its ETerm range
         plan.kops[i].aux = off;
         off += (uint32_t)op_table_size(plan.kops[i].type);
     }
@@ -372,6 +406,41 @@ struct Affine {
     }
 };
 
+// Lower a K_EXPV op for register set S: x bits -> register mask (rcm),
+// terms sorted by their register z pattern.
+static void lower_expv(const POp &o, const LocalMap &L, const uint8_t *S, int Rr, PlanPass &pp, KOp &k,
+                       Plan &plan) {
+    auto reg = [&](int p) -> int {
+        if (L.loc[p] < 0) return -1;
+        for (int i = 0; i < Rr; i++) if (S[i] == L.loc[p]) return i;
+        return -1;
+    };
+    uint32_t xreg = 0;
+    uint64_t x = o.xm;
+    while (x) { int b = __builtin_ctzll(x); xreg |= 1u << reg(b); x &= x - 1; }
+    uint64_t sphys = 0;
+    for (int i = 0; i < Rr; i++) sphys |= bit(L.T[S[i]]);
+    std::vector<ETerm> ts;
+    for (auto &t : plan.groups[o.group].terms) {
+        ETerm e{};
+        e.c = t.c;
+        e.znr = t.z & ~sphys;
+        uint64_t zr = t.z & sphys;
+        while (zr) { int b = __builtin_ctzll(zr); e.zreg |= 1u << reg(b); zr &= zr - 1; }
+        e.y = t.y;
+        ts.push_back(e);
+    }
+    std::stable_sort(ts.begin(), ts.end(), [](const ETerm &a, const ETerm &b) { return a.zreg < b.zreg; });
+    k.type = K_EXPV;
+    k.rcm = (uint8_t)xreg;
+    k.cmask = 0;
+    k.mat = (uint32_t)(plan.eterms.size() - pp.kp.eterm_begin);
+    k.aux = (uint32_t)ts.size();
+    plan.eterms.insert(plan.eterms.end(), ts.begin(), ts.end());
+    pp.kp.eterm_end = (uint32_t)plan.eterms.size();
+    pp.kp.flags |= PF_EXPV;
+}
+
 static int32_t build_perm(const std::vector<POp> &ops, const std::vector<int> &group, const LocalMap &L,
                           const PlanPass &pp, Plan &plan) {
     if (group.empty()) return -1;
@@ -412,7 +481,9 @@ static void emit_tile(int n, int K, int Rr, uint64_t Tm, const std::vector<POp> 
     memcpy(pp.kp.T, L.T, MAXK);
     pp.kp.sub_begin = (uint32_t)plan.subs.size();
     pp.kp.perm_begin = (uint32_t)plan.perms.size();
+    pp.kp.eterm_begin = pp.kp.eterm_end = (uint32_t)plan.eterms.size();
     pp.n_ops = (int)absorbed.size();
+    bool all_expv = true;
 
     std::vector<int> rem = absorbed;
     auto collect_perm = [&](std::vector<int> &group) {
@@ -473,11 +544,23 @@ static void emit_tile(int n, int K, int Rr, uint64_t Tm, const std::vector<POp> 
         mask_to_S(sg.Sm, sb.S);
         sb.perm = build_perm(ops, sg.entry, L, pp, plan);
         sb.op_begin = (uint32_t)plan.kops.size();
-        for (int i : sg.taken) plan.kops.push_back(lower_tile_op(ops[i], L, sb.S, Rr, mat_off));
+        for (int i : sg.taken) {
+            KOp k = lower_tile_op(ops[i], L, sb.S, Rr, mat_off);
+            if (ops[i].type == K_EXPV) lower_expv(ops[i], L, sb.S, Rr, pp, k, plan);
+            else all_expv = false;
+            plan.kops.push_back(k);
+        }
         sb.op_end = (uint32_t)plan.kops.size();
         plan.subs.push_back(sb);
     }
+    if (pp.kp.eterm_end > pp.kp.eterm_begin || (pp.kp.flags & PF_EXPV)) {
+        pp.kp.flags |= PF_EXPV;
+        pp.kp.eslot = plan.n_slots;
+        plan.n_slots += (uint32_t)(1u << (n - K));
+    }
     pp.kp.store_perm = build_perm(ops, store_group, L, pp, plan);
+    // read-only pass: nothing but Pauli groups (no gate, no folded permutation)
+    if (all_expv && plan.perms.size() == pp.kp.perm_begin) pp.kp.flags |= PF_NO_STORE;
     pp.kp.sub_end = (uint32_t)plan.subs.size();
     pp.kp.perm_end = (uint32_t)plan.perms.size();
     finalize_pass_tables(pp, plan);
@@ -498,8 +581,26 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
     plan.Rr = Rr;
     plan.n = n;
     plan.K = K;
+    int c = std::max(0, std::min(opt.coalesce, K - 2));
+    uint64_t mand = (n > K) ? ((1ull << c) - 1) : ((n >= 64) ? ~0ull : ((1ull << n) - 1));
+    // Pauli groups whose x mask cannot share a tile with the coalescing run
+    // go to the direct kernel
+    std::vector<char> skip(ops.size(), 0);
+    for (size_t i = 0; i < ops.size(); i++)
+        if (ops[i].type == K_EXPV && (popc(mand | ops[i].xm) > K || popc(ops[i].xm) > Rr)) {
+            skip[i] = 1;
+            plan.wide_groups.push_back((uint32_t)ops[i].group);
+        }
     if (!opt.fusion) {
-        for (const POp &o : ops) {
+        for (size_t i = 0; i < ops.size(); i++) {
+            const POp &o = ops[i];
+            if (skip[i]) continue;
+            if (o.type == K_EXPV) {
+                uint64_t Tm = mand | o.xm;
+                for (int b = 0; b < n && popc(Tm) < K; b++) Tm |= bit(b);
+                emit_tile(n, K, Rr, Tm, ops, std::vector<int>{(int)i}, mat_off, plan);
+                continue;
+            }
             PlanPass pp;
             pp.kind = o.diag() ? PASS_DIAG : PASS_PAIR;
             pp.op_begin = (uint32_t)plan.kops.size();
@@ -512,10 +613,9 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
         return;
     }
     // the coalescing run must leave room for a 2-qubit gate's two target bits
-    int c = std::max(0, std::min(opt.coalesce, K - 2));
-    uint64_t mand = (n > K) ? ((1ull << c) - 1) : ((n >= 64) ? ~0ull : ((1ull << n) - 1));
-    std::vector<int> rem(ops.size());
-    for (size_t i = 0; i < ops.size(); i++) rem[i] = (int)i;
+    std::vector<int> rem;
+    for (size_t i = 0; i < ops.size(); i++)
+        if (!skip[i]) rem.push_back((int)i);
     while (!rem.empty()) {
         uint64_t Tm = mand;
         std::vector<int> absorbed, absorbed_w;
@@ -564,7 +664,11 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
         if (absorbed.empty()) absorbed.push_back(rem[0]);   // progress guarantee
         if (absorbed.size() > (size_t)MAX_PASS_OPS) absorbed.resize(MAX_PASS_OPS);   // a valid prefix
         int n_full = 0;
-        for (int i : absorbed) n_full += ops[i].diag() ? 0 : 1;
+        bool has_expv = false;
+        for (int i : absorbed) {
+            n_full += ops[i].diag() ? 0 : 1;
+            has_expv |= ops[i].type == K_EXPV;
+        }
         if (n_full == 0) {
             PlanPass pp;
             pp.kind = PASS_DIAG;
@@ -574,7 +678,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
             pp.n_ops = (int)absorbed.size();
             plan.passes.push_back(pp);
             plan.n_diag++;
-        } else if (absorbed.size() == 1 && (n > K || popc(ops[absorbed[0]].full()) > K)) {
+        } else if (absorbed.size() == 1 && !has_expv && (n > K || popc(ops[absorbed[0]].full()) > K)) {
             PlanPass pp;
             pp.kind = PASS_PAIR;
             pp.op_begin = (uint32_t)plan.kops.size();
@@ -658,6 +762,7 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
         pp.kp.sub_begin = (uint32_t)plan.subs.size();
         pp.kp.perm_begin = pp.kp.perm_end = (uint32_t)plan.perms.size();
         pp.kp.store_perm = -1;
+        pp.kp.eterm_begin = pp.kp.eterm_end = (uint32_t)plan.eterms.size();
         pp.n_ops = (int)st.size();
         std::vector<uint32_t> Sms;
         for (size_t a = 0; a < st.size(); a += Rr) {
@@ -730,91 +835,6 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
     return true;
 }
 
-// --------------------------------------------------------------------------
-// Pauli-sum expectation planning.
-// --------------------------------------------------------------------------
-void plan_pauli(int n, const int32_t *qmap, const lq_pauli_term *terms, size_t n_terms,
-                const PlanOptions &opt, PauliPlan &pp) {
-    int K = opt.K > 0 ? std::min(opt.K, n) : auto_tile_bits(n);
-    if (K > 13) K = 13;
-    if (n <= K) K = n;
-    pp.n = n;
-    pp.K = K;
-    struct T { double c; uint64_t x, z; uint32_t y; };
-    std::vector<uint64_t> gx;
-    std::vector<std::vector<T>> gt;
-    for (size_t t = 0; t < n_terms; t++) {
-        uint64_t x = 0, z = 0;
-        for (int q = 0; q < n; q++) {
-            if (terms[t].x_mask & bit(q)) x |= bit(qmap[q]);
-            if (terms[t].z_mask & bit(q)) z |= bit(qmap[q]);
-        }
-        uint32_t y = (uint32_t)(popc(terms[t].x_mask & terms[t].z_mask) & 3);
-        size_t g = 0;
-        while (g < gx.size() && gx[g] != x) g++;
-        if (g == gx.size()) { gx.push_back(x); gt.push_back({}); }
-        gt[g].push_back({terms[t].coeff, x, z, y});
-    }
-    int c = std::max(0, std::min(opt.coalesce, K - 2));
-    uint64_t mand = (n > K) ? ((1ull << c) - 1) : ((1ull << n) - 1);
-    std::vector<char> done(gx.size(), 0);
-    uint32_t tiles = (uint32_t)(1ull << (n - K));
-    for (size_t g = 0; g < gx.size(); g++)
-        if (popc(mand | gx[g]) > K) {
-            done[g] = 1;
-            PauliPlan::Direct d;
-            d.x = gx[g];
-            d.term_begin = (uint32_t)pp.terms.size();
-            for (auto &t : gt[g]) {
-                PTerm p{};
-                p.coeff = t.c; p.zfull = t.z; p.yph = t.y;
-                pp.terms.push_back(p);
-            }
-            d.term_end = (uint32_t)pp.terms.size();
-            uint64_t pairs = 1ull << (n - 1);
-            uint64_t blocks = (pairs + 1023) / 1024;
-            d.n_blocks = (uint32_t)std::min<uint64_t>(blocks, 148 * 16);
-            d.slot = pp.n_slots;
-            pp.n_slots += d.n_blocks;
-            pp.direct.push_back(d);
-        }
-    for (;;) {
-        uint64_t Tm = mand;
-        std::vector<size_t> sel;
-        for (size_t g = 0; g < gx.size(); g++) {
-            if (done[g]) continue;
-            if (popc(Tm | gx[g]) <= K) { Tm |= gx[g]; sel.push_back(g); done[g] = 1; }
-        }
-        if (sel.empty()) break;
-        for (int b = 0; b < n && popc(Tm) < K; b++) Tm |= bit(b);
-        LocalMap L(Tm);
-        uint32_t tb = (uint32_t)pp.terms.size();
-        for (size_t g : sel)
-            for (auto &t : gt[g]) {
-                PTerm p{};
-                p.coeff = t.c;
-                p.zfull = t.z;
-                p.zloc = L.local(t.z);
-                p.xloc = L.local(t.x);
-                p.yph = t.y;
-                pp.terms.push_back(p);
-            }
-        uint32_t te = (uint32_t)pp.terms.size();
-        // the kernel stages at most PAULI_MAX_TERMS terms in shared memory
-        for (uint32_t b = tb; b < te; b += PAULI_MAX_TERMS_PLAN) {
-            KPauliPass P{};
-            P.n = n;
-            P.K = K;
-            memcpy(P.T, L.T, MAXK);
-            P.term_begin = b;
-            P.term_end = std::min<uint32_t>(te, b + PAULI_MAX_TERMS_PLAN);
-            P.slot = pp.n_slots;
-            pp.n_slots += tiles;
-            pp.passes.push_back(P);
-        }
-    }
-}
-
 std::string describe(const Plan &plan) {
     std::ostringstream os;
     os << "n=" << plan.n << " K=" << plan.K << " passes=" << plan.passes.size()
@@ -831,6 +851,86 @@ std::string describe(const Plan &plan) {
         }
     }
     return os.str();
+}
+
+std::string export_json(const Plan &plan, const MatBuilder &mb, const int32_t *qmap) {
+    std::ostringstream o;
+    o.precision(17);
+    auto arr = [&](const char *name, size_t cnt, auto f) {
+        o << "\"" << name << "\":[";
+        for (size_t i = 0; i < cnt; i++) { if (i) o << ","; f(i); }
+        o << "]";
+    };
+    o << "{\"n\":" << plan.n << ",\"K\":" << plan.K << ",\"Rr\":" << plan.Rr << ",\"n_slots\":" << plan.n_slots
+      << ",\"mat_size\":" << mb.mat_size << ",";
+    arr("qmap", (size_t)plan.n, [&](size_t i) { o << qmap[i]; });
+    o << ",";
+    arr("passes", plan.passes.size(), [&](size_t i) {
+        const PlanPass &p = plan.passes[i];
+        const KPass &k = p.kp;
+        o << "{\"kind\":" << (int)p.kind << ",\"op_begin\":" << p.op_begin << ",\"op_end\":" << p.op_end
+          << ",\"K\":" << k.K << ",\"sub_begin\":" << k.sub_begin << ",\"sub_end\":" << k.sub_end
+          << ",\"kop_begin\":" << k.op_begin << ",\"kop_end\":" << k.op_end << ",\"perm_begin\":" << k.perm_begin
+          << ",\"store_perm\":" << k.store_perm << ",\"eterm_begin\":" << k.eterm_begin << ",\"eslot\":" << k.eslot
+          << ",\"flags\":" << k.flags << ",\"T\":[";
+        for (int b = 0; b < (p.kind == PASS_TILE ? k.K : 0); b++) o << (b ? "," : "") << (int)k.T[b];
+        o << "],\"Sstore\":[" << (int)k.Sstore[0] << "," << (int)k.Sstore[1] << "," << (int)k.Sstore[2] << ","
+          << (int)k.Sstore[3] << "]}";
+    });
+    o << ",";
+    arr("subs", plan.subs.size(), [&](size_t i) {
+        const KSub &sb = plan.subs[i];
+        o << "{\"S\":[" << (int)sb.S[0] << "," << (int)sb.S[1] << "," << (int)sb.S[2] << "," << (int)sb.S[3]
+          << "],\"op_begin\":" << sb.op_begin << ",\"op_end\":" << sb.op_end << ",\"perm\":" << sb.perm << "}";
+    });
+    o << ",";
+    arr("kops", plan.kops.size(), [&](size_t i) {
+        const KOp &k = plan.kops[i];
+        o << "{\"type\":" << (int)k.type << ",\"code\":" << (int)k.code << ",\"r0\":" << (int)k.r0 << ",\"r1\":"
+          << (int)k.r1 << ",\"rcm\":" << (int)k.rcm << ",\"b0\":" << (int)k.b0 << ",\"b1\":" << (int)k.b1
+          << ",\"flags\":" << (int)k.flags << ",\"cmask\":" << k.cmask << ",\"mat\":" << k.mat << ",\"aux\":" << k.aux
+          << ",\"qj\":" << (int)k.qj << "}";
+    });
+    o << ",";
+    arr("perms", plan.perms.size(), [&](size_t i) {
+        const KPerm &p = plan.perms[i];
+        o << "{\"col\":[";
+        for (int b = 0; b < plan.K; b++) o << (b ? "," : "") << p.col[b];
+        o << "],\"term_begin\":" << p.term_begin << ",\"term_end\":" << p.term_end << "}";
+    });
+    o << ",";
+    arr("perm_terms", plan.perm_terms.size(), [&](size_t i) {
+        o << "[" << plan.perm_terms[i].cmask << "," << plan.perm_terms[i].vec << "]";
+    });
+    o << ",";
+    arr("eterms", plan.eterms.size(), [&](size_t i) {
+        const ETerm &e = plan.eterms[i];
+        o << "[" << e.c << "," << e.znr << "," << e.zreg << "," << e.y << "]";
+    });
+    o << ",";
+    arr("specs", mb.specs.size(), [&](size_t i) {
+        const MSpec &m = mb.specs[i];
+        o << "[" << m.out << "," << m.f_begin << "," << m.f_end << "," << m.form << "]";
+    });
+    o << ",";
+    arr("factors", mb.factors.size(), [&](size_t i) {
+        const MFactor &f = mb.factors[i];
+        o << "[" << f.kind << "," << f.pidx << "," << f.angle << "," << f.cst << "]";
+    });
+    o << ",";
+    arr("cst", mb.cst.size(), [&](size_t i) { o << mb.cst[i]; });
+    o << ",";
+    arr("wide_groups", plan.wide_groups.size(), [&](size_t i) { o << plan.wide_groups[i]; });
+    o << ",";
+    arr("groups", plan.groups.size(), [&](size_t i) {
+        const PGroup &g = plan.groups[i];
+        o << "{\"x\":" << g.x << ",\"terms\":[";
+        for (size_t t = 0; t < g.terms.size(); t++)
+            o << (t ? "," : "") << "[" << g.terms[t].c << "," << g.terms[t].z << "," << g.terms[t].y << "]";
+        o << "]}";
+    });
+    o << "}";
+    return o.str();
 }
 
 }  // namespace lq

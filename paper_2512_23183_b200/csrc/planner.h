@@ -24,9 +24,18 @@ struct POp {
     int spec = -1;            // MSpec index (matrix), -1 if none
     uint8_t qflags = 0, qj = 0;
     double scale = 1.0;
+    uint64_t xm = 0, zm = 0;  // K_EXPV: group x mask, union of the terms' z masks (physical)
+    int group = -1;           // K_EXPV: index into Plan::groups
     uint64_t full() const;    // bits on which the op is not diagonal
     uint64_t touch() const;   // every bit the op reads
     bool diag() const { return type == K_D1 || type == K_D2 || type == K_SCALE; }
+};
+
+// A Pauli group: the terms of a Pauli sum that share one x mask.
+struct PGroup {
+    uint64_t x = 0;
+    struct Term { double c; uint64_t z; uint32_t y; };
+    std::vector<Term> terms;
 };
 
 bool commute(const POp &a, const POp &b);
@@ -49,6 +58,10 @@ struct Plan {
     std::vector<KOp> kops;
     std::vector<KPerm> perms;
     std::vector<KPermTerm> perm_terms;
+    std::vector<PGroup> groups;       // Pauli groups referenced by K_EXPV ops
+    std::vector<ETerm> eterms;        // their terms lowered per tile pass
+    uint32_t n_slots = 0;             // partial sums per circuit (tile passes with PF_EXPV)
+    std::vector<uint32_t> wide_groups;   // groups whose x mask exceeds a tile (direct kernel)
     size_t n_tile = 0, n_pair = 0, n_diag = 0;
     size_t n_folded = 0;      // permutation gates folded into exchanges
 };
@@ -82,26 +95,19 @@ void canonicalize_ops(int n, int32_t *qmap, std::vector<POp> &ops);
 void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, const MatBuilder &mb,
                   Plan &plan);
 
+// Pauli groups of a Pauli sum (bit q of a mask = qubit q -> physical
+// qmap[q]) as K_EXPV ops appended to `ops`; groups are stored in plan.groups.
+void lower_pauli(int n, const int32_t *qmap, const lq_pauli_term *terms, size_t n_terms,
+                 std::vector<POp> &ops, Plan &plan);
+
 // Plan the QFT (forward or inverse) as tile passes; updates qmap (layout
 // flips between identity and reversed).  Requires qmap identity or reversed.
 bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &plan,
               MatBuilder &mb);
 
-// Pauli expectation planning.
-struct PauliPlan {
-    int n = 0, K = 0;
-    std::vector<KPauliPass> passes;     // tiled passes
-    std::vector<PTerm> terms;
-    uint32_t n_slots = 0;               // partial sums per circuit
-    // groups whose x mask does not fit in a tile: direct pair passes
-    struct Direct { uint64_t x; uint32_t term_begin, term_end; uint32_t slot; uint32_t n_blocks; };
-    std::vector<Direct> direct;
-};
-void plan_pauli(int n, const int32_t *qmap, const lq_pauli_term *terms, size_t n_terms,
-                const PlanOptions &opt, PauliPlan &pp);
-
 int auto_tile_bits(int n);
 
 std::string describe(const Plan &plan);
+std::string export_json(const Plan &plan, const MatBuilder &mb, const int32_t *qmap);
 
 }  // namespace lq

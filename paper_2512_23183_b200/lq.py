@@ -94,6 +94,7 @@ _SIGS = {
     "lq_get_option": ([_i32], _i64),
     "lq_plan_describe": ([_i32, _GP, _sz, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.c_char_p, _sz], _i32),
     "lq_launch_count": ([], _u64),
+    "lq_plan_export_json": ([_i32, _GP, _sz, _TP, _sz, ctypes.c_char_p, _sz, ctypes.POINTER(_sz)], _i32),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -343,6 +344,17 @@ def lq_plan_describe(n_qubits: int, gates) -> Tuple[int, int, str]:
     buf = ctypes.create_string_buffer(1 << 16)
     _chk(_lib.lq_plan_describe(n_qubits, ga.ptr, ga.n, ctypes.byref(np_), ctypes.byref(nt), buf, len(buf)))
     return np_.value, nt.value, buf.value.decode()
+
+
+def lq_plan_export_json(n_qubits: int, gates, terms=()) -> dict:
+    import json
+    ga = gates if isinstance(gates, GateArray) else GateArray(gates)
+    ta = terms if isinstance(terms, TermArray) else TermArray(terms)
+    need = ctypes.c_size_t()
+    _chk(_lib.lq_plan_export_json(n_qubits, ga.ptr, ga.n, ta.ptr, ta.n, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _chk(_lib.lq_plan_export_json(n_qubits, ga.ptr, ga.n, ta.ptr, ta.n, buf, len(buf), ctypes.byref(need)))
+    return json.loads(buf.value.decode())
 
 
 # ---- convenience: a torch-owned state ---------------------------------------

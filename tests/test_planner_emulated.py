@@ -1,0 +1,62 @@
+"""Host planner checked on CPU: liblq's exported plans executed by the
+test-side plan emulator (tests/plan_emulator.py) must reproduce the oracle.
+Covers tiling, register sub-blocks, folded permutations, 1q fusion and the
+Pauli-group (expectation) ops without a GPU."""
+import numpy as np
+import pytest
+
+import workloads as W
+import plan_emulator as EM
+from test_gpu_parity import rich_circuit
+
+
+@pytest.fixture(scope="module")
+def lq():
+    from paper_2512_23183_b200 import build
+    build.build()
+    from paper_2512_23183_b200 import lq as _lq
+    yield _lq
+    _lq.lq_set_option(_lq.LQ_OPT_TILE_BITS, 0)
+    _lq.lq_set_option(_lq.LQ_OPT_REG_BITS, 4)
+
+
+def emulate(lq, n, gates, psi0, theta=None, terms=(), shift=None):
+    plan = lq.lq_plan_export_json(n, gates, terms)
+    psi = psi0.copy()
+    E = EM.run(plan, psi, theta, shift)
+    return EM.logical_state(plan["qmap"], psi), E, plan
+
+
+@pytest.mark.parametrize("K,rb", [(0, 4), (5, 4), (6, 3), (3, 3)])
+@pytest.mark.parametrize("n", [3, 9, 14])
+def test_emulated_rich_circuits(lq, oracle, n, K, rb):
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
+    lq.lq_set_option(lq.LQ_OPT_REG_BITS, rb)
+    rng = np.random.default_rng(7000 + 31 * n + K)
+    gates = rich_circuit(n, 120, rng)
+    psi0 = oracle.init_random(n, 5 + n)
+    got, _, _ = emulate(lq, n, gates, psi0)
+    ref = oracle.apply_circuit(psi0.copy(), gates)
+    assert np.abs(got - ref).max() <= 1e-10
+
+
+@pytest.mark.parametrize("K", [0, 5])
+@pytest.mark.parametrize("n", [6, 14])
+def test_emulated_psr_energy(lq, oracle, n, K):
+    """Gates + Pauli groups planned together (the parameter-shift path)."""
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
+    gates = W.hea_ansatz(n, 2, "ring")
+    theta = np.random.default_rng(n).uniform(0, 2 * np.pi, 4 * n)
+    for terms in (W.xyz_terms(n), W.random_pauli_sum(n, 20, np.random.default_rng(n + 1))):
+        psi0 = oracle.zeros(n)
+        _, E, plan = emulate(lq, n, gates, psi0, theta, terms)
+        assert E == pytest.approx(oracle.energy(n, gates, theta, terms), abs=1e-10)
+
+
+@pytest.mark.parametrize("n", [5, 13])
+def test_emulated_expval_only(lq, oracle, n):
+    rng = np.random.default_rng(n)
+    terms = W.random_pauli_sum(n, 30, rng)
+    psi0 = oracle.init_random(n, 9)
+    _, E, plan = emulate(lq, n, [], psi0, None, terms)
+    assert E == pytest.approx(oracle.expval(psi0, terms), abs=1e-10)
