@@ -208,7 +208,11 @@ typedef enum {
     LQ_OPT_TILE_BITS = 1,  /* tile size K in bits (default 0 = automatic) */
     LQ_OPT_COALESCE_BITS = 2, /* low physical bits every strided tile includes (default 3) */
     LQ_OPT_REG_BITS = 3,      /* amplitudes per thread in tile passes = 2^value, 3 or 4 (default 4) */
-    LQ_OPT_KERNEL_TIMING = 4  /* 1: bracket every launch with CUDA events on its stream (lq_kernel_timing) */
+    LQ_OPT_KERNEL_TIMING = 4, /* 1: bracket every launch with CUDA events on its stream (lq_kernel_timing) */
+    LQ_OPT_JIT = 5            /* tile passes as per-plan specialised kernels compiled with NVRTC for
+                                 sm_100a (cached per process) instead of the op-list interpreter kernel;
+                                 both execute the same device op templates (tile.cuh).  0: off;
+                                 1 (default): auto -- PSR plans and states with n >= 26; 2: always. */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);
@@ -226,11 +230,21 @@ lq_status lq_plan_describe(int n_qubits, const lq_gate *gates, size_t n_gates, u
 lq_status lq_plan_export_json(int n_qubits, const lq_gate *gates, size_t n_gates, const lq_pauli_term *terms,
                               size_t n_terms, char *buf, size_t buf_len, size_t *needed);
 
+/* Host-only: generate and NVRTC-compile (for sm_100a, without loading) the
+ * JIT pass programs of `gates` followed by the Pauli sum `terms` (may be
+ * empty).  No device needed; LQ_ERR_CUDA with the compiler log on failure. */
+lq_status lq_jit_compile_check(int n_qubits, const lq_gate *gates, size_t n_gates, const lq_pauli_term *terms,
+                               size_t n_terms, uint64_t *n_kernels);
+
 /* Accumulated device time of launches made while LQ_OPT_KERNEL_TIMING was
  * on, per kernel class: 0 tile pass, 1 pair pass, 2 diagonal pass,
  * 3 Pauli expectation, 4 other.  Synchronises on the recorded events. */
 lq_status lq_kernel_timing(int kernel_class, double *total_ms, uint64_t *count);
 lq_status lq_kernel_timing_reset(void);
+
+/* JIT compiler accounting (LQ_OPT_JIT): pass kernels compiled, cache hits,
+ * total compile wall time.  Any output pointer may be NULL. */
+lq_status lq_jit_stats(uint64_t *compiled, uint64_t *cache_hits, double *compile_seconds);
 
 /* Kernel launches issued by this process so far (all entry points). */
 uint64_t lq_launch_count(void);

@@ -17,6 +17,7 @@
 
 #include "kernels.cuh"
 #include "planner.h"
+#include "jit.h"
 
 using namespace lq;
 
@@ -31,6 +32,7 @@ std::atomic<int64_t> g_opt_fusion{1};
 std::atomic<int64_t> g_opt_K{0};
 std::atomic<int64_t> g_opt_coalesce{3};
 std::atomic<int64_t> g_opt_regbits{4};
+std::atomic<int64_t> g_opt_jit{1};
 const double PI = 3.14159265358979323846264338327950288;
 
 lq_status fail(lq_status s, const std::string &msg) {
@@ -123,6 +125,23 @@ PlanOptions options() {
     o.fusion = g_opt_fusion.load() != 0;
     o.reg_bits = (int)g_opt_regbits.load();
     return o;
+}
+
+// JIT-specialise the plan's tile passes (LQ_OPT_JIT).  Auto mode (1)
+// compiles plans that will stream enough amplitudes to amortise NVRTC
+// (~1-5 s per pass): every PSR plan (it runs 2P+1 circuits) and single
+// states with n >= 26; 2 forces it, 0 disables it.
+lq_status prepare(Plan &plan, bool reused = false) {
+    plan.jit.clear();
+    const int64_t mode = g_opt_jit.load();
+    if (mode == 0 || plan.n_tile == 0) return LQ_OK;
+    if (mode == 1 && !reused && plan.n < 26) return LQ_OK;
+    std::string err;
+    if (!jit_plan(plan, plan.jit, err)) {
+        plan.jit.clear();
+        return fail(LQ_ERR_CUDA, err);
+    }
+    return LQ_OK;
 }
 
 // Stream-ordered growable device buffer.
@@ -248,7 +267,7 @@ lq_status validate_terms(int n, const lq_pauli_term *t, size_t nt) {
 
 // ---------------------------------------------------------------- launches
 template <int RR>
-lq_status launch_tile_rr(const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
+lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
                          const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                          uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride,
                          int n_circ, double *partials, uint64_t slot_stride, cudaStream_t st) {
@@ -273,17 +292,26 @@ lq_status launch_tile_rr(const KPass &kp, const KSub *subs, const KOp *kops, con
     const unsigned grid = (unsigned)std::min<uint64_t>(total, (uint64_t)n_sm);
     LaunchTimer lt_(KC_TILE, st);
     if ((kp.flags & PF_EXPV) && !partials) return fail(LQ_ERR_STATE, "expectation pass without partial buffer");
+    if (jk) {   // JIT-specialised program of this pass (jit.h): same parameters as k_tile
+        uint32_t tot32 = (uint32_t)total;
+        void *args[] = {(void *)&kp,      (void *)&subs,   (void *)&kops,       (void *)&perms, (void *)&pterms,
+                        (void *)&eterms,  (void *)&mats,   (void *)&mat_stride, (void *)&cst,   (void *)&state,
+                        (void *)&state_stride, (void *)&tiles_log2, (void *)&tot32, (void *)&partials,
+                        (void *)&slot_stride};
+        CUDA_TRY(cudaLaunchKernel(jk, dim3(grid), dim3(1u << (kp.K - RR)), args, smem, st));
+        return check_launch("k_tile (jit)");
+    }
     k_tile<RR><<<grid, 1u << (kp.K - RR), smem, st>>>(kp, subs, kops, perms, pterms, eterms, mats, mat_stride, cst,
                                                       state, state_stride, tiles_log2, (uint32_t)total, partials,
                                                       slot_stride);
     return check_launch("k_tile");
 }
 
-lq_status launch_tile(int Rr, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
+lq_status launch_tile(int Rr, const void *jk, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
                       const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                       uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride, int n_circ,
                       double *partials, uint64_t slot_stride, cudaStream_t st) {
-#define LT(RRV) launch_tile_rr<RRV>(kp, subs, kops, perms, pterms, n_pterms, eterms, mats, mat_stride, cst, state, \
+#define LT(RRV) launch_tile_rr<RRV>(jk, kp, subs, kops, perms, pterms, n_pterms, eterms, mats, mat_stride, cst, state, \
                                     state_stride, n_circ, partials, slot_stride, st)
     switch (Rr) {
     case 1: return LT(1);
@@ -328,7 +356,8 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
             uint32_t npt = 0;
             if (kp.perm_end > kp.perm_begin)
                 npt = plan.perms[kp.perm_end - 1].term_end - plan.perms[kp.perm_begin].term_begin;
-            LQ_TRY(launch_tile(plan.Rr, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, dp.eterms, mats, mat_stride,
+            const void *jk = i < plan.jit.size() ? plan.jit[i] : nullptr;
+            LQ_TRY(launch_tile(plan.Rr, jk, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, dp.eterms, mats, mat_stride,
                                dp.cst, state, state_stride, n_circ, partials, slot_stride, st));
         } else if (p.kind == PASS_PAIR) {
             const KOp op = plan.kops[p.op_begin];
@@ -433,8 +462,9 @@ lq_status check_sv(const lq_sv *sv) {
 }
 
 // Run a circuit-level plan on one state (apply_circuit / canonicalize / qft).
-lq_status run_single(lq_sv *sv, const Plan &plan, const MatBuilder &mb, const double *theta, size_t n_theta) {
+lq_status run_single(lq_sv *sv, Plan &plan, const MatBuilder &mb, const double *theta, size_t n_theta) {
     if (plan.passes.empty()) return LQ_OK;
+    LQ_TRY(prepare(plan));
     Blob blob;
     size_t o_sub = blob.add(plan.subs), o_kop = blob.add(plan.kops), o_spec = blob.add(mb.specs),
            o_fac = blob.add(mb.factors), o_cst = blob.add(mb.cst), o_perm = blob.add(plan.perms),
@@ -498,6 +528,11 @@ int lq_device_count(void) {
 
 uint64_t lq_launch_count(void) { return g_launches.load(); }
 
+lq_status lq_jit_stats(uint64_t *compiled, uint64_t *cache_hits, double *compile_seconds) {
+    jit_stats(compiled, cache_hits, compile_seconds);
+    return LQ_OK;
+}
+
 lq_status lq_kernel_timing(int kernel_class, double *total_ms, uint64_t *count) {
     if (kernel_class < 0 || kernel_class >= KC_N) return fail(LQ_ERR_ARG, "bad kernel class");
     harvest_timing();
@@ -530,6 +565,10 @@ lq_status lq_set_option(int option, int64_t value) {
     case LQ_OPT_KERNEL_TIMING:
         g_opt_timing = value ? 1 : 0;
         return LQ_OK;
+    case LQ_OPT_JIT:
+        if (value < 0 || value > 2) return fail(LQ_ERR_ARG, "jit must be 0 (off), 1 (auto) or 2 (always)");
+        g_opt_jit = value;
+        return LQ_OK;
     default: return fail(LQ_ERR_ARG, "unknown option");
     }
 }
@@ -541,6 +580,7 @@ int64_t lq_get_option(int option) {
     case LQ_OPT_COALESCE_BITS: return g_opt_coalesce.load();
     case LQ_OPT_REG_BITS: return g_opt_regbits.load();
     case LQ_OPT_KERNEL_TIMING: return g_opt_timing.load();
+    case LQ_OPT_JIT: return g_opt_jit.load();
     default: return -1;
     }
 }
@@ -768,6 +808,7 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
     std::vector<POp> ops;
     lower_pauli(sv->n, sv->qmap, terms, n_terms, ops, plan);
     plan_circuit(sv->n, ops, options(), mb, plan);
+    LQ_TRY(prepare(plan));
     DirectSet dset;
     dset.build(plan);
     Blob blob;
@@ -866,6 +907,13 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     // last gate that touches their qubits)
     lower_pauli(n_qubits, qm, terms, n_terms, ops, P->plan);
     plan_circuit(n_qubits, ops, options(), P->mb, P->plan);
+    {
+        lq_status js = prepare(P->plan, true);
+        if (js != LQ_OK) {
+            delete P;
+            return js;
+        }
+    }
     P->dset.build(P->plan);
     // circuits of this shard: (p, +pi/2), (p, -pi/2) for owned p; base on shard 0.
     // Parameters used by no gate have E+ == E- identically: g_p = 0 (written by combine).
@@ -1011,6 +1059,29 @@ lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gate
     lq_psr_free(P);
     if (s != LQ_OK) g_err = keep;
     return s;
+}
+
+// Host-only: generate and NVRTC-compile (without loading) the JIT pass
+// programs of `gates` (+ an optional Pauli sum, planned as the PSR driver
+// does).  No device needed.
+lq_status lq_jit_compile_check(int n_qubits, const lq_gate *gates, size_t n_gates, const lq_pauli_term *terms,
+                               size_t n_terms, uint64_t *n_kernels) {
+    if (n_qubits < 1 || n_qubits > 40) return fail(LQ_ERR_ARG, "n_qubits must be in [1, 40]");
+    LQ_TRY(validate_gates(n_qubits, gates, n_gates, nullptr, 1 << 16, false, nullptr));
+    LQ_TRY(validate_terms(n_qubits, terms, n_terms));
+    int32_t qm[64];
+    for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
+    std::vector<POp> ops;
+    MatBuilder mb;
+    Plan plan;
+    lower_gates(n_qubits, gates, n_gates, qm, ops, mb);
+    if (n_terms) lower_pauli(n_qubits, qm, terms, n_terms, ops, plan);
+    plan_circuit(n_qubits, ops, options(), mb, plan);
+    size_t nk = 0;
+    std::string err;
+    if (!jit_check(plan, &nk, err)) return fail(LQ_ERR_CUDA, err);
+    if (n_kernels) *n_kernels = nk;
+    return LQ_OK;
 }
 
 // Host-only planning diagnostics (no device needed): plan `gates` on n

@@ -22,8 +22,17 @@
 // Physical bit p of an amplitude index holds logical qubit q with
 // qmap[q] = p (identity: p = n-1-q).
 #pragma once
+#ifdef __CUDACC_RTC__   // JIT (NVRTC): no host headers
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+#else
 #include <cstddef>
 #include <cstdint>
+#endif
 
 #ifdef __CUDACC__
 #define LQ_HD __host__ __device__
@@ -47,8 +56,22 @@ enum KOpType : uint8_t {
     K_SWAP = 5, // exchange register bits r0, r1
     K_QFT = 6,  // QFT stage on register bit r0 (logical bit qj); aux = twiddle table
     K_SCALE = 7, // multiply every amplitude by `scale`
-    K_EXPV = 8   // Pauli-group expectation contribution (read-only; see ETerm)
+    K_EXPV = 8,  // Pauli-group expectation contribution (read-only; see ETerm)
+    K_G = 9      // scaled 2x2 rotation on register bit r0 (RY / RX / H, see GKind)
 };
+
+// Scaled rotation families (K_G; qj holds the family).  Every matrix is
+// lambda * M with M having unit entries, so an amplitude pair costs 4 DFMA
+// (or 4 DADD) instead of 16 FP64 ops; lambda is a real scalar the kernel
+// defers.  Table: [0] = (p, lambda), [1] = (variant, 0).
+//   GK_REAL (RY):  variant 0: M = [[1, -p], [p, 1]]   (p = tan(theta/2), lambda = cos)
+//                  variant 1: M = [[p, -1], [1, p]]   (p = cot(theta/2), lambda = sin)
+//   GK_IMAG (RX):  variant 0: M = [[1, -ip], [-ip, 1]]; variant 1: M = [[p, -i], [-i, p]]
+//   GK_HAD  (H):   M = [[1, 1], [1, -1]], lambda = 1/sqrt(2)
+enum GKind : uint8_t { GK_REAL = 0, GK_IMAG = 1, GK_HAD = 2 };
+
+// Internal factor kinds (beyond lq_kind) used by the matrix builder.
+constexpr int FK_YDIAG = 100;   // diag(i, -i): Y = X * diag(i, -i)
 
 enum KOpFlags : uint8_t {
     QF_INVERSE = 1,   // inverse stage (conj twiddle before the butterfly)
@@ -85,7 +108,16 @@ enum CodeTile : uint8_t {
     C_QFT = 29,      // + r0
     C_SCALE = 33,
     C_GENERIC = 34,
-    C_EXPV = 35      // Pauli group: rcm = x mask in register positions, mat/aux = ETerm range
+    C_EXPV = 35,     // Pauli group: rcm = x mask in register positions, mat/aux = ETerm range
+    C_G = 36,        // + 4*GKind + r0: scaled rotation on a register bit, no register control
+    C_D1U = 48,      // diagonal on a bit outside the tile, controls outside the tile (tile-uniform factor)
+    C_NUM = 49
+};
+
+// KOp.flags bits for diagonal ops (QF_* are QFT-only)
+enum KOpDiagFlags : uint8_t {
+    OF_UNIFORM = 8,   // every control bit lies outside the tile: the op acts alike on all threads of a tile
+    OF_OUTSIDE = 16   // the target bit lies outside the tile
 };
 
 // One Pauli term of a group lowered to a sub-block:
@@ -130,17 +162,18 @@ enum PassFlags : uint32_t {
 };
 
 // Tile pass descriptor, passed by value to the kernel.
-constexpr int MAX_PASS_OPS = 96;   // ops staged in shared memory per tile pass
+constexpr int MAX_PASS_OPS = 192;  // ops staged in shared memory per tile pass
 
 // table size (double2) an op stages in shared memory
 LQ_HD inline int op_table_size(uint8_t type) {
     switch (type) {
     case K_U1: return 4;
-    case K_D1: return 2;
+    case K_D1: return 3;      // d0, d1, d1/d0
     case K_U2: return 16;
     case K_D2: return 4;
     case K_QFT: return 16;
     case K_SCALE: return 1;
+    case K_G: return 2;
     default: return 0;
     }
 }
@@ -164,7 +197,7 @@ struct KPass {
 
 // Matrix construction (device-side, per circuit): every fused op has a
 // MSpec that multiplies its factor gates (later factors on the left).
-enum MForm : uint8_t { MF_U2x2 = 0, MF_DIAG2 = 1, MF_U4x4 = 2, MF_DIAG4 = 3 };
+enum MForm : uint8_t { MF_U2x2 = 0, MF_DIAG2 = 1, MF_U4x4 = 2, MF_DIAG4 = 3, MF_G = 4 };
 
 // Factor kinds use lq_kind numbering for gates; the angle is theta[pidx]
 // (+ the circuit's shift if pidx is the shifted parameter) or `angle`.

@@ -14,7 +14,7 @@ static inline uint64_t bit(int b) { return 1ull << b; }
 
 uint64_t POp::full() const {
     switch (type) {
-    case K_U1: case K_X: case K_QFT: return bit(t0);
+    case K_U1: case K_X: case K_QFT: case K_G: return bit(t0);
     case K_U2: case K_SWAP: return bit(t0) | bit(t1);
     case K_EXPV: return xm;
     default: return 0;
@@ -42,7 +42,7 @@ int MatBuilder::add_spec(MForm form, const std::vector<MFactor> &f) {
     factors.insert(factors.end(), f.begin(), f.end());
     s.f_end = (uint32_t)factors.size();
     s.form = form;
-    static const uint32_t sz[4] = {4, 2, 16, 4};
+    static const uint32_t sz[5] = {4, 3, 16, 4, 2};
     mat_size += sz[form];
     specs.push_back(s);
     return (int)specs.size() - 1;
@@ -86,22 +86,37 @@ void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
             if (k == LQ_U1) f.cst = mb.add_const(G.mat, 4);
             int b = qmap[G.q0];
             int prev = last[b];
-            if (prev >= (int)base && fusable[prev - base] && ops[prev].t0 == b) {
-                // no op touched bit b since `prev`: this gate commutes with
-                // everything in between, so it can join `prev`.
-                POp &P = ops[prev];
+            const bool dg = is_diag_1q(k) || k == LQ_Y;
+            if (k == LQ_Y) f.kind = FK_YDIAG;   // Y = X * diag(i, -i): the diagonal part, then X
+            if (dg && prev >= (int)base && fusable[prev - base] && ops[prev].t0 == b && ops[prev].type == K_D1) {
+                // no op touched bit b since `prev` (a diagonal op): the diagonal
+                // factor joins it.  Non-diagonal 1q gates are NOT fused: two
+                // scaled rotations (K_G, 4 DFMA per pair each) are cheaper than
+                // one general complex 2x2 (16 FP64 ops per pair).
                 fl[prev - base].push_back(f);
-                bool d = (P.type == K_D1) && is_diag_1q(k);
-                P.type = d ? K_D1 : K_U1;
-                continue;
+            } else {
+                POp op;
+                op.t0 = b;
+                if (dg) op.type = K_D1;
+                else if (k == LQ_X) op.type = K_X;
+                else if (k == LQ_RY || k == LQ_RX || k == LQ_H) {
+                    op.type = K_G;
+                    op.qj = (uint8_t)(k == LQ_RY ? GK_REAL : k == LQ_RX ? GK_IMAG : GK_HAD);
+                } else op.type = K_U1;
+                ops.push_back(op);
+                fl.push_back(op.type == K_X ? std::vector<MFactor>{} : std::vector<MFactor>{f});
+                fusable.push_back(op.type == K_D1 ? 1 : 0);
+                touch_all((int)ops.size() - 1);
             }
-            POp op;
-            op.type = is_diag_1q(k) ? K_D1 : (k == LQ_X ? K_X : K_U1);
-            op.t0 = b;
-            ops.push_back(op);
-            fl.push_back({f});
-            fusable.push_back(1);
-            touch_all((int)ops.size() - 1);
+            if (k == LQ_Y) {
+                POp op;
+                op.type = K_X;
+                op.t0 = b;
+                ops.push_back(op);
+                fl.push_back({});
+                fusable.push_back(0);
+                touch_all((int)ops.size() - 1);
+            }
             continue;
         }
         POp op;
@@ -125,9 +140,8 @@ void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
     for (size_t i = base; i < ops.size(); i++) {
         POp &P = ops[i];
         auto &F = fl[i - base];
-        if (P.type == K_X && F.size() <= 1) { P.spec = -1; continue; }
-        if (P.type == K_X) P.type = K_U1;
-        MForm form = P.type == K_D1 ? MF_DIAG2 : P.type == K_U1 ? MF_U2x2
+        if (P.type == K_X) { P.spec = -1; continue; }
+        MForm form = P.type == K_D1 ? MF_DIAG2 : P.type == K_U1 ? MF_U2x2 : P.type == K_G ? MF_G
                    : P.type == K_U2 ? MF_U4x4 : MF_DIAG4;
         P.spec = mb.add_spec(form, F);
     }
@@ -278,6 +292,13 @@ static KOp lower_tile_op(const POp &o, const LocalMap &L, const uint8_t *S, int 
         c &= c - 1;
     }
     k.flags = o.qflags;
+    if (o.type == K_D1) {
+        bool uni = true;
+        uint64_t cc = o.ctrl;
+        while (cc) { if (L.loc[__builtin_ctzll(cc)] >= 0) uni = false; cc &= cc - 1; }
+        if (uni) k.flags |= OF_UNIFORM;
+        if (L.loc[o.t0] < 0) k.flags |= OF_OUTSIDE;
+    }
     k.qj = o.qj;
     k.mat = o.spec >= 0 ? mat_off[o.spec] : 0;
     return k;
@@ -290,6 +311,7 @@ static KOp lower_flat_op(const POp &o, const std::vector<uint32_t> &mat_off) {
     k.b0 = (uint8_t)(o.t0 >= 0 ? o.t0 : 0);
     k.b1 = (uint8_t)(o.t1 >= 0 ? o.t1 : 0);
     k.cmask = o.ctrl;
+    k.qj = o.qj;
     k.mat = o.spec >= 0 ? mat_off[o.spec] : 0;
     k.code = C_GENERIC;
     return k;
@@ -301,12 +323,18 @@ static uint8_t tile_code(const KOp &k) {
     case K_U1:
         if (k.rcm == 0 && k.r0 < R) return (uint8_t)(C_U1 + k.r0);
         break;
+    case K_G:
+        if (k.rcm == 0 && k.r0 < R) return (uint8_t)(C_G + 4 * k.qj + k.r0);
+        break;
     case K_X:
         if (k.rcm == 0 && k.r0 < R) return (uint8_t)(C_X + k.r0);
         if (__builtin_popcount(k.rcm) == 1 && k.r0 < R) return (uint8_t)(C_CX + 4 * __builtin_ctz(k.rcm) + k.r0);
         break;
     case K_D1:
-        if (k.rcm == 0) return k.r0 < R ? (uint8_t)(C_D1R + k.r0) : (uint8_t)C_D1T;
+        if (k.rcm == 0) {
+            if (k.r0 < R) return (uint8_t)(C_D1R + k.r0);
+            return ((k.flags & OF_UNIFORM) && (k.flags & OF_OUTSIDE)) ? (uint8_t)C_D1U : (uint8_t)C_D1T;
+        }
         break;
     case K_QFT:
         if (k.r0 < R) return (uint8_t)(C_QFT + k.r0);

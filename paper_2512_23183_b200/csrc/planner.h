@@ -64,6 +64,7 @@ struct Plan {
     std::vector<uint32_t> wide_groups;   // groups whose x mask exceeds a tile (direct kernel)
     size_t n_tile = 0, n_pair = 0, n_diag = 0;
     size_t n_folded = 0;      // permutation gates folded into exchanges
+    std::vector<const void *> jit;    // per pass: JIT-compiled tile kernel (cudaKernel_t) or nullptr (jit.h)
 };
 
 struct MatBuilder {

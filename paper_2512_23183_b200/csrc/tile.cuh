@@ -1,0 +1,1089 @@
+// tile.cuh -- the fused tile-pass kernel of liblq.
+//
+// Included by kernels.cuh (nvcc) and embedded verbatim in liblq.so as the
+// prelude of JIT-compiled pass programs (NVRTC, jit.cpp): it must compile
+// without host headers.  Every dense complex128 gate update is 2-14 FP64
+// ops per 32 B of HBM traffic, far below the FP64 ridge, and tcgen05 has no
+// FP64 kind: the design target is coalesced 16-byte accesses, enough bytes
+// in flight, as many gates per HBM round trip as possible and as few
+// instructions per gate as possible.  See DESIGN.md §5, §7.
+#pragma once
+#ifndef __CUDACC_RTC__
+#include <cuda_runtime.h>
+#include <stdint.h>
+#endif
+#include "lq_internal.h"
+
+namespace lq {
+
+// ---------------------------------------------------------------- complex
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a*b + c
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+// Deterministic block reduction (fixed shuffle tree + fixed smem tree).
+// red: >= max(32, blockDim.x) doubles of shared memory.  blockDim.x must be
+// a power of two.  Result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double *red) {
+    const int nt = blockDim.x, t = threadIdx.x;
+    if (nt >= 32) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        const int w = t >> 5, l = t & 31;
+        if (l == 0) red[w] = v;
+        __syncthreads();
+        double r = 0.0;
+        if (w == 0) {
+            r = (l < (nt >> 5)) ? red[l] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+        }
+        __syncthreads();
+        return r;
+    }
+    red[t] = v;
+    __syncthreads();
+    for (int s = nt >> 1; s > 0; s >>= 1) {
+        if (t < s) red[t] += red[t + s];
+        __syncthreads();
+    }
+    double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// In-place register swap the compiler cannot turn into a renaming (a
+// renaming would force loop-carried copies of the whole register tile).
+__device__ __forceinline__ void swap_inplace(double2 &x, double2 &y) {
+    asm volatile("{\n\t.reg .f64 t;\n\tmov.f64 t, %0;\n\tmov.f64 %0, %2;\n\tmov.f64 %2, t;\n\t"
+                 "mov.f64 t, %1;\n\tmov.f64 %1, %3;\n\tmov.f64 %3, t;\n\t}"
+                 : "+d"(x.x), "+d"(x.y), "+d"(y.x), "+d"(y.y));
+}
+
+__device__ __forceinline__ uint64_t insert_zero64(uint64_t x, int b) {
+    uint64_t lo = x & ((1ull << b) - 1);
+    return ((x ^ lo) << 1) | lo;
+}
+__device__ __forceinline__ uint32_t insert_zero32(uint32_t x, int b) {
+    uint32_t lo = x & ((1u << b) - 1);
+    return ((x ^ lo) << 1) | lo;
+}
+
+// ---------------------------------------------------------------- tile kernel
+// Shared-memory index swizzle for the 16-byte exchange buffer: XOR-folds the
+// higher 3-bit groups into the bank-group bits (idx mod 8), so the 8 lanes
+// of a quarter warp hit distinct bank groups whenever the lowest three
+// non-register local bits have distinct residues mod 3.  GF(2)-linear, so
+// swz(a ^ b) = swz(a) ^ swz(b).
+__host__ __device__ constexpr uint32_t swz(uint32_t x) {
+    return x ^ (((x >> 3) ^ (x >> 6) ^ (x >> 9) ^ (x >> 12)) & 7u);
+}
+
+// Register mapping of a sub-block: thread t holds the 2^RR amplitudes with
+// local index lt + loff(v), loff(v) = sum_{i: v_i} 2^{S[i]}; global index
+// gt + goff(v), goff(v) = sum_{i: v_i} 2^{T[S[i]]}.  Shared-memory slots
+// are swizzled: slot = swz(lt) ^ swz(loff(v)).
+template <int RR>
+struct Mapping {
+    uint32_t lt;         // local index of v = 0
+    uint32_t slt;        // shared-memory slot of v = 0 (plain, used for writes)
+    uint32_t slm[RR];    // slot offsets (XOR) of the register bits
+    uint64_t gt;         // global index of v = 0
+    uint64_t gm[RR];     // global offsets of the register bits
+    // dep: deposit tables of the local->global bit map (dep[0][l & 255] |
+    // dep[1][l >> 8] = the global bits of local index l)
+    __device__ __forceinline__ void make(uint32_t t, const uint8_t *S, const uint64_t *dlo, const uint64_t *dhi,
+                                         uint64_t tb) {
+        uint32_t l = t;
+#pragma unroll
+        for (int i = 0; i < RR; i++) l = insert_zero32(l, S[i]);
+        lt = l;
+        gt = tb | dlo[l & 255] | dhi[l >> 8];
+        slt = swz(l);
+#pragma unroll
+        for (int i = 0; i < RR; i++) {
+            slm[i] = swz(1u << S[i]);
+            gm[i] = S[i] < 8 ? dlo[1u << S[i]] : dhi[1u << (S[i] - 8)];
+        }
+    }
+    template <int V>
+    __device__ __forceinline__ uint32_t sidx() const {
+        uint32_t o = slt;
+#pragma unroll
+        for (int i = 0; i < RR; i++)
+            if (V & (1 << i)) o ^= slm[i];
+        return o;
+    }
+    // slot offset of a runtime register index u (folds the flip mask)
+    __device__ __forceinline__ uint32_t soff_dyn(uint32_t u) const {
+        uint32_t o = 0;
+#pragma unroll
+        for (int i = 0; i < RR; i++)
+            if ((u >> i) & 1) o ^= slm[i];
+        return o;
+    }
+    template <int V>
+    __device__ __forceinline__ uint64_t goff() const {
+        uint64_t o = 0;
+#pragma unroll
+        for (int i = 0; i < RR; i++)
+            if (V & (1 << i)) o |= gm[i];
+        return o;
+    }
+};
+
+// Read slots of a mapping through an entry permutation: register slot l
+// reads position P^-1(l) = Ainv l + binv.
+template <int RR>
+struct PermSlots {
+    uint32_t slt, slm[RR];
+    __device__ __forceinline__ void make(const Mapping<RR> &m, const uint8_t *S, int K, const KPerm &pm,
+                                         uint32_t binv) {
+        uint32_t lp = binv;
+        for (int i = 0; i < K; i++)
+            if ((m.lt >> i) & 1) lp ^= pm.col[i];
+        slt = swz(lp);
+#pragma unroll
+        for (int i = 0; i < RR; i++) slm[i] = swz(pm.col[S[i]]);
+    }
+    template <int V>
+    __device__ __forceinline__ uint32_t sidx() const {
+        uint32_t o = slt;
+#pragma unroll
+        for (int i = 0; i < RR; i++)
+            if (V & (1 << i)) o ^= slm[i];
+        return o;
+    }
+};
+
+template <int V> struct IC { static constexpr int value = V; };
+
+template <int RR, int V = 0>
+struct Unroll {
+    template <class F>
+    __device__ __forceinline__ static void run(F &&f) {
+        f(IC<V>());
+        Unroll<RR, V + 1>::run(f);
+    }
+};
+template <int RR>
+struct Unroll<RR, (1 << RR)> {
+    template <class F>
+    __device__ __forceinline__ static void run(F &&) {}
+};
+
+template <int RR, int P>
+__device__ __forceinline__ void ap_u1(double2 (&a)[1 << RR], double2 u00, double2 u01, double2 u10,
+                                      double2 u11, uint32_t rcm) {
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++) {
+        if (v & (1 << P)) continue;
+        if ((v & rcm) != rcm) continue;
+        const int w = v | (1 << P);
+        double2 x = a[v], y = a[w];
+        a[v] = cfma(u00, x, cmul(u01, y));
+        a[w] = cfma(u10, x, cmul(u11, y));
+    }
+}
+
+template <int RR, int P>
+__device__ __forceinline__ void ap_x(double2 (&a)[1 << RR], uint32_t rcm) {
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++) {
+        if (v & (1 << P)) continue;
+        if ((v & rcm) != rcm) continue;
+        const int w = v | (1 << P);
+        swap_inplace(a[v], a[w]);
+    }
+}
+
+template <int RR, int P0, int P1>
+__device__ __forceinline__ void ap_u2(double2 (&a)[1 << RR], const double2 *U, uint32_t rcm) {
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++) {
+        if (v & ((1 << P0) | (1 << P1))) continue;
+        if ((v & rcm) != rcm) continue;
+        const int i0 = v, i1 = v | (1 << P1), i2 = v | (1 << P0), i3 = v | (1 << P0) | (1 << P1);
+        double2 x0 = a[i0], x1 = a[i1], x2 = a[i2], x3 = a[i3];
+        a[i0] = cfma(U[0], x0, cfma(U[1], x1, cfma(U[2], x2, cmul(U[3], x3))));
+        a[i1] = cfma(U[4], x0, cfma(U[5], x1, cfma(U[6], x2, cmul(U[7], x3))));
+        a[i2] = cfma(U[8], x0, cfma(U[9], x1, cfma(U[10], x2, cmul(U[11], x3))));
+        a[i3] = cfma(U[12], x0, cfma(U[13], x1, cfma(U[14], x2, cmul(U[15], x3))));
+    }
+}
+
+template <int RR, int P0, int P1>
+__device__ __forceinline__ void ap_swap(double2 (&a)[1 << RR], uint32_t rcm) {
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++) {
+        if (v & ((1 << P0) | (1 << P1))) continue;
+        if ((v & rcm) != rcm) continue;
+        const int i1 = v | (1 << P1), i2 = v | (1 << P0);
+        swap_inplace(a[i1], a[i2]);
+    }
+}
+
+// Scaled rotation lambda * M on one amplitude pair (x: logical bit 0, y:
+// logical bit 1); the GKind table of lq_internal.h.  4 DFMA (or 4 DADD) per
+// pair; lambda is deferred by the caller.
+template <int GK, bool ALT>
+__device__ __forceinline__ void g_pair(double2 &x, double2 &y, double p) {
+    const double2 X = x, Y = y;
+    if constexpr (GK == GK_REAL) {
+        if constexpr (!ALT) {   // [[1, -p], [p, 1]]
+            x = make_double2(fma(-p, Y.x, X.x), fma(-p, Y.y, X.y));
+            y = make_double2(fma(p, X.x, Y.x), fma(p, X.y, Y.y));
+        } else {                // [[p, -1], [1, p]]
+            x = make_double2(fma(p, X.x, -Y.x), fma(p, X.y, -Y.y));
+            y = make_double2(fma(p, Y.x, X.x), fma(p, Y.y, X.y));
+        }
+    } else if constexpr (GK == GK_IMAG) {
+        if constexpr (!ALT) {   // [[1, -ip], [-ip, 1]]
+            x = make_double2(fma(p, Y.y, X.x), fma(-p, Y.x, X.y));
+            y = make_double2(fma(p, X.y, Y.x), fma(-p, X.x, Y.y));
+        } else {                // [[p, -i], [-i, p]]
+            x = make_double2(fma(p, X.x, Y.y), fma(p, X.y, -Y.x));
+            y = make_double2(fma(p, Y.x, X.y), fma(p, Y.y, -X.x));
+        }
+    } else {                    // [[1, 1], [1, -1]]
+        x = cadd(X, Y);
+        y = csub(X, Y);
+    }
+}
+
+template <int RR, int P, int GK, bool ALT, bool F>
+__device__ __forceinline__ void ap_g_(double2 (&a)[1 << RR], double p) {
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++) {
+        if (v & (1 << P)) continue;
+        const int w = v | (1 << P);
+        if constexpr (!F) g_pair<GK, ALT>(a[v], a[w], p);
+        else g_pair<GK, ALT>(a[w], a[v], p);   // flipped: register w holds logical bit 0
+    }
+}
+
+template <int RR, int P, int GK>
+__device__ __forceinline__ void ap_g(double2 (&a)[1 << RR], const double2 *M, bool f) {
+    const double p = M[0].x;
+    if constexpr (GK == GK_HAD) {
+        if (f) ap_g_<RR, P, GK, false, true>(a, p);
+        else ap_g_<RR, P, GK, false, false>(a, p);
+    } else {
+        if (M[1].x != 0.0) {
+            if (f) ap_g_<RR, P, GK, true, true>(a, p);
+            else ap_g_<RR, P, GK, true, false>(a, p);
+        } else {
+            if (f) ap_g_<RR, P, GK, false, true>(a, p);
+            else ap_g_<RR, P, GK, false, false>(a, p);
+        }
+    }
+}
+
+// Deferred scalars.  The register tile holds
+// psi / (tsc * ph):
+//   tsc (complex) collects factors identical on every thread of the tile --
+//       scaled-rotation lambdas, QFT scales, d0 of register-bit diagonals and
+//       diagonal factors on bits outside the tile -- and may stay pending
+//       across exchanges; it is applied once, before the store;
+//   ph  (complex, unit modulus) collects thread-dependent diagonal factors and
+//       is applied before amplitudes move between threads.
+struct TState {
+    uint32_t fb;       // pending register flip mask
+    bool hph;          // ph != 1
+    double eacc;       // Pauli-group contributions of this thread
+    double2 tsc, ph;
+    double2 ttmax;     // QFT twiddle state of the current sub-block
+    uint64_t lg;
+    __device__ __forceinline__ void reset() {
+        fb = 0;
+        hph = false;
+        eacc = 0.0;
+        tsc = make_double2(1.0, 0.0);
+        ph = make_double2(1.0, 0.0);
+        ttmax = make_double2(1.0, 0.0);
+        lg = 0;
+    }
+};
+
+// apply ph (exchange) or tsc * ph (store) to the register tile
+template <int RR>
+__device__ __forceinline__ void materialize(double2 (&a)[1 << RR], TState &ts, bool with_tsc) {
+    if (with_tsc) {
+        const double2 s = ts.hph ? cmul(ts.tsc, ts.ph) : ts.tsc;
+        if (s.x != 1.0 || s.y != 0.0) {
+            if (s.y == 0.0) {
+#pragma unroll
+                for (int v = 0; v < (1 << RR); v++) a[v] = cscale(a[v], s.x);
+            } else {
+#pragma unroll
+                for (int v = 0; v < (1 << RR); v++) a[v] = cmul(a[v], s);
+            }
+        }
+        ts.tsc = make_double2(1.0, 0.0);
+    } else if (ts.hph) {
+#pragma unroll
+        for (int v = 0; v < (1 << RR); v++) a[v] = cmul(a[v], ts.ph);
+    }
+    ts.ph = make_double2(1.0, 0.0);
+    ts.hph = false;
+}
+
+// QFT stage on register position P (see planner.cpp plan_qft).
+template <int RR, int P>
+__device__ __forceinline__ void ap_qft(double2 (&a)[1 << RR], double2 tt, const double2 *__restrict__ W,
+                                       bool inverse) {
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++) {
+        if (v & (1 << P)) continue;
+        const int w = v | (1 << P);
+        double2 tw = cmul(tt, W[w]);
+        if (!inverse) {
+            double2 u = a[v], x = a[w];
+            a[v] = cadd(u, x);
+            a[w] = cmul(csub(u, x), tw);
+        } else {
+            double2 u = a[v], y = cmul(a[w], tw);
+            a[v] = cadd(u, y);
+            a[w] = csub(u, y);
+        }
+    }
+}
+
+#define LQ_SW4(r, CALL)                         \
+    switch (r) {                                \
+    case 0: CALL(0); break;                     \
+    case 1: if (RR > 1) CALL((RR > 1 ? 1 : 0)); break; \
+    case 2: if (RR > 2) CALL((RR > 2 ? 2 : 0)); break; \
+    case 3: if (RR > 3) CALL((RR > 3 ? 3 : 0)); break; \
+    default: break;                             \
+    }
+
+// QFT thread twiddle exp(+-i pi Lt / 2^j), Lt = logical(gbase) mod 2^j: one
+// sincospi per sub-block (at its largest j), then the exact recurrence
+// tt_{k-1} = tt_k^2 (-1)^{bit k-1 of Lt}.
+__device__ __forceinline__ double2 qft_thread_twiddle(const KOp &op, uint64_t gbase, int n, double2 &ttmax,
+                                                      uint64_t &lg) {
+    const bool inv = op.flags & QF_INVERSE;
+    if (op.flags & QF_HEAD) {
+        const int jm = op.b1;
+        lg = (op.flags & QF_REVERSED) ? (__brevll(gbase) >> (64 - n)) : gbase;
+        const uint64_t Lt = (jm == 0) ? 0ull : (lg & ((1ull << jm) - 1));
+        double s, c;
+        sincospi(ldexp((double)Lt, -jm), &s, &c);
+        ttmax = make_double2(c, inv ? -s : s);
+    }
+    double2 tt = ttmax;
+    for (int k = op.b1; k > op.qj; k--) {
+        tt = cmul(tt, tt);
+        if ((lg >> (k - 1)) & 1) tt = make_double2(-tt.x, -tt.y);
+    }
+    return tt;
+}
+
+template <int RR, int C, int T>
+__device__ __forceinline__ void ap_cx(double2 (&a)[1 << RR]) {
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++) {
+        if ((v & (1 << T)) || !(v & (1 << C))) continue;
+        const int w = v | (1 << T);
+        swap_inplace(a[v], a[w]);
+    }
+}
+
+template <int RR, int C, int T>
+__device__ __forceinline__ void ap_cx_n(double2 (&a)[1 << RR]) {   // control bit sense inverted
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++) {
+        if ((v & (1 << T)) || (v & (1 << C))) continue;
+        const int w = v | (1 << T);
+        swap_inplace(a[v], a[w]);
+    }
+}
+
+// Materialise a pending register flip mask (see apply_ops).
+template <int RR>
+__device__ __forceinline__ void flush_flips(double2 (&a)[1 << RR], uint32_t &fb) {
+    if (fb == 0) return;
+#pragma unroll
+    for (int p = 0; p < RR; p++)
+        if ((fb >> p) & 1) {
+#pragma unroll
+            for (int v = 0; v < (1 << RR); v++)
+                if (!(v & (1 << p))) swap_inplace(a[v], a[v | (1 << p)]);
+        }
+    fb = 0;
+}
+
+// Rare op shapes (register-controlled U1/D1, multi-register controls, U2,
+// D2, SWAP): a switch on the op type.
+template <int RR>
+__device__ __forceinline__ void apply_generic(double2 (&a)[1 << RR], const KOp &op, const double2 *M, uint64_t gbase) {
+    const uint32_t rcm = op.rcm;
+    switch (op.type) {
+    case K_U1: {
+        const double2 u00 = M[0], u01 = M[1], u10 = M[2], u11 = M[3];
+#define CALL_U1(P) ap_u1<RR, P>(a, u00, u01, u10, u11, rcm)
+        LQ_SW4(op.r0, CALL_U1)
+#undef CALL_U1
+        break;
+    }
+    case K_X: {
+#define CALL_X(P) ap_x<RR, P>(a, rcm)
+        LQ_SW4(op.r0, CALL_X)
+#undef CALL_X
+        break;
+    }
+    case K_D1: {
+        const double2 d0 = M[0], d1 = M[1];
+        if (op.r0 != NOREG) {
+#pragma unroll
+            for (int v = 0; v < (1 << RR); v++) {
+                if ((v & rcm) != rcm) continue;
+                a[v] = cmul(a[v], ((v >> op.r0) & 1) ? d1 : d0);
+            }
+        } else {
+            const double2 d = ((gbase >> op.b0) & 1) ? d1 : d0;
+#pragma unroll
+            for (int v = 0; v < (1 << RR); v++) {
+                if ((v & rcm) != rcm) continue;
+                a[v] = cmul(a[v], d);
+            }
+        }
+        break;
+    }
+    case K_D2: {
+        const uint32_t ha = (op.r0 == NOREG) ? (uint32_t)((gbase >> op.b0) & 1) : 0u;
+        const uint32_t hb = (op.r1 == NOREG) ? (uint32_t)((gbase >> op.b1) & 1) : 0u;
+#pragma unroll
+        for (int v = 0; v < (1 << RR); v++) {
+            if ((v & rcm) != rcm) continue;
+            uint32_t ia = (op.r0 == NOREG) ? ha : ((v >> op.r0) & 1);
+            uint32_t ib = (op.r1 == NOREG) ? hb : ((v >> op.r1) & 1);
+            a[v] = cmul(a[v], M[2 * ia + ib]);
+        }
+        break;
+    }
+    case K_U2: {
+        if constexpr (RR >= 2) {
+            const double2 *U = M;   // shared memory: entries are re-read per quad
+            const int code = op.r0 * 4 + op.r1;
+            switch (code) {
+#define CU2(p0, p1) case p0 * 4 + p1: if (RR > p0 && RR > p1) ap_u2<RR, (RR > p0 ? p0 : 0), (RR > p1 ? p1 : 1)>(a, U, rcm); break;
+            CU2(0, 1) CU2(1, 0) CU2(0, 2) CU2(2, 0) CU2(0, 3) CU2(3, 0)
+            CU2(1, 2) CU2(2, 1) CU2(1, 3) CU2(3, 1) CU2(2, 3) CU2(3, 2)
+#undef CU2
+            default: break;
+            }
+        }
+        break;
+    }
+    case K_SWAP: {
+        if constexpr (RR >= 2) {
+            const int lo = op.r0 < op.r1 ? op.r0 : op.r1, hi = op.r0 < op.r1 ? op.r1 : op.r0;
+            const int code = hi * 4 + lo;
+            switch (code) {
+#define CSW(p0, p1) case p0 * 4 + p1: if (RR > p0) ap_swap<RR, (RR > p0 ? p0 : 1), (RR > p0 ? p1 : 0)>(a, rcm); break;
+            CSW(1, 0) CSW(2, 0) CSW(2, 1) CSW(3, 0) CSW(3, 1) CSW(3, 2)
+#undef CSW
+            default: break;
+            }
+        }
+        break;
+    }
+    default:
+        break;
+    }
+}
+
+// Pauli-group expectation on the register tile (SURVEY
+// §8(a) a7).  For the group's x mask X (register positions) and register
+// index v: w_v = conj(a[v ^ X]) a[v]; a term (c, z, y) contributes
+//   c (-1)^{popcount(gbase & znr)} Re[ i^y sum_v chi_zreg(v) w_v ].
+// sum_v chi_p(v) w_v for all 16 patterns p is one Walsh-Hadamard transform
+// of w.  Pairs (v, v ^ X) give conjugate w, so only half are formed.
+template <int RR, int X, bool IM>
+__device__ __forceinline__ void expv_w(const double2 (&a)[1 << RR], double (&w)[1 << RR]) {
+    if constexpr (X == 0) {
+#pragma unroll
+        for (int v = 0; v < (1 << RR); v++) w[v] = IM ? 0.0 : fma(a[v].x, a[v].x, a[v].y * a[v].y);
+    } else {
+        constexpr int lowb = X & -X;
+#pragma unroll
+        for (int v = 0; v < (1 << RR); v++) {
+            if (v & lowb) continue;
+            const double2 p = a[v ^ X], q = a[v];
+            if constexpr (IM) {
+                const double im = fma(p.x, q.y, -p.y * q.x);
+                w[v] = im;
+                w[v ^ X] = -im;
+            } else {
+                const double r = fma(p.x, q.x, p.y * q.y);
+                w[v] = r;
+                w[v ^ X] = r;
+            }
+        }
+    }
+}
+
+template <int RR>
+__device__ __forceinline__ void wht(double (&w)[1 << RR]) {
+#pragma unroll
+    for (int b = 0; b < RR; b++)
+#pragma unroll
+        for (int v = 0; v < (1 << RR); v++) {
+            if (v & (1 << b)) continue;
+            const double x = w[v], y = w[v | (1 << b)];
+            w[v] = x + y;
+            w[v | (1 << b)] = x - y;
+        }
+}
+
+template <int RR>
+__device__ __forceinline__ double pick(const double (&w)[1 << RR], uint32_t p) {
+    double r = 0.0;
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++)
+        if (p == (uint32_t)v) r = w[v];
+    return r;
+}
+
+template <int RR, bool IM>
+__device__ __forceinline__ double expv_part(const double2 (&a)[1 << RR], uint32_t xreg, const ETerm *et, uint32_t nt,
+                                            uint64_t gbase) {
+    double w[1 << RR];
+    switch (xreg) {
+#define EW(X) case X: if constexpr (X < (1 << RR)) expv_w<RR, (X < (1 << RR) ? X : 0), IM>(a, w); break;
+    EW(0) EW(1) EW(2) EW(3) EW(4) EW(5) EW(6) EW(7) EW(8) EW(9) EW(10) EW(11) EW(12) EW(13) EW(14) EW(15)
+#undef EW
+    default: break;
+    }
+    wht<RR>(w);
+    double e = 0.0;
+    uint32_t k = 0;
+    while (k < nt) {
+        const uint32_t z = et[k].zreg;
+        double cz = 0.0;
+        for (; k < nt && et[k].zreg == z; k++) {
+            const ETerm t = et[k];
+            if ((bool)(t.y & 1) != IM) continue;
+            double c = (__popcll(gbase & t.znr) & 1) ? -t.c : t.c;
+            if (t.y & 2) c = -c;
+            cz += IM ? -c : c;   // Re[i w] = -Im w, Re[-i w] = Im w
+        }
+        if (cz != 0.0) e = fma(cz, pick<RR>(w, z), e);
+    }
+    return e;
+}
+
+template <int RR>
+__device__ __forceinline__ double expv_group(const double2 (&a)[1 << RR], uint32_t xreg, const ETerm *et, uint32_t nt,
+                                             uint64_t gbase) {
+    double e = expv_part<RR, false>(a, xreg, et, nt, gbase);
+    bool need_im = false;
+    for (uint32_t k = 0; k < nt; k++) need_im |= (et[k].y & 1);
+    if (need_im) e += expv_part<RR, true>(a, xreg, et, nt, gbase);
+    return e;
+}
+
+// One lowered op with its code known at compile time (the interpreter's
+// switch and the JIT-generated programs both land here).  op.cmask has
+// already been checked by the caller.  Register v holds logical register
+// index v ^ fb: X, and CNOT/CCX whose controls are thread constants, only
+// toggle fb; other ops read logical bit values through it.
+template <int RR, int CODE>
+__device__ __forceinline__ void exec_op(double2 (&a)[1 << RR], const KOp &op, const double2 *M, uint64_t gbase,
+                                        int n, TState &ts, const ETerm *et) {
+    if constexpr (CODE >= C_U1 && CODE < C_U1 + 4) {
+        constexpr int P = CODE - C_U1;
+        if constexpr (RR > P) {
+            const bool f = (ts.fb >> P) & 1;
+            const double2 m00 = M[0], m01 = M[1], m10 = M[2], m11 = M[3];
+            ap_u1<RR, P>(a, f ? m11 : m00, f ? m10 : m01, f ? m01 : m10, f ? m00 : m11, 0u);
+        }
+    } else if constexpr (CODE >= C_X && CODE < C_X + 4) {
+        ts.fb ^= 1u << (CODE - C_X);
+    } else if constexpr (CODE >= C_CX && CODE < C_CX + 16) {
+        constexpr int Cc = (CODE - C_CX) / 4, Tt = (CODE - C_CX) % 4;
+        if constexpr (RR > Cc && RR > Tt && Cc != Tt) {
+            if ((ts.fb >> Cc) & 1) ap_cx_n<RR, Cc, Tt>(a);
+            else ap_cx<RR, Cc, Tt>(a);
+        }
+    } else if constexpr (CODE >= C_D1R && CODE < C_D1R + 4) {
+        // register-bit diagonal: d0 joins a deferred scalar, only the
+        // logical-bit-1 half is multiplied by d1/d0
+        constexpr int P = CODE - C_D1R;
+        if constexpr (RR > P) {
+            const double2 r = M[2];
+            if (op.flags & OF_UNIFORM) ts.tsc = cmul(ts.tsc, M[0]);
+            else { ts.ph = cmul(ts.ph, M[0]); ts.hph = true; }
+            if ((ts.fb >> P) & 1) {
+#pragma unroll
+                for (int v = 0; v < (1 << RR); v++)
+                    if (!(v & (1 << P))) a[v] = cmul(a[v], r);
+            } else {
+#pragma unroll
+                for (int v = 0; v < (1 << RR); v++)
+                    if (v & (1 << P)) a[v] = cmul(a[v], r);
+            }
+        }
+    } else if constexpr (CODE == C_D1T) {   // thread-dependent constant bit: one multiply per thread
+        ts.ph = cmul(ts.ph, ((gbase >> op.b0) & 1) ? M[1] : M[0]);
+        ts.hph = true;
+    } else if constexpr (CODE == C_D1U) {   // bit (and controls) outside the tile: tile-uniform
+        ts.tsc = cmul(ts.tsc, ((gbase >> op.b0) & 1) ? M[1] : M[0]);
+    } else if constexpr (CODE >= C_G && CODE < C_G + 12) {
+        constexpr int GK = (CODE - C_G) / 4, P = (CODE - C_G) % 4;
+        if constexpr (RR > P) {
+            ap_g<RR, P, GK>(a, M, (ts.fb >> P) & 1);
+            ts.tsc = cscale(ts.tsc, M[0].y);
+        }
+    } else if constexpr (CODE >= C_QFT && CODE < C_QFT + 4) {
+        constexpr int P = CODE - C_QFT;
+        if constexpr (RR > P) {
+            flush_flips<RR>(a, ts.fb);
+            const double2 tt = qft_thread_twiddle(op, gbase, n, ts.ttmax, ts.lg);
+            ap_qft<RR, P>(a, tt, M, op.flags & QF_INVERSE);
+        }
+    } else if constexpr (CODE == C_SCALE) {
+        ts.tsc = cscale(ts.tsc, M[0].x);
+    } else if constexpr (CODE == C_EXPV) {
+        flush_flips<RR>(a, ts.fb);
+        // the registers hold psi / (tsc * ph)
+        double sc = fma(ts.tsc.x, ts.tsc.x, ts.tsc.y * ts.tsc.y);
+        if (ts.hph) sc *= fma(ts.ph.x, ts.ph.x, ts.ph.y * ts.ph.y);
+        ts.eacc = fma(sc, expv_group<RR>(a, op.rcm, et + op.mat, op.aux, gbase), ts.eacc);
+    } else {
+        flush_flips<RR>(a, ts.fb);
+        apply_generic<RR>(a, op, M, gbase);
+    }
+}
+
+#define LQ_OP_CODES(X)                                                                                    \
+    X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17)   \
+    X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32) X(33)     \
+    X(34) X(35) X(36) X(37) X(38) X(39) X(40) X(41) X(42) X(43) X(44) X(45) X(46) X(47) X(48)
+
+// The interpreter: walks the sub-block's op list in shared memory.
+struct InterpProg {
+    template <int RR>
+    __device__ __forceinline__ static void run(uint32_t /*sub*/, const KSub &sb, uint32_t op0, double2 (&a)[1 << RR],
+                                               const KOp *ops, uint64_t gbase, int n, const double2 *tab,
+                                               TState &ts, const ETerm *et) {
+        ts.ttmax = make_double2(1.0, 0.0);
+        ts.lg = 0;
+        for (uint32_t oi = sb.op_begin - op0; oi < sb.op_end - op0; oi++) {
+            const KOp op = ops[oi];
+            if (op.cmask && (gbase & op.cmask) != op.cmask) continue;
+            const double2 *M = tab + op.aux;
+            switch (op.code) {
+#define LQ_CASE(c) case c: exec_op<RR, c>(a, op, M, gbase, n, ts, et); break;
+                LQ_OP_CODES(LQ_CASE)
+#undef LQ_CASE
+            default: break;
+            }
+        }
+    }
+};
+
+template <int RR>
+__device__ __forceinline__ uint32_t smask(const uint8_t *S) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < RR; i++) m |= 1u << S[i];
+    return m;
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// Persistent tile kernel.  One CTA per SM walks the
+// tiles of all circuits of the launch (tile g = circuit * tiles_per_circ +
+// tile).  While it computes tile i out of shared buffer i&1 it streams tile
+// i+1 into the other buffer with cp.async (LDGSTS), so HBM reads overlap the
+// FP64 work; results go back to HBM with plain 16-byte stores.
+// Shared memory: [buf0 2^K][buf1 2^K][staged op tables][ops]...
+// Prog executes the ops of one sub-block: InterpProg (op list in shared
+// memory) or a JIT-generated straight-line program (jit.cpp).
+#define LQ_TILE_PARAMS                                                                                   \
+    const __grid_constant__ lq::KPass P, const lq::KSub *__restrict__ subs, const lq::KOp *__restrict__ ops, \
+        const lq::KPerm *__restrict__ perms, const lq::KPermTerm *__restrict__ pterms,                      \
+        const lq::ETerm *__restrict__ eterms, const double2 *__restrict__ mats, uint64_t mat_stride,        \
+        const double2 *__restrict__ cst, double2 *__restrict__ state, uint64_t state_stride,                 \
+        uint32_t tiles_log2, uint32_t total_tiles, double *__restrict__ partials, uint64_t slot_stride
+#define LQ_TILE_ARGS \
+    P, subs, ops, perms, pterms, eterms, mats, mat_stride, cst, state, state_stride, tiles_log2, total_tiles, partials, slot_stride
+
+template <int RR, class Prog>
+__device__ __forceinline__ void tile_body(const KPass &P, const KSub *__restrict__ subs,
+                                          const KOp *__restrict__ ops, const KPerm *__restrict__ perms,
+                                          const KPermTerm *__restrict__ pterms, const ETerm *__restrict__ eterms,
+                                          const double2 *__restrict__ mats,
+                                          uint64_t mat_stride, const double2 *__restrict__ cst,
+                                          double2 *__restrict__ state, uint64_t state_stride,
+                                          uint32_t tiles_log2, uint32_t total_tiles,
+                                          double *__restrict__ partials, uint64_t slot_stride) {
+    extern __shared__ double2 sm[];
+    constexpr int NV = 1 << RR;
+    const int K = P.K;
+    const uint32_t TS = 1u << K;
+    const uint32_t NT = 1u << (K - RR);
+    const uint32_t t = threadIdx.x;
+    double2 *s_tab = sm + 2 * TS;
+    KOp *s_ops = reinterpret_cast<KOp *>(s_tab + P.smat);
+    const uint32_t nops = P.op_end - P.op_begin;
+    const uint32_t nperm = P.perm_end - P.perm_begin;
+    KPerm *s_perm = reinterpret_cast<KPerm *>(s_ops + nops);
+    const uint32_t pt0 = nperm ? perms[P.perm_begin].term_begin : 0;
+    const uint32_t npt = nperm ? perms[P.perm_end - 1].term_end - pt0 : 0;
+    KPermTerm *s_pt = reinterpret_cast<KPermTerm *>(s_perm + nperm);
+    uint64_t *s_dlo = reinterpret_cast<uint64_t *>(s_pt + npt);
+    uint64_t *s_dhi = s_dlo + 256;
+    KSub *s_sub = reinterpret_cast<KSub *>(s_dhi + 32);
+    const uint32_t nsub = P.sub_end - P.sub_begin;
+    const uint32_t net = P.eterm_end - P.eterm_begin;
+    ETerm *s_et = reinterpret_cast<ETerm *>(s_sub + nsub + (nsub & 1));   // 8-byte aligned
+    for (uint32_t k = threadIdx.x; k < net; k += blockDim.x) s_et[k] = eterms[P.eterm_begin + k];
+    const bool zero = P.flags & PF_LOAD_ZERO;
+    for (uint32_t k = threadIdx.x; k < 256 + 32; k += blockDim.x) {
+        uint64_t g = 0;
+        const uint32_t l = k < 256 ? k : (k - 256) << 8;
+        for (int i = 0; i < K; i++)
+            if ((l >> i) & 1) g |= 1ull << P.T[i];
+        s_dlo[k] = g;   // s_dhi = s_dlo + 256
+    }
+    for (uint32_t k = threadIdx.x; k < P.sub_end - P.sub_begin; k += blockDim.x) s_sub[k] = subs[P.sub_begin + k];
+    for (uint32_t k = threadIdx.x; k < nperm; k += blockDim.x) s_perm[k] = perms[P.perm_begin + k];
+    for (uint32_t k = threadIdx.x; k < npt; k += blockDim.x) s_pt[k] = pterms[pt0 + k];
+    // translation of an entry permutation for this tile
+    auto binv_of = [&](int pi, uint64_t tb) {
+        uint32_t b = 0;
+        const KPerm &pm = s_perm[pi];
+        for (uint32_t k = pm.term_begin - pt0; k < pm.term_end - pt0; k++)
+            if ((tb & s_pt[k].cmask) == s_pt[k].cmask) b ^= s_pt[k].vec;
+        return b;
+    };
+
+    // this thread's copy slots: local index l = t + v * NT (top RR bits = v)
+    uint64_t dep_t = 0;
+    for (int i = 0; i < K - RR; i++)
+        if ((t >> i) & 1) dep_t |= 1ull << P.T[i];
+    const uint32_t sw_t = swz(t);
+
+    auto tile_base = [&](uint32_t g) {
+        uint64_t tb = g & ((1u << tiles_log2) - 1);
+        for (int i = 0; i < K; i++) tb = insert_zero64(tb, P.T[i]);
+        return tb;
+    };
+    auto issue = [&](uint32_t g, double2 *buf) {
+        const double2 *psi = state + (uint64_t)(g >> tiles_log2) * state_stride + tile_base(g) + dep_t;
+        Unroll<RR>::run([&](auto V) {
+            constexpr int v = decltype(V)::value;
+            uint64_t o = 0;
+#pragma unroll
+            for (int i = 0; i < RR; i++)
+                if (v & (1 << i)) o |= 1ull << P.T[K - RR + i];
+            cp_async16(buf + (sw_t ^ swz((uint32_t)v * NT)), psi + o);
+        });
+    };
+
+    uint32_t g = blockIdx.x;
+    if (g >= total_tiles) return;
+    if (!zero) issue(g, sm);
+    cp_async_commit();
+    int cur_circ = -1;
+    for (uint32_t i = 0; g < total_tiles; i++, g += gridDim.x) {
+        const uint32_t gn = g + gridDim.x;
+        double2 *b = sm + (i & 1) * TS;
+        if (gn < total_tiles && !zero) issue(gn, sm + ((i + 1) & 1) * TS);
+        cp_async_commit();
+        const int circ = (int)(g >> tiles_log2);
+        if (circ != cur_circ) {   // (re)stage the ops and this circuit's matrices
+            const double2 *M = mats + (uint64_t)circ * mat_stride;
+            for (uint32_t k = t; k < nops; k += blockDim.x) {
+                const KOp o = ops[P.op_begin + k];
+                s_ops[k] = o;
+                const int sz = op_table_size(o.type);
+                const double2 *src = ((o.type == K_QFT || o.type == K_SCALE) ? cst : M) + o.mat;
+                for (int e = 0; e < sz; e++) s_tab[o.aux + e] = src[e];
+            }
+            cur_circ = circ;
+        }
+        cp_async_wait1();
+        __syncthreads();
+
+        const uint64_t tb = tile_base(g);
+        double2 a[NV];
+        Mapping<RR> cur;
+        KSub sb = s_sub[0];
+        cur.make(t, sb.S, s_dlo, s_dhi, tb);
+        uint32_t cur_m = smask<RR>(sb.S);
+        // registers <- buffer (through the entry permutation, if any)
+        auto load_regs = [&](int perm, const uint8_t *S) {
+            if (perm >= 0) {
+                PermSlots<RR> ps;
+                ps.make(cur, S, K, s_perm[perm], binv_of(perm, tb));
+                Unroll<RR>::run([&](auto V) { a[decltype(V)::value] = b[ps.template sidx<decltype(V)::value>()]; });
+            } else {
+                Unroll<RR>::run([&](auto V) { a[decltype(V)::value] = b[cur.template sidx<decltype(V)::value>()]; });
+            }
+        };
+        if (zero) {   // |0...0>: amplitude 1 where the source position is local 0 of tile 0
+            if (sb.perm >= 0) {
+                PermSlots<RR> ps;
+                ps.make(cur, sb.S, K, s_perm[sb.perm], binv_of(sb.perm, tb));
+                Unroll<RR>::run([&](auto V) {
+                    a[decltype(V)::value] = make_double2((tb == 0 && ps.template sidx<decltype(V)::value>() == 0) ? 1.0 : 0.0, 0.0);
+                });
+            } else {
+                Unroll<RR>::run([&](auto V) {
+                    a[decltype(V)::value] = make_double2((tb == 0 && cur.template sidx<decltype(V)::value>() == 0) ? 1.0 : 0.0, 0.0);
+                });
+            }
+        } else {
+            load_regs(sb.perm, sb.S);
+        }
+        TState ts;
+        ts.reset();
+        for (uint32_t s = P.sub_begin; s < P.sub_end; s++) {
+            if (s != P.sub_begin) {
+                sb = s_sub[s - P.sub_begin];
+                const uint32_t m = smask<RR>(sb.S);
+                if (m != cur_m || sb.perm >= 0) {
+                    materialize<RR>(a, ts, false);
+                    __syncthreads();   // everyone has read the previous mapping's slots
+                    const uint32_t adj = cur.soff_dyn(ts.fb);
+                    Unroll<RR>::run([&](auto V) { b[cur.template sidx<decltype(V)::value>() ^ adj] = a[decltype(V)::value]; });
+                    ts.fb = 0;
+                    __syncthreads();
+                    cur.make(t, sb.S, s_dlo, s_dhi, tb);
+                    cur_m = m;
+                    load_regs(sb.perm, sb.S);
+                }
+            }
+            Prog::template run<RR>(s - P.sub_begin, sb, P.op_begin, a, s_ops, cur.gt, P.n, s_tab, ts, s_et);
+        }
+        double2 *psi = state + (uint64_t)circ * state_stride;
+        if (P.flags & PF_EXPV) {   // one deterministic partial per tile
+            __syncthreads();       // all reads of b done: reuse it as reduction scratch
+            const double r = block_sum(ts.eacc, reinterpret_cast<double *>(b));
+            if (t == 0) partials[(uint64_t)circ * slot_stride + P.eslot + (g & ((1u << tiles_log2) - 1))] = r;
+        }
+        if (P.flags & PF_NO_STORE) {
+            __syncthreads();
+            continue;
+        }
+        materialize<RR>(a, ts, true);
+        const uint32_t ms = smask<RR>(P.Sstore);
+        // a non-zero flip mask would scatter the lanes of each store: go
+        // through shared memory (collective decision: the exchange syncs)
+        if (__syncthreads_or(ms != cur_m || ts.fb != 0 || P.store_perm >= 0)) {
+            const uint32_t adj = cur.soff_dyn(ts.fb);
+            Unroll<RR>::run([&](auto V) { b[cur.template sidx<decltype(V)::value>() ^ adj] = a[decltype(V)::value]; });
+            ts.fb = 0;
+            __syncthreads();
+            cur.make(t, P.Sstore, s_dlo, s_dhi, tb);
+            load_regs(P.store_perm, P.Sstore);
+        }
+        Unroll<RR>::run([&](auto V) {
+            psi[cur.gt + cur.template goff<decltype(V)::value>()] = a[decltype(V)::value];
+        });
+        __syncthreads();   // buffer b is refilled by the next iteration's prefetch
+    }
+}
+
+
+
+// ---------------------------------------------------------------- static skeleton (JIT)
+// tile_body_static<RR, D, Prog> is tile_body with the pass's layout known at
+// compile time.  D (generated by jit.cpp) holds K, NSUB; SM[s] = local
+// register-bit mask of sub-block s; PERM[s] = entry permutation (-1: none);
+// SSTORE, STORE_PERM; and generated functions dep(l) (local index ->
+// physical bits), tbase(g) (tile index -> the physical bits outside the
+// tile), ainv<p>(l) and binv<p>(tile base) (permutation p's inverse map and
+// its tile-dependent translation).  Every shared-memory slot offset and global offset
+// of a register then folds to a constant; per tile only the tile base, one
+// XOR per register access and one add per global address remain.
+__host__ __device__ constexpr int nth_set_bit(uint32_t m, int i) {
+    for (int b = 0; b < 32; b++)
+        if ((m >> b) & 1) {
+            if (i == 0) return b;
+            i--;
+        }
+    return 0;
+}
+template <uint32_t SMm>
+__host__ __device__ constexpr uint32_t loff_c(uint32_t v) {   // register index -> local offset
+    uint32_t o = 0;
+    for (int i = 0; i < 4; i++)
+        if ((v >> i) & 1) o |= 1u << nth_set_bit(SMm, i);
+    return o;
+}
+template <uint32_t SMm, int K>
+__device__ __forceinline__ uint32_t ins_zeros(uint32_t t) {   // thread -> local index of register 0
+#pragma unroll
+    for (int b = 0; b < K; b++)
+        if ((SMm >> b) & 1) t = ((t >> b) << (b + 1)) | (t & ((1u << b) - 1u));
+    return t;
+}
+// registers -> shared slots of mapping SMm (pending flips folded into the address)
+template <int RR, int K, uint32_t SMm>
+__device__ __forceinline__ void xwrite_c(double2 *b, const double2 (&a)[1 << RR], uint32_t t, uint32_t fb) {
+    const uint32_t slt = swz(ins_zeros<SMm, K>(t));
+    uint32_t adj = 0;
+#pragma unroll
+    for (int i = 0; i < RR; i++)
+        if ((fb >> i) & 1) adj ^= swz(1u << nth_set_bit(SMm, i));
+    const uint32_t base = slt ^ adj;
+    Unroll<RR>::run([&](auto V) {
+        constexpr uint32_t so = swz(loff_c<SMm>(decltype(V)::value));
+        b[base ^ so] = a[decltype(V)::value];
+    });
+}
+// shared slots -> registers of mapping SMm, through entry permutation PI
+// (ZERO: synthesise |0...0> -- amplitude 1 at position 0 of tile 0)
+template <int RR, class D, uint32_t SMm, int PI, bool ZERO>
+__device__ __forceinline__ void xread_c(const double2 *b, double2 (&a)[1 << RR], uint32_t t, uint64_t tb) {
+    const uint32_t lt = ins_zeros<SMm, D::K>(t);
+    if constexpr (PI < 0) {
+        const uint32_t base = swz(lt);
+        Unroll<RR>::run([&](auto V) {
+            constexpr uint32_t so = swz(loff_c<SMm>(decltype(V)::value));
+            if constexpr (ZERO) a[decltype(V)::value] = make_double2((tb == 0 && (base ^ so) == 0) ? 1.0 : 0.0, 0.0);
+            else a[decltype(V)::value] = b[base ^ so];
+        });
+    } else {
+        const uint32_t base = swz(D::template ainv<PI>(lt) ^ D::template binv<PI>(tb));
+        Unroll<RR>::run([&](auto V) {
+            constexpr uint32_t so = swz(D::template ainv<PI>(loff_c<SMm>(decltype(V)::value)));
+            if constexpr (ZERO) a[decltype(V)::value] = make_double2((tb == 0 && (base ^ so) == 0) ? 1.0 : 0.0, 0.0);
+            else a[decltype(V)::value] = b[base ^ so];
+        });
+    }
+}
+
+template <int RR, class D, class Prog, int S>
+__device__ __forceinline__ void run_subs_c(double2 (&a)[1 << RR], double2 *b, TState &ts, uint64_t tb, uint32_t t,
+                                           const double2 *tab, const ETerm *et, int n) {
+    if constexpr (S < D::NSUB) {
+        if constexpr (S > 0 && (D::SM[S] != D::SM[S - 1] || D::PERM[S] >= 0)) {
+            materialize<RR>(a, ts, false);
+            __syncthreads();   // everyone has read the previous mapping's slots
+            xwrite_c<RR, D::K, D::SM[S - 1]>(b, a, t, ts.fb);
+            ts.fb = 0;
+            __syncthreads();
+            xread_c<RR, D, D::SM[S], D::PERM[S], false>(b, a, t, tb);
+        }
+        const uint64_t gbase = tb | D::dep(ins_zeros<D::SM[S], D::K>(t));
+        Prog::template run<S, RR>(a, gbase, n, tab, ts, et);
+        run_subs_c<RR, D, Prog, S + 1>(a, b, ts, tb, t, tab, et, n);
+    }
+}
+
+template <int RR, class D, class Prog>
+__device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__restrict__ ops,
+                                                 const ETerm *__restrict__ eterms, const double2 *__restrict__ mats,
+                                                 uint64_t mat_stride, const double2 *__restrict__ cst,
+                                                 double2 *__restrict__ state, uint64_t state_stride,
+                                                 uint32_t tiles_log2, uint32_t total_tiles,
+                                                 double *__restrict__ partials, uint64_t slot_stride) {
+    extern __shared__ double2 sm[];
+    constexpr int K = D::K;
+    constexpr int NV = 1 << RR;
+    constexpr uint32_t TS = 1u << K;
+    constexpr uint32_t NT = 1u << (K - RR);
+    constexpr int LAST = D::NSUB - 1;
+    const uint32_t t = threadIdx.x;
+    double2 *s_tab = sm + 2 * TS;
+    ETerm *s_et = reinterpret_cast<ETerm *>(s_tab + P.smat);
+    const uint32_t nops = P.op_end - P.op_begin;
+    const uint32_t net = P.eterm_end - P.eterm_begin;
+    for (uint32_t k = t; k < net; k += blockDim.x) s_et[k] = eterms[P.eterm_begin + k];
+    const bool zero = P.flags & PF_LOAD_ZERO;
+    const uint64_t dep_t = D::dep(t);
+    const uint32_t sw_t = swz(t);
+    const uint32_t tmask = (1u << tiles_log2) - 1u;
+    auto issue = [&](uint32_t g, double2 *buf) {
+        const double2 *psi = state + (uint64_t)(g >> tiles_log2) * state_stride + D::tbase(g & tmask) + dep_t;
+        Unroll<RR>::run([&](auto V) {
+            constexpr uint32_t l = (uint32_t)decltype(V)::value * NT;
+            constexpr uint64_t o = D::dep(l);
+            cp_async16(buf + (sw_t ^ swz(l)), psi + o);
+        });
+    };
+    uint32_t g = blockIdx.x;
+    if (g >= total_tiles) return;
+    if (!zero) issue(g, sm);
+    cp_async_commit();
+    int cur_circ = -1;
+    for (uint32_t i = 0; g < total_tiles; i++, g += gridDim.x) {
+        const uint32_t gn = g + gridDim.x;
+        double2 *b = sm + (i & 1) * TS;
+        if (gn < total_tiles && !zero) issue(gn, sm + ((i + 1) & 1) * TS);
+        cp_async_commit();
+        const int circ = (int)(g >> tiles_log2);
+        if (circ != cur_circ) {   // (re)stage this circuit's op tables
+            const double2 *M = mats + (uint64_t)circ * mat_stride;
+            for (uint32_t k = t; k < nops; k += blockDim.x) {
+                const KOp o = ops[P.op_begin + k];
+                const int sz = op_table_size(o.type);
+                const double2 *src = ((o.type == K_QFT || o.type == K_SCALE) ? cst : M) + o.mat;
+                for (int e = 0; e < sz; e++) s_tab[o.aux + e] = src[e];
+            }
+            cur_circ = circ;
+        }
+        cp_async_wait1();
+        __syncthreads();
+
+        const uint64_t tb = D::tbase(g & tmask);
+        double2 a[NV];
+        if (zero) xread_c<RR, D, D::SM[0], D::PERM[0], true>(b, a, t, tb);
+        else xread_c<RR, D, D::SM[0], D::PERM[0], false>(b, a, t, tb);
+        TState ts;
+        ts.reset();
+        run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, t, s_tab, s_et, P.n);
+        double2 *psi = state + (uint64_t)circ * state_stride;
+        if (P.flags & PF_EXPV) {   // one deterministic partial per tile
+            __syncthreads();
+            const double r = block_sum(ts.eacc, reinterpret_cast<double *>(b));
+            if (t == 0) partials[(uint64_t)circ * slot_stride + P.eslot + (g & tmask)] = r;
+        }
+        if (P.flags & PF_NO_STORE) {
+            __syncthreads();
+            continue;
+        }
+        materialize<RR>(a, ts, true);
+        constexpr bool need_x = D::SSTORE != D::SM[LAST] || D::STORE_PERM >= 0;
+        bool ex = need_x;
+        if constexpr (!need_x) ex = __syncthreads_or(ts.fb != 0);
+        if (ex) {
+            if constexpr (need_x) __syncthreads();
+            xwrite_c<RR, K, D::SM[LAST]>(b, a, t, ts.fb);
+            __syncthreads();
+            xread_c<RR, D, D::SSTORE, D::STORE_PERM, false>(b, a, t, tb);
+        }
+        const uint64_t gst = tb | D::dep(ins_zeros<D::SSTORE, K>(t));
+        Unroll<RR>::run([&](auto V) {
+            constexpr uint64_t go = D::dep(loff_c<D::SSTORE>(decltype(V)::value));
+            psi[gst + go] = a[decltype(V)::value];
+        });
+        __syncthreads();   // buffer b is refilled by the next iteration's prefetch
+    }
+}
+
+template <int RR>
+__global__ void __launch_bounds__(RR >= 4 ? 256 : 512, 1) k_tile(LQ_TILE_PARAMS) {
+    tile_body<RR, InterpProg>(LQ_TILE_ARGS);
+}
+
+}  // namespace lq

@@ -35,7 +35,8 @@ STATUS_NAMES = {0: "LQ_OK", -1: "LQ_ERR_ARG", -2: "LQ_ERR_OOM", -3: "LQ_ERR_CUDA
 KIND_NAMES = ["H", "X", "Y", "Z", "S", "SDG", "T", "TDG", "RX", "RY", "RZ", "CNOT", "CZ", "CP",
               "SWAP", "U1", "U2", "CRY", "CCX", "RXX", "RYY", "RZZ"]
 KINDS = {k: i for i, k in enumerate(KIND_NAMES)}
-LQ_OPT_FUSION, LQ_OPT_TILE_BITS, LQ_OPT_COALESCE_BITS, LQ_OPT_REG_BITS, LQ_OPT_KERNEL_TIMING = 0, 1, 2, 3, 4
+LQ_OPT_FUSION, LQ_OPT_TILE_BITS, LQ_OPT_COALESCE_BITS, LQ_OPT_REG_BITS, LQ_OPT_KERNEL_TIMING, LQ_OPT_JIT = \
+    0, 1, 2, 3, 4, 5
 KC_TILE, KC_PAIR, KC_DIAG, KC_PAULI, KC_OTHER = 0, 1, 2, 3, 4
 
 
@@ -95,6 +96,8 @@ _SIGS = {
     "lq_plan_describe": ([_i32, _GP, _sz, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.c_char_p, _sz], _i32),
     "lq_launch_count": ([], _u64),
     "lq_plan_export_json": ([_i32, _GP, _sz, _TP, _sz, ctypes.c_char_p, _sz, ctypes.POINTER(_sz)], _i32),
+    "lq_jit_stats": ([ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_dbl)], _i32),
+    "lq_jit_compile_check": ([_i32, _GP, _sz, _TP, _sz, ctypes.POINTER(_u64)], _i32),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -355,6 +358,22 @@ def lq_plan_export_json(n_qubits: int, gates, terms=()) -> dict:
     buf = ctypes.create_string_buffer(need.value)
     _chk(_lib.lq_plan_export_json(n_qubits, ga.ptr, ga.n, ta.ptr, ta.n, buf, len(buf), ctypes.byref(need)))
     return json.loads(buf.value.decode())
+
+
+def lq_jit_stats() -> Tuple[int, int, float]:
+    """(pass kernels compiled, cache hits, compile seconds) of this process."""
+    c, h, t = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_double()
+    _chk(_lib.lq_jit_stats(ctypes.byref(c), ctypes.byref(h), ctypes.byref(t)))
+    return c.value, h.value, t.value
+
+
+def lq_jit_compile_check(n_qubits: int, gates, terms=()) -> int:
+    """Host-only: NVRTC-compile the plan's JIT pass programs (no device)."""
+    ga = gates if isinstance(gates, GateArray) else GateArray(gates)
+    ta = terms if isinstance(terms, TermArray) else TermArray(terms)
+    nk = ctypes.c_uint64()
+    _chk(_lib.lq_jit_compile_check(n_qubits, ga.ptr, ga.n, ta.ptr, ta.n, ctypes.byref(nk)))
+    return nk.value
 
 
 # ---- convenience: a torch-owned state ---------------------------------------

@@ -14,9 +14,11 @@ import math
 import numpy as np
 
 NOREG = 255
-K_U1, K_D1, K_X, K_U2, K_D2, K_SWAP, K_QFT, K_SCALE, K_EXPV = range(9)
+K_U1, K_D1, K_X, K_U2, K_D2, K_SWAP, K_QFT, K_SCALE, K_EXPV, K_G = range(10)
+GK_REAL, GK_IMAG, GK_HAD = range(3)
+FK_YDIAG = 100
 PASS_TILE, PASS_PAIR, PASS_DIAG = 0, 1, 2
-MF_U2x2, MF_DIAG2, MF_U4x4, MF_DIAG4 = range(4)
+MF_U2x2, MF_DIAG2, MF_U4x4, MF_DIAG4, MF_G = range(5)
 PF_EXPV, PF_NO_STORE = 2, 4
 QF_INVERSE, QF_REVERSED = 1, 2
 # lq_kind numbering
@@ -34,6 +36,8 @@ def _gate2(kind, th, cst):
            LQ_RZ: [[c - 1j * s, 0], [0, c + 1j * s]], LQ_CP: [[1, 0], [0, complex(math.cos(th), math.sin(th))]]}
     if kind == LQ_U1:
         return np.array(cst, np.complex128).reshape(2, 2)
+    if kind == FK_YDIAG:
+        return np.array([[1j, 0], [0, -1j]], np.complex128)
     return np.array(tab[kind], np.complex128)
 
 
@@ -61,7 +65,15 @@ def build_mats(plan, theta, shift=None):
             if form == MF_U2x2:
                 mats[out:out + 4] = A.reshape(-1)
             else:
-                mats[out:out + 2] = [A[0, 0], A[1, 1]]
+                mats[out:out + 3] = [A[0, 0], A[1, 1], A[1, 1] / A[0, 0]]
+        elif form == MF_G:
+            # the op's exact matrix; _apply_op expands (p, lambda, variant)
+            f = fac[fb]
+            if f[0] == LQ_H:
+                mats[out:out + 2] = [0.7071067811865476j, 0]
+            else:
+                c, s = math.cos(angle(f) / 2), math.sin(angle(f) / 2)
+                mats[out:out + 2] = [complex(s / c, c), 0] if abs(c) >= abs(s) else [complex(c / s, s), 1]
         else:
             f = fac[fb]
             th = angle(f)
@@ -103,7 +115,18 @@ def _apply_op(x, g, op, S, mats, cstc, n, et_all, et0):
     """One lowered op on a tile vector x (index = local l), g = global index."""
     typ = op["type"]
     lb = lambda r: 1 << S[r]
-    M = mats[op["mat"]:op["mat"] + 16] if typ in (K_U1, K_D1, K_U2, K_D2) else None
+    M = mats[op["mat"]:op["mat"] + 16] if typ in (K_U1, K_D1, K_U2, K_D2, K_G) else None
+    if typ == K_G:   # lambda * M (lq_internal.h GKind)
+        p, lam, alt = M[0].real, M[0].imag, M[1].real != 0
+        one, off = (p, 1.0) if alt else (1.0, p)
+        gk = op["qj"]
+        if gk == GK_REAL:
+            M = lam * np.array([one, -off, off, one], np.complex128)
+        elif gk == GK_IMAG:
+            M = lam * np.array([one, -1j * off, -1j * off, one], np.complex128)
+        else:
+            M = lam * np.array([1, 1, 1, -1], np.complex128)
+        typ = K_U1
     L = np.arange(x.size, dtype=np.int64)
     ok = np.ones(x.size, bool)
     for r in range(4):
@@ -193,9 +216,9 @@ def run(plan, psi, theta=None, shift=None):
                 # physical form: b0/b1 are bits, controls in cmask
                 S_phys = [op["b0"], op["b1"], 0, 0]
                 op2 = dict(op)
-                if op["type"] in (K_U1, K_X, K_U2, K_SWAP):
+                if op["type"] in (K_U1, K_X, K_U2, K_SWAP, K_G):
                     op2["r0"], op2["r1"] = 0, 1
-                _apply_op(psi, gidx, op2 if op["type"] in (K_U1, K_X, K_U2, K_SWAP) else op,
+                _apply_op(psi, gidx, op2 if op["type"] in (K_U1, K_X, K_U2, K_SWAP, K_G) else op,
                           S_phys, mats, cstc, n, et_all, 0)
             continue
         T = p["T"]
