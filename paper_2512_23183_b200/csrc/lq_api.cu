@@ -289,7 +289,14 @@ lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, cons
     const uint32_t tiles_log2 = (uint32_t)(kp.n - kp.K);
     const uint64_t total = (uint64_t)n_circ << tiles_log2;
     if (total >= (1ull << 32)) return fail(LQ_ERR_DIM, "too many tiles in one launch");
-    const unsigned grid = (unsigned)std::min<uint64_t>(total, (uint64_t)n_sm);
+    // persistent grid: as many CTAs as fit on every SM (2 per SM for K <= 11)
+    int per_sm = 1;
+    const void *fn = jk ? jk : (const void *)k_tile<RR>;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 1 << (kp.K - RR), smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    const unsigned grid = (unsigned)std::min<uint64_t>(total, (uint64_t)n_sm * (uint64_t)per_sm);
     LaunchTimer lt_(KC_TILE, st);
     if ((kp.flags & PF_EXPV) && !partials) return fail(LQ_ERR_STATE, "expectation pass without partial buffer");
     if (jk) {   // JIT-specialised program of this pass (jit.h): same parameters as k_tile

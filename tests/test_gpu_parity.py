@@ -33,6 +33,7 @@ def _restore_options(lq):
     lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 0)
     lq.lq_set_option(lq.LQ_OPT_COALESCE_BITS, 3)
     lq.lq_set_option(lq.LQ_OPT_REG_BITS, 4)
+    lq.lq_set_option(lq.LQ_OPT_JIT, 1)
 
 
 def grad_close(g, go):
