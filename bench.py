@@ -254,9 +254,11 @@ def run_ours(args):
     value = updates_per_step * args.steps / (ms_max / 1e3)
 
     # roofline of the dominant kernel on this rank: algorithmic bytes / event time.
-    # Each circuit streams the state through `tile_passes` tile passes; the
-    # first one synthesises |0...0> (16 B/amp write), the others read+write (32 B/amp).
-    alg_bytes = args.steps * n_circ * (1 << n) * 16 * (2 * tile_passes - 1)
+    # Each circuit streams the state through `tile_passes` tile passes: 16 B/amp
+    # per load and per store; the first pass synthesises |0...0> (no load),
+    # read-only and final passes skip the store (lq_psr_traffic, exact per plan).
+    tile_bytes_circ, _other = lq.lq_psr_traffic(plan)
+    alg_bytes = args.steps * n_circ * tile_bytes_circ
     peak, peak_src = peaks()
     achieved = alg_bytes / (tile_ms / 1e3) / 1e9 if tile_ms > 0 else None
     tr = ncu_traffic()
@@ -305,7 +307,8 @@ def run_ours(args):
         dist.all_reduce(dtt, op=dist.ReduceOp.MAX)
     dt = float(dtt[0])
     e2e_value = updates_per_step * e2e_steps / dt
-    h2d = 8 * P + plan_bytes + (8 * P if world > 1 else 0)
+    # theta in; the plan is built and uploaded once (lq_param_shift_grad's plan cache, warm-up call)
+    h2d = 8 * P + (8 * P if world > 1 else 0)
     d2h = 8 * P + 8 + (8 * P if world > 1 else 0)
     g_e2e = g_pin.numpy().copy()
     if not np.allclose(g_e2e, g_check, rtol=0, atol=1e-12):

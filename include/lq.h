@@ -188,6 +188,11 @@ lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gate
                               int shard_rank, int shard_world, void *cuda_stream,
                               double *grad_out, double *energy_out);
 
+/* lq_param_shift_grad keeps the plans (and device buffers) of its two most
+ * recent distinct (circuit, Hamiltonian, shard, stream, options) arguments
+ * and reuses them; this frees them. */
+lq_status lq_psr_cache_clear(void);
+
 /* Same computation split into a reusable plan and an asynchronous run on
  * DEVICE pointers (theta_dev: n_params doubles; grad_dev: n_params doubles;
  * energy_dev: 1 double or NULL).  lq_psr_run does not sync. */
@@ -201,6 +206,13 @@ lq_status lq_psr_free(lq_psr *plan);
  * per circuit.  Any output pointer may be NULL. */
 lq_status lq_psr_stats(const lq_psr *plan, uint64_t *n_circuits, uint64_t *n_launches, uint64_t *plan_bytes,
                        uint64_t *tile_passes);
+/* Algorithmic HBM bytes ONE circuit of the plan moves: through tile passes
+ * (16 B/amp per load, 16 B/amp per store; the first pass synthesises
+ * |0...0> without a load, read-only and final passes skip the store) and
+ * through other kernels (pair/diag passes, wide Pauli groups).  Either
+ * pointer may be NULL.  This is the numerator of the roofline bench.py
+ * reports. */
+lq_status lq_psr_traffic(const lq_psr *plan, uint64_t *tile_bytes_per_circuit, uint64_t *other_bytes_per_circuit);
 
 /* ---- execution options (testing / measurement) -------------------------- */
 typedef enum {

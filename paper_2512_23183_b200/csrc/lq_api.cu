@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstddef>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1023,6 +1025,32 @@ lq_status lq_psr_stats(const lq_psr *P, uint64_t *n_circuits, uint64_t *n_launch
     return LQ_OK;
 }
 
+lq_status lq_psr_traffic(const lq_psr *P, uint64_t *tile_bytes_per_circuit, uint64_t *direct_bytes_per_circuit) {
+    if (!P) return fail(LQ_ERR_ARG, "invalid plan");
+    // algorithmic HBM bytes of one circuit, as launch_passes runs it: the
+    // first tile pass synthesises |0...0> (write only), read-only passes and
+    // the final pass (when no wide Pauli group reads the state afterwards)
+    // skip the store; every other pass reads and writes 16 B per amplitude.
+    const uint64_t N = 1ull << P->n;
+    uint64_t tb = 0, other = 0;
+    const size_t np = P->plan.passes.size();
+    for (size_t i = 0; i < np; i++) {
+        const PlanPass &p = P->plan.passes[i];
+        bool load = !(i == 0 && p.kind == PASS_TILE);
+        bool store = true;
+        if (p.kind == PASS_TILE) {
+            if (p.kp.flags & PF_NO_STORE) store = false;
+            if (i + 1 == np && P->dset.ds.empty()) store = false;
+        }
+        uint64_t b = 16 * N * ((load ? 1 : 0) + (store ? 1 : 0));
+        (p.kind == PASS_TILE ? tb : other) += b;
+    }
+    other += 32 * N * P->dset.ds.size();   // direct Pauli groups read psi[j] and psi[j ^ x]
+    if (tile_bytes_per_circuit) *tile_bytes_per_circuit = tb;
+    if (direct_bytes_per_circuit) *direct_bytes_per_circuit = other;
+    return LQ_OK;
+}
+
 lq_status lq_psr_free(lq_psr *P) {
     if (!P) return LQ_OK;
     P->blob_buf.release(P->stream);
@@ -1034,20 +1062,103 @@ lq_status lq_psr_free(lq_psr *P) {
     return LQ_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// One-shot gradients (lq_param_shift_grad) reuse their plan across calls with
+// the same circuit, Hamiltonian, shard and options: planning, JIT lookup and
+// device buffers are paid once, as a VQE loop over theta would want.
+struct CachedPsr {
+    std::string key;
+    lq_psr *P = nullptr;
+    DevBuf io;   // theta, grad, energy
+};
+std::mutex g_psr_mu;
+std::vector<CachedPsr *> g_psr_cache;   // most recent last
+constexpr size_t PSR_CACHE_MAX = 2;
+
+std::string psr_key(int n, const lq_gate *g, size_t ng, size_t np, const lq_pauli_term *t, size_t nt, int rank,
+                    int world, void *stream) {
+    std::string k;
+    auto put = [&](const void *p, size_t b) { k.append(static_cast<const char *>(p), b); };
+    int64_t hdr[8] = {n, (int64_t)ng, (int64_t)np, (int64_t)nt, rank, world, (int64_t)(intptr_t)stream, 0};
+    put(hdr, sizeof(hdr));
+    int64_t opt[5] = {g_opt_fusion.load(), g_opt_K.load(), g_opt_coalesce.load(), g_opt_regbits.load(),
+                      g_opt_jit.load()};
+    put(opt, sizeof(opt));
+    for (size_t i = 0; i < ng; i++) {
+        put(&g[i], offsetof(lq_gate, mat));
+        if (g[i].kind == LQ_U1) put(g[i].mat, 8 * sizeof(double));
+        if (g[i].kind == LQ_U2) put(g[i].mat, 32 * sizeof(double));
+    }
+    if (nt) put(t, nt * sizeof(lq_pauli_term));
+    return k;
+}
+}  // namespace
+
+extern "C" {
+
+lq_status lq_psr_cache_clear(void) {
+    std::lock_guard<std::mutex> lk(g_psr_mu);
+    for (CachedPsr *c : g_psr_cache) {
+        c->io.release(c->P->stream);
+        lq_psr_free(c->P);
+        delete c;
+    }
+    g_psr_cache.clear();
+    return LQ_OK;
+}
+
 lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gates, const double *theta,
                               size_t n_params, const lq_pauli_term *terms, size_t n_terms, int shard_rank,
                               int shard_world, void *cuda_stream, double *grad_out, double *energy_out) {
     if (n_params && (!theta || !grad_out)) return fail(LQ_ERR_ARG, "theta/grad_out is NULL");
     for (size_t p = 0; p < n_params; p++)
         if (!std::isfinite(theta[p])) return fail(LQ_ERR_NONFINITE, "non-finite theta[" + std::to_string(p) + "]");
-    lq_psr *P = nullptr;
-    LQ_TRY(lq_psr_create(n_qubits, ansatz, n_gates, n_params, terms, n_terms, shard_rank, shard_world, cuda_stream,
-                         &P));
+    if (n_gates && !ansatz) return fail(LQ_ERR_ARG, "gates is NULL");
+    if (n_terms && !terms) return fail(LQ_ERR_ARG, "terms is NULL");
+    for (size_t i = 0; i < n_gates; i++)   // the key reads user matrices: validate them first
+        if ((ansatz[i].kind == LQ_U1 || ansatz[i].kind == LQ_U2) && !ansatz[i].mat)
+            return fail(LQ_ERR_ARG, "gate " + std::to_string(i) + ": matrix is NULL");
+    std::lock_guard<std::mutex> lk(g_psr_mu);
+    const std::string key =
+        psr_key(n_qubits, ansatz, n_gates, n_params, terms, n_terms, shard_rank, shard_world, cuda_stream);
+    CachedPsr *C = nullptr;
+    for (size_t i = 0; i < g_psr_cache.size(); i++)
+        if (g_psr_cache[i]->key == key) {
+            C = g_psr_cache[i];
+            g_psr_cache.erase(g_psr_cache.begin() + i);
+            break;
+        }
+    if (!C) {
+        lq_psr *P = nullptr;
+        LQ_TRY(lq_psr_create(n_qubits, ansatz, n_gates, n_params, terms, n_terms, shard_rank, shard_world,
+                             cuda_stream, &P));
+        C = new CachedPsr();
+        C->key = key;
+        C->P = P;
+        lq_status s = C->io.reserve(sizeof(double) * (2 * n_params + 2), P->stream);
+        if (s != LQ_OK) {
+            std::string keep = g_err;
+            lq_psr_free(P);
+            delete C;
+            g_err = keep;
+            return s;
+        }
+        if (g_psr_cache.size() >= PSR_CACHE_MAX) {   // evict the least recently used
+            CachedPsr *old = g_psr_cache.front();
+            g_psr_cache.erase(g_psr_cache.begin());
+            old->io.release(old->P->stream);
+            lq_psr_free(old->P);
+            delete old;
+        }
+    }
+    g_psr_cache.push_back(C);
+    lq_psr *P = C->P;
     cudaStream_t st = P->stream;
-    DevBuf io;
-    lq_status s = io.reserve(sizeof(double) * (2 * n_params + 2), st);
-    double *d_theta = io.at<double>(0), *d_grad = d_theta + n_params, *d_e = d_grad + n_params;
-    if (s == LQ_OK && n_params) {
+    double *d_theta = C->io.at<double>(0), *d_grad = d_theta + n_params, *d_e = d_grad + n_params;
+    lq_status s = LQ_OK;
+    if (n_params) {
         cudaError_t e = cudaMemcpyAsync(d_theta, theta, n_params * sizeof(double), cudaMemcpyHostToDevice, st);
         if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, cudaGetErrorString(e));
     }
@@ -1061,10 +1172,6 @@ lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gate
         if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, cudaGetErrorString(e));
     }
     if (s == LQ_OK) s = sync(st);
-    std::string keep = g_err;
-    io.release(st);
-    lq_psr_free(P);
-    if (s != LQ_OK) g_err = keep;
     return s;
 }
 

@@ -96,6 +96,8 @@ _SIGS = {
     "lq_plan_describe": ([_i32, _GP, _sz, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.c_char_p, _sz], _i32),
     "lq_launch_count": ([], _u64),
     "lq_plan_export_json": ([_i32, _GP, _sz, _TP, _sz, ctypes.c_char_p, _sz, ctypes.POINTER(_sz)], _i32),
+    "lq_psr_cache_clear": ([], _i32),
+    "lq_psr_traffic": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i32),
     "lq_jit_stats": ([ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_dbl)], _i32),
     "lq_jit_compile_check": ([_i32, _GP, _sz, _TP, _sz, ctypes.POINTER(_u64)], _i32),
 }
@@ -329,6 +331,13 @@ def lq_psr_stats(plan) -> Tuple[int, int, int, int]:
     c, l, b, t = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
     _chk(_lib.lq_psr_stats(plan, ctypes.byref(c), ctypes.byref(l), ctypes.byref(b), ctypes.byref(t)))
     return c.value, l.value, b.value, t.value
+
+
+def lq_psr_traffic(plan) -> Tuple[int, int]:
+    """(algorithmic HBM bytes per circuit through tile passes, through other kernels)"""
+    a, b = ctypes.c_uint64(), ctypes.c_uint64()
+    _chk(_lib.lq_psr_traffic(plan, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def lq_kernel_timing(kernel_class: int) -> Tuple[float, int]:
