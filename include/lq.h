@@ -148,6 +148,54 @@ lq_status lq_sv_norm2(lq_sv *sv, double *out);
  * (natural MSB-first order in device memory). */
 lq_status lq_sv_canonicalize(lq_sv *sv);
 
+/* ---- sharded states --------------------------
+ * A state too large for one GPU is split over G = 2^m ranks on its top m
+ * physical bits: rank r holds the 2^(n-m) amplitudes whose global bits are
+ * r ^ xmask (xmask: pending rank relabel; 0 after an init).  Gates acting
+ * non-diagonally on a global qubit are preceded by a global<->local qubit
+ * swap (pairwise half-shard exchange); controls, diagonal gates and Pauli Z
+ * factors on global qubits are rank constants; an uncontrolled X (or Y) on a
+ * global qubit is a rank relabel.  Every call on a sharded handle is
+ * COLLECTIVE: all ranks make the same calls with the same arguments, in the
+ * same order; host results (norm, expectation, read/gather) are returned on
+ * every rank.  lq_sv_write and lq_sv_canonicalize reject sharded handles. */
+typedef struct lq_comm lq_comm;   /* NCCL communicator (one process per GPU) */
+
+/* ncclUniqueId for lq_comm_init (len >= 128): call on rank 0 and broadcast
+ * the bytes (e.g. torch.distributed.broadcast_object_list). */
+lq_status lq_comm_unique_id(void *out, size_t len);
+/* Join the communicator (collective over `world` processes).  NCCL is loaded
+ * at run time (the copy torch already loaded, else libnccl.so.2);
+ * LQ_ERR_NCCL if it is unavailable. */
+lq_status lq_comm_init(const void *unique_id, size_t len, int rank, int world, lq_comm **out);
+lq_status lq_comm_free(lq_comm *comm);
+
+/* This process's shard of an n-qubit state on comm's ranks (world a power of
+ * two, n - log2(world) >= 1); world == 1 is lq_sv_alloc.  The handle keeps
+ * the comm pointer: free the state before the comm. */
+lq_status lq_sv_alloc_sharded(int n_qubits, lq_comm *comm, void *cuda_stream, lq_sv **out);
+
+/* All `world` shards of an n-qubit state in THIS process, exchanging halves
+ * with device copies instead of NCCL: the same schedules and kernels on one
+ * GPU (tests and single-GPU runs of the sharded data path). */
+lq_status lq_sv_alloc_group(int n_qubits, int world, void *cuda_stream, lq_sv **out);
+
+/* log2 of the number of shards (0: unsharded), rank of this process's first
+ * shard, number of shards held here, current rank relabel.  NULLs allowed. */
+lq_status lq_sv_shard_info(const lq_sv *sv, int *log2_world, int *first_rank, int *n_local_shards,
+                           uint32_t *xmask);
+/* Device pointer of local shard k (2^(n-m) amplitudes, physical local order). */
+void *lq_sv_shard_ptr(const lq_sv *sv, int k);
+
+/* Host-only: the distributed schedule (steps: local tile plans with the rank
+ * relabel in effect, global<->local swaps) of `gates`, then an optional QFT
+ * (qft = 1 forward, -1 inverse, 0 none), then an optional Pauli sum, for an
+ * n-qubit state on 2^log2_world ranks starting in the identity layout, as
+ * JSON (final qmap and xmask included).  *needed = buffer size required. */
+lq_status lq_dist_schedule_json(int n_qubits, int log2_world, const lq_gate *gates, size_t n_gates, int qft,
+                                const lq_pauli_term *terms, size_t n_terms, char *buf, size_t buf_len,
+                                size_t *needed);
+
 /* ---- circuits (Circuit::execute) ----------------------- */
 
 /* Apply gates[0..n_gates) in order (Circuit::execute semantics).  theta

@@ -14,9 +14,10 @@ namespace lq {
 // ---------------------------------------------------------------- pair kernel (a4)
 // One 1q/2q gate on arbitrary physical bits: strided pairs (i, i | 2^b) or
 // quads, 16-byte loads, controls as a bit mask (Alg. 1 generalised).
-__global__ void __launch_bounds__(256) k_pair(int n, const KOp op, const double2 *__restrict__ mats,
+__global__ void __launch_bounds__(256) k_pair(int n, uint64_t gofs, const KOp op, const double2 *__restrict__ mats,
                                               uint64_t mat_stride, double2 *__restrict__ state,
                                               uint64_t state_stride) {
+    // n: local index bits; gofs: this shard's physical global bits (controls only)
     double2 *__restrict__ psi = state + (uint64_t)blockIdx.y * state_stride;
     const double2 *__restrict__ M = mats + (uint64_t)blockIdx.y * mat_stride;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(256) k_pair(int n, const KOp op, const double2
         }
         for (; i < np; i += stride) {
             const uint64_t i0 = insert_zero64(i, op.b0);
-            if ((i0 & op.cmask) != op.cmask) continue;
+            if (((i0 | gofs) & op.cmask) != op.cmask) continue;
             const uint64_t i1 = i0 | mb;
             double2 x = psi[i0], y = psi[i1];
             if (op.type == K_X) { psi[i0] = y; psi[i1] = x; }
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(256) k_pair(int n, const KOp op, const double2
             for (int k = 0; k < 16; k++) U[k] = M[op.mat + k];
         for (; i < nq; i += stride) {
             const uint64_t base = insert_zero64(insert_zero64(i, lb), hb);
-            if ((base & op.cmask) != op.cmask) continue;
+            if (((base | gofs) & op.cmask) != op.cmask) continue;
             const uint64_t j0 = base, j1 = base | m1, j2 = base | m0, j3 = base | m0 | m1;
             if (op.type == K_SWAP) {
                 double2 x = psi[j1];
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(256) k_pair(int n, const KOp op, const double2
 // factors in one read-modify-write pass ("phase rotations based on bitwise
 // masks").
 constexpr int DIAG_MAX_OPS = 128;
-__global__ void __launch_bounds__(256) k_diag(int n, const KOp *__restrict__ ops, int n_ops,
+__global__ void __launch_bounds__(256) k_diag(int n, uint64_t gofs, const KOp *__restrict__ ops, int n_ops,
                                               const double2 *__restrict__ mats, uint64_t mat_stride,
                                               double2 *__restrict__ state, uint64_t state_stride) {
     __shared__ KOp sop[DIAG_MAX_OPS];
@@ -95,11 +96,12 @@ __global__ void __launch_bounds__(256) k_diag(int n, const KOp *__restrict__ ops
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
         double2 ph = make_double2(1.0, 0.0);
+        const uint64_t x = i | gofs;   // logic index (global bits of a shard are constants)
         for (int k = 0; k < n_ops; k++) {
             const KOp &o = sop[k];
-            if ((i & o.cmask) != o.cmask) continue;
-            uint32_t idx = (uint32_t)((i >> o.b0) & 1);
-            if (o.type == K_D2) idx = 2 * idx + (uint32_t)((i >> o.b1) & 1);
+            if ((x & o.cmask) != o.cmask) continue;
+            uint32_t idx = (uint32_t)((x >> o.b0) & 1);
+            if (o.type == K_D2) idx = 2 * idx + (uint32_t)((x >> o.b1) & 1);
             ph = cmul(ph, sd[k][idx]);
         }
         psi[i] = cmul(psi[i], ph);
@@ -237,10 +239,11 @@ __device__ __forceinline__ double2 gauss_amp(uint64_t seed, uint64_t i) {
 
 constexpr int RED_BLOCKS = 1184;   // 8 x 148 SMs; fixed => deterministic reduction order
 
-__global__ void __launch_bounds__(256) k_random_norm(uint64_t N, uint64_t seed, double *partial) {
+// off: logical index of the shard's first amplitude (sharded states)
+__global__ void __launch_bounds__(256) k_random_norm(uint64_t N, uint64_t off, uint64_t seed, double *partial) {
     double acc = 0.0;
     for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < N; i += (uint64_t)gridDim.x * 256) {
-        double2 a = gauss_amp(seed, i);
+        double2 a = gauss_amp(seed, off + i);
         acc = fma(a.x, a.x, fma(a.y, a.y, acc));
     }
     __shared__ double red[256];
@@ -248,11 +251,44 @@ __global__ void __launch_bounds__(256) k_random_norm(uint64_t N, uint64_t seed, 
     if (threadIdx.x == 0) partial[blockIdx.x] = r;
 }
 
-__global__ void __launch_bounds__(256) k_random_write(uint64_t N, uint64_t seed, const double *norm2,
+__global__ void __launch_bounds__(256) k_random_write(uint64_t N, uint64_t off, uint64_t seed, const double *norm2,
                                                       double2 *__restrict__ psi) {
     const double inv = 1.0 / sqrt(*norm2);
     for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < N; i += (uint64_t)gridDim.x * 256)
-        psi[i] = cscale(gauss_amp(seed, i), inv);
+        psi[i] = cscale(gauss_amp(seed, off + i), inv);
+}
+
+// ---------------------------------------------------------------- global-qubit swap (a9)
+// Sharded states (dist.h): swapping global bit g with local bit l, rank r
+// trades the half of its shard whose l-bit differs from its own g-bit with
+// the matching half of its partner.  Half-index i <-> shard position with
+// bit l = v inserted.
+__device__ __forceinline__ uint64_t insert_bit64(uint64_t x, int b, uint64_t v) {
+    const uint64_t lo = x & ((1ull << b) - 1);
+    return ((x ^ lo) << 1) | (v << b) | lo;
+}
+
+// both shards in this process (group mode): swap element-wise in place
+__global__ void __launch_bounds__(256) k_swap_halves(double2 *__restrict__ a, double2 *__restrict__ b, int l,
+                                                     int va, int vb, uint64_t half) {
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < half; i += (uint64_t)gridDim.x * 256) {
+        const uint64_t pa = insert_bit64(i, l, (uint64_t)va), pb = insert_bit64(i, l, (uint64_t)vb);
+        const double2 x = a[pa];
+        a[pa] = b[pb];
+        b[pb] = x;
+    }
+}
+
+// NCCL mode: chunk [off, off + cnt) of the outgoing half -> contiguous staging, and back
+__global__ void __launch_bounds__(256) k_pack_half(const double2 *__restrict__ src, double2 *__restrict__ dst, int l,
+                                                   int v, uint64_t off, uint64_t cnt) {
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * 256)
+        dst[i] = src[insert_bit64(off + i, l, (uint64_t)v)];
+}
+__global__ void __launch_bounds__(256) k_unpack_half(double2 *__restrict__ dst, const double2 *__restrict__ src, int l,
+                                                     int v, uint64_t off, uint64_t cnt) {
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * 256)
+        dst[insert_bit64(off + i, l, (uint64_t)v)] = src[i];
 }
 
 __global__ void __launch_bounds__(256) k_fill_basis(uint64_t N, uint64_t k, double2 *__restrict__ state,
@@ -325,7 +361,7 @@ __device__ __forceinline__ double re_iy(double2 w, uint32_t y) {
 }
 
 // Direct (non-tiled) pass for x masks wider than a tile.
-__global__ void __launch_bounds__(256) k_pauli_direct(int n, uint64_t x, const PTerm *__restrict__ terms,
+__global__ void __launch_bounds__(256) k_pauli_direct(int n, uint64_t gofs, uint64_t x, const PTerm *__restrict__ terms,
                                                       uint32_t nterm, const double2 *__restrict__ state,
                                                       uint64_t state_stride, double *__restrict__ partial,
                                                       uint64_t slot_stride, uint32_t slot) {
@@ -337,7 +373,7 @@ __global__ void __launch_bounds__(256) k_pauli_direct(int n, uint64_t x, const P
         const double2 w = make_double2(fma(p.x, a.x, p.y * a.y), fma(p.x, a.y, -p.y * a.x));
         for (uint32_t k = 0; k < nterm; k++) {
             const PTerm pt = terms[k];
-            const double c = (__popcll(j & pt.zfull) & 1) ? -pt.coeff : pt.coeff;
+            const double c = (__popcll((j | gofs) & pt.zfull) & 1) ? -pt.coeff : pt.coeff;
             acc = fma(c, re_iy(w, pt.yph), acc);
         }
     }

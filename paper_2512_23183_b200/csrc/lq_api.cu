@@ -20,6 +20,10 @@
 #include "kernels.cuh"
 #include "planner.h"
 #include "jit.h"
+#include "dist.h"
+
+#include <dlfcn.h>
+#include <nccl.h>   // types only: the functions are resolved with dlsym (liblq loads without NCCL)
 
 using namespace lq;
 
@@ -288,7 +292,7 @@ lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, cons
         attr = true;
     }
     if (smem > 227 * 1024) return fail(LQ_ERR_STATE, "tile pass exceeds shared memory (planner bug)");
-    const uint32_t tiles_log2 = (uint32_t)(kp.n - kp.K);
+    const uint32_t tiles_log2 = (uint32_t)(kp.nl - kp.K);
     const uint64_t total = (uint64_t)n_circ << tiles_log2;
     if (total >= (1ull << 32)) return fail(LQ_ERR_DIM, "too many tiles in one launch");
     // persistent grid: as many CTAs as fit on every SM (2 per SM for K <= 11)
@@ -349,8 +353,9 @@ struct DevPlan {
 
 lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uint64_t state_stride, int n_circ,
                         const double2 *mats, uint64_t mat_stride, cudaStream_t st, bool zero_first,
-                        double *partials = nullptr, uint64_t slot_stride = 0, bool no_final_store = false) {
-    const int n = plan.n;
+                        double *partials = nullptr, uint64_t slot_stride = 0, bool no_final_store = false,
+                        uint64_t gofs = 0) {
+    const int n = plan.nl;   // local index bits
     if (zero_first && (plan.passes.empty() || plan.passes[0].kind != PASS_TILE)) {
         dim3 grid(grid_for(1ull << n), n_circ);
         k_fill_basis<<<grid, 256, 0, st>>>(1ull << n, 0, state, state_stride);
@@ -360,6 +365,7 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
         const PlanPass &p = plan.passes[i];
         if (p.kind == PASS_TILE) {
             KPass kp = p.kp;
+            kp.gofs = gofs;
             if (zero_first && i == 0) kp.flags |= PF_LOAD_ZERO;
             if (no_final_store && i + 1 == plan.passes.size()) kp.flags |= PF_NO_STORE;
             uint32_t npt = 0;
@@ -373,14 +379,14 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
             uint64_t work = (op.type == K_U1 || op.type == K_X) ? (1ull << (n - 1)) : (1ull << (n - 2));
             dim3 grid(grid_for(work), n_circ);
             LaunchTimer lt_(KC_PAIR, st);
-            k_pair<<<grid, 256, 0, st>>>(n, op, mats, mat_stride, state, state_stride);
+            k_pair<<<grid, 256, 0, st>>>(n, gofs, op, mats, mat_stride, state, state_stride);
             LQ_TRY(check_launch("k_pair"));
         } else {
             for (uint32_t b = p.op_begin; b < p.op_end; b += DIAG_MAX_OPS) {
                 int cnt = (int)std::min<uint32_t>(DIAG_MAX_OPS, p.op_end - b);
                 dim3 grid(grid_for(1ull << n), n_circ);
                 LaunchTimer lt_(KC_DIAG, st);
-                k_diag<<<grid, 256, 0, st>>>(n, dp.kops + b, cnt, mats, mat_stride, state, state_stride);
+                k_diag<<<grid, 256, 0, st>>>(n, gofs, dp.kops + b, cnt, mats, mat_stride, state, state_stride);
                 LQ_TRY(check_launch("k_diag"));
             }
         }
@@ -408,7 +414,7 @@ struct DirectSet {
                 terms.push_back(p);
             }
             d.te = (uint32_t)terms.size();
-            uint64_t blocks = ((1ull << plan.n) + 255) / 256;
+            uint64_t blocks = ((1ull << plan.nl) + 255) / 256;
             d.nblocks = (uint32_t)std::min<uint64_t>(blocks, 148ull * 8);
             d.slot = slots;
             slots += d.nblocks;
@@ -420,11 +426,11 @@ struct DirectSet {
 // Direct groups, then E[c] = fixed-order sum of the circuit's partials.
 lq_status finish_expv(const Plan &plan, const DirectSet &dset, const PTerm *dterms, const double2 *state,
                       uint64_t state_stride, int n_circ, double *partial, uint64_t slot_stride, double *E,
-                      cudaStream_t st) {
+                      cudaStream_t st, uint64_t gofs = 0) {
     for (const auto &D : dset.ds) {
         dim3 grid(D.nblocks, n_circ);
         LaunchTimer lt_(KC_PAULI, st);
-        k_pauli_direct<<<grid, 256, 0, st>>>(plan.n, D.x, dterms + D.tb, D.te - D.tb, state, state_stride, partial,
+        k_pauli_direct<<<grid, 256, 0, st>>>(plan.nl, gofs, D.x, dterms + D.tb, D.te - D.tb, state, state_stride, partial,
                                              slot_stride, D.slot);
         LQ_TRY(check_launch("k_pauli_direct"));
     }
@@ -452,6 +458,11 @@ QMap to_qmap(int n, const int32_t *qm) {
 }  // namespace
 
 // ---------------------------------------------------------------- handles
+struct lq_comm {
+    ncclComm_t c = nullptr;
+    int rank = 0, world = 1;
+};
+
 struct lq_sv {
     int n = 0;
     double2 *d = nullptr;
@@ -459,9 +470,18 @@ struct lq_sv {
     cudaStream_t stream = nullptr;
     int32_t qmap[64];
     DevBuf plan_buf, work_buf;
+    // ---- sharded states (dist.h): m > 0
+    int m = 0, nl = 0;               // log2 G; local index bits
+    lq_comm *comm = nullptr;         // NCCL mode: one shard per process
+    int rank0 = 0;                   // rank of shards[0]
+    std::vector<double2 *> shards;   // this process's shards (group mode: all G)
+    uint32_t xmask = 0;              // rank relabel: rank r holds physical global bits r ^ xmask
+    DevBuf mats_buf, part_buf, stage_buf;
     void reset_map() {
         for (int q = 0; q < n; q++) qmap[q] = n - 1 - q;
+        xmask = 0;
     }
+    uint64_t gofs(int k) const { return (uint64_t)(uint32_t)((rank0 + k) ^ (int)xmask) << nl; }
 };
 
 namespace {
@@ -517,6 +537,259 @@ lq_status canonicalize(lq_sv *sv) {
 lq_status sync(cudaStream_t s) {
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
+    return LQ_OK;
+}
+
+// ---------------------------------------------------------------- NCCL (a9 transport)
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclSend) Send = nullptr;
+    decltype(&ncclRecv) Recv = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+NcclApi &nccl() {
+    static NcclApi a = [] {
+        NcclApi x;
+        // reuse the NCCL torch already loaded (same soname), else the system one
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            x.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return x;
+        }
+#define LQ_SYM(f) x.f = reinterpret_cast<decltype(x.f)>(dlsym(h, "nccl" #f)); if (!x.f) { x.why = "missing nccl" #f; return x; }
+        LQ_SYM(GetUniqueId) LQ_SYM(CommInitRank) LQ_SYM(CommDestroy) LQ_SYM(GroupStart) LQ_SYM(GroupEnd)
+        LQ_SYM(Send) LQ_SYM(Recv) LQ_SYM(AllReduce) LQ_SYM(GetErrorString)
+#undef LQ_SYM
+        x.ok = true;
+        return x;
+    }();
+    return a;
+}
+#define NCCL_TRY(x)                                                                             \
+    do {                                                                                        \
+        ncclResult_t r_ = (x);                                                                  \
+        if (r_ != ncclSuccess) return fail(LQ_ERR_NCCL, std::string(#x) + ": " + nccl().GetErrorString(r_)); \
+    } while (0)
+
+// ---------------------------------------------------------------- sharded states
+lq_status sh_check(int n, int world) {
+    if (world < 2 || (world & (world - 1))) return fail(LQ_ERR_ARG, "world size must be a power of two >= 2");
+    int m = __builtin_ctz((unsigned)world);
+    if (n - m < 1) return fail(LQ_ERR_ARG, "state has fewer qubits than log2(world)");
+    if (m > 16) return fail(LQ_ERR_ARG, "at most 2^16 shards");
+    return LQ_OK;
+}
+
+// sum one double per local shard (device array), in rank order, then over
+// processes (NCCL): the value every rank gets back
+lq_status sh_sum(lq_sv *sv, const double *dev_vals, double *out) {
+    const size_t nk = sv->shards.size();
+    std::vector<double> h(nk);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), dev_vals, nk * sizeof(double), cudaMemcpyDeviceToHost, sv->stream));
+    LQ_TRY(sync(sv->stream));
+    double acc = 0.0;
+    for (double v : h) acc += v;
+    if (sv->comm) {
+        LQ_TRY(sv->stage_buf.reserve(sizeof(double), sv->stream));
+        double *d = sv->stage_buf.at<double>(0);
+        CUDA_TRY(cudaMemcpyAsync(d, &acc, sizeof(double), cudaMemcpyHostToDevice, sv->stream));
+        NCCL_TRY(nccl().AllReduce(d, d, 1, ncclFloat64, ncclSum, sv->comm->c, sv->stream));
+        CUDA_TRY(cudaMemcpyAsync(&acc, d, sizeof(double), cudaMemcpyDeviceToHost, sv->stream));
+        LQ_TRY(sync(sv->stream));
+    }
+    *out = acc;
+    return LQ_OK;
+}
+
+// global-qubit swap: global physical bit g <-> local bit l
+constexpr uint64_t SWAP_CHUNK = 1ull << 24;   // amplitudes per staged NCCL message (256 MiB)
+lq_status sh_swap(lq_sv *sv, int g, int l, uint32_t xmask) {
+    const int j = g - sv->nl;
+    const uint64_t half = 1ull << (sv->nl - 1);
+    cudaStream_t st = sv->stream;
+    if (!sv->comm) {   // group mode: every pair lives in this process
+        const int G = (int)sv->shards.size();
+        for (int k = 0; k < G; k++) {
+            const int p = k ^ (1 << j);
+            if (p < k) continue;
+            const int bk = ((k ^ (int)xmask) >> j) & 1;   // k's physical g-bit; p has the other value
+            k_swap_halves<<<grid_for(half), 256, 0, st>>>(sv->shards[k], sv->shards[p], l, 1 - bk, bk, half);
+            LQ_TRY(check_launch("k_swap_halves"));
+        }
+        return LQ_OK;
+    }
+    const int rank = sv->comm->rank, peer = rank ^ (1 << j);
+    const int v = 1 - (((rank ^ (int)xmask) >> j) & 1);   // the half this rank gives away (and refills)
+    const uint64_t ch = std::min(half, SWAP_CHUNK);
+    LQ_TRY(sv->stage_buf.reserve(2 * ch * sizeof(double2), st));
+    double2 *out = sv->stage_buf.at<double2>(0), *in = out + ch;
+    for (uint64_t off = 0; off < half; off += ch) {
+        const uint64_t cnt = std::min(ch, half - off);
+        k_pack_half<<<grid_for(cnt), 256, 0, st>>>(sv->shards[0], out, l, v, off, cnt);
+        LQ_TRY(check_launch("k_pack_half"));
+        NCCL_TRY(nccl().GroupStart());
+        NCCL_TRY(nccl().Send(out, 2 * cnt, ncclFloat64, peer, sv->comm->c, st));
+        NCCL_TRY(nccl().Recv(in, 2 * cnt, ncclFloat64, peer, sv->comm->c, st));
+        NCCL_TRY(nccl().GroupEnd());
+        k_unpack_half<<<grid_for(cnt), 256, 0, st>>>(sv->shards[0], in, l, v, off, cnt);
+        LQ_TRY(check_launch("k_unpack_half"));
+    }
+    return LQ_OK;
+}
+
+// Run a schedule on the shards; E (nullable) receives the Pauli sum of the
+// schedule's expectation step.
+lq_status sh_run(lq_sv *sv, Schedule &sc, const double *theta, size_t n_theta, double *E) {
+    cudaStream_t st = sv->stream;
+    plan_steps(sc, options());
+    for (auto &stp : sc.steps)
+        if (stp.kind == 0) LQ_TRY(prepare(stp.plan));
+    Blob blob;
+    struct Off { size_t sub, kop, perm, pt, et, dt; };
+    std::vector<Off> offs(sc.steps.size());
+    std::vector<DirectSet> dsets(sc.steps.size());
+    for (size_t i = 0; i < sc.steps.size(); i++) {
+        const DStep &stp = sc.steps[i];
+        if (stp.kind != 0) continue;
+        dsets[i].build(stp.plan);
+        offs[i] = {blob.add(stp.plan.subs), blob.add(stp.plan.kops), blob.add(stp.plan.perms),
+                   blob.add(stp.plan.perm_terms), blob.add(stp.plan.eterms), blob.add(dsets[i].terms)};
+    }
+    size_t o_spec = blob.add(sc.mb.specs), o_fac = blob.add(sc.mb.factors), o_cst = blob.add(sc.mb.cst);
+    size_t o_th = blob.add(theta, theta ? n_theta * sizeof(double) : 0);
+    LQ_TRY(blob.upload(sv->plan_buf, st));
+    double2 *mats = nullptr;
+    if (sc.mb.mat_size) {
+        LQ_TRY(sv->mats_buf.reserve((size_t)sc.mb.mat_size * sizeof(double2), st));
+        mats = sv->mats_buf.at<double2>(0);
+        k_build_mats<<<grid_for(sc.mb.specs.size()), 256, 0, st>>>(
+            sv->plan_buf.at<MSpec>(o_spec), (int)sc.mb.specs.size(), sv->plan_buf.at<MFactor>(o_fac),
+            theta ? sv->plan_buf.at<double>(o_th) : nullptr, nullptr, sv->plan_buf.at<double2>(o_cst), mats,
+            sc.mb.mat_size, 1);
+        LQ_TRY(check_launch("k_build_mats"));
+    }
+    const size_t nk = sv->shards.size();
+    if (E) *E = 0.0;
+    for (size_t i = 0; i < sc.steps.size(); i++) {
+        const DStep &stp = sc.steps[i];
+        if (stp.kind == 1) {
+            LQ_TRY(sh_swap(sv, stp.g, stp.l, stp.xmask));
+            continue;
+        }
+        DevPlan dp;
+        dp.subs = sv->plan_buf.at<KSub>(offs[i].sub);
+        dp.kops = sv->plan_buf.at<KOp>(offs[i].kop);
+        dp.perms = sv->plan_buf.at<KPerm>(offs[i].perm);
+        dp.pterms = sv->plan_buf.at<KPermTerm>(offs[i].pt);
+        dp.eterms = sv->plan_buf.at<ETerm>(offs[i].et);
+        dp.specs = sv->plan_buf.at<MSpec>(o_spec);
+        dp.factors = sv->plan_buf.at<MFactor>(o_fac);
+        dp.cst = sv->plan_buf.at<double2>(o_cst);
+        const uint32_t slots = std::max<uint32_t>(dsets[i].slots, 1);
+        double *part = nullptr, *Ek = nullptr;
+        if (stp.expv) {
+            LQ_TRY(sv->part_buf.reserve(sizeof(double) * (slots + 1) * nk, st));
+            part = sv->part_buf.at<double>(0);
+            Ek = part + (size_t)slots * nk;
+        }
+        const uint32_t saved_xmask = sv->xmask;
+        sv->xmask = stp.xmask;
+        for (size_t k = 0; k < nk; k++) {
+            lq_status r = launch_passes(stp.plan, dp, sv->shards[k], 0, 1, mats, 0, st, false,
+                                        part ? part + (size_t)slots * k : nullptr, slots, false, sv->gofs((int)k));
+            if (r == LQ_OK && stp.expv)
+                r = finish_expv(stp.plan, dsets[i], sv->plan_buf.at<PTerm>(offs[i].dt), sv->shards[k], 0, 1,
+                                part + (size_t)slots * k, slots, Ek + k, st, sv->gofs((int)k));
+            if (r != LQ_OK) {
+                sv->xmask = saved_xmask;
+                return r;
+            }
+        }
+        sv->xmask = saved_xmask;
+        if (stp.expv && E) {
+            double e = 0.0;
+            LQ_TRY(sh_sum(sv, Ek, &e));
+            *E += e;
+        }
+    }
+    return LQ_OK;
+}
+
+// logical index -> (local shard slot k or -1 if another process owns it, local index)
+void sh_locate(const lq_sv *sv, uint64_t x, int *k, uint64_t *li) {
+    uint64_t phys = 0;
+    for (int q = 0; q < sv->n; q++)
+        if ((x >> (sv->n - 1 - q)) & 1) phys |= 1ull << sv->qmap[q];
+    const uint64_t gb = phys >> sv->nl;
+    const int rank = (int)(gb ^ sv->xmask);
+    *li = phys & ((1ull << sv->nl) - 1);
+    const int kk = rank - sv->rank0;
+    *k = (kk >= 0 && kk < (int)sv->shards.size()) ? kk : -1;
+}
+
+lq_status sh_gather(lq_sv *sv, const uint64_t *idx, uint64_t offset, uint64_t count, double *host_out) {
+    cudaStream_t st = sv->stream;
+    const size_t nk = sv->shards.size();
+    std::vector<std::vector<uint64_t>> li(nk), pos(nk);
+    for (uint64_t i = 0; i < count; i++) {
+        int k;
+        uint64_t l;
+        sh_locate(sv, idx ? idx[i] : offset + i, &k, &l);
+        if (k >= 0) { li[k].push_back(l); pos[k].push_back(i); }
+    }
+    std::vector<double2> res(count, make_double2(0.0, 0.0));
+    QMap ident;
+    memset(&ident, 0, sizeof(ident));
+    for (int q = 0; q < sv->nl; q++) ident.q[q] = (int8_t)(sv->nl - 1 - q);
+    // local physical index p as a "logical" index of the identity map on nl bits
+    for (size_t k = 0; k < nk; k++) {
+        const uint64_t c = li[k].size();
+        if (!c) continue;
+        LQ_TRY(sv->work_buf.reserve(c * (sizeof(double2) + sizeof(uint64_t)), st));
+        double2 *tmp = sv->work_buf.at<double2>(0);
+        uint64_t *didx = reinterpret_cast<uint64_t *>(tmp + c);
+        CUDA_TRY(cudaMemcpyAsync(didx, li[k].data(), c * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+        k_gather<<<grid_for(c), 256, 0, st>>>(sv->nl, ident, sv->shards[k], didx, 0, c, tmp);
+        LQ_TRY(check_launch("k_gather"));
+        std::vector<double2> h(c);
+        CUDA_TRY(cudaMemcpyAsync(h.data(), tmp, c * sizeof(double2), cudaMemcpyDeviceToHost, st));
+        LQ_TRY(sync(st));
+        for (uint64_t i = 0; i < c; i++) res[pos[k][i]] = h[i];
+    }
+    if (sv->comm && count) {   // exactly one rank owns each index: a sum gathers them
+        LQ_TRY(sv->stage_buf.reserve(count * sizeof(double2), st));
+        double *d = sv->stage_buf.at<double>(0);
+        CUDA_TRY(cudaMemcpyAsync(d, res.data(), count * sizeof(double2), cudaMemcpyHostToDevice, st));
+        NCCL_TRY(nccl().AllReduce(d, d, 2 * count, ncclFloat64, ncclSum, sv->comm->c, st));
+        CUDA_TRY(cudaMemcpyAsync(res.data(), d, count * sizeof(double2), cudaMemcpyDeviceToHost, st));
+        LQ_TRY(sync(st));
+    }
+    memcpy(host_out, res.data(), count * sizeof(double2));
+    return LQ_OK;
+}
+
+lq_status sh_alloc_shards(lq_sv *sv, int n_local_shards) {
+    const size_t bytes = (size_t)16 << sv->nl;
+    for (int k = 0; k < n_local_shards; k++) {
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            for (double2 *q : sv->shards) cudaFree(q);
+            sv->shards.clear();
+            return fail(LQ_ERR_OOM, std::string("shard allocation failed: ") + cudaGetErrorString(e));
+        }
+        sv->shards.push_back((double2 *)p);
+    }
+    sv->d = sv->shards[0];
     return LQ_OK;
 }
 }  // namespace
@@ -636,11 +909,147 @@ lq_status lq_sv_wrap(int n_qubits, void *cuda_stream, void *dev_ptr, size_t byte
     return LQ_OK;
 }
 
+lq_status lq_comm_unique_id(void *out, size_t len) {
+    if (!out || len < sizeof(ncclUniqueId)) return fail(LQ_ERR_ARG, "need a 128-byte buffer");
+    if (!nccl().ok) return fail(LQ_ERR_NCCL, nccl().why);
+    ncclUniqueId id;
+    NCCL_TRY(nccl().GetUniqueId(&id));
+    memcpy(out, &id, sizeof(id));
+    return LQ_OK;
+}
+
+lq_status lq_comm_init(const void *unique_id, size_t len, int rank, int world, lq_comm **out) {
+    if (!out || !unique_id || len < sizeof(ncclUniqueId)) return fail(LQ_ERR_ARG, "bad unique id / out");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return fail(LQ_ERR_ARG, "bad rank/world");
+    LQ_TRY(have_device());
+    if (!nccl().ok) return fail(LQ_ERR_NCCL, nccl().why);
+    ncclUniqueId id;
+    memcpy(&id, unique_id, sizeof(id));
+    lq_comm *c = new lq_comm();
+    c->rank = rank;
+    c->world = world;
+    ncclResult_t r = nccl().CommInitRank(&c->c, world, id, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return fail(LQ_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
+    }
+    *out = c;
+    return LQ_OK;
+}
+
+lq_status lq_comm_free(lq_comm *c) {
+    if (!c) return LQ_OK;
+    if (c->c) nccl().CommDestroy(c->c);
+    delete c;
+    return LQ_OK;
+}
+
+lq_status lq_sv_alloc_group(int n_qubits, int world, void *cuda_stream, lq_sv **out) {
+    if (!out) return fail(LQ_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (n_qubits < 2 || n_qubits > 40) return fail(LQ_ERR_ARG, "n_qubits must be in [2, 40]");
+    LQ_TRY(sh_check(n_qubits, world));
+    LQ_TRY(have_device());
+    lq_sv *sv = new lq_sv();
+    sv->n = n_qubits;
+    sv->m = __builtin_ctz((unsigned)world);
+    sv->nl = n_qubits - sv->m;
+    sv->stream = (cudaStream_t)cuda_stream;
+    sv->owned = false;
+    sv->reset_map();
+    lq_status s = sh_alloc_shards(sv, world);
+    if (s != LQ_OK) { delete sv; return s; }
+    *out = sv;
+    return LQ_OK;
+}
+
+lq_status lq_sv_alloc_sharded(int n_qubits, lq_comm *comm, void *cuda_stream, lq_sv **out) {
+    if (!out) return fail(LQ_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (!comm) return fail(LQ_ERR_ARG, "comm is NULL");
+    if (n_qubits < 2 || n_qubits > 44) return fail(LQ_ERR_ARG, "n_qubits must be in [2, 44]");
+    if (comm->world == 1) return lq_sv_alloc(n_qubits, cuda_stream, out);
+    LQ_TRY(sh_check(n_qubits, comm->world));
+    LQ_TRY(have_device());
+    lq_sv *sv = new lq_sv();
+    sv->n = n_qubits;
+    sv->m = __builtin_ctz((unsigned)comm->world);
+    sv->nl = n_qubits - sv->m;
+    sv->comm = comm;
+    sv->rank0 = comm->rank;
+    sv->stream = (cudaStream_t)cuda_stream;
+    sv->reset_map();
+    lq_status s = sh_alloc_shards(sv, 1);
+    if (s != LQ_OK) { delete sv; return s; }
+    *out = sv;
+    return LQ_OK;
+}
+
+lq_status lq_sv_shard_info(const lq_sv *sv, int *log2_world, int *first_rank, int *n_local_shards, uint32_t *xmask) {
+    LQ_TRY(check_sv(sv));
+    if (log2_world) *log2_world = sv->m;
+    if (first_rank) *first_rank = sv->rank0;
+    if (n_local_shards) *n_local_shards = sv->m ? (int)sv->shards.size() : 1;
+    if (xmask) *xmask = sv->xmask;
+    return LQ_OK;
+}
+
+void *lq_sv_shard_ptr(const lq_sv *sv, int k) {
+    if (!sv) return nullptr;
+    if (!sv->m) return k == 0 ? (void *)sv->d : nullptr;
+    return (k >= 0 && k < (int)sv->shards.size()) ? (void *)sv->shards[k] : nullptr;
+}
+
+lq_status lq_dist_schedule_json(int n_qubits, int log2_world, const lq_gate *gates, size_t n_gates, int qft,
+                                const lq_pauli_term *terms, size_t n_terms, char *buf, size_t buf_len,
+                                size_t *needed) {
+    if (n_qubits < 2 || n_qubits > 44 || log2_world < 1 || log2_world >= n_qubits)
+        return fail(LQ_ERR_ARG, "need 1 <= log2_world < n_qubits <= 44");
+    LQ_TRY(validate_gates(n_qubits, gates, n_gates, nullptr, 1 << 16, false, nullptr));
+    LQ_TRY(validate_terms(n_qubits, terms, n_terms));
+    Schedule sc;
+    sc.n = n_qubits;
+    sc.m = log2_world;
+    sc.nl = n_qubits - log2_world;
+    int32_t qm[64];
+    for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
+    uint32_t xm = 0;
+    schedule_gates(sc, gates, n_gates, qm, xm);
+    if (qft) {
+        std::vector<lq_gate> g = qft_gates(n_qubits, qft < 0);
+        schedule_gates(sc, g.data(), g.size(), qm, xm);
+    }
+    if (n_terms && !schedule_expval(sc, terms, n_terms, qm, xm))
+        return fail(LQ_ERR_ARG, "a Pauli term acts with X/Y on more qubits than a shard holds");
+    plan_steps(sc, options());
+    std::string j = schedule_json(sc, qm, xm);
+    if (needed) *needed = j.size() + 1;
+    if (buf && buf_len) {
+        size_t k = std::min(buf_len - 1, j.size());
+        memcpy(buf, j.data(), k);
+        buf[k] = 0;
+    }
+    return LQ_OK;
+}
+
 lq_status lq_sv_free(lq_sv *sv) {
     if (!sv) return LQ_OK;
     sv->plan_buf.release(sv->stream);
     sv->work_buf.release(sv->stream);
+    sv->mats_buf.release(sv->stream);
+    sv->part_buf.release(sv->stream);
+    sv->stage_buf.release(sv->stream);
     cudaError_t e = cudaSuccess;
+    if (!sv->shards.empty()) {
+        cudaStreamSynchronize(sv->stream);
+        for (double2 *p : sv->shards) {
+            cudaError_t e2 = cudaFree(p);
+            if (e2 != cudaSuccess) e = e2;
+        }
+        sv->shards.clear();
+        sv->d = nullptr;
+    }
     if (sv->owned && sv->d) {
         cudaStreamSynchronize(sv->stream);
         e = cudaFree(sv->d);
@@ -672,6 +1081,16 @@ lq_status lq_sv_init_basis(lq_sv *sv, uint64_t k) {
     LQ_TRY(check_sv(sv));
     if (k >= (1ull << sv->n)) return fail(LQ_ERR_ARG, "basis index out of range");
     sv->reset_map();
+    if (sv->m) {   // identity layout: logical k lives on rank k >> nl
+        const uint64_t Nl = 1ull << sv->nl;
+        for (size_t s2 = 0; s2 < sv->shards.size(); s2++) {
+            const bool own = (int)(k >> sv->nl) == sv->rank0 + (int)s2;
+            k_fill_basis<<<dim3(grid_for(Nl), 1), 256, 0, sv->stream>>>(Nl, own ? (k & (Nl - 1)) : ~0ull,
+                                                                         sv->shards[s2], 0);
+            LQ_TRY(check_launch("k_fill_basis"));
+        }
+        return LQ_OK;
+    }
     const uint64_t N = 1ull << sv->n;
     k_fill_basis<<<dim3(grid_for(N), 1), 256, 0, sv->stream>>>(N, k, sv->d, 0);
     return check_launch("k_fill_basis");
@@ -680,20 +1099,53 @@ lq_status lq_sv_init_basis(lq_sv *sv, uint64_t k) {
 lq_status lq_sv_init_random(lq_sv *sv, uint64_t seed) {
     LQ_TRY(check_sv(sv));
     sv->reset_map();
+    if (sv->m) {   // norm over all shards (sh_sum), then each shard writes its range
+        const uint64_t Nl = 1ull << sv->nl;
+        const size_t nk = sv->shards.size();
+        LQ_TRY(sv->work_buf.reserve(sizeof(double) * (RED_BLOCKS * nk + nk + 1), sv->stream));
+        double *part = sv->work_buf.at<double>(0), *sums = part + RED_BLOCKS * nk, *tot = sums + nk;
+        for (size_t k2 = 0; k2 < nk; k2++) {
+            k_random_norm<<<RED_BLOCKS, 256, 0, sv->stream>>>(Nl, sv->gofs((int)k2), seed, part + RED_BLOCKS * k2);
+            LQ_TRY(check_launch("k_random_norm"));
+            k_sum_partials<<<1, 256, 0, sv->stream>>>(part + RED_BLOCKS * k2, 0, RED_BLOCKS, sums + k2);
+            LQ_TRY(check_launch("k_sum_partials"));
+        }
+        double total = 0.0;
+        LQ_TRY(sh_sum(sv, sums, &total));
+        CUDA_TRY(cudaMemcpyAsync(tot, &total, sizeof(double), cudaMemcpyHostToDevice, sv->stream));
+        for (size_t k2 = 0; k2 < nk; k2++) {
+            k_random_write<<<grid_for(Nl), 256, 0, sv->stream>>>(Nl, sv->gofs((int)k2), seed, tot, sv->shards[k2]);
+            LQ_TRY(check_launch("k_random_write"));
+        }
+        return sync(sv->stream);   // `total` lives on this stack frame
+    }
     const uint64_t N = 1ull << sv->n;
     LQ_TRY(sv->work_buf.reserve(sizeof(double) * (RED_BLOCKS + 1), sv->stream));
     double *part = sv->work_buf.at<double>(0);
-    k_random_norm<<<RED_BLOCKS, 256, 0, sv->stream>>>(N, seed, part);
+    k_random_norm<<<RED_BLOCKS, 256, 0, sv->stream>>>(N, 0, seed, part);
     LQ_TRY(check_launch("k_random_norm"));
     k_sum_partials<<<1, 256, 0, sv->stream>>>(part, 0, RED_BLOCKS, part + RED_BLOCKS);
     LQ_TRY(check_launch("k_sum_partials"));
-    k_random_write<<<grid_for(N), 256, 0, sv->stream>>>(N, seed, part + RED_BLOCKS, sv->d);
+    k_random_write<<<grid_for(N), 256, 0, sv->stream>>>(N, 0, seed, part + RED_BLOCKS, sv->d);
     return check_launch("k_random_write");
 }
 
 lq_status lq_sv_norm2(lq_sv *sv, double *out) {
     LQ_TRY(check_sv(sv));
     if (!out) return fail(LQ_ERR_ARG, "out is NULL");
+    if (sv->m) {
+        const uint64_t Nl = 1ull << sv->nl;
+        const size_t nk = sv->shards.size();
+        LQ_TRY(sv->work_buf.reserve(sizeof(double) * (RED_BLOCKS * nk + nk), sv->stream));
+        double *part = sv->work_buf.at<double>(0), *sums = part + RED_BLOCKS * nk;
+        for (size_t k2 = 0; k2 < nk; k2++) {
+            k_norm2<<<RED_BLOCKS, 256, 0, sv->stream>>>(Nl, sv->shards[k2], part + RED_BLOCKS * k2);
+            LQ_TRY(check_launch("k_norm2"));
+            k_sum_partials<<<1, 256, 0, sv->stream>>>(part + RED_BLOCKS * k2, 0, RED_BLOCKS, sums + k2);
+            LQ_TRY(check_launch("k_sum_partials"));
+        }
+        return sh_sum(sv, sums, out);
+    }
     const uint64_t N = 1ull << sv->n;
     LQ_TRY(sv->work_buf.reserve(sizeof(double) * (RED_BLOCKS + 1), sv->stream));
     double *part = sv->work_buf.at<double>(0);
@@ -732,6 +1184,7 @@ lq_status lq_sv_read(lq_sv *sv, uint64_t offset, uint64_t count, double *host_ou
     uint64_t N = 1ull << sv->n;
     if (offset > N || count > N - offset) return fail(LQ_ERR_DIM, "read range out of bounds");
     if (!count) return LQ_OK;
+    if (sv->m) return sh_gather(sv, nullptr, offset, count, host_out);
     return read_impl(sv, nullptr, offset, count, host_out);
 }
 
@@ -742,11 +1195,13 @@ lq_status lq_sv_gather(lq_sv *sv, const uint64_t *idx, size_t count, double *hos
     for (size_t i = 0; i < count; i++)
         if (idx[i] >= N) return fail(LQ_ERR_DIM, "gather index out of range");
     if (!count) return LQ_OK;
+    if (sv->m) return sh_gather(sv, idx, 0, count, host_out);
     return read_impl(sv, idx, 0, count, host_out);
 }
 
 lq_status lq_sv_write(lq_sv *sv, uint64_t offset, uint64_t count, const double *host_in) {
     LQ_TRY(check_sv(sv));
+    if (sv->m) return fail(LQ_ERR_ARG, "lq_sv_write is not supported on sharded states");
     if (!host_in && count) return fail(LQ_ERR_ARG, "host_in is NULL");
     uint64_t N = 1ull << sv->n;
     if (offset > N || count > N - offset) return fail(LQ_ERR_DIM, "write range out of bounds");
@@ -768,6 +1223,7 @@ lq_status lq_sv_write(lq_sv *sv, uint64_t offset, uint64_t count, const double *
 
 lq_status lq_sv_canonicalize(lq_sv *sv) {
     LQ_TRY(check_sv(sv));
+    if (sv->m) return fail(LQ_ERR_ARG, "lq_sv_canonicalize is not supported on sharded states (reads resolve the layout)");
     return canonicalize(sv);
 }
 
@@ -775,6 +1231,20 @@ lq_status lq_apply_circuit(lq_sv *sv, const lq_gate *gates, size_t n_gates, cons
     LQ_TRY(check_sv(sv));
     LQ_TRY(validate_gates(sv->n, gates, n_gates, theta, n_theta, true, nullptr));
     if (!n_gates) return LQ_OK;
+    if (sv->m) {
+        Schedule sc;
+        sc.n = sv->n;
+        sc.m = sv->m;
+        sc.nl = sv->nl;
+        int32_t qm[64];
+        memcpy(qm, sv->qmap, sizeof(qm));
+        uint32_t xm = sv->xmask;
+        schedule_gates(sc, gates, n_gates, qm, xm);
+        LQ_TRY(sh_run(sv, sc, theta, n_theta, nullptr));
+        memcpy(sv->qmap, qm, sizeof(qm));
+        sv->xmask = xm;
+        return LQ_OK;
+    }
     int32_t qm[64];
     memcpy(qm, sv->qmap, sizeof(qm));
     std::vector<POp> ops;
@@ -789,6 +1259,10 @@ lq_status lq_apply_circuit(lq_sv *sv, const lq_gate *gates, size_t n_gates, cons
 
 lq_status lq_qft(lq_sv *sv, int inverse) {
     LQ_TRY(check_sv(sv));
+    if (sv->m) {   // Alg. 3 as gates through the distributed scheduler
+        std::vector<lq_gate> g = qft_gates(sv->n, inverse != 0);
+        return lq_apply_circuit(sv, g.data(), g.size(), nullptr, 0);
+    }
     int32_t qm[64];
     memcpy(qm, sv->qmap, sizeof(qm));
     bool ident = true, rev = true;
@@ -812,6 +1286,21 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
     LQ_TRY(check_sv(sv));
     if (!out_energy) return fail(LQ_ERR_ARG, "out_energy is NULL");
     LQ_TRY(validate_terms(sv->n, terms, n_terms));
+    if (sv->m) {
+        Schedule sc;
+        sc.n = sv->n;
+        sc.m = sv->m;
+        sc.nl = sv->nl;
+        int32_t qm[64];
+        memcpy(qm, sv->qmap, sizeof(qm));
+        uint32_t xm = sv->xmask;
+        if (!schedule_expval(sc, terms, n_terms, qm, xm))
+            return fail(LQ_ERR_ARG, "a Pauli term acts with X/Y on more qubits than a shard holds");
+        LQ_TRY(sh_run(sv, sc, nullptr, 0, out_energy));
+        memcpy(sv->qmap, qm, sizeof(qm));
+        sv->xmask = xm;
+        return LQ_OK;
+    }
     Plan plan;
     MatBuilder mb;
     std::vector<POp> ops;

@@ -179,7 +179,9 @@ LQ_HD inline int op_table_size(uint8_t type) {
 }
 
 struct KPass {
-    int32_t n;           // index bits of one state
+    int32_t n;           // index bits of the (logical) state
+    int32_t nl;          // index bits held locally (n - log2 G for a sharded state, else n)
+    uint64_t gofs;       // physical global bits of this shard (OR-ed into the logic index, never into addresses)
     int32_t K;           // tile bits
     uint32_t sub_begin, sub_end;
     uint32_t op_begin, op_end;   // contiguous op range of the pass
@@ -192,7 +194,7 @@ struct KPass {
     uint8_t T[MAXK];     // physical bit of each local bit, ascending
     uint8_t Sload[R];    // (unused by the persistent kernel; kept for layout)
     uint8_t Sstore[R];   // local bits of the register mapping used for the HBM store
-    uint8_t pad[2];
+    uint8_t pad[6];
 };
 
 // Matrix construction (device-side, per circuit): every fused op has a

@@ -499,14 +499,15 @@ static int32_t build_perm(const std::vector<POp> &ops, const std::vector<int> &g
 // Build a TILE pass from absorbed ops (execution order) and tile mask Tm:
 // segments = [entry permutation group][register sub-block], the entry
 // permutations being folded into the exchange that starts the sub-block.
-static void emit_tile(int n, int K, int Rr, uint64_t Tm, const std::vector<POp> &ops,
+static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vector<POp> &ops,
                       const std::vector<int> &absorbed, const std::vector<uint32_t> &mat_off,
                       Plan &plan) {
     LocalMap L(Tm);
-    int lowrun = (n > K) ? lowrun_of(L) : 0;
+    int lowrun = (nl > K) ? lowrun_of(L) : 0;
     PlanPass pp;
     pp.kind = PASS_TILE;
     pp.kp.n = n;
+    pp.kp.nl = nl;
     pp.kp.K = K;
     pp.kp.flags = 0;
     memcpy(pp.kp.T, L.T, MAXK);
@@ -587,7 +588,7 @@ static void emit_tile(int n, int K, int Rr, uint64_t Tm, const std::vector<POp> 
     if (pp.kp.eterm_end > pp.kp.eterm_begin || (pp.kp.flags & PF_EXPV)) {
         pp.kp.flags |= PF_EXPV;
         pp.kp.eslot = plan.n_slots;
-        plan.n_slots += (uint32_t)(1u << (n - K));
+        plan.n_slots += (uint32_t)(1u << (nl - K));
     }
     pp.kp.store_perm = build_perm(ops, store_group, L, pp, plan);
     // read-only pass: nothing but Pauli groups (no gate, no folded permutation)
@@ -605,15 +606,17 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
                   Plan &plan) {
     std::vector<uint32_t> mat_off;
     for (auto &sp : mb.specs) mat_off.push_back(sp.out);
-    int K = opt.K > 0 ? std::min(opt.K, n) : auto_tile_bits(n);
+    const int nl = opt.n_local > 0 ? std::min(opt.n_local, n) : n;   // tile bits come from [0, nl)
+    int K = opt.K > 0 ? std::min(opt.K, nl) : auto_tile_bits(nl);
     if (K > 12) K = 12;   // two 2^K buffers must fit in shared memory
-    if (n <= K) K = n;
+    if (nl <= K) K = nl;
     int Rr = std::min(std::max(1, std::min(opt.reg_bits, R)), K);
     plan.Rr = Rr;
     plan.n = n;
+    plan.nl = nl;
     plan.K = K;
     int c = std::max(0, std::min(opt.coalesce, K - 2));
-    uint64_t mand = (n > K) ? ((1ull << c) - 1) : ((n >= 64) ? ~0ull : ((1ull << n) - 1));
+    uint64_t mand = (nl > K) ? ((1ull << c) - 1) : ((1ull << nl) - 1);
     // Pauli groups whose x mask cannot share a tile with the coalescing run
     // go to the direct kernel
     std::vector<char> skip(ops.size(), 0);
@@ -628,8 +631,8 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
             if (skip[i]) continue;
             if (o.type == K_EXPV) {
                 uint64_t Tm = mand | o.xm;
-                for (int b = 0; b < n && popc(Tm) < K; b++) Tm |= bit(b);
-                emit_tile(n, K, Rr, Tm, ops, std::vector<int>{(int)i}, mat_off, plan);
+                for (int b = 0; b < nl && popc(Tm) < K; b++) Tm |= bit(b);
+                emit_tile(n, nl, K, Rr, Tm, ops, std::vector<int>{(int)i}, mat_off, plan);
                 continue;
             }
             PlanPass pp;
@@ -661,13 +664,13 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
         int best = score(ops, absorbed_w);
         uint64_t Tm0 = Tm;
         // local search: swap one free tile bit for another if it absorbs more
-        if (n > K) {
+        if (nl > K) {
             for (int iter = 0; iter < 2; iter++) {
                 bool improved = false;
                 // fill Tm to K bits first with the bits most used by blocked ops
-                for (int out = 0; out < n; out++) {
+                for (int out = 0; out < nl; out++) {
                     if (!(Tm & bit(out)) || (mand & bit(out))) continue;
-                    for (int in = 0; in < n; in++) {
+                    for (int in = 0; in < nl; in++) {
                         if (Tm & bit(in)) continue;
                         uint64_t T2 = (Tm & ~bit(out)) | bit(in);
                         std::vector<int> a2;
@@ -677,7 +680,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
                     }
                 }
                 if (popc(Tm) < K) {
-                    for (int in = 0; in < n && popc(Tm) < K; in++) {
+                    for (int in = 0; in < nl && popc(Tm) < K; in++) {
                         if (Tm & bit(in)) continue;
                         std::vector<int> a2;
                         absorb_fixed(ops, window, Tm | bit(in), a2);
@@ -709,7 +712,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
             pp.n_ops = (int)absorbed.size();
             plan.passes.push_back(pp);
             plan.n_diag++;
-        } else if (absorbed.size() == 1 && !has_expv && (n > K || popc(ops[absorbed[0]].full()) > K)) {
+        } else if (absorbed.size() == 1 && !has_expv && (nl > K || popc(ops[absorbed[0]].full()) > K)) {
             PlanPass pp;
             pp.kind = PASS_PAIR;
             pp.op_begin = (uint32_t)plan.kops.size();
@@ -721,8 +724,8 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
         } else {
             // fill the tile to exactly K bits, lowest free bits first (longer
             // contiguous runs for coalescing)
-            for (int b = 0; b < n && popc(Tm) < K; b++) Tm |= bit(b);
-            emit_tile(n, K, Rr, Tm, ops, absorbed, mat_off, plan);
+            for (int b = 0; b < nl && popc(Tm) < K; b++) Tm |= bit(b);
+            emit_tile(n, nl, K, Rr, Tm, ops, absorbed, mat_off, plan);
         }
         // remove absorbed from rem (absorbed is a subsequence of rem)
         std::vector<int> left;
@@ -772,6 +775,7 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
     int c = std::max(0, std::min(opt.coalesce, K - 1));   // room for at least one stage bit
     uint64_t mand = (n > K) ? ((1ull << c) - 1) : ((1ull << n) - 1);
     plan.n = n;
+    plan.nl = n;
     plan.K = K;
     size_t s = 0;
     while (s < js.size()) {
@@ -788,6 +792,7 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
         PlanPass pp;
         pp.kind = PASS_TILE;
         pp.kp.n = n;
+        pp.kp.nl = n;
         pp.kp.K = K;
         memcpy(pp.kp.T, L.T, MAXK);
         pp.kp.sub_begin = (uint32_t)plan.subs.size();
@@ -892,7 +897,7 @@ std::string export_json(const Plan &plan, const MatBuilder &mb, const int32_t *q
         for (size_t i = 0; i < cnt; i++) { if (i) o << ","; f(i); }
         o << "]";
     };
-    o << "{\"n\":" << plan.n << ",\"K\":" << plan.K << ",\"Rr\":" << plan.Rr << ",\"n_slots\":" << plan.n_slots
+    o << "{\"n\":" << plan.n << ",\"nl\":" << plan.nl << ",\"K\":" << plan.K << ",\"Rr\":" << plan.Rr << ",\"n_slots\":" << plan.n_slots
       << ",\"mat_size\":" << mb.mat_size << ",";
     arr("qmap", (size_t)plan.n, [&](size_t i) { o << qmap[i]; });
     o << ",";

@@ -51,6 +51,7 @@ struct PlanPass {
 
 struct Plan {
     int n = 0;
+    int nl = 0;               // local index bits (tile bits are chosen among [0, nl)); n for an unsharded state
     int K = 0;
     int Rr = 0;               // register bits of the tile passes
     std::vector<PlanPass> passes;
@@ -81,6 +82,7 @@ struct PlanOptions {
     int coalesce = 3;        // low physical bits a strided tile always holds
     bool fusion = true;      // false: one PAIR/DIAG pass per op
     int reg_bits = 4;        // register bits per thread (R); tile kernels run 2^(K-R) threads
+    int n_local = 0;         // sharded state: only bits [0, n_local) are local (0 = all n bits)
 };
 
 // Lower user gates (already validated) to POps on physical bits.  SWAP

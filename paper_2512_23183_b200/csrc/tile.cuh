@@ -832,7 +832,7 @@ __device__ __forceinline__ void tile_body(const KPass &P, const KSub *__restrict
         auto load_regs = [&](int perm, const uint8_t *S) {
             if (perm >= 0) {
                 PermSlots<RR> ps;
-                ps.make(cur, S, K, s_perm[perm], binv_of(perm, tb));
+                ps.make(cur, S, K, s_perm[perm], binv_of(perm, tb | P.gofs));
                 Unroll<RR>::run([&](auto V) { a[decltype(V)::value] = b[ps.template sidx<decltype(V)::value>()]; });
             } else {
                 Unroll<RR>::run([&](auto V) { a[decltype(V)::value] = b[cur.template sidx<decltype(V)::value>()]; });
@@ -841,13 +841,13 @@ __device__ __forceinline__ void tile_body(const KPass &P, const KSub *__restrict
         if (zero) {   // |0...0>: amplitude 1 where the source position is local 0 of tile 0
             if (sb.perm >= 0) {
                 PermSlots<RR> ps;
-                ps.make(cur, sb.S, K, s_perm[sb.perm], binv_of(sb.perm, tb));
+                ps.make(cur, sb.S, K, s_perm[sb.perm], binv_of(sb.perm, tb | P.gofs));
                 Unroll<RR>::run([&](auto V) {
-                    a[decltype(V)::value] = make_double2((tb == 0 && ps.template sidx<decltype(V)::value>() == 0) ? 1.0 : 0.0, 0.0);
+                    a[decltype(V)::value] = make_double2(((tb | P.gofs) == 0 && ps.template sidx<decltype(V)::value>() == 0) ? 1.0 : 0.0, 0.0);
                 });
             } else {
                 Unroll<RR>::run([&](auto V) {
-                    a[decltype(V)::value] = make_double2((tb == 0 && cur.template sidx<decltype(V)::value>() == 0) ? 1.0 : 0.0, 0.0);
+                    a[decltype(V)::value] = make_double2(((tb | P.gofs) == 0 && cur.template sidx<decltype(V)::value>() == 0) ? 1.0 : 0.0, 0.0);
                 });
             }
         } else {
@@ -871,7 +871,7 @@ __device__ __forceinline__ void tile_body(const KPass &P, const KSub *__restrict
                     load_regs(sb.perm, sb.S);
                 }
             }
-            Prog::template run<RR>(s - P.sub_begin, sb, P.op_begin, a, s_ops, cur.gt, P.n, s_tab, ts, s_et);
+            Prog::template run<RR>(s - P.sub_begin, sb, P.op_begin, a, s_ops, cur.gt | P.gofs, P.n, s_tab, ts, s_et);
         }
         double2 *psi = state + (uint64_t)circ * state_stride;
         if (P.flags & PF_EXPV) {   // one deterministic partial per tile
@@ -953,28 +953,29 @@ __device__ __forceinline__ void xwrite_c(double2 *b, const double2 (&a)[1 << RR]
 // shared slots -> registers of mapping SMm, through entry permutation PI
 // (ZERO: synthesise |0...0> -- amplitude 1 at position 0 of tile 0)
 template <int RR, class D, uint32_t SMm, int PI, bool ZERO>
-__device__ __forceinline__ void xread_c(const double2 *b, double2 (&a)[1 << RR], uint32_t t, uint64_t tb) {
+__device__ __forceinline__ void xread_c(const double2 *b, double2 (&a)[1 << RR], uint32_t t, uint64_t tb,
+                                        uint64_t gofs) {
     const uint32_t lt = ins_zeros<SMm, D::K>(t);
     if constexpr (PI < 0) {
         const uint32_t base = swz(lt);
         Unroll<RR>::run([&](auto V) {
             constexpr uint32_t so = swz(loff_c<SMm>(decltype(V)::value));
-            if constexpr (ZERO) a[decltype(V)::value] = make_double2((tb == 0 && (base ^ so) == 0) ? 1.0 : 0.0, 0.0);
+            if constexpr (ZERO) a[decltype(V)::value] = make_double2(((tb | gofs) == 0 && (base ^ so) == 0) ? 1.0 : 0.0, 0.0);
             else a[decltype(V)::value] = b[base ^ so];
         });
     } else {
-        const uint32_t base = swz(D::template ainv<PI>(lt) ^ D::template binv<PI>(tb));
+        const uint32_t base = swz(D::template ainv<PI>(lt) ^ D::template binv<PI>(tb | gofs));
         Unroll<RR>::run([&](auto V) {
             constexpr uint32_t so = swz(D::template ainv<PI>(loff_c<SMm>(decltype(V)::value)));
-            if constexpr (ZERO) a[decltype(V)::value] = make_double2((tb == 0 && (base ^ so) == 0) ? 1.0 : 0.0, 0.0);
+            if constexpr (ZERO) a[decltype(V)::value] = make_double2(((tb | gofs) == 0 && (base ^ so) == 0) ? 1.0 : 0.0, 0.0);
             else a[decltype(V)::value] = b[base ^ so];
         });
     }
 }
 
 template <int RR, class D, class Prog, int S>
-__device__ __forceinline__ void run_subs_c(double2 (&a)[1 << RR], double2 *b, TState &ts, uint64_t tb, uint32_t t,
-                                           const double2 *tab, const ETerm *et, int n) {
+__device__ __forceinline__ void run_subs_c(double2 (&a)[1 << RR], double2 *b, TState &ts, uint64_t tb, uint64_t gofs,
+                                           uint32_t t, const double2 *tab, const ETerm *et, int n) {
     if constexpr (S < D::NSUB) {
         if constexpr (S > 0 && (D::SM[S] != D::SM[S - 1] || D::PERM[S] >= 0)) {
             materialize<RR>(a, ts, false);
@@ -982,11 +983,11 @@ __device__ __forceinline__ void run_subs_c(double2 (&a)[1 << RR], double2 *b, TS
             xwrite_c<RR, D::K, D::SM[S - 1]>(b, a, t, ts.fb);
             ts.fb = 0;
             __syncthreads();
-            xread_c<RR, D, D::SM[S], D::PERM[S], false>(b, a, t, tb);
+            xread_c<RR, D, D::SM[S], D::PERM[S], false>(b, a, t, tb, gofs);
         }
-        const uint64_t gbase = tb | D::dep(ins_zeros<D::SM[S], D::K>(t));
+        const uint64_t gbase = tb | gofs | D::dep(ins_zeros<D::SM[S], D::K>(t));
         Prog::template run<S, RR>(a, gbase, n, tab, ts, et);
-        run_subs_c<RR, D, Prog, S + 1>(a, b, ts, tb, t, tab, et, n);
+        run_subs_c<RR, D, Prog, S + 1>(a, b, ts, tb, gofs, t, tab, et, n);
     }
 }
 
@@ -1047,11 +1048,11 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
 
         const uint64_t tb = D::tbase(g & tmask);
         double2 a[NV];
-        if (zero) xread_c<RR, D, D::SM[0], D::PERM[0], true>(b, a, t, tb);
-        else xread_c<RR, D, D::SM[0], D::PERM[0], false>(b, a, t, tb);
+        if (zero) xread_c<RR, D, D::SM[0], D::PERM[0], true>(b, a, t, tb, P.gofs);
+        else xread_c<RR, D, D::SM[0], D::PERM[0], false>(b, a, t, tb, P.gofs);
         TState ts;
         ts.reset();
-        run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, t, s_tab, s_et, P.n);
+        run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, P.gofs, t, s_tab, s_et, P.n);
         double2 *psi = state + (uint64_t)circ * state_stride;
         if (P.flags & PF_EXPV) {   // one deterministic partial per tile
             __syncthreads();
@@ -1070,7 +1071,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
             if constexpr (need_x) __syncthreads();
             xwrite_c<RR, K, D::SM[LAST]>(b, a, t, ts.fb);
             __syncthreads();
-            xread_c<RR, D, D::SSTORE, D::STORE_PERM, false>(b, a, t, tb);
+            xread_c<RR, D, D::SSTORE, D::STORE_PERM, false>(b, a, t, tb, P.gofs);
         }
         const uint64_t gst = tb | D::dep(ins_zeros<D::SSTORE, K>(t));
         Unroll<RR>::run([&](auto V) {

@@ -97,6 +97,15 @@ _SIGS = {
     "lq_launch_count": ([], _u64),
     "lq_plan_export_json": ([_i32, _GP, _sz, _TP, _sz, ctypes.c_char_p, _sz, ctypes.POINTER(_sz)], _i32),
     "lq_psr_cache_clear": ([], _i32),
+    "lq_comm_unique_id": ([_P, _sz], _i32),
+    "lq_comm_init": ([_P, _sz, _i32, _i32, ctypes.POINTER(_P)], _i32),
+    "lq_comm_free": ([_P], _i32),
+    "lq_sv_alloc_sharded": ([_i32, _P, _P, ctypes.POINTER(_P)], _i32),
+    "lq_sv_alloc_group": ([_i32, _i32, _P, ctypes.POINTER(_P)], _i32),
+    "lq_sv_shard_info": ([_P, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                          ctypes.POINTER(ctypes.c_uint32)], _i32),
+    "lq_sv_shard_ptr": ([_P, _i32], _P),
+    "lq_dist_schedule_json": ([_i32, _i32, _GP, _sz, _i32, _TP, _sz, ctypes.c_char_p, _sz, ctypes.POINTER(_sz)], _i32),
     "lq_psr_traffic": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i32),
     "lq_jit_stats": ([ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_dbl)], _i32),
     "lq_jit_compile_check": ([_i32, _GP, _sz, _TP, _sz, ctypes.POINTER(_u64)], _i32),
@@ -383,6 +392,129 @@ def lq_jit_compile_check(n_qubits: int, gates, terms=()) -> int:
     nk = ctypes.c_uint64()
     _chk(_lib.lq_jit_compile_check(n_qubits, ga.ptr, ga.n, ta.ptr, ta.n, ctypes.byref(nk)))
     return nk.value
+
+
+# ---- sharded states (a9) ---------------------------------------------------
+def lq_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _chk(_lib.lq_comm_unique_id(buf, 128))
+    return buf.raw
+
+
+def lq_comm_init(unique_id: bytes, rank: int, world: int):
+    h = _P()
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    _chk(_lib.lq_comm_init(buf, 128, rank, world, ctypes.byref(h)))
+    return h
+
+
+def lq_comm_free(h):
+    _chk(_lib.lq_comm_free(h))
+
+
+def comm_from_torch(group=None):
+    """An lq_comm over the ranks of a torch.distributed process group: rank 0
+    creates the NCCL unique id, torch broadcasts it (plumbing only)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [lq_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return lq_comm_init(obj[0], rank, world)
+
+
+def lq_sv_alloc_sharded(n_qubits: int, comm, stream=None):
+    h = _P()
+    _chk(_lib.lq_sv_alloc_sharded(n_qubits, comm, _stream_ptr(stream), ctypes.byref(h)))
+    return h
+
+
+def lq_sv_alloc_group(n_qubits: int, world: int, stream=None):
+    h = _P()
+    _chk(_lib.lq_sv_alloc_group(n_qubits, world, _stream_ptr(stream), ctypes.byref(h)))
+    return h
+
+
+def lq_sv_shard_info(h) -> Tuple[int, int, int, int]:
+    """(log2 world, first rank held here, shards held here, rank relabel xmask)"""
+    m, r, k, x = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_uint32()
+    _chk(_lib.lq_sv_shard_info(h, ctypes.byref(m), ctypes.byref(r), ctypes.byref(k), ctypes.byref(x)))
+    return m.value, r.value, k.value, x.value
+
+
+def lq_sv_shard_ptr(h, k: int) -> int:
+    return _lib.lq_sv_shard_ptr(h, k)
+
+
+def lq_dist_schedule_json(n_qubits: int, log2_world: int, gates, qft: int = 0, terms=()) -> dict:
+    import json
+    ga = gates if isinstance(gates, GateArray) else GateArray(gates)
+    ta = terms if isinstance(terms, TermArray) else TermArray(terms)
+    need = ctypes.c_size_t()
+    _chk(_lib.lq_dist_schedule_json(n_qubits, log2_world, ga.ptr, ga.n, qft, ta.ptr, ta.n, None, 0,
+                                    ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _chk(_lib.lq_dist_schedule_json(n_qubits, log2_world, ga.ptr, ga.n, qft, ta.ptr, ta.n, buf, len(buf),
+                                    ctypes.byref(need)))
+    return json.loads(buf.value.decode())
+
+
+class ShardedState:
+    """A state sharded over 2^m ranks (library-owned shards).  ``comm`` = an
+    lq_comm (one process per GPU, NCCL), or ``group_world`` = G shards held
+    by this process (device-copy exchanges on one GPU).  Calls are
+    collective across the comm's ranks."""
+
+    def __init__(self, n_qubits: int, comm=None, group_world: Optional[int] = None, stream=None):
+        self.n = n_qubits
+        if comm is not None:
+            self.h = lq_sv_alloc_sharded(n_qubits, comm, stream)
+        else:
+            self.h = lq_sv_alloc_group(n_qubits, int(group_world), stream)
+
+    def free(self):
+        if self.h is not None:
+            lq_sv_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def init_basis(self, k: int):
+        lq_sv_init_basis(self.h, k)
+        return self
+
+    def init_random(self, seed: int):
+        lq_sv_init_random(self.h, seed)
+        return self
+
+    def apply(self, gates, theta=None):
+        lq_apply_circuit(self.h, gates, theta)
+        return self
+
+    def qft(self, inverse: bool = False):
+        lq_qft(self.h, inverse)
+        return self
+
+    def expval(self, terms) -> float:
+        return lq_expval_pauli_sum(self.h, terms)
+
+    def read(self, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
+        return lq_sv_read(self.h, offset, count)
+
+    def gather(self, idx) -> np.ndarray:
+        return lq_sv_gather(self.h, idx)
+
+    def norm2(self) -> float:
+        return lq_sv_norm2(self.h)
+
+    def qubit_map(self) -> List[int]:
+        return lq_sv_qubit_map(self.h)
+
+    def shard_info(self):
+        return lq_sv_shard_info(self.h)
 
 
 # ---- convenience: a torch-owned state ---------------------------------------

@@ -200,18 +200,20 @@ def _apply_op(x, g, op, S, mats, cstc, n, et_all, et0):
     return 0.0
 
 
-def run(plan, psi, theta=None, shift=None):
+def run(plan, psi, theta=None, shift=None, gofs=0):
     """Run the plan on the physical-layout state psi (modified in place).
     Returns the Pauli-sum value accumulated by the plan's K_EXPV ops plus the
-    wide groups (direct)."""
-    n, K = plan["n"], plan["K"]
+    wide groups (direct).  For a shard of a distributed state psi holds the
+    2^nl local amplitudes and gofs the shard's physical global bits (they
+    enter the logic index only, as in the kernels)."""
+    n, K = plan.get("nl", plan["n"]), plan["K"]
     mats, cstc = build_mats(plan, theta if theta is not None else np.zeros(0), shift)
     subs, kops, perms, pts = plan["subs"], plan["kops"], plan["perms"], plan["perm_terms"]
     et_all = plan["eterms"]
     E = 0.0
     for p in plan["passes"]:
         if p["kind"] != PASS_TILE:
-            gidx = np.arange(psi.size, dtype=np.int64)
+            gidx = np.arange(psi.size, dtype=np.int64) | gofs
             for op in kops[p["op_begin"]:p["op_end"]]:
                 # physical form: b0/b1 are bits, controls in cmask
                 S_phys = [op["b0"], op["b1"], 0, 0]
@@ -235,6 +237,7 @@ def run(plan, psi, theta=None, shift=None):
                 tb |= ((tile >> i) & 1) << b
             g = tb | dep
             x = psi[g].copy()
+            tb |= gofs   # logic index of the tile (controls / phases on global bits)
 
             def apply_perm(x, pi):
                 P = perms[p["perm_begin"] + pi]
@@ -250,7 +253,7 @@ def run(plan, psi, theta=None, shift=None):
                 if sb["perm"] >= 0:
                     x = apply_perm(x, sb["perm"])
                 for op in kops[sb["op_begin"]:sb["op_end"]]:
-                    E += _apply_op(x, g, op, sb["S"], mats, cstc, n, et_all, p["eterm_begin"])
+                    E += _apply_op(x, g | gofs, op, sb["S"], mats, cstc, plan["n"], et_all, p["eterm_begin"])
             if p["store_perm"] >= 0:
                 x = apply_perm(x, p["store_perm"])
             if not (p["flags"] & PF_NO_STORE):
@@ -261,7 +264,7 @@ def run(plan, psi, theta=None, shift=None):
         G = plan["groups"][gi]
         w = np.conj(psi[j ^ G["x"]]) * psi
         for c, z, y in G["terms"]:
-            E += c * np.sum((1 - 2 * _parity(j & int(z))) * (w * (1j ** y)).real)
+            E += c * np.sum((1 - 2 * _parity((j | gofs) & int(z))) * (w * (1j ** y)).real)
     return E
 
 

@@ -1,0 +1,152 @@
+"""Distributed (sharded-state) host logic on CPU: the schedules of dist.cpp
+executed by a per-rank emulator -- in one process over G shards, and over
+two processes with torch.distributed gloo (global/local
+classification, rank relabels, Belady swaps, expectation on shards) --
+against the CPU oracle.  No GPU involved."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import dist_emulator as DE
+import workloads as W
+from test_gpu_parity import rich_circuit
+
+
+@pytest.fixture(scope="module")
+def lq():
+    from paper_2512_23183_b200 import lq as _lq
+    return _lq
+
+
+TOL = 1e-12
+
+
+@pytest.mark.parametrize("n,m", [(6, 1), (8, 2), (9, 3)])
+def test_group_rich_circuit(lq, oracle, n, m):
+    rng = np.random.default_rng(40 + n)
+    gates = [g for g in rich_circuit(n, 80, rng)]
+    sched = lq.lq_dist_schedule_json(n, m, gates)
+    psi0 = oracle.init_random(n, 11 + n)
+    got, _ = DE.run_group(sched, psi0.copy())
+    ref = oracle.init_random(n, 11 + n)
+    oracle.apply_circuit(ref, gates)
+    assert np.abs(got - ref).max() <= TOL
+    assert sched["n_swaps"] > 0
+
+
+@pytest.mark.parametrize("m", [1, 2])
+def test_group_config5_twin_with_qft(lq, oracle, m):
+    """The config-5 generator (30 % of gates on global qubits) + full QFT."""
+    n = 10
+    w = W.config5(n, m, 200)
+    for qft in (1, -1):
+        sched = lq.lq_dist_schedule_json(n, m, w.gates, qft=qft)
+        psi0 = oracle.init_random(n, w.seed)
+        got, _ = DE.run_group(sched, psi0.copy())
+        ref = oracle.init_random(n, w.seed)
+        oracle.apply_circuit(ref, w.gates)
+        oracle.qft(ref, inverse=qft < 0)
+        assert np.abs(got - ref).max() <= TOL
+
+
+def test_expval_rejects_too_wide_x(lq):
+    from paper_2512_23183_b200.lq import LQError
+    with pytest.raises(LQError):
+        lq.lq_dist_schedule_json(4, 2, [], terms=[(1.0, 0b111, 0)])
+
+
+def test_global_x_and_y_are_relabels(lq, oracle):
+    n, m = 6, 2
+    gates = [("H", 3, -1, -1, 0.0), ("X", 0, -1, -1, 0.0), ("Y", 1, -1, -1, 0.0), ("CNOT", 0, 4, -1, 0.0),
+             ("RZ", 1, -1, -1, 0.7), ("CZ", 0, 1, -1, 0.0), ("X", 1, -1, -1, 0.0)]
+    sched = lq.lq_dist_schedule_json(n, m, gates)
+    assert sched["n_relabels"] == 3 and sched["n_swaps"] == 0 and sched["xmask"] != 0
+    psi0 = oracle.init_random(n, 5)
+    got, _ = DE.run_group(sched, psi0.copy())
+    ref = oracle.init_random(n, 5)
+    oracle.apply_circuit(ref, gates)
+    assert np.abs(got - ref).max() <= TOL
+
+
+def test_group_expval(lq, oracle):
+    n, m = 9, 2
+    rng = np.random.default_rng(8)
+    gates = rich_circuit(n, 40, rng)
+    # a term may act with X/Y on at most n - m qubits (a shard's worth: its
+    # pairs (j, j ^ x) must fit on one rank after swaps)
+    terms = [t for t in W.random_pauli_sum(n, 40, rng) if bin(t[1]).count("1") <= n - m][:25]
+    assert any(t[1] & ((1 << m) - 1) for t in terms)   # some X/Y on global qubits (q < m)
+    sched = lq.lq_dist_schedule_json(n, m, gates, terms=terms)
+    psi0 = oracle.init_random(n, 21)
+    _, E = DE.run_group(sched, psi0.copy())
+    ref = oracle.init_random(n, 21)
+    oracle.apply_circuit(ref, gates)
+    eo = oracle.expval(ref, terms)
+    assert abs(E - eo) <= 1e-10 * max(1.0, abs(eo))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, n, m, seed, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2512_23183_b200 import lq
+    w = W.config5(n, m, 150)
+    terms = W.xyz_terms(n)
+    sched = lq.lq_dist_schedule_json(n, m, w.gates, qft=1, terms=terms)
+    nl = sched["nl"]
+    psi = oracle.init_random(n, w.seed)[rank << nl:(rank + 1) << nl].copy()
+
+    def exchange(send, peer):
+        t_send = torch.from_numpy(send.view(np.float64).copy())
+        t_recv = torch.empty_like(t_send)
+        reqs = [dist.isend(t_send, peer), dist.irecv(t_recv, peer)]
+        for r in reqs:
+            r.wait()
+        return t_recv.numpy().view(np.complex128)
+
+    E = 0.0
+    for st in sched["steps"]:
+        E += DE.run_step(sched, st, psi, rank, exchange=exchange)
+    e = torch.tensor([E], dtype=torch.float64)
+    dist.all_reduce(e)
+    shards = [torch.empty(2 << nl, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(shards, torch.from_numpy(psi.view(np.float64).copy()))
+    if rank == 0:
+        full = DE.assemble(sched, [s.numpy().view(np.complex128) for s in shards])
+        q.put((full, float(e[0])))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_config5_twin_qft_expval(oracle):
+    """world_size 2 over gloo: each process runs its shard; swaps are real
+    point-to-point exchanges; the energy is an all-reduce."""
+    import torch.multiprocessing as mp
+    n, m, world = 9, 1, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, n, m, 0, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    full, E = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    w = W.config5(n, m, 150)
+    ref = oracle.init_random(n, w.seed)
+    oracle.apply_circuit(ref, w.gates)
+    oracle.qft(ref)
+    assert np.abs(full - ref).max() <= TOL
+    eo = oracle.expval(ref, W.xyz_terms(n))
+    assert abs(E - eo) <= 1e-10 * max(1.0, abs(eo))
