@@ -703,7 +703,10 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
             n_full += ops[i].diag() ? 0 : 1;
             has_expv |= ops[i].type == K_EXPV;
         }
-        if (n_full == 0) {
+        if (n_full == 0 && !has_expv && absorbed.size() == 1) {
+            // a lone diagonal op: k_diag (one complex multiply per amplitude).
+            // Longer diagonal runs go to tile passes, which apply factors on
+            // bits outside the register set once per thread, not per amplitude.
             PlanPass pp;
             pp.kind = PASS_DIAG;
             pp.op_begin = (uint32_t)plan.kops.size();

@@ -911,7 +911,10 @@ __device__ __forceinline__ void tile_body(const KPass &P, const KSub *__restrict
 // SSTORE, STORE_PERM; and generated functions dep(l) (local index ->
 // physical bits), tbase(g) (tile index -> the physical bits outside the
 // tile), ainv<p>(l) and binv<p>(tile base) (permutation p's inverse map and
-// its tile-dependent translation).  Every shared-memory slot offset and global offset
+// its tile-dependent translation), and swz(x), the pass's shared-memory
+// swizzle: x ^ (a GF(2)-linear function of x >> 3 into the low 3 bits), chosen
+// by jit.cpp so that the 8 lanes of every quarter-warp hit distinct 16-byte
+// bank groups in every exchange of the pass.  Every shared-memory slot offset and global offset
 // of a register then folds to a constant; per tile only the tile base, one
 // XOR per register access and one add per global address remain.
 __host__ __device__ constexpr int nth_set_bit(uint32_t m, int i) {
@@ -937,16 +940,16 @@ __device__ __forceinline__ uint32_t ins_zeros(uint32_t t) {   // thread -> local
     return t;
 }
 // registers -> shared slots of mapping SMm (pending flips folded into the address)
-template <int RR, int K, uint32_t SMm>
+template <int RR, class D, uint32_t SMm>
 __device__ __forceinline__ void xwrite_c(double2 *b, const double2 (&a)[1 << RR], uint32_t t, uint32_t fb) {
-    const uint32_t slt = swz(ins_zeros<SMm, K>(t));
+    const uint32_t slt = D::swz(ins_zeros<SMm, D::K>(t));
     uint32_t adj = 0;
 #pragma unroll
     for (int i = 0; i < RR; i++)
-        if ((fb >> i) & 1) adj ^= swz(1u << nth_set_bit(SMm, i));
+        if ((fb >> i) & 1) adj ^= D::swz(1u << nth_set_bit(SMm, i));
     const uint32_t base = slt ^ adj;
     Unroll<RR>::run([&](auto V) {
-        constexpr uint32_t so = swz(loff_c<SMm>(decltype(V)::value));
+        constexpr uint32_t so = D::swz(loff_c<SMm>(decltype(V)::value));
         b[base ^ so] = a[decltype(V)::value];
     });
 }
@@ -957,16 +960,16 @@ __device__ __forceinline__ void xread_c(const double2 *b, double2 (&a)[1 << RR],
                                         uint64_t gofs) {
     const uint32_t lt = ins_zeros<SMm, D::K>(t);
     if constexpr (PI < 0) {
-        const uint32_t base = swz(lt);
+        const uint32_t base = D::swz(lt);
         Unroll<RR>::run([&](auto V) {
-            constexpr uint32_t so = swz(loff_c<SMm>(decltype(V)::value));
+            constexpr uint32_t so = D::swz(loff_c<SMm>(decltype(V)::value));
             if constexpr (ZERO) a[decltype(V)::value] = make_double2(((tb | gofs) == 0 && (base ^ so) == 0) ? 1.0 : 0.0, 0.0);
             else a[decltype(V)::value] = b[base ^ so];
         });
     } else {
-        const uint32_t base = swz(D::template ainv<PI>(lt) ^ D::template binv<PI>(tb | gofs));
+        const uint32_t base = D::swz(D::template ainv<PI>(lt) ^ D::template binv<PI>(tb | gofs));
         Unroll<RR>::run([&](auto V) {
-            constexpr uint32_t so = swz(D::template ainv<PI>(loff_c<SMm>(decltype(V)::value)));
+            constexpr uint32_t so = D::swz(D::template ainv<PI>(loff_c<SMm>(decltype(V)::value)));
             if constexpr (ZERO) a[decltype(V)::value] = make_double2(((tb | gofs) == 0 && (base ^ so) == 0) ? 1.0 : 0.0, 0.0);
             else a[decltype(V)::value] = b[base ^ so];
         });
@@ -980,7 +983,7 @@ __device__ __forceinline__ void run_subs_c(double2 (&a)[1 << RR], double2 *b, TS
         if constexpr (S > 0 && (D::SM[S] != D::SM[S - 1] || D::PERM[S] >= 0)) {
             materialize<RR>(a, ts, false);
             __syncthreads();   // everyone has read the previous mapping's slots
-            xwrite_c<RR, D::K, D::SM[S - 1]>(b, a, t, ts.fb);
+            xwrite_c<RR, D, D::SM[S - 1]>(b, a, t, ts.fb);
             ts.fb = 0;
             __syncthreads();
             xread_c<RR, D, D::SM[S], D::PERM[S], false>(b, a, t, tb, gofs);
@@ -1012,14 +1015,14 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
     for (uint32_t k = t; k < net; k += blockDim.x) s_et[k] = eterms[P.eterm_begin + k];
     const bool zero = P.flags & PF_LOAD_ZERO;
     const uint64_t dep_t = D::dep(t);
-    const uint32_t sw_t = swz(t);
+    const uint32_t sw_t = D::swz(t);
     const uint32_t tmask = (1u << tiles_log2) - 1u;
     auto issue = [&](uint32_t g, double2 *buf) {
         const double2 *psi = state + (uint64_t)(g >> tiles_log2) * state_stride + D::tbase(g & tmask) + dep_t;
         Unroll<RR>::run([&](auto V) {
             constexpr uint32_t l = (uint32_t)decltype(V)::value * NT;
             constexpr uint64_t o = D::dep(l);
-            cp_async16(buf + (sw_t ^ swz(l)), psi + o);
+            cp_async16(buf + (sw_t ^ D::swz(l)), psi + o);
         });
     };
     uint32_t g = blockIdx.x;
@@ -1069,7 +1072,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         if constexpr (!need_x) ex = __syncthreads_or(ts.fb != 0);
         if (ex) {
             if constexpr (need_x) __syncthreads();
-            xwrite_c<RR, K, D::SM[LAST]>(b, a, t, ts.fb);
+            xwrite_c<RR, D, D::SM[LAST]>(b, a, t, ts.fb);
             __syncthreads();
             xread_c<RR, D, D::SSTORE, D::STORE_PERM, false>(b, a, t, tb, P.gofs);
         }
