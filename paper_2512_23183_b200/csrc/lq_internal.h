@@ -57,7 +57,9 @@ enum KOpType : uint8_t {
     K_QFT = 6,  // QFT stage on register bit r0 (logical bit qj); aux = twiddle table
     K_SCALE = 7, // multiply every amplitude by `scale`
     K_EXPV = 8,  // Pauli-group expectation contribution (read-only; see ETerm)
-    K_G = 9      // scaled 2x2 rotation on register bit r0 (RY / RX / H, see GKind)
+    K_G = 9,     // scaled 2x2 rotation on register bit r0 (RY / RX / H, see GKind)
+    K_DT = 10    // run of uncontrolled register-bit diagonals as one 16-entry phase table (flags = count;
+                 // mat = offset in cst of the members' (register position, table offset) pairs)
 };
 
 // Scaled rotation families (K_G; qj holds the family).  Every matrix is
@@ -111,7 +113,8 @@ enum CodeTile : uint8_t {
     C_EXPV = 35,     // Pauli group: rcm = x mask in register positions, mat/aux = ETerm range
     C_G = 36,        // + 4*GKind + r0: scaled rotation on a register bit, no register control
     C_D1U = 48,      // diagonal on a bit outside the tile, controls outside the tile (tile-uniform factor)
-    C_NUM = 49
+    C_DT = 49,       // K_DT phase table
+    C_NUM = 50
 };
 
 // KOp.flags bits for diagonal ops (QF_* are QFT-only)
@@ -174,6 +177,7 @@ LQ_HD inline int op_table_size(uint8_t type) {
     case K_QFT: return 16;
     case K_SCALE: return 1;
     case K_G: return 2;
+    case K_DT: return 17;     // prod d0, then T[v] = prod over members with bit set of d1/d0
     default: return 0;
     }
 }

@@ -344,6 +344,8 @@ static uint8_t tile_code(const KOp &k) {
         break;
     case K_SCALE:
         return C_SCALE;
+    case K_DT:
+        return C_DT;
     case K_EXPV:
         return C_EXPV;
     default:
@@ -472,6 +474,41 @@ static void lower_expv(const POp &o, const LocalMap &L, const uint8_t *S, int Rr
     pp.kp.flags |= PF_EXPV;
 }
 
+// Runs of >= 2 consecutive uncontrolled diagonals on distinct register bits
+// become one K_DT op: 15 complex multiplies per thread instead of 8 per
+// member.  Members are recorded in the plan constants as (position, offset).
+static void merge_diag_runs(Plan &plan, uint32_t begin, MatBuilder &mb) {
+    auto simple = [](const KOp &k) { return k.type == K_D1 && k.rcm == 0 && k.cmask == 0 && k.r0 < R; };
+    std::vector<KOp> out;
+    for (size_t i = begin; i < plan.kops.size();) {
+        size_t j = i;
+        uint32_t pos = 0;
+        while (j < plan.kops.size() && simple(plan.kops[j]) && !(pos >> plan.kops[j].r0 & 1)) {
+            pos |= 1u << plan.kops[j].r0;
+            j++;
+        }
+        if (j - i >= 2) {
+            std::vector<double> mem;
+            for (size_t q = i; q < j; q++) {
+                mem.push_back((double)plan.kops[q].r0);
+                mem.push_back((double)plan.kops[q].mat);
+            }
+            KOp d{};
+            d.type = K_DT;
+            d.r0 = d.r1 = NOREG;
+            d.flags = (uint8_t)(j - i);
+            d.mat = (uint32_t)mb.add_const(mem.data(), (int)(j - i));
+            out.push_back(d);
+            i = j;
+        } else {
+            out.push_back(plan.kops[i]);
+            i++;
+        }
+    }
+    plan.kops.resize(begin);
+    plan.kops.insert(plan.kops.end(), out.begin(), out.end());
+}
+
 static int32_t build_perm(const std::vector<POp> &ops, const std::vector<int> &group, const LocalMap &L,
                           const PlanPass &pp, Plan &plan) {
     if (group.empty()) return -1;
@@ -501,7 +538,7 @@ static int32_t build_perm(const std::vector<POp> &ops, const std::vector<int> &g
 // permutations being folded into the exchange that starts the sub-block.
 static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vector<POp> &ops,
                       const std::vector<int> &absorbed, const std::vector<uint32_t> &mat_off,
-                      Plan &plan) {
+                      Plan &plan, MatBuilder &mb) {
     LocalMap L(Tm);
     int lowrun = (nl > K) ? lowrun_of(L) : 0;
     PlanPass pp;
@@ -582,6 +619,7 @@ static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vect
             else all_expv = false;
             plan.kops.push_back(k);
         }
+        merge_diag_runs(plan, sb.op_begin, mb);
         sb.op_end = (uint32_t)plan.kops.size();
         plan.subs.push_back(sb);
     }
@@ -602,7 +640,7 @@ static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vect
 
 }  // namespace
 
-void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, const MatBuilder &mb,
+void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, MatBuilder &mb,
                   Plan &plan) {
     std::vector<uint32_t> mat_off;
     for (auto &sp : mb.specs) mat_off.push_back(sp.out);
@@ -632,7 +670,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
             if (o.type == K_EXPV) {
                 uint64_t Tm = mand | o.xm;
                 for (int b = 0; b < nl && popc(Tm) < K; b++) Tm |= bit(b);
-                emit_tile(n, nl, K, Rr, Tm, ops, std::vector<int>{(int)i}, mat_off, plan);
+                emit_tile(n, nl, K, Rr, Tm, ops, std::vector<int>{(int)i}, mat_off, plan, mb);
                 continue;
             }
             PlanPass pp;
@@ -728,7 +766,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, co
             // fill the tile to exactly K bits, lowest free bits first (longer
             // contiguous runs for coalescing)
             for (int b = 0; b < nl && popc(Tm) < K; b++) Tm |= bit(b);
-            emit_tile(n, nl, K, Rr, Tm, ops, absorbed, mat_off, plan);
+            emit_tile(n, nl, K, Rr, Tm, ops, absorbed, mat_off, plan, mb);
         }
         // remove absorbed from rem (absorbed is a subsequence of rem)
         std::vector<int> left;

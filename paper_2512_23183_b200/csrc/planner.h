@@ -95,7 +95,7 @@ void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
 void canonicalize_ops(int n, int32_t *qmap, std::vector<POp> &ops);
 
 // Plan generic passes for `ops`.
-void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, const MatBuilder &mb,
+void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, MatBuilder &mb,
                   Plan &plan);
 
 // Pauli groups of a Pauli sum (bit q of a mask = qubit q -> physical

@@ -651,6 +651,17 @@ __device__ __forceinline__ void exec_op(double2 (&a)[1 << RR], const KOp &op, co
             const double2 tt = qft_thread_twiddle(op, gbase, n, ts.ttmax, ts.lg);
             ap_qft<RR, P>(a, tt, M, op.flags & QF_INVERSE);
         }
+    } else if constexpr (CODE == C_DT) {
+        // several register-bit diagonals at once: one complex multiply per
+        // amplitude (v = 0 is 1), their d0 product joins the tile scalar
+        ts.tsc = cmul(ts.tsc, M[0]);
+        if (ts.fb == 0) {
+#pragma unroll
+            for (int v = 1; v < (1 << RR); v++) a[v] = cmul(a[v], M[1 + v]);
+        } else {
+#pragma unroll
+            for (int v = 0; v < (1 << RR); v++) a[v] = cmul(a[v], M[1 + (v ^ ts.fb)]);
+        }
     } else if constexpr (CODE == C_SCALE) {
         ts.tsc = cscale(ts.tsc, M[0].x);
     } else if constexpr (CODE == C_EXPV) {
@@ -668,7 +679,7 @@ __device__ __forceinline__ void exec_op(double2 (&a)[1 << RR], const KOp &op, co
 #define LQ_OP_CODES(X)                                                                                    \
     X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17)   \
     X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32) X(33)     \
-    X(34) X(35) X(36) X(37) X(38) X(39) X(40) X(41) X(42) X(43) X(44) X(45) X(46) X(47) X(48)
+    X(34) X(35) X(36) X(37) X(38) X(39) X(40) X(41) X(42) X(43) X(44) X(45) X(46) X(47) X(48) X(49)
 
 // The interpreter: walks the sub-block's op list in shared memory.
 struct InterpProg {
@@ -691,6 +702,30 @@ struct InterpProg {
         }
     }
 };
+
+// Stage one op's table into shared memory (once per circuit per CTA): a copy
+// of the circuit's matrices (M) or of the plan constants (cst); a K_DT table
+// is built here from its members' diagonal tables (d0, d1, d1/d0).
+__device__ __forceinline__ void stage_table(const KOp &o, double2 *s_tab, const double2 *M, const double2 *cst) {
+    if (o.type == K_DT) {
+        double2 T[16], D0 = make_double2(1.0, 0.0);
+        for (int v = 0; v < 16; v++) T[v] = make_double2(1.0, 0.0);
+        for (int i = 0; i < (int)o.flags; i++) {
+            const double2 mem = cst[o.mat + i];   // (register position, table offset)
+            const int pos = (int)mem.x;
+            const double2 *d = M + (uint32_t)mem.y;
+            D0 = cmul(D0, d[0]);
+            for (int v = 0; v < 16; v++)
+                if ((v >> pos) & 1) T[v] = cmul(T[v], d[2]);
+        }
+        s_tab[o.aux] = D0;
+        for (int v = 0; v < 16; v++) s_tab[o.aux + 1 + v] = T[v];
+        return;
+    }
+    const int sz = op_table_size(o.type);
+    const double2 *src = ((o.type == K_QFT || o.type == K_SCALE) ? cst : M) + o.mat;
+    for (int e = 0; e < sz; e++) s_tab[o.aux + e] = src[e];
+}
 
 template <int RR>
 __device__ __forceinline__ uint32_t smask(const uint8_t *S) {
@@ -813,9 +848,7 @@ __device__ __forceinline__ void tile_body(const KPass &P, const KSub *__restrict
             for (uint32_t k = t; k < nops; k += blockDim.x) {
                 const KOp o = ops[P.op_begin + k];
                 s_ops[k] = o;
-                const int sz = op_table_size(o.type);
-                const double2 *src = ((o.type == K_QFT || o.type == K_SCALE) ? cst : M) + o.mat;
-                for (int e = 0; e < sz; e++) s_tab[o.aux + e] = src[e];
+                stage_table(o, s_tab, M, cst);
             }
             cur_circ = circ;
         }
@@ -1038,12 +1071,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         const int circ = (int)(g >> tiles_log2);
         if (circ != cur_circ) {   // (re)stage this circuit's op tables
             const double2 *M = mats + (uint64_t)circ * mat_stride;
-            for (uint32_t k = t; k < nops; k += blockDim.x) {
-                const KOp o = ops[P.op_begin + k];
-                const int sz = op_table_size(o.type);
-                const double2 *src = ((o.type == K_QFT || o.type == K_SCALE) ? cst : M) + o.mat;
-                for (int e = 0; e < sz; e++) s_tab[o.aux + e] = src[e];
-            }
+            for (uint32_t k = t; k < nops; k += blockDim.x) stage_table(ops[P.op_begin + k], s_tab, M, cst);
             cur_circ = circ;
         }
         cp_async_wait1();

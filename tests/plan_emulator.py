@@ -14,7 +14,7 @@ import math
 import numpy as np
 
 NOREG = 255
-K_U1, K_D1, K_X, K_U2, K_D2, K_SWAP, K_QFT, K_SCALE, K_EXPV, K_G = range(10)
+K_U1, K_D1, K_X, K_U2, K_D2, K_SWAP, K_QFT, K_SCALE, K_EXPV, K_G, K_DT = range(11)
 GK_REAL, GK_IMAG, GK_HAD = range(3)
 FK_YDIAG = 100
 PASS_TILE, PASS_PAIR, PASS_DIAG = 0, 1, 2
@@ -115,6 +115,14 @@ def _apply_op(x, g, op, S, mats, cstc, n, et_all, et0):
     """One lowered op on a tile vector x (index = local l), g = global index."""
     typ = op["type"]
     lb = lambda r: 1 << S[r]
+    if typ == K_DT:   # members (register position, table offset) in the plan constants
+        L = np.arange(x.size, dtype=np.int64)
+        for k in range(op["flags"]):
+            m = cstc[op["mat"] + k]
+            pos, off = int(m.real), int(m.imag)
+            bit = (L >> S[pos]) & 1
+            x *= np.where(bit == 1, mats[off + 1], mats[off])
+        return 0.0
     M = mats[op["mat"]:op["mat"] + 16] if typ in (K_U1, K_D1, K_U2, K_D2, K_G) else None
     if typ == K_G:   # lambda * M (lq_internal.h GKind)
         p, lam, alt = M[0].real, M[0].imag, M[1].real != 0
