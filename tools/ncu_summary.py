@@ -1,0 +1,42 @@
+"""Summarise an ncu --set full report of the tile-pass launches of one
+config-4 batch (2 circuits per launch) into profiles/ncu_k_tile_summary.json:
+per launch dram read+write bytes vs the algorithmic bytes of that pass."""
+import csv, io, json, os, subprocess, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+rep, out, src = sys.argv[1], sys.argv[2], sys.argv[3]
+txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(txt)))
+h, units, data = rows[0], rows[1], rows[2:]
+col = {k: i for i, k in enumerate(h)}
+def val(r, k):
+    v = r[col[k]].replace(",", "")
+    x = float(v) if v else 0.0
+    u = units[col[k]]
+    return x * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "ns": 1e-3, "us": 1, "ms": 1e3}.get(u, 1)
+import workloads as W
+from paper_2512_23183_b200 import lq
+w = W.config4()
+plan = lq.lq_plan_export_json(w.n, w.gates, w.terms)
+N = 1 << w.n
+B = 2
+passes = plan["passes"]
+launches = []
+for i, r in enumerate(data):
+    if i >= len(passes):
+        break
+    p = passes[i]
+    load = i > 0
+    store = not (p["flags"] & 4) and i + 1 < len(passes)
+    alg = B * N * 16 * (int(load) + int(store))
+    dr, dw = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
+    launches.append({"pass": i, "us": round(val(r, "gpu__time_duration.sum"), 2), "dram_read": dr, "dram_write": dw,
+                     "alg_bytes": alg, "traffic_over_alg": round((dr + dw) / alg, 4),
+                     "fp64_pipe_pct": round(val(r, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"), 1),
+                     "regs": int(val(r, "launch__registers_per_thread")), "grid": int(val(r, "launch__grid_size"))})
+tot_dram = sum(l["dram_read"] + l["dram_write"] for l in launches)
+tot_alg = sum(l["alg_bytes"] for l in launches)
+s = {"source": src, "n_qubits": w.n, "circuits_per_launch": B, "launches": len(launches),
+     "dram_bytes_per_launch": tot_dram / len(launches), "algorithmic_bytes_per_launch": tot_alg / len(launches),
+     "traffic_over_algorithmic": tot_dram / tot_alg, "per_launch": launches}
+json.dump(s, open(out, "w"), indent=1)
+print(json.dumps({k: v for k, v in s.items() if k != "per_launch"}))
