@@ -19,6 +19,7 @@ int nondiag_qubits(const lq_gate &G, int *q) {
     case LQ_CZ: case LQ_CP: case LQ_RZZ: case LQ_SWAP:
         return 0;
     case LQ_CNOT: case LQ_CRY: q[0] = G.q1; return 1;
+    case LQK_QFT_STAGE: q[0] = G.q0; return 1;
     case LQ_CCX: q[0] = G.q2; return 1;
     case LQ_U2: case LQ_RXX: case LQ_RYY: q[0] = G.q0; q[1] = G.q1; return 2;
     default: q[0] = G.q0; return 1;   // H X Y RX RY U1
@@ -142,7 +143,6 @@ void schedule_gates(Schedule &sc, const lq_gate *gates, size_t ng, int32_t *qmap
 }
 
 std::vector<lq_gate> qft_gates(int n, bool inverse) {
-    const double PI = 3.14159265358979323846264338327950288;
     std::vector<lq_gate> g;
     auto mk = [](int kind, int a, int b, double ang) {
         lq_gate x;
@@ -156,15 +156,13 @@ std::vector<lq_gate> qft_gates(int n, bool inverse) {
         x.mat = nullptr;
         return x;
     };
-    for (int i = 0; i < n; i++) {
-        g.push_back(mk(LQ_H, i, -1, 0.0));
-        for (int j = i + 1; j < n; j++) g.push_back(mk(LQ_CP, j, i, PI / std::ldexp(1.0, j - i)));
-    }
+    // Alg. 3: stage i = H(i) then CP(pi / 2^(k-i)), k > i -- one op each
+    for (int i = 0; i < n; i++) g.push_back(mk(LQK_QFT_STAGE, i, -1, 1.0));
     for (int i = 0; i < n / 2; i++) g.push_back(mk(LQ_SWAP, i, n - 1 - i, 0.0));
     if (inverse) {
         std::reverse(g.begin(), g.end());
         for (auto &x : g)
-            if (x.kind == LQ_CP) x.angle = -x.angle;
+            if (x.kind == LQK_QFT_STAGE) x.angle = -1.0;
     }
     return g;
 }

@@ -47,9 +47,10 @@ struct Schedule {
 // and xmask are updated to the layout after the circuit.
 void schedule_gates(Schedule &sc, const lq_gate *gates, size_t n_gates, int32_t *qmap, uint32_t &xmask);
 
-// Alg. 3 as gates: H(i), CP(pi / 2^(j-i)) control j ->
-// target i for j > i, then the SWAP layer; inverse: the reversed sequence
-// with negated phases.
+// Alg. 3 as n stage ops (LQK_QFT_STAGE: H(i) and the CPs
+// controlled by the later qubits, one butterfly-with-twiddle each) followed
+// by the SWAP layer (relabels); inverse: the reversed sequence of inverse
+// stages.
 std::vector<lq_gate> qft_gates(int n, bool inverse);
 
 // LOCAL steps (expv = true) whose K_EXPV ops evaluate the Pauli sum

@@ -1227,9 +1227,11 @@ lq_status lq_sv_canonicalize(lq_sv *sv) {
     return canonicalize(sv);
 }
 
-lq_status lq_apply_circuit(lq_sv *sv, const lq_gate *gates, size_t n_gates, const double *theta, size_t n_theta) {
-    LQ_TRY(check_sv(sv));
-    LQ_TRY(validate_gates(sv->n, gates, n_gates, theta, n_theta, true, nullptr));
+}  // extern "C"
+
+namespace {
+// apply already-validated gates (internal kinds allowed)
+lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const double *theta, size_t n_theta) {
     if (!n_gates) return LQ_OK;
     if (sv->m) {
         Schedule sc;
@@ -1256,13 +1258,18 @@ lq_status lq_apply_circuit(lq_sv *sv, const lq_gate *gates, size_t n_gates, cons
     memcpy(sv->qmap, qm, sizeof(qm));
     return LQ_OK;
 }
+}  // namespace
+
+extern "C" {
+
+lq_status lq_apply_circuit(lq_sv *sv, const lq_gate *gates, size_t n_gates, const double *theta, size_t n_theta) {
+    LQ_TRY(check_sv(sv));
+    LQ_TRY(validate_gates(sv->n, gates, n_gates, theta, n_theta, true, nullptr));
+    return apply_impl(sv, gates, n_gates, theta, n_theta);
+}
 
 lq_status lq_qft(lq_sv *sv, int inverse) {
     LQ_TRY(check_sv(sv));
-    if (sv->m) {   // Alg. 3 as gates through the distributed scheduler
-        std::vector<lq_gate> g = qft_gates(sv->n, inverse != 0);
-        return lq_apply_circuit(sv, g.data(), g.size(), nullptr, 0);
-    }
     int32_t qm[64];
     memcpy(qm, sv->qmap, sizeof(qm));
     bool ident = true, rev = true;
@@ -1270,9 +1277,11 @@ lq_status lq_qft(lq_sv *sv, int inverse) {
         ident &= qm[q] == sv->n - 1 - q;
         rev &= qm[q] == q;
     }
-    if (!ident && !rev) {
-        LQ_TRY(canonicalize(sv));
-        memcpy(qm, sv->qmap, sizeof(qm));
+    if (sv->m || (!ident && !rev)) {
+        // sharded or permuted layout: Alg. 3's stages as generic ops (any
+        // layout; the scheduler swaps global qubits in), SWAP layer = relabel
+        std::vector<lq_gate> g = qft_gates(sv->n, inverse != 0);
+        return apply_impl(sv, g.data(), g.size(), nullptr, 0);
     }
     Plan plan;
     MatBuilder mb;

@@ -74,11 +74,17 @@ enum GKind : uint8_t { GK_REAL = 0, GK_IMAG = 1, GK_HAD = 2 };
 
 // Internal factor kinds (beyond lq_kind) used by the matrix builder.
 constexpr int FK_YDIAG = 100;   // diag(i, -i): Y = X * diag(i, -i)
+// Internal gate kind (never accepted at the ABI): one QFT stage of Alg. 3 --
+// H on qubit q0 then every CP(pi / 2^(k - q0)) controlled by qubit k > q0 --
+// as a single butterfly-with-twiddle op; angle < 0: the inverse stage.
+constexpr int LQK_QFT_STAGE = 200;
 
 enum KOpFlags : uint8_t {
     QF_INVERSE = 1,   // inverse stage (conj twiddle before the butterfly)
     QF_REVERSED = 2,  // layout is bit-reversed (logical index = brev(physical))
-    QF_HEAD = 4       // first QFT op of its sub-block: compute the thread twiddle for j = b1
+    QF_HEAD = 4,      // first QFT op of its sub-block: compute the thread twiddle for j = b1
+    QF_GENERAL = 8,   // any layout: logical index from the pass's physical->logical map (KPass::lpos)
+    QF_SCALE = 16     // the stage carries its own 1/sqrt(2) (deferred into the tile scalar)
 };
 
 // One op inside a sub-block.  Controls on register bits are the register
@@ -199,6 +205,7 @@ struct KPass {
     uint8_t Sload[R];    // (unused by the persistent kernel; kept for layout)
     uint8_t Sstore[R];   // local bits of the register mapping used for the HBM store
     uint8_t pad[6];
+    uint8_t lpos[64];    // QFT stages (QF_GENERAL): logical bit held by physical bit p (255: none)
 };
 
 // Matrix construction (device-side, per circuit): every fused op has a

@@ -22,7 +22,7 @@ uint64_t POp::full() const {
 }
 
 uint64_t POp::touch() const {
-    uint64_t m = ctrl | full();
+    uint64_t m = ctrl | full() | rd;
     if (type == K_EXPV) m |= zm;
     if (type == K_D1) m |= bit(t0);
     if (type == K_D2) m |= bit(t0) | bit(t1);
@@ -122,6 +122,26 @@ void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
             }
             continue;
         }
+        if (k == LQK_QFT_STAGE) {   // Alg. 3 stage as one op (reads the qubits after q0 diagonally)
+            POp op;
+            op.type = K_QFT;
+            op.t0 = qmap[G.q0];
+            op.qj = (uint8_t)(n - 1 - G.q0);
+            op.qflags = QF_GENERAL | QF_SCALE | (G.angle < 0 ? QF_INVERSE : 0);
+            for (int q = G.q0 + 1; q < n; q++) op.rd |= bit(qmap[q]);
+            std::vector<uint8_t> lp(64, 255);
+            for (int q = 0; q < n; q++) lp[qmap[q]] = (uint8_t)(n - 1 - q);
+            int li = -1;
+            for (size_t x = 0; x < mb.layouts.size(); x++)
+                if (mb.layouts[x] == lp) li = (int)x;
+            if (li < 0) { mb.layouts.push_back(lp); li = (int)mb.layouts.size() - 1; }
+            op.layout = li;
+            ops.push_back(op);
+            fl.push_back({});
+            fusable.push_back(0);
+            touch_all((int)ops.size() - 1);
+            continue;
+        }
         POp op;
         switch (k) {
         case LQ_CNOT: op.type = K_X; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); break;
@@ -143,7 +163,7 @@ void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
     for (size_t i = base; i < ops.size(); i++) {
         POp &P = ops[i];
         auto &F = fl[i - base];
-        if (P.type == K_X) { P.spec = -1; continue; }
+        if (P.type == K_X || P.type == K_QFT) { P.spec = -1; continue; }
         MForm form = P.type == K_D1 ? MF_DIAG2 : P.type == K_U1 ? MF_U2x2 : P.type == K_G ? MF_G
                    : P.type == K_U2 ? MF_U4x4 : MF_DIAG4;
         P.spec = mb.add_spec(form, F);
@@ -509,6 +529,43 @@ static void merge_diag_runs(Plan &plan, uint32_t begin, MatBuilder &mb) {
     plan.kops.insert(plan.kops.end(), out.begin(), out.end());
 }
 
+// Generic QFT stages (QF_GENERAL) of a sub-block: register twiddle table of
+// each stage for this register set, the sub-block head (thread twiddle at the
+// largest j), and the pass's physical -> logical map.
+static void lower_qft_stages(Plan &plan, const KSub &sb, const LocalMap &L, int Rr, const std::vector<POp> &ops,
+                             const std::vector<int> &taken, MatBuilder &mb, PlanPass &pp) {
+    int jmax = -1, layout = -1;
+    for (int i : taken)
+        if (ops[i].type == K_QFT && ops[i].layout >= 0) { jmax = std::max(jmax, (int)ops[i].qj); layout = ops[i].layout; }
+    if (layout < 0) return;
+    const std::vector<uint8_t> &lp = mb.layouts[layout];
+    for (int b = 0; b < 64; b++) pp.kp.lpos[b] = lp[b];
+    bool head = true;
+    for (uint32_t k = sb.op_begin; k < plan.kops.size(); k++) {
+        KOp &op = plan.kops[k];
+        if (op.type != K_QFT || !(op.flags & QF_GENERAL)) continue;
+        const int j = op.qj;
+        const bool inv = op.flags & QF_INVERSE;
+        double tab[2 * NREG];
+        for (int v = 0; v < NREG; v++) {
+            uint64_t lg = 0;
+            for (int i = 0; i < Rr; i++)
+                if (v & (1 << i)) {
+                    const int p = L.T[sb.S[i]];
+                    if (lp[p] < 64) lg |= bit(lp[p]);
+                }
+            const uint64_t Lm = (j == 0) ? 0 : (lg & (bit(j) - 1));
+            const long double ang = 3.141592653589793238462643383279502884L * (long double)Lm / ldexpl(1.0L, j);
+            tab[2 * v] = (double)cosl(ang);
+            tab[2 * v + 1] = (inv ? -1.0 : 1.0) * (double)sinl(ang);
+        }
+        op.mat = (uint32_t)mb.add_const(tab, NREG);
+        op.b1 = (uint8_t)jmax;
+        if (head) op.flags |= QF_HEAD;
+        head = false;
+    }
+}
+
 static int32_t build_perm(const std::vector<POp> &ops, const std::vector<int> &group, const LocalMap &L,
                           const PlanPass &pp, Plan &plan) {
     if (group.empty()) return -1;
@@ -547,6 +604,7 @@ static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vect
     pp.kp.nl = nl;
     pp.kp.K = K;
     pp.kp.flags = 0;
+    memset(pp.kp.lpos, 255, sizeof(pp.kp.lpos));
     memcpy(pp.kp.T, L.T, MAXK);
     pp.kp.sub_begin = (uint32_t)plan.subs.size();
     pp.kp.perm_begin = (uint32_t)plan.perms.size();
@@ -620,6 +678,7 @@ static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vect
             plan.kops.push_back(k);
         }
         merge_diag_runs(plan, sb.op_begin, mb);
+        lower_qft_stages(plan, sb, L, Rr, ops, sg.taken, mb, pp);
         sb.op_end = (uint32_t)plan.kops.size();
         plan.subs.push_back(sb);
     }
@@ -639,6 +698,10 @@ static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vect
 }
 
 }  // namespace
+
+// op types the strided pair kernel (k_pair) executes; everything else
+// (QFT stages, ...) runs in a tile pass even when alone
+static bool pair_kernel_op(uint8_t t) { return t == K_U1 || t == K_X || t == K_G || t == K_U2 || t == K_SWAP; }
 
 void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, MatBuilder &mb,
                   Plan &plan) {
@@ -667,8 +730,8 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
         for (size_t i = 0; i < ops.size(); i++) {
             const POp &o = ops[i];
             if (skip[i]) continue;
-            if (o.type == K_EXPV) {
-                uint64_t Tm = mand | o.xm;
+            if (o.type == K_EXPV || (!o.diag() && !pair_kernel_op(o.type))) {
+                uint64_t Tm = mand | o.full() | (o.type == K_EXPV ? o.xm : 0);
                 for (int b = 0; b < nl && popc(Tm) < K; b++) Tm |= bit(b);
                 emit_tile(n, nl, K, Rr, Tm, ops, std::vector<int>{(int)i}, mat_off, plan, mb);
                 continue;
@@ -753,7 +816,8 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
             pp.n_ops = (int)absorbed.size();
             plan.passes.push_back(pp);
             plan.n_diag++;
-        } else if (absorbed.size() == 1 && !has_expv && (nl > K || popc(ops[absorbed[0]].full()) > K)) {
+        } else if (absorbed.size() == 1 && !has_expv && pair_kernel_op(ops[absorbed[0]].type) &&
+                   (nl > K || popc(ops[absorbed[0]].full()) > K)) {
             PlanPass pp;
             pp.kind = PASS_PAIR;
             pp.op_begin = (uint32_t)plan.kops.size();
@@ -835,6 +899,7 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
         pp.kp.n = n;
         pp.kp.nl = n;
         pp.kp.K = K;
+        memset(pp.kp.lpos, 255, sizeof(pp.kp.lpos));
         memcpy(pp.kp.T, L.T, MAXK);
         pp.kp.sub_begin = (uint32_t)plan.subs.size();
         pp.kp.perm_begin = pp.kp.perm_end = (uint32_t)plan.perms.size();
@@ -949,7 +1014,9 @@ std::string export_json(const Plan &plan, const MatBuilder &mb, const int32_t *q
           << ",\"K\":" << k.K << ",\"sub_begin\":" << k.sub_begin << ",\"sub_end\":" << k.sub_end
           << ",\"kop_begin\":" << k.op_begin << ",\"kop_end\":" << k.op_end << ",\"perm_begin\":" << k.perm_begin
           << ",\"store_perm\":" << k.store_perm << ",\"eterm_begin\":" << k.eterm_begin << ",\"eslot\":" << k.eslot
-          << ",\"flags\":" << k.flags << ",\"T\":[";
+          << ",\"flags\":" << k.flags << ",\"lpos\":[";
+        for (int b = 0; b < 64; b++) o << (b ? "," : "") << (int)k.lpos[b];
+        o << "],\"T\":[";
         for (int b = 0; b < (p.kind == PASS_TILE ? k.K : 0); b++) o << (b ? "," : "") << (int)k.T[b];
         o << "],\"Sstore\":[" << (int)k.Sstore[0] << "," << (int)k.Sstore[1] << "," << (int)k.Sstore[2] << ","
           << (int)k.Sstore[3] << "]}";

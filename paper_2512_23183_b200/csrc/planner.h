@@ -26,6 +26,8 @@ struct POp {
     double scale = 1.0;
     uint64_t xm = 0, zm = 0;  // K_EXPV: group x mask, union of the terms' z masks (physical)
     int group = -1;           // K_EXPV: index into Plan::groups
+    uint64_t rd = 0;          // bits read diagonally without being controls (QFT stage twiddle inputs)
+    int layout = -1;          // K_QFT (QF_GENERAL): index into MatBuilder::layouts
     uint64_t full() const;    // bits on which the op is not diagonal
     uint64_t touch() const;   // every bit the op reads
     bool diag() const { return type == K_D1 || type == K_D2 || type == K_SCALE; }
@@ -72,6 +74,7 @@ struct MatBuilder {
     std::vector<MSpec> specs;
     std::vector<MFactor> factors;
     std::vector<double> cst;      // constant complex entries (re, im) -- U1/U2 user matrices, QFT twiddles
+    std::vector<std::vector<uint8_t>> layouts;   // physical -> logical bit maps (64 entries, 255 = none)
     uint32_t mat_size = 0;        // per-circuit matrix block size (double2 units)
     int add_spec(MForm form, const std::vector<MFactor> &f);
     int add_const(const double *re_im_pairs, int n_complex);

@@ -301,6 +301,7 @@ struct TState {
     double2 tsc, ph;
     double2 ttmax;     // QFT twiddle state of the current sub-block
     uint64_t lg;
+    const uint8_t *lpos;   // physical -> logical bit map of the pass (QF_GENERAL stages)
     __device__ __forceinline__ void reset() {
         fb = 0;
         hph = false;
@@ -369,11 +370,19 @@ __device__ __forceinline__ void ap_qft(double2 (&a)[1 << RR], double2 tt, const 
 // sincospi per sub-block (at its largest j), then the exact recurrence
 // tt_{k-1} = tt_k^2 (-1)^{bit k-1 of Lt}.
 __device__ __forceinline__ double2 qft_thread_twiddle(const KOp &op, uint64_t gbase, int n, double2 &ttmax,
-                                                      uint64_t &lg) {
+                                                      uint64_t &lg, const uint8_t *lpos) {
     const bool inv = op.flags & QF_INVERSE;
     if (op.flags & QF_HEAD) {
         const int jm = op.b1;
-        lg = (op.flags & QF_REVERSED) ? (__brevll(gbase) >> (64 - n)) : gbase;
+        if (op.flags & QF_GENERAL) {   // logical bits of this thread's base index
+            lg = 0;
+            for (uint64_t g = gbase; g; g &= g - 1) {
+                const uint32_t l = lpos[__ffsll((long long)g) - 1];
+                if (l < 64) lg |= 1ull << l;
+            }
+        } else {
+            lg = (op.flags & QF_REVERSED) ? (__brevll(gbase) >> (64 - n)) : gbase;
+        }
         const uint64_t Lt = (jm == 0) ? 0ull : (lg & ((1ull << jm) - 1));
         double s, c;
         sincospi(ldexp((double)Lt, -jm), &s, &c);
@@ -648,8 +657,9 @@ __device__ __forceinline__ void exec_op(double2 (&a)[1 << RR], const KOp &op, co
         constexpr int P = CODE - C_QFT;
         if constexpr (RR > P) {
             flush_flips<RR>(a, ts.fb);
-            const double2 tt = qft_thread_twiddle(op, gbase, n, ts.ttmax, ts.lg);
+            const double2 tt = qft_thread_twiddle(op, gbase, n, ts.ttmax, ts.lg, ts.lpos);
             ap_qft<RR, P>(a, tt, M, op.flags & QF_INVERSE);
+            if (op.flags & QF_SCALE) ts.tsc = cscale(ts.tsc, 0.70710678118654752440);
         }
     } else if constexpr (CODE == C_DT) {
         // several register-bit diagonals at once: one complex multiply per
@@ -888,6 +898,7 @@ __device__ __forceinline__ void tile_body(const KPass &P, const KSub *__restrict
         }
         TState ts;
         ts.reset();
+        ts.lpos = P.lpos;
         for (uint32_t s = P.sub_begin; s < P.sub_end; s++) {
             if (s != P.sub_begin) {
                 sb = s_sub[s - P.sub_begin];
@@ -1083,6 +1094,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         else xread_c<RR, D, D::SM[0], D::PERM[0], false>(b, a, t, tb, P.gofs);
         TState ts;
         ts.reset();
+        ts.lpos = P.lpos;
         run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, P.gofs, t, s_tab, s_et, P.n);
         double2 *psi = state + (uint64_t)circ * state_stride;
         if (P.flags & PF_EXPV) {   // one deterministic partial per tile

@@ -20,7 +20,7 @@ FK_YDIAG = 100
 PASS_TILE, PASS_PAIR, PASS_DIAG = 0, 1, 2
 MF_U2x2, MF_DIAG2, MF_U4x4, MF_DIAG4, MF_G = range(5)
 PF_EXPV, PF_NO_STORE = 2, 4
-QF_INVERSE, QF_REVERSED = 1, 2
+QF_INVERSE, QF_REVERSED, QF_GENERAL, QF_SCALE = 1, 2, 8, 16
 # lq_kind numbering
 (LQ_H, LQ_X, LQ_Y, LQ_Z, LQ_S, LQ_SDG, LQ_T, LQ_TDG, LQ_RX, LQ_RY, LQ_RZ, LQ_CNOT, LQ_CZ, LQ_CP,
  LQ_SWAP, LQ_U1, LQ_U2, LQ_CRY, LQ_CCX, LQ_RXX, LQ_RYY, LQ_RZZ) = range(22)
@@ -111,7 +111,16 @@ def _brev(x, n):
     return r
 
 
-def _apply_op(x, g, op, S, mats, cstc, n, et_all, et0):
+def _logical(g, lpos):
+    """Logical index bits of physical indices g under a pass's lpos map."""
+    out = np.zeros_like(g)
+    for p, l in enumerate(lpos):
+        if l < 64:
+            out |= ((g >> p) & 1) << l
+    return out
+
+
+def _apply_op(x, g, op, S, mats, cstc, n, et_all, et0, lpos=None):
     """One lowered op on a tile vector x (index = local l), g = global index."""
     typ = op["type"]
     lb = lambda r: 1 << S[r]
@@ -172,7 +181,10 @@ def _apply_op(x, g, op, S, mats, cstc, n, et_all, et0):
         m = lb(op["r0"])
         j = op["qj"]
         inv = bool(op["flags"] & QF_INVERSE)
-        lg = _brev(g, n) if op["flags"] & QF_REVERSED else g
+        if op["flags"] & QF_GENERAL:
+            lg = _logical(g, lpos)
+        else:
+            lg = _brev(g, n) if op["flags"] & QF_REVERSED else g
         l0 = L[(L & m) == 0]
         l1 = l0 | m
         Lt = (lg[l1] & ((1 << j) - 1)) if j > 0 else np.zeros(l1.size, np.int64)
@@ -183,6 +195,8 @@ def _apply_op(x, g, op, S, mats, cstc, n, et_all, et0):
         else:
             y = w * tw
             x[l0], x[l1] = u + y, u - y
+        if op["flags"] & QF_SCALE:
+            x *= 1 / np.sqrt(2)
     elif typ == K_SCALE:
         x *= cstc[op["mat"]].real
     elif typ == K_EXPV:
@@ -261,7 +275,8 @@ def run(plan, psi, theta=None, shift=None, gofs=0):
                 if sb["perm"] >= 0:
                     x = apply_perm(x, sb["perm"])
                 for op in kops[sb["op_begin"]:sb["op_end"]]:
-                    E += _apply_op(x, g | gofs, op, sb["S"], mats, cstc, plan["n"], et_all, p["eterm_begin"])
+                    E += _apply_op(x, g | gofs, op, sb["S"], mats, cstc, plan["n"], et_all, p["eterm_begin"],
+                                   p.get("lpos"))
             if p["store_perm"] >= 0:
                 x = apply_perm(x, p["store_perm"])
             if not (p["flags"] & PF_NO_STORE):

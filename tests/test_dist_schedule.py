@@ -150,3 +150,24 @@ def test_gloo_two_ranks_config5_twin_qft_expval(oracle):
     assert np.abs(full - ref).max() <= TOL
     eo = oracle.expval(ref, W.xyz_terms(n))
     assert abs(E - eo) <= 1e-10 * max(1.0, abs(eo))
+
+
+@pytest.mark.parametrize("K", [4, 6])
+def test_group_small_tiles_single_op_passes(lq, oracle, K):
+    """Tiles much smaller than a shard: LOCAL steps with a lone QFT stage or
+    gate must become tile passes (k_pair runs only 1q/2q matrix gates)."""
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
+    try:
+        n, m = 11, 2
+        w = W.config5(n, m, 120)
+        sched = lq.lq_dist_schedule_json(n, m, w.gates, qft=1)
+        kinds = {p["kind"] for s in sched["steps"] if s["kind"] == "local" for p in s["plan"]["passes"]}
+        psi0 = oracle.init_random(n, w.seed)
+        got, _ = DE.run_group(sched, psi0.copy())
+    finally:
+        lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 0)
+    ref = oracle.init_random(n, w.seed)
+    oracle.apply_circuit(ref, w.gates)
+    oracle.qft(ref)
+    assert np.abs(got - ref).max() <= TOL
+    assert 0 in kinds

@@ -89,3 +89,22 @@ def test_jit_psr_config3_and_ring(lq, oracle):
     which = [0, 5, 13, 30, 47]
     go = oracle.param_shift_grad(n, gates, theta, terms, which=which)
     grad_close(g[which], go)
+
+
+@pytest.mark.parametrize("jit", [0, 2])
+def test_qft_on_permuted_layout(lq, oracle, jit):
+    """SWAP gates leave a permuted qubit map; the QFT then runs as generic
+    Alg. 3 stage ops with a physical->logical map (no canonicalisation)."""
+    lq.lq_set_option(lq.LQ_OPT_JIT, jit)
+    n = 15
+    rng = np.random.default_rng(5)
+    perm = [("SWAP", int(a), int(b), -1, 0.0) for a, b in (rng.choice(n, 2, replace=False) for _ in range(9))]
+    gates = perm + [("H", 3, -1, -1, 0.0), ("CNOT", 3, 11, -1, 0.0)]
+    for inverse in (False, True):
+        sv = lq.StateVector(n)
+        sv.init_random(8).apply(gates).qft(inverse=inverse)
+        ref = oracle.init_random(n, 8)
+        oracle.apply_circuit(ref, gates)
+        oracle.qft(ref, inverse=inverse)
+        assert np.abs(sv.read() - ref).max() <= AMP_TOL
+        sv.free()
