@@ -269,10 +269,12 @@ typedef enum {
     LQ_OPT_COALESCE_BITS = 2, /* low physical bits every strided tile includes (default 3) */
     LQ_OPT_REG_BITS = 3,      /* amplitudes per thread in tile passes = 2^value, 3 or 4 (default 4) */
     LQ_OPT_KERNEL_TIMING = 4, /* 1: bracket every launch with CUDA events on its stream (lq_kernel_timing) */
-    LQ_OPT_JIT = 5            /* tile passes as per-plan specialised kernels compiled with NVRTC for
+    LQ_OPT_JIT = 5,           /* tile passes as per-plan specialised kernels compiled with NVRTC for
                                  sm_100a (cached per process) instead of the op-list interpreter kernel;
                                  both execute the same device op templates (tile.cuh).  0: off;
                                  1 (default): auto -- PSR plans and states with n >= 26; 2: always. */
+    LQ_OPT_PASS_BUDGET = 6    /* planner: estimated FP64 instructions per amplitude (x10) a tile pass may
+                                 absorb before it stops (default 400; 0 = no limit, absorb greedily) */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);

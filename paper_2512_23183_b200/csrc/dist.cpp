@@ -36,7 +36,7 @@ int all_qubits(const lq_gate &G, int *q) {
 
 }  // namespace
 
-void schedule_gates(Schedule &sc, const lq_gate *gates, size_t ng, int32_t *qmap, uint32_t &xmask) {
+bool schedule_gates(Schedule &sc, const lq_gate *gates, size_t ng, int32_t *qmap, uint32_t &xmask) {
     const int n = sc.n, nl = sc.nl;
     // future non-diagonal uses of each logical qubit (Belady victim choice)
     std::vector<std::vector<size_t>> uses(n);
@@ -122,6 +122,7 @@ void schedule_gates(Schedule &sc, const lq_gate *gates, size_t ng, int32_t *qmap
                     best_next = nu;
                 }
             }
+            if (best < 0) return false;
             DStep sw;
             sw.kind = 1;
             sw.g = g;
@@ -140,6 +141,7 @@ void schedule_gates(Schedule &sc, const lq_gate *gates, size_t ng, int32_t *qmap
     }
     flush(ng, nullptr);
     for (int j = 0; j < n; j++) qmap[j] = qm[j];
+    return true;
 }
 
 std::vector<lq_gate> qft_gates(int n, bool inverse) {

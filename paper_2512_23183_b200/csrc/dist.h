@@ -45,7 +45,9 @@ struct Schedule {
 
 // Append the steps of `gates` to `sc`; qmap (logical -> physical, n entries)
 // and xmask are updated to the layout after the circuit.
-void schedule_gates(Schedule &sc, const lq_gate *gates, size_t n_gates, int32_t *qmap, uint32_t &xmask);
+// Returns false (schedule unusable) if a gate cannot be made local -- only
+// possible when a shard holds fewer than 3 qubits (sh_check forbids that).
+bool schedule_gates(Schedule &sc, const lq_gate *gates, size_t n_gates, int32_t *qmap, uint32_t &xmask);
 
 // Alg. 3 as n stage ops (LQK_QFT_STAGE: H(i) and the CPs
 // controlled by the later qubits, one butterfly-with-twiddle each) followed

@@ -39,6 +39,7 @@ std::atomic<int64_t> g_opt_K{0};
 std::atomic<int64_t> g_opt_coalesce{3};
 std::atomic<int64_t> g_opt_regbits{4};
 std::atomic<int64_t> g_opt_jit{1};
+std::atomic<int64_t> g_opt_budget{400};   // keeps first passes from turning FP64-bound
 const double PI = 3.14159265358979323846264338327950288;
 
 lq_status fail(lq_status s, const std::string &msg) {
@@ -130,6 +131,7 @@ PlanOptions options() {
     o.coalesce = (int)g_opt_coalesce.load();
     o.fusion = g_opt_fusion.load() != 0;
     o.reg_bits = (int)g_opt_regbits.load();
+    o.budget = (int)g_opt_budget.load();
     return o;
 }
 
@@ -583,7 +585,8 @@ NcclApi &nccl() {
 lq_status sh_check(int n, int world) {
     if (world < 2 || (world & (world - 1))) return fail(LQ_ERR_ARG, "world size must be a power of two >= 2");
     int m = __builtin_ctz((unsigned)world);
-    if (n - m < 1) return fail(LQ_ERR_ARG, "state has fewer qubits than log2(world)");
+    // a shard must hold the target and both controls of any gate (CCX)
+    if (n - m < 3) return fail(LQ_ERR_ARG, "each shard must hold at least 3 qubits (n - log2(world) >= 3)");
     if (m > 16) return fail(LQ_ERR_ARG, "at most 2^16 shards");
     return LQ_OK;
 }
@@ -847,6 +850,10 @@ lq_status lq_set_option(int option, int64_t value) {
     case LQ_OPT_KERNEL_TIMING:
         g_opt_timing = value ? 1 : 0;
         return LQ_OK;
+    case LQ_OPT_PASS_BUDGET:
+        if (value < 0 || value > 100000) return fail(LQ_ERR_ARG, "pass budget must be 0..100000");
+        g_opt_budget = value;
+        return LQ_OK;
     case LQ_OPT_JIT:
         if (value < 0 || value > 2) return fail(LQ_ERR_ARG, "jit must be 0 (off), 1 (auto) or 2 (always)");
         g_opt_jit = value;
@@ -863,6 +870,7 @@ int64_t lq_get_option(int option) {
     case LQ_OPT_REG_BITS: return g_opt_regbits.load();
     case LQ_OPT_KERNEL_TIMING: return g_opt_timing.load();
     case LQ_OPT_JIT: return g_opt_jit.load();
+    case LQ_OPT_PASS_BUDGET: return g_opt_budget.load();
     default: return -1;
     }
 }
@@ -1004,8 +1012,8 @@ void *lq_sv_shard_ptr(const lq_sv *sv, int k) {
 lq_status lq_dist_schedule_json(int n_qubits, int log2_world, const lq_gate *gates, size_t n_gates, int qft,
                                 const lq_pauli_term *terms, size_t n_terms, char *buf, size_t buf_len,
                                 size_t *needed) {
-    if (n_qubits < 2 || n_qubits > 44 || log2_world < 1 || log2_world >= n_qubits)
-        return fail(LQ_ERR_ARG, "need 1 <= log2_world < n_qubits <= 44");
+    if (n_qubits < 2 || n_qubits > 44 || log2_world < 1 || n_qubits - log2_world < 3)
+        return fail(LQ_ERR_ARG, "need log2_world >= 1 and n_qubits - log2_world >= 3 (n_qubits <= 44)");
     LQ_TRY(validate_gates(n_qubits, gates, n_gates, nullptr, 1 << 16, false, nullptr));
     LQ_TRY(validate_terms(n_qubits, terms, n_terms));
     Schedule sc;
@@ -1015,10 +1023,10 @@ lq_status lq_dist_schedule_json(int n_qubits, int log2_world, const lq_gate *gat
     int32_t qm[64];
     for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
     uint32_t xm = 0;
-    schedule_gates(sc, gates, n_gates, qm, xm);
+    if (!schedule_gates(sc, gates, n_gates, qm, xm)) return fail(LQ_ERR_ARG, "shard too small for a gate");
     if (qft) {
         std::vector<lq_gate> g = qft_gates(n_qubits, qft < 0);
-        schedule_gates(sc, g.data(), g.size(), qm, xm);
+        if (!schedule_gates(sc, g.data(), g.size(), qm, xm)) return fail(LQ_ERR_ARG, "shard too small");
     }
     if (n_terms && !schedule_expval(sc, terms, n_terms, qm, xm))
         return fail(LQ_ERR_ARG, "a Pauli term acts with X/Y on more qubits than a shard holds");
@@ -1241,7 +1249,7 @@ lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const doub
         int32_t qm[64];
         memcpy(qm, sv->qmap, sizeof(qm));
         uint32_t xm = sv->xmask;
-        schedule_gates(sc, gates, n_gates, qm, xm);
+        if (!schedule_gates(sc, gates, n_gates, qm, xm)) return fail(LQ_ERR_ARG, "shard too small for a gate");
         LQ_TRY(sh_run(sv, sc, theta, n_theta, nullptr));
         memcpy(sv->qmap, qm, sizeof(qm));
         sv->xmask = xm;
@@ -1581,8 +1589,8 @@ std::string psr_key(int n, const lq_gate *g, size_t ng, size_t np, const lq_paul
     auto put = [&](const void *p, size_t b) { k.append(static_cast<const char *>(p), b); };
     int64_t hdr[8] = {n, (int64_t)ng, (int64_t)np, (int64_t)nt, rank, world, (int64_t)(intptr_t)stream, 0};
     put(hdr, sizeof(hdr));
-    int64_t opt[5] = {g_opt_fusion.load(), g_opt_K.load(), g_opt_coalesce.load(), g_opt_regbits.load(),
-                      g_opt_jit.load()};
+    int64_t opt[6] = {g_opt_fusion.load(), g_opt_K.load(), g_opt_coalesce.load(), g_opt_regbits.load(),
+                      g_opt_jit.load(), g_opt_budget.load()};
     put(opt, sizeof(opt));
     for (size_t i = 0; i < ng; i++) {
         put(&g[i], offsetof(lq_gate, mat));

@@ -35,6 +35,19 @@ bool commute(const POp &a, const POp &b) {
     return (a.full() & b.touch()) == 0 && (b.full() & a.touch()) == 0;
 }
 
+int op_fp64_cost(const POp &o) {
+    switch (o.type) {
+    case K_G: return 20;       // 4 DFMA per amplitude pair
+    case K_U1: return 80;      // general complex 2x2
+    case K_U2: return 160;     // general complex 4x4
+    case K_D1: return 12;      // register-bit half multiply / table share / thread constant
+    case K_D2: return 30;
+    case K_QFT: return 50;     // butterfly + twiddle multiply
+    case K_EXPV: return 30;    // pair products + Walsh-Hadamard share
+    default: return 0;         // X / CNOT / SWAP: folded permutations or flips
+    }
+}
+
 int MatBuilder::add_spec(MForm form, const std::vector<MFactor> &f) {
     MSpec s;
     s.out = mat_size;
@@ -226,14 +239,19 @@ struct Blocker {
 };
 
 // first-fit absorption of `rem` into a tile whose bit set starts at Tm.
+// Absorption stops at the pass's FP64 budget: a pass whose arithmetic
+// exceeds its HBM time is FP64-bound, and the ops it leaves behind fill
+// lighter passes later.
 static void first_fit(const std::vector<POp> &ops, const std::vector<int> &rem, int K,
-                      uint64_t &Tm, std::vector<int> &absorbed) {
+                      uint64_t &Tm, std::vector<int> &absorbed, int budget) {
     Blocker blk;
+    int cost = 0;
     for (int i : rem) {
         const POp &o = ops[i];
         if (blk.blocked(o)) { blk.add(o); continue; }
         uint64_t need = o.full() & ~Tm;
-        if (popc(Tm | need) <= K) { Tm |= need; absorbed.push_back(i); }
+        const int c = op_fp64_cost(o);
+        if (popc(Tm | need) <= K && (!budget || cost + c <= budget)) { Tm |= need; absorbed.push_back(i); cost += c; }
         else blk.add(o);
     }
 }
@@ -246,12 +264,15 @@ static int score(const std::vector<POp> &ops, const std::vector<int> &absorbed) 
 
 // Count ops absorbable with a FIXED tile bit set Tm.
 static void absorb_fixed(const std::vector<POp> &ops, const std::vector<int> &rem, uint64_t Tm,
-                         std::vector<int> &absorbed) {
+                         std::vector<int> &absorbed, int budget) {
     Blocker blk;
+    int cost = 0;
     for (int i : rem) {
         const POp &o = ops[i];
-        if (blk.blocked(o) || (o.full() & ~Tm)) { blk.add(o); continue; }
+        const int c = op_fp64_cost(o);
+        if (blk.blocked(o) || (o.full() & ~Tm) || (budget && cost + c > budget)) { blk.add(o); continue; }
         absorbed.push_back(i);
+        cost += c;
     }
 }
 
@@ -754,12 +775,12 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
     while (!rem.empty()) {
         uint64_t Tm = mand;
         std::vector<int> absorbed, absorbed_w;
-        first_fit(ops, rem, K, Tm, absorbed);
+        first_fit(ops, rem, K, Tm, absorbed, opt.budget);
         // local search works on a window of the next ops (bounded cost)
         std::vector<int> window(rem.begin(), rem.begin() + std::min<size_t>(rem.size(), 384));
         {
             std::vector<int> a0;
-            absorb_fixed(ops, window, Tm, a0);
+            absorb_fixed(ops, window, Tm, a0, opt.budget);
             absorbed_w.swap(a0);
         }
         int best = score(ops, absorbed_w);
@@ -775,7 +796,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
                         if (Tm & bit(in)) continue;
                         uint64_t T2 = (Tm & ~bit(out)) | bit(in);
                         std::vector<int> a2;
-                        absorb_fixed(ops, window, T2, a2);
+                        absorb_fixed(ops, window, T2, a2, opt.budget);
                         int s2 = score(ops, a2);
                         if (s2 > best) { best = s2; Tm = T2; improved = true; break; }
                     }
@@ -784,7 +805,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
                     for (int in = 0; in < nl && popc(Tm) < K; in++) {
                         if (Tm & bit(in)) continue;
                         std::vector<int> a2;
-                        absorb_fixed(ops, window, Tm | bit(in), a2);
+                        absorb_fixed(ops, window, Tm | bit(in), a2, opt.budget);
                         int s2 = score(ops, a2);
                         if (s2 > best) { best = s2; Tm |= bit(in); improved = true; }
                     }
@@ -793,7 +814,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
             }
             if (Tm != Tm0) {
                 absorbed.clear();
-                absorb_fixed(ops, rem, Tm, absorbed);
+                absorb_fixed(ops, rem, Tm, absorbed, opt.budget);
             }
         }
         if (absorbed.empty()) absorbed.push_back(rem[0]);   // progress guarantee

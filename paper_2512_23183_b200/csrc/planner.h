@@ -86,7 +86,11 @@ struct PlanOptions {
     bool fusion = true;      // false: one PAIR/DIAG pass per op
     int reg_bits = 4;        // register bits per thread (R); tile kernels run 2^(K-R) threads
     int n_local = 0;         // sharded state: only bits [0, n_local) are local (0 = all n bits)
+    int budget = 0;          // FP64 budget of a tile pass in tenths of an instruction per amplitude (0: none)
 };
+
+// Estimated FP64 instructions per amplitude (x10) an op costs in a tile pass.
+int op_fp64_cost(const POp &o);
 
 // Lower user gates (already validated) to POps on physical bits.  SWAP
 // gates update qmap (relabel) and emit nothing.  Adjacent 1q gates on the

@@ -35,8 +35,8 @@ STATUS_NAMES = {0: "LQ_OK", -1: "LQ_ERR_ARG", -2: "LQ_ERR_OOM", -3: "LQ_ERR_CUDA
 KIND_NAMES = ["H", "X", "Y", "Z", "S", "SDG", "T", "TDG", "RX", "RY", "RZ", "CNOT", "CZ", "CP",
               "SWAP", "U1", "U2", "CRY", "CCX", "RXX", "RYY", "RZZ"]
 KINDS = {k: i for i, k in enumerate(KIND_NAMES)}
-LQ_OPT_FUSION, LQ_OPT_TILE_BITS, LQ_OPT_COALESCE_BITS, LQ_OPT_REG_BITS, LQ_OPT_KERNEL_TIMING, LQ_OPT_JIT = \
-    0, 1, 2, 3, 4, 5
+LQ_OPT_FUSION, LQ_OPT_TILE_BITS, LQ_OPT_COALESCE_BITS, LQ_OPT_REG_BITS, LQ_OPT_KERNEL_TIMING, LQ_OPT_JIT, \
+    LQ_OPT_PASS_BUDGET = 0, 1, 2, 3, 4, 5, 6
 KC_TILE, KC_PAIR, KC_DIAG, KC_PAULI, KC_OTHER = 0, 1, 2, 3, 4
 
 

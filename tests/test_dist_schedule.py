@@ -171,3 +171,27 @@ def test_group_small_tiles_single_op_passes(lq, oracle, K):
     oracle.qft(ref)
     assert np.abs(got - ref).max() <= TOL
     assert 0 in kinds
+
+
+@pytest.mark.parametrize("n,m", [(4, 1), (5, 2), (6, 3), (7, 4)])
+def test_minimal_shards_every_gate_qft_expval(lq, oracle, n, m):
+    """Shards of 3 qubits (the minimum: a Toffoli's three qubits must fit):
+    every gate kind, QFT and a Pauli sum."""
+    rng = np.random.default_rng(n)
+    gates = rich_circuit(n, 40, rng)
+    terms = [t for t in W.random_pauli_sum(n, 8, rng) if bin(t[1]).count("1") <= n - m]
+    sched = lq.lq_dist_schedule_json(n, m, gates, qft=1, terms=terms)
+    got, E = DE.run_group(sched, oracle.init_random(n, 3))
+    ref = oracle.init_random(n, 3)
+    oracle.apply_circuit(ref, gates)
+    oracle.qft(ref)
+    assert np.abs(got - ref).max() <= TOL
+    eo = oracle.expval(ref, terms)
+    assert abs(E - eo) <= 1e-10 * max(1.0, abs(eo))
+
+
+def test_shards_smaller_than_three_qubits_rejected(lq):
+    from paper_2512_23183_b200.lq import LQError
+    for n, m in [(3, 1), (4, 2), (2, 1)]:
+        with pytest.raises(LQError):
+            lq.lq_dist_schedule_json(n, m, [])

@@ -43,7 +43,7 @@ def test_sharded_init_random_norm_read(lq, oracle, n, G):
     sv.free()
 
 
-@pytest.mark.parametrize("n,G,jit", [(10, 2, 0), (13, 4, 0), (16, 2, 2), (18, 8, 0)])
+@pytest.mark.parametrize("n,G,jit", [(10, 2, 0), (13, 4, 0), (16, 2, 2), (18, 8, 0), (6, 8, 0), (5, 4, 2)])
 def test_sharded_rich_circuit(lq, oracle, n, G, jit):
     lq.lq_set_option(lq.LQ_OPT_JIT, jit)
     rng = np.random.default_rng(900 + n)
@@ -100,6 +100,11 @@ def test_sharded_matches_unsharded_bitwise_layout_free(lq):
     assert np.abs(a.read() - b.read()).max() <= 1e-13
     a.free()
     b.free()
+
+
+def test_group_rejects_too_small_shards(lq):
+    with pytest.raises(lq.LQError):
+        lq.ShardedState(4, group_world=4)
 
 
 def test_nccl_loads_and_single_rank_comm(lq):

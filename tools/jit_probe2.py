@@ -12,6 +12,7 @@ st = torch.cuda.current_stream()
 lq.lq_set_option(lq.LQ_OPT_JIT, 2)
 ref = None
 cb = int(os.environ.get("LQ_COALESCE", "3"))
+lq.lq_set_option(lq.LQ_OPT_PASS_BUDGET, int(os.environ.get("LQ_BUDGET", "0")))
 lq.lq_set_option(lq.LQ_OPT_COALESCE_BITS, cb)
 for K in [int(k) for k in os.environ.get("KS", "12,11").split(",")]:
     lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
@@ -23,7 +24,7 @@ for K in [int(k) for k in os.environ.get("KS", "12,11").split(",")]:
     a.record(); lq.lq_psr_run(P, th.data_ptr(), g.data_ptr(), e.data_ptr()); b.record(); torch.cuda.synchronize()
     gg = g.cpu().numpy().copy()
     if ref is None: ref = gg
-    print(f"coalesce={cb} K={K}: create {tc:.1f}s  passes {lq.lq_psr_stats(P)[3]}  gradient {a.elapsed_time(b):.1f} ms  "
+    print(f"budget={lq.lq_get_option(lq.LQ_OPT_PASS_BUDGET)} coalesce={cb} K={K}: create {tc:.1f}s  passes {lq.lq_psr_stats(P)[3]}  gradient {a.elapsed_time(b):.1f} ms  "
           f"E={e.item():.15f}  max|dg| vs first {np.abs(gg-ref).max():.2e}", flush=True)
     lq.lq_psr_free(P)
 print("jit stats", lq.lq_jit_stats())

@@ -1,2 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-N=30 GS=1,2,4 timeout 1200 python tools/cfg5_probe.py 2>&1 | tail -3
+for b in 0 400 300 250; do LQ_BUDGET=$b KS=11 timeout 600 python tools/jit_probe2.py 2>&1 | grep "K="; done
