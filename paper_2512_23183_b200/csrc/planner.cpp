@@ -772,15 +772,18 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
     std::vector<int> rem;
     for (size_t i = 0; i < ops.size(); i++)
         if (!skip[i]) rem.push_back((int)i);
+    // the FP64 budget trades an extra HBM round trip for less arithmetic per
+    // pass; a state that is one tile has no HBM round trip to trade
+    const int budget = nl > K ? opt.budget : 0;
     while (!rem.empty()) {
         uint64_t Tm = mand;
         std::vector<int> absorbed, absorbed_w;
-        first_fit(ops, rem, K, Tm, absorbed, opt.budget);
+        first_fit(ops, rem, K, Tm, absorbed, budget);
         // local search works on a window of the next ops (bounded cost)
         std::vector<int> window(rem.begin(), rem.begin() + std::min<size_t>(rem.size(), 384));
         {
             std::vector<int> a0;
-            absorb_fixed(ops, window, Tm, a0, opt.budget);
+            absorb_fixed(ops, window, Tm, a0, budget);
             absorbed_w.swap(a0);
         }
         int best = score(ops, absorbed_w);
@@ -796,7 +799,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
                         if (Tm & bit(in)) continue;
                         uint64_t T2 = (Tm & ~bit(out)) | bit(in);
                         std::vector<int> a2;
-                        absorb_fixed(ops, window, T2, a2, opt.budget);
+                        absorb_fixed(ops, window, T2, a2, budget);
                         int s2 = score(ops, a2);
                         if (s2 > best) { best = s2; Tm = T2; improved = true; break; }
                     }
@@ -805,7 +808,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
                     for (int in = 0; in < nl && popc(Tm) < K; in++) {
                         if (Tm & bit(in)) continue;
                         std::vector<int> a2;
-                        absorb_fixed(ops, window, Tm | bit(in), a2, opt.budget);
+                        absorb_fixed(ops, window, Tm | bit(in), a2, budget);
                         int s2 = score(ops, a2);
                         if (s2 > best) { best = s2; Tm |= bit(in); improved = true; }
                     }
@@ -814,7 +817,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
             }
             if (Tm != Tm0) {
                 absorbed.clear();
-                absorb_fixed(ops, rem, Tm, absorbed, opt.budget);
+                absorb_fixed(ops, rem, Tm, absorbed, budget);
             }
         }
         if (absorbed.empty()) absorbed.push_back(rem[0]);   // progress guarantee
