@@ -224,9 +224,14 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
 
 /* g_p = ( E(theta + (pi/2) e_p) - E(theta - (pi/2) e_p) ) / 2 for the ansatz
  * ansatz[0..n_gates) run from |0...0> and the Pauli sum
- * terms.  Each parameter must be used by exactly one rotation gate
- * (reading A7); all 2*n_params shifted circuits are independent and are
- * batched.  shard_rank/shard_world: compute only parameters with
+ * terms.  A parameter of a controlled rotation (LQ_CRY: generator
+ * eigenvalues {0, +-1/2}, where the two-term rule is not exact, reading A8)
+ * takes the exact four-term rule
+ *   g_p = c1 (E(+pi/2) - E(-pi/2)) - c2 (E(+3pi/2) - E(-3pi/2)),
+ *   c1 = (sqrt2 + 1) / (4 sqrt2), c2 = (sqrt2 - 1) / (4 sqrt2)
+ * (shifts of theta_p; reading A8).  Each parameter must be used by
+ * exactly one rotation gate (reading A7); all shifted circuits are
+ * independent and are batched.  shard_rank/shard_world: compute only parameters with
  * p % shard_world == shard_rank (others are written as 0); the caller sums
  * the shards (e.g. torch.distributed.all_reduce).  energy_out (nullable)
  * receives E(theta) on shard 0 (0 elsewhere).  Host in/out (syncs). */
@@ -238,7 +243,9 @@ lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gate
 
 /* lq_param_shift_grad keeps the plans (and device buffers) of its two most
  * recent distinct (circuit, Hamiltonian, shard, stream, options) arguments
- * and reuses them; this frees them. */
+ * and reuses them, and lq_apply_circuit / lq_qft / lq_expval_pauli_sum keep
+ * the plans of their 32 most recent distinct (gates or terms, n, qubit
+ * map, options) arguments (theta is not part of a plan); this frees both. */
 lq_status lq_psr_cache_clear(void);
 
 /* Same computation split into a reusable plan and an asynchronous run on
@@ -249,6 +256,56 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
                         int shard_world, void *cuda_stream, lq_psr **out);
 lq_status lq_psr_run(lq_psr *plan, const double *theta_dev, double *grad_dev, double *energy_dev);
 lq_status lq_psr_free(lq_psr *plan);
+/* ---- Trotterised XYZ time evolution --- */
+
+typedef struct lq_xyz_model {
+    double jx, jy, jz;            /* couplings J_x, J_y, J_z */
+    double amp, omega;            /* field h(t) = amp * sin(omega * t) */
+} lq_xyz_model;
+
+/* Evolve sv in place under H(t) = -sum_{i<n-1} (J_x X_i X_{i+1} + J_y Y_i Y_{i+1}
+ * + J_z Z_i Z_{i+1}) - h(t) sum_i Z_i (Eq. 9, open chain) by n_steps
+ * first-order Trotter steps of size dt starting at time t0 (Eq. 12):
+ * step j applies RXX(-2 J_x dt) on every pair (i, i+1), i ascending, then
+ * RYY(-2 J_y dt), then RZZ(-2 J_z dt), then RZ(-2 h(t0 + j dt) dt) on every
+ * qubit (the gates of P:825-831 with the signs of Eq. 9, reading A20).  The
+ * caller prepares the initial state (the paper starts from |1...1>:
+ * lq_sv_init_basis(sv, 2^n - 1)).  energy_out (nullable, host):
+ * E(t) = <psi(t)|H(t)|psi(t)> (Eq. 13) at t0 and after every record_every
+ * steps -- 1 + n_steps / record_every values.  Sharded states are supported
+ * (the gates go through the usual scheduler).  LQ_ERR_ARG for n < 2, dt <= 0,
+ * n_steps < 0 or record_every < 1; LQ_ERR_NONFINITE for a non-finite model. */
+lq_status lq_trotter_xyz(lq_sv *sv, const lq_xyz_model *model, double t0, double dt, int n_steps,
+                         int record_every, double *energy_out);
+
+/* ---- VQE outer loop ---------------- */
+
+/* Adam settings.  The paper fixes lr = 1e-2, at most 350 iterations and a
+ * convergence tolerance of 1e-7; beta1 = 0.9, beta2 = 0.999,
+ * eps = 1e-8 are Adam's standard constants. */
+typedef struct lq_adam_cfg {
+    double lr, beta1, beta2, eps, tol;
+    int32_t max_iter;
+    int32_t reserved;             /* must be 0 */
+} lq_adam_cfg;
+
+/* Minimise E(theta) = <0|U(theta)^+ H U(theta)|0> for the ansatz and Pauli
+ * sum (same rules as lq_param_shift_grad) with Adam on parameter-shift
+ * gradients: for t = 0, 1, ...: evaluate E_t and g_t at theta^t (one batched
+ * gradient, "2 N_theta circuit evaluations per gradient");
+ * stop if t >= 1 and |E_t - E_{t-1}| < tol, or t == max_iter; otherwise
+ * theta^{t+1} = theta^t - lr m_hat / (sqrt(v_hat) + eps) with
+ * m = beta1 m + (1 - beta1) g, v = beta2 v + (1 - beta2) g^2,
+ * m_hat = m / (1 - beta1^{t+1}), v_hat = v / (1 - beta2^{t+1}).
+ * theta: host, in/out (n_params; the final iterate).  energy_trace
+ * (nullable, host, >= max_iter + 1 entries): E_0 .. E_T.  iters_out
+ * (nullable): T = number of Adam updates taken.  One GPU; syncs every
+ * iteration (8 bytes).  LQ_ERR_NONFINITE for non-finite settings, theta or
+ * an energy (with its iteration index in lq_last_error). */
+lq_status lq_vqe_adam(int n_qubits, const lq_gate *ansatz, size_t n_gates, double *theta, size_t n_params,
+                      const lq_pauli_term *terms, size_t n_terms, const lq_adam_cfg *cfg, void *cuda_stream,
+                      double *energy_trace, int32_t *iters_out);
+
 /* Accounting for one lq_psr_run on this shard: circuits evaluated, kernel
  * launches issued (by the last run), bytes of the uploaded plan, tile passes
  * per circuit.  Any output pointer may be NULL. */
@@ -297,6 +354,10 @@ lq_status lq_plan_export_json(int n_qubits, const lq_gate *gates, size_t n_gates
  * empty).  No device needed; LQ_ERR_CUDA with the compiler log on failure. */
 lq_status lq_jit_compile_check(int n_qubits, const lq_gate *gates, size_t n_gates, const lq_pauli_term *terms,
                                size_t n_terms, uint64_t *n_kernels);
+
+/* Host-only: the same for the JIT pass programs of the QFT (inverse != 0:
+ * QFT^-1) on n qubits in the identity layout. */
+lq_status lq_qft_jit_compile_check(int n_qubits, int inverse, uint64_t *n_kernels);
 
 /* Accumulated device time of launches made while LQ_OPT_KERNEL_TIMING was
  * on, per kernel class: 0 tile pass, 1 pair pass, 2 diagonal pass,

@@ -211,3 +211,29 @@ def param_shift_grad(n: int, gates, theta, terms, which: Optional[Iterable[int]]
         return np.array([one(p) for p in which])
     with ThreadPoolExecutor(max_workers=threads) as ex:
         return np.array(list(ex.map(one, which)))
+
+
+def vqe_adam(n: int, gates, theta0, terms, lr: float = 1e-2, beta1: float = 0.9, beta2: float = 0.999,
+             eps: float = 1e-8, tol: float = 1e-7, max_iter: int = 350, threads: int = 1):
+    """VQE outer loop: theta^{t+1} = theta^t - lr Adam(g^t)
+     with Adam's bias-corrected moments (the paper cites Kingma
+    & Ba; beta/eps defaults), gradients by the parameter-shift
+    rule above.  Stops when |E_t - E_{t-1}| < tol (t >= 1) or t == max_iter
+    (SPEC.md:478).  Returns (theta_T, [E_0 .. E_T], T)."""
+    theta = np.array(theta0, np.float64, copy=True)
+    m = np.zeros_like(theta)
+    v = np.zeros_like(theta)
+    trace = []
+    t = 0
+    while True:
+        e = energy(n, gates, theta, terms)
+        trace.append(e)
+        if (t >= 1 and abs(e - trace[-2]) < tol) or t == max_iter:
+            return theta, np.array(trace), t
+        g = param_shift_grad(n, gates, theta, terms, threads=threads)
+        m = beta1 * m + (1.0 - beta1) * g
+        v = beta2 * v + (1.0 - beta2) * (g * g)
+        m_hat = m / (1.0 - beta1 ** (t + 1))
+        v_hat = v / (1.0 - beta2 ** (t + 1))
+        theta = theta - (lr * m_hat) / (np.sqrt(v_hat) + eps)
+        t += 1

@@ -433,7 +433,14 @@ int or_energy(int n, int n_gates, const int *kinds, const int *q0, const int *q1
  * fixed prefactor 1/2 (reading A6):
  *   g_p = ( E(theta + s e_p) - E(theta - s e_p) ) / 2
  * for each p in which[0..n_which).  Each evaluation rebuilds the circuit from
- * a fresh |0...0>. */
+ * a fresh |0...0>.
+ * A parameter of a CRY gate (generator |1><1| (x) Y/2, eigenvalues 0, +-1/2:
+ * E(theta) = a0 + a1 cos(theta/2) + b1 sin(theta/2) + a2 cos(theta) +
+ * b2 sin(theta), for which the two-term rule is not exact -- reading A8;
+ * the paper is silent) takes the four-term rule that is exact for those two
+ * frequencies (reading A8):
+ *   g_p = c1 [E(+pi/2) - E(-pi/2)] - c2 [E(+3pi/2) - E(-3pi/2)],
+ *   c1 = (sqrt2 + 1)/(4 sqrt2), c2 = (sqrt2 - 1)/(4 sqrt2). */
 int or_param_shift(int n, int n_gates, const int *kinds, const int *q0, const int *q1,
                    const int *q2, const int *pidx, const double *angles,
                    const double *mats, const double *theta, int n_params,
@@ -447,6 +454,25 @@ int or_param_shift(int n, int n_gates, const int *kinds, const int *q0, const in
     for (int w = 0; w < n_which; w++) {
         int i = which[w];
         double e_plus, e_minus;
+        int controlled = 0;
+        for (int k = 0; k < n_gates; k++)
+            if (pidx[k] == i && kinds[k] == OR_CRY)
+                controlled = 1;
+        if (controlled) {
+            const double s[4] = {OR_PI / 2.0, -OR_PI / 2.0, 3.0 * OR_PI / 2.0, -3.0 * OR_PI / 2.0};
+            double e[4];
+            for (int k = 0; k < 4; k++) {
+                memcpy(tp, theta, (size_t)n_params * sizeof(double));
+                tp[i] += s[k];
+                int rc = or_energy(n, n_gates, kinds, q0, q1, q2, pidx, angles, mats, tp,
+                                   n_terms, coeffs, xm, zm, &e[k]);
+                if (rc != OR_OK) { free(tp); return rc; }
+            }
+            const double r2 = sqrt(2.0);
+            const double c1 = (r2 + 1.0) / (4.0 * r2), c2 = (r2 - 1.0) / (4.0 * r2);
+            grad[w] = c1 * (e[0] - e[1]) - c2 * (e[2] - e[3]);
+            continue;
+        }
         memcpy(tp, theta, (size_t)n_params * sizeof(double));
         tp[i] += shift;
         int rc = or_energy(n, n_gates, kinds, q0, q1, q2, pidx, angles, mats, tp,

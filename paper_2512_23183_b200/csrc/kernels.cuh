@@ -239,13 +239,26 @@ __device__ __forceinline__ double2 gauss_amp(uint64_t seed, uint64_t i) {
 
 constexpr int RED_BLOCKS = 1184;   // 8 x 148 SMs; fixed => deterministic reduction order
 
-// off: logical index of the shard's first amplitude (sharded states)
+// off: logical index of the shard's first amplitude (sharded states).
+// |a_i|^2 = r_i^2 = -2 ln u0_i: the phase draw never enters the norm, and
+// the sum of logs is the log of a running product (renormalised with frexp
+// every 16 factors: u0 >= 2^-54, so 16 factors stay above 2^-1022), so this
+// sweep costs one splitmix64 and one DMUL per amplitude instead of a log, a
+// sqrt and a sincospi.
 __global__ void __launch_bounds__(256) k_random_norm(uint64_t N, uint64_t off, uint64_t seed, double *partial) {
-    double acc = 0.0;
+    double p = 1.0;
+    int e = 0, cnt = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < N; i += (uint64_t)gridDim.x * 256) {
-        double2 a = gauss_amp(seed, off + i);
-        acc = fma(a.x, a.x, fma(a.y, a.y, acc));
+        const uint64_t x0 = splitmix64(seed ^ (2 * (off + i)));
+        p *= ((double)(x0 >> 11) + 0.5) * 0x1.0p-53;
+        if (++cnt == 16) {
+            int ex;
+            p = frexp(p, &ex);
+            e += ex;
+            cnt = 0;
+        }
     }
+    const double acc = -2.0 * (log(p) + (double)e * 0.69314718055994530942);
     __shared__ double red[256];
     double r = block_sum(acc, red);
     if (threadIdx.x == 0) partial[blockIdx.x] = r;
@@ -320,6 +333,19 @@ __global__ void __launch_bounds__(256) k_sum_partials(const double *__restrict__
     if (threadIdx.x == 0) out[blockIdx.x] = r;
 }
 
+// chunk sums: out[c * stride + b] = sum of partial[c * stride + b * chunk ..
+// + chunk) (clipped to n), fixed order; grid (n_chunks, n_circ)
+__global__ void __launch_bounds__(256) k_sum_chunks(const double *__restrict__ partial, uint64_t stride, uint32_t n,
+                                                    uint32_t chunk, double *out) {
+    const double *p = partial + (uint64_t)blockIdx.y * stride;
+    const uint32_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    double acc = 0.0;
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += 256) acc += p[i];
+    __shared__ double red[256];
+    double r = block_sum(acc, red);
+    if (threadIdx.x == 0) out[(uint64_t)blockIdx.y * stride + blockIdx.x] = r;
+}
+
 // ---------------------------------------------------------------- logical <-> physical
 struct QMap { int8_t q[64]; };
 
@@ -383,18 +409,46 @@ __global__ void __launch_bounds__(256) k_pauli_direct(int n, uint64_t gofs, uint
 }
 
 // ---------------------------------------------------------------- PSR combine (a8)
-// g_p = (E(theta + pi/2 e_p) - E(theta - pi/2 e_p)) / 2
-struct PsrPair { int32_t p, plus, minus, pad; };
-__global__ void k_psr_combine(const double *__restrict__ E, const PsrPair *__restrict__ pairs, int n_pairs,
+// g_p = sum_k w_k E(theta + s_k e_p).  Rotations exp(-i theta G / 2) with
+// G^2 = 1 take the paper's two-term rule, s = +-pi/2, w = +-1/2
+// (PAPER.md:374-377, 533-534).  A controlled rotation (CRY) has generator
+// eigenvalues {0, +-1/2}, so E(theta) carries frequencies 1/2 and 1 and the
+// two-term rule is not exact (reading A8): it takes the four-term rule
+// s = +-pi/2, +-3pi/2 with w = +-(sqrt2+1)/(4 sqrt2), -+(sqrt2-1)/(4 sqrt2)
+// (reading A8; derived there).  One component per thread, terms
+// summed in fixed order.
+struct PsrRule { int32_t p, nc; int32_t c[4]; double w[4]; };
+__global__ void k_psr_combine(const double *__restrict__ E, const PsrRule *__restrict__ rules, int n_rules,
                               int base_idx, double *__restrict__ grad, int n_params, double *energy) {
     // launched as ONE block: zero, barrier, then the owned components
     for (int i = threadIdx.x; i < n_params; i += blockDim.x) grad[i] = 0.0;
     __syncthreads();
-    for (int i = threadIdx.x; i < n_pairs; i += blockDim.x) {
-        const PsrPair pr = pairs[i];
-        grad[pr.p] = 0.5 * (E[pr.plus] - E[pr.minus]);
+    for (int i = threadIdx.x; i < n_rules; i += blockDim.x) {
+        const PsrRule r = rules[i];
+        double g = 0.0;
+        for (int k = 0; k < r.nc; k++) g = fma(r.w[k], E[r.c[k]], g);
+        grad[r.p] = g;
     }
     if (energy && threadIdx.x == 0) *energy = base_idx >= 0 ? E[base_idx] : 0.0;
+}
+
+// ---------------------------------------------------------------- Adam (VQE outer loop)
+// theta^{t+1} = theta^t - lr * Adam(g^t) (Adam of the cited
+// Kingma & Ba: bias-corrected first and second moments).  bc1 = 1 - b1^t,
+// bc2 = 1 - b2^t.  Explicit _rn intrinsics keep the update free of FMA
+// contraction (the update is O(P) work; exact rounding is worth more).
+__global__ void k_adam_step(double *__restrict__ theta, double *__restrict__ m, double *__restrict__ v,
+                            const double *__restrict__ g, int n, double lr, double b1, double b2, double eps,
+                            double bc1, double bc2) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double gi = g[i];
+        const double mi = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(__dadd_rn(1.0, -b1), gi));
+        const double vi = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dadd_rn(1.0, -b2), __dmul_rn(gi, gi)));
+        m[i] = mi;
+        v[i] = vi;
+        const double mh = __ddiv_rn(mi, bc1), vh = __ddiv_rn(vi, bc2);
+        theta[i] = __dadd_rn(theta[i], -__ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), eps)));
+    }
 }
 
 }  // namespace lq

@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstddef>
+#include <list>
+#include <memory>
 #include <mutex>
 #include <cmath>
 #include <cstdio>
@@ -140,6 +142,7 @@ PlanOptions options() {
 // (~1-5 s per pass): every PSR plan (it runs 2P+1 circuits) and single
 // states with n >= 26; 2 forces it, 0 disables it.
 lq_status prepare(Plan &plan, bool reused = false) {
+    if (plan.prepared) return LQ_OK;   // a cached plan (PlanCache) keeps its kernels
     plan.jit.clear();
     const int64_t mode = g_opt_jit.load();
     if (mode == 0 || plan.n_tile == 0) return LQ_OK;
@@ -150,6 +153,65 @@ lq_status prepare(Plan &plan, bool reused = false) {
         return fail(LQ_ERR_CUDA, err);
     }
     return LQ_OK;
+}
+
+// Plans of single-state calls (apply, QFT, expectation) for repeated use:
+// an LRU keyed by everything the plan depends on -- the call kind, n, the
+// qubit map, the planner options and the gate / term arrays (U1/U2 matrices
+// by value, angles included; theta is not part of a plan: parameterised
+// angles are resolved on the device by k_build_mats).  A hit skips
+// planning and JIT source generation, which otherwise cost 0.1-30 ms per
+// call on the host.
+struct CachedPlan {
+    Plan plan;
+    MatBuilder mb;
+    int32_t qmap_after[64];
+};
+struct PlanCache {
+    std::mutex mu;
+    std::list<std::pair<std::string, std::shared_ptr<CachedPlan>>> lru;
+    static constexpr size_t CAP = 32;
+    std::shared_ptr<CachedPlan> get(const std::string &k) {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto it = lru.begin(); it != lru.end(); ++it)
+            if (it->first == k) {
+                lru.splice(lru.begin(), lru, it);
+                return it->second;
+            }
+        return nullptr;
+    }
+    void put(const std::string &k, std::shared_ptr<CachedPlan> p) {
+        std::lock_guard<std::mutex> lk(mu);
+        lru.emplace_front(k, std::move(p));
+        if (lru.size() > CAP) lru.pop_back();
+    }
+    void clear() {
+        std::lock_guard<std::mutex> lk(mu);
+        lru.clear();
+    }
+};
+PlanCache g_plan_cache;
+
+std::string plan_key(char kind, int n, const int32_t *qmap, const void *payload, size_t bytes) {
+    std::string k(1, kind);
+    int64_t o[7] = {n, g_opt_K.load(), g_opt_coalesce.load(), g_opt_fusion.load(), g_opt_regbits.load(),
+                    g_opt_jit.load(), g_opt_budget.load()};
+    k.append(reinterpret_cast<const char *>(o), sizeof(o));
+    k.append(reinterpret_cast<const char *>(qmap), sizeof(int32_t) * (size_t)n);
+    if (bytes) k.append(reinterpret_cast<const char *>(payload), bytes);
+    return k;
+}
+
+std::string gates_key(int n, const int32_t *qmap, const lq_gate *g, size_t ng) {
+    std::string k = plan_key('a', n, qmap, nullptr, 0);
+    for (size_t i = 0; i < ng; i++) {
+        lq_gate c = g[i];
+        c.mat = nullptr;
+        k.append(reinterpret_cast<const char *>(&c), sizeof(c));
+        const int nm = g[i].kind == LQ_U1 ? 8 : g[i].kind == LQ_U2 ? 32 : 0;
+        if (nm && g[i].mat) k.append(reinterpret_cast<const char *>(g[i].mat), sizeof(double) * nm);
+    }
+    return k;
 }
 
 // Stream-ordered growable device buffer.
@@ -402,6 +464,10 @@ struct DirectSet {
     struct D { uint64_t x; uint32_t tb, te, slot, nblocks; };
     std::vector<D> ds;
     uint32_t slots = 0;          // total partial slots (tile passes + direct)
+    uint32_t scratch = 0;        // per-circuit chunk sums of the two-level reduction (finish_expv)
+    static constexpr uint32_t CHUNK = 8192;
+    // per-circuit stride of the partial buffer: the slots, then the chunk sums
+    uint32_t stride() const { return std::max<uint32_t>(slots + scratch, 1); }
     void build(const Plan &plan) {
         slots = plan.n_slots;
         for (uint32_t g : plan.wide_groups) {
@@ -422,6 +488,7 @@ struct DirectSet {
             slots += d.nblocks;
             ds.push_back(d);
         }
+        scratch = slots > CHUNK ? (slots + CHUNK - 1) / CHUNK : 0;
     }
 };
 
@@ -439,6 +506,13 @@ lq_status finish_expv(const Plan &plan, const DirectSet &dset, const PTerm *dter
     if (dset.slots == 0) {
         CUDA_TRY(cudaMemsetAsync(E, 0, sizeof(double) * n_circ, st));
         return LQ_OK;
+    }
+    if (dset.scratch) {   // many slots (one per warp of every tile): chunk sums first, fixed order
+        k_sum_chunks<<<dim3(dset.scratch, n_circ), 256, 0, st>>>(partial, slot_stride, dset.slots, DirectSet::CHUNK,
+                                                                 partial + dset.slots);
+        LQ_TRY(check_launch("k_sum_chunks"));
+        k_sum_partials<<<n_circ, 256, 0, st>>>(partial + dset.slots, slot_stride, dset.scratch, E);
+        return check_launch("k_sum_partials");
     }
     k_sum_partials<<<n_circ, 256, 0, st>>>(partial, slot_stride, dset.slots, E);
     return check_launch("k_sum_partials");
@@ -696,7 +770,7 @@ lq_status sh_run(lq_sv *sv, Schedule &sc, const double *theta, size_t n_theta, d
         dp.specs = sv->plan_buf.at<MSpec>(o_spec);
         dp.factors = sv->plan_buf.at<MFactor>(o_fac);
         dp.cst = sv->plan_buf.at<double2>(o_cst);
-        const uint32_t slots = std::max<uint32_t>(dsets[i].slots, 1);
+        const uint32_t slots = dsets[i].stride();
         double *part = nullptr, *Ek = nullptr;
         if (stp.expv) {
             LQ_TRY(sv->part_buf.reserve(sizeof(double) * (slots + 1) * nk, st));
@@ -1255,15 +1329,20 @@ lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const doub
         sv->xmask = xm;
         return LQ_OK;
     }
-    int32_t qm[64];
-    memcpy(qm, sv->qmap, sizeof(qm));
-    std::vector<POp> ops;
-    MatBuilder mb;
-    lower_gates(sv->n, gates, n_gates, qm, ops, mb);
-    Plan plan;
-    plan_circuit(sv->n, ops, options(), mb, plan);
-    LQ_TRY(run_single(sv, plan, mb, theta, n_theta));
-    memcpy(sv->qmap, qm, sizeof(qm));
+    const std::string key = gates_key(sv->n, sv->qmap, gates, n_gates);
+    std::shared_ptr<CachedPlan> cp = g_plan_cache.get(key);
+    if (!cp) {
+        cp = std::make_shared<CachedPlan>();
+        memcpy(cp->qmap_after, sv->qmap, sizeof(cp->qmap_after));
+        std::vector<POp> ops;
+        lower_gates(sv->n, gates, n_gates, cp->qmap_after, ops, cp->mb);
+        plan_circuit(sv->n, ops, options(), cp->mb, cp->plan);
+        if (!cp->plan.passes.empty()) LQ_TRY(prepare(cp->plan));
+        cp->plan.prepared = true;
+        g_plan_cache.put(key, cp);
+    }
+    LQ_TRY(run_single(sv, cp->plan, cp->mb, theta, n_theta));
+    memcpy(sv->qmap, cp->qmap_after, sizeof(sv->qmap));
     return LQ_OK;
 }
 }  // namespace
@@ -1291,11 +1370,20 @@ lq_status lq_qft(lq_sv *sv, int inverse) {
         std::vector<lq_gate> g = qft_gates(sv->n, inverse != 0);
         return apply_impl(sv, g.data(), g.size(), nullptr, 0);
     }
-    Plan plan;
-    MatBuilder mb;
-    if (!plan_qft(sv->n, qm, inverse != 0, options(), plan, mb)) return fail(LQ_ERR_STATE, "qft planning failed");
-    LQ_TRY(run_single(sv, plan, mb, nullptr, 0));
-    memcpy(sv->qmap, qm, sizeof(qm));
+    const int inv = inverse != 0;
+    const std::string key = plan_key('q', sv->n, qm, &inv, sizeof(inv));
+    std::shared_ptr<CachedPlan> cp = g_plan_cache.get(key);
+    if (!cp) {
+        cp = std::make_shared<CachedPlan>();
+        memcpy(cp->qmap_after, qm, sizeof(qm));
+        if (!plan_qft(sv->n, cp->qmap_after, inv, options(), cp->plan, cp->mb))
+            return fail(LQ_ERR_STATE, "qft planning failed");
+        LQ_TRY(prepare(cp->plan));
+        cp->plan.prepared = true;
+        g_plan_cache.put(key, cp);
+    }
+    LQ_TRY(run_single(sv, cp->plan, cp->mb, nullptr, 0));
+    memcpy(sv->qmap, cp->qmap_after, sizeof(sv->qmap));
     return LQ_OK;
 }
 
@@ -1318,12 +1406,18 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
         sv->xmask = xm;
         return LQ_OK;
     }
-    Plan plan;
-    MatBuilder mb;
-    std::vector<POp> ops;
-    lower_pauli(sv->n, sv->qmap, terms, n_terms, ops, plan);
-    plan_circuit(sv->n, ops, options(), mb, plan);
-    LQ_TRY(prepare(plan));
+    const std::string key = plan_key('e', sv->n, sv->qmap, terms, sizeof(lq_pauli_term) * n_terms);
+    std::shared_ptr<CachedPlan> cp = g_plan_cache.get(key);
+    if (!cp) {
+        cp = std::make_shared<CachedPlan>();
+        std::vector<POp> ops;
+        lower_pauli(sv->n, sv->qmap, terms, n_terms, ops, cp->plan);
+        plan_circuit(sv->n, ops, options(), cp->mb, cp->plan);
+        LQ_TRY(prepare(cp->plan));
+        cp->plan.prepared = true;
+        g_plan_cache.put(key, cp);
+    }
+    const Plan &plan = cp->plan;
     DirectSet dset;
     dset.build(plan);
     Blob blob;
@@ -1336,13 +1430,90 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
     dp.perms = sv->plan_buf.at<KPerm>(o_perm);
     dp.pterms = sv->plan_buf.at<KPermTerm>(o_pt);
     dp.eterms = sv->plan_buf.at<ETerm>(o_et);
-    LQ_TRY(sv->work_buf.reserve(sizeof(double) * (dset.slots + 2), sv->stream));
+    LQ_TRY(sv->work_buf.reserve(sizeof(double) * (dset.stride() + 2), sv->stream));
     double *part = sv->work_buf.at<double>(0);
-    double *E = part + dset.slots + 1;
-    LQ_TRY(launch_passes(plan, dp, sv->d, 0, 1, nullptr, 0, sv->stream, false, part, dset.slots, false));
-    LQ_TRY(finish_expv(plan, dset, sv->plan_buf.at<PTerm>(o_dt), sv->d, 0, 1, part, dset.slots, E, sv->stream));
+    double *E = part + dset.stride() + 1;
+    LQ_TRY(launch_passes(plan, dp, sv->d, 0, 1, nullptr, 0, sv->stream, false, part, dset.stride(), false));
+    LQ_TRY(finish_expv(plan, dset, sv->plan_buf.at<PTerm>(o_dt), sv->d, 0, 1, part, dset.stride(), E, sv->stream));
     CUDA_TRY(cudaMemcpyAsync(out_energy, E, sizeof(double), cudaMemcpyDeviceToHost, sv->stream));
     return sync(sv->stream);
+}
+
+// First-order Trotter evolution of the XYZ chain (
+// PAPER.md:777-836).  Every step is the gate list of P:825-831 with the
+// signs of Eq. (9) (reading A20): RXX(-2 Jx dt) on each pair left to right,
+// then RYY(-2 Jy dt), RZZ(-2 Jz dt), then RZ(-2 h(t_j) dt) on each site
+// (SPEC.md:539-541 order).  The field angles are parameters (theta), so up
+// to 8 steps share one cached plan whatever h(t) is, and the planner fuses
+// across step boundaries.  E(t) = E_int - h(t) M with E_int = <-sum J PP>
+// and M = <sum Z_i> (two cached expectation plans).
+lq_status lq_trotter_xyz(lq_sv *sv, const lq_xyz_model *mdl, double t0, double dt, int n_steps, int record_every,
+                         double *energy_out) {
+    LQ_TRY(check_sv(sv));
+    if (!mdl) return fail(LQ_ERR_ARG, "model is NULL");
+    const double v[7] = {mdl->jx, mdl->jy, mdl->jz, mdl->amp, mdl->omega, t0, dt};
+    for (double x : v)
+        if (!std::isfinite(x)) return fail(LQ_ERR_NONFINITE, "non-finite model, t0 or dt");
+    const int n = sv->n;
+    if (n < 2) return fail(LQ_ERR_ARG, "the XYZ chain needs n >= 2");
+    if (!(dt > 0) || n_steps < 0 || record_every < 1) return fail(LQ_ERR_ARG, "need dt > 0, n_steps >= 0, record_every >= 1");
+    // observables: interaction part and magnetisation
+    std::vector<lq_pauli_term> hint, mag;
+    const double J[3] = {mdl->jx, mdl->jy, mdl->jz};
+    for (int k = 0; k < 3; k++)
+        for (int i = 0; i + 1 < n; i++) {
+            const uint64_t m = (1ull << i) | (1ull << (i + 1));
+            hint.push_back({-J[k], k == 2 ? 0ull : m, k == 0 ? 0ull : m});
+        }
+    for (int i = 0; i < n; i++) mag.push_back({1.0, 0ull, 1ull << i});
+    auto h = [&](double t) { return mdl->amp * std::sin(mdl->omega * t); };
+    int rec = 0;
+    auto record = [&](double t) -> lq_status {
+        if (!energy_out) return LQ_OK;
+        double ei = 0.0, m = 0.0;
+        LQ_TRY(lq_expval_pauli_sum(sv, hint.data(), hint.size(), &ei));
+        LQ_TRY(lq_expval_pauli_sum(sv, mag.data(), mag.size(), &m));
+        energy_out[rec++] = ei - h(t) * m;
+        return LQ_OK;
+    };
+    LQ_TRY(record(t0));
+    const int SMAX = 8;
+    std::vector<lq_gate> gates;
+    std::vector<double> theta;
+    for (int j = 0; j < n_steps;) {
+        const int to_rec = record_every - (j % record_every);
+        const int S = std::min({SMAX, n_steps - j, to_rec});
+        gates.clear();
+        theta.assign((size_t)S * n, 0.0);
+        for (int s2 = 0; s2 < S; s2++) {
+            const int kinds[3] = {LQ_RXX, LQ_RYY, LQ_RZZ};
+            for (int k = 0; k < 3; k++)
+                for (int i = 0; i + 1 < n; i++) {
+                    lq_gate g{};
+                    g.kind = kinds[k];
+                    g.q0 = i;
+                    g.q1 = i + 1;
+                    g.q2 = -1;
+                    g.param_idx = -1;
+                    g.angle = -2.0 * J[k] * dt;
+                    gates.push_back(g);
+                }
+            const double tj = t0 + (double)(j + s2) * dt;
+            for (int i = 0; i < n; i++) {
+                lq_gate g{};
+                g.kind = LQ_RZ;
+                g.q0 = i;
+                g.q1 = g.q2 = -1;
+                g.param_idx = s2 * n + i;
+                gates.push_back(g);
+                theta[(size_t)s2 * n + i] = -2.0 * h(tj) * dt;
+            }
+        }
+        LQ_TRY(apply_impl(sv, gates.data(), gates.size(), theta.data(), theta.size()));
+        j += S;
+        if (j % record_every == 0) LQ_TRY(record(t0 + (double)j * dt));
+    }
+    return LQ_OK;
 }
 
 // Plan export (JSON) for host-side inspection and the test-suite's plan
@@ -1383,13 +1554,13 @@ struct lq_psr {
     MatBuilder mb;
     DirectSet dset;
     std::vector<Shift> shifts;
-    std::vector<PsrPair> pairs;
+    std::vector<PsrRule> pairs;
     int base_idx = -1;
     int B = 1;
     DevBuf blob_buf, states, mats, partials, E;
     DevPlan dp;
     const Shift *d_shifts = nullptr;
-    const PsrPair *d_pairs = nullptr;
+    const PsrRule *d_pairs = nullptr;
     const PTerm *d_terms = nullptr;
     uint64_t launches_per_run = 0;
     uint64_t blob_bytes = 0;
@@ -1432,15 +1603,22 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     P->dset.build(P->plan);
     // circuits of this shard: (p, +pi/2), (p, -pi/2) for owned p; base on shard 0.
     // Parameters used by no gate have E+ == E- identically: g_p = 0 (written by combine).
+    std::vector<char> four(n_params, 0);   // parameters of controlled rotations (k_psr_combine)
+    for (size_t i = 0; i < n_gates; i++)
+        if (ansatz[i].param_idx >= 0 && ansatz[i].kind == LQ_CRY) four[(size_t)ansatz[i].param_idx] = 1;
+    const double c1 = (std::sqrt(2.0) + 1.0) / (4.0 * std::sqrt(2.0)), c2 = (std::sqrt(2.0) - 1.0) / (4.0 * std::sqrt(2.0));
     for (size_t p = 0; p < n_params; p++) {
         if ((int)(p % shard_world) != shard_rank || uses[p] == 0) continue;
-        PsrPair pr;
+        PsrRule pr{};
         pr.p = (int)p;
-        pr.plus = (int)P->shifts.size();
-        P->shifts.push_back({(int)p, 0, PI / 2});
-        pr.minus = (int)P->shifts.size();
-        P->shifts.push_back({(int)p, 0, -PI / 2});
-        pr.pad = 0;
+        const double s[4] = {PI / 2, -PI / 2, 3 * PI / 2, -3 * PI / 2};
+        const double w2[4] = {0.5, -0.5, 0.0, 0.0}, w4[4] = {c1, -c1, -c2, c2};
+        pr.nc = four[p] ? 4 : 2;
+        for (int k = 0; k < pr.nc; k++) {
+            pr.c[k] = (int)P->shifts.size();
+            pr.w[k] = four[p] ? w4[k] : w2[k];
+            P->shifts.push_back({(int)p, 0, s[k]});
+        }
         P->pairs.push_back(pr);
     }
     if (shard_rank == 0) {
@@ -1465,7 +1643,7 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     lq_status s = blob.upload(P->blob_buf, st);
     if (s == LQ_OK) s = P->states.reserve((size_t)B * N * sizeof(double2), st);
     if (s == LQ_OK) s = P->mats.reserve((size_t)B * std::max<uint32_t>(P->mb.mat_size, 1) * sizeof(double2), st);
-    if (s == LQ_OK) s = P->partials.reserve((size_t)B * std::max<uint32_t>(P->dset.slots, 1) * sizeof(double), st);
+    if (s == LQ_OK) s = P->partials.reserve((size_t)B * P->dset.stride() * sizeof(double), st);
     if (s == LQ_OK) s = P->E.reserve(sizeof(double) * std::max(n_circ, 1), st);
     if (s != LQ_OK) {
         std::string keep = g_err;
@@ -1482,7 +1660,7 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     P->dp.pterms = P->blob_buf.at<KPermTerm>(o_pt);
     P->dp.eterms = P->blob_buf.at<ETerm>(o_et);
     P->d_shifts = P->blob_buf.at<Shift>(o_sh);
-    P->d_pairs = P->blob_buf.at<PsrPair>(o_pr);
+    P->d_pairs = P->blob_buf.at<PsrRule>(o_pr);
     P->d_terms = P->blob_buf.at<PTerm>(o_t);
     *out = P;
     return LQ_OK;
@@ -1508,7 +1686,7 @@ lq_status lq_psr_run(lq_psr *P, const double *theta_dev, double *grad_dev, doubl
                 ms, nb);
             LQ_TRY(check_launch("k_build_mats"));
         }
-        const uint32_t ss = std::max<uint32_t>(P->dset.slots, 1);
+        const uint32_t ss = P->dset.stride();
         // the state after the last pass is only read by the Pauli groups of
         // that pass: no store (unless a wide group still has to read it)
         LQ_TRY(launch_passes(P->plan, P->dp, states, N, nb, mats, ms, st, true, part, ss, P->dset.ds.empty()));
@@ -1519,6 +1697,71 @@ lq_status lq_psr_run(lq_psr *P, const double *theta_dev, double *grad_dev, doubl
     LQ_TRY(check_launch("k_psr_combine"));
     P->launches_per_run = g_launches.load() - l0;
     return LQ_OK;
+}
+
+// VQE outer loop: Adam on parameter-shift
+// gradients.  The plan is built once; every iteration is one lq_psr_run (E and
+// g at theta^t), one k_adam_step, and one 8-byte read of E for the stopping
+// rule.
+lq_status lq_vqe_adam(int n_qubits, const lq_gate *ansatz, size_t n_gates, double *theta, size_t n_params,
+                      const lq_pauli_term *terms, size_t n_terms, const lq_adam_cfg *cfg, void *cuda_stream,
+                      double *energy_trace, int32_t *iters_out) {
+    if (!cfg) return fail(LQ_ERR_ARG, "cfg is NULL");
+    if (n_params && !theta) return fail(LQ_ERR_ARG, "theta is NULL");
+    if (cfg->max_iter < 0 || cfg->reserved != 0) return fail(LQ_ERR_ARG, "max_iter must be >= 0, reserved 0");
+    const double cf[5] = {cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->tol};
+    for (double x : cf)
+        if (!std::isfinite(x)) return fail(LQ_ERR_NONFINITE, "non-finite Adam setting");
+    if (!(cfg->beta1 >= 0 && cfg->beta1 < 1 && cfg->beta2 >= 0 && cfg->beta2 < 1 && cfg->eps > 0 && cfg->tol >= 0))
+        return fail(LQ_ERR_ARG, "Adam needs 0 <= beta < 1, eps > 0, tol >= 0");
+    for (size_t p = 0; p < n_params; p++)
+        if (!std::isfinite(theta[p])) return fail(LQ_ERR_NONFINITE, "non-finite theta[" + std::to_string(p) + "]");
+    lq_psr *P = nullptr;
+    LQ_TRY(lq_psr_create(n_qubits, ansatz, n_gates, n_params, terms, n_terms, 0, 1, cuda_stream, &P));
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    DevBuf buf;
+    const size_t np = std::max<size_t>(n_params, 1);
+    lq_status s = buf.reserve(sizeof(double) * (4 * np + 1), st);
+    double *d_th = buf.at<double>(0), *d_g = d_th + np, *d_m = d_g + np, *d_v = d_m + np, *d_e = d_v + np;
+    if (s == LQ_OK && n_params) {
+        cudaError_t e = cudaMemcpyAsync(d_th, theta, sizeof(double) * n_params, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(d_m, 0, sizeof(double) * 2 * np, st);
+        if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe setup: ") + cudaGetErrorString(e));
+    }
+    int t = 0;
+    double prev = 0.0;
+    for (; s == LQ_OK; t++) {
+        s = lq_psr_run(P, d_th, d_g, d_e);
+        double E = 0.0;
+        if (s == LQ_OK) {
+            cudaError_t e = cudaMemcpyAsync(&E, d_e, sizeof(double), cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe: ") + cudaGetErrorString(e));
+        }
+        if (s != LQ_OK) break;
+        if (!std::isfinite(E)) {
+            s = fail(LQ_ERR_NONFINITE, "non-finite energy at iteration " + std::to_string(t));
+            break;
+        }
+        if (energy_trace) energy_trace[t] = E;
+        if ((t >= 1 && std::fabs(E - prev) < cfg->tol) || t == cfg->max_iter) break;
+        prev = E;
+        if (n_params) {
+            const double bc1 = 1.0 - std::pow(cfg->beta1, (double)(t + 1)), bc2 = 1.0 - std::pow(cfg->beta2, (double)(t + 1));
+            k_adam_step<<<grid_for(n_params), 256, 0, st>>>(d_th, d_m, d_v, d_g, (int)n_params, cfg->lr, cfg->beta1,
+                                                             cfg->beta2, cfg->eps, bc1, bc2);
+            s = check_launch("k_adam_step");
+        }
+    }
+    if (s == LQ_OK && n_params) {
+        cudaError_t e = cudaMemcpyAsync(theta, d_th, sizeof(double) * n_params, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe: ") + cudaGetErrorString(e));
+    }
+    if (iters_out) *iters_out = t;
+    buf.release(st);
+    lq_psr_free(P);
+    return s;
 }
 
 lq_status lq_psr_stats(const lq_psr *P, uint64_t *n_circuits, uint64_t *n_launches, uint64_t *plan_bytes,
@@ -1612,6 +1855,7 @@ lq_status lq_psr_cache_clear(void) {
         delete c;
     }
     g_psr_cache.clear();
+    g_plan_cache.clear();
     return LQ_OK;
 }
 
@@ -1697,6 +1941,22 @@ lq_status lq_jit_compile_check(int n_qubits, const lq_gate *gates, size_t n_gate
     lower_gates(n_qubits, gates, n_gates, qm, ops, mb);
     if (n_terms) lower_pauli(n_qubits, qm, terms, n_terms, ops, plan);
     plan_circuit(n_qubits, ops, options(), mb, plan);
+    size_t nk = 0;
+    std::string err;
+    if (!jit_check(plan, &nk, err)) return fail(LQ_ERR_CUDA, err);
+    if (n_kernels) *n_kernels = nk;
+    return LQ_OK;
+}
+
+// Host-only: NVRTC-compile (without loading) the JIT pass programs of the
+// QFT plan on n qubits (identity layout).  No device needed.
+lq_status lq_qft_jit_compile_check(int n_qubits, int inverse, uint64_t *n_kernels) {
+    if (n_qubits < 1 || n_qubits > 40) return fail(LQ_ERR_ARG, "n_qubits must be in [1, 40]");
+    int32_t qm[64];
+    for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
+    MatBuilder mb;
+    Plan plan;
+    if (!plan_qft(n_qubits, qm, inverse != 0, options(), plan, mb)) return fail(LQ_ERR_STATE, "qft planning failed");
     size_t nk = 0;
     std::string err;
     if (!jit_check(plan, &nk, err)) return fail(LQ_ERR_CUDA, err);

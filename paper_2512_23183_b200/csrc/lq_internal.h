@@ -102,7 +102,9 @@ struct KOp {
     uint32_t mat;        // source of the op's table (double2 units): per-circuit matrix block, or cst
     uint32_t aux;        // where the kernel stages that table in shared memory (pass-local, double2 units)
     uint8_t qj;          // QFT: logical bit j of the stage
-    uint8_t pad[7];
+    uint8_t tdep;        // QFT: 0x80 | register positions whose logical bit is below j (the
+                         // only ones the register twiddle depends on); 0: unknown
+    uint8_t pad[6];
 };
 static_assert(sizeof(KOp) == 32, "KOp layout");
 

@@ -80,8 +80,45 @@ static bool is_diag_1q(int k) {
     return k == LQ_Z || k == LQ_S || k == LQ_SDG || k == LQ_T || k == LQ_TDG || k == LQ_RZ;
 }
 
-void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
+// RXX and RYY as cheap ops (Trotter steps of PAPER.md:825-831, SURVEY §8(f)
+// f1): CNOT_ab X_a CNOT_ab = X_a X_b, so RXX_ab(t) = CNOT_ab RX_a(t) CNOT_ab
+// (two folded permutations and one scaled rotation, 2 FP64 ops per
+// amplitude instead of a general 4x4); Y = S X S^dag, so RYY_ab(t) =
+// (S_a S_b) RXX_ab(t) (S_a^dag S_b^dag) (diagonals join the diagonal runs).
+static std::vector<lq_gate> expand_pair_rotations(const lq_gate *gates, size_t n_gates) {
+    std::vector<lq_gate> out;
+    out.reserve(n_gates);
+    for (size_t i = 0; i < n_gates; i++) {
+        const lq_gate &G = gates[i];
+        if (G.kind != LQ_RXX && G.kind != LQ_RYY) {
+            out.push_back(G);
+            continue;
+        }
+        auto mk = [&](int kind, int a, int b) {
+            lq_gate x = G;
+            x.kind = kind;
+            x.q0 = a;
+            x.q1 = b;
+            x.q2 = -1;
+            x.mat = nullptr;
+            if (kind != LQ_RX) { x.param_idx = -1; x.angle = 0.0; }
+            return x;
+        };
+        const bool yy = G.kind == LQ_RYY;
+        if (yy) { out.push_back(mk(LQ_SDG, G.q0, -1)); out.push_back(mk(LQ_SDG, G.q1, -1)); }
+        out.push_back(mk(LQ_CNOT, G.q0, G.q1));
+        out.push_back(mk(LQ_RX, G.q0, -1));
+        out.push_back(mk(LQ_CNOT, G.q0, G.q1));
+        if (yy) { out.push_back(mk(LQ_S, G.q0, -1)); out.push_back(mk(LQ_S, G.q1, -1)); }
+    }
+    return out;
+}
+
+void lower_gates(int n, const lq_gate *gates_in, size_t n_gates_in, int32_t *qmap,
                  std::vector<POp> &ops, MatBuilder &mb) {
+    const std::vector<lq_gate> expanded = expand_pair_rotations(gates_in, n_gates_in);
+    const lq_gate *gates = expanded.data();
+    const size_t n_gates = expanded.size();
     std::vector<std::vector<MFactor>> fl;   // factor list per op
     std::vector<int> last(64, -1);          // last op touching each physical bit
     std::vector<char> fusable;              // op is an uncontrolled 1q op
@@ -581,6 +618,11 @@ static void lower_qft_stages(Plan &plan, const KSub &sb, const LocalMap &L, int 
             tab[2 * v + 1] = (inv ? -1.0 : 1.0) * (double)sinl(ang);
         }
         op.mat = (uint32_t)mb.add_const(tab, NREG);
+        op.tdep = 0x80;
+        for (int i = 0; i < Rr; i++) {
+            const int p = L.T[sb.S[i]];
+            if (lp[p] < 64 && lp[p] < j) op.tdep |= (uint8_t)(1u << i);
+        }
         op.b1 = (uint8_t)jmax;
         if (head) op.flags |= QF_HEAD;
         head = false;
@@ -705,8 +747,8 @@ static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vect
     }
     if (pp.kp.eterm_end > pp.kp.eterm_begin || (pp.kp.flags & PF_EXPV)) {
         pp.kp.flags |= PF_EXPV;
-        pp.kp.eslot = plan.n_slots;
-        plan.n_slots += (uint32_t)(1u << (nl - K));
+        pp.kp.eslot = plan.n_slots;   // one partial per warp of every tile (tile.cuh expv_partial)
+        plan.n_slots += (uint32_t)(1u << (nl - K)) * (uint32_t)std::max(1, (1 << (K - Rr)) / 32);
     }
     pp.kp.store_perm = build_perm(ops, store_group, L, pp, plan);
     // read-only pass: nothing but Pauli groups (no gate, no folded permutation)
@@ -973,6 +1015,11 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
                     tab[2 * v + 1] = sgn * (double)sinl(ang);
                 }
                 k.mat = (uint32_t)mb.add_const(tab, NREG);
+                k.tdep = 0x80;
+                for (int i = 0; i < Rr; i++) {
+                    const int p = L.T[sb.S[i]], l = layout_rev ? n - 1 - p : p;
+                    if (l < j) k.tdep |= (uint8_t)(1u << i);
+                }
                 if (b == a) k.flags |= QF_HEAD;
                 int jmax = 0;
                 for (size_t b2 = a; b2 < std::min(st.size(), a + Rr); b2++) jmax = std::max(jmax, st[b2]);

@@ -68,6 +68,7 @@ struct Plan {
     size_t n_tile = 0, n_pair = 0, n_diag = 0;
     size_t n_folded = 0;      // permutation gates folded into exchanges
     std::vector<const void *> jit;    // per pass: JIT-compiled tile kernel (cudaKernel_t) or nullptr (jit.h)
+    bool prepared = false;            // jit resolved (prepare() in lq_api.cu)
 };
 
 struct MatBuilder {

@@ -59,6 +59,24 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
     return r;
 }
 
+// Expectation partial of one tile (a7): with >= 32 threads every warp
+// writes its own fixed-order shuffle sum to slot base + tile * W + warp (W =
+// warps per tile) -- no barrier; smaller tiles reduce through `red` (block
+// tree, W = 1).  Deterministic either way; k_sum_partials adds the slots in
+// index order.
+__device__ __forceinline__ void expv_partial(double v, double *red, double *slots, uint64_t tile) {
+    const int nt = blockDim.x, t = threadIdx.x;
+    if (nt >= 32) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if ((t & 31) == 0) slots[tile * (uint64_t)(nt >> 5) + (t >> 5)] = v;
+        return;
+    }
+    __syncthreads();   // all reads of `red` (the tile buffer) are done
+    const double r = block_sum(v, red);
+    if (t == 0) slots[tile] = r;
+}
+
 // In-place register swap the compiler cannot turn into a renaming (a
 // renaming would force loop-carried copies of the whole register tile).
 __device__ __forceinline__ void swap_inplace(double2 &x, double2 &y) {
@@ -336,15 +354,23 @@ __device__ __forceinline__ void materialize(double2 (&a)[1 << RR], TState &ts, b
     ts.hph = false;
 }
 
-// QFT stage on register position P (see planner.cpp plan_qft).
+// QFT stage on register position P (see planner.cpp plan_qft).  The
+// twiddle of pair (v, w) is tt * W[w]; W[w] depends only on the register
+// positions in tdep (logical bits below j), so with tdep known at compile
+// time (JIT) the 8 butterflies share 2^|tdep| distinct twiddles and pairs
+// with no such bit set use tt itself (W = 1 exactly there).
 template <int RR, int P>
 __device__ __forceinline__ void ap_qft(double2 (&a)[1 << RR], double2 tt, const double2 *__restrict__ W,
-                                       bool inverse) {
+                                       bool inverse, uint32_t tdep) {
 #pragma unroll
     for (int v = 0; v < (1 << RR); v++) {
         if (v & (1 << P)) continue;
         const int w = v | (1 << P);
-        double2 tw = cmul(tt, W[w]);
+        const bool known = tdep & 0x80u;
+        const int lo = (int)(w & tdep & 0x7Fu);
+        double2 tw;
+        if (known && lo == 0) tw = tt;
+        else tw = cmul(tt, W[known ? (lo | (1 << P)) : w]);
         if (!inverse) {
             double2 u = a[v], x = a[w];
             a[v] = cadd(u, x);
@@ -658,7 +684,7 @@ __device__ __forceinline__ void exec_op(double2 (&a)[1 << RR], const KOp &op, co
         if constexpr (RR > P) {
             flush_flips<RR>(a, ts.fb);
             const double2 tt = qft_thread_twiddle(op, gbase, n, ts.ttmax, ts.lg, ts.lpos);
-            ap_qft<RR, P>(a, tt, M, op.flags & QF_INVERSE);
+            ap_qft<RR, P>(a, tt, M, op.flags & QF_INVERSE, op.tdep);
             if (op.flags & QF_SCALE) ts.tsc = cscale(ts.tsc, 0.70710678118654752440);
         }
     } else if constexpr (CODE == C_DT) {
@@ -918,11 +944,9 @@ __device__ __forceinline__ void tile_body(const KPass &P, const KSub *__restrict
             Prog::template run<RR>(s - P.sub_begin, sb, P.op_begin, a, s_ops, cur.gt | P.gofs, P.n, s_tab, ts, s_et);
         }
         double2 *psi = state + (uint64_t)circ * state_stride;
-        if (P.flags & PF_EXPV) {   // one deterministic partial per tile
-            __syncthreads();       // all reads of b done: reuse it as reduction scratch
-            const double r = block_sum(ts.eacc, reinterpret_cast<double *>(b));
-            if (t == 0) partials[(uint64_t)circ * slot_stride + P.eslot + (g & ((1u << tiles_log2) - 1))] = r;
-        }
+        if (P.flags & PF_EXPV)     // deterministic partials: one per warp of the tile
+            expv_partial(ts.eacc, reinterpret_cast<double *>(b), partials + (uint64_t)circ * slot_stride + P.eslot,
+                         g & ((1u << tiles_log2) - 1));
         if (P.flags & PF_NO_STORE) {
             __syncthreads();
             continue;
@@ -1022,19 +1046,27 @@ __device__ __forceinline__ void xread_c(const double2 *b, double2 (&a)[1 << RR],
 
 template <int RR, class D, class Prog, int S>
 __device__ __forceinline__ void run_subs_c(double2 (&a)[1 << RR], double2 *b, TState &ts, uint64_t tb, uint64_t gofs,
-                                           uint32_t t, const double2 *tab, const ETerm *et, int n) {
+                                           uint32_t t, const double2 *tab, const ETerm *et, int n, bool zero) {
     if constexpr (S < D::NSUB) {
         if constexpr (S > 0 && (D::SM[S] != D::SM[S - 1] || D::PERM[S] >= 0)) {
-            materialize<RR>(a, ts, false);
-            __syncthreads();   // everyone has read the previous mapping's slots
-            xwrite_c<RR, D, D::SM[S - 1]>(b, a, t, ts.fb);
-            ts.fb = 0;
-            __syncthreads();
-            xread_c<RR, D, D::SM[S], D::PERM[S], false>(b, a, t, tb, gofs);
+            // The buffer still holds the register contents (jit.cpp RO: only
+            // Pauli groups since it was filled), so the new mapping reads it
+            // directly -- no write-back, no barrier -- unless the pass never
+            // loaded it (PF_LOAD_ZERO).
+            if (D::RO[S - 1] && !zero) {
+                xread_c<RR, D, D::SM[S], D::PERM[S], false>(b, a, t, tb, gofs);
+            } else {
+                materialize<RR>(a, ts, false);
+                __syncthreads();   // everyone has read the previous mapping's slots
+                xwrite_c<RR, D, D::SM[S - 1]>(b, a, t, ts.fb);
+                ts.fb = 0;
+                __syncthreads();
+                xread_c<RR, D, D::SM[S], D::PERM[S], false>(b, a, t, tb, gofs);
+            }
         }
         const uint64_t gbase = tb | gofs | D::dep(ins_zeros<D::SM[S], D::K>(t));
         Prog::template run<S, RR>(a, gbase, n, tab, ts, et);
-        run_subs_c<RR, D, Prog, S + 1>(a, b, ts, tb, gofs, t, tab, et, n);
+        run_subs_c<RR, D, Prog, S + 1>(a, b, ts, tb, gofs, t, tab, et, n, zero);
     }
 }
 
@@ -1095,13 +1127,11 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         TState ts;
         ts.reset();
         ts.lpos = P.lpos;
-        run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, P.gofs, t, s_tab, s_et, P.n);
+        run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, P.gofs, t, s_tab, s_et, P.n, zero);
         double2 *psi = state + (uint64_t)circ * state_stride;
-        if (P.flags & PF_EXPV) {   // one deterministic partial per tile
-            __syncthreads();
-            const double r = block_sum(ts.eacc, reinterpret_cast<double *>(b));
-            if (t == 0) partials[(uint64_t)circ * slot_stride + P.eslot + (g & tmask)] = r;
-        }
+        if (P.flags & PF_EXPV)     // deterministic partials: one per warp of the tile
+            expv_partial(ts.eacc, reinterpret_cast<double *>(b), partials + (uint64_t)circ * slot_stride + P.eslot,
+                         g & tmask);
         if (P.flags & PF_NO_STORE) {
             __syncthreads();
             continue;

@@ -50,6 +50,17 @@ class lq_pauli_term(ctypes.Structure):
     _fields_ = [("coeff", ctypes.c_double), ("x_mask", ctypes.c_uint64), ("z_mask", ctypes.c_uint64)]
 
 
+class lq_xyz_model(ctypes.Structure):
+    _fields_ = [("jx", ctypes.c_double), ("jy", ctypes.c_double), ("jz", ctypes.c_double),
+                ("amp", ctypes.c_double), ("omega", ctypes.c_double)]
+
+
+class lq_adam_cfg(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double), ("tol", ctypes.c_double), ("max_iter", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
 class LQError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
@@ -109,6 +120,9 @@ _SIGS = {
     "lq_psr_traffic": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i32),
     "lq_jit_stats": ([ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_dbl)], _i32),
     "lq_jit_compile_check": ([_i32, _GP, _sz, _TP, _sz, ctypes.POINTER(_u64)], _i32),
+    "lq_qft_jit_compile_check": ([_i32, _i32, ctypes.POINTER(_u64)], _i32),
+    "lq_trotter_xyz": ([_P, _P, _dbl, _dbl, _i32, _i32, _DP], _i32),
+    "lq_vqe_adam": ([_i32, _GP, _sz, _DP, _sz, _TP, _sz, _P, _P, _DP, ctypes.POINTER(ctypes.c_int32)], _i32),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -317,6 +331,32 @@ def lq_param_shift_grad(n_qubits: int, ansatz, theta, terms, shard_rank: int = 0
     return grad, (e.value if with_energy else None)
 
 
+def lq_trotter_xyz(h, jx: float, jy: float, jz: float, amp: float, omega: float, t0: float, dt: float,
+                   n_steps: int, record_every: int = 1) -> np.ndarray:
+    """First-order Trotter evolution of the XYZ chain on
+    state handle h; returns E(t) at t0 and after every record_every steps."""
+    m = lq_xyz_model(jx, jy, jz, amp, omega)
+    out = np.zeros(1 + n_steps // record_every, np.float64)
+    _chk(_lib.lq_trotter_xyz(h, ctypes.byref(m), t0, dt, n_steps, record_every, _dptr(out)))
+    return out
+
+
+def lq_vqe_adam(n_qubits: int, ansatz, theta0, terms, lr: float = 1e-2, beta1: float = 0.9,
+                beta2: float = 0.999, eps: float = 1e-8, tol: float = 1e-7, max_iter: int = 350,
+                stream=None) -> Tuple[np.ndarray, np.ndarray, int]:
+    """VQE outer loop: Adam on parameter-shift gradients.
+    Returns (final theta, energy trace E_0..E_T, T = Adam updates)."""
+    ga = ansatz if isinstance(ansatz, GateArray) else GateArray(ansatz)
+    ta = terms if isinstance(terms, TermArray) else TermArray(terms)
+    th = np.array(theta0, np.float64, copy=True)
+    trace = np.zeros(max_iter + 1, np.float64)
+    cfg = lq_adam_cfg(lr, beta1, beta2, eps, tol, max_iter, 0)
+    it = ctypes.c_int32()
+    _chk(_lib.lq_vqe_adam(n_qubits, ga.ptr, ga.n, _dptr(th), th.size, ta.ptr, ta.n, ctypes.byref(cfg),
+                          _stream_ptr(stream), _dptr(trace), ctypes.byref(it)))
+    return th, trace[: it.value + 1].copy(), it.value
+
+
 def lq_psr_create(n_qubits: int, ansatz, n_params: int, terms, shard_rank: int = 0, shard_world: int = 1,
                   stream=None):
     ga = ansatz if isinstance(ansatz, GateArray) else GateArray(ansatz)
@@ -391,6 +431,12 @@ def lq_jit_compile_check(n_qubits: int, gates, terms=()) -> int:
     ta = terms if isinstance(terms, TermArray) else TermArray(terms)
     nk = ctypes.c_uint64()
     _chk(_lib.lq_jit_compile_check(n_qubits, ga.ptr, ga.n, ta.ptr, ta.n, ctypes.byref(nk)))
+    return nk.value
+
+
+def lq_qft_jit_compile_check(n_qubits: int, inverse: bool = False) -> int:
+    nk = _u64()
+    _chk(_lib.lq_qft_jit_compile_check(n_qubits, int(bool(inverse)), ctypes.byref(nk)))
     return nk.value
 
 
@@ -558,6 +604,9 @@ class StateVector:
 
     def expval(self, terms) -> float:
         return lq_expval_pauli_sum(self.h, terms)
+
+    def trotter_xyz(self, jx, jy, jz, amp, omega, t0, dt, n_steps, record_every=1) -> np.ndarray:
+        return lq_trotter_xyz(self.h, jx, jy, jz, amp, omega, t0, dt, n_steps, record_every)
 
     def read(self, offset: int = 0, count: Optional[int] = None) -> np.ndarray:
         return lq_sv_read(self.h, offset, count)

@@ -341,7 +341,33 @@ def test_psr_app_e_table(lq, oracle):
         g, _ = lq.lq_param_shift_grad(2, gates, th, [(1.0, 0, 1)])
         go = oracle.param_shift_grad(2, gates, np.array(th), [(1.0, 0, 1)])
         assert np.all(np.isfinite(g))
-        np.testing.assert_allclose(g, go, rtol=0, atol=1e-15)
+        # theta_3 (CRY) takes the four-term rule on both sides (reading A8)
+        np.testing.assert_allclose(g, go, rtol=0, atol=1e-14)
+
+
+def test_psr_cry_four_term_closed_form_and_oracle(lq, oracle):
+    """Reading A8 (f3): H(0), CRY(t; 0 -> 1): <X_0> = cos(t/2), dE/dt =
+    -sin(t/2)/2 exactly (the two-term rule would be off by a factor sqrt2);
+    then a 10-qubit circuit mixing CRY and RX/RY/RZ parameters vs the
+    oracle's four-term rule."""
+    for t in [0.0, 0.4, 1.3, 2.9, 5.1]:
+        g, e = lq.lq_param_shift_grad(2, [("H", 0, -1, -1, 0.0), ("CRY", 0, 1, 0, 0.0)], [t], [(1.0, 1, 0)])
+        assert abs(e - math.cos(t / 2)) <= 1e-15 and abs(g[0] + math.sin(t / 2) / 2) <= 1e-15
+    n = 10
+    rng = np.random.default_rng(123)
+    gates, p = [], 0
+    for layer in range(3):
+        for q in range(n):
+            gates.append((["RY", "RX", "RZ"][(q + layer) % 3], q, -1, p, 0.0)); p += 1
+        for q in range(layer % 2, n - 1, 2):
+            gates.append(("CRY", q, q + 1, p, 0.0)); p += 1
+            gates.append(("CNOT", q + 1, q, -1, 0.0))
+    theta = rng.uniform(0, 2 * np.pi, p)
+    terms = W.random_pauli_sum(n, 20, rng)
+    g, e = lq.lq_param_shift_grad(n, gates, theta, terms)
+    go = oracle.param_shift_grad(n, gates, theta, terms, threads=8)
+    grad_close(g, go)
+    assert abs(e - oracle.energy(n, gates, theta, terms)) <= 1e-10 * max(1.0, abs(e))
 
 
 def test_config3_gradient(lq, oracle):
@@ -442,3 +468,29 @@ def test_boundary_rejections_leave_state_untouched(lq):
     with pytest.raises(lq.LQError):
         sv.expval([(1.0, 1 << 6, 0)])
     sv.free()
+
+
+# ---------------------------------------------------------------- VQE outer loop (f2)
+
+def test_vqe_adam_config3_trajectory_vs_oracle(lq, oracle):
+    """lq_vqe_adam (batched PSR + device Adam) follows the oracle's Adam
+    trajectory on config 3 for 30 iterations (gradients agree to ~1e-15, so
+    the iterates may drift only by rounding)."""
+    w = W.config3()
+    th, tr, T = lq.lq_vqe_adam(w.n, w.gates, w.theta, w.terms, max_iter=30)
+    tho, tro, To = oracle.vqe_adam(w.n, w.gates, w.theta, w.terms, max_iter=30, threads=8)
+    assert T == To == 30 and tr.size == 31
+    np.testing.assert_allclose(tr, tro, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(th, tho, rtol=0, atol=1e-10)
+
+
+def test_vqe_adam_single_qubit_and_zero_hamiltonian(lq):
+    th, tr, T = lq.lq_vqe_adam(1, [("RY", 0, -1, 0, 0.0)], [0.1], [(1.0, 0, 1)], lr=0.05, tol=1e-12,
+                               max_iter=3000)
+    assert abs(tr[-1] + 1.0) < 1e-6 and abs(math.cos(th[0]) - tr[-1]) < 1e-15
+    w = W.config3()
+    th, tr, T = lq.lq_vqe_adam(w.n, w.gates, w.theta, [], max_iter=10)
+    assert T == 1 and np.all(tr == 0.0)
+    np.testing.assert_array_equal(th, w.theta)
+    with pytest.raises(lq.LQError):
+        lq.lq_vqe_adam(1, [("RY", 0, -1, 0, 0.0)], [float("nan")], [(1.0, 0, 1)])

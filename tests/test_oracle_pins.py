@@ -402,9 +402,91 @@ def test_psr_vs_matrix_route_gradient(oracle):
     np.testing.assert_allclose(g, exact, atol=1e-13)
 
 
+def test_psr_cry_closed_form_four_term(oracle):
+    """Reading A8 (f3): after H(0), CRY(t; 0 -> 1) the state is
+    (|00> + cos(t/2)|10> + sin(t/2)|11>)/sqrt2, so <X_0> = cos(t/2) and
+    dE/dt = -sin(t/2)/2 exactly.  The paper's two-term rule would give
+    -(sqrt2/2) sin(t/2) here (E carries frequency 1/2); the four-term rule
+    must reproduce the exact derivative."""
+    gates = [("H", 0, -1, -1, 0.0), ("CRY", 0, 1, 0, 0.0)]
+    for t in [0.0, 0.4, 1.3, math.pi / 2, 2.9, 5.1]:
+        assert oracle.energy(2, gates, [t], [(1.0, 1, 0)]) == pytest.approx(math.cos(t / 2), abs=1e-15)
+        g = oracle.param_shift_grad(2, gates, np.array([t]), [(1.0, 1, 0)])
+        assert g[0] == pytest.approx(-math.sin(t / 2) / 2, abs=1e-15)
+        if abs(math.sin(t / 2)) > 0.1:   # the two-term value is really different
+            assert abs(g[0] - (-math.sqrt(2) / 2 * math.sin(t / 2))) > 1e-2
+
+
+def test_psr_cry_vs_matrix_route_gradient(oracle):
+    """Exact derivative through the matrix route for a circuit mixing RX/RY/RZ
+    and CRY parameters: CRY(t) = exp(-i t G / 2), G = |1><1|_c (x) Y_t."""
+    n = 3
+    rng = np.random.default_rng(77)
+    gates = [("RY", 0, -1, 0, 0.0), ("RX", 1, -1, 1, 0.0), ("H", 2, -1, -1, 0.0),
+             ("CRY", 0, 1, 2, 0.0), ("CNOT", 1, 2, -1, 0.0), ("CRY", 2, 0, 3, 0.0),
+             ("RZ", 1, -1, 4, 0.0), ("CRY", 1, 2, 5, 0.0), ("RY", 2, -1, 6, 0.0)]
+    theta = rng.uniform(0, 2 * np.pi, 7)
+    terms = W.random_pauli_sum(n, 12, rng)
+    Hm = FM.hamiltonian_matrix(n, terms)
+    psi0 = np.zeros(1 << n, np.complex128)
+    psi0[0] = 1
+    exact = np.zeros(theta.size)
+    for k, (name, a, b, p, _) in enumerate(gates):
+        if p < 0:
+            continue
+        pre = FM.circuit_unitary(n, gates[:k + 1], theta)
+        post = FM.circuit_unitary(n, gates[k + 1:], theta)
+        G = FM.embed(n, {a: FM.P1, b: FM.Y}) if name == "CRY" else FM.embed(n, {a: {"RX": FM.X, "RY": FM.Y, "RZ": FM.Z}[name]})
+        dpsi = post @ (-0.5j * G) @ pre @ psi0
+        exact[p] = 2 * np.real(np.vdot(post @ pre @ psi0, Hm @ dpsi))
+    g = oracle.param_shift_grad(n, gates, theta, terms)
+    np.testing.assert_allclose(g, exact, atol=1e-13)
+
+
 def test_expval_rejects_non_hermitian_imag(oracle):
     """a non-real <P> is an error, never silent.  A Pauli
     product is Hermitian, so this only fires on a corrupted state buffer."""
     psi = np.array([1, 1j], np.complex128) / math.sqrt(2)
     # <Y> on (|0> + i|1>)/sqrt2 = 1 (real) -- must pass
     assert oracle.expval(psi, [(1.0, 1, 1)]) == pytest.approx(1.0)
+
+
+# ---------------------------------------------------------------- VQE outer loop (f2)
+
+def test_vqe_first_adam_step_closed_form(oracle):
+    """At t = 1 the bias-corrected moments are m_hat = g, v_hat = g^2, so the
+    first update is theta_1 = theta_0 - lr g / (|g| + eps) componentwise
+    (sign descent of size lr) -- a property of Adam, not a retyping of it."""
+    w = W.config3()
+    th1, trace, T = oracle.vqe_adam(w.n, w.gates, w.theta, w.terms, max_iter=1)
+    g0 = oracle.param_shift_grad(w.n, w.gates, w.theta, w.terms)
+    assert T == 1 and trace.size == 2
+    np.testing.assert_allclose(th1, w.theta - 1e-2 * g0 / (np.abs(g0) + 1e-8), rtol=0, atol=1e-15)
+    assert trace[0] == pytest.approx(oracle.energy(w.n, w.gates, w.theta, w.terms), abs=0)
+    assert trace[1] == pytest.approx(oracle.energy(w.n, w.gates, th1, w.terms), abs=0)
+
+
+def test_vqe_single_qubit_converges_to_ground_state(oracle):
+    """H = Z, ansatz RY(theta), theta_0 = 0.1: E = cos theta has
+    its minimum -1 at theta = pi (ground state |1>)."""
+    th, trace, T = oracle.vqe_adam(1, [("RY", 0, -1, 0, 0.0)], [0.1], [(1.0, 0, 1)], lr=0.05, tol=1e-12,
+                                   max_iter=3000)
+    assert trace[-1] == pytest.approx(-1.0, abs=1e-6)
+    assert abs(math.cos(th[0]) - trace[-1]) < 1e-15
+    assert trace[0] == pytest.approx(math.cos(0.1), abs=1e-15)
+
+
+def test_vqe_zero_hamiltonian_converges_at_once(oracle):
+    """a zero-term Hamiltonian gives E = 0 and g = 0, so Adam's
+    moments stay 0, theta is unchanged and |E_1 - E_0| = 0 < tol stops the loop."""
+    w = W.config3()
+    th, trace, T = oracle.vqe_adam(w.n, w.gates, w.theta, [], max_iter=10)
+    assert T == 1 and np.all(trace == 0.0)
+    np.testing.assert_array_equal(th, w.theta)
+
+
+def test_vqe_config3_energy_decreases(oracle):
+    """Descent: with lr = 1e-2 the config-3 energy trace falls over 25 steps."""
+    w = W.config3()
+    th, trace, T = oracle.vqe_adam(w.n, w.gates, w.theta, w.terms, max_iter=25)
+    assert T == 25 and trace[-1] < trace[0] - 0.05

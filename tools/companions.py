@@ -44,7 +44,8 @@ row("k_diag RZ x8 fused", 32, timed(lambda: sv.apply([("RZ", q, -1, -1, 0.1 * q)
 lq.lq_set_option(lq.LQ_OPT_FUSION, 1)
 # one fused diagonal pass: many diagonal gates
 dg = [("RZ", q, -1, -1, 0.1 * q) for q in range(n)] + [("CZ", q, q + 1, -1, 0.0) for q in range(n - 1)]
-row("tile pass: 59 diagonal gates", 32, timed(lambda: sv.apply(dg)), "one pass")
+npd = lq.lq_plan_describe(n, dg)[0]
+row(f"tile pass: 59 diagonal gates ({npd} pass)", 32 * npd, timed(lambda: sv.apply(dg)), "FP64 pass budget splits the run")
 # one tile pass of 40 random 1q/2q gates inside an 11-bit tile
 rng = np.random.default_rng(3)
 tq = list(range(n - 11, n))
@@ -57,11 +58,13 @@ npass = lq.lq_plan_describe(n, tg)[0]
 row(f"tile pass: 40 random gates ({npass} pass)", 32 * npass, timed(lambda: sv.apply(tg)))
 row("tile pass: 10 RY+10 RZ layer slice", 32, timed(lambda: sv.apply(
     [("RY", q, -1, -1, 0.3 + q) for q in range(n - 10, n)] + [("RZ", q, -1, -1, 0.2 * q) for q in range(n - 10, n)])))
-qp = (n + 10) // 11
+l0 = lq.lq_launch_count(); sv.qft(); qp = lq.lq_launch_count() - l0
 row(f"QFT({n}) ({qp} tile passes, bit reversal = relabel)", 32 * qp, timed(lambda: sv.qft()))
 xyz = W.xyz_terms(n)
-row("expval XYZ chain (93+ terms)", None or 16 * 0 + 16 * 3, timed(lambda: sv.expval(xyz)),
-    "read-only tile passes; bytes assume 3 read passes")
+ep = lq.lq_plan_export_json(n, [], xyz)
+ne, nw = len(ep["passes"]), len(ep["wide_groups"])
+row(f"expval XYZ chain ({len(xyz)} terms, {ne} read-only passes)", 16 * ne + 32 * nw, timed(lambda: sv.expval(xyz)),
+    f"{len(ep['groups'])} x-mask groups in {ne} read-only tile passes, {nw} wide groups")
 row("expval single Z group (read-only pass)", 16, timed(lambda: sv.expval([(1.0, 0, 1 << (n - 1))])))
 row("init_random (norm pass + write pass)", 16, timed(lambda: sv.init_random(5)), "ALU-heavy: log + sincospi per amp")
 print("JSON " + json.dumps(out))
