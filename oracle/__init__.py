@@ -17,6 +17,7 @@ oracle at n <= 6.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 from concurrent.futures import ThreadPoolExecutor
@@ -237,3 +238,39 @@ def vqe_adam(n: int, gates, theta0, terms, lr: float = 1e-2, beta1: float = 0.9,
         v_hat = v / (1.0 - beta2 ** (t + 1))
         theta = theta - (lr * m_hat) / (np.sqrt(v_hat) + eps)
         t += 1
+
+
+def xyz_hamiltonian(n: int, jx: float, jy: float, jz: float, h: float):
+    """Eq. (9), PAPER.md:786: H = -sum_{i<n-1} (Jx X_i X_{i+1} + Jy Y_i Y_{i+1}
+    + Jz Z_i Z_{i+1}) - h sum_i Z_i (open chain, reading A10) as Pauli terms
+    (coeff, x_mask, z_mask) with bit q = qubit q."""
+    terms = []
+    for i in range(n - 1):
+        m = (1 << i) | (1 << (i + 1))
+        terms += [(-jx, m, 0), (-jy, m, m), (-jz, 0, m)]
+    terms += [(-h, 0, 1 << i) for i in range(n)]
+    return terms
+
+
+def trotter_xyz(psi: np.ndarray, jx: float, jy: float, jz: float, amp: float, omega: float, t0: float,
+                dt: float, n_steps: int, record_every: int = 1) -> np.ndarray:
+    """First-order Trotter evolution (Eq. 12) of psi in place:
+    step j applies exp(-i H_k(t_j) dt) for the groups of P:825-831 in the
+    order RXX(-2 Jx dt) on (i, i+1) for i ascending, RYY(-2 Jy dt), RZZ(-2 Jz
+    dt), RZ(-2 h(t_j) dt) on each qubit, h(t) = amp sin(omega t)
+    (signs of Eq. 9, reading A20; order SPEC.md:541), each gate as its
+    native matrix.  Returns E(t) = <psi|H(t)|psi> (Eq. 13) at t0 and after
+    every record_every steps."""
+    n = psi.size.bit_length() - 1
+    h = lambda t: amp * math.sin(omega * t)
+    out = [expval(psi, xyz_hamiltonian(n, jx, jy, jz, h(t0)))]
+    for j in range(n_steps):
+        tj = t0 + j * dt
+        gates = []
+        for name, J in (("RXX", jx), ("RYY", jy), ("RZZ", jz)):
+            gates += [(name, i, i + 1, -1, -2.0 * J * dt) for i in range(n - 1)]
+        gates += [("RZ", i, -1, -1, -2.0 * h(tj) * dt) for i in range(n)]
+        apply_circuit(psi, gates)
+        if (j + 1) % record_every == 0:
+            out.append(expval(psi, xyz_hamiltonian(n, jx, jy, jz, h(t0 + (j + 1) * dt))))
+    return np.array(out)

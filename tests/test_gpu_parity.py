@@ -494,3 +494,39 @@ def test_vqe_adam_single_qubit_and_zero_hamiltonian(lq):
     np.testing.assert_array_equal(th, w.theta)
     with pytest.raises(lq.LQError):
         lq.lq_vqe_adam(1, [("RY", 0, -1, 0, 0.0)], [float("nan")], [(1.0, 0, 1)])
+
+
+# ---------------------------------------------------------------- Trotter XYZ (f1)
+
+def test_trotter_xyz_vs_oracle(lq, oracle):
+    """lq_trotter_xyz (macro-steps of up to 8 Trotter steps per fused plan,
+    RXX/RYY lowered to CNOT-RX-CNOT) vs the oracle's native-matrix steps:
+    energies and final amplitudes, n = 11, from |1...1> and from a random
+    state, record cadences 1 and 5."""
+    n = 11
+    for init, rec, steps in (("ones", 1, 12), ("random", 5, 23)):
+        sv = lq.StateVector(n)
+        ref = oracle.init_basis(n, (1 << n) - 1) if init == "ones" else oracle.init_random(n, 17)
+        if init == "ones":
+            sv.init_basis((1 << n) - 1)
+        else:
+            sv.init_random(17)
+        E = sv.trotter_xyz(1.0, 0.7, 0.4, 2.0, 1.0, 0.1, 0.05, steps, rec)
+        Eo = oracle.trotter_xyz(ref, 1.0, 0.7, 0.4, 2.0, 1.0, 0.1, 0.05, steps, rec)
+        assert E.size == Eo.size == 1 + steps // rec
+        np.testing.assert_allclose(E, Eo, rtol=0, atol=1e-10 * max(1.0, np.abs(Eo).max()))
+        assert np.abs(sv.read() - ref).max() <= AMP_TOL
+        sv.free()
+
+
+def test_trotter_diagonal_chain_closed_form_n20(lq):
+    """Jx = Jy = 0 from |1...1>: E(t) = -Jz (n-1) + n A sin(w t) exactly."""
+    n = 20
+    sv = lq.StateVector(n).init_basis((1 << n) - 1)
+    E = sv.trotter_xyz(0.0, 0.0, 1.0, 2.0, 1.0, 0.0, 0.02, 50, 10)
+    t = 0.02 * 10 * np.arange(E.size)
+    np.testing.assert_allclose(E, -(n - 1) + n * 2.0 * np.sin(t), rtol=0, atol=1e-12)
+    assert abs(sv.norm2() - 1) < 1e-12
+    with pytest.raises(lq.LQError):
+        sv.trotter_xyz(1.0, 1.0, 1.0, 0.0, 1.0, 0.0, -0.1, 3)
+    sv.free()

@@ -490,3 +490,60 @@ def test_vqe_config3_energy_decreases(oracle):
     w = W.config3()
     th, trace, T = oracle.vqe_adam(w.n, w.gates, w.theta, w.terms, max_iter=25)
     assert T == 25 and trace[-1] < trace[0] - 0.05
+
+
+# ---------------------------------------------------------------- Trotter XYZ (f1)
+
+def test_trotter_diagonal_chain_closed_form(oracle):
+    """with Jx = Jy = 0 the Hamiltonian is diagonal and |1...1>
+    stays an eigenstate: <Z_i Z_{i+1}> = 1, <Z_i> = -1, so
+    E(t) = -Jz (n-1) + n h(t) exactly at every recorded time."""
+    n, jz, A, w = 6, 1.0, 2.0, 1.0
+    psi = oracle.init_basis(n, (1 << n) - 1)
+    E = oracle.trotter_xyz(psi, 0.0, 0.0, jz, A, w, 0.0, 0.05, 40, record_every=4)
+    t = 0.05 * 4 * np.arange(E.size)
+    np.testing.assert_allclose(E, -jz * (n - 1) + n * A * np.sin(w * t), rtol=0, atol=1e-13)
+    assert abs(oracle.norm2(psi) - 1) < 1e-13
+
+
+def _expm_reference(oracle, n, jx, jy, jz, A, w, t0, dt, steps):
+    """Piecewise-constant exact propagator: prod_j exp(-i H(t_j) dt) through
+    dense matrices (fullmatrix route + scipy expm), from |1...1>."""
+    from scipy.linalg import expm
+    psi = np.zeros(1 << n, np.complex128)
+    psi[-1] = 1.0
+    for j in range(steps):
+        Hm = FM.hamiltonian_matrix(n, oracle.xyz_hamiltonian(n, jx, jy, jz, A * math.sin(w * (t0 + j * dt))))
+        psi = expm(-1j * dt * Hm) @ psi
+    return psi
+
+
+def test_trotter_first_order_error_ratio(oracle):
+    """halving dt halves the first-order Trotter error against
+    the exact piecewise-constant propagator (ratio in [1.7, 2.3]), N = 4."""
+    n, T = 4, 1.0
+    errs = []
+    for steps in (50, 100):
+        dt = T / steps
+        psi = oracle.init_basis(n, (1 << n) - 1)
+        oracle.trotter_xyz(psi, 1.0, 0.7, 0.4, 2.0, 1.0, 0.0, dt, steps, record_every=steps)
+        ref = _expm_reference(oracle, n, 1.0, 0.7, 0.4, 2.0, 1.0, 0.0, dt, steps)
+        errs.append(np.abs(psi - ref).max())
+    assert 1.7 <= errs[0] / errs[1] <= 2.3, errs
+    assert errs[1] < 1e-2
+
+
+def test_trotter_small_step_and_static_drift(oracle):
+    """One step with dt -> 0 is the identity to O(dt); with A = 0 the energy
+    drift over a fixed time shrinks with dt."""
+    n = 5
+    psi = oracle.init_random(n, 3)
+    ref = psi.copy()
+    oracle.trotter_xyz(psi, 1.0, 0.7, 0.4, 2.0, 1.0, 0.3, 1e-6, 1)
+    assert 0 < np.abs(psi - ref).max() < 1e-5
+    drift = []
+    for steps in (20, 80):
+        psi = oracle.init_random(n, 4)
+        E = oracle.trotter_xyz(psi, 1.0, 0.7, 0.4, 0.0, 1.0, 0.0, 1.0 / steps, steps, record_every=steps)
+        drift.append(abs(E[-1] - E[0]))
+    assert drift[1] < drift[0]
