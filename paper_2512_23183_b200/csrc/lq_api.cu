@@ -1592,7 +1592,14 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     // the Pauli groups ride on the circuit's own tile passes (read after the
     // last gate that touches their qubits)
     lower_pauli(n_qubits, qm, terms, n_terms, ops, P->plan);
-    plan_circuit(n_qubits, ops, options(), P->mb, P->plan);
+    PlanOptions po = options();
+    {
+        // tuning experiments only: a smaller budget for the write-only first
+        // pass added passes and time (3.07 -> 3.12-3.21 s), so it is off
+        const char *fb = getenv("LQ_FIRST_BUDGET");
+        po.first_budget = fb ? atoi(fb) : 0;
+    }
+    plan_circuit(n_qubits, ops, po, P->mb, P->plan);
     {
         lq_status js = prepare(P->plan, true);
         if (js != LQ_OK) {

@@ -58,9 +58,12 @@ enum KOpType : uint8_t {
     K_SCALE = 7, // multiply every amplitude by `scale`
     K_EXPV = 8,  // Pauli-group expectation contribution (read-only; see ETerm)
     K_G = 9,     // scaled 2x2 rotation on register bit r0 (RY / RX / H, see GKind)
-    K_DT = 10    // run of uncontrolled register-bit diagonals as one 16-entry phase table (flags = count;
+    K_DT = 10,   // run of uncontrolled register-bit diagonals as one 16-entry phase table (flags = count;
                  // mat = offset in cst of the members' (register position, table offset) pairs)
+    K_GG = 11    // RXX / RYY: scaled rotation on the register pairs (v, v ^ (r0 | r1)) (GK_IMAG table;
+                 // flags & GG_YY: RYY, whose 00<->11 pairs rotate the other way)
 };
+constexpr uint8_t GG_YY = 1;
 
 // Scaled rotation families (K_G; qj holds the family).  Every matrix is
 // lambda * M with M having unit entries, so an amplitude pair costs 4 DFMA
@@ -122,7 +125,8 @@ enum CodeTile : uint8_t {
     C_G = 36,        // + 4*GKind + r0: scaled rotation on a register bit, no register control
     C_D1U = 48,      // diagonal on a bit outside the tile, controls outside the tile (tile-uniform factor)
     C_DT = 49,       // K_DT phase table
-    C_NUM = 50
+    C_GG = 50,       // + pair index of (r0, r1): (0,1) (0,2) (0,3) (1,2) (1,3) (2,3)
+    C_NUM = 56
 };
 
 // KOp.flags bits for diagonal ops (QF_* are QFT-only)
@@ -185,6 +189,7 @@ LQ_HD inline int op_table_size(uint8_t type) {
     case K_QFT: return 16;
     case K_SCALE: return 1;
     case K_G: return 2;
+    case K_GG: return 2;
     case K_DT: return 17;     // prod d0, then T[v] = prod over members with bit set of d1/d0
     default: return 0;
     }

@@ -15,7 +15,7 @@ static inline uint64_t bit(int b) { return 1ull << b; }
 uint64_t POp::full() const {
     switch (type) {
     case K_U1: case K_X: case K_QFT: case K_G: return bit(t0);
-    case K_U2: case K_SWAP: return bit(t0) | bit(t1);
+    case K_U2: case K_SWAP: case K_GG: return bit(t0) | bit(t1);
     case K_EXPV: return xm;
     default: return 0;
     }
@@ -38,6 +38,7 @@ bool commute(const POp &a, const POp &b) {
 int op_fp64_cost(const POp &o) {
     switch (o.type) {
     case K_G: return 20;       // 4 DFMA per amplitude pair
+    case K_GG: return 20;      // 4 DFMA per amplitude pair (RXX / RYY)
     case K_U1: return 80;      // general complex 2x2
     case K_U2: return 160;     // general complex 4x4
     case K_D1: return 12;      // register-bit half multiply / table share / thread constant
@@ -80,45 +81,8 @@ static bool is_diag_1q(int k) {
     return k == LQ_Z || k == LQ_S || k == LQ_SDG || k == LQ_T || k == LQ_TDG || k == LQ_RZ;
 }
 
-// RXX and RYY as cheap ops (Trotter steps of PAPER.md:825-831, SURVEY §8(f)
-// f1): CNOT_ab X_a CNOT_ab = X_a X_b, so RXX_ab(t) = CNOT_ab RX_a(t) CNOT_ab
-// (two folded permutations and one scaled rotation, 2 FP64 ops per
-// amplitude instead of a general 4x4); Y = S X S^dag, so RYY_ab(t) =
-// (S_a S_b) RXX_ab(t) (S_a^dag S_b^dag) (diagonals join the diagonal runs).
-static std::vector<lq_gate> expand_pair_rotations(const lq_gate *gates, size_t n_gates) {
-    std::vector<lq_gate> out;
-    out.reserve(n_gates);
-    for (size_t i = 0; i < n_gates; i++) {
-        const lq_gate &G = gates[i];
-        if (G.kind != LQ_RXX && G.kind != LQ_RYY) {
-            out.push_back(G);
-            continue;
-        }
-        auto mk = [&](int kind, int a, int b) {
-            lq_gate x = G;
-            x.kind = kind;
-            x.q0 = a;
-            x.q1 = b;
-            x.q2 = -1;
-            x.mat = nullptr;
-            if (kind != LQ_RX) { x.param_idx = -1; x.angle = 0.0; }
-            return x;
-        };
-        const bool yy = G.kind == LQ_RYY;
-        if (yy) { out.push_back(mk(LQ_SDG, G.q0, -1)); out.push_back(mk(LQ_SDG, G.q1, -1)); }
-        out.push_back(mk(LQ_CNOT, G.q0, G.q1));
-        out.push_back(mk(LQ_RX, G.q0, -1));
-        out.push_back(mk(LQ_CNOT, G.q0, G.q1));
-        if (yy) { out.push_back(mk(LQ_S, G.q0, -1)); out.push_back(mk(LQ_S, G.q1, -1)); }
-    }
-    return out;
-}
-
-void lower_gates(int n, const lq_gate *gates_in, size_t n_gates_in, int32_t *qmap,
+void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
                  std::vector<POp> &ops, MatBuilder &mb) {
-    const std::vector<lq_gate> expanded = expand_pair_rotations(gates_in, n_gates_in);
-    const lq_gate *gates = expanded.data();
-    const size_t n_gates = expanded.size();
     std::vector<std::vector<MFactor>> fl;   // factor list per op
     std::vector<int> last(64, -1);          // last op touching each physical bit
     std::vector<char> fusable;              // op is an uncontrolled 1q op
@@ -200,8 +164,9 @@ void lower_gates(int n, const lq_gate *gates_in, size_t n_gates_in, int32_t *qma
         case LQ_CP:   op.type = K_D1; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); break;
         case LQ_CRY:  op.type = K_U1; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); f.kind = LQ_RY; break;
         case LQ_U2:   op.type = K_U2; op.t0 = qmap[G.q0]; op.t1 = qmap[G.q1]; f.cst = mb.add_const(G.mat, 16); break;
-        case LQ_RXX: case LQ_RYY:
-                      op.type = K_U2; op.t0 = qmap[G.q0]; op.t1 = qmap[G.q1]; break;
+        case LQ_RXX: case LQ_RYY:   // scaled pair rotation on two register bits (tile.cuh ap_gg)
+                      op.type = K_GG; op.t0 = qmap[G.q0]; op.t1 = qmap[G.q1];
+                      op.qj = GK_IMAG; op.qflags = G.kind == LQ_RYY ? GG_YY : 0; break;
         case LQ_RZZ:  op.type = K_D2; op.t0 = qmap[G.q0]; op.t1 = qmap[G.q1]; break;
         default: break;
         }
@@ -214,7 +179,7 @@ void lower_gates(int n, const lq_gate *gates_in, size_t n_gates_in, int32_t *qma
         POp &P = ops[i];
         auto &F = fl[i - base];
         if (P.type == K_X || P.type == K_QFT) { P.spec = -1; continue; }
-        MForm form = P.type == K_D1 ? MF_DIAG2 : P.type == K_U1 ? MF_U2x2 : P.type == K_G ? MF_G
+        MForm form = P.type == K_D1 ? MF_DIAG2 : P.type == K_U1 ? MF_U2x2 : (P.type == K_G || P.type == K_GG) ? MF_G
                    : P.type == K_U2 ? MF_U4x4 : MF_DIAG4;
         P.spec = mb.add_spec(form, F);
     }
@@ -406,6 +371,13 @@ static uint8_t tile_code(const KOp &k) {
         break;
     case K_G:
         if (k.rcm == 0 && k.r0 < R) return (uint8_t)(C_G + 4 * k.qj + k.r0);
+        break;
+    case K_GG:
+        if (k.rcm == 0 && k.r0 < R && k.r1 < R && k.r0 != k.r1) {
+            const int lo = std::min(k.r0, k.r1), hi = std::max(k.r0, k.r1);
+            static const int idx[4][4] = {{-1, 0, 1, 2}, {-1, -1, 3, 4}, {-1, -1, -1, 5}, {-1, -1, -1, -1}};
+            return (uint8_t)(C_GG + idx[lo][hi]);
+        }
         break;
     case K_X:
         if (k.rcm == 0 && k.r0 < R) return (uint8_t)(C_X + k.r0);
@@ -816,8 +788,11 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
         if (!skip[i]) rem.push_back((int)i);
     // the FP64 budget trades an extra HBM round trip for less arithmetic per
     // pass; a state that is one tile has no HBM round trip to trade
-    const int budget = nl > K ? opt.budget : 0;
+    const int budget_all = nl > K ? opt.budget : 0;
     while (!rem.empty()) {
+        // the first pass of a PSR circuit synthesises |0...0> (no load): half
+        // the HBM time, so half the FP64 budget (opt.first_budget)
+        const int budget = (plan.passes.empty() && opt.first_budget > 0 && budget_all) ? opt.first_budget : budget_all;
         uint64_t Tm = mand;
         std::vector<int> absorbed, absorbed_w;
         first_fit(ops, rem, K, Tm, absorbed, budget);
@@ -938,7 +913,22 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
     else for (int j = 0; j < n; j++) js.push_back(j);
     auto phys = [&](int j) { return layout_rev ? n - 1 - j : j; };
 
+    // passes the greedy stage packing below makes with K tile bits
+    auto count_passes = [&](int Kc) {
+        const int cc = std::max(0, std::min(opt.coalesce, Kc - 1));
+        const uint64_t m0 = (n > Kc) ? ((1ull << cc) - 1) : ((1ull << n) - 1);
+        int np = 0;
+        for (size_t s0 = 0; s0 < js.size(); np++) {
+            uint64_t Tm = m0;
+            while (s0 < js.size() && popc(Tm | bit(phys(js[s0]))) <= Kc) Tm |= bit(phys(js[s0++]));
+        }
+        return np;
+    };
     int K = opt.K > 0 ? std::min(opt.K, n) : auto_tile_bits(n);
+    // automatic size: 12 tile bits (one CTA per SM) when that saves a whole
+    // pass -- at n = 30 four passes of 11 bits take 29.2 ms, three of 12 take
+    // 25.0 ms (B200)
+    if (opt.K <= 0 && n > 12 && count_passes(12) < count_passes(K)) K = 12;
     if (K > 12) K = 12;
     if (n <= K) K = n;
     int Rr = std::min(std::max(1, std::min(opt.reg_bits, R)), K);

@@ -88,6 +88,7 @@ struct PlanOptions {
     int reg_bits = 4;        // register bits per thread (R); tile kernels run 2^(K-R) threads
     int n_local = 0;         // sharded state: only bits [0, n_local) are local (0 = all n bits)
     int budget = 0;          // FP64 budget of a tile pass in tenths of an instruction per amplitude (0: none)
+    int first_budget = 0;    // budget of the plan's first pass when it does not load (PSR, PF_LOAD_ZERO); 0: budget
 };
 
 // Estimated FP64 instructions per amplitude (x10) an op costs in a tile pass.

@@ -304,6 +304,50 @@ __device__ __forceinline__ void ap_g(double2 (&a)[1 << RR], const double2 *M, bo
     }
 }
 
+// RXX / RYY on register positions (P0, P1):
+// RXX(t) = cos(t/2) I - i sin(t/2) X(x)X rotates every pair (v, v ^ m),
+// m = 2^P0 | 2^P1, by [[c, -is], [-is, c]] = lambda * (GK_IMAG table); RYY
+// does the same on the 01<->10 pairs and the opposite rotation on the
+// 00<->11 pairs (Y(x)Y|00> = -|11>).  NEG flips the sign of the imaginary
+// off-diagonal: [[1, +ip], [+ip, 1]] (variant 0) or [[p, +i], [+i, p]]
+// (variant 1).  Register flips (fb) keep the pairing; they swap the RYY
+// classes when exactly one of the two bits is flipped.
+template <bool ALT, bool NEG>
+__device__ __forceinline__ void gg_pair(double2 &x, double2 &y, double p) {
+    const double2 X = x, Y = y;
+    if constexpr (!ALT) {
+        const double q = NEG ? -p : p;
+        x = make_double2(fma(q, Y.y, X.x), fma(-q, Y.x, X.y));
+        y = make_double2(fma(q, X.y, Y.x), fma(-q, X.x, Y.y));
+    } else if constexpr (!NEG) {
+        x = make_double2(fma(p, X.x, Y.y), fma(p, X.y, -Y.x));
+        y = make_double2(fma(p, Y.x, X.y), fma(p, Y.y, -X.x));
+    } else {
+        x = make_double2(fma(p, X.x, -Y.y), fma(p, X.y, Y.x));
+        y = make_double2(fma(p, Y.x, -X.y), fma(p, Y.y, X.x));
+    }
+}
+
+template <int RR, int P0, int P1, bool ALT>
+__device__ __forceinline__ void ap_gg_(double2 (&a)[1 << RR], double p, bool yy, bool swapc) {
+#pragma unroll
+    for (int v = 0; v < (1 << RR); v++) {
+        if (v & (1 << P0)) continue;
+        const int w = v ^ ((1 << P0) | (1 << P1));
+        const bool same = !((v >> P1) & 1);   // v, w hold 00 / 11 (before flips)
+        if (yy && (same != swapc)) gg_pair<ALT, true>(a[v], a[w], p);
+        else gg_pair<ALT, false>(a[v], a[w], p);
+    }
+}
+
+template <int RR, int P0, int P1>
+__device__ __forceinline__ void ap_gg(double2 (&a)[1 << RR], const double2 *M, bool yy, uint32_t fb) {
+    const double p = M[0].x;
+    const bool swapc = (((fb >> P0) ^ (fb >> P1)) & 1) != 0;
+    if (M[1].x != 0.0) ap_gg_<RR, P0, P1, true>(a, p, yy, swapc);
+    else ap_gg_<RR, P0, P1, false>(a, p, yy, swapc);
+}
+
 // Deferred scalars.  The register tile holds
 // psi / (tsc * ph):
 //   tsc (complex) collects factors identical on every thread of the tile --
@@ -519,6 +563,19 @@ __device__ __forceinline__ void apply_generic(double2 (&a)[1 << RR], const KOp &
         }
         break;
     }
+    case K_GG: {   // (normally specialised as C_GG; kept complete for the generic path)
+        if constexpr (RR >= 2) {
+            const int lo = op.r0 < op.r1 ? op.r0 : op.r1, hi = op.r0 < op.r1 ? op.r1 : op.r0;
+            const bool yy = op.flags & GG_YY;
+            switch (lo * 4 + hi) {
+#define CGG(p0, p1) case p0 * 4 + p1: if (RR > p1) ap_gg<RR, p0, (RR > p1 ? p1 : 1)>(a, M, yy, 0u); break;
+            CGG(0, 1) CGG(0, 2) CGG(0, 3) CGG(1, 2) CGG(1, 3) CGG(2, 3)
+#undef CGG
+            default: break;
+            }
+        }
+        break;
+    }
     case K_SWAP: {
         if constexpr (RR >= 2) {
             const int lo = op.r0 < op.r1 ? op.r0 : op.r1, hi = op.r0 < op.r1 ? op.r1 : op.r0;
@@ -698,6 +755,14 @@ __device__ __forceinline__ void exec_op(double2 (&a)[1 << RR], const KOp &op, co
 #pragma unroll
             for (int v = 0; v < (1 << RR); v++) a[v] = cmul(a[v], M[1 + (v ^ ts.fb)]);
         }
+    } else if constexpr (CODE >= C_GG && CODE < C_GG + 6) {
+        constexpr int PI = CODE - C_GG;
+        constexpr int P0 = PI < 3 ? 0 : (PI < 5 ? 1 : 2);
+        constexpr int P1 = PI < 3 ? PI + 1 : (PI < 5 ? PI - 1 : 3);
+        if constexpr (RR > P1) {
+            ap_gg<RR, P0, P1>(a, M, (op.flags & GG_YY) != 0, ts.fb);
+            ts.tsc = cscale(ts.tsc, M[0].y);
+        }
     } else if constexpr (CODE == C_SCALE) {
         ts.tsc = cscale(ts.tsc, M[0].x);
     } else if constexpr (CODE == C_EXPV) {
@@ -709,13 +774,15 @@ __device__ __forceinline__ void exec_op(double2 (&a)[1 << RR], const KOp &op, co
     } else {
         flush_flips<RR>(a, ts.fb);
         apply_generic<RR>(a, op, M, gbase);
+        if (op.type == K_GG) ts.tsc = cscale(ts.tsc, M[0].y);   // the deferred lambda
     }
 }
 
 #define LQ_OP_CODES(X)                                                                                    \
     X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17)   \
     X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32) X(33)     \
-    X(34) X(35) X(36) X(37) X(38) X(39) X(40) X(41) X(42) X(43) X(44) X(45) X(46) X(47) X(48) X(49)
+    X(34) X(35) X(36) X(37) X(38) X(39) X(40) X(41) X(42) X(43) X(44) X(45) X(46) X(47) X(48) X(49)     \
+    X(50) X(51) X(52) X(53) X(54) X(55)
 
 // The interpreter: walks the sub-block's op list in shared memory.
 struct InterpProg {

@@ -20,3 +20,74 @@ def product_energy_and_grad(n, theta, terms_j=(1.0, 0.7, 0.4), hz=0.3):
                 gp[q] += np.sum(J * db_dp[q] * b[nb])
         gt[q] += hz * db_dt[q, 2]
     return E, np.concatenate([gt, gp])
+
+
+# ---- monomial circuits (SURVEY c.4 (i), (vi)): X, Y, Z, S, T, RZ, CNOT, CZ
+# map basis states to phased basis states; qubit q <-> index bit n-1-q.
+_DIAG1 = {"Z": lambda a: -1.0, "S": lambda a: 1j, "T": lambda a: np.exp(1j * np.pi / 4)}
+
+
+def _bit(k, n, q):
+    return (k >> (n - 1 - q)) & 1
+
+
+def monomial_forward(n, gates, k):
+    """|k> -> phase |k'> through the circuit (closed form, O(#gates))."""
+    ph = 1.0 + 0j
+    for name, a, b, _, ang in gates:
+        if name == "X":
+            k ^= 1 << (n - 1 - a)
+        elif name == "Y":              # Y|0> = i|1>, Y|1> = -i|0>
+            ph *= -1j if _bit(k, n, a) else 1j
+            k ^= 1 << (n - 1 - a)
+        elif name in _DIAG1:
+            if _bit(k, n, a):
+                ph *= _DIAG1[name](ang)
+        elif name == "RZ":             # diag(e^{-i t/2}, e^{i t/2})
+            ph *= np.exp(0.5j * ang) if _bit(k, n, a) else np.exp(-0.5j * ang)
+        elif name == "CNOT":
+            if _bit(k, n, a):
+                k ^= 1 << (n - 1 - b)
+        elif name == "CZ":
+            if _bit(k, n, a) and _bit(k, n, b):
+                ph = -ph
+        else:
+            raise ValueError(name)
+    return k, ph
+
+
+def monomial_backward(n, gates, j):
+    """Output basis index j -> (input index k, phase) with <j|C|k> = phase."""
+    ph = 1.0 + 0j
+    for name, a, b, _, ang in reversed(gates):
+        if name == "X":
+            j ^= 1 << (n - 1 - a)
+        elif name == "Y":              # out bit 1 came from |0> with i, out 0 from |1> with -i
+            ph *= 1j if _bit(j, n, a) else -1j
+            j ^= 1 << (n - 1 - a)
+        elif name in _DIAG1:
+            if _bit(j, n, a):
+                ph *= _DIAG1[name](ang)
+        elif name == "RZ":
+            ph *= np.exp(0.5j * ang) if _bit(j, n, a) else np.exp(-0.5j * ang)
+        elif name == "CNOT":
+            if _bit(j, n, a):
+                j ^= 1 << (n - 1 - b)
+        elif name == "CZ":
+            if _bit(j, n, a) and _bit(j, n, b):
+                ph = -ph
+        else:
+            raise ValueError(name)
+    return j, ph
+
+
+def monomial_inverse(gates):
+    inv = {"S": "SDG", "T": "TDG"}
+    return [(inv.get(g[0], g[0]), g[1], g[2], g[3], -g[4] if g[0] == "RZ" else g[4]) for g in reversed(gates)]
+
+
+def qft_of_basis(n, k, idx):
+    """QFT|k> at indices idx: N^-1/2 e^{2 pi i ((j k) mod N) / N}."""
+    N = 1 << n
+    jk = (np.asarray(idx, dtype=object) * int(k)) % N
+    return np.exp(2j * np.pi * np.array([float(x) for x in jk]) / N) / np.sqrt(N)

@@ -14,7 +14,8 @@ import math
 import numpy as np
 
 NOREG = 255
-K_U1, K_D1, K_X, K_U2, K_D2, K_SWAP, K_QFT, K_SCALE, K_EXPV, K_G, K_DT = range(11)
+K_U1, K_D1, K_X, K_U2, K_D2, K_SWAP, K_QFT, K_SCALE, K_EXPV, K_G, K_DT, K_GG = range(12)
+GG_YY = 1
 GK_REAL, GK_IMAG, GK_HAD = range(3)
 FK_YDIAG = 100
 PASS_TILE, PASS_PAIR, PASS_DIAG = 0, 1, 2
@@ -132,7 +133,18 @@ def _apply_op(x, g, op, S, mats, cstc, n, et_all, et0, lpos=None):
             bit = (L >> S[pos]) & 1
             x *= np.where(bit == 1, mats[off + 1], mats[off])
         return 0.0
-    M = mats[op["mat"]:op["mat"] + 16] if typ in (K_U1, K_D1, K_U2, K_D2, K_G) else None
+    M = mats[op["mat"]:op["mat"] + 16] if typ in (K_U1, K_D1, K_U2, K_D2, K_G, K_GG) else None
+    if typ == K_GG:  # RXX / RYY: lambda * [[one, -i off] on 01<->10, -+i off on 00<->11]
+        p, lam, alt = M[0].real, M[0].imag, M[1].real != 0
+        one, off = (p, 1.0) if alt else (1.0, p)
+        s3 = 1j * off if op["flags"] & GG_YY else -1j * off
+        U = np.zeros((4, 4), np.complex128)
+        for d in range(4):
+            U[d, d] = one
+        U[0, 3] = U[3, 0] = s3
+        U[1, 2] = U[2, 1] = -1j * off
+        M = lam * U.reshape(-1)
+        typ = K_U2
     if typ == K_G:   # lambda * M (lq_internal.h GKind)
         p, lam, alt = M[0].real, M[0].imag, M[1].real != 0
         one, off = (p, 1.0) if alt else (1.0, p)
@@ -240,9 +252,9 @@ def run(plan, psi, theta=None, shift=None, gofs=0):
                 # physical form: b0/b1 are bits, controls in cmask
                 S_phys = [op["b0"], op["b1"], 0, 0]
                 op2 = dict(op)
-                if op["type"] in (K_U1, K_X, K_U2, K_SWAP, K_G):
+                if op["type"] in (K_U1, K_X, K_U2, K_SWAP, K_G, K_GG):
                     op2["r0"], op2["r1"] = 0, 1
-                _apply_op(psi, gidx, op2 if op["type"] in (K_U1, K_X, K_U2, K_SWAP, K_G) else op,
+                _apply_op(psi, gidx, op2 if op["type"] in (K_U1, K_X, K_U2, K_SWAP, K_G, K_GG) else op,
                           S_phys, mats, cstc, n, et_all, 0)
             continue
         T = p["T"]

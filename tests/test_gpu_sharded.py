@@ -117,3 +117,67 @@ def test_nccl_loads_and_single_rank_comm(lq):
     assert sv.read()[3] == 1
     sv.free()
     lq.lq_comm_free(c)
+
+
+# ---------------------------------------------------------------- full-scale sharded runs (c.4)
+
+def _big(lq, n, G):
+    import torch
+    torch.cuda.empty_cache()
+    return lq.ShardedState(n, group_world=G)
+
+
+def test_sharded_n32_monomial_qft_closed_form_and_roundtrip(lq):
+    """SURVEY c.4 (i)+(ii)+(iii) at n = 32 on G = 2 shards (64 GiB): a
+    1000-gate monomial circuit (30 % on the global qubit) from a basis state,
+    then the full QFT; 2^20 sampled amplitudes against the closed form
+    e^{i phi} N^-1/2 e^{2 pi i j k' / N}; then QFT^-1 and the inverse circuit
+    return the basis state; the norm stays 1."""
+    from closed_forms import monomial_forward, monomial_inverse, qft_of_basis
+    n, G = 32, 2
+    rng = np.random.default_rng(3232)
+    gates = W.monomial_circuit(n, 1000, rng, global_qubits=1, p_global=0.3)
+    k = int(rng.integers(0, 1 << n))
+    kp, ph = monomial_forward(n, gates, k)
+    sv = _big(lq, n, G)
+    sv.init_basis(k).apply(gates).qft()
+    idx = np.unique(rng.integers(0, 1 << n, size=1 << 20, dtype=np.uint64))
+    got = sv.gather(idx)
+    want = ph * qft_of_basis(n, kp, idx)
+    assert np.abs(got - want).max() <= 1e-12
+    assert abs(sv.norm2() - 1.0) <= 1e-11
+    sv.qft(inverse=True).apply(monomial_inverse(gates))
+    back = sv.gather(np.array([k, k ^ 1, (k + 12345) % (1 << n)], dtype=np.uint64))
+    assert abs(back[0] - 1.0) <= 1e-11 and np.abs(back[1:]).max() <= 1e-11
+    sv.free()
+
+
+def test_sharded_n32_single_qubit_layer_monomial_tail(lq):
+    """SURVEY c.4 (vi) at n = 32, G = 2: an H/RX/RY on every qubit from
+    |0...0> (H/RX/RY on the global qubit force real swaps), then a monomial
+    tail (30 % global); any amplitude j = phase(j) prod_q (U_q|0>)_{b_q(k(j))}
+    by walking the tail backwards; 2^16 sampled indices."""
+    from closed_forms import monomial_backward
+    n, G = 32, 2
+    rng = np.random.default_rng(3233)
+    layer, col = [], []
+    for q in range(n):
+        kind = ["H", "RX", "RY"][int(rng.integers(0, 3))]
+        t = float(rng.uniform(0, 2 * np.pi))
+        layer.append((kind, q, -1, -1, t if kind != "H" else 0.0))
+        c, s = np.cos(t / 2), np.sin(t / 2)
+        col.append({"H": (1 / np.sqrt(2), 1 / np.sqrt(2)), "RX": (c, -1j * s), "RY": (c, s)}[kind])
+    tail = W.monomial_circuit(n, 600, rng, global_qubits=1, p_global=0.3)
+    sv = _big(lq, n, G)
+    sv.init_basis(0).apply(layer + tail)
+    idx = np.unique(rng.integers(0, 1 << n, size=1 << 16, dtype=np.uint64))
+    got = sv.gather(idx)
+    want = np.empty(idx.size, np.complex128)
+    for i, j in enumerate(idx.tolist()):
+        kk, ph = monomial_backward(n, tail, j)
+        a = ph
+        for q in range(n):
+            a *= col[q][(kk >> (n - 1 - q)) & 1]
+        want[i] = a
+    assert np.abs(got - want).max() <= 1e-12
+    sv.free()

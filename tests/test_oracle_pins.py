@@ -547,3 +547,39 @@ def test_trotter_small_step_and_static_drift(oracle):
         E = oracle.trotter_xyz(psi, 1.0, 0.7, 0.4, 0.0, 1.0, 0.0, 1.0 / steps, steps, record_every=steps)
         drift.append(abs(E[-1] - E[0]))
     assert drift[1] < drift[0]
+
+
+def test_monomial_closed_forms_match_oracle(oracle):
+    """The monomial trackers used by the full-scale sharded GPU tests (c.4 (i),
+    (vi)) agree with the oracle at n = 8 (forward map + QFT closed form,
+    inverse circuit, backward walk after a 1q layer)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from closed_forms import monomial_backward, monomial_forward, monomial_inverse, qft_of_basis
+    n = 8
+    rng = np.random.default_rng(1)
+    g = W.monomial_circuit(n, 200, rng, global_qubits=1, p_global=0.3)
+    k = 77
+    kp, ph = monomial_forward(n, g, k)
+    psi = oracle.init_basis(n, k)
+    oracle.apply_circuit(psi, g)
+    assert abs(psi[kp] - ph) < 1e-14 and abs(np.abs(psi).sum() - 1) < 1e-14
+    oracle.qft(psi)
+    assert np.abs(psi - ph * qft_of_basis(n, kp, np.arange(1 << n))).max() < 1e-14
+    oracle.qft(psi, inverse=True)
+    oracle.apply_circuit(psi, monomial_inverse(g))
+    assert abs(psi[k] - 1) < 1e-13
+    layer, col = [], []
+    for q in range(n):
+        kind, t = ["H", "RX", "RY"][q % 3], 0.3 + q
+        layer.append((kind, q, -1, -1, t if kind != "H" else 0.0))
+        c, s = np.cos(t / 2), np.sin(t / 2)
+        col.append({"H": (1 / np.sqrt(2), 1 / np.sqrt(2)), "RX": (c, -1j * s), "RY": (c, s)}[kind])
+    psi = oracle.init_basis(n, 0)
+    oracle.apply_circuit(psi, layer + g)
+    for j in range(1 << n):
+        kk, ph = monomial_backward(n, g, j)
+        a = ph
+        for q in range(n):
+            a *= col[q][(kk >> (n - 1 - q)) & 1]
+        assert abs(psi[j] - a) < 1e-14

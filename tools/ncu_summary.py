@@ -4,7 +4,10 @@ per launch dram read+write bytes vs the algorithmic bytes of that pass."""
 import csv, io, json, os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 rep, out, src = sys.argv[1], sys.argv[2], sys.argv[3]
-txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.endswith(".csv"):   # an `ncu --page raw --csv` dump made on the GPU box
+    txt = open(rep).read()
+else:
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 h, units, data = rows[0], rows[1], rows[2:]
 col = {k: i for i, k in enumerate(h)}
@@ -32,6 +35,7 @@ for i, r in enumerate(data):
     launches.append({"pass": i, "us": round(val(r, "gpu__time_duration.sum"), 2), "dram_read": dr, "dram_write": dw,
                      "alg_bytes": alg, "traffic_over_alg": round((dr + dw) / alg, 4),
                      "fp64_pipe_pct": round(val(r, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"), 1),
+                     "issue_pct": round(val(r, "sm__inst_issued.avg.pct_of_peak_sustained_active"), 1),
                      "regs": int(val(r, "launch__registers_per_thread")), "grid": int(val(r, "launch__grid_size"))})
 tot_dram = sum(l["dram_read"] + l["dram_write"] for l in launches)
 tot_alg = sum(l["alg_bytes"] for l in launches)
