@@ -40,13 +40,29 @@ __global__ void __launch_bounds__(256) k_pair(int n, uint64_t gofs, const KOp op
                 u00 = make_double2(l, 0); u01 = u00; u10 = u00; u11 = make_double2(-l, 0);
             }
         }
-        for (; i < np; i += stride) {
-            const uint64_t i0 = insert_zero64(i, op.b0);
-            if (((i0 | gofs) & op.cmask) != op.cmask) continue;
-            const uint64_t i1 = i0 | mb;
-            double2 x = psi[i0], y = psi[i1];
-            if (op.type == K_X) { psi[i0] = y; psi[i1] = x; }
-            else { psi[i0] = cfma(u00, x, cmul(u01, y)); psi[i1] = cfma(u10, x, cmul(u11, y)); }
+        // four pairs per thread and iteration, all loads issued before any
+        // store: 128 bytes in flight per thread (HBM latency hiding)
+        constexpr int U = 4;
+        for (; i < np; i += U * stride) {
+            uint64_t i0[U];
+            bool on[U];
+            double2 x[U], y[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint64_t j = i + (uint64_t)u * stride;
+                i0[u] = insert_zero64(j, op.b0);
+                on[u] = j < np && ((i0[u] | gofs) & op.cmask) == op.cmask;
+                if (on[u]) { x[u] = psi[i0[u]]; y[u] = psi[i0[u] | mb]; }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (!on[u]) continue;
+                if (op.type == K_X) { psi[i0[u]] = y[u]; psi[i0[u] | mb] = x[u]; }
+                else {
+                    psi[i0[u]] = cfma(u00, x[u], cmul(u01, y[u]));
+                    psi[i0[u] | mb] = cfma(u10, x[u], cmul(u11, y[u]));
+                }
+            }
         }
     } else {
         const uint64_t nq = 1ull << (n - 2);

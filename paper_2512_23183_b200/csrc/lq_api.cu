@@ -147,6 +147,10 @@ lq_status prepare(Plan &plan, bool reused = false) {
     const int64_t mode = g_opt_jit.load();
     if (mode == 0 || plan.n_tile == 0) return LQ_OK;
     if (mode == 1 && !reused && plan.n < 26) return LQ_OK;
+    {
+        const char *sb = getenv("LQ_SINGLEBUF");   // experiments: one tile buffer, two CTAs per SM
+        plan.single_buf = sb && atoi(sb) != 0;
+    }
     std::string err;
     if (!jit_plan(plan, plan.jit, err)) {
         plan.jit.clear();
@@ -340,10 +344,10 @@ template <int RR>
 lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
                          const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                          uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride,
-                         int n_circ, double *partials, uint64_t slot_stride, cudaStream_t st) {
+                         int n_circ, double *partials, uint64_t slot_stride, cudaStream_t st, bool single) {
     static bool attr = false;
     static int n_sm = 0;
-    const size_t smem = ((size_t)32 << kp.K) + (size_t)kp.smat * sizeof(double2) +
+    const size_t smem = ((size_t)(jk && single ? 16 : 32) << kp.K) + (size_t)kp.smat * sizeof(double2) +
                         (size_t)(kp.op_end - kp.op_begin) * sizeof(KOp) +
                         (size_t)(kp.perm_end - kp.perm_begin) * sizeof(KPerm) + (size_t)n_pterms * sizeof(KPermTerm) +
                         (256 + 32) * sizeof(uint64_t) + (size_t)(kp.sub_end - kp.sub_begin + 1) * sizeof(KSub) +
@@ -387,9 +391,9 @@ lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, cons
 lq_status launch_tile(int Rr, const void *jk, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
                       const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                       uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride, int n_circ,
-                      double *partials, uint64_t slot_stride, cudaStream_t st) {
+                      double *partials, uint64_t slot_stride, cudaStream_t st, bool single = false) {
 #define LT(RRV) launch_tile_rr<RRV>(jk, kp, subs, kops, perms, pterms, n_pterms, eterms, mats, mat_stride, cst, state, \
-                                    state_stride, n_circ, partials, slot_stride, st)
+                                    state_stride, n_circ, partials, slot_stride, st, single)
     switch (Rr) {
     case 1: return LT(1);
     case 2: return LT(2);
@@ -437,7 +441,7 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
                 npt = plan.perms[kp.perm_end - 1].term_end - plan.perms[kp.perm_begin].term_begin;
             const void *jk = i < plan.jit.size() ? plan.jit[i] : nullptr;
             LQ_TRY(launch_tile(plan.Rr, jk, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, dp.eterms, mats, mat_stride,
-                               dp.cst, state, state_stride, n_circ, partials, slot_stride, st));
+                               dp.cst, state, state_stride, n_circ, partials, slot_stride, st, plan.single_buf));
         } else if (p.kind == PASS_PAIR) {
             const KOp op = plan.kops[p.op_begin];
             uint64_t work = (op.type == K_U1 || op.type == K_X) ? (1ull << (n - 1)) : (1ull << (n - 2));

@@ -162,7 +162,9 @@ void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
         case LQ_CCX:  op.type = K_X; op.t0 = qmap[G.q2]; op.ctrl = bit(qmap[G.q0]) | bit(qmap[G.q1]); break;
         case LQ_CZ:   op.type = K_D1; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); f.kind = LQ_Z; break;
         case LQ_CP:   op.type = K_D1; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); break;
-        case LQ_CRY:  op.type = K_U1; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); f.kind = LQ_RY; break;
+        case LQ_CRY:  // controlled scaled rotation: lambda goes to the controlled threads' phase (tile.cuh)
+                      op.type = K_G; op.t0 = qmap[G.q1]; op.ctrl = bit(qmap[G.q0]); f.kind = LQ_RY;
+                      op.qj = GK_REAL; break;
         case LQ_U2:   op.type = K_U2; op.t0 = qmap[G.q0]; op.t1 = qmap[G.q1]; f.cst = mb.add_const(G.mat, 16); break;
         case LQ_RXX: case LQ_RYY:   // scaled pair rotation on two register bits (tile.cuh ap_gg)
                       op.type = K_GG; op.t0 = qmap[G.q0]; op.t1 = qmap[G.q1];

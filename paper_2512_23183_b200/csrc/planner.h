@@ -69,6 +69,7 @@ struct Plan {
     size_t n_folded = 0;      // permutation gates folded into exchanges
     std::vector<const void *> jit;    // per pass: JIT-compiled tile kernel (cudaKernel_t) or nullptr (jit.h)
     bool prepared = false;            // jit resolved (prepare() in lq_api.cu)
+    bool single_buf = false;          // JIT passes use one tile buffer, two CTAs per SM (tile.cuh D::SINGLE)
 };
 
 struct MatBuilder {

@@ -563,6 +563,23 @@ __device__ __forceinline__ void apply_generic(double2 (&a)[1 << RR], const KOp &
         }
         break;
     }
+    case K_G: {   // register-controlled scaled rotation (CRY): lambda * M applied in full on the controlled half
+        const double p = M[0].x, l = M[0].y;
+        const bool alt = M[1].x != 0.0;
+        const double one = alt ? p : 1.0, off = alt ? 1.0 : p;
+        double2 u00, u01, u10, u11;
+        if (op.qj == GK_REAL) {
+            u00 = make_double2(l * one, 0); u01 = make_double2(-l * off, 0); u10 = make_double2(l * off, 0); u11 = u00;
+        } else if (op.qj == GK_IMAG) {
+            u00 = make_double2(l * one, 0); u01 = make_double2(0, -l * off); u10 = u01; u11 = u00;
+        } else {
+            u00 = make_double2(l, 0); u01 = u00; u10 = u00; u11 = make_double2(-l, 0);
+        }
+#define CALL_U1(P) ap_u1<RR, P>(a, u00, u01, u10, u11, rcm)
+        LQ_SW4(op.r0, CALL_U1)
+#undef CALL_U1
+        break;
+    }
     case K_GG: {   // (normally specialised as C_GG; kept complete for the generic path)
         if constexpr (RR >= 2) {
             const int lo = op.r0 < op.r1 ? op.r0 : op.r1, hi = op.r0 < op.r1 ? op.r1 : op.r0;
@@ -734,7 +751,12 @@ __device__ __forceinline__ void exec_op(double2 (&a)[1 << RR], const KOp &op, co
         constexpr int GK = (CODE - C_G) / 4, P = (CODE - C_G) % 4;
         if constexpr (RR > P) {
             ap_g<RR, P, GK>(a, M, (ts.fb >> P) & 1);
-            ts.tsc = cscale(ts.tsc, M[0].y);
+            if (op.cmask) {   // thread-constant control (CRY): only this thread's amplitudes carry lambda
+                ts.ph = cscale(ts.ph, M[0].y);
+                ts.hph = true;
+            } else {
+                ts.tsc = cscale(ts.tsc, M[0].y);
+            }
         }
     } else if constexpr (CODE >= C_QFT && CODE < C_QFT + 4) {
         constexpr int P = CODE - C_QFT;
@@ -844,6 +866,7 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // Persistent tile kernel.  One CTA per SM walks the
 // tiles of all circuits of the launch (tile g = circuit * tiles_per_circ +
@@ -1151,7 +1174,9 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
     constexpr uint32_t NT = 1u << (K - RR);
     constexpr int LAST = D::NSUB - 1;
     const uint32_t t = threadIdx.x;
-    double2 *s_tab = sm + 2 * TS;
+    // D::SINGLE: one tile buffer (no in-CTA prefetch; two CTAs per SM overlap
+    // each other's loads instead) -- lets 12-bit tiles run two CTAs per SM
+    double2 *s_tab = sm + (D::SINGLE ? 1 : 2) * TS;
     ETerm *s_et = reinterpret_cast<ETerm *>(s_tab + P.smat);
     const uint32_t nops = P.op_end - P.op_begin;
     const uint32_t net = P.eterm_end - P.eterm_begin;
@@ -1170,13 +1195,19 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
     };
     uint32_t g = blockIdx.x;
     if (g >= total_tiles) return;
-    if (!zero) issue(g, sm);
-    cp_async_commit();
+    if constexpr (!D::SINGLE) {
+        if (!zero) issue(g, sm);
+        cp_async_commit();
+    }
     int cur_circ = -1;
     for (uint32_t i = 0; g < total_tiles; i++, g += gridDim.x) {
         const uint32_t gn = g + gridDim.x;
-        double2 *b = sm + (i & 1) * TS;
-        if (gn < total_tiles && !zero) issue(gn, sm + ((i + 1) & 1) * TS);
+        double2 *b = D::SINGLE ? sm : sm + (i & 1) * TS;
+        if constexpr (D::SINGLE) {
+            if (!zero) issue(g, sm);
+        } else {
+            if (gn < total_tiles && !zero) issue(gn, sm + ((i + 1) & 1) * TS);
+        }
         cp_async_commit();
         const int circ = (int)(g >> tiles_log2);
         if (circ != cur_circ) {   // (re)stage this circuit's op tables
@@ -1184,7 +1215,8 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
             for (uint32_t k = t; k < nops; k += blockDim.x) stage_table(ops[P.op_begin + k], s_tab, M, cst);
             cur_circ = circ;
         }
-        cp_async_wait1();
+        if constexpr (D::SINGLE) cp_async_wait0();
+        else cp_async_wait1();
         __syncthreads();
 
         const uint64_t tb = D::tbase(g & tmask);

@@ -530,3 +530,26 @@ def test_trotter_diagonal_chain_closed_form_n20(lq):
     with pytest.raises(lq.LQError):
         sv.trotter_xyz(1.0, 1.0, 1.0, 0.0, 1.0, 0.0, -0.1, 3)
     sv.free()
+
+
+def test_max_size_n33_monomial_qft_closed_form(lq):
+    """Largest single-GPU state (n = 33, 128 GiB): a 400-gate monomial
+    circuit from a basis state, then the full QFT (3 tile passes of 12 bits,
+    bit reversal as a relabel); 2^18 sampled amplitudes against the closed
+    form e^{i phi} N^-1/2 e^{2 pi i j k' / N} (SURVEY c.4 (i)); norm."""
+    import torch
+    from closed_forms import monomial_forward, qft_of_basis
+    n = 33
+    torch.cuda.empty_cache()
+    rng = np.random.default_rng(3333)
+    gates = W.monomial_circuit(n, 400, rng)
+    k = int(rng.integers(0, 1 << n))
+    kp, ph = monomial_forward(n, gates, k)
+    sv = lq.StateVector(n)
+    sv.init_basis(k).apply(gates).qft()
+    idx = np.unique(rng.integers(0, 1 << n, size=1 << 18, dtype=np.uint64))
+    assert np.abs(sv.gather(idx) - ph * qft_of_basis(n, kp, idx)).max() <= 1e-12
+    assert abs(sv.norm2() - 1.0) <= 1e-11
+    sv.free()
+    del sv
+    torch.cuda.empty_cache()

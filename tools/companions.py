@@ -38,9 +38,10 @@ lq.lq_set_option(lq.LQ_OPT_FUSION, 0)
 for b in (0, 15, 29):
     q = n - 1 - b
     row(f"k_pair H on bit {b}", 32, timed(lambda: sv.apply([("H", q, -1, -1, 0.0)])), "unfused 1q pair pass")
-row("k_pair CNOT bits (29,0)", 32, timed(lambda: sv.apply([("CNOT", 0, n - 1, -1, 0.0)])))
-row("k_diag RZ x8 fused", 32, timed(lambda: sv.apply([("RZ", q, -1, -1, 0.1 * q) for q in range(8)] )),
-    "unfused mode runs each diagonal op as its own k_diag pass: 8 passes")
+row("k_pair CNOT bits (29,0)", 16, timed(lambda: sv.apply([("CNOT", 0, n - 1, -1, 0.0)])),
+    "controlled permutation: only the controlled half moves (16 B/amp averaged over the state)")
+row("k_diag RZ x8 (8 unfused diagonal passes)", 8 * 32, timed(lambda: sv.apply([("RZ", q, -1, -1, 0.1 * q) for q in range(8)] )),
+    "unfused mode runs each diagonal op as its own k_diag pass")
 lq.lq_set_option(lq.LQ_OPT_FUSION, 1)
 # one fused diagonal pass: many diagonal gates
 dg = [("RZ", q, -1, -1, 0.1 * q) for q in range(n)] + [("CZ", q, q + 1, -1, 0.0) for q in range(n - 1)]
