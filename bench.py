@@ -270,9 +270,11 @@ def run_ours(args):
     achieved = alg_bytes / (tile_ms / 1e3) / 1e9 if tile_ms > 0 else None
     tr = ncu_traffic()
     traffic = None
-    if tr and tr.get("n_qubits") == n:
-        traffic = tr["dram_bytes_per_launch"]
     alg_per_launch = alg_bytes / max(tile_cnt, 1)
+    if tr and tr.get("n_qubits") == n:
+        # the capture's DRAM bytes per launch, rescaled by the ratio of
+        # algorithmic bytes per launch (the capture may batch differently)
+        traffic = tr["dram_bytes_per_launch"] * alg_per_launch / tr["algorithmic_bytes_per_launch"]
     roof = {"kernel": "k_tile (fused tile pass)", "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "algorithmic_bytes_per_launch": alg_per_launch, "launches": int(tile_cnt),

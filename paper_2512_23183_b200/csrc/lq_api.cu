@@ -1638,11 +1638,14 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     }
     const int n_circ = (int)P->shifts.size();
     const uint64_t N = 1ull << n_qubits;
-    // batch: >= 2^25 amplitudes per launch when possible, <= 4 GiB of states
-    uint64_t B = std::max<uint64_t>(1, (1ull << 25) / N);
+    // batch: >= 2^26 amplitudes per launch when possible (config 4: 4 circuits,
+    // 3.022 s vs 3.043 s with 2), <= 4 GiB of states
+    uint64_t B = std::max<uint64_t>(1, (1ull << 26) / N);
     B = std::min<uint64_t>(B, std::max<uint64_t>(1, (1ull << 28) / N));
     B = std::min<uint64_t>(B, std::max(1, n_circ));
     B = std::min<uint64_t>(B, 65535);
+    if (const char *be = getenv("LQ_PSR_BATCH"))   // tuning experiments
+        B = std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)atoi(be), std::max(1, n_circ)));
     P->B = (int)B;
     cudaStream_t st = P->stream;
     Blob blob;

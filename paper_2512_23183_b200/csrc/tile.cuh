@@ -1147,7 +1147,9 @@ __device__ __forceinline__ void run_subs_c(double2 (&a)[1 << RR], double2 *b, TS
                 xread_c<RR, D, D::SM[S], D::PERM[S], false>(b, a, t, tb, gofs);
             } else {
                 materialize<RR>(a, ts, false);
-                __syncthreads();   // everyone has read the previous mapping's slots
+                // everyone has read the previous mapping's slots -- needed only
+                // if this thread's writes can reach slots another thread reads
+                if constexpr (!D::WSAFE[S - 1]) __syncthreads();
                 xwrite_c<RR, D, D::SM[S - 1]>(b, a, t, ts.fb);
                 ts.fb = 0;
                 __syncthreads();
@@ -1240,7 +1242,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         bool ex = need_x;
         if constexpr (!need_x) ex = __syncthreads_or(ts.fb != 0);
         if (ex) {
-            if constexpr (need_x) __syncthreads();
+            if constexpr (need_x && !D::WSAFE[LAST]) __syncthreads();
             xwrite_c<RR, D, D::SM[LAST]>(b, a, t, ts.fb);
             __syncthreads();
             xread_c<RR, D, D::SSTORE, D::STORE_PERM, false>(b, a, t, tb, P.gofs);

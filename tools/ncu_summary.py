@@ -21,7 +21,7 @@ from paper_2512_23183_b200 import lq
 w = W.config4()
 plan = lq.lq_plan_export_json(w.n, w.gates, w.terms)
 N = 1 << w.n
-B = 2
+B = int(os.environ.get("LQ_SUMMARY_B", "4"))   # circuits per launch in the capture (lq_psr_create's batch)
 passes = plan["passes"]
 launches = []
 for i, r in enumerate(data):
@@ -40,6 +40,7 @@ for i, r in enumerate(data):
 tot_dram = sum(l["dram_read"] + l["dram_write"] for l in launches)
 tot_alg = sum(l["alg_bytes"] for l in launches)
 s = {"source": src, "n_qubits": w.n, "circuits_per_launch": B, "launches": len(launches),
+     "dram_bytes_per_circuit_pass": tot_dram / len(launches) / B,
      "dram_bytes_per_launch": tot_dram / len(launches), "algorithmic_bytes_per_launch": tot_alg / len(launches),
      "traffic_over_algorithmic": tot_dram / tot_alg, "per_launch": launches}
 json.dump(s, open(out, "w"), indent=1)
