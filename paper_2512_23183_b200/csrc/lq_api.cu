@@ -1604,6 +1604,7 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
         po.first_budget = fb ? atoi(fb) : 0;
     }
     plan_circuit(n_qubits, ops, po, P->mb, P->plan);
+    P->plan.zero_first = true;   // lq_psr_run launches the first pass with PF_LOAD_ZERO
     {
         lq_status js = prepare(P->plan, true);
         if (js != LQ_OK) {

@@ -70,6 +70,7 @@ struct Plan {
     std::vector<const void *> jit;    // per pass: JIT-compiled tile kernel (cudaKernel_t) or nullptr (jit.h)
     bool prepared = false;            // jit resolved (prepare() in lq_api.cu)
     bool single_buf = false;          // JIT passes use one tile buffer, two CTAs per SM (tile.cuh D::SINGLE)
+    bool zero_first = false;          // the first pass synthesises |0...0> (PSR plans: PF_LOAD_ZERO)
 };
 
 struct MatBuilder {

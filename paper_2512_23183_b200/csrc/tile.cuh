@@ -1097,39 +1097,69 @@ __device__ __forceinline__ uint32_t ins_zeros(uint32_t t) {   // thread -> local
         if ((SMm >> b) & 1) t = ((t >> b) << (b + 1)) | (t & ((1u << b) - 1u));
     return t;
 }
-// registers -> shared slots of mapping SMm (pending flips folded into the address)
-template <int RR, class D, uint32_t SMm>
+// The dynamic shared memory base (both tile buffers, then the tables).  The
+// swizzled accesses below index it with (base | boff) ^ offset, boff = the
+// buffer's element offset (0 or 2^K, above every slot bit), so a slot costs
+// one XOR and one LEA with the buffer choice folded into the per-exchange base.
+__device__ __forceinline__ double2 *dyn_smem() {
+    extern __shared__ double2 lq_dyn_smem[];
+    return lq_dyn_smem;
+}
+
+// registers -> shared slots of mapping SMm (pending flips folded into the address).
+// ADD: identity layout (an additive epoch, jit.cpp): slot = the thread's base
+// plus a compile-time register offset, so each store is [base + immediate].
+template <int RR, class D, uint32_t SMm, bool ADD = false>
 __device__ __forceinline__ void xwrite_c(double2 *b, const double2 (&a)[1 << RR], uint32_t t, uint32_t fb) {
+    if constexpr (ADD) {
+        double2 *p = b + ins_zeros<SMm, D::K>(t);
+        if (fb == 0) {
+            Unroll<RR>::run([&](auto V) { p[loff_c<SMm>(decltype(V)::value)] = a[decltype(V)::value]; });
+        } else {
+            const uint32_t adj = loff_c<SMm>(fb);   // register v holds logical v ^ fb
+            Unroll<RR>::run([&](auto V) { p[loff_c<SMm>(decltype(V)::value) ^ adj] = a[decltype(V)::value]; });
+        }
+        return;
+    }
     const uint32_t slt = D::swz(ins_zeros<SMm, D::K>(t));
     uint32_t adj = 0;
 #pragma unroll
     for (int i = 0; i < RR; i++)
         if ((fb >> i) & 1) adj ^= D::swz(1u << nth_set_bit(SMm, i));
-    const uint32_t base = slt ^ adj;
+    double2 *const s0 = dyn_smem();
+    const uint32_t base = (slt ^ adj) | (uint32_t)(b - s0);
     Unroll<RR>::run([&](auto V) {
         constexpr uint32_t so = D::swz(loff_c<SMm>(decltype(V)::value));
-        b[base ^ so] = a[decltype(V)::value];
+        s0[base ^ so] = a[decltype(V)::value];
     });
 }
 // shared slots -> registers of mapping SMm, through entry permutation PI
 // (ZERO: synthesise |0...0> -- amplitude 1 at position 0 of tile 0)
-template <int RR, class D, uint32_t SMm, int PI, bool ZERO>
+template <int RR, class D, uint32_t SMm, int PI, bool ZERO, bool ADD = false>
 __device__ __forceinline__ void xread_c(const double2 *b, double2 (&a)[1 << RR], uint32_t t, uint64_t tb,
                                         uint64_t gofs) {
     const uint32_t lt = ins_zeros<SMm, D::K>(t);
+    if constexpr (ADD && !ZERO) {   // identity layout, no permutation (an additive epoch)
+        static_assert(PI < 0, "additive epochs read through no permutation");
+        const double2 *p = b + lt;
+        Unroll<RR>::run([&](auto V) { a[decltype(V)::value] = p[loff_c<SMm>(decltype(V)::value)]; });
+        return;
+    }
+    const double2 *const s0 = dyn_smem();
+    const uint32_t boff = (uint32_t)(b - s0);
     if constexpr (PI < 0) {
         const uint32_t base = D::swz(lt);
         Unroll<RR>::run([&](auto V) {
             constexpr uint32_t so = D::swz(loff_c<SMm>(decltype(V)::value));
             if constexpr (ZERO) a[decltype(V)::value] = make_double2(((tb | gofs) == 0 && (base ^ so) == 0) ? 1.0 : 0.0, 0.0);
-            else a[decltype(V)::value] = b[base ^ so];
+            else a[decltype(V)::value] = s0[(base | boff) ^ so];
         });
     } else {
         const uint32_t base = D::swz(D::template ainv<PI>(lt) ^ D::template binv<PI>(tb | gofs));
         Unroll<RR>::run([&](auto V) {
             constexpr uint32_t so = D::swz(D::template ainv<PI>(loff_c<SMm>(decltype(V)::value)));
             if constexpr (ZERO) a[decltype(V)::value] = make_double2(((tb | gofs) == 0 && (base ^ so) == 0) ? 1.0 : 0.0, 0.0);
-            else a[decltype(V)::value] = b[base ^ so];
+            else a[decltype(V)::value] = s0[(base | boff) ^ so];
         });
     }
 }
@@ -1143,17 +1173,17 @@ __device__ __forceinline__ void run_subs_c(double2 (&a)[1 << RR], double2 *b, TS
             // Pauli groups since it was filled), so the new mapping reads it
             // directly -- no write-back, no barrier -- unless the pass never
             // loaded it (PF_LOAD_ZERO).
-            if (D::RO[S - 1] && !zero) {
-                xread_c<RR, D, D::SM[S], D::PERM[S], false>(b, a, t, tb, gofs);
+            if constexpr (D::RO[S - 1]) {
+                xread_c<RR, D, D::SM[S], D::PERM[S], false, D::RADD[S]>(b, a, t, tb, gofs);
             } else {
                 materialize<RR>(a, ts, false);
                 // everyone has read the previous mapping's slots -- needed only
                 // if this thread's writes can reach slots another thread reads
                 if constexpr (!D::WSAFE[S - 1]) __syncthreads();
-                xwrite_c<RR, D, D::SM[S - 1]>(b, a, t, ts.fb);
+                xwrite_c<RR, D, D::SM[S - 1], D::WADD[S - 1]>(b, a, t, ts.fb);
                 ts.fb = 0;
                 __syncthreads();
-                xread_c<RR, D, D::SM[S], D::PERM[S], false>(b, a, t, tb, gofs);
+                xread_c<RR, D, D::SM[S], D::PERM[S], false, D::RADD[S]>(b, a, t, tb, gofs);
             }
         }
         const uint64_t gbase = tb | gofs | D::dep(ins_zeros<D::SM[S], D::K>(t));
@@ -1192,7 +1222,8 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         Unroll<RR>::run([&](auto V) {
             constexpr uint32_t l = (uint32_t)decltype(V)::value * NT;
             constexpr uint64_t o = D::dep(l);
-            cp_async16(buf + (sw_t ^ D::swz(l)), psi + o);
+            if constexpr (D::ADD_F) cp_async16(buf + t + l, psi + o);
+            else cp_async16(buf + (sw_t ^ D::swz(l)), psi + o);
         });
     };
     uint32_t g = blockIdx.x;
@@ -1224,7 +1255,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         const uint64_t tb = D::tbase(g & tmask);
         double2 a[NV];
         if (zero) xread_c<RR, D, D::SM[0], D::PERM[0], true>(b, a, t, tb, P.gofs);
-        else xread_c<RR, D, D::SM[0], D::PERM[0], false>(b, a, t, tb, P.gofs);
+        else xread_c<RR, D, D::SM[0], D::PERM[0], false, D::RADD[0]>(b, a, t, tb, P.gofs);
         TState ts;
         ts.reset();
         ts.lpos = P.lpos;
@@ -1243,9 +1274,9 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         if constexpr (!need_x) ex = __syncthreads_or(ts.fb != 0);
         if (ex) {
             if constexpr (need_x && !D::WSAFE[LAST]) __syncthreads();
-            xwrite_c<RR, D, D::SM[LAST]>(b, a, t, ts.fb);
+            xwrite_c<RR, D, D::SM[LAST], D::ADD_S>(b, a, t, ts.fb);
             __syncthreads();
-            xread_c<RR, D, D::SSTORE, D::STORE_PERM, false>(b, a, t, tb, P.gofs);
+            xread_c<RR, D, D::SSTORE, D::STORE_PERM, false, D::ADD_S>(b, a, t, tb, P.gofs);
         }
         const uint64_t gst = tb | D::dep(ins_zeros<D::SSTORE, K>(t));
         Unroll<RR>::run([&](auto V) {

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$? >> gpurun_out/gpu_tests.log
+tail -4 gpurun_out/gpu_tests.log
+KS=11 timeout 600 python tools/sb_probe.py cfg4 qft 2>&1 | grep -E "SB|rror"
+LQ_JIT_NO_ADDITIVE=1 KS=11 timeout 600 python tools/sb_probe.py cfg4 qft 2>&1 | grep -E "SB|rror" | sed 's/^/noadd /'
+timeout 600 python tools/host_probe.py 2>&1 | grep expval
