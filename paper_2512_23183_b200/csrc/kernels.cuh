@@ -298,26 +298,54 @@ __device__ __forceinline__ uint64_t insert_bit64(uint64_t x, int b, uint64_t v) 
 }
 
 // both shards in this process (group mode): swap element-wise in place
+// All three move U elements per thread per iteration, loads first (HBM
+// latency hiding; the same pattern as k_pair).
+constexpr int MOVE_U = 4;
 __global__ void __launch_bounds__(256) k_swap_halves(double2 *__restrict__ a, double2 *__restrict__ b, int l,
                                                      int va, int vb, uint64_t half) {
-    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < half; i += (uint64_t)gridDim.x * 256) {
-        const uint64_t pa = insert_bit64(i, l, (uint64_t)va), pb = insert_bit64(i, l, (uint64_t)vb);
-        const double2 x = a[pa];
-        a[pa] = b[pb];
-        b[pb] = x;
+    const uint64_t stride = (uint64_t)gridDim.x * 256;
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < half; i += MOVE_U * stride) {
+        uint64_t pa[MOVE_U], pb[MOVE_U];
+        double2 x[MOVE_U], y[MOVE_U];
+#pragma unroll
+        for (int u = 0; u < MOVE_U; u++) {
+            const uint64_t j = i + u * stride;
+            pa[u] = insert_bit64(j, l, (uint64_t)va);
+            pb[u] = insert_bit64(j, l, (uint64_t)vb);
+            if (j < half) { x[u] = a[pa[u]]; y[u] = b[pb[u]]; }
+        }
+#pragma unroll
+        for (int u = 0; u < MOVE_U; u++)
+            if (i + u * stride < half) { a[pa[u]] = y[u]; b[pb[u]] = x[u]; }
     }
 }
 
 // NCCL mode: chunk [off, off + cnt) of the outgoing half -> contiguous staging, and back
 __global__ void __launch_bounds__(256) k_pack_half(const double2 *__restrict__ src, double2 *__restrict__ dst, int l,
                                                    int v, uint64_t off, uint64_t cnt) {
-    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * 256)
-        dst[i] = src[insert_bit64(off + i, l, (uint64_t)v)];
+    const uint64_t stride = (uint64_t)gridDim.x * 256;
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < cnt; i += MOVE_U * stride) {
+        double2 x[MOVE_U];
+#pragma unroll
+        for (int u = 0; u < MOVE_U; u++)
+            if (i + u * stride < cnt) x[u] = src[insert_bit64(off + i + u * stride, l, (uint64_t)v)];
+#pragma unroll
+        for (int u = 0; u < MOVE_U; u++)
+            if (i + u * stride < cnt) dst[i + u * stride] = x[u];
+    }
 }
 __global__ void __launch_bounds__(256) k_unpack_half(double2 *__restrict__ dst, const double2 *__restrict__ src, int l,
                                                      int v, uint64_t off, uint64_t cnt) {
-    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * 256)
-        dst[insert_bit64(off + i, l, (uint64_t)v)] = src[i];
+    const uint64_t stride = (uint64_t)gridDim.x * 256;
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < cnt; i += MOVE_U * stride) {
+        double2 x[MOVE_U];
+#pragma unroll
+        for (int u = 0; u < MOVE_U; u++)
+            if (i + u * stride < cnt) x[u] = src[i + u * stride];
+#pragma unroll
+        for (int u = 0; u < MOVE_U; u++)
+            if (i + u * stride < cnt) dst[insert_bit64(off + i + u * stride, l, (uint64_t)v)] = x[u];
+    }
 }
 
 __global__ void __launch_bounds__(256) k_fill_basis(uint64_t N, uint64_t k, double2 *__restrict__ state,

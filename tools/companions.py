@@ -68,4 +68,22 @@ row(f"expval XYZ chain ({len(xyz)} terms, {ne} read-only passes)", 16 * ne + 32 
     f"{len(ep['groups'])} x-mask groups in {ne} read-only tile passes, {nw} wide groups")
 row("expval single Z group (read-only pass)", 16, timed(lambda: sv.expval([(1.0, 0, 1 << (n - 1))])))
 row("init_random (norm pass + write pass)", 16, timed(lambda: sv.init_random(5)), "ALU-heavy: log + sincospi per amp")
+
+# a9: one global-qubit swap in group mode (G = 2 shards in this process, the
+# same swap kernel pair the NCCL path packs/unpacks): H on a global qubit =
+# swap + the gate's pass; H on a local qubit = the pass alone.
+sv.free(); del sv; torch.cuda.empty_cache()
+sh = lq.ShardedState(n, group_world=2, stream=st)
+sh.init_random(2)
+def glob_q():   # the qubit currently on the global (rank) bit: the scheduler moves it after each swap
+    qm = sh.qubit_map()
+    return max(range(n), key=lambda q: qm[q])
+def loc_q():
+    qm = sh.qubit_map()
+    return min(range(n), key=lambda q: qm[q])
+t_loc = timed(lambda: sh.apply([("H", loc_q(), -1, -1, 0.0)]))
+t_glob = timed(lambda: sh.apply([("H", glob_q(), -1, -1, 0.0)]))
+row("sharded G=2: H on a local qubit (one pass)", 32, t_loc)
+row("sharded G=2: global-local swap (H on the global qubit minus H on a local one)", 32, t_glob - t_loc,
+    "k_swap_halves: each shard exchanges half its amplitudes in place (16 B read + 16 B write per amplitude of the state)")
 print("JSON " + json.dumps(out))
