@@ -19,8 +19,10 @@ namespace lq {
 
 // Compile (or fetch from the cache) one kernel per TILE pass of `plan`;
 // kernels[i] is the cudaKernel_t (as const void*) for plan.passes[i], or
-// nullptr for non-tile passes.  Returns false and fills `err` on failure.
-bool jit_plan(const Plan &plan, std::vector<const void *> &kernels, std::string &err);
+// nullptr for non-tile passes; ctabs[i] the device address of the pass's
+// __constant__ op-table bank (plan.ctab) or nullptr.  Returns false and
+// fills `err` on failure.
+bool jit_plan(const Plan &plan, std::vector<const void *> &kernels, std::vector<void *> &ctabs, std::string &err);
 
 // Generated CUDA source of one tile pass (exposed for lq_plan_export_json /
 // debugging).

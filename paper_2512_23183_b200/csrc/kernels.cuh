@@ -452,6 +452,20 @@ __global__ void __launch_bounds__(256) k_pauli_direct(int n, uint64_t gofs, uint
     if (threadIdx.x == 0) partial[(uint64_t)blockIdx.y * slot_stride + slot + blockIdx.x] = r;
 }
 
+// ---------------------------------------------------------------- constant op tables
+// Stage every JIT pass's op tables for circuits 0..n_circ-1 of a launch into
+// `out` (layout: CtabDesc); the host then copies each pass's slice into the
+// pass module's __constant__ bank.  grid (n_pass, n_circ).
+__global__ void k_stage_ctab(const KOp *__restrict__ kops, const CtabDesc *__restrict__ desc,
+                             const double2 *__restrict__ mats, uint64_t mat_stride, const double2 *__restrict__ cst,
+                             double2 *__restrict__ out) {
+    const CtabDesc D = desc[blockIdx.x];
+    const uint32_t c = blockIdx.y;
+    double2 *o = out + D.out + (uint64_t)c * D.smat;
+    const double2 *M = mats ? mats + (uint64_t)c * mat_stride : nullptr;
+    for (uint32_t k = D.op_begin + threadIdx.x; k < D.op_end; k += blockDim.x) stage_table(kops[k], o, M, cst);
+}
+
 // ---------------------------------------------------------------- PSR combine (a8)
 // g_p = sum_k w_k E(theta + s_k e_p).  Rotations exp(-i theta G / 2) with
 // G^2 = 1 take the paper's two-term rule, s = +-pi/2, w = +-1/2

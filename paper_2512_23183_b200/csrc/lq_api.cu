@@ -151,10 +151,20 @@ lq_status prepare(Plan &plan, bool reused = false) {
         const char *sb = getenv("LQ_SINGLEBUF");   // experiments: one tile buffer, two CTAs per SM
         plan.single_buf = sb && atoi(sb) != 0;
     }
+    plan.ctab = getenv("LQ_JIT_NO_CTAB") == nullptr;   // constant-bank op tables (A/B switch for experiments)
     std::string err;
-    if (!jit_plan(plan, plan.jit, err)) {
+    if (!jit_plan(plan, plan.jit, plan.jit_ctab, err)) {
         plan.jit.clear();
+        plan.jit_ctab.clear();
         return fail(LQ_ERR_CUDA, err);
+    }
+    plan.ctab_desc.clear();
+    plan.ctab_total = 0;
+    for (size_t i = 0; i < plan.passes.size(); i++) {
+        if (!plan.jit_ctab[i]) continue;
+        const KPass &kp = plan.passes[i].kp;
+        plan.ctab_desc.push_back({kp.op_begin, kp.op_end, kp.smat, plan.ctab_total});
+        plan.ctab_total += kp.smat * (uint32_t)plan.ctab_circ;
     }
     return LQ_OK;
 }
@@ -409,6 +419,8 @@ unsigned grid_for(uint64_t work, unsigned per_block = 256) {
 }
 
 struct DevPlan {
+    const CtabDesc *ctab_desc = nullptr;   // plan.ctab_desc on the device
+    double2 *ctab_stage = nullptr;         // >= plan.ctab_total double2 of staging
     const KSub *subs = nullptr;
     const KOp *kops = nullptr;
     const KPerm *perms = nullptr;
@@ -429,9 +441,22 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
         k_fill_basis<<<grid, 256, 0, st>>>(1ull << n, 0, state, state_stride);
         LQ_TRY(check_launch("k_fill_basis"));
     }
+    if (!plan.ctab_desc.empty()) {   // constant op tables of this launch's circuits
+        if (!dp.ctab_desc || !dp.ctab_stage || n_circ > plan.ctab_circ)
+            return fail(LQ_ERR_STATE, "constant op tables without staging (internal)");
+        k_stage_ctab<<<dim3((unsigned)plan.ctab_desc.size(), (unsigned)n_circ), 128, 0, st>>>(
+            dp.kops, dp.ctab_desc, mats, mat_stride, dp.cst, dp.ctab_stage);
+        LQ_TRY(check_launch("k_stage_ctab"));
+    }
+    size_t ci = 0;
     for (size_t i = 0; i < plan.passes.size(); i++) {
         const PlanPass &p = plan.passes[i];
         if (p.kind == PASS_TILE) {
+            if (i < plan.jit_ctab.size() && plan.jit_ctab[i]) {
+                const CtabDesc &D = plan.ctab_desc[ci++];
+                CUDA_TRY(cudaMemcpyAsync(plan.jit_ctab[i], dp.ctab_stage + D.out,
+                                         (size_t)n_circ * D.smat * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+            }
             KPass kp = p.kp;
             kp.gofs = gofs;
             if (zero_first && i == 0) kp.flags |= PF_LOAD_ZERO;
@@ -556,7 +581,7 @@ struct lq_sv {
     int rank0 = 0;                   // rank of shards[0]
     std::vector<double2 *> shards;   // this process's shards (group mode: all G)
     uint32_t xmask = 0;              // rank relabel: rank r holds physical global bits r ^ xmask
-    DevBuf mats_buf, part_buf, stage_buf;
+    DevBuf mats_buf, part_buf, stage_buf, ctab_buf;
     void reset_map() {
         for (int q = 0; q < n; q++) qmap[q] = n - 1 - q;
         xmask = 0;
@@ -579,8 +604,14 @@ lq_status run_single(lq_sv *sv, Plan &plan, const MatBuilder &mb, const double *
            o_fac = blob.add(mb.factors), o_cst = blob.add(mb.cst), o_perm = blob.add(plan.perms),
            o_pt = blob.add(plan.perm_terms);
     size_t o_th = blob.add(theta, theta ? n_theta * sizeof(double) : 0);
+    size_t o_cd = blob.add(plan.ctab_desc);
     LQ_TRY(blob.upload(sv->plan_buf, sv->stream));
     DevPlan dp;
+    if (plan.ctab_total) {
+        LQ_TRY(sv->ctab_buf.reserve((size_t)plan.ctab_total * sizeof(double2), sv->stream));
+        dp.ctab_desc = sv->plan_buf.at<CtabDesc>(o_cd);
+        dp.ctab_stage = sv->ctab_buf.at<double2>(0);
+    }
     dp.subs = sv->plan_buf.at<KSub>(o_sub);
     dp.kops = sv->plan_buf.at<KOp>(o_kop);
     dp.specs = sv->plan_buf.at<MSpec>(o_spec);
@@ -734,16 +765,20 @@ lq_status sh_run(lq_sv *sv, Schedule &sc, const double *theta, size_t n_theta, d
     for (auto &stp : sc.steps)
         if (stp.kind == 0) LQ_TRY(prepare(stp.plan));
     Blob blob;
-    struct Off { size_t sub, kop, perm, pt, et, dt; };
+    struct Off { size_t sub, kop, perm, pt, et, dt, cd; };
     std::vector<Off> offs(sc.steps.size());
     std::vector<DirectSet> dsets(sc.steps.size());
+    uint32_t ctab_max = 0;
     for (size_t i = 0; i < sc.steps.size(); i++) {
         const DStep &stp = sc.steps[i];
         if (stp.kind != 0) continue;
         dsets[i].build(stp.plan);
         offs[i] = {blob.add(stp.plan.subs), blob.add(stp.plan.kops), blob.add(stp.plan.perms),
-                   blob.add(stp.plan.perm_terms), blob.add(stp.plan.eterms), blob.add(dsets[i].terms)};
+                   blob.add(stp.plan.perm_terms), blob.add(stp.plan.eterms), blob.add(dsets[i].terms),
+                   blob.add(stp.plan.ctab_desc)};
+        ctab_max = std::max(ctab_max, stp.plan.ctab_total);
     }
+    if (ctab_max) LQ_TRY(sv->ctab_buf.reserve((size_t)ctab_max * sizeof(double2), st));
     size_t o_spec = blob.add(sc.mb.specs), o_fac = blob.add(sc.mb.factors), o_cst = blob.add(sc.mb.cst);
     size_t o_th = blob.add(theta, theta ? n_theta * sizeof(double) : 0);
     LQ_TRY(blob.upload(sv->plan_buf, st));
@@ -766,6 +801,10 @@ lq_status sh_run(lq_sv *sv, Schedule &sc, const double *theta, size_t n_theta, d
             continue;
         }
         DevPlan dp;
+        if (stp.plan.ctab_total) {
+            dp.ctab_desc = sv->plan_buf.at<CtabDesc>(offs[i].cd);
+            dp.ctab_stage = sv->ctab_buf.at<double2>(0);
+        }
         dp.subs = sv->plan_buf.at<KSub>(offs[i].sub);
         dp.kops = sv->plan_buf.at<KOp>(offs[i].kop);
         dp.perms = sv->plan_buf.at<KPerm>(offs[i].perm);
@@ -1126,6 +1165,7 @@ lq_status lq_sv_free(lq_sv *sv) {
     sv->mats_buf.release(sv->stream);
     sv->part_buf.release(sv->stream);
     sv->stage_buf.release(sv->stream);
+    sv->ctab_buf.release(sv->stream);
     cudaError_t e = cudaSuccess;
     if (!sv->shards.empty()) {
         cudaStreamSynchronize(sv->stream);
@@ -1426,9 +1466,15 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
     dset.build(plan);
     Blob blob;
     size_t o_sub = blob.add(plan.subs), o_kop = blob.add(plan.kops), o_perm = blob.add(plan.perms),
-           o_pt = blob.add(plan.perm_terms), o_et = blob.add(plan.eterms), o_dt = blob.add(dset.terms);
+           o_pt = blob.add(plan.perm_terms), o_et = blob.add(plan.eterms), o_dt = blob.add(dset.terms),
+           o_cd = blob.add(plan.ctab_desc);
     LQ_TRY(blob.upload(sv->plan_buf, sv->stream));
     DevPlan dp;
+    if (plan.ctab_total) {
+        LQ_TRY(sv->ctab_buf.reserve((size_t)plan.ctab_total * sizeof(double2), sv->stream));
+        dp.ctab_desc = sv->plan_buf.at<CtabDesc>(o_cd);
+        dp.ctab_stage = sv->ctab_buf.at<double2>(0);
+    }
     dp.subs = sv->plan_buf.at<KSub>(o_sub);
     dp.kops = sv->plan_buf.at<KOp>(o_kop);
     dp.perms = sv->plan_buf.at<KPerm>(o_perm);
@@ -1561,7 +1607,7 @@ struct lq_psr {
     std::vector<PsrRule> pairs;
     int base_idx = -1;
     int B = 1;
-    DevBuf blob_buf, states, mats, partials, E;
+    DevBuf blob_buf, states, mats, partials, E, ctab;
     DevPlan dp;
     const Shift *d_shifts = nullptr;
     const PsrRule *d_pairs = nullptr;
@@ -1605,13 +1651,6 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     }
     plan_circuit(n_qubits, ops, po, P->mb, P->plan);
     P->plan.zero_first = true;   // lq_psr_run launches the first pass with PF_LOAD_ZERO
-    {
-        lq_status js = prepare(P->plan, true);
-        if (js != LQ_OK) {
-            delete P;
-            return js;
-        }
-    }
     P->dset.build(P->plan);
     // circuits of this shard: (p, +pi/2), (p, -pi/2) for owned p; base on shard 0.
     // Parameters used by no gate have E+ == E- identically: g_p = 0 (written by combine).
@@ -1648,23 +1687,37 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     if (const char *be = getenv("LQ_PSR_BATCH"))   // tuning experiments
         B = std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)atoi(be), std::max(1, n_circ)));
     P->B = (int)B;
+    P->plan.ctab_circ = (int)B;   // constant op-table banks hold one launch's circuits
+    {
+        lq_status js = prepare(P->plan, true);
+        if (js != LQ_OK) {
+            delete P;
+            return js;
+        }
+    }
     cudaStream_t st = P->stream;
     Blob blob;
     size_t o_sub = blob.add(P->plan.subs), o_kop = blob.add(P->plan.kops), o_spec = blob.add(P->mb.specs),
            o_fac = blob.add(P->mb.factors), o_cst = blob.add(P->mb.cst), o_perm = blob.add(P->plan.perms),
            o_pt = blob.add(P->plan.perm_terms), o_sh = blob.add(P->shifts),
-           o_pr = blob.add(P->pairs), o_t = blob.add(P->dset.terms), o_et = blob.add(P->plan.eterms);
+           o_pr = blob.add(P->pairs), o_t = blob.add(P->dset.terms), o_et = blob.add(P->plan.eterms),
+           o_cd = blob.add(P->plan.ctab_desc);
     P->blob_bytes = blob.h.size();
     lq_status s = blob.upload(P->blob_buf, st);
     if (s == LQ_OK) s = P->states.reserve((size_t)B * N * sizeof(double2), st);
     if (s == LQ_OK) s = P->mats.reserve((size_t)B * std::max<uint32_t>(P->mb.mat_size, 1) * sizeof(double2), st);
     if (s == LQ_OK) s = P->partials.reserve((size_t)B * P->dset.stride() * sizeof(double), st);
     if (s == LQ_OK) s = P->E.reserve(sizeof(double) * std::max(n_circ, 1), st);
+    if (s == LQ_OK && P->plan.ctab_total) s = P->ctab.reserve((size_t)P->plan.ctab_total * sizeof(double2), st);
     if (s != LQ_OK) {
         std::string keep = g_err;
         lq_psr_free(P);
         g_err = keep;
         return s;
+    }
+    if (P->plan.ctab_total) {
+        P->dp.ctab_desc = P->blob_buf.at<CtabDesc>(o_cd);
+        P->dp.ctab_stage = P->ctab.at<double2>(0);
     }
     P->dp.subs = P->blob_buf.at<KSub>(o_sub);
     P->dp.kops = P->blob_buf.at<KOp>(o_kop);
@@ -1822,6 +1875,7 @@ lq_status lq_psr_free(lq_psr *P) {
     P->mats.release(P->stream);
     P->partials.release(P->stream);
     P->E.release(P->stream);
+    P->ctab.release(P->stream);
     delete P;
     return LQ_OK;
 }
@@ -1956,6 +2010,8 @@ lq_status lq_jit_compile_check(int n_qubits, const lq_gate *gates, size_t n_gate
     lower_gates(n_qubits, gates, n_gates, qm, ops, mb);
     if (n_terms) lower_pauli(n_qubits, qm, terms, n_terms, ops, plan);
     plan_circuit(n_qubits, ops, options(), mb, plan);
+    plan.ctab = getenv("LQ_JIT_NO_CTAB") == nullptr;   // as prepare() would
+    plan.ctab_circ = 4;
     size_t nk = 0;
     std::string err;
     if (!jit_check(plan, &nk, err)) return fail(LQ_ERR_CUDA, err);
@@ -1972,6 +2028,7 @@ lq_status lq_qft_jit_compile_check(int n_qubits, int inverse, uint64_t *n_kernel
     MatBuilder mb;
     Plan plan;
     if (!plan_qft(n_qubits, qm, inverse != 0, options(), plan, mb)) return fail(LQ_ERR_STATE, "qft planning failed");
+    plan.ctab = getenv("LQ_JIT_NO_CTAB") == nullptr;
     size_t nk = 0;
     std::string err;
     if (!jit_check(plan, &nk, err)) return fail(LQ_ERR_CUDA, err);

@@ -215,6 +215,15 @@ struct KPass {
     uint8_t lpos[64];    // QFT stages (QF_GENERAL): logical bit held by physical bit p (255: none)
 };
 
+// Constant-bank op tables (JIT passes): pass p's staged
+// tables for circuit c live at out + c * smat in the staging buffer and are
+// copied to the pass module's __constant__ lqj_ctab before its launch.
+struct CtabDesc {
+    uint32_t op_begin, op_end;   // the pass's ops (global kop indices)
+    uint32_t smat;               // staged table size of one circuit (double2)
+    uint32_t out;                // offset of circuit 0's tables in the staging buffer (double2)
+};
+
 // Matrix construction (device-side, per circuit): every fused op has a
 // MSpec that multiplies its factor gates (later factors on the left).
 enum MForm : uint8_t { MF_U2x2 = 0, MF_DIAG2 = 1, MF_U4x4 = 2, MF_DIAG4 = 3, MF_G = 4 };

@@ -71,6 +71,11 @@ struct Plan {
     bool prepared = false;            // jit resolved (prepare() in lq_api.cu)
     bool single_buf = false;          // JIT passes use one tile buffer, two CTAs per SM (tile.cuh D::SINGLE)
     bool zero_first = false;          // the first pass synthesises |0...0> (PSR plans: PF_LOAD_ZERO)
+    bool ctab = false;                // JIT passes read op tables from a __constant__ bank (jit.cpp)
+    int ctab_circ = 1;                // circuits per launch the constant tables are sized for
+    std::vector<void *> jit_ctab;     // per pass: device address of its lqj_ctab, or nullptr (smem tables)
+    std::vector<CtabDesc> ctab_desc;  // the passes with jit_ctab, in pass order (staging layout)
+    uint32_t ctab_total = 0;          // staging buffer size (double2) for ctab_circ circuits
 };
 
 struct MatBuilder {

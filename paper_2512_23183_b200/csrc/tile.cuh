@@ -364,6 +364,8 @@ struct TState {
     double2 ttmax;     // QFT twiddle state of the current sub-block
     uint64_t lg;
     const uint8_t *lpos;   // physical -> logical bit map of the pass (QF_GENERAL stages)
+    const double2 *gtab;   // this circuit's matrix block in global memory (JIT, LQ_JIT_GTAB)
+    uint32_t cbase;        // this circuit's offset in the pass's constant op-table bank (JIT, D::CTAB)
     __device__ __forceinline__ void reset() {
         fb = 0;
         hph = false;
@@ -1243,10 +1245,12 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         }
         cp_async_commit();
         const int circ = (int)(g >> tiles_log2);
-        if (circ != cur_circ) {   // (re)stage this circuit's op tables
-            const double2 *M = mats + (uint64_t)circ * mat_stride;
-            for (uint32_t k = t; k < nops; k += blockDim.x) stage_table(ops[P.op_begin + k], s_tab, M, cst);
-            cur_circ = circ;
+        if constexpr (!D::CTAB) {
+            if (circ != cur_circ) {   // (re)stage this circuit's op tables
+                const double2 *M = mats + (uint64_t)circ * mat_stride;
+                for (uint32_t k = t; k < nops; k += blockDim.x) stage_table(ops[P.op_begin + k], s_tab, M, cst);
+                cur_circ = circ;
+            }
         }
         if constexpr (D::SINGLE) cp_async_wait0();
         else cp_async_wait1();
@@ -1259,6 +1263,8 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         TState ts;
         ts.reset();
         ts.lpos = P.lpos;
+        ts.gtab = mats + (uint64_t)circ * mat_stride;
+        ts.cbase = (uint32_t)circ * D::SMAT;
         run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, P.gofs, t, s_tab, s_et, P.n, zero);
         double2 *psi = state + (uint64_t)circ * state_stride;
         if (P.flags & PF_EXPV)     // deterministic partials: one per warp of the tile
