@@ -1235,15 +1235,21 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         cp_async_commit();
     }
     int cur_circ = -1;
+    // LATE (constant op tables, two buffers): the next tile's prefetch is
+    // issued right after the barrier that starts this tile -- every thread has
+    // then finished the previous tile, whose buffer the prefetch refills -- so
+    // no barrier is needed at the end of a tile.
+    constexpr bool LATE = D::CTAB && !D::SINGLE;
     for (uint32_t i = 0; g < total_tiles; i++, g += gridDim.x) {
         const uint32_t gn = g + gridDim.x;
         double2 *b = D::SINGLE ? sm : sm + (i & 1) * TS;
         if constexpr (D::SINGLE) {
             if (!zero) issue(g, sm);
-        } else {
+            cp_async_commit();
+        } else if constexpr (!LATE) {
             if (gn < total_tiles && !zero) issue(gn, sm + ((i + 1) & 1) * TS);
+            cp_async_commit();
         }
-        cp_async_commit();
         const int circ = (int)(g >> tiles_log2);
         if constexpr (!D::CTAB) {
             if (circ != cur_circ) {   // (re)stage this circuit's op tables
@@ -1252,9 +1258,13 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
                 cur_circ = circ;
             }
         }
-        if constexpr (D::SINGLE) cp_async_wait0();
+        if constexpr (D::SINGLE || LATE) cp_async_wait0();
         else cp_async_wait1();
         __syncthreads();
+        if constexpr (LATE) {
+            if (gn < total_tiles && !zero) issue(gn, sm + ((i + 1) & 1) * TS);
+            cp_async_commit();
+        }
 
         const uint64_t tb = D::tbase(g & tmask);
         double2 a[NV];
@@ -1271,7 +1281,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
             expv_partial(ts.eacc, reinterpret_cast<double *>(b), partials + (uint64_t)circ * slot_stride + P.eslot,
                          g & tmask);
         if (P.flags & PF_NO_STORE) {
-            __syncthreads();
+            if constexpr (!LATE) __syncthreads();
             continue;
         }
         materialize<RR>(a, ts, true);
@@ -1289,7 +1299,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
             constexpr uint64_t go = D::dep(loff_c<D::SSTORE>(decltype(V)::value));
             psi[gst + go] = a[decltype(V)::value];
         });
-        __syncthreads();   // buffer b is refilled by the next iteration's prefetch
+        if constexpr (!LATE) __syncthreads();   // buffer b is refilled by the next iteration's prefetch
     }
 }
 

@@ -553,3 +553,46 @@ def test_max_size_n33_monomial_qft_closed_form(lq):
     sv.free()
     del sv
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- degenerate cases
+
+@pytest.mark.parametrize("jit", [0, 2])
+def test_degenerate_sizes_and_empty_inputs(lq, oracle, jit):
+    """n = 1 and n = 2 states through every 1q gate, QFT and expectation;
+    empty gate lists and Pauli sums; a PSR ansatz with no gates (its only
+    pass synthesises |0...0> and reads it, PF_LOAD_ZERO + read-only); an
+    unused parameter (gradient exactly 0) -- interpreter and JIT."""
+    lq.lq_set_option(lq.LQ_OPT_JIT, jit)
+    try:
+        oneq = [("H", 0, -1, -1, 0.0), ("RX", 0, -1, -1, 0.7), ("RY", 0, -1, -1, 1.1), ("RZ", 0, -1, -1, 2.3),
+                ("S", 0, -1, -1, 0.0), ("T", 0, -1, -1, 0.0), ("X", 0, -1, -1, 0.0), ("Y", 0, -1, -1, 0.0),
+                ("Z", 0, -1, -1, 0.0), ("SDG", 0, -1, -1, 0.0), ("TDG", 0, -1, -1, 0.0)]
+        for n in (1, 2):
+            gates = oneq + ([("CNOT", 0, 1, -1, 0.0), ("RYY", 1, 0, -1, 0.4), ("CRY", 1, 0, -1, 0.9)] if n == 2 else [])
+            sv = lq.StateVector(n).init_random(40 + n)
+            ref = oracle.init_random(n, 40 + n)
+            sv.apply(gates).qft()
+            oracle.apply_circuit(ref, gates)
+            oracle.qft(ref)
+            assert np.abs(sv.read() - ref).max() <= AMP_TOL
+            terms = [(0.5, 1, 0), (-0.3, 1, 1), (0.8, 0, 1)] + ([(0.2, 3, 3)] if n == 2 else [])
+            assert abs(sv.expval(terms) - oracle.expval(ref, terms)) <= 1e-12
+            before = sv.read()
+            sv.apply([])
+            np.testing.assert_array_equal(sv.read(), before)
+            assert sv.expval([]) == 0.0
+            sv.free()
+        n = 6
+        terms = W.random_pauli_sum(n, 12, np.random.default_rng(3))
+        g, e = lq.lq_param_shift_grad(n, [], [], terms)
+        psi0 = oracle.init_basis(n, 0)
+        assert g.size == 0 and abs(e - oracle.expval(psi0, terms)) <= 1e-12
+        gates = [("RY", 0, -1, 0, 0.0), ("RX", 3, -1, 2, 0.0), ("CNOT", 0, 5, -1, 0.0)]   # param 1 unused
+        th = np.array([0.3, 1.7, -0.4])
+        g, e = lq.lq_param_shift_grad(n, gates, th, terms)
+        assert g[1] == 0.0
+        go = oracle.param_shift_grad(n, gates, th, terms)
+        grad_close(g, go)
+    finally:
+        lq.lq_set_option(lq.LQ_OPT_JIT, 1)
