@@ -1220,13 +1220,28 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
     const uint32_t sw_t = D::swz(t);
     const uint32_t tmask = (1u << tiles_log2) - 1u;
     auto issue = [&](uint32_t g, double2 *buf) {
-        const double2 *psi = state + (uint64_t)(g >> tiles_log2) * state_stride + D::tbase(g & tmask) + dep_t;
-        Unroll<RR>::run([&](auto V) {
-            constexpr uint32_t l = (uint32_t)decltype(V)::value * NT;
-            constexpr uint64_t o = D::dep(l);
-            if constexpr (D::ADD_F) cp_async16(buf + t + l, psi + o);
-            else cp_async16(buf + (sw_t ^ D::swz(l)), psi + o);
-        });
+        const uint64_t tbg = D::tbase(g & tmask);
+        const double2 *psi = state + (uint64_t)(g >> tiles_log2) * state_stride + tbg + dep_t;
+        if constexpr (D::FILLPI >= 0) {
+            // the first sub-block's entry permutation P applied by the fill:
+            // loaded element m lands in slot swz(A (m ^ binv)), P^-1 l = A^-1 l ^ binv
+            double2 *const s0 = dyn_smem();
+            const uint32_t base =
+                D::swz(D::afwd(t ^ D::template binv<D::FILLPI>(tbg | P.gofs))) | (uint32_t)(buf - s0);
+            Unroll<RR>::run([&](auto V) {
+                constexpr uint32_t l = (uint32_t)decltype(V)::value * NT;
+                constexpr uint64_t o = D::dep(l);
+                constexpr uint32_t cv = D::swz(D::afwd(l));
+                cp_async16(s0 + (base ^ cv), psi + o);
+            });
+        } else {
+            Unroll<RR>::run([&](auto V) {
+                constexpr uint32_t l = (uint32_t)decltype(V)::value * NT;
+                constexpr uint64_t o = D::dep(l);
+                if constexpr (D::ADD_F) cp_async16(buf + t + l, psi + o);
+                else cp_async16(buf + (sw_t ^ D::swz(l)), psi + o);
+            });
+        }
     };
     uint32_t g = blockIdx.x;
     if (g >= total_tiles) return;

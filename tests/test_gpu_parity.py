@@ -590,6 +590,7 @@ def test_degenerate_sizes_and_empty_inputs(lq, oracle, jit):
         assert g.size == 0 and abs(e - oracle.expval(psi0, terms)) <= 1e-12
         gates = [("RY", 0, -1, 0, 0.0), ("RX", 3, -1, 2, 0.0), ("CNOT", 0, 5, -1, 0.0)]   # param 1 unused
         th = np.array([0.3, 1.7, -0.4])
+        terms = [(0.7, 0, 1 << 0), (0.4, 0, 1 << 3), (0.3, 1 << 0, 1 << 5), (-0.2, 1 << 3, 0)]
         g, e = lq.lq_param_shift_grad(n, gates, th, terms)
         assert g[1] == 0.0
         go = oracle.param_shift_grad(n, gates, th, terms)

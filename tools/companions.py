@@ -59,7 +59,10 @@ npass = lq.lq_plan_describe(n, tg)[0]
 row(f"tile pass: 40 random gates ({npass} pass)", 32 * npass, timed(lambda: sv.apply(tg)))
 row("tile pass: 10 RY+10 RZ layer slice", 32, timed(lambda: sv.apply(
     [("RY", q, -1, -1, 0.3 + q) for q in range(n - 10, n)] + [("RZ", q, -1, -1, 0.2 * q) for q in range(n - 10, n)])))
-l0 = lq.lq_launch_count(); sv.qft(); qp = lq.lq_launch_count() - l0
+lq.lq_set_option(lq.LQ_OPT_KERNEL_TIMING, 1); lq.lq_kernel_timing_reset()
+sv.qft(); torch.cuda.synchronize()
+qp = lq.lq_kernel_timing(lq.KC_TILE)[1]   # tile passes only (not the op-table staging kernel)
+lq.lq_set_option(lq.LQ_OPT_KERNEL_TIMING, 0)
 row(f"QFT({n}) ({qp} tile passes, bit reversal = relabel)", 32 * qp, timed(lambda: sv.qft()))
 xyz = W.xyz_terms(n)
 ep = lq.lq_plan_export_json(n, [], xyz)
