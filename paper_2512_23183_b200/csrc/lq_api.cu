@@ -206,18 +206,18 @@ struct PlanCache {
 };
 PlanCache g_plan_cache;
 
-std::string plan_key(char kind, int n, const int32_t *qmap, const void *payload, size_t bytes) {
+std::string plan_key(char kind, int n, const int32_t *qmap, const void *payload, size_t bytes, const void *stream) {
     std::string k(1, kind);
-    int64_t o[7] = {n, g_opt_K.load(), g_opt_coalesce.load(), g_opt_fusion.load(), g_opt_regbits.load(),
-                    g_opt_jit.load(), g_opt_budget.load()};
+    int64_t o[8] = {n, g_opt_K.load(), g_opt_coalesce.load(), g_opt_fusion.load(), g_opt_regbits.load(),
+                    g_opt_jit.load(), g_opt_budget.load(), (int64_t)(intptr_t)stream};
     k.append(reinterpret_cast<const char *>(o), sizeof(o));
     k.append(reinterpret_cast<const char *>(qmap), sizeof(int32_t) * (size_t)n);
     if (bytes) k.append(reinterpret_cast<const char *>(payload), bytes);
     return k;
 }
 
-std::string gates_key(int n, const int32_t *qmap, const lq_gate *g, size_t ng) {
-    std::string k = plan_key('a', n, qmap, nullptr, 0);
+std::string gates_key(int n, const int32_t *qmap, const lq_gate *g, size_t ng, const void *stream) {
+    std::string k = plan_key('a', n, qmap, nullptr, 0, stream);
     for (size_t i = 0; i < ng; i++) {
         lq_gate c = g[i];
         c.mat = nullptr;
@@ -598,6 +598,7 @@ lq_status check_sv(const lq_sv *sv) {
 // Run a circuit-level plan on one state (apply_circuit / canonicalize / qft).
 lq_status run_single(lq_sv *sv, Plan &plan, const MatBuilder &mb, const double *theta, size_t n_theta) {
     if (plan.passes.empty()) return LQ_OK;
+    if (!plan.prepared) plan.stream_tag = (uint64_t)(uintptr_t)sv->stream;
     LQ_TRY(prepare(plan));
     Blob blob;
     size_t o_sub = blob.add(plan.subs), o_kop = blob.add(plan.kops), o_spec = blob.add(mb.specs),
@@ -763,7 +764,10 @@ lq_status sh_run(lq_sv *sv, Schedule &sc, const double *theta, size_t n_theta, d
     cudaStream_t st = sv->stream;
     plan_steps(sc, options());
     for (auto &stp : sc.steps)
-        if (stp.kind == 0) LQ_TRY(prepare(stp.plan));
+        if (stp.kind == 0) {
+            stp.plan.stream_tag = (uint64_t)(uintptr_t)st;
+            LQ_TRY(prepare(stp.plan));
+        }
     Blob blob;
     struct Off { size_t sub, kop, perm, pt, et, dt, cd; };
     std::vector<Off> offs(sc.steps.size());
@@ -1373,7 +1377,7 @@ lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const doub
         sv->xmask = xm;
         return LQ_OK;
     }
-    const std::string key = gates_key(sv->n, sv->qmap, gates, n_gates);
+    const std::string key = gates_key(sv->n, sv->qmap, gates, n_gates, sv->stream);
     std::shared_ptr<CachedPlan> cp = g_plan_cache.get(key);
     if (!cp) {
         cp = std::make_shared<CachedPlan>();
@@ -1381,6 +1385,7 @@ lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const doub
         std::vector<POp> ops;
         lower_gates(sv->n, gates, n_gates, cp->qmap_after, ops, cp->mb);
         plan_circuit(sv->n, ops, options(), cp->mb, cp->plan);
+        cp->plan.stream_tag = (uint64_t)(uintptr_t)sv->stream;
         if (!cp->plan.passes.empty()) LQ_TRY(prepare(cp->plan));
         cp->plan.prepared = true;
         g_plan_cache.put(key, cp);
@@ -1415,13 +1420,14 @@ lq_status lq_qft(lq_sv *sv, int inverse) {
         return apply_impl(sv, g.data(), g.size(), nullptr, 0);
     }
     const int inv = inverse != 0;
-    const std::string key = plan_key('q', sv->n, qm, &inv, sizeof(inv));
+    const std::string key = plan_key('q', sv->n, qm, &inv, sizeof(inv), sv->stream);
     std::shared_ptr<CachedPlan> cp = g_plan_cache.get(key);
     if (!cp) {
         cp = std::make_shared<CachedPlan>();
         memcpy(cp->qmap_after, qm, sizeof(qm));
         if (!plan_qft(sv->n, cp->qmap_after, inv, options(), cp->plan, cp->mb))
             return fail(LQ_ERR_STATE, "qft planning failed");
+        cp->plan.stream_tag = (uint64_t)(uintptr_t)sv->stream;
         LQ_TRY(prepare(cp->plan));
         cp->plan.prepared = true;
         g_plan_cache.put(key, cp);
@@ -1450,13 +1456,14 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
         sv->xmask = xm;
         return LQ_OK;
     }
-    const std::string key = plan_key('e', sv->n, sv->qmap, terms, sizeof(lq_pauli_term) * n_terms);
+    const std::string key = plan_key('e', sv->n, sv->qmap, terms, sizeof(lq_pauli_term) * n_terms, sv->stream);
     std::shared_ptr<CachedPlan> cp = g_plan_cache.get(key);
     if (!cp) {
         cp = std::make_shared<CachedPlan>();
         std::vector<POp> ops;
         lower_pauli(sv->n, sv->qmap, terms, n_terms, ops, cp->plan);
         plan_circuit(sv->n, ops, options(), cp->mb, cp->plan);
+        cp->plan.stream_tag = (uint64_t)(uintptr_t)sv->stream;
         LQ_TRY(prepare(cp->plan));
         cp->plan.prepared = true;
         g_plan_cache.put(key, cp);
@@ -1688,6 +1695,7 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
         B = std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)atoi(be), std::max(1, n_circ)));
     P->B = (int)B;
     P->plan.ctab_circ = (int)B;   // constant op-table banks hold one launch's circuits
+    P->plan.stream_tag = (uint64_t)(uintptr_t)P->stream;
     {
         lq_status js = prepare(P->plan, true);
         if (js != LQ_OK) {

@@ -76,6 +76,8 @@ struct Plan {
     std::vector<void *> jit_ctab;     // per pass: device address of its lqj_ctab, or nullptr (smem tables)
     std::vector<CtabDesc> ctab_desc;  // the passes with jit_ctab, in pass order (staging layout)
     uint32_t ctab_total = 0;          // staging buffer size (double2) for ctab_circ circuits
+    uint64_t stream_tag = 0;          // the stream the plan runs on: constant banks are per module, so
+                                      // JIT modules with constant tables are private to one stream
 };
 
 struct MatBuilder {

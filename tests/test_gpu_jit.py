@@ -108,3 +108,27 @@ def test_qft_on_permuted_layout(lq, oracle, jit):
         oracle.qft(ref, inverse=inverse)
         assert np.abs(sv.read() - ref).max() <= AMP_TOL
         sv.free()
+
+
+def test_jit_constant_tables_two_streams(lq, oracle):
+    """JIT passes read their op tables from a per-module constant bank that
+    is refilled before each launch; modules are private to a stream, so the
+    same circuit with different angles on two concurrent streams must not
+    interfere."""
+    import torch
+    n = 14
+    gates = W.hea_ansatz(n, 2, "ring")
+    rng = np.random.default_rng(77)
+    th = [rng.uniform(0, 2 * np.pi, 4 * n) for _ in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    svs = [lq.StateVector(n, stream=s) for s in streams]
+    for rep in range(3):
+        for sv, t in zip(svs, th):
+            sv.init_random(5).apply(gates, t)
+        torch.cuda.synchronize()
+        for sv, t in zip(svs, th):
+            ref = oracle.init_random(n, 5)
+            oracle.apply_circuit(ref, gates, t)
+            assert np.abs(sv.read() - ref).max() <= AMP_TOL
+    for sv in svs:
+        sv.free()
