@@ -177,6 +177,26 @@ void lower_gates(int n, const lq_gate *gates, size_t n_gates, int32_t *qmap,
         fusable.push_back(0);
         touch_all((int)ops.size() - 1);
     }
+    for (size_t i = base; i < ops.size(); i++) {   // Pauli generators (Blocker)
+        POp &P = ops[i];
+        if (P.ctrl) continue;
+        const uint64_t b0 = P.t0 >= 0 ? bit(P.t0) : 0, b1 = P.t1 >= 0 ? bit(P.t1) : 0;
+        switch (P.type) {
+        case K_D1: P.pgen = true; P.gz = b0; break;                 // any diagonal: a function of Z
+        case K_D2: P.pgen = true; P.gz = b0 | b1; break;
+        case K_X: P.pgen = true; P.gx = b0; break;
+        case K_G:
+            if (P.qj == GK_REAL) { P.pgen = true; P.gx = P.gz = b0; }    // RY
+            else if (P.qj == GK_IMAG) { P.pgen = true; P.gx = b0; }     // RX
+            break;
+        case K_GG:
+            P.pgen = true;
+            P.gx = b0 | b1;
+            if (P.qflags & GG_YY) P.gz = b0 | b1;
+            break;
+        default: break;
+        }
+    }
     for (size_t i = base; i < ops.size(); i++) {
         POp &P = ops[i];
         auto &F = fl[i - base];
@@ -236,10 +256,34 @@ void lower_pauli(int n, const int32_t *qmap, const lq_pauli_term *terms, size_t 
 // --------------------------------------------------------------------------
 namespace {
 
+// Ops left behind block later ops that do not commute with them.  The
+// bit-mask rule (two ops commute if every shared bit is diagonal in both)
+// covers everything; for two Pauli-generator ops (POp::pgen) the letters are
+// compared per bit instead -- conservatively: any bit on which the letters
+// differ counts as a conflict -- so e.g. X(x)X rotations on overlapping pairs
+// pass each other.
 struct Blocker {
-    uint64_t bF = 0, bT = 0;
-    bool blocked(const POp &o) const { return (o.full() & bT) || (o.touch() & bF); }
-    void add(const POp &o) { bF |= o.full(); bT |= o.touch(); }
+    uint64_t bF = 0, bT = 0;         // every blocked op
+    uint64_t nF = 0, nT = 0;         // blocked ops without a Pauli generator
+    uint64_t mX = 0, mY = 0, mZ = 0; // letters of blocked Pauli-generator ops, per bit
+    bool blocked(const POp &o) const {
+        if (!o.pgen) return (o.full() & bT) || (o.touch() & bF);
+        if ((o.full() & nT) || (o.touch() & nF)) return true;
+        const uint64_t oX = o.gx & ~o.gz, oY = o.gx & o.gz, oZ = o.gz & ~o.gx;
+        return ((oX & (mY | mZ)) | (oY & (mX | mZ)) | (oZ & (mX | mY))) != 0;
+    }
+    void add(const POp &o) {
+        bF |= o.full();
+        bT |= o.touch();
+        if (!o.pgen) {
+            nF |= o.full();
+            nT |= o.touch();
+            return;
+        }
+        mX |= o.gx & ~o.gz;
+        mY |= o.gx & o.gz;
+        mZ |= o.gz & ~o.gx;
+    }
 };
 
 // first-fit absorption of `rem` into a tile whose bit set starts at Tm.

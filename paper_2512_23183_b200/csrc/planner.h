@@ -28,6 +28,12 @@ struct POp {
     int group = -1;           // K_EXPV: index into Plan::groups
     uint64_t rd = 0;          // bits read diagonally without being controls (QFT stage twiddle inputs)
     int layout = -1;          // K_QFT (QF_GENERAL): index into MatBuilder::layouts
+    // Pauli generator: an uncontrolled op exp(-i t P / 2) (or P itself) with
+    // P = X^gx Z^gz up to a phase.  Two such ops commute when P and P' do,
+    // which the planner's blocker uses beyond the bit-mask rule (Trotter
+    // chains: X(x)X rotations on overlapping pairs commute).
+    bool pgen = false;
+    uint64_t gx = 0, gz = 0;
     uint64_t full() const;    // bits on which the op is not diagonal
     uint64_t touch() const;   // every bit the op reads
     bool diag() const { return type == K_D1 || type == K_D2 || type == K_SCALE; }
