@@ -180,7 +180,22 @@ struct CachedPlan {
     Plan plan;
     MatBuilder mb;
     int32_t qmap_after[64];
+    int uses = 0;
+    bool promoted = false;
 };
+
+// Compile on second use: in auto JIT mode small single-state plans start on
+// the interpreter (NVRTC costs ~1 s per pass); a cached plan that runs a
+// second time is specialised like a PSR plan (config 1 / config 2 shapes).
+lq_status promote(CachedPlan &cp) {
+    if (++cp.uses < 2 || cp.promoted || g_opt_jit.load() != 1) return LQ_OK;
+    cp.promoted = true;
+    if (cp.plan.passes.empty() || cp.plan.n_tile == 0 || !cp.plan.jit.empty()) return LQ_OK;
+    cp.plan.prepared = false;
+    lq_status s = prepare(cp.plan, true);
+    cp.plan.prepared = true;
+    return s;
+}
 struct PlanCache {
     std::mutex mu;
     std::list<std::pair<std::string, std::shared_ptr<CachedPlan>>> lru;
@@ -1390,6 +1405,7 @@ lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const doub
         cp->plan.prepared = true;
         g_plan_cache.put(key, cp);
     }
+    LQ_TRY(promote(*cp));
     LQ_TRY(run_single(sv, cp->plan, cp->mb, theta, n_theta));
     memcpy(sv->qmap, cp->qmap_after, sizeof(sv->qmap));
     return LQ_OK;
@@ -1432,6 +1448,7 @@ lq_status lq_qft(lq_sv *sv, int inverse) {
         cp->plan.prepared = true;
         g_plan_cache.put(key, cp);
     }
+    LQ_TRY(promote(*cp));
     LQ_TRY(run_single(sv, cp->plan, cp->mb, nullptr, 0));
     memcpy(sv->qmap, cp->qmap_after, sizeof(sv->qmap));
     return LQ_OK;
@@ -1468,6 +1485,7 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
         cp->plan.prepared = true;
         g_plan_cache.put(key, cp);
     }
+    LQ_TRY(promote(*cp));
     const Plan &plan = cp->plan;
     DirectSet dset;
     dset.build(plan);
