@@ -264,9 +264,13 @@ namespace {
 // pass each other.
 struct Blocker {
     uint64_t bF = 0, bT = 0;         // every blocked op
+    uint64_t gF = 0, gT = 0;         // blocked ops that change the state (not Pauli-group reads)
     uint64_t nF = 0, nT = 0;         // blocked ops without a Pauli generator
     uint64_t mX = 0, mY = 0, mZ = 0; // letters of blocked Pauli-generator ops, per bit
     bool blocked(const POp &o) const {
+        // Pauli-group expectations only read the state: they never block
+        // each other, only the gates before them
+        if (o.type == K_EXPV) return (o.full() & gT) || (o.touch() & gF);
         if (!o.pgen) return (o.full() & bT) || (o.touch() & bF);
         if ((o.full() & nT) || (o.touch() & nF)) return true;
         const uint64_t oX = o.gx & ~o.gz, oY = o.gx & o.gz, oZ = o.gz & ~o.gx;
@@ -275,6 +279,10 @@ struct Blocker {
     void add(const POp &o) {
         bF |= o.full();
         bT |= o.touch();
+        if (o.type != K_EXPV) {
+            gF |= o.full();
+            gT |= o.touch();
+        }
         if (!o.pgen) {
             nF |= o.full();
             nT |= o.touch();
