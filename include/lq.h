@@ -331,7 +331,7 @@ typedef enum {
                                  both execute the same device op templates (tile.cuh).  0: off;
                                  1 (default): auto -- PSR plans and states with n >= 26; 2: always. */
     LQ_OPT_PASS_BUDGET = 6    /* planner: estimated FP64 instructions per amplitude (x10) a tile pass may
-                                 absorb before it stops (default 350; 0 = no limit, absorb greedily) */
+                                 absorb before it stops (default 400; 0 = no limit, absorb greedily) */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);

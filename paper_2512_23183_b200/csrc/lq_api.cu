@@ -41,7 +41,7 @@ std::atomic<int64_t> g_opt_K{0};
 std::atomic<int64_t> g_opt_coalesce{3};
 std::atomic<int64_t> g_opt_regbits{4};
 std::atomic<int64_t> g_opt_jit{1};
-std::atomic<int64_t> g_opt_budget{350};   // keeps passes from turning compute-bound (swept: 350 best)
+std::atomic<int64_t> g_opt_budget{400};   // keeps passes from turning compute-bound (swept; 350 gains 0.4 % on config 4 but costs 5-12 % on Trotter / random circuits)
 const double PI = 3.14159265358979323846264338327950288;
 
 lq_status fail(lq_status s, const std::string &msg) {

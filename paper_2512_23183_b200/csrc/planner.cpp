@@ -1,6 +1,8 @@
 // planner.cpp -- host gate-fusion planner.  See planner.h.
 #include "planner.h"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -270,7 +272,8 @@ struct Blocker {
     bool blocked(const POp &o) const {
         // Pauli-group expectations only read the state: they never block
         // each other, only the gates before them
-        if (o.type == K_EXPV) return (o.full() & gT) || (o.touch() & gF);
+        static const bool old_rule = getenv("LQ_EXPV_BLOCK_ALL") != nullptr;   // A/B experiments
+        if (o.type == K_EXPV && !old_rule) return (o.full() & gT) || (o.touch() & gF);
         if (!o.pgen) return (o.full() & bT) || (o.touch() & bF);
         if ((o.full() & nT) || (o.touch() & nF)) return true;
         const uint64_t oX = o.gx & ~o.gz, oY = o.gx & o.gz, oZ = o.gz & ~o.gx;
