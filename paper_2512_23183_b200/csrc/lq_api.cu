@@ -147,10 +147,6 @@ lq_status prepare(Plan &plan, bool reused = false) {
     const int64_t mode = g_opt_jit.load();
     if (mode == 0 || plan.n_tile == 0) return LQ_OK;
     if (mode == 1 && !reused && plan.n < 26) return LQ_OK;
-    {
-        const char *sb = getenv("LQ_SINGLEBUF");   // experiments: one tile buffer, two CTAs per SM
-        plan.single_buf = sb && atoi(sb) != 0;
-    }
     plan.ctab = getenv("LQ_JIT_NO_CTAB") == nullptr;   // constant-bank op tables (A/B switch for experiments)
     std::string err;
     if (!jit_plan(plan, plan.jit, plan.jit_ctab, err)) {
@@ -369,10 +365,10 @@ template <int RR>
 lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
                          const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                          uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride,
-                         int n_circ, double *partials, uint64_t slot_stride, cudaStream_t st, bool single) {
+                         int n_circ, double *partials, uint64_t slot_stride, cudaStream_t st) {
     static bool attr = false;
     static int n_sm = 0;
-    const size_t smem = ((size_t)(jk && single ? 16 : 32) << kp.K) + (size_t)kp.smat * sizeof(double2) +
+    const size_t smem = ((size_t)32 << kp.K) + (size_t)kp.smat * sizeof(double2) +
                         (size_t)(kp.op_end - kp.op_begin) * sizeof(KOp) +
                         (size_t)(kp.perm_end - kp.perm_begin) * sizeof(KPerm) + (size_t)n_pterms * sizeof(KPermTerm) +
                         (256 + 32) * sizeof(uint64_t) + (size_t)(kp.sub_end - kp.sub_begin + 1) * sizeof(KSub) +
@@ -416,9 +412,9 @@ lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, cons
 lq_status launch_tile(int Rr, const void *jk, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
                       const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                       uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride, int n_circ,
-                      double *partials, uint64_t slot_stride, cudaStream_t st, bool single = false) {
+                      double *partials, uint64_t slot_stride, cudaStream_t st) {
 #define LT(RRV) launch_tile_rr<RRV>(jk, kp, subs, kops, perms, pterms, n_pterms, eterms, mats, mat_stride, cst, state, \
-                                    state_stride, n_circ, partials, slot_stride, st, single)
+                                    state_stride, n_circ, partials, slot_stride, st)
     switch (Rr) {
     case 1: return LT(1);
     case 2: return LT(2);
@@ -481,7 +477,7 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
                 npt = plan.perms[kp.perm_end - 1].term_end - plan.perms[kp.perm_begin].term_begin;
             const void *jk = i < plan.jit.size() ? plan.jit[i] : nullptr;
             LQ_TRY(launch_tile(plan.Rr, jk, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, dp.eterms, mats, mat_stride,
-                               dp.cst, state, state_stride, n_circ, partials, slot_stride, st, plan.single_buf));
+                               dp.cst, state, state_stride, n_circ, partials, slot_stride, st));
         } else if (p.kind == PASS_PAIR) {
             const KOp op = plan.kops[p.op_begin];
             uint64_t work = (op.type == K_U1 || op.type == K_X) ? (1ull << (n - 1)) : (1ull << (n - 2));
@@ -1667,14 +1663,7 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     // the Pauli groups ride on the circuit's own tile passes (read after the
     // last gate that touches their qubits)
     lower_pauli(n_qubits, qm, terms, n_terms, ops, P->plan);
-    PlanOptions po = options();
-    {
-        // tuning experiments only: a smaller budget for the write-only first
-        // pass added passes and time (3.07 -> 3.12-3.21 s), so it is off
-        const char *fb = getenv("LQ_FIRST_BUDGET");
-        po.first_budget = fb ? atoi(fb) : 0;
-    }
-    plan_circuit(n_qubits, ops, po, P->mb, P->plan);
+    plan_circuit(n_qubits, ops, options(), P->mb, P->plan);
     P->plan.zero_first = true;   // lq_psr_run launches the first pass with PF_LOAD_ZERO
     P->dset.build(P->plan);
     // circuits of this shard: (p, +pi/2), (p, -pi/2) for owned p; base on shard 0.

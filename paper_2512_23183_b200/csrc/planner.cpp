@@ -845,11 +845,8 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
         if (!skip[i]) rem.push_back((int)i);
     // the FP64 budget trades an extra HBM round trip for less arithmetic per
     // pass; a state that is one tile has no HBM round trip to trade
-    const int budget_all = nl > K ? opt.budget : 0;
+    const int budget = nl > K ? opt.budget : 0;
     while (!rem.empty()) {
-        // the first pass of a PSR circuit synthesises |0...0> (no load): half
-        // the HBM time, so half the FP64 budget (opt.first_budget)
-        const int budget = (plan.passes.empty() && opt.first_budget > 0 && budget_all) ? opt.first_budget : budget_all;
         uint64_t Tm = mand;
         std::vector<int> absorbed, absorbed_w;
         first_fit(ops, rem, K, Tm, absorbed, budget);

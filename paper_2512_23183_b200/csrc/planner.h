@@ -75,7 +75,6 @@ struct Plan {
     size_t n_folded = 0;      // permutation gates folded into exchanges
     std::vector<const void *> jit;    // per pass: JIT-compiled tile kernel (cudaKernel_t) or nullptr (jit.h)
     bool prepared = false;            // jit resolved (prepare() in lq_api.cu)
-    bool single_buf = false;          // JIT passes use one tile buffer, two CTAs per SM (tile.cuh D::SINGLE)
     bool zero_first = false;          // the first pass synthesises |0...0> (PSR plans: PF_LOAD_ZERO)
     bool ctab = false;                // JIT passes read op tables from a __constant__ bank (jit.cpp)
     int ctab_circ = 1;                // circuits per launch the constant tables are sized for
@@ -103,7 +102,6 @@ struct PlanOptions {
     int reg_bits = 4;        // register bits per thread (R); tile kernels run 2^(K-R) threads
     int n_local = 0;         // sharded state: only bits [0, n_local) are local (0 = all n bits)
     int budget = 0;          // FP64 budget of a tile pass in tenths of an instruction per amplitude (0: none)
-    int first_budget = 0;    // budget of the plan's first pass when it does not load (PSR, PF_LOAD_ZERO); 0: budget
 };
 
 // Estimated FP64 instructions per amplitude (x10) an op costs in a tile pass.

@@ -364,7 +364,6 @@ struct TState {
     double2 ttmax;     // QFT twiddle state of the current sub-block
     uint64_t lg;
     const uint8_t *lpos;   // physical -> logical bit map of the pass (QF_GENERAL stages)
-    const double2 *gtab;   // this circuit's matrix block in global memory (JIT, LQ_JIT_GTAB)
     uint32_t cbase;        // this circuit's offset in the pass's constant op-table bank (JIT, D::CTAB)
     __device__ __forceinline__ void reset() {
         fb = 0;
@@ -1208,9 +1207,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
     constexpr uint32_t NT = 1u << (K - RR);
     constexpr int LAST = D::NSUB - 1;
     const uint32_t t = threadIdx.x;
-    // D::SINGLE: one tile buffer (no in-CTA prefetch; two CTAs per SM overlap
-    // each other's loads instead) -- lets 12-bit tiles run two CTAs per SM
-    double2 *s_tab = sm + (D::SINGLE ? 1 : 2) * TS;
+    double2 *s_tab = sm + 2 * TS;
     ETerm *s_et = reinterpret_cast<ETerm *>(s_tab + P.smat);
     const uint32_t nops = P.op_end - P.op_begin;
     const uint32_t net = P.eterm_end - P.eterm_begin;
@@ -1222,46 +1219,27 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
     auto issue = [&](uint32_t g, double2 *buf) {
         const uint64_t tbg = D::tbase(g & tmask);
         const double2 *psi = state + (uint64_t)(g >> tiles_log2) * state_stride + tbg + dep_t;
-        if constexpr (D::FILLPI >= 0) {
-            // the first sub-block's entry permutation P applied by the fill:
-            // loaded element m lands in slot swz(A (m ^ binv)), P^-1 l = A^-1 l ^ binv
-            double2 *const s0 = dyn_smem();
-            const uint32_t base =
-                D::swz(D::afwd(t ^ D::template binv<D::FILLPI>(tbg | P.gofs))) | (uint32_t)(buf - s0);
-            Unroll<RR>::run([&](auto V) {
-                constexpr uint32_t l = (uint32_t)decltype(V)::value * NT;
-                constexpr uint64_t o = D::dep(l);
-                constexpr uint32_t cv = D::swz(D::afwd(l));
-                cp_async16(s0 + (base ^ cv), psi + o);
-            });
-        } else {
-            Unroll<RR>::run([&](auto V) {
-                constexpr uint32_t l = (uint32_t)decltype(V)::value * NT;
-                constexpr uint64_t o = D::dep(l);
-                if constexpr (D::ADD_F) cp_async16(buf + t + l, psi + o);
-                else cp_async16(buf + (sw_t ^ D::swz(l)), psi + o);
-            });
-        }
+        Unroll<RR>::run([&](auto V) {
+            constexpr uint32_t l = (uint32_t)decltype(V)::value * NT;
+            constexpr uint64_t o = D::dep(l);
+            if constexpr (D::ADD_F) cp_async16(buf + t + l, psi + o);
+            else cp_async16(buf + (sw_t ^ D::swz(l)), psi + o);
+        });
     };
     uint32_t g = blockIdx.x;
     if (g >= total_tiles) return;
-    if constexpr (!D::SINGLE) {
-        if (!zero) issue(g, sm);
-        cp_async_commit();
-    }
+    if (!zero) issue(g, sm);
+    cp_async_commit();
     int cur_circ = -1;
-    // LATE (constant op tables, two buffers): the next tile's prefetch is
+    // LATE (constant op tables): the next tile's prefetch is
     // issued right after the barrier that starts this tile -- every thread has
     // then finished the previous tile, whose buffer the prefetch refills -- so
     // no barrier is needed at the end of a tile.
-    constexpr bool LATE = D::CTAB && !D::SINGLE;
+    constexpr bool LATE = D::CTAB;
     for (uint32_t i = 0; g < total_tiles; i++, g += gridDim.x) {
         const uint32_t gn = g + gridDim.x;
-        double2 *b = D::SINGLE ? sm : sm + (i & 1) * TS;
-        if constexpr (D::SINGLE) {
-            if (!zero) issue(g, sm);
-            cp_async_commit();
-        } else if constexpr (!LATE) {
+        double2 *b = sm + (i & 1) * TS;
+        if constexpr (!LATE) {
             if (gn < total_tiles && !zero) issue(gn, sm + ((i + 1) & 1) * TS);
             cp_async_commit();
         }
@@ -1273,7 +1251,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
                 cur_circ = circ;
             }
         }
-        if constexpr (D::SINGLE || LATE) cp_async_wait0();
+        if constexpr (LATE) cp_async_wait0();
         else cp_async_wait1();
         __syncthreads();
         if constexpr (LATE) {
@@ -1288,7 +1266,6 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         TState ts;
         ts.reset();
         ts.lpos = P.lpos;
-        ts.gtab = mats + (uint64_t)circ * mat_stride;
         ts.cbase = (uint32_t)circ * D::SMAT;
         run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, P.gofs, t, s_tab, s_et, P.n, zero);
         double2 *psi = state + (uint64_t)circ * state_stride;

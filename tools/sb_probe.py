@@ -1,12 +1,12 @@
-"""Single- vs double-buffered tile passes (LQ_SINGLEBUF env, read at plan
-time): QFT(30) and the config-4 gradient at tile bits KS (env)."""
+"""Quick timing probe: QFT(30) (automatic and 11-bit tiles) and the config-4
+gradient at tile bits KS (env), CUDA events, min of 3."""
 import os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import workloads as W
 from paper_2512_23183_b200 import lq
 st = torch.cuda.current_stream()
-tag = f"SB={os.environ.get('LQ_SINGLEBUF', '0')}"
+tag = "probe"
 def timed(fn, R=3):
     fn(); torch.cuda.synchronize()
     ts = []
