@@ -319,6 +319,15 @@ lq_status lq_psr_stats(const lq_psr *plan, uint64_t *n_circuits, uint64_t *n_lau
  * reports. */
 lq_status lq_psr_traffic(const lq_psr *plan, uint64_t *tile_bytes_per_circuit, uint64_t *other_bytes_per_circuit);
 
+/* The same per launched pass, in launch order: bytes_out[i] = algorithmic
+ * HBM bytes of pass i for one circuit, kind_out[i] = 0 tile / 1 pair / 2
+ * diagonal.  Passes of a zero-first plan that run only over their nonzero
+ * tiles (lq_psr_run: tiles whose free bits lie outside the union of the
+ * earlier passes' tiles hold zeros and are never launched) count only those
+ * tiles.  Fills min(cap, *n_passes) entries; cap may be 0 to query the count. */
+lq_status lq_psr_pass_bytes(const lq_psr *plan, uint64_t *bytes_out, int32_t *kind_out, size_t cap,
+                            size_t *n_passes);
+
 /* ---- execution options (testing / measurement) -------------------------- */
 typedef enum {
     LQ_OPT_FUSION = 0,     /* 1 (default): tile-fused passes; 0: one pass per gate (pair/diag kernels) */
@@ -330,8 +339,11 @@ typedef enum {
                                  sm_100a (cached per process) instead of the op-list interpreter kernel;
                                  both execute the same device op templates (tile.cuh).  0: off;
                                  1 (default): auto -- PSR plans and states with n >= 26; 2: always. */
-    LQ_OPT_PASS_BUDGET = 6    /* planner: estimated FP64 instructions per amplitude (x10) a tile pass may
+    LQ_OPT_PASS_BUDGET = 6,   /* planner: estimated FP64 instructions per amplitude (x10) a tile pass may
                                  absorb before it stops (default 400; 0 = no limit, absorb greedily) */
+    LQ_OPT_FIRST_PASS_FREE = 7 /* PSR plans: 1 (default) exempts the first pass -- it synthesises |0...0>,
+                                 so every tile but one is stored as zeros without arithmetic -- from
+                                 the pass budget; 0: budget it like the others */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);

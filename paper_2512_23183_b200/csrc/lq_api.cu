@@ -41,6 +41,7 @@ std::atomic<int64_t> g_opt_K{0};
 std::atomic<int64_t> g_opt_coalesce{3};
 std::atomic<int64_t> g_opt_regbits{4};
 std::atomic<int64_t> g_opt_jit{1};
+std::atomic<int64_t> g_opt_first_free{1};   // PSR plans: the |0...0> pass is exempt from the budget
 std::atomic<int64_t> g_opt_budget{400};   // keeps passes from turning compute-bound (swept; 350 gains 0.4 % on config 4 but costs 5-12 % on Trotter / random circuits)
 const double PI = 3.14159265358979323846264338327950288;
 
@@ -147,6 +148,31 @@ lq_status prepare(Plan &plan, bool reused = false) {
     const int64_t mode = g_opt_jit.load();
     if (mode == 0 || plan.n_tile == 0) return LQ_OK;
     if (mode == 1 && !reused && plan.n < 26) return LQ_OK;
+    if (plan.zero_first && getenv("LQ_NO_SUPPORT") == nullptr) {
+        // The first pass writes every amplitude (|0...0> evolved inside its
+        // tile, zeros elsewhere) and a tile pass changes only its own tile
+        // bits, so after passes 0..i-1 the state is zero wherever a local bit
+        // outside the union U of their tiles is set.  Pass i needs only the
+        // tiles whose free bits lie in U; the others are zero in HBM and stay
+        // zero.  (Passes with Pauli groups write one partial per tile: never
+        // restricted.  A non-tile pass ends the tracking.)
+        const uint64_t all = plan.nl >= 64 ? ~0ull : ((1ull << plan.nl) - 1);
+        uint64_t U = 0;
+        bool track = true;
+        for (size_t i = 0; i < plan.passes.size(); i++) {
+            PlanPass &p = plan.passes[i];
+            p.sup_free = ~0ull;
+            p.tiles_log2 = -1;
+            if (p.kind != PASS_TILE) { track = false; continue; }
+            uint64_t tm = 0;
+            for (int b = 0; b < p.kp.K; b++) tm |= 1ull << p.kp.T[b];
+            if (track && i > 0 && !(p.kp.flags & PF_EXPV) && (U & ~tm & all) != (all & ~tm)) {
+                p.sup_free = U & ~tm & all;
+                p.tiles_log2 = __builtin_popcountll(p.sup_free);
+            }
+            U |= tm;
+        }
+    }
     plan.ctab = getenv("LQ_JIT_NO_CTAB") == nullptr;   // constant-bank op tables (A/B switch for experiments)
     std::string err;
     if (!jit_plan(plan, plan.jit, plan.jit_ctab, err)) {
@@ -365,7 +391,7 @@ template <int RR>
 lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
                          const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                          uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride,
-                         int n_circ, double *partials, uint64_t slot_stride, cudaStream_t st) {
+                         int n_circ, double *partials, uint64_t slot_stride, cudaStream_t st, int tl2) {
     static bool attr = false;
     static int n_sm = 0;
     const size_t smem = ((size_t)32 << kp.K) + (size_t)kp.smat * sizeof(double2) +
@@ -381,7 +407,9 @@ lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, cons
         attr = true;
     }
     if (smem > 227 * 1024) return fail(LQ_ERR_STATE, "tile pass exceeds shared memory (planner bug)");
-    const uint32_t tiles_log2 = (uint32_t)(kp.nl - kp.K);
+    // tl2 >= 0: a JIT pass launched over its nonzero tiles only (PlanPass::sup_free)
+    if (tl2 >= 0 && !jk) return fail(LQ_ERR_STATE, "restricted tile range without a JIT program (internal)");
+    const uint32_t tiles_log2 = tl2 >= 0 ? (uint32_t)tl2 : (uint32_t)(kp.nl - kp.K);
     const uint64_t total = (uint64_t)n_circ << tiles_log2;
     if (total >= (1ull << 32)) return fail(LQ_ERR_DIM, "too many tiles in one launch");
     // persistent grid: as many CTAs as fit on every SM (2 per SM for K <= 11)
@@ -412,9 +440,9 @@ lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, cons
 lq_status launch_tile(int Rr, const void *jk, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
                       const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                       uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride, int n_circ,
-                      double *partials, uint64_t slot_stride, cudaStream_t st) {
+                      double *partials, uint64_t slot_stride, cudaStream_t st, int tl2 = -1) {
 #define LT(RRV) launch_tile_rr<RRV>(jk, kp, subs, kops, perms, pterms, n_pterms, eterms, mats, mat_stride, cst, state, \
-                                    state_stride, n_circ, partials, slot_stride, st)
+                                    state_stride, n_circ, partials, slot_stride, st, tl2)
     switch (Rr) {
     case 1: return LT(1);
     case 2: return LT(2);
@@ -476,8 +504,12 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
             if (kp.perm_end > kp.perm_begin)
                 npt = plan.perms[kp.perm_end - 1].term_end - plan.perms[kp.perm_begin].term_begin;
             const void *jk = i < plan.jit.size() ? plan.jit[i] : nullptr;
+            // a restricted tile range presumes the zero-first pass ran (prepare())
+            if (p.tiles_log2 >= 0 && jk && !zero_first)
+                return fail(LQ_ERR_STATE, "restricted tile range outside a zero-first run (internal)");
+            const int tl2 = jk ? p.tiles_log2 : -1;
             LQ_TRY(launch_tile(plan.Rr, jk, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, dp.eterms, mats, mat_stride,
-                               dp.cst, state, state_stride, n_circ, partials, slot_stride, st));
+                               dp.cst, state, state_stride, n_circ, partials, slot_stride, st, tl2));
         } else if (p.kind == PASS_PAIR) {
             const KOp op = plan.kops[p.op_begin];
             uint64_t work = (op.type == K_U1 || op.type == K_X) ? (1ull << (n - 1)) : (1ull << (n - 2));
@@ -990,6 +1022,7 @@ lq_status lq_set_option(int option, int64_t value) {
         if (value < 0 || value > 2) return fail(LQ_ERR_ARG, "jit must be 0 (off), 1 (auto) or 2 (always)");
         g_opt_jit = value;
         return LQ_OK;
+    case LQ_OPT_FIRST_PASS_FREE: g_opt_first_free = value ? 1 : 0; return LQ_OK;
     default: return fail(LQ_ERR_ARG, "unknown option");
     }
 }
@@ -1003,6 +1036,7 @@ int64_t lq_get_option(int option) {
     case LQ_OPT_KERNEL_TIMING: return g_opt_timing.load();
     case LQ_OPT_JIT: return g_opt_jit.load();
     case LQ_OPT_PASS_BUDGET: return g_opt_budget.load();
+    case LQ_OPT_FIRST_PASS_FREE: return g_opt_first_free.load();
     default: return -1;
     }
 }
@@ -1663,7 +1697,9 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     // the Pauli groups ride on the circuit's own tile passes (read after the
     // last gate that touches their qubits)
     lower_pauli(n_qubits, qm, terms, n_terms, ops, P->plan);
-    plan_circuit(n_qubits, ops, options(), P->mb, P->plan);
+    PlanOptions po = options();
+    po.first_free = g_opt_first_free.load() != 0;
+    plan_circuit(n_qubits, ops, po, P->mb, P->plan);
     P->plan.zero_first = true;   // lq_psr_run launches the first pass with PF_LOAD_ZERO
     P->dset.build(P->plan);
     // circuits of this shard: (p, +pi/2), (p, -pi/2) for owned p; base on shard 0.
@@ -1857,29 +1893,49 @@ lq_status lq_psr_stats(const lq_psr *P, uint64_t *n_circuits, uint64_t *n_launch
     return LQ_OK;
 }
 
+// Algorithmic HBM bytes of pass i of one circuit, as launch_passes runs it:
+// the first tile pass synthesises |0...0> (write only), read-only passes and
+// the final pass (when no wide Pauli group reads the state afterwards) skip
+// the store, a pass restricted to its nonzero tiles (PlanPass::sup_free)
+// moves only those; every other pass reads and writes 16 B per amplitude.
+static uint64_t psr_pass_bytes(const lq_psr *P, size_t i) {
+    const uint64_t N = 1ull << P->n;
+    const size_t np = P->plan.passes.size();
+    const PlanPass &p = P->plan.passes[i];
+    bool load = !(i == 0 && p.kind == PASS_TILE);
+    bool store = true;
+    if (p.kind == PASS_TILE) {
+        if (p.kp.flags & PF_NO_STORE) store = false;
+        if (i + 1 == np && P->dset.ds.empty()) store = false;
+    }
+    const bool restricted = p.kind == PASS_TILE && p.tiles_log2 >= 0 && i < P->plan.jit.size() && P->plan.jit[i];
+    const uint64_t amps = restricted ? 1ull << (p.tiles_log2 + p.kp.K) : N;
+    uint64_t b = 16 * amps * ((load ? 1 : 0) + (store ? 1 : 0));
+    if (p.kind == PASS_DIAG) b *= (p.op_end - p.op_begin + DIAG_MAX_OPS - 1) / DIAG_MAX_OPS;   // one k_diag per chunk
+    return b;
+}
+
 lq_status lq_psr_traffic(const lq_psr *P, uint64_t *tile_bytes_per_circuit, uint64_t *direct_bytes_per_circuit) {
     if (!P) return fail(LQ_ERR_ARG, "invalid plan");
-    // algorithmic HBM bytes of one circuit, as launch_passes runs it: the
-    // first tile pass synthesises |0...0> (write only), read-only passes and
-    // the final pass (when no wide Pauli group reads the state afterwards)
-    // skip the store; every other pass reads and writes 16 B per amplitude.
     const uint64_t N = 1ull << P->n;
     uint64_t tb = 0, other = 0;
-    const size_t np = P->plan.passes.size();
-    for (size_t i = 0; i < np; i++) {
-        const PlanPass &p = P->plan.passes[i];
-        bool load = !(i == 0 && p.kind == PASS_TILE);
-        bool store = true;
-        if (p.kind == PASS_TILE) {
-            if (p.kp.flags & PF_NO_STORE) store = false;
-            if (i + 1 == np && P->dset.ds.empty()) store = false;
-        }
-        uint64_t b = 16 * N * ((load ? 1 : 0) + (store ? 1 : 0));
-        (p.kind == PASS_TILE ? tb : other) += b;
-    }
+    for (size_t i = 0; i < P->plan.passes.size(); i++)
+        (P->plan.passes[i].kind == PASS_TILE ? tb : other) += psr_pass_bytes(P, i);
     other += 32 * N * P->dset.ds.size();   // direct Pauli groups read psi[j] and psi[j ^ x]
     if (tile_bytes_per_circuit) *tile_bytes_per_circuit = tb;
     if (direct_bytes_per_circuit) *direct_bytes_per_circuit = other;
+    return LQ_OK;
+}
+
+lq_status lq_psr_pass_bytes(const lq_psr *P, uint64_t *bytes_out, int32_t *kind_out, size_t cap, size_t *n_passes) {
+    if (!P) return fail(LQ_ERR_ARG, "invalid plan");
+    const size_t np = P->plan.passes.size();
+    if (n_passes) *n_passes = np;
+    if (cap && (!bytes_out || !kind_out)) return fail(LQ_ERR_ARG, "output arrays are NULL");
+    for (size_t i = 0; i < np && i < cap; i++) {
+        bytes_out[i] = psr_pass_bytes(P, i);
+        kind_out[i] = (int32_t)P->plan.passes[i].kind;
+    }
     return LQ_OK;
 }
 
@@ -1916,8 +1972,8 @@ std::string psr_key(int n, const lq_gate *g, size_t ng, size_t np, const lq_paul
     auto put = [&](const void *p, size_t b) { k.append(static_cast<const char *>(p), b); };
     int64_t hdr[8] = {n, (int64_t)ng, (int64_t)np, (int64_t)nt, rank, world, (int64_t)(intptr_t)stream, 0};
     put(hdr, sizeof(hdr));
-    int64_t opt[6] = {g_opt_fusion.load(), g_opt_K.load(), g_opt_coalesce.load(), g_opt_regbits.load(),
-                      g_opt_jit.load(), g_opt_budget.load()};
+    int64_t opt[7] = {g_opt_fusion.load(), g_opt_K.load(), g_opt_coalesce.load(), g_opt_regbits.load(),
+                      g_opt_jit.load(), g_opt_budget.load(), g_opt_first_free.load()};
     put(opt, sizeof(opt));
     for (size_t i = 0; i < ng; i++) {
         put(&g[i], offsetof(lq_gate, mat));

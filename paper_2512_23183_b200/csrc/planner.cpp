@@ -845,8 +845,11 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
         if (!skip[i]) rem.push_back((int)i);
     // the FP64 budget trades an extra HBM round trip for less arithmetic per
     // pass; a state that is one tile has no HBM round trip to trade
-    const int budget = nl > K ? opt.budget : 0;
+    const int budget_all = nl > K ? opt.budget : 0;
     while (!rem.empty()) {
+        // a pass that synthesises |0...0> (PlanOptions::first_free) does its
+        // arithmetic on one tile per state only: no budget
+        const int budget = (opt.first_free && plan.passes.empty()) ? 0 : budget_all;
         uint64_t Tm = mand;
         std::vector<int> absorbed, absorbed_w;
         first_fit(ops, rem, K, Tm, absorbed, budget);

@@ -55,6 +55,11 @@ struct PlanPass {
     KPass kp{};               // TILE: descriptor (sub range into Plan::subs)
     uint32_t op_begin = 0, op_end = 0;   // PAIR/DIAG: range into Plan::kops (physical-bit form)
     int n_ops = 0;            // user-level ops fused into this pass (for stats)
+    // zero_first plans (JIT): the local bits outside the pass's tile that may
+    // be nonzero in its input.  Tiles with any other bit set hold zeros before
+    // and after the pass and are never launched (lq_api.cu prepare()).
+    uint64_t sup_free = ~0ull;
+    int tiles_log2 = -1;      // popcount(sup_free) when restricted, else -1 (nl - K)
 };
 
 struct Plan {
@@ -102,6 +107,7 @@ struct PlanOptions {
     int reg_bits = 4;        // register bits per thread (R); tile kernels run 2^(K-R) threads
     int n_local = 0;         // sharded state: only bits [0, n_local) are local (0 = all n bits)
     int budget = 0;          // FP64 budget of a tile pass in tenths of an instruction per amplitude (0: none)
+    bool first_free = false; // the first pass starts from |0...0> (PSR plans): exempt from the budget
 };
 
 // Estimated FP64 instructions per amplitude (x10) an op costs in a tile pass.

@@ -983,6 +983,16 @@ __device__ __forceinline__ void tile_body(const KPass &P, const KSub *__restrict
         __syncthreads();
 
         const uint64_t tb = tile_base(g);
+        if (zero && (tb | P.gofs) != 0 && !(P.flags & PF_EXPV)) {   // an all-zero tile (tile_body_static)
+            if (!(P.flags & PF_NO_STORE)) {
+                Mapping<RR> st;
+                st.make(t, P.Sstore, s_dlo, s_dhi, tb);
+                double2 *psi = state + (uint64_t)circ * state_stride;
+                Unroll<RR>::run([&](auto V) { psi[st.gt + st.template goff<decltype(V)::value>()] = make_double2(0.0, 0.0); });
+            }
+            __syncthreads();
+            continue;
+        }
         double2 a[NV];
         Mapping<RR> cur;
         KSub sb = s_sub[0];
@@ -1260,6 +1270,21 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         }
 
         const uint64_t tb = D::tbase(g & tmask);
+        if (D::ZSKIP && zero && (tb | P.gofs) != 0 && !(P.flags & PF_EXPV)) {
+            // |0...0> lives in tile 0 and the pass's ops act inside a tile:
+            // every other tile is zero before and after the pass -- store
+            // zeros, skip the arithmetic (CTA-uniform branch)
+            if (!(P.flags & PF_NO_STORE)) {
+                double2 *psi = state + (uint64_t)circ * state_stride;
+                const uint64_t gst = tb | D::dep(ins_zeros<D::SSTORE, K>(t));
+                Unroll<RR>::run([&](auto V) {
+                    constexpr uint64_t go = D::dep(loff_c<D::SSTORE>(decltype(V)::value));
+                    psi[gst + go] = make_double2(0.0, 0.0);
+                });
+            }
+            if constexpr (!LATE) __syncthreads();
+            continue;
+        }
         double2 a[NV];
         if (zero) xread_c<RR, D, D::SM[0], D::PERM[0], true>(b, a, t, tb, P.gofs);
         else xread_c<RR, D, D::SM[0], D::PERM[0], false, D::RADD[0]>(b, a, t, tb, P.gofs);

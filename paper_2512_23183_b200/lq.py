@@ -36,7 +36,7 @@ KIND_NAMES = ["H", "X", "Y", "Z", "S", "SDG", "T", "TDG", "RX", "RY", "RZ", "CNO
               "SWAP", "U1", "U2", "CRY", "CCX", "RXX", "RYY", "RZZ"]
 KINDS = {k: i for i, k in enumerate(KIND_NAMES)}
 LQ_OPT_FUSION, LQ_OPT_TILE_BITS, LQ_OPT_COALESCE_BITS, LQ_OPT_REG_BITS, LQ_OPT_KERNEL_TIMING, LQ_OPT_JIT, \
-    LQ_OPT_PASS_BUDGET = 0, 1, 2, 3, 4, 5, 6
+    LQ_OPT_PASS_BUDGET, LQ_OPT_FIRST_PASS_FREE = 0, 1, 2, 3, 4, 5, 6, 7
 KC_TILE, KC_PAIR, KC_DIAG, KC_PAULI, KC_OTHER = 0, 1, 2, 3, 4
 
 
@@ -118,6 +118,8 @@ _SIGS = {
     "lq_sv_shard_ptr": ([_P, _i32], _P),
     "lq_dist_schedule_json": ([_i32, _i32, _GP, _sz, _i32, _TP, _sz, ctypes.c_char_p, _sz, ctypes.POINTER(_sz)], _i32),
     "lq_psr_traffic": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i32),
+    "lq_psr_pass_bytes": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_i32), ctypes.c_size_t,
+                           ctypes.POINTER(ctypes.c_size_t)], _i32),
     "lq_jit_stats": ([ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_dbl)], _i32),
     "lq_jit_compile_check": ([_i32, _GP, _sz, _TP, _sz, ctypes.POINTER(_u64)], _i32),
     "lq_qft_jit_compile_check": ([_i32, _i32, ctypes.POINTER(_u64)], _i32),
@@ -387,6 +389,20 @@ def lq_psr_traffic(plan) -> Tuple[int, int]:
     a, b = ctypes.c_uint64(), ctypes.c_uint64()
     _chk(_lib.lq_psr_traffic(plan, ctypes.byref(a), ctypes.byref(b)))
     return a.value, b.value
+
+
+def lq_psr_cache_clear() -> None:
+    """Drop the cached PSR handles and single-state plans (lq_param_shift_grad)."""
+    _chk(_lib.lq_psr_cache_clear())
+
+
+def lq_psr_pass_bytes(plan) -> List[Tuple[int, int]]:
+    """[(kind, algorithmic HBM bytes per circuit)] per launched pass (0 tile, 1 pair, 2 diagonal)"""
+    n = ctypes.c_size_t()
+    _chk(_lib.lq_psr_pass_bytes(plan, None, None, 0, ctypes.byref(n)))
+    b, k = (_u64 * max(n.value, 1))(), (_i32 * max(n.value, 1))()
+    _chk(_lib.lq_psr_pass_bytes(plan, b, k, n.value, ctypes.byref(n)))
+    return [(k[i], b[i]) for i in range(n.value)]
 
 
 def lq_kernel_timing(kernel_class: int) -> Tuple[float, int]:

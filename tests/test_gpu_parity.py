@@ -34,6 +34,7 @@ def _restore_options(lq):
     lq.lq_set_option(lq.LQ_OPT_COALESCE_BITS, 3)
     lq.lq_set_option(lq.LQ_OPT_REG_BITS, 4)
     lq.lq_set_option(lq.LQ_OPT_JIT, 1)
+    lq.lq_set_option(lq.LQ_OPT_FIRST_PASS_FREE, 1)
 
 
 def grad_close(g, go):
@@ -407,6 +408,55 @@ def test_xyz_ring_gradient_small(lq, oracle, n, rb):
     grad_close(g, go)
     eo = oracle.energy(n, gates, theta, terms)
     assert abs(e - eo) <= 1e-10 * max(abs(eo), 1)
+
+
+@pytest.mark.parametrize("first_free", [0, 1])
+def test_psr_zero_first_support_restriction(lq, oracle, first_free, monkeypatch):
+    """A PSR plan's first pass synthesises |0...0>; later passes launch only
+    the tiles whose free bits lie in the union of the earlier tiles (the rest
+    are zero in HBM and stay zero).  The restricted run must equal the
+    unrestricted one bit for bit (same arithmetic on the nonzero tiles) and
+    the oracle; lq_psr_pass_bytes must show the restricted passes (n = 20 >
+    2K - 3: the first two 11-bit tiles cannot cover every qubit)."""
+    import torch
+    n = 20
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 11)
+    lq.lq_set_option(lq.LQ_OPT_FIRST_PASS_FREE, first_free)
+    gates = W.hea_ansatz(n, 3, "ring")
+    npar = 6 * n
+    theta = np.random.default_rng(20).uniform(0, 2 * np.pi, npar)
+    terms = W.xyz_terms(n)
+    st = torch.cuda.current_stream()
+    th = torch.tensor(theta, device="cuda")
+
+    def run():
+        lq.lq_psr_cache_clear()
+        P = lq.lq_psr_create(n, gates, npar, terms, stream=st)
+        g = torch.zeros(npar, dtype=torch.float64, device="cuda")
+        e = torch.zeros(1, dtype=torch.float64, device="cuda")
+        lq.lq_psr_run(P, th.data_ptr(), g.data_ptr(), e.data_ptr())
+        torch.cuda.synchronize()
+        pb = lq.lq_psr_pass_bytes(P)
+        lq.lq_psr_free(P)
+        return g.cpu().numpy(), e.item(), pb
+
+    g1, e1, pb1 = run()
+    monkeypatch.setenv("LQ_NO_SUPPORT", "1")
+    g0, e0, pb0 = run()
+    monkeypatch.delenv("LQ_NO_SUPPORT")
+    N = 1 << n
+    assert pb0[0] == (0, 16 * N) and pb1[0] == (0, 16 * N)     # the zero-first pass: write only
+    assert all(b in (16 * N, 32 * N) for k, b in pb0[1:] if k == 0)
+    assert [k for k, _ in pb1] == [k for k, _ in pb0]
+    restricted = [(b1, b0) for (k, b1), (_, b0) in zip(pb1, pb0) if k == 0 and b1 < b0]
+    assert restricted and all(b1 % (16 << 11) == 0 for b1, _ in restricted)
+    assert np.array_equal(g1, g0) and e1 == e0
+    which = [0, n, 2 * n + 5, npar - 1]
+    go = oracle.param_shift_grad(n, gates, theta, terms, which=which, threads=8)
+    scale = float(np.abs(g1).max())
+    for p, v in zip(which, go):
+        assert abs(g1[p] - v) <= 1e-10 * max(abs(v), scale), (p, g1[p], v)
+    assert abs(e1 - oracle.energy(n, gates, theta, terms)) <= 1e-10 * max(abs(e1), 1)
 
 
 def test_config4_full_size_closed_forms(lq):
