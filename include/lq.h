@@ -321,9 +321,10 @@ lq_status lq_psr_traffic(const lq_psr *plan, uint64_t *tile_bytes_per_circuit, u
 
 /* The same per launched pass, in launch order: bytes_out[i] = algorithmic
  * HBM bytes of pass i for one circuit, kind_out[i] = 0 tile / 1 pair / 2
- * diagonal.  Passes of a zero-first plan that run only over their nonzero
- * tiles (lq_psr_run: tiles whose free bits lie outside the union of the
- * earlier passes' tiles hold zeros and are never launched) count only those
+ * diagonal.  Passes of a zero-first plan under support tracking (lq_psr_run:
+ * while the union U of the tiles run so far misses some local bits, the state
+ * is zero at every index outside U, a pass reads only the indices inside U and
+ * runs only the tiles whose free bits lie in U) count only those reads and
  * tiles.  Fills min(cap, *n_passes) entries; cap may be 0 to query the count. */
 lq_status lq_psr_pass_bytes(const lq_psr *plan, uint64_t *bytes_out, int32_t *kind_out, size_t cap,
                             size_t *n_passes);

@@ -148,25 +148,40 @@ lq_status prepare(Plan &plan, bool reused = false) {
     const int64_t mode = g_opt_jit.load();
     if (mode == 0 || plan.n_tile == 0) return LQ_OK;
     if (mode == 1 && !reused && plan.n < 26) return LQ_OK;
+    for (PlanPass &p : plan.passes) {
+        p.support = p.sup_free = ~0ull;
+        p.tiles_log2 = -1;
+    }
     if (plan.zero_first && getenv("LQ_NO_SUPPORT") == nullptr) {
-        // The first pass writes every amplitude (|0...0> evolved inside its
-        // tile, zeros elsewhere) and a tile pass changes only its own tile
-        // bits, so after passes 0..i-1 the state is zero wherever a local bit
-        // outside the union U of their tiles is set.  Pass i needs only the
-        // tiles whose free bits lie in U; the others are zero in HBM and stay
-        // zero.  (Passes with Pauli groups write one partial per tile: never
-        // restricted.  A non-tile pass ends the tracking.)
+        // Support tracking.  The state starts as |0...0> and a tile pass
+        // changes only its own tile bits, so the state entering pass i is zero
+        // wherever a local bit outside U_i = T_0 | ... | T_{i-1} is set.
+        // Invariant: HBM holds the state at the indices inside U_i (garbage
+        // elsewhere).  Pass i loads only those indices (zeros synthesised for
+        // the rest of its tiles), runs only the tiles whose free bits lie in
+        // U_i (every other tile is zero and stays zero) and stores them whole:
+        // indices inside U_{i+1} = U_i | T_i, so the invariant carries over.
+        // Pass 0 (U = 0) is tile 0 only, |0...0> synthesised: no HBM read and
+        // 2^K amplitudes written.  Passes with Pauli groups run every tile
+        // (one partial per tile).  Valid when no non-tile pass comes before U
+        // covers every local bit, and the state after the plan is either whole
+        // (U = all) or read by nothing but the tile passes' own Pauli groups.
         const uint64_t all = plan.nl >= 64 ? ~0ull : ((1ull << plan.nl) - 1);
         uint64_t U = 0;
-        bool track = true;
-        for (size_t i = 0; i < plan.passes.size(); i++) {
+        bool ok = true;
+        for (const PlanPass &p : plan.passes) {
+            if (U == all) break;
+            if (p.kind != PASS_TILE) { ok = false; break; }
+            for (int b = 0; b < p.kp.K; b++) U |= 1ull << p.kp.T[b];
+        }
+        if (U != all && !plan.wide_groups.empty()) ok = false;
+        U = 0;
+        for (size_t i = 0; ok && i < plan.passes.size() && U != all; i++) {
             PlanPass &p = plan.passes[i];
-            p.sup_free = ~0ull;
-            p.tiles_log2 = -1;
-            if (p.kind != PASS_TILE) { track = false; continue; }
             uint64_t tm = 0;
             for (int b = 0; b < p.kp.K; b++) tm |= 1ull << p.kp.T[b];
-            if (track && i > 0 && !(p.kp.flags & PF_EXPV) && (U & ~tm & all) != (all & ~tm)) {
+            p.support = U;
+            if (!(p.kp.flags & PF_EXPV)) {
                 p.sup_free = U & ~tm & all;
                 p.tiles_log2 = __builtin_popcountll(p.sup_free);
             }
@@ -505,7 +520,7 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
                 npt = plan.perms[kp.perm_end - 1].term_end - plan.perms[kp.perm_begin].term_begin;
             const void *jk = i < plan.jit.size() ? plan.jit[i] : nullptr;
             // a restricted tile range presumes the zero-first pass ran (prepare())
-            if (p.tiles_log2 >= 0 && jk && !zero_first)
+            if ((p.tiles_log2 >= 0 || p.support != ~0ull) && jk && !zero_first)
                 return fail(LQ_ERR_STATE, "restricted tile range outside a zero-first run (internal)");
             const int tl2 = jk ? p.tiles_log2 : -1;
             LQ_TRY(launch_tile(plan.Rr, jk, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, dp.eterms, mats, mat_stride,
@@ -1896,8 +1911,9 @@ lq_status lq_psr_stats(const lq_psr *P, uint64_t *n_circuits, uint64_t *n_launch
 // Algorithmic HBM bytes of pass i of one circuit, as launch_passes runs it:
 // the first tile pass synthesises |0...0> (write only), read-only passes and
 // the final pass (when no wide Pauli group reads the state afterwards) skip
-// the store, a pass restricted to its nonzero tiles (PlanPass::sup_free)
-// moves only those; every other pass reads and writes 16 B per amplitude.
+// the store, a pass under support tracking (PlanPass::support) reads only the
+// indices inside its support and writes only the tiles it runs; every other
+// pass reads and writes 16 B per amplitude.
 static uint64_t psr_pass_bytes(const lq_psr *P, size_t i) {
     const uint64_t N = 1ull << P->n;
     const size_t np = P->plan.passes.size();
@@ -1908,9 +1924,12 @@ static uint64_t psr_pass_bytes(const lq_psr *P, size_t i) {
         if (p.kp.flags & PF_NO_STORE) store = false;
         if (i + 1 == np && P->dset.ds.empty()) store = false;
     }
-    const bool restricted = p.kind == PASS_TILE && p.tiles_log2 >= 0 && i < P->plan.jit.size() && P->plan.jit[i];
-    const uint64_t amps = restricted ? 1ull << (p.tiles_log2 + p.kp.K) : N;
-    uint64_t b = 16 * amps * ((load ? 1 : 0) + (store ? 1 : 0));
+    // support tracking (prepare()): loads of the indices inside the pass's
+    // support only, stores of the tiles it runs
+    const bool jit = p.kind == PASS_TILE && i < P->plan.jit.size() && P->plan.jit[i];
+    const uint64_t rd = (jit && p.support != ~0ull) ? 1ull << __builtin_popcountll(p.support & (N - 1)) : N;
+    const uint64_t wr = (jit && p.tiles_log2 >= 0) ? 1ull << (p.tiles_log2 + p.kp.K) : N;
+    uint64_t b = 16 * ((load ? rd : 0) + (store ? wr : 0));
     if (p.kind == PASS_DIAG) b *= (p.op_end - p.op_begin + DIAG_MAX_OPS - 1) / DIAG_MAX_OPS;   // one k_diag per chunk
     return b;
 }

@@ -55,9 +55,12 @@ struct PlanPass {
     KPass kp{};               // TILE: descriptor (sub range into Plan::subs)
     uint32_t op_begin = 0, op_end = 0;   // PAIR/DIAG: range into Plan::kops (physical-bit form)
     int n_ops = 0;            // user-level ops fused into this pass (for stats)
-    // zero_first plans (JIT): the local bits outside the pass's tile that may
-    // be nonzero in its input.  Tiles with any other bit set hold zeros before
-    // and after the pass and are never launched (lq_api.cu prepare()).
+    // zero_first plans (JIT, lq_api.cu prepare()): the state entering the
+    // pass is zero at every index with a local bit outside `support`, and HBM
+    // holds it only at the other indices.  The pass loads those and
+    // synthesises zeros for the rest; tiles whose free bits leave sup_free =
+    // support minus the tile hold zeros before and after and are not launched.
+    uint64_t support = ~0ull;
     uint64_t sup_free = ~0ull;
     int tiles_log2 = -1;      // popcount(sup_free) when restricted, else -1 (nl - K)
 };

@@ -1229,11 +1229,20 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
     auto issue = [&](uint32_t g, double2 *buf) {
         const uint64_t tbg = D::tbase(g & tmask);
         const double2 *psi = state + (uint64_t)(g >> tiles_log2) * state_stride + tbg + dep_t;
+        // UMASK (zero-first plans, lq_api.cu prepare()): the state is zero at
+        // every index with a bit outside UMASK and HBM holds garbage there --
+        // write zeros into those slots instead of loading them
+        const bool tok = D::UMASK == ~0ull || ((tbg | dep_t) & ~D::UMASK) == 0;
         Unroll<RR>::run([&](auto V) {
             constexpr uint32_t l = (uint32_t)decltype(V)::value * NT;
             constexpr uint64_t o = D::dep(l);
-            if constexpr (D::ADD_F) cp_async16(buf + t + l, psi + o);
-            else cp_async16(buf + (sw_t ^ D::swz(l)), psi + o);
+            double2 *dst = D::ADD_F ? buf + t + l : buf + (sw_t ^ D::swz(l));
+            if constexpr ((o & ~D::UMASK) != 0) {
+                *dst = make_double2(0.0, 0.0);
+            } else {
+                if (tok) cp_async16(dst, psi + o);
+                else *dst = make_double2(0.0, 0.0);
+            }
         });
     };
     uint32_t g = blockIdx.x;

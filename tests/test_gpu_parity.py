@@ -412,9 +412,10 @@ def test_xyz_ring_gradient_small(lq, oracle, n, rb):
 
 @pytest.mark.parametrize("first_free", [0, 1])
 def test_psr_zero_first_support_restriction(lq, oracle, first_free, monkeypatch):
-    """A PSR plan's first pass synthesises |0...0>; later passes launch only
-    the tiles whose free bits lie in the union of the earlier tiles (the rest
-    are zero in HBM and stay zero).  The restricted run must equal the
+    """A PSR plan's first pass synthesises |0...0>; while the union U of the
+    tiles run so far misses some qubits, a pass loads only the indices inside
+    U (the state is zero elsewhere; HBM holds garbage there) and runs only the
+    tiles whose free bits lie in U.  The restricted run must equal the
     unrestricted one bit for bit (same arithmetic on the nonzero tiles) and
     the oracle; lq_psr_pass_bytes must show the restricted passes (n = 20 >
     2K - 3: the first two 11-bit tiles cannot cover every qubit)."""
@@ -445,7 +446,9 @@ def test_psr_zero_first_support_restriction(lq, oracle, first_free, monkeypatch)
     g0, e0, pb0 = run()
     monkeypatch.delenv("LQ_NO_SUPPORT")
     N = 1 << n
-    assert pb0[0] == (0, 16 * N) and pb1[0] == (0, 16 * N)     # the zero-first pass: write only
+    # the zero-first pass writes only (every tile without support tracking,
+    # tile 0 alone with it: HBM holds the state only inside the support)
+    assert pb0[0] == (0, 16 * N) and pb1[0] == (0, 16 << 11)
     assert all(b in (16 * N, 32 * N) for k, b in pb0[1:] if k == 0)
     assert [k for k, _ in pb1] == [k for k, _ in pb0]
     restricted = [(b1, b0) for (k, b1), (_, b0) in zip(pb1, pb0) if k == 0 and b1 < b0]
