@@ -325,9 +325,13 @@ lq_status lq_psr_traffic(const lq_psr *plan, uint64_t *tile_bytes_per_circuit, u
  * while the union U of the tiles run so far misses some local bits, the state
  * is zero at every index outside U, a pass reads only the indices inside U and
  * runs only the tiles whose free bits lie in U) count only those reads and
- * tiles.  Fills min(cap, *n_passes) entries; cap may be 0 to query the count. */
-lq_status lq_psr_pass_bytes(const lq_psr *plan, uint64_t *bytes_out, int32_t *kind_out, size_t cap,
-                            size_t *n_passes);
+ * tiles.  support_amps_out (may be NULL) receives the amplitudes per circuit
+ * the pass's gates act on: 2^n, or fewer for a pass that runs only the tiles
+ * inside its support (the others are provably zero); ops_out (may be NULL)
+ * the planner ops fused into the pass (fused gates, Pauli groups).
+ * Fills min(cap, *n_passes) entries; cap may be 0 to query the count. */
+lq_status lq_psr_pass_bytes(const lq_psr *plan, uint64_t *bytes_out, int32_t *kind_out, uint64_t *support_amps_out,
+                            uint32_t *ops_out, size_t cap, size_t *n_passes);
 
 /* ---- execution options (testing / measurement) -------------------------- */
 typedef enum {

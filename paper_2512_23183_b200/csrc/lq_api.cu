@@ -1946,14 +1946,22 @@ lq_status lq_psr_traffic(const lq_psr *P, uint64_t *tile_bytes_per_circuit, uint
     return LQ_OK;
 }
 
-lq_status lq_psr_pass_bytes(const lq_psr *P, uint64_t *bytes_out, int32_t *kind_out, size_t cap, size_t *n_passes) {
+lq_status lq_psr_pass_bytes(const lq_psr *P, uint64_t *bytes_out, int32_t *kind_out, uint64_t *support_amps_out,
+                            uint32_t *ops_out, size_t cap, size_t *n_passes) {
     if (!P) return fail(LQ_ERR_ARG, "invalid plan");
     const size_t np = P->plan.passes.size();
     if (n_passes) *n_passes = np;
     if (cap && (!bytes_out || !kind_out)) return fail(LQ_ERR_ARG, "output arrays are NULL");
+    const uint64_t N = 1ull << P->n;
     for (size_t i = 0; i < np && i < cap; i++) {
+        const PlanPass &p = P->plan.passes[i];
         bytes_out[i] = psr_pass_bytes(P, i);
-        kind_out[i] = (int32_t)P->plan.passes[i].kind;
+        kind_out[i] = (int32_t)p.kind;
+        if (support_amps_out) {   // amplitudes the pass's gates act on (the rest are provably zero)
+            const bool jit = p.kind == PASS_TILE && i < P->plan.jit.size() && P->plan.jit[i];
+            support_amps_out[i] = (jit && p.tiles_log2 >= 0) ? 1ull << (p.tiles_log2 + p.kp.K) : N;
+        }
+        if (ops_out) ops_out[i] = (uint32_t)p.n_ops;
     }
     return LQ_OK;
 }

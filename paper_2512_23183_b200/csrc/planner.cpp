@@ -846,10 +846,17 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
     // the FP64 budget trades an extra HBM round trip for less arithmetic per
     // pass; a state that is one tile has no HBM round trip to trade
     const int budget_all = nl > K ? opt.budget : 0;
+    // zero-first plans (PlanOptions::first_free): the support U = union of the
+    // tiles planned so far (lq_api.cu prepare() runs a pass only over the
+    // tiles inside U).  A pass with |U| <= free_upto is exempt from the
+    // budget.  Pass 0 (U empty: one tile per state) always; exempting pass 1
+    // too (|U| = K, at most 2^(K-3) tiles) measured 0.8 % slower on config 4
+    // (the extra ops it absorbs leave later passes no lighter), hence 0.
+    uint64_t U = 0;
+    bool track = opt.first_free;
+    const int free_upto = getenv("LQ_FREE_UPTO") ? atoi(getenv("LQ_FREE_UPTO")) : 0;   // A/B experiments
     while (!rem.empty()) {
-        // a pass that synthesises |0...0> (PlanOptions::first_free) does its
-        // arithmetic on one tile per state only: no budget
-        const int budget = (opt.first_free && plan.passes.empty()) ? 0 : budget_all;
+        const int budget = (track && popc(U) <= free_upto) ? 0 : budget_all;
         uint64_t Tm = mand;
         std::vector<int> absorbed, absorbed_w;
         first_fit(ops, rem, K, Tm, absorbed, budget);
@@ -914,6 +921,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
             pp.n_ops = (int)absorbed.size();
             plan.passes.push_back(pp);
             plan.n_diag++;
+            track = false;
         } else if (absorbed.size() == 1 && !has_expv && pair_kernel_op(ops[absorbed[0]].type) &&
                    (nl > K || popc(ops[absorbed[0]].full()) > K)) {
             PlanPass pp;
@@ -924,11 +932,13 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
             pp.n_ops = 1;
             plan.passes.push_back(pp);
             plan.n_pair++;
+            track = false;
         } else {
             // fill the tile to exactly K bits, lowest free bits first (longer
             // contiguous runs for coalescing)
             for (int b = 0; b < nl && popc(Tm) < K; b++) Tm |= bit(b);
             emit_tile(n, nl, K, Rr, Tm, ops, absorbed, mat_off, plan, mb);
+            U |= Tm;
         }
         // remove absorbed from rem (absorbed is a subsequence of rem)
         std::vector<int> left;

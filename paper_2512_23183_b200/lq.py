@@ -118,7 +118,8 @@ _SIGS = {
     "lq_sv_shard_ptr": ([_P, _i32], _P),
     "lq_dist_schedule_json": ([_i32, _i32, _GP, _sz, _i32, _TP, _sz, ctypes.c_char_p, _sz, ctypes.POINTER(_sz)], _i32),
     "lq_psr_traffic": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i32),
-    "lq_psr_pass_bytes": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_i32), ctypes.c_size_t,
+    "lq_psr_pass_bytes": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_i32), ctypes.POINTER(_u64),
+                           ctypes.POINTER(ctypes.c_uint32), ctypes.c_size_t,
                            ctypes.POINTER(ctypes.c_size_t)], _i32),
     "lq_jit_stats": ([ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_dbl)], _i32),
     "lq_jit_compile_check": ([_i32, _GP, _sz, _TP, _sz, ctypes.POINTER(_u64)], _i32),
@@ -396,12 +397,16 @@ def lq_psr_cache_clear() -> None:
     _chk(_lib.lq_psr_cache_clear())
 
 
-def lq_psr_pass_bytes(plan) -> List[Tuple[int, int]]:
-    """[(kind, algorithmic HBM bytes per circuit)] per launched pass (0 tile, 1 pair, 2 diagonal)"""
+def lq_psr_pass_bytes(plan, with_support: bool = False):
+    """[(kind, algorithmic HBM bytes per circuit)] per launched pass (0 tile, 1 pair, 2 diagonal);
+    with_support: [(kind, bytes, amplitudes per circuit the pass's gates act on, planner ops in the pass)]"""
     n = ctypes.c_size_t()
-    _chk(_lib.lq_psr_pass_bytes(plan, None, None, 0, ctypes.byref(n)))
-    b, k = (_u64 * max(n.value, 1))(), (_i32 * max(n.value, 1))()
-    _chk(_lib.lq_psr_pass_bytes(plan, b, k, n.value, ctypes.byref(n)))
+    _chk(_lib.lq_psr_pass_bytes(plan, None, None, None, None, 0, ctypes.byref(n)))
+    m = max(n.value, 1)
+    b, k, a, o = (_u64 * m)(), (_i32 * m)(), (_u64 * m)(), (ctypes.c_uint32 * m)()
+    _chk(_lib.lq_psr_pass_bytes(plan, b, k, a, o, n.value, ctypes.byref(n)))
+    if with_support:
+        return [(k[i], b[i], a[i], o[i]) for i in range(n.value)]
     return [(k[i], b[i]) for i in range(n.value)]
 
 

@@ -462,6 +462,50 @@ def test_psr_zero_first_support_restriction(lq, oracle, first_free, monkeypatch)
     assert abs(e1 - oracle.energy(n, gates, theta, terms)) <= 1e-10 * max(abs(e1), 1)
 
 
+@pytest.mark.parametrize("wide", [False, True])
+def test_psr_support_tracking_untouched_qubits(lq, oracle, wide, monkeypatch):
+    """Support tracking when the ansatz never touches qubits 15..19: the
+    union of tiles may never cover every bit, the Pauli-group passes then read
+    through the support mask, and a group whose x mask is wider than a tile
+    (read by the direct kernel from HBM) must switch the tracking off.  Bit
+    for bit equal to the untracked run, and equal to the oracle."""
+    import torch
+    n = 20
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 11)
+    gates = W.hea_ansatz(15, 2, "ring")
+    npar = 60
+    theta = np.random.default_rng(15).uniform(0, 2 * np.pi, npar)
+    terms = W.xyz_terms(n) + [(0.5, (1 << 19) | 1, 0), (0.25, 0, (1 << 19) | (1 << 3))]
+    if wide:
+        terms.append((0.125, (1 << 12) - 1, 0b101))   # x over 12 bits: a direct group
+    st = torch.cuda.current_stream()
+    th = torch.tensor(theta, device="cuda")
+
+    def run():
+        P = lq.lq_psr_create(n, gates, npar, terms, stream=st)
+        g = torch.zeros(npar, dtype=torch.float64, device="cuda")
+        e = torch.zeros(1, dtype=torch.float64, device="cuda")
+        lq.lq_psr_run(P, th.data_ptr(), g.data_ptr(), e.data_ptr())
+        torch.cuda.synchronize()
+        pb = lq.lq_psr_pass_bytes(P)
+        lq.lq_psr_free(P)
+        return g.cpu().numpy(), e.item(), pb
+
+    g1, e1, pb1 = run()
+    monkeypatch.setenv("LQ_NO_SUPPORT", "1")
+    g0, e0, pb0 = run()
+    monkeypatch.delenv("LQ_NO_SUPPORT")
+    assert np.array_equal(g1, g0) and e1 == e0
+    # (with the wide group the tracking stays on only if the tiles end up
+    # covering every bit; either way the results must agree)
+    if not wide:
+        assert sum(b for _, b in pb1) < sum(b for _, b in pb0)
+    go = oracle.param_shift_grad(n, gates, theta, terms, threads=8)
+    grad_close(g1, go)
+    eo = oracle.energy(n, gates, theta, terms)
+    assert abs(e1 - eo) <= 1e-10 * max(abs(eo), 1)
+
+
 def test_config4_full_size_closed_forms(lq):
     """n=24 (configs[3] size): theta = 0 gives E = 0.4*23 + 0.3*24 = 16.4
     exactly; the product ansatz has a closed-form energy and gradient."""

@@ -1,5 +1,5 @@
 """Summarise an ncu --set full report of the tile-pass launches of one
-config-4 batch (2 circuits per launch) into profiles/ncu_k_tile_summary.json:
+config-4 batch (B circuits per launch) into profiles/ncu_k_tile_summary.json:
 per launch dram read+write bytes vs the algorithmic bytes of that pass."""
 import csv, io, json, os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -17,20 +17,18 @@ def val(r, k):
     u = units[col[k]]
     return x * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1, "ns": 1e-3, "us": 1, "ms": 1e3}.get(u, 1)
 import workloads as W
-from paper_2512_23183_b200 import lq
 w = W.config4()
-plan = lq.lq_plan_export_json(w.n, w.gates, w.terms)
-N = 1 << w.n
 B = int(os.environ.get("LQ_SUMMARY_B", "4"))   # circuits per launch in the capture (lq_psr_create's batch)
-passes = plan["passes"]
+# algorithmic bytes per pass of the captured plan, written on the GPU box by
+# tools/prof_cfg4.py (lq_psr_pass_bytes: support tracking, write-only first
+# pass, read-only and final passes)
+pb = json.load(open(os.environ.get("LQ_PASS_BYTES", "gpurun_out/cfg4_pass_bytes.json")))
+passes = [p for p in pb["passes"] if p["kind"] == 0]
 launches = []
 for i, r in enumerate(data):
     if i >= len(passes):
         break
-    p = passes[i]
-    load = i > 0
-    store = not (p["flags"] & 4) and i + 1 < len(passes)
-    alg = B * N * 16 * (int(load) + int(store))
+    alg = B * passes[i]["bytes_per_circuit"]
     dr, dw = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
     launches.append({"pass": i, "us": round(val(r, "gpu__time_duration.sum"), 2), "dram_read": dr, "dram_write": dw,
                      "alg_bytes": alg, "traffic_over_alg": round((dr + dw) / alg, 4),

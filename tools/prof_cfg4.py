@@ -11,3 +11,10 @@ npar = layers * 2 * w.n
 g, e = lq.lq_param_shift_grad(w.n, gates, w.theta[:npar], w.terms)
 torch.cuda.synchronize()
 print("E", e, "launches", lq.lq_launch_count())
+# per-pass algorithmic bytes of the same plan (tools/ncu_summary.py)
+import json
+P = lq.lq_psr_create(w.n, gates, npar, w.terms, stream=torch.cuda.current_stream())
+os.makedirs("gpurun_out", exist_ok=True)
+json.dump({"n": w.n, "passes": [{"kind": k, "bytes_per_circuit": b} for k, b in lq.lq_psr_pass_bytes(P)]},
+          open("gpurun_out/cfg4_pass_bytes.json", "w"))
+lq.lq_psr_free(P)
