@@ -442,6 +442,9 @@ def test_psr_zero_first_support_restriction(lq, oracle, first_free, monkeypatch)
         return g.cpu().numpy(), e.item(), pb
 
     g1, e1, pb1 = run()
+    for _ in range(3):   # shared-memory races in the zero-slot synthesis would show as run-to-run noise
+        g2, e2, _ = run()
+        assert np.array_equal(g2, g1) and e2 == e1
     monkeypatch.setenv("LQ_NO_SUPPORT", "1")
     g0, e0, pb0 = run()
     monkeypatch.delenv("LQ_NO_SUPPORT")

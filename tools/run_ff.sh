@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$? >> gpurun_out/gpu_tests.log
-tail -2 gpurun_out/gpu_tests.log
-timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
-tail -1 gpurun_out/bench.json | cut -c1-200
+for tool in memcheck racecheck synccheck; do
+timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_probe.py > gpurun_out/san_$tool.log 2>&1; echo $tool=$?
+tail -3 gpurun_out/san_$tool.log
+done
