@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-for tool in memcheck racecheck synccheck; do
-timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize_probe.py > gpurun_out/san_$tool.log 2>&1; echo $tool=$?
-tail -3 gpurun_out/san_$tool.log
+for b in 4 8 2 16 4; do
+LQ_PSR_BATCH=$b KS=11 timeout 600 python tools/sb_probe.py cfg4 2>&1 | grep -E "probe|rror" | sed "s/^/B=$b /"
 done
