@@ -8,6 +8,7 @@ from paper_2512_23183_b200 import lq
 st = torch.cuda.current_stream()
 tag = "probe"
 if "FF" in os.environ: lq.lq_set_option(lq.LQ_OPT_FIRST_PASS_FREE, int(os.environ["FF"]))
+if "RB" in os.environ: lq.lq_set_option(lq.LQ_OPT_REG_BITS, int(os.environ["RB"]))
 if "BUDGET" in os.environ: lq.lq_set_option(lq.LQ_OPT_PASS_BUDGET, int(os.environ["BUDGET"]))
 def timed(fn, R=3):
     fn(); torch.cuda.synchronize()
