@@ -1294,38 +1294,52 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
             if constexpr (!LATE) __syncthreads();
             continue;
         }
-        double2 a[NV];
-        if (zero) xread_c<RR, D, D::SM[0], D::PERM[0], true>(b, a, t, tb, P.gofs);
-        else xread_c<RR, D, D::SM[0], D::PERM[0], false, D::RADD[0]>(b, a, t, tb, P.gofs);
-        TState ts;
-        ts.reset();
-        ts.lpos = P.lpos;
-        ts.cbase = (uint32_t)circ * D::SMAT;
-        run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, P.gofs, t, s_tab, s_et, P.n, zero);
-        double2 *psi = state + (uint64_t)circ * state_stride;
-        if (P.flags & PF_EXPV)     // deterministic partials: one per warp of the tile
-            expv_partial(ts.eacc, reinterpret_cast<double *>(b), partials + (uint64_t)circ * slot_stride + P.eslot,
-                         g & tmask);
-        if (P.flags & PF_NO_STORE) {
-            if constexpr (!LATE) __syncthreads();
-            continue;
+        // CIRC: the launch's circuit index as a compile-time value (D::NCIRC
+        // copies of the body, chosen by a CTA-uniform branch), so the op-table
+        // offsets fold into immediate constant-bank operands; -1: runtime
+        auto body = [&](auto CV) {
+            constexpr int CIRC = decltype(CV)::value;
+            double2 a[NV];
+            if (zero) xread_c<RR, D, D::SM[0], D::PERM[0], true>(b, a, t, tb, P.gofs);
+            else xread_c<RR, D, D::SM[0], D::PERM[0], false, D::RADD[0]>(b, a, t, tb, P.gofs);
+            TState ts;
+            ts.reset();
+            ts.lpos = P.lpos;
+            ts.cbase = CIRC >= 0 ? (uint32_t)CIRC * D::SMAT : (uint32_t)circ * D::SMAT;
+            run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, P.gofs, t, s_tab, s_et, P.n, zero);
+            double2 *psi = state + (uint64_t)circ * state_stride;
+            if (P.flags & PF_EXPV)     // deterministic partials: one per warp of the tile
+                expv_partial(ts.eacc, reinterpret_cast<double *>(b), partials + (uint64_t)circ * slot_stride + P.eslot,
+                             g & tmask);
+            if (P.flags & PF_NO_STORE) {
+                if constexpr (!LATE) __syncthreads();
+                return;
+            }
+            materialize<RR>(a, ts, true);
+            constexpr bool need_x = D::SSTORE != D::SM[LAST] || D::STORE_PERM >= 0;
+            bool ex = need_x;
+            if constexpr (!need_x) ex = __syncthreads_or(ts.fb != 0);
+            if (ex) {
+                if constexpr (need_x && !D::WSAFE[LAST]) __syncthreads();
+                xwrite_c<RR, D, D::SM[LAST], D::ADD_S>(b, a, t, ts.fb);
+                __syncthreads();
+                xread_c<RR, D, D::SSTORE, D::STORE_PERM, false, D::ADD_S>(b, a, t, tb, P.gofs);
+            }
+            const uint64_t gst = tb | D::dep(ins_zeros<D::SSTORE, K>(t));
+            Unroll<RR>::run([&](auto V) {
+                constexpr uint64_t go = D::dep(loff_c<D::SSTORE>(decltype(V)::value));
+                psi[gst + go] = a[decltype(V)::value];
+            });
+            if constexpr (!LATE) __syncthreads();   // buffer b is refilled by the next iteration's prefetch
+        };
+        if constexpr (D::CTAB && D::NCIRC >= 1 && D::NCIRC <= 4) {
+            if (D::NCIRC == 1 || circ == 0) body(IC<0>());
+            else if (D::NCIRC == 2 || circ == 1) body(IC<(D::NCIRC > 1 ? 1 : 0)>());
+            else if (D::NCIRC == 3 || circ == 2) body(IC<(D::NCIRC > 2 ? 2 : 0)>());
+            else body(IC<(D::NCIRC > 3 ? 3 : 0)>());
+        } else {
+            body(IC<-1>());
         }
-        materialize<RR>(a, ts, true);
-        constexpr bool need_x = D::SSTORE != D::SM[LAST] || D::STORE_PERM >= 0;
-        bool ex = need_x;
-        if constexpr (!need_x) ex = __syncthreads_or(ts.fb != 0);
-        if (ex) {
-            if constexpr (need_x && !D::WSAFE[LAST]) __syncthreads();
-            xwrite_c<RR, D, D::SM[LAST], D::ADD_S>(b, a, t, ts.fb);
-            __syncthreads();
-            xread_c<RR, D, D::SSTORE, D::STORE_PERM, false, D::ADD_S>(b, a, t, tb, P.gofs);
-        }
-        const uint64_t gst = tb | D::dep(ins_zeros<D::SSTORE, K>(t));
-        Unroll<RR>::run([&](auto V) {
-            constexpr uint64_t go = D::dep(loff_c<D::SSTORE>(decltype(V)::value));
-            psi[gst + go] = a[decltype(V)::value];
-        });
-        if constexpr (!LATE) __syncthreads();   // buffer b is refilled by the next iteration's prefetch
     }
 }
 
