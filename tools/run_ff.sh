@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-for b in 4 2 3 4; do
-LQ_PSR_BATCH=$b KS=11 timeout 900 python tools/sb_probe.py cfg4 2>&1 | grep -E "probe|rror" | sed "s/^/B=$b /"
-done
+timeout 900 python tools/small_configs.py > gpurun_out/small_configs.jsonl 2> gpurun_out/small_configs.err; echo small=$?
+cat gpurun_out/small_configs.jsonl | cut -c1-200
