@@ -509,6 +509,34 @@ def test_psr_support_tracking_untouched_qubits(lq, oracle, wide, monkeypatch):
     assert abs(e1 - eo) <= 1e-10 * max(abs(eo), 1)
 
 
+def test_psr_compile_time_circuit_index(lq, monkeypatch):
+    """Launches of B <= 4 circuits compile one tile-body copy per circuit
+    (the op-table offset as a constant).  B = 3 over 241 circuits (last batch:
+    one circuit), B = 4, and the runtime-index build must agree bit for bit
+    (each circuit's arithmetic and its fixed-order sums do not depend on B)."""
+    n = 20
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 11)
+    gates = W.hea_ansatz(n, 3, "ring")
+    npar = 6 * n
+    theta = np.random.default_rng(7).uniform(0, 2 * np.pi, npar)
+    terms = W.xyz_terms(n)
+    out = []
+    for env in ({"LQ_PSR_BATCH": "3"}, {"LQ_PSR_BATCH": "4"}, {"LQ_PSR_BATCH": "3", "LQ_JIT_RUNTIME_CIRC": "1"},
+                {}):
+        for k in ("LQ_PSR_BATCH", "LQ_JIT_RUNTIME_CIRC"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        lq.lq_psr_cache_clear()
+        out.append(lq.lq_param_shift_grad(n, gates, theta, terms))
+    for k in ("LQ_PSR_BATCH", "LQ_JIT_RUNTIME_CIRC"):
+        monkeypatch.delenv(k, raising=False)
+    lq.lq_psr_cache_clear()
+    g0, e0 = out[0]
+    for g, e in out[1:]:
+        assert np.array_equal(g, g0) and e == e0
+
+
 def test_config4_full_size_closed_forms(lq):
     """n=24 (configs[3] size): theta = 0 gives E = 0.4*23 + 0.3*24 = 16.4
     exactly; the product ansatz has a closed-form energy and gradient."""

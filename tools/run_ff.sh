@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python tools/small_configs.py > gpurun_out/small_configs.jsonl 2> gpurun_out/small_configs.err; echo small=$?
-cat gpurun_out/small_configs.jsonl | cut -c1-200
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "compile_time_circuit or support" 2>&1 | tail -3
