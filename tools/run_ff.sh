@@ -1,2 +1,7 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "compile_time_circuit or support" 2>&1 | tail -3
+KS=11 timeout 900 python tools/sb_probe.py cfg4 2>&1 | grep -E "probe|rror" | sed "s/^/base /"
+LQ_JIT_EXTRA_OPTS=-extra-device-vectorization KS=11 timeout 900 python tools/sb_probe.py cfg4 2>&1 | grep -E "probe|rror" | sed "s/^/edv /"
+LQ_JIT_EXTRA_OPTS=--maxrregcount=160 KS=11 timeout 900 python tools/sb_probe.py cfg4 2>&1 | grep -E "probe|rror" | sed "s/^/r160 /"
+LQ_JIT_EXTRA_OPTS=-Xptxas=-O2 KS=11 timeout 900 python tools/sb_probe.py cfg4 2>&1 | grep -E "probe|rror" | sed "s/^/O2 /"
+LQ_JIT_EXTRA_OPTS=--ftz=true KS=11 timeout 900 python tools/sb_probe.py cfg4 2>&1 | grep -E "probe|rror" | sed "s/^/ftz /"
+KS=11 timeout 900 python tools/sb_probe.py cfg4 2>&1 | grep -E "probe|rror" | sed "s/^/base /"
