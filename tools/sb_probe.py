@@ -9,6 +9,7 @@ st = torch.cuda.current_stream()
 tag = "probe"
 if "FF" in os.environ: lq.lq_set_option(lq.LQ_OPT_FIRST_PASS_FREE, int(os.environ["FF"]))
 if "RB" in os.environ: lq.lq_set_option(lq.LQ_OPT_REG_BITS, int(os.environ["RB"]))
+if "CO" in os.environ: lq.lq_set_option(lq.LQ_OPT_COALESCE_BITS, int(os.environ["CO"]))
 if "BUDGET" in os.environ: lq.lq_set_option(lq.LQ_OPT_PASS_BUDGET, int(os.environ["BUDGET"]))
 def timed(fn, R=3):
     fn(); torch.cuda.synchronize()
