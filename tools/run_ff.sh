@@ -1,4 +1,5 @@
+# A/B and check scratch script (edited per experiment)
 mkdir -p gpurun_out
-for co in 3 4 3; do
-CO=$co KS=11 timeout 900 python tools/sb_probe.py cfg4 2>&1 | grep -E "probe|rror" | sed "s/^/co=$co /"
-done
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$? >> gpurun_out/gpu_tests.log
+tail -2 gpurun_out/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
