@@ -250,7 +250,11 @@ lq_status lq_psr_cache_clear(void);
 
 /* Same computation split into a reusable plan and an asynchronous run on
  * DEVICE pointers (theta_dev: n_params doubles; grad_dev: n_params doubles;
- * energy_dev: 1 double or NULL).  lq_psr_run does not sync. */
+ * energy_dev: 1 double or NULL).  lq_psr_run does not sync.  Every circuit
+ * starts from |0...0>: the first tile pass synthesises it,
+ * and while the tiles run so far leave some qubits untouched the state is zero
+ * outside their union, so passes read and run only inside it (support
+ * tracking; results are bit-identical to full passes, lq_psr_pass_bytes). */
 lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, size_t n_params,
                         const lq_pauli_term *terms, size_t n_terms, int shard_rank,
                         int shard_world, void *cuda_stream, lq_psr **out);
