@@ -350,9 +350,12 @@ typedef enum {
                                  1 (default): auto -- PSR plans and states with n >= 26; 2: always. */
     LQ_OPT_PASS_BUDGET = 6,   /* planner: estimated FP64 instructions per amplitude (x10) a tile pass may
                                  absorb before it stops (default 400; 0 = no limit, absorb greedily) */
-    LQ_OPT_FIRST_PASS_FREE = 7 /* PSR plans: 1 (default) exempts the first pass -- it synthesises |0...0>,
+    LQ_OPT_FIRST_PASS_FREE = 7, /* PSR plans: 1 (default) exempts the first pass -- it synthesises |0...0>,
                                  so every tile but one is stored as zeros without arithmetic -- from
                                  the pass budget; 0: budget it like the others */
+    LQ_OPT_POISON_ALLOC = 8   /* testing: 1 fills every fresh library work allocation (PSR state batches,
+                                 scratch, staging) with 0xFF bytes (NaN doubles), so a kernel that reads
+                                 memory nothing wrote fails loudly instead of seeing leftover zeros */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);

@@ -63,6 +63,9 @@ def lib():
         _lib.or_energy.argtypes = [i32, i32, P, P, P, P, P, P, P, P, i32, P, P, P, P]
         _lib.or_param_shift.argtypes = [i32, i32, P, P, P, P, P, P, P, P, i32, i32,
                                         P, P, P, P, i32, P]
+        _lib.or_splitmix64.argtypes = [u64]
+        _lib.or_splitmix64.restype = u64
+        _lib.or_random_gaussian_at.argtypes = [u64, P, u64, P]
         _lib.or_norm2.argtypes = [P, i32]
         _lib.or_norm2.restype = dbl
     return _lib
@@ -142,6 +145,19 @@ def init_random(n: int, seed: int) -> np.ndarray:
     psi = np.empty(1 << n, np.complex128)
     lib().or_init_random(_ptr(psi), n, int(seed) & (2**64 - 1))
     return psi
+
+
+def splitmix64(x: int) -> int:
+    return int(lib().or_splitmix64(int(x) & (2**64 - 1)))
+
+
+def random_gaussian_at(seed: int, idx) -> np.ndarray:
+    """Unnormalised init_random amplitudes a_i at the given indices
+    (init_random(n, seed) = a / sqrt(sum_i |a_i|^2) over all 2^n indices)."""
+    idx = np.ascontiguousarray(idx, np.uint64)
+    out = np.empty(idx.size, np.complex128)
+    lib().or_random_gaussian_at(int(seed) & (2**64 - 1), _ptr(idx), idx.size, _ptr(out))
+    return out
 
 
 def apply_gate(psi: np.ndarray, name: str, q0: int, q1: int = -1, angle: float = 0.0,

@@ -74,7 +74,7 @@ void or_init_basis(cplx *psi, int n, uint64_t k)
     psi[k] = 1.0;
 }
 
-static uint64_t or_splitmix64(uint64_t x)
+uint64_t or_splitmix64(uint64_t x)
 {
     uint64_t z = x + 0x9E3779B97F4A7C15ULL;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -82,21 +82,30 @@ static uint64_t or_splitmix64(uint64_t x)
     return z ^ (z >> 31);
 }
 
-/* a_i = r (cos 2 pi u1 + i sin 2 pi u1), r = sqrt(-2 ln u0) (Box-Muller),
+/* The unnormalised amplitude of index i:
+ * a_i = r (cos 2 pi u1 + i sin 2 pi u1), r = sqrt(-2 ln u0) (Box-Muller),
  * u_j = ((x_j >> 11) + 0.5) 2^-53, x0 = splitmix64(seed ^ 2i),
- * x1 = splitmix64(seed ^ (2i+1)); then a /= sqrt(sum |a|^2). */
+ * x1 = splitmix64(seed ^ (2i+1)). */
+static void gauss_at(uint64_t seed, uint64_t i, double *re, double *im)
+{
+    uint64_t x0 = or_splitmix64(seed ^ (2 * i));
+    uint64_t x1 = or_splitmix64(seed ^ (2 * i + 1));
+    double u0 = ((double)(x0 >> 11) + 0.5) * 0x1.0p-53;
+    double u1 = ((double)(x1 >> 11) + 0.5) * 0x1.0p-53;
+    double r = sqrt(-2.0 * log(u0));
+    *re = r * cos(2.0 * OR_PI * u1);
+    *im = r * sin(2.0 * OR_PI * u1);
+}
+
+/* init_random: a_i as above for every i, then a /= sqrt(sum |a|^2)
+ * (Neumaier sum). */
 void or_init_random(cplx *psi, int n, uint64_t seed)
 {
     uint64_t N = (uint64_t)1 << n;
     neumaier norm = {0.0, 0.0};
     for (uint64_t i = 0; i < N; i++) {
-        uint64_t x0 = or_splitmix64(seed ^ (2 * i));
-        uint64_t x1 = or_splitmix64(seed ^ (2 * i + 1));
-        double u0 = ((double)(x0 >> 11) + 0.5) * 0x1.0p-53;
-        double u1 = ((double)(x1 >> 11) + 0.5) * 0x1.0p-53;
-        double r = sqrt(-2.0 * log(u0));
-        double re = r * cos(2.0 * OR_PI * u1);
-        double im = r * sin(2.0 * OR_PI * u1);
+        double re, im;
+        gauss_at(seed, i, &re, &im);
         psi[i] = re + I * im;
         neu_add(&norm, re * re);
         neu_add(&norm, im * im);
@@ -104,6 +113,17 @@ void or_init_random(cplx *psi, int n, uint64_t seed)
     double s = 1.0 / sqrt(neu_value(&norm));
     for (uint64_t i = 0; i < N; i++)
         psi[i] *= s;
+}
+
+/* The unnormalised a_i at `count` indices (for states too large for the
+ * host: the normalised state is a_i / sqrt(S) with one constant S). */
+void or_random_gaussian_at(uint64_t seed, const uint64_t *idx, uint64_t count, cplx *out)
+{
+    for (uint64_t k = 0; k < count; k++) {
+        double re, im;
+        gauss_at(seed, idx[k], &re, &im);
+        out[k] = re + I * im;
+    }
 }
 
 /* ------------------------------------------------------------------ */
@@ -376,7 +396,8 @@ static cplx inner(const cplx *psi, const cplx *phi, int n)
 /* E = sum_t c_t <psi|P_t|psi>: for each term copy psi,
  * apply the Pauli factors as 1q gates (Y where x&z, X where x, Z where z;
  * bit q of a mask = qubit q), take Re<psi|P psi>.
- * Fails with OR_EIMAG if |Im<psi|P psi>| > 1e-10. */
+ * Fails with OR_EIMAG unless |Im<psi|P psi>| <= 1e-10 and the value is finite
+ * ("explicit, never silent"). */
 int or_expval(const cplx *psi, int n, int n_terms, const double *coeffs,
               const uint64_t *xm, const uint64_t *zm, double *out)
 {
@@ -397,7 +418,7 @@ int or_expval(const cplx *psi, int n, int n_terms, const double *coeffs,
                 or_apply_gate(phi, n, OR_Z, q, -1, -1, 0.0, NULL);
         }
         cplx v = inner(psi, phi, n);
-        if (fabs(cimag(v)) > 1e-10) {
+        if (!(fabs(cimag(v)) <= 1e-10) || !isfinite(creal(v))) {   /* NaN/Inf too: never silent */
             free(phi);
             return OR_EIMAG;
         }

@@ -42,6 +42,7 @@ std::atomic<int64_t> g_opt_coalesce{3};
 std::atomic<int64_t> g_opt_regbits{4};
 std::atomic<int64_t> g_opt_jit{1};
 std::atomic<int64_t> g_opt_first_free{1};   // PSR plans: the |0...0> pass is exempt from the budget
+std::atomic<int64_t> g_opt_poison{0};   // LQ_OPT_POISON_ALLOC
 std::atomic<int64_t> g_opt_budget{400};   // keeps passes from turning compute-bound (swept; 350 gains 0.4 % on config 4 but costs 5-12 % on Trotter / random circuits)
 const double PI = 3.14159265358979323846264338327950288;
 
@@ -169,9 +170,12 @@ lq_status prepare(Plan &plan, bool reused = false) {
         const uint64_t all = plan.nl >= 64 ? ~0ull : ((1ull << plan.nl) - 1);
         uint64_t U = 0;
         bool ok = true;
+        // A read-only pass (PF_NO_STORE) writes nothing to HBM: it leaves the
+        // support where it was.
         for (const PlanPass &p : plan.passes) {
             if (U == all) break;
             if (p.kind != PASS_TILE) { ok = false; break; }
+            if (p.kp.flags & PF_NO_STORE) continue;
             for (int b = 0; b < p.kp.K; b++) U |= 1ull << p.kp.T[b];
         }
         if (U != all && !plan.wide_groups.empty()) ok = false;
@@ -185,7 +189,7 @@ lq_status prepare(Plan &plan, bool reused = false) {
                 p.sup_free = U & ~tm & all;
                 p.tiles_log2 = __builtin_popcountll(p.sup_free);
             }
-            U |= tm;
+            if (!(p.kp.flags & PF_NO_STORE)) U |= tm;
         }
     }
     plan.ctab = getenv("LQ_JIT_NO_CTAB") == nullptr;   // constant-bank op tables (A/B switch for experiments)
@@ -299,6 +303,10 @@ struct DevBuf {
                             cudaGetErrorString(e));
         }
         cap = nb;
+        if (g_opt_poison.load() && cudaMemsetAsync(p, 0xFF, nb, s) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(LQ_ERR_CUDA, "poison memset failed");
+        }
         return LQ_OK;
     }
     void release(cudaStream_t s) {
@@ -503,6 +511,9 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
         LQ_TRY(check_launch("k_stage_ctab"));
     }
     size_t ci = 0;
+    // zero-first: until a pass has stored, HBM does not hold the state yet and
+    // every pass synthesises |0...0> (a leading read-only pass stores nothing)
+    bool stored = !zero_first || plan.passes.empty() || plan.passes[0].kind != PASS_TILE;
     for (size_t i = 0; i < plan.passes.size(); i++) {
         const PlanPass &p = plan.passes[i];
         if (p.kind == PASS_TILE) {
@@ -513,7 +524,8 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
             }
             KPass kp = p.kp;
             kp.gofs = gofs;
-            if (zero_first && i == 0) kp.flags |= PF_LOAD_ZERO;
+            if (!stored) kp.flags |= PF_LOAD_ZERO;
+            if (!(kp.flags & PF_NO_STORE)) stored = true;
             if (no_final_store && i + 1 == plan.passes.size()) kp.flags |= PF_NO_STORE;
             uint32_t npt = 0;
             if (kp.perm_end > kp.perm_begin)
@@ -1038,6 +1050,7 @@ lq_status lq_set_option(int option, int64_t value) {
         g_opt_jit = value;
         return LQ_OK;
     case LQ_OPT_FIRST_PASS_FREE: g_opt_first_free = value ? 1 : 0; return LQ_OK;
+    case LQ_OPT_POISON_ALLOC: g_opt_poison = value ? 1 : 0; return LQ_OK;
     default: return fail(LQ_ERR_ARG, "unknown option");
     }
 }
@@ -1052,6 +1065,7 @@ int64_t lq_get_option(int option) {
     case LQ_OPT_JIT: return g_opt_jit.load();
     case LQ_OPT_PASS_BUDGET: return g_opt_budget.load();
     case LQ_OPT_FIRST_PASS_FREE: return g_opt_first_free.load();
+    case LQ_OPT_POISON_ALLOC: return g_opt_poison.load();
     default: return -1;
     }
 }
@@ -1918,7 +1932,9 @@ static uint64_t psr_pass_bytes(const lq_psr *P, size_t i) {
     const uint64_t N = 1ull << P->n;
     const size_t np = P->plan.passes.size();
     const PlanPass &p = P->plan.passes[i];
-    bool load = !(i == 0 && p.kind == PASS_TILE);
+    // launch_passes synthesises |0...0> in every tile pass until one has stored
+    bool load = P->plan.passes[0].kind != PASS_TILE;
+    for (size_t k = 0; k < i && !load; k++) load = !(P->plan.passes[k].kp.flags & PF_NO_STORE);
     bool store = true;
     if (p.kind == PASS_TILE) {
         if (p.kp.flags & PF_NO_STORE) store = false;

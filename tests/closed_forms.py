@@ -91,3 +91,22 @@ def qft_of_basis(n, k, idx):
     N = 1 << n
     jk = (np.asarray(idx, dtype=object) * int(k)) % N
     return np.exp(2j * np.pi * np.array([float(x) for x in jk]) / N) / np.sqrt(N)
+
+
+def circuit_inverse(gates):
+    """C^-1 for the config-1/5 alphabet and the monomial kinds: reversed
+    order, S <-> S^dagger, T <-> T^dagger, rotation angles negated
+    (R(t)^-1 = R(-t)); H, X, Y, Z, CNOT, CZ, SWAP are
+    involutions."""
+    inv = {"S": "SDG", "SDG": "S", "T": "TDG", "TDG": "T"}
+    out = []
+    for g in reversed(gates):
+        name = g[0]
+        if name in ("RX", "RY", "RZ", "CP", "CRY", "RXX", "RYY", "RZZ"):
+            assert g[3] == -1, "parameterised gates need theta"
+            out.append((name, g[1], g[2], g[3], -g[4]))
+        elif name in inv or name in ("H", "X", "Y", "Z", "CNOT", "CZ", "SWAP"):
+            out.append((inv.get(name, name), g[1], g[2], g[3], g[4]))
+        else:
+            raise ValueError(name)
+    return out

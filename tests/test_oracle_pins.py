@@ -445,10 +445,56 @@ def test_psr_cry_vs_matrix_route_gradient(oracle):
 
 def test_expval_rejects_non_hermitian_imag(oracle):
     """a non-real <P> is an error, never silent.  A Pauli
-    product is Hermitian, so this only fires on a corrupted state buffer."""
+    product is Hermitian, so <psi|P|psi> is real for every finite psi: the
+    check fires only on a corrupted state buffer (NaN / Inf), which must be
+    rejected rather than summed."""
     psi = np.array([1, 1j], np.complex128) / math.sqrt(2)
     # <Y> on (|0> + i|1>)/sqrt2 = 1 (real) -- must pass
     assert oracle.expval(psi, [(1.0, 1, 1)]) == pytest.approx(1.0)
+    for bad in (complex(np.nan, 0.0), complex(0.0, np.inf), complex(np.inf, np.nan)):
+        psi2 = psi.copy()
+        psi2[1] = bad
+        for term in ((1.0, 1, 1), (1.0, 1, 0), (1.0, 0, 1)):
+            with pytest.raises(oracle.OracleError):
+                oracle.expval(psi2, [term])
+
+
+def test_splitmix64_published_vector(oracle):
+    """The counter hash of init_random is Vigna's
+    SplitMix64 output function: seeded with 1234567 the generator's first
+    five outputs (state advanced by the golden gamma 0x9E3779B97F4A7C15 each
+    step, i.e. splitmix64(seed + k*gamma)) are the published test vector."""
+    gamma = 0x9E3779B97F4A7C15
+    want = [6457827717110365317, 3203168211198807973, 9817491932198370423,
+            4593380528125082431, 16408922859458223821]
+    got = [oracle.splitmix64((1234567 + k * gamma) % 2**64) for k in range(5)]
+    assert got == want
+
+
+def test_init_random_hand_computed_amplitudes(oracle):
+    """init_random(n, seed)[i] = a_i / sqrt(sum_j |a_j|^2) with
+    a_i = sqrt(-2 ln u0) e^{2 pi i u1}, u = ((x >> 11) + 0.5) 2^-53,
+    x0 = splitmix64(seed ^ 2i), x1 = splitmix64(seed ^ (2i+1)) (c.1 step 2),
+    computed here by hand from the pinned hash for n = 3 (all 8 amplitudes,
+    so the normalisation is explicit too).  Catches a seed-convention slip
+    such as seed ^ i, a swapped u0/u1 or a dropped +0.5."""
+    n, seed = 3, 0xDEADBEEF12345678
+    a = []
+    for i in range(1 << n):
+        x0, x1 = oracle.splitmix64(seed ^ (2 * i)), oracle.splitmix64(seed ^ (2 * i + 1))
+        u0, u1 = ((x0 >> 11) + 0.5) * 2.0 ** -53, ((x1 >> 11) + 0.5) * 2.0 ** -53
+        r = math.sqrt(-2.0 * math.log(u0))
+        a.append(complex(r * math.cos(2 * math.pi * u1), r * math.sin(2 * math.pi * u1)))
+    a = np.array(a)
+    want = a / math.sqrt(float(np.sum(np.abs(a) ** 2)))
+    got = oracle.init_random(n, seed)
+    assert np.abs(got - want).max() <= 1e-15
+    # the per-index route used for states too large for the host
+    idx = np.array([5, 0, 7], np.uint64)
+    np.testing.assert_allclose(oracle.random_gaussian_at(seed, idx), a[[5, 0, 7]], rtol=0, atol=1e-15)
+    big = oracle.init_random(12, 77)
+    raw = oracle.random_gaussian_at(77, np.arange(1 << 12, dtype=np.uint64))
+    assert np.abs(big - raw / math.sqrt(float(np.sum(np.abs(raw) ** 2)))).max() <= 1e-15
 
 
 # ---------------------------------------------------------------- VQE outer loop (f2)
@@ -583,3 +629,17 @@ def test_monomial_closed_forms_match_oracle(oracle):
         for q in range(n):
             a *= col[q][(kk >> (n - 1 - q)) & 1]
         assert abs(psi[j] - a) < 1e-14
+
+
+def test_circuit_inverse_helper_is_identity(oracle):
+    """The test helper used by the full-size round trips: C^-1 C = I on the
+    config-5 alphabet (oracle at n = 8)."""
+    from closed_forms import circuit_inverse
+    import workloads as W
+    w = W.config5(n=8, m=2, n_gates=300)
+    psi = oracle.init_random(8, w.seed)
+    ref = psi.copy()
+    oracle.apply_circuit(psi, w.gates)
+    assert np.abs(psi - ref).max() > 1e-3
+    oracle.apply_circuit(psi, circuit_inverse(w.gates))
+    assert np.abs(psi - ref).max() <= 1e-13
