@@ -1,26 +1,36 @@
 #!/usr/bin/env python
 """bench.py -- one JSON line for the driver.
 
-Workload (BASELINE.json configs[3], the largest single-GPU config; the
-metric's "1/2/4/8 B200" scaling applies to it): n=24 XYZ-Heisenberg
-parameter-shift gradient, RY/RZ + CNOT-ring ansatz of depth 10 (720 gates,
-480 parameters), 93-term Pauli sum; one step = one full gradient = 961
-circuits (960 shifted + the base circuit for E(theta)) from |0...0>.
-With N GPUs the 961 circuits are sharded by parameter (p % N == rank) and
-the gradient is summed with one NCCL all-reduce ("scaling": "strong": the
-job is the configured gradient).
+Default workload (--workload cfg4; BASELINE.json configs[3], the largest
+single-GPU config; the metric's "1/2/4/8 B200" applies to it): n=24
+XYZ-Heisenberg parameter-shift gradient, RY/RZ + CNOT-ring ansatz of depth 10
+(720 gates, 480 parameters), 93-term Pauli sum; one step = one full gradient
+= 961 circuits (960 shifted + the base circuit for E(theta)) from |0...0>.
+With N GPUs the circuits are sharded by parameter (p % N == rank) and the
+library all-reduces the gradient and E over NCCL inside lq_psr_run
+("scaling": "strong": the job is the configured gradient).
 
-value  = gate-amplitude updates/s over all ranks: circuits x 720 x 2^24 /
+--workload cfg5 (BASELINE.json configs[4], weak scaling): n = 33 + log2 N
+(2^33 amplitudes = 128 GiB per GPU), init_random, the config-5 generator's
+1000 gates (30 % on the m = max(1, log2 N) top qubits), then the full QFT;
+N > 1 shards the state over the ranks (global-qubit exchanges over NCCL).
+
+value  = gate-amplitude updates/s over all ranks: user-level gates x 2^n /
          max-over-ranks device time (CUDA events on the launch stream),
-         inputs (theta) already in HBM.
-e2e    = the same metric through lq_param_shift_grad with HOST buffers
-         (pinned theta in, gradient out), plan upload and copies included.
-roofline = the dominant kernel (k_tile, the fused gate pass): algorithmic
-         HBM bytes / its CUDA-event time inside the timed region.
+         inputs already in HBM.
+e2e    = the same metric through the public C-ABI call with HOST buffers
+         (cfg4: lq_param_shift_grad, pinned theta in, gradient out; cfg5:
+         host gate list in, 2^16 sampled amplitudes out), copies included.
+roofline = the dominant kernel (the fused tile pass): algorithmic HBM bytes /
+         its CUDA-event time inside an instrumented copy of the timed region.
 cpu_baseline = the CPU oracle (oracle/, test infrastructure) on a bounded
-         sample of the same workload, rank 0, N=1 only.
+         sample of the same workload, rank 0, N=1 only: one core, and all
+         host cores over independent circuits.
 
-`--impl reference` times the oracle itself (this tier's reference arm).
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+with N ranks; it fails (exit 2) if fewer than N GPUs are visible or if the
+launcher's WORLD_SIZE differs from N.  `--impl reference` times the oracle
+(this tier's reference arm).
 """
 from __future__ import annotations
 
@@ -29,9 +39,12 @@ import ctypes
 import json
 import math
 import os
+import platform
+import socket
 import statistics
 import subprocess
 import sys
+import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -39,6 +52,14 @@ sys.path.insert(0, ROOT)
 
 METRIC = "gate-amplitude updates/s & achieved HBM GB/s (frac. of peak) at 1/2/4/8 B200"
 UNIT = "gate-amplitude updates/s"
+NVLINK_GBS = 900.0   # NVLink 5 per direction per GPU (task statement)
+PAPER_CONTEXT = {
+    "note": "the paper reports no GPU or absolute gate throughput; its CPU-library speedups, quoted as context "
+            "only (Intel Core i9-10980XE, 18 cores, PAPER.md:50)",
+    "vqe": "VQE wall-clock 2-5x faster than Qiskit / PennyLane, 4-qubit H2 (PAPER.md:762)",
+    "qft": "QFT 120-900x vs PennyLane / Qiskit, 6-22x vs Yao.jl; 0.72 us at n=1 (dense path) "
+           "(PAPER.md:648, 670)",
+}
 
 
 def parse():
@@ -47,6 +68,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg5"])
+    ap.add_argument("--n", type=int, default=None, help="cfg5: override n (default 33 + log2 N)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -57,13 +80,43 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
-def workload():
+def die(msg):
+    sys.stderr.write(f"bench.py: {msg}\n")
+    sys.exit(2)
+
+
+def launch_or_check(args):
+    """--gpus N: re-exec under torchrun when no launcher set WORLD_SIZE;
+    refuse a world size that differs from N."""
+    if args.gpus < 1 or (args.gpus & (args.gpus - 1)):
+        die(f"--gpus must be a power of two >= 1, got {args.gpus}")
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            die(f"launched with WORLD_SIZE={world} but --gpus {args.gpus}")
+        return
+    if args.gpus == 1:
+        return
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            die(f"--gpus {args.gpus} needs {args.gpus} visible GPUs, this box has {have}")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+# ------------------------------------------------------------------ workloads
+def cfg4_workload():
     import workloads as W
-    w = W.config4()
-    return w
+    return W.config4()
 
 
-def workload_config(w, extra=None):
+def cfg4_config(w, extra=None):
     cfg = {"workload": "BASELINE configs[3]: n=24 XYZ Heisenberg open chain (Jx=1.0, Jy=0.7, Jz=0.4, "
                        "hz=0.3; 93 terms), RY/RZ + CNOT-ring ansatz depth 10 (720 gates, 480 params); "
                        "one step = full parameter-shift gradient (960 shifted + 1 base circuit)",
@@ -76,6 +129,27 @@ def workload_config(w, extra=None):
     return cfg
 
 
+def cfg5_shape(args, world):
+    m_sh = world.bit_length() - 1            # log2 of the ranks the state is sharded over
+    n = args.n if args.n else 33 + m_sh
+    m_gen = max(1, m_sh)                     # the generator's "global" qubits (reading A13)
+    return n, m_sh, m_gen
+
+
+def cfg5_config(n, m_sh, m_gen, n_gates, qft_gates, extra=None):
+    cfg = {"workload": f"BASELINE configs[4] (weak scaling): n={n} = 33 + log2 N, init_random, {n_gates} gates "
+                       f"from the config-5 generator (30 % on the top m={m_gen} qubits), then the full QFT "
+                       f"({qft_gates} Alg. 3 gates); one step = init + circuit + QFT",
+           "n_qubits": n, "state_bytes_per_gpu": 16 << (n - m_sh), "sharded_over": 1 << m_sh,
+           "gates_per_step": n_gates + qft_gates,
+           "l2": "no flush needed: a 2^33-amplitude shard (128 GiB) per GPU streams through HBM every pass",
+           "seed": "SeedSequence(251223183 + 5)"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# ------------------------------------------------------------------ measurement helpers
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -132,96 +206,122 @@ def peaks():
 
 
 def ncu_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per k_tile launch from the
-    committed ncu --set full capture summary (profiles/), normalised per
-    circuit-state in the launch."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per tile-pass launch from
+    the committed ncu --set full capture summary (profiles/)."""
     p = os.path.join(ROOT, "profiles", "ncu_k_tile_summary.json")
     if not os.path.exists(p):
         return None
     try:
-        d = json.load(open(p))
-        return d
+        return json.load(open(p))
     except Exception:
         return None
 
 
-def cpu_oracle_sample(w, n_gates):
-    """The oracle (plain single-thread C) applying the first n_gates of the
-    first shifted circuit (theta + pi/2 e_0) from |0...0> at n = 24."""
-    import numpy as np
+def host_info():
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+def oracle_gate_sample(n, gates, theta, n_threads=1):
+    """The oracle (plain single-thread C) applying `gates` from |0...0> at n
+    qubits, on n_threads independent circuits at once (one state each; the
+    oracle releases the GIL): returns (aggregate updates/s, wall seconds)."""
     import oracle
+    states = [oracle.zeros(n) for _ in range(n_threads)]
+    t0 = time.perf_counter()
+    if n_threads == 1:
+        oracle.apply_circuit(states[0], gates, theta)
+    else:
+        ts = [threading.Thread(target=oracle.apply_circuit, args=(s, gates, theta)) for s in states]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+    dt = time.perf_counter() - t0
+    return n_threads * len(gates) * (1 << n) / dt, dt
+
+
+def cfg4_oracle_sample(w, n_gates, n_threads=1):
+    """first n_gates of the first shifted circuit (theta + pi/2 e_0) at n=24"""
     th = w.theta.copy()
     th[0] += math.pi / 2
-    psi = oracle.zeros(w.n)
-    t0 = time.perf_counter()
-    oracle.apply_circuit(psi, w.gates[:n_gates], th)
-    dt = time.perf_counter() - t0
-    return n_gates * (1 << w.n) / dt, dt
+    return oracle_gate_sample(w.n, w.gates[:n_gates], th, n_threads)
 
 
+def cpu_baseline_block(sample_fn, desc_1, desc_all):
+    model, ncpu = host_info()
+    r1, s1 = sample_fn(1)
+    threads = max(1, min(ncpu, 32))
+    out = {"value": r1, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"{desc_1}: {s1:.1f} s",
+           "cpu_model": model, "os_cpu_count": ncpu}
+    if threads > 1:
+        ra, sa = sample_fn(threads)
+        out["all_core"] = {"value": ra, "unit": UNIT, "cores": threads,
+                           "sample": f"{desc_all} on {threads} threads (one independent circuit each): {sa:.1f} s"}
+    return out
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
 def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
         return
-    w = workload()
-    n_gates = 72   # one ansatz layer per step (bounded sample, ~5 s of single-core work)
+    model, ncpu = host_info()
+    if args.workload == "cfg4":
+        w = cfg4_workload()
+        n_gates = 72   # one ansatz layer per step (bounded sample, ~5 s of single-core work)
+        fn = lambda: cfg4_oracle_sample(w, n_gates)   # noqa: E731
+        sample = (f"oracle (plain single-thread C, oracle/oracle.c) applying one ansatz layer "
+                  f"({n_gates} gates) of the first shifted circuit at n={w.n} per step")
+        cfg = cfg4_config(w, {"sample": sample})
+        scaling = "strong"
+    else:
+        import workloads as W
+        n, m_sh, m_gen = cfg5_shape(args, world)
+        tw = W.config5(n=24, m=m_gen)
+        n_gates = 60
+        fn = lambda: oracle_gate_sample(24, tw.gates[:n_gates], None)   # noqa: E731
+        sample = (f"oracle (plain single-thread C) applying the first {n_gates} gates of the config-5 generator "
+                  f"(m={m_gen}) to a 2^24-amplitude state per step (the n={n} state does not fit host memory)")
+        cfg = cfg5_config(n, m_sh, m_gen, 1000, W.qft_gate_count(n), {"sample": sample})
+        scaling = "weak"
     for _ in range(args.warmup):
-        cpu_oracle_sample(w, n_gates)
+        fn()
     rates, times = [], []
     for _ in range(args.steps):
-        r, dt = cpu_oracle_sample(w, n_gates)
+        r, dt = fn()
         rates.append(r)
         times.append(dt)
-    tot_updates = args.steps * n_gates * (1 << w.n)
-    value = tot_updates / sum(times)
-    sample = (f"oracle (plain single-thread C, oracle/oracle.c) applying one ansatz layer "
-              f"({n_gates} gates) of the first shifted circuit at n={w.n} per step")
+    value = statistics.mean(rates)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(w, {"sample": sample}),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu_model": model, "os_cpu_count": ncpu},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args):
-    import numpy as np
+# ------------------------------------------------------------------ our arm
+def timed(args, world, local, stream, step, lq):
+    """K steps between a barrier + synchronize on both sides; returns
+    (plain ms, instrumented ms, launches, clocks, per-class event timings).
+    The instrumented copy brackets every launch with CUDA events on its
+    stream (the roofline's per-launch time; ~2 % overhead), so `value`
+    comes from the plain region."""
     import torch
     import torch.distributed as dist
-    from paper_2512_23183_b200 import lq
 
-    rank, local, world = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    w = workload()
-    n, P = w.n, int(w.theta.size)
-    stream = torch.cuda.current_stream()
-    plan = lq.lq_psr_create(n, w.gates, P, w.terms, rank, world, stream)
-    n_circ, _, plan_bytes, tile_passes = lq.lq_psr_stats(plan)
-    total_circ = 2 * P + 1
-    theta = torch.tensor(w.theta, dtype=torch.float64, device=dev)
-    grad = torch.zeros(P, dtype=torch.float64, device=dev)
-    energy = torch.zeros(1, dtype=torch.float64, device=dev)
-
-    def step():
-        lq.lq_psr_run(plan, theta.data_ptr(), grad.data_ptr(), energy.data_ptr())
-        if world > 1:
-            dist.all_reduce(grad)
-            dist.all_reduce(energy)
-
-    for _ in range(max(args.warmup, 1)):
-        step()
-    torch.cuda.synchronize()
-    g_check = grad.cpu().numpy().copy()
-
-    def timed_region(instrumented):
-        """K steps between a barrier + synchronize on both sides; with
-        `instrumented`, every launch is bracketed by CUDA events on its
-        stream (lq_kernel_timing) for the roofline -- that costs ~2 % of step
-        time, so `value` comes from the plain region."""
+    def region(instrumented):
         lq.lq_kernel_timing_reset()
         lq.lq_set_option(lq.LQ_OPT_KERNEL_TIMING, 1 if instrumented else 0)
         l0 = lq.lq_launch_count()
@@ -243,27 +343,54 @@ def run_ours(args):
         lq.lq_set_option(lq.LQ_OPT_KERNEL_TIMING, 0)
         return ev0.elapsed_time(ev1), lq.lq_launch_count() - l0, clk
 
-    ms, launches, clk = timed_region(False)
-    ms_inst, _, clk_inst = timed_region(True)
-    tile_ms, tile_cnt = lq.lq_kernel_timing(lq.KC_TILE)
-    pauli_ms, pauli_cnt = lq.lq_kernel_timing(lq.KC_PAULI)
-    t = torch.tensor([ms, launches, tile_ms, tile_cnt, pauli_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum)
-        ms_max = float(tmax[0])
-        launches_all = int(tsum[1])
-    else:
-        ms_max, launches_all = ms, launches
+    ms, launches, clk = region(False)
+    ms_inst, _, clk_inst = region(True)
+    cls = {k: lq.lq_kernel_timing(getattr(lq, k)) for k in ("KC_TILE", "KC_PAULI", "KC_SWAP")}
+    return ms, ms_inst, launches, clk, clk_inst, cls
+
+
+def reduce_max_sum(vals, world, dev):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    if world == 1:
+        return t.tolist(), t.tolist()
+    tmax, tsum = t.clone(), t.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tsum)
+    return tmax.tolist(), tsum.tolist()
+
+
+def run_cfg4(args, lq, rank, local, world, dev, comm):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    w = cfg4_workload()
+    n, P = w.n, int(w.theta.size)
+    stream = torch.cuda.current_stream()
+    plan = lq.lq_psr_create(n, w.gates, P, w.terms, comm=comm, stream=stream)
+    n_circ, _, plan_bytes, tile_passes = lq.lq_psr_stats(plan)
+    total_circ = 2 * P + 1
+    theta = torch.tensor(w.theta, dtype=torch.float64, device=dev)
+    grad = torch.zeros(P, dtype=torch.float64, device=dev)
+    energy = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def step():   # one full gradient; with N ranks the all-reduce runs inside lq_psr_run
+        lq.lq_psr_run(plan, theta.data_ptr(), grad.data_ptr(), energy.data_ptr())
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    g_check = grad.cpu().numpy().copy()
+    ms, ms_inst, launches, clk, clk_inst, cls = timed(args, world, local, stream, step, lq)
+    tile_ms, tile_cnt = cls["KC_TILE"]
+    pauli_ms, _ = cls["KC_PAULI"]
+    mx, sm = reduce_max_sum([ms, launches], world, dev)
+    ms_max, launches_all = mx[0], int(sm[1])
     updates_per_step = total_circ * len(w.gates) * (1 << n)
     value = updates_per_step * args.steps / (ms_max / 1e3)
 
     # roofline of the dominant kernel on this rank: algorithmic bytes / event time.
-    # Each circuit streams the state through `tile_passes` tile passes: 16 B/amp
-    # per load and per store; the first pass synthesises |0...0> (no load),
-    # read-only and final passes skip the store (lq_psr_traffic, exact per plan).
     tile_bytes_circ, _other = lq.lq_psr_traffic(plan)
     alg_bytes = args.steps * n_circ * tile_bytes_circ
     peak, peak_src = peaks()
@@ -272,13 +399,12 @@ def run_ours(args):
     traffic = None
     alg_per_launch = alg_bytes / max(tile_cnt, 1)
     if tr and tr.get("n_qubits") == n:
-        # the capture's DRAM bytes per launch, rescaled by the ratio of
-        # algorithmic bytes per launch (the capture may batch differently)
         traffic = tr["dram_bytes_per_launch"] * alg_per_launch / tr["algorithmic_bytes_per_launch"]
-    roof = {"kernel": "k_tile (fused tile pass)", "bound": "hbm", "achieved": achieved, "peak": peak,
-            "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+    roof = {"kernel": "lqj tile pass (fused gates + Pauli groups)", "bound": "hbm", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "algorithmic_bytes_per_launch": alg_per_launch, "launches": int(tile_cnt),
             "avg_launch_ms": tile_ms / max(tile_cnt, 1), "peak_source": peak_src,
+            "frac_of_nominal_8tbs": (achieved / 8000.0) if achieved else None,
             "kernel_share_of_step": tile_ms / ms_inst if ms_inst > 0 else None,
             "pauli_share_of_step": pauli_ms / ms_inst if ms_inst > 0 else None,
             "timing": "separate instrumented region of the same K steps (per-launch CUDA events); "
@@ -286,7 +412,7 @@ def run_ours(args):
             "clocks_instrumented_region": clk_inst,
             "traffic_source": (tr or {}).get("source")}
 
-    # ---- e2e: host buffers through the public API ------------------------------------------
+    # ---- e2e: host buffers through the public API (collective with N ranks) -----------------
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
     th_pin = torch.tensor(w.theta, dtype=torch.float64).pin_memory()
     g_pin = torch.zeros(P, dtype=torch.float64).pin_memory()
@@ -295,15 +421,9 @@ def run_ours(args):
     DP = ctypes.POINTER(ctypes.c_double)
 
     def e2e_step():
-        st = lq._lib.lq_param_shift_grad(n, ga.ptr, ga.n, ctypes.cast(th_pin.data_ptr(), DP), P, ta.ptr, ta.n,
-                                         rank, world, stream.cuda_stream, ctypes.cast(g_pin.data_ptr(), DP),
-                                         ctypes.cast(e_pin.data_ptr(), DP))
-        lq._chk(st)
-        if world > 1:
-            gd = g_pin.to(dev, non_blocking=True)
-            dist.all_reduce(gd)
-            g_pin.copy_(gd)
-        return g_pin
+        lq._chk(lq._lib.lq_param_shift_grad(n, ga.ptr, ga.n, ctypes.cast(th_pin.data_ptr(), DP), P, ta.ptr, ta.n,
+                                            comm, stream.cuda_stream, ctypes.cast(g_pin.data_ptr(), DP),
+                                            ctypes.cast(e_pin.data_ptr(), DP)))
 
     e2e_step()
     if world > 1:
@@ -313,30 +433,24 @@ def run_ours(args):
     for _ in range(e2e_steps):
         e2e_step()
     torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    dtt = torch.tensor([dt], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(dtt, op=dist.ReduceOp.MAX)
-    dt = float(dtt[0])
+    dt = reduce_max_sum([time.perf_counter() - t0], world, dev)[0][0]
     e2e_value = updates_per_step * e2e_steps / dt
-    # theta in; the plan is built and uploaded once (lq_param_shift_grad's plan cache, warm-up call)
-    h2d = 8 * P + (8 * P if world > 1 else 0)
-    d2h = 8 * P + 8 + (8 * P if world > 1 else 0)
+    h2d = 8 * P                 # theta in (the plan is built and uploaded once: the warm-up call)
+    d2h = 8 * P + 8             # gradient + E out
     g_e2e = g_pin.numpy().copy()
-    if not np.allclose(g_e2e, g_check, rtol=0, atol=1e-12):
+    if not np.array_equal(g_e2e, g_check):
         raise RuntimeError("e2e gradient differs from the device-resident gradient")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_gates = 144
-        rate, secs = cpu_oracle_sample(w, n_gates)
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"oracle (single-thread C) applying the first {n_gates} gates (2 ansatz layers) "
-                         f"of one shifted circuit at n={n}: {secs:.1f} s"}
-    # support tracking: the first passes run only the tiles that
-    # can be nonzero.  The counted updates stay nominal (every gate on all 2^n
-    # amplitudes); this is the share of the plan's ops x
-    # amplitudes that fall on provably-zero amplitudes and are not executed.
+        cpu = cpu_baseline_block(lambda t: cfg4_oracle_sample(w, n_gates if t == 1 else 72, t),
+                                 f"oracle (single-thread C) applying the first {n_gates} gates (2 ansatz layers) "
+                                 f"of one shifted circuit at n={n}",
+                                 "the same oracle applying one ansatz layer (72 gates)")
+    # support tracking: counted updates stay nominal (every gate
+    # on all 2^n amplitudes); this is the share of the plan's ops
+    # x amplitudes that fall on provably-zero amplitudes and are not executed.
     ps = lq.lq_psr_pass_bytes(plan, with_support=True)
     N = 1 << n
     tot_ops = sum(o for _, _, _, o in ps) or 1
@@ -346,23 +460,147 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": workload_config(w, {"parallelism": f"psr-shard{world}" if world > 1 else "single",
-                                              "circuits_this_rank": int(n_circ),
-                                              "tile_passes_per_circuit": int(tile_passes),
-                                              "updates_counted": "nominal: gates x 2^n per circuit",
-                                              "nominal_share_on_provably_zero_amplitudes": round(zero_share, 4)}),
+                "executed_value": value * (1.0 - zero_share),
+                "executed_value_note": "value x (1 - nominal_share_on_provably_zero_amplitudes): the updates "
+                                       "that actually execute (support tracking skips provably-zero amplitudes)",
+                "config": cfg4_config(w, {"parallelism": f"psr-shard{world} + NCCL all-reduce in lq_psr_run"
+                                          if world > 1 else "single",
+                                          "circuits_this_rank": int(n_circ),
+                                          "tile_passes_per_circuit": int(tile_passes),
+                                          "updates_counted": "nominal: gates x 2^n per circuit",
+                                          "nominal_share_on_provably_zero_amplitudes": round(zero_share, 4)}),
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                        "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
-                "gpu_launches": launches_all, "clocks": clk,
+                        "d2h_bytes_per_step": int(d2h), "steps": e2e_steps, "api": "lq_param_shift_grad"},
+                "gpu_launches": launches_all, "clocks": clk, "paper_context": PAPER_CONTEXT,
                 "energy": float(energy.cpu()[0]), "grad_inf_norm": float(np.abs(g_check).max())}
         print(json.dumps(line), flush=True)
+
+
+def run_cfg5(args, lq, rank, local, world, dev, comm):
+    import numpy as np
+    import torch
+    import workloads as W
+    n, m_sh, m_gen = cfg5_shape(args, world)
+    w = W.config5(n=n, m=m_gen)
+    qg = W.qft_gate_count(n)
+    stream = torch.cuda.current_stream()
     if world > 1:
-        dist.destroy_process_group()
+        sv = lq.ShardedState(n, comm=comm, stream=stream)
+    else:
+        sv = lq.StateVector(n, stream=stream)
+    ga = lq.GateArray(w.gates)
+
+    def step():
+        sv.init_random(w.seed)
+        sv.apply(ga)
+        sv.qft()
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    ex0 = lq.lq_sv_exchange_stats(sv.h)
+    ms, ms_inst, launches, clk, clk_inst, cls = timed(args, world, local, stream, step, lq)
+    ex1 = lq.lq_sv_exchange_stats(sv.h)
+    tile_ms, tile_cnt = cls["KC_TILE"]
+    swap_ms, swap_cnt = cls["KC_SWAP"]
+    mx, sm = reduce_max_sum([ms, launches, swap_ms], world, dev)
+    ms_max, launches_all, swap_ms_max = mx[0], int(sm[1]), mx[2]
+    updates_per_step = (len(w.gates) + qg) * (1 << n)
+    value = updates_per_step * args.steps / (ms_max / 1e3)
+    nloc = 1 << (n - m_sh)
+    # tile passes of circuit and QFT plans read and write every local
+    # amplitude once: 32 B per amplitude per launch
+    alg_per_launch = 32 * nloc
+    peak, peak_src = peaks()
+    achieved = alg_per_launch * tile_cnt / (tile_ms / 1e3) / 1e9 if tile_ms > 0 else None
+    roof = {"kernel": "lqj tile pass (fused gates / QFT butterflies)", "bound": "hbm", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": None,
+            "algorithmic_bytes_per_launch": alg_per_launch, "launches": int(tile_cnt),
+            "avg_launch_ms": tile_ms / max(tile_cnt, 1), "peak_source": peak_src,
+            "frac_of_nominal_8tbs": (achieved / 8000.0) if achieved else None,
+            "kernel_share_of_step": tile_ms / ms_inst if ms_inst > 0 else None,
+            "clocks_instrumented_region": clk_inst}
+    exchanges = (ex1[0] - ex0[0]) // 2          # two timed regions
+    sent = (ex1[1] - ex0[1]) // 2
+    nvl = None
+    if world > 1:
+        nvl = {"exchanges_per_step": exchanges / args.steps, "bytes_sent_per_rank_per_step": sent / args.steps,
+               "exchange_ms_per_step": swap_ms_max / args.steps,
+               "achieved_gbs": (sent / args.steps) / (swap_ms_max / args.steps / 1e3) / 1e9 if swap_ms_max else None,
+               "peak_gbs": NVLINK_GBS, "unit": "GB/s (bytes sent per GPU / exchange time, pack + unpack included)"}
+        if nvl["achieved_gbs"]:
+            nvl["frac"] = nvl["achieved_gbs"] / NVLINK_GBS
+
+    # e2e: host gate list in, sampled amplitudes out, through the public API
+    e2e_steps = args.e2e_steps or 1
+    idx = np.unique(np.random.default_rng(5).integers(0, 1 << n, size=1 << 16, dtype=np.uint64))
+
+    def e2e_step():
+        sv.init_random(w.seed)
+        sv.apply(w.gates)
+        sv.qft()
+        return sv.gather(idx)
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        amps = e2e_step()
+    torch.cuda.synchronize()
+    dt = reduce_max_sum([time.perf_counter() - t0], world, dev)[0][0]
+    e2e_value = updates_per_step * e2e_steps / dt
+    norm = sv.norm2()
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tw = W.config5(n=24, m=m_gen)
+        cpu = cpu_baseline_block(lambda t: oracle_gate_sample(24, tw.gates[:60 if t == 1 else 30], None, t),
+                                 f"oracle (single-thread C) applying the first 60 config-5 gates (m={m_gen}) to a "
+                                 "2^24-amplitude state (the 2^33 state exceeds host memory)",
+                                 "the same oracle applying 30 gates")
+    sv.free()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": cfg5_config(n, m_sh, m_gen, len(w.gates), qg,
+                                      {"parallelism": f"state sharded on {m_sh} global qubits over NCCL"
+                                       if world > 1 else "single"}),
+                "roofline": roof, "nvlink": nvl, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(ga.n * 40 + idx.size * 8),
+                        "d2h_bytes_per_step": int(idx.size * 16), "steps": e2e_steps,
+                        "api": "lq_sv_init_random + lq_apply_circuit + lq_qft + lq_sv_gather"},
+                "gpu_launches": launches_all, "clocks": clk, "paper_context": PAPER_CONTEXT,
+                "norm2": norm, "sample_abs_max": float(np.abs(amps).max())}
+        print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2512_23183_b200 import lq
+
+    rank, local, world = dist_env()
+    if not torch.cuda.is_available():
+        die("no CUDA device: liblq has no CPU path")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = lq.comm_from_torch()
+    try:
+        (run_cfg4 if args.workload == "cfg4" else run_cfg5)(args, lq, rank, local, world, dev, comm)
+    finally:
+        if comm is not None:
+            lq.lq_psr_cache_clear()
+            lq.lq_comm_free(comm)
+        if world > 1:
+            dist.destroy_process_group()
 
 
 def main():
     args = parse()
+    launch_or_check(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -40,10 +40,12 @@ typedef enum {
     LQ_ERR_ARG = -1,        /* bad argument (qubit range, duplicate qubits, angle on a fixed gate, ...) */
     LQ_ERR_OOM = -2,        /* device allocation failed / state too large */
     LQ_ERR_CUDA = -3,       /* CUDA runtime error (incl. no device) */
-    LQ_ERR_NCCL = -4,       /* reserved: collective failure */
+    LQ_ERR_NCCL = -4,       /* collective failure (NCCL error, asynchronous error or timeout) */
     LQ_ERR_DIM = -5,        /* size mismatch (wrapped buffer too small, count out of range) */
     LQ_ERR_NONFINITE = -6,  /* NaN/Inf angle, parameter or coefficient */
-    LQ_ERR_STATE = -7       /* handle unusable after an earlier asynchronous failure */
+    LQ_ERR_STATE = -7       /* handle unusable after an earlier asynchronous failure: once a call on a
+                               state / gradient plan / comm returned LQ_ERR_CUDA or LQ_ERR_NCCL from
+                               work it had enqueued, every later call on it returns LQ_ERR_STATE */
 } lq_status;
 
 /* Gate kinds.  Fixed gates take no angle; rotation
@@ -153,7 +155,9 @@ lq_status lq_sv_canonicalize(lq_sv *sv);
  * physical bits: rank r holds the 2^(n-m) amplitudes whose global bits are
  * r ^ xmask (xmask: pending rank relabel; 0 after an init).  Gates acting
  * non-diagonally on a global qubit are preceded by a global<->local qubit
- * swap (pairwise half-shard exchange); controls, diagonal gates and Pauli Z
+ * exchange (k global with k local qubits at once: an all-to-all among 2^k
+ * ranks, chunked and in place, transfers overlapped with packing on a second
+ * stream; LQ_OPT_SWAP_QUBITS); controls, diagonal gates and Pauli Z
  * factors on global qubits are rank constants; an uncontrolled X (or Y) on a
  * global qubit is a rank relabel.  Every call on a sharded handle is
  * COLLECTIVE: all ranks make the same calls with the same arguments, in the
@@ -168,6 +172,16 @@ lq_status lq_comm_unique_id(void *out, size_t len);
  * at run time (the copy torch already loaded, else libnccl.so.2);
  * LQ_ERR_NCCL if it is unavailable. */
 lq_status lq_comm_init(const void *unique_id, size_t len, int rank, int world, lq_comm **out);
+/* A communicator WITHOUT transport: (rank, world) only.  Work partitioned over
+ * ranks (lq_psr_create / lq_param_shift_grad) computes this rank's share and
+ * the collectives are the identity, so every host or device result is the
+ * rank's PARTIAL one (gradient components it does not own are 0; E only on
+ * rank 0).  For callers that reduce themselves and for testing the partition
+ * on one device.  Sharded states reject it (they need a transport). */
+lq_status lq_comm_init_local(int rank, int world, lq_comm **out);
+/* rank, world, and whether NCCL carries data (0 for lq_comm_init_local).
+ * LQ_ERR_STATE once the communicator was aborted (LQ_OPT_COMM_TIMEOUT_MS). */
+lq_status lq_comm_info(const lq_comm *comm, int *rank, int *world, int *has_transport);
 lq_status lq_comm_free(lq_comm *comm);
 
 /* This process's shard of an n-qubit state on comm's ranks (world a power of
@@ -186,6 +200,9 @@ lq_status lq_sv_shard_info(const lq_sv *sv, int *log2_world, int *first_rank, in
                            uint32_t *xmask);
 /* Device pointer of local shard k (2^(n-m) amplitudes, physical local order). */
 void *lq_sv_shard_ptr(const lq_sv *sv, int k);
+/* Global-qubit exchanges run on this handle so far, and the bytes each rank
+ * sent in them (a k-qubit exchange sends (2^k - 1) / 2^k of a shard). */
+lq_status lq_sv_exchange_stats(const lq_sv *sv, uint64_t *n_exchanges, uint64_t *bytes_sent_per_rank);
 
 /* Host-only: the distributed schedule (steps: local tile plans with the rank
  * relabel in effect, global<->local swaps) of `gates`, then an optional QFT
@@ -231,14 +248,21 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
  *   c1 = (sqrt2 + 1) / (4 sqrt2), c2 = (sqrt2 - 1) / (4 sqrt2)
  * (shifts of theta_p; reading A8).  Each parameter must be used by
  * exactly one rotation gate (reading A7); all shifted circuits are
- * independent and are batched.  shard_rank/shard_world: compute only parameters with
- * p % shard_world == shard_rank (others are written as 0); the caller sums
- * the shards (e.g. torch.distributed.all_reduce).  energy_out (nullable)
- * receives E(theta) on shard 0 (0 elsewhere).  Host in/out (syncs). */
+ * independent and are batched.
+ * comm (nullable): with a communicator of `world`
+ * ranks the call is COLLECTIVE (same arguments on every rank): rank r
+ * evaluates the circuits of the parameters p with p % world == r (and rank 0
+ * the unshifted circuit), then one NCCL all-reduce over the n_params + 1
+ * values returns the full gradient and E(theta) on EVERY rank.  Each value
+ * comes from exactly one rank (zeros elsewhere), so the result is
+ * bit-identical to the 1-GPU one.  A transport-less comm
+ * (lq_comm_init_local) returns the rank's partial gradient instead.
+ * energy_out (nullable) receives E(theta).  Host in/out (syncs; with NCCL the
+ * wait polls for asynchronous errors, LQ_OPT_COMM_TIMEOUT_MS). */
 lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gates,
                               const double *theta, size_t n_params,
                               const lq_pauli_term *terms, size_t n_terms,
-                              int shard_rank, int shard_world, void *cuda_stream,
+                              lq_comm *comm, void *cuda_stream,
                               double *grad_out, double *energy_out);
 
 /* lq_param_shift_grad keeps the plans (and device buffers) of its two most
@@ -254,10 +278,14 @@ lq_status lq_psr_cache_clear(void);
  * starts from |0...0>: the first tile pass synthesises it,
  * and while the tiles run so far leave some qubits untouched the state is zero
  * outside their union, so passes read and run only inside it (support
- * tracking; results are bit-identical to full passes, lq_psr_pass_bytes). */
+ * tracking; results are bit-identical to full passes, lq_psr_pass_bytes).
+ * comm: as lq_param_shift_grad -- the plan holds this rank's circuits and
+ * lq_psr_run ends with the all-reduce (enqueued on the stream; the comm must
+ * outlive the plan).  A plan that met an asynchronous CUDA / NCCL failure
+ * returns LQ_ERR_STATE from every later run. */
 lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, size_t n_params,
-                        const lq_pauli_term *terms, size_t n_terms, int shard_rank,
-                        int shard_world, void *cuda_stream, lq_psr **out);
+                        const lq_pauli_term *terms, size_t n_terms, lq_comm *comm,
+                        void *cuda_stream, lq_psr **out);
 lq_status lq_psr_run(lq_psr *plan, const double *theta_dev, double *grad_dev, double *energy_dev);
 lq_status lq_psr_free(lq_psr *plan);
 /* ---- Trotterised XYZ time evolution --- */
@@ -353,9 +381,15 @@ typedef enum {
     LQ_OPT_FIRST_PASS_FREE = 7, /* PSR plans: 1 (default) exempts the first pass -- it synthesises |0...0>,
                                  so every tile but one is stored as zeros without arithmetic -- from
                                  the pass budget; 0: budget it like the others */
-    LQ_OPT_POISON_ALLOC = 8   /* testing: 1 fills every fresh library work allocation (PSR state batches,
+    LQ_OPT_POISON_ALLOC = 8,  /* testing: 1 fills every fresh library work allocation (PSR state batches,
                                  scratch, staging) with 0xFF bytes (NaN doubles), so a kernel that reads
                                  memory nothing wrote fails loudly instead of seeing leftover zeros */
+    LQ_OPT_COMM_TIMEOUT_MS = 9, /* host waits on work that includes NCCL operations poll the stream and
+                                 ncclCommGetAsyncError; after this many ms (default 600000; 0 = forever)
+                                 or on an asynchronous NCCL error the communicator is aborted and the
+                                 call returns LQ_ERR_NCCL (later calls on its handles: LQ_ERR_STATE) */
+    LQ_OPT_SWAP_QUBITS = 10   /* sharded states: most global qubits one exchange may move (1..4, default
+                                 4; 1 = pairwise half-shard swaps only, k > 1 = all-to-all among 2^k ranks) */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);
@@ -385,7 +419,9 @@ lq_status lq_qft_jit_compile_check(int n_qubits, int inverse, uint64_t *n_kernel
 
 /* Accumulated device time of launches made while LQ_OPT_KERNEL_TIMING was
  * on, per kernel class: 0 tile pass, 1 pair pass, 2 diagonal pass,
- * 3 Pauli expectation, 4 other.  Synchronises on the recorded events. */
+ * 3 Pauli expectation, 4 other, 5 global-qubit exchange of a sharded state
+ * (one record per exchange step: pack, transfer and unpack on the handle's
+ * stream).  Synchronises on the recorded events. */
 lq_status lq_kernel_timing(int kernel_class, double *total_ms, uint64_t *count);
 lq_status lq_kernel_timing_reset(void);
 

@@ -11,6 +11,8 @@ namespace lq {
 
 namespace {
 
+constexpr int COALESCE_BITS = 3;   // 8 amplitudes = one 128-byte run
+
 // Logical qubits a gate acts on non-diagonally (controls and diagonal
 // factors are rank constants when global).
 int nondiag_qubits(const lq_gate &G, int *q) {
@@ -35,6 +37,28 @@ int all_qubits(const lq_gate &G, int *q) {
 }
 
 }  // namespace
+
+void push_swap(Schedule &sc, int k, const int *g, const int *l, uint32_t xmask, int32_t *qm, int *at) {
+    DStep sw;
+    sw.kind = 1;
+    sw.k = k;
+    sw.xmask = xmask;
+    int idx[MAX_SWAP_K];
+    for (int j = 0; j < k; j++) idx[j] = j;
+    std::sort(idx, idx + k, [&](int a, int b) { return l[a] < l[b]; });
+    for (int j = 0; j < k; j++) {
+        sw.g[j] = g[idx[j]];
+        sw.l[j] = l[idx[j]];
+        const int qg = at[sw.g[j]], ql = at[sw.l[j]];
+        if (qg >= 0) qm[qg] = sw.l[j];
+        if (ql >= 0) qm[ql] = sw.g[j];
+        std::swap(at[sw.g[j]], at[sw.l[j]]);
+    }
+    sc.steps.push_back(std::move(sw));
+    sc.n_swaps++;
+    sc.n_swapped_qubits += (size_t)k;
+    sc.shard_fraction_sent += 1.0 - std::ldexp(1.0, -k);
+}
 
 bool schedule_gates(Schedule &sc, const lq_gate *gates, size_t ng, int32_t *qmap, uint32_t &xmask) {
     const int n = sc.n, nl = sc.nl;
@@ -110,31 +134,45 @@ bool schedule_gates(Schedule &sc, const lq_gate *gates, size_t ng, int32_t *qmap
             int na = all_qubits(G, a);
             for (int j = 0; j < na; j++) busy |= 1ull << qm[a[j]];
         }
-        for (int qg : glob) {
-            const int g = qm[qg];
-            int best = -1;
-            size_t best_next = 0;
-            for (int l = nl - 1; l >= 0; l--) {   // prefer high local bits on ties
-                if (busy >> l & 1) continue;
-                const size_t nu = at[l] >= 0 ? next_use(at[l], i) : (size_t)SIZE_MAX;
-                if (best < 0 || nu > best_next) {
-                    best = l;
-                    best_next = nu;
-                }
+        // victims: free local bits, furthest next use first (ties: high
+        // bits); the lowest COALESCE_BITS come last: an exchange over them
+        // would pack and unpack every part with a stride of 2^k amplitudes
+        // (partial 32-byte sectors), one over higher bits moves whole runs
+        std::vector<std::pair<size_t, int>> vict;
+        for (int l = nl - 1; l >= 0; l--) {
+            if (busy >> l & 1) continue;
+            vict.push_back({at[l] >= 0 ? next_use(at[l], i) : (size_t)SIZE_MAX, l});
+        }
+        std::stable_sort(vict.begin(), vict.end(), [](const std::pair<size_t, int> &x, const std::pair<size_t, int> &y) {
+            const bool lx = x.second < COALESCE_BITS, ly = y.second < COALESCE_BITS;
+            if (lx != ly) return ly;
+            return x.first > y.first;
+        });
+        if (vict.size() < glob.size()) return false;
+        std::vector<int> want(glob);
+        // other global qubits needed before the local qubit they would displace
+        std::vector<std::pair<size_t, int>> cand;
+        for (int g = nl; g < n; g++) {
+            const int q2 = at[g];
+            if (q2 < 0 || std::find(glob.begin(), glob.end(), q2) != glob.end()) continue;
+            const size_t u = next_use(q2, i);
+            if (u != (size_t)SIZE_MAX) cand.push_back({u, q2});
+        }
+        std::sort(cand.begin(), cand.end());
+        const int kmax = std::max(1, std::min(sc.max_k, MAX_SWAP_K));
+        for (size_t j = 0; j < cand.size(); j++) {
+            const size_t v = want.size();
+            if ((int)v >= kmax || v >= vict.size() || !(cand[j].first < vict[v].first)) break;
+            want.push_back(cand[j].second);
+        }
+        int gb[MAX_SWAP_K], lb[MAX_SWAP_K];
+        for (size_t j = 0; j < want.size(); j += kmax) {   // (a gate has at most 2 global non-diagonal qubits)
+            const int k = (int)std::min<size_t>(kmax, want.size() - j);
+            for (int t = 0; t < k; t++) {
+                gb[t] = qm[want[j + t]];
+                lb[t] = vict[j + t].second;
             }
-            if (best < 0) return false;
-            DStep sw;
-            sw.kind = 1;
-            sw.g = g;
-            sw.l = best;
-            sw.xmask = xmask;
-            sc.steps.push_back(std::move(sw));
-            sc.n_swaps++;
-            const int ql = at[best];
-            qm[qg] = best;
-            if (ql >= 0) qm[ql] = g;
-            rebuild_at();
-            busy |= 1ull << best;
+            push_swap(sc, k, gb, lb, xmask, qm.data(), at.data());
         }
         run_begin = i;
         run_qm = qm;
@@ -194,26 +232,20 @@ bool schedule_expval(Schedule &sc, const lq_pauli_term *terms, size_t nt, int32_
         else if (std::find(xs.begin(), xs.end(), terms[t].x_mask) == xs.end()) xs.push_back(terms[t].x_mask);
     }
     if (!now.empty()) emit(now);
-    for (uint64_t x : xs) {   // swap this group's global X/Y qubits in, then evaluate it
+    for (uint64_t x : xs) {   // swap this group's global X/Y qubits in (one exchange), then evaluate it
         if (__builtin_popcountll(x) > nl) return false;
+        std::vector<int> gs, ls;
         for (int g = nl; g < n; g++) {
             const int qg = at[g];
-            if (qg < 0 || !(x >> qg & 1)) continue;
-            int best = -1;
-            for (int l = nl - 1; l >= 0; l--)
-                if (at[l] < 0 || !(x >> at[l] & 1)) { best = l; break; }
-            if (best < 0) return false;
-            DStep sw;
-            sw.kind = 1;
-            sw.g = g;
-            sw.l = best;
-            sw.xmask = xmask;
-            sc.steps.push_back(std::move(sw));
-            sc.n_swaps++;
-            const int ql = at[best];
-            qmap[qg] = best;
-            if (ql >= 0) qmap[ql] = g;
-            std::swap(at[g], at[best]);
+            if (qg >= 0 && (x >> qg & 1)) gs.push_back(g);
+        }
+        for (int l = nl - 1; l >= 0 && ls.size() < gs.size(); l--)   // high bits first (COALESCE_BITS last)
+            if (at[l] < 0 || !(x >> at[l] & 1)) ls.push_back(l);
+        if (ls.size() < gs.size()) return false;
+        const size_t kmax = (size_t)std::max(1, std::min(sc.max_k, MAX_SWAP_K));
+        for (size_t j = 0; j < gs.size(); j += kmax) {
+            const int k = (int)std::min(kmax, gs.size() - j);
+            push_swap(sc, k, gs.data() + j, ls.data() + j, xmask, qmap, at.data());
         }
         std::vector<lq_pauli_term> grp;
         for (size_t t = 0; t < nt; t++)
@@ -234,14 +266,19 @@ void plan_steps(Schedule &sc, const PlanOptions &opt) {
 std::string schedule_json(const Schedule &sc, const int32_t *qmap, uint32_t xmask) {
     std::ostringstream o;
     o << "{\"n\":" << sc.n << ",\"m\":" << sc.m << ",\"nl\":" << sc.nl << ",\"n_swaps\":" << sc.n_swaps
-      << ",\"n_relabels\":" << sc.n_relabels << ",\"xmask\":" << xmask << ",\"qmap\":[";
+      << ",\"n_relabels\":" << sc.n_relabels << ",\"n_swapped_qubits\":" << sc.n_swapped_qubits
+      << ",\"shard_fraction_sent\":" << sc.shard_fraction_sent << ",\"xmask\":" << xmask << ",\"qmap\":[";
     for (int q = 0; q < sc.n; q++) o << (q ? "," : "") << qmap[q];
     o << "],\"steps\":[";
     for (size_t i = 0; i < sc.steps.size(); i++) {
         const DStep &st = sc.steps[i];
         if (i) o << ",";
         if (st.kind == 1) {
-            o << "{\"kind\":\"swap\",\"g\":" << st.g << ",\"l\":" << st.l << ",\"xmask\":" << st.xmask << "}";
+            o << "{\"kind\":\"swap\",\"g\":[";
+            for (int j = 0; j < st.k; j++) o << (j ? "," : "") << st.g[j];
+            o << "],\"l\":[";
+            for (int j = 0; j < st.k; j++) o << (j ? "," : "") << st.l[j];
+            o << "],\"xmask\":" << st.xmask << "}";
         } else {
             int32_t dummy[64];
             for (int q = 0; q < 64; q++) dummy[q] = 0;

@@ -287,64 +287,79 @@ __global__ void __launch_bounds__(256) k_random_write(uint64_t N, uint64_t off, 
         psi[i] = cscale(gauss_amp(seed, off + i), inv);
 }
 
-// ---------------------------------------------------------------- global-qubit swap (a9)
-// Sharded states (dist.h): swapping global bit g with local bit l, rank r
-// trades the half of its shard whose l-bit differs from its own g-bit with
-// the matching half of its partner.  Half-index i <-> shard position with
-// bit l = v inserted.
+// ---------------------------------------------------------------- global-qubit exchange (a9)
+// Sharded states (dist.h): exchanging k global bits g_j with k local bits
+// l_j (ascending), a shard splits into 2^k parts by the value b of its
+// l-bits (bit j of b <-> l_j); part b travels to the rank whose g-bits are b
+// and the part coming back lands in the same positions.  Part index i (the
+// other nl - k bits, ascending) <-> shard position with b deposited at the
+// l positions.  k = 1 is the pairwise half-shard swap.
+struct PartSpec {
+    int k;
+    int l[4];   // ascending local bit positions (dist.h MAX_SWAP_K)
+};
 __device__ __forceinline__ uint64_t insert_bit64(uint64_t x, int b, uint64_t v) {
     const uint64_t lo = x & ((1ull << b) - 1);
     return ((x ^ lo) << 1) | (v << b) | lo;
 }
+__device__ __forceinline__ uint64_t part_pos(const PartSpec &ps, uint64_t i, uint32_t b) {
+    for (int j = 0; j < ps.k; j++) i = insert_bit64(i, ps.l[j], (b >> j) & 1u);
+    return i;
+}
 
-// both shards in this process (group mode): swap element-wise in place
-// All three move U elements per thread per iteration, loads first (HBM
-// latency hiding; the same pattern as k_pair).
+// both shards in this process (group mode): part va of shard a <-> part vb
+// of shard b, element-wise in place.  All three kernels move U elements per
+// thread per iteration, loads first (HBM latency hiding, as k_pair).
 constexpr int MOVE_U = 4;
-__global__ void __launch_bounds__(256) k_swap_halves(double2 *__restrict__ a, double2 *__restrict__ b, int l,
-                                                     int va, int vb, uint64_t half) {
+__global__ void __launch_bounds__(256) k_swap_parts(double2 *__restrict__ a, double2 *__restrict__ b, PartSpec ps,
+                                                    uint32_t va, uint32_t vb, uint64_t cnt) {
     const uint64_t stride = (uint64_t)gridDim.x * 256;
-    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < half; i += MOVE_U * stride) {
+    for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < cnt; i += MOVE_U * stride) {
         uint64_t pa[MOVE_U], pb[MOVE_U];
         double2 x[MOVE_U], y[MOVE_U];
 #pragma unroll
         for (int u = 0; u < MOVE_U; u++) {
             const uint64_t j = i + u * stride;
-            pa[u] = insert_bit64(j, l, (uint64_t)va);
-            pb[u] = insert_bit64(j, l, (uint64_t)vb);
-            if (j < half) { x[u] = a[pa[u]]; y[u] = b[pb[u]]; }
+            pa[u] = part_pos(ps, j, va);
+            pb[u] = part_pos(ps, j, vb);
+            if (j < cnt) { x[u] = a[pa[u]]; y[u] = b[pb[u]]; }
         }
 #pragma unroll
         for (int u = 0; u < MOVE_U; u++)
-            if (i + u * stride < half) { a[pa[u]] = y[u]; b[pb[u]] = x[u]; }
+            if (i + u * stride < cnt) { a[pa[u]] = y[u]; b[pb[u]] = x[u]; }
     }
 }
 
-// NCCL mode: chunk [off, off + cnt) of the outgoing half -> contiguous staging, and back
-__global__ void __launch_bounds__(256) k_pack_half(const double2 *__restrict__ src, double2 *__restrict__ dst, int l,
-                                                   int v, uint64_t off, uint64_t cnt) {
+// NCCL mode: chunk [off, off + cnt) of every outgoing part -> contiguous
+// staging (blockIdx.y = peer slot p: part b = p < own ? p : p + 1), and back
+__global__ void __launch_bounds__(256) k_pack_parts(const double2 *__restrict__ src, double2 *__restrict__ dst,
+                                                    PartSpec ps, uint32_t own, uint64_t off, uint64_t cnt) {
+    const uint32_t p = blockIdx.y, bv = p < own ? p : p + 1;
+    double2 *d = dst + (uint64_t)p * cnt;
     const uint64_t stride = (uint64_t)gridDim.x * 256;
     for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < cnt; i += MOVE_U * stride) {
         double2 x[MOVE_U];
 #pragma unroll
         for (int u = 0; u < MOVE_U; u++)
-            if (i + u * stride < cnt) x[u] = src[insert_bit64(off + i + u * stride, l, (uint64_t)v)];
+            if (i + u * stride < cnt) x[u] = src[part_pos(ps, off + i + u * stride, bv)];
 #pragma unroll
         for (int u = 0; u < MOVE_U; u++)
-            if (i + u * stride < cnt) dst[i + u * stride] = x[u];
+            if (i + u * stride < cnt) d[i + u * stride] = x[u];
     }
 }
-__global__ void __launch_bounds__(256) k_unpack_half(double2 *__restrict__ dst, const double2 *__restrict__ src, int l,
-                                                     int v, uint64_t off, uint64_t cnt) {
+__global__ void __launch_bounds__(256) k_unpack_parts(double2 *__restrict__ dst, const double2 *__restrict__ src,
+                                                      PartSpec ps, uint32_t own, uint64_t off, uint64_t cnt) {
+    const uint32_t p = blockIdx.y, bv = p < own ? p : p + 1;
+    const double2 *s = src + (uint64_t)p * cnt;
     const uint64_t stride = (uint64_t)gridDim.x * 256;
     for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < cnt; i += MOVE_U * stride) {
         double2 x[MOVE_U];
 #pragma unroll
         for (int u = 0; u < MOVE_U; u++)
-            if (i + u * stride < cnt) x[u] = src[i + u * stride];
+            if (i + u * stride < cnt) x[u] = s[i + u * stride];
 #pragma unroll
         for (int u = 0; u < MOVE_U; u++)
-            if (i + u * stride < cnt) dst[insert_bit64(off + i + u * stride, l, (uint64_t)v)] = x[u];
+            if (i + u * stride < cnt) dst[part_pos(ps, off + i + u * stride, bv)] = x[u];
     }
 }
 

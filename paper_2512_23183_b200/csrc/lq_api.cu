@@ -7,8 +7,12 @@
 // returns LQ_ERR_CUDA.
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <thread>
 #include <cstddef>
 #include <list>
 #include <memory>
@@ -43,6 +47,8 @@ std::atomic<int64_t> g_opt_regbits{4};
 std::atomic<int64_t> g_opt_jit{1};
 std::atomic<int64_t> g_opt_first_free{1};   // PSR plans: the |0...0> pass is exempt from the budget
 std::atomic<int64_t> g_opt_poison{0};   // LQ_OPT_POISON_ALLOC
+std::atomic<int64_t> g_opt_comm_timeout{600000};   // LQ_OPT_COMM_TIMEOUT_MS
+std::atomic<int64_t> g_opt_swap_k{4};   // LQ_OPT_SWAP_QUBITS: qubits per global exchange (dist.h)
 std::atomic<int64_t> g_opt_budget{400};   // keeps passes from turning compute-bound (swept; 350 gains 0.4 % on config 4 but costs 5-12 % on Trotter / random circuits)
 const double PI = 3.14159265358979323846264338327950288;
 
@@ -65,13 +71,13 @@ lq_status fail(lq_status s, const std::string &msg) {
     } while (0)
 
 // ---- optional per-launch CUDA-event timing (LQ_OPT_KERNEL_TIMING) ----
-enum KClass { KC_TILE = 0, KC_PAIR = 1, KC_DIAG = 2, KC_PAULI = 3, KC_OTHER = 4, KC_N = 5 };
+enum KClass { KC_TILE = 0, KC_PAIR = 1, KC_DIAG = 2, KC_PAULI = 3, KC_OTHER = 4, KC_SWAP = 5, KC_N = 6 };
 std::atomic<int64_t> g_opt_timing{0};
 struct TimedLaunch { int cls; cudaEvent_t a, b; };
 std::vector<TimedLaunch> g_timed;
 std::vector<cudaEvent_t> g_event_pool;
-double g_time_ms[KC_N] = {0, 0, 0, 0, 0};
-uint64_t g_time_cnt[KC_N] = {0, 0, 0, 0, 0};
+double g_time_ms[KC_N] = {0, 0, 0, 0, 0, 0};
+uint64_t g_time_cnt[KC_N] = {0, 0, 0, 0, 0, 0};
 
 cudaEvent_t pool_event() {
     if (!g_event_pool.empty()) {
@@ -98,6 +104,13 @@ struct LaunchTimer {
         }
     }
 };
+// NVTX ranges (nsys / ncu --nvtx): one per tile pass launch, exchange and
+// collective; a no-op unless a tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 void harvest_timing() {
     for (auto &t : g_timed) {
         float ms = 0.f;
@@ -444,6 +457,7 @@ lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, cons
     }
     const unsigned grid = (unsigned)std::min<uint64_t>(total, (uint64_t)n_sm * (uint64_t)per_sm);
     LaunchTimer lt_(KC_TILE, st);
+    NvtxRange nr_("lq tile pass");
     if ((kp.flags & PF_EXPV) && !partials) return fail(LQ_ERR_STATE, "expectation pass without partial buffer");
     if (jk) {   // JIT-specialised program of this pass (jit.h): same parameters as k_tile
         uint32_t tot32 = (uint32_t)total;
@@ -634,8 +648,11 @@ QMap to_qmap(int n, const int32_t *qm) {
 
 // ---------------------------------------------------------------- handles
 struct lq_comm {
-    ncclComm_t c = nullptr;
+    ncclComm_t c = nullptr;          // nullptr: a partition-only comm (lq_comm_init_local) or aborted
     int rank = 0, world = 1;
+    bool local = false;              // lq_comm_init_local: no transport, collectives are the identity
+    bool dead = false;               // aborted after an asynchronous NCCL error or a timeout
+    std::string why;                 // the failure that killed it
 };
 
 struct lq_sv {
@@ -652,6 +669,13 @@ struct lq_sv {
     std::vector<double2 *> shards;   // this process's shards (group mode: all G)
     uint32_t xmask = 0;              // rank relabel: rank r holds physical global bits r ^ xmask
     DevBuf mats_buf, part_buf, stage_buf, ctab_buf;
+    // exchange pipeline (NCCL mode): a second stream carries the transfers
+    // while this handle's stream packs the next chunk and unpacks the last
+    cudaStream_t xs = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_packed[2] = {nullptr, nullptr}, ev_moved[2] = {nullptr, nullptr};
+    uint64_t stat_exchanges = 0, stat_bytes_sent = 0;   // per rank (group mode: per shard)
+    bool dead = false;               // poisoned after an asynchronous CUDA / NCCL failure
+    std::string why;
     void reset_map() {
         for (int q = 0; q < n; q++) qmap[q] = n - 1 - q;
         xmask = 0;
@@ -662,7 +686,21 @@ struct lq_sv {
 namespace {
 lq_status check_sv(const lq_sv *sv) {
     if (!sv || !sv->d) return fail(LQ_ERR_ARG, "invalid state handle");
+    if (sv->dead) return fail(LQ_ERR_STATE, "state handle unusable after an earlier asynchronous failure: " + sv->why);
+    if (sv->comm && sv->comm->dead)
+        return fail(LQ_ERR_STATE, "communicator aborted after an earlier failure: " + sv->comm->why);
     return LQ_OK;
+}
+
+// An asynchronous CUDA or NCCL failure leaves the handle's contents
+// undefined: every later call on it returns LQ_ERR_STATE.
+// Validation errors and OOM leave it usable.
+lq_status seal(lq_sv *sv, lq_status s) {
+    if (sv && (s == LQ_ERR_CUDA || s == LQ_ERR_NCCL)) {
+        sv->dead = true;
+        sv->why = g_err;
+    }
+    return s;
 }
 
 // Run a circuit-level plan on one state (apply_circuit / canonicalize / qft).
@@ -735,6 +773,8 @@ struct NcclApi {
     decltype(&ncclRecv) Recv = nullptr;
     decltype(&ncclAllReduce) AllReduce = nullptr;
     decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
+    decltype(&ncclCommAbort) CommAbort = nullptr;
 };
 NcclApi &nccl() {
     static NcclApi a = [] {
@@ -748,7 +788,8 @@ NcclApi &nccl() {
         }
 #define LQ_SYM(f) x.f = reinterpret_cast<decltype(x.f)>(dlsym(h, "nccl" #f)); if (!x.f) { x.why = "missing nccl" #f; return x; }
         LQ_SYM(GetUniqueId) LQ_SYM(CommInitRank) LQ_SYM(CommDestroy) LQ_SYM(GroupStart) LQ_SYM(GroupEnd)
-        LQ_SYM(Send) LQ_SYM(Recv) LQ_SYM(AllReduce) LQ_SYM(GetErrorString)
+        LQ_SYM(Send) LQ_SYM(Recv) LQ_SYM(AllReduce) LQ_SYM(GetErrorString) LQ_SYM(CommGetAsyncError)
+        LQ_SYM(CommAbort)
 #undef LQ_SYM
         x.ok = true;
         return x;
@@ -760,6 +801,49 @@ NcclApi &nccl() {
         ncclResult_t r_ = (x);                                                                  \
         if (r_ != ncclSuccess) return fail(LQ_ERR_NCCL, std::string(#x) + ": " + nccl().GetErrorString(r_)); \
     } while (0)
+
+// Wait for the stream's work when it includes NCCL operations: poll the
+// stream and ncclCommGetAsyncError instead of blocking, so a dead or stuck
+// peer surfaces as LQ_ERR_NCCL after LQ_OPT_COMM_TIMEOUT_MS instead of a
+// hang; the communicator is then aborted (later calls: LQ_ERR_STATE).
+lq_status comm_abort(lq_comm *c, const std::string &why) {
+    if (c->c) nccl().CommAbort(c->c);
+    c->c = nullptr;
+    c->dead = true;
+    c->why = why;
+    return fail(LQ_ERR_NCCL, why);
+}
+lq_status comm_sync(lq_comm *c, cudaStream_t s) {
+    if (!c || !c->c) return sync(s);
+    const auto t0 = std::chrono::steady_clock::now();
+    const int64_t limit_ms = g_opt_comm_timeout.load();
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaSuccess) break;
+        if (e != cudaErrorNotReady) {
+            cudaGetLastError();
+            return fail(LQ_ERR_CUDA, std::string("stream failed during a collective: ") + cudaGetErrorString(e));
+        }
+        ncclResult_t ar = ncclSuccess;
+        nccl().CommGetAsyncError(c->c, &ar);
+        if (ar != ncclSuccess && ar != ncclInProgress)
+            return comm_abort(c, std::string("asynchronous NCCL error: ") + nccl().GetErrorString(ar));
+        const int64_t ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+        if (limit_ms > 0 && ms > limit_ms)
+            return comm_abort(c, "collective did not complete within " + std::to_string(limit_ms) + " ms (peer lost?)");
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    CUDA_TRY(cudaGetLastError());
+    return LQ_OK;
+}
+lq_status comm_check(lq_comm *c) {
+    if (!c || !c->c) return LQ_OK;
+    ncclResult_t ar = ncclSuccess;
+    nccl().CommGetAsyncError(c->c, &ar);
+    if (ar != ncclSuccess && ar != ncclInProgress)
+        return comm_abort(c, std::string("asynchronous NCCL error: ") + nccl().GetErrorString(ar));
+    return LQ_OK;
+}
 
 // ---------------------------------------------------------------- sharded states
 lq_status sh_check(int n, int world) {
@@ -784,46 +868,99 @@ lq_status sh_sum(lq_sv *sv, const double *dev_vals, double *out) {
         LQ_TRY(sv->stage_buf.reserve(sizeof(double), sv->stream));
         double *d = sv->stage_buf.at<double>(0);
         CUDA_TRY(cudaMemcpyAsync(d, &acc, sizeof(double), cudaMemcpyHostToDevice, sv->stream));
+        LQ_TRY(comm_check(sv->comm));
         NCCL_TRY(nccl().AllReduce(d, d, 1, ncclFloat64, ncclSum, sv->comm->c, sv->stream));
         CUDA_TRY(cudaMemcpyAsync(&acc, d, sizeof(double), cudaMemcpyDeviceToHost, sv->stream));
-        LQ_TRY(sync(sv->stream));
+        LQ_TRY(comm_sync(sv->comm, sv->stream));
     }
     *out = acc;
     return LQ_OK;
 }
 
-// global-qubit swap: global physical bit g <-> local bit l
-constexpr uint64_t SWAP_CHUNK = 1ull << 24;   // amplitudes per staged NCCL message (256 MiB)
-lq_status sh_swap(lq_sv *sv, int g, int l, uint32_t xmask) {
-    const int j = g - sv->nl;
-    const uint64_t half = 1ull << (sv->nl - 1);
+// global-qubit exchange: k global physical bits
+// g_j <-> k local bits l_j (dist.h).  Rank r (physical global bits r ^
+// xmask, g-value a) sends part b of its shard to the rank whose g-value is b
+// and receives that rank's part a into the same positions.
+constexpr uint64_t SWAP_CHUNK = 1ull << 22;   // amplitudes per part per staged NCCL message (64 MiB)
+lq_status sh_swap(lq_sv *sv, const DStep &stp) {
+    const int k = stp.k, nl = sv->nl;
+    PartSpec ps;
+    memset(&ps, 0, sizeof(ps));
+    ps.k = k;
+    for (int j = 0; j < k; j++) ps.l[j] = stp.l[j];
+    const uint64_t part = 1ull << (nl - k);
+    const uint32_t np = (1u << k) - 1;   // parts that leave (= peers)
+    auto gval = [&](int rank) {
+        const uint32_t R = (uint32_t)rank ^ stp.xmask;
+        uint32_t a = 0;
+        for (int j = 0; j < k; j++) a |= ((R >> (stp.g[j] - nl)) & 1u) << j;
+        return a;
+    };
+    auto peer_of = [&](int rank, uint32_t a, uint32_t b) {
+        const uint32_t d = a ^ b;
+        for (int j = 0; j < k; j++)
+            if (d >> j & 1) rank ^= 1 << (stp.g[j] - nl);
+        return rank;
+    };
     cudaStream_t st = sv->stream;
-    if (!sv->comm) {   // group mode: every pair lives in this process
+    LaunchTimer lt_(KC_SWAP, st);
+    NvtxRange nr_("lq exchange");
+    sv->stat_exchanges++;
+    sv->stat_bytes_sent += (uint64_t)np * part * sizeof(double2);
+    if (!sv->comm) {   // group mode: every rank of the group lives in this process
         const int G = (int)sv->shards.size();
-        for (int k = 0; k < G; k++) {
-            const int p = k ^ (1 << j);
-            if (p < k) continue;
-            const int bk = ((k ^ (int)xmask) >> j) & 1;   // k's physical g-bit; p has the other value
-            k_swap_halves<<<grid_for(half), 256, 0, st>>>(sv->shards[k], sv->shards[p], l, 1 - bk, bk, half);
-            LQ_TRY(check_launch("k_swap_halves"));
+        for (int r = 0; r < G; r++) {
+            const uint32_t a = gval(r);
+            for (uint32_t b = 0; b < (1u << k); b++) {
+                if (b == a) continue;
+                const int r2 = peer_of(r, a, b);
+                if (r2 < r) continue;   // each pair of regions once: (r, part b) <-> (r2, part a)
+                k_swap_parts<<<grid_for(part), 256, 0, st>>>(sv->shards[r], sv->shards[r2], ps, b, a, part);
+                LQ_TRY(check_launch("k_swap_parts"));
+            }
         }
         return LQ_OK;
     }
-    const int rank = sv->comm->rank, peer = rank ^ (1 << j);
-    const int v = 1 - (((rank ^ (int)xmask) >> j) & 1);   // the half this rank gives away (and refills)
-    const uint64_t ch = std::min(half, SWAP_CHUNK);
-    LQ_TRY(sv->stage_buf.reserve(2 * ch * sizeof(double2), st));
-    double2 *out = sv->stage_buf.at<double2>(0), *in = out + ch;
-    for (uint64_t off = 0; off < half; off += ch) {
-        const uint64_t cnt = std::min(ch, half - off);
-        k_pack_half<<<grid_for(cnt), 256, 0, st>>>(sv->shards[0], out, l, v, off, cnt);
-        LQ_TRY(check_launch("k_pack_half"));
+    LQ_TRY(comm_check(sv->comm));
+    const int rank = sv->comm->rank;
+    const uint32_t a = gval(rank);
+    const uint64_t ch = std::min(part, SWAP_CHUNK), nch = part / ch;
+    LQ_TRY(sv->stage_buf.reserve(4 * (size_t)np * ch * sizeof(double2), st));
+    double2 *out[2] = {sv->stage_buf.at<double2>(0), sv->stage_buf.at<double2>(np * ch * sizeof(double2))};
+    double2 *in[2] = {out[1] + np * ch, out[1] + 2 * np * ch};
+    if (!sv->xs) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&sv->xs, cudaStreamNonBlocking));
+        cudaEvent_t *evs[5] = {&sv->ev_start, &sv->ev_packed[0], &sv->ev_packed[1], &sv->ev_moved[0], &sv->ev_moved[1]};
+        for (cudaEvent_t *e : evs) CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    int peers[15];
+    for (uint32_t p = 0; p < np; p++) peers[p] = peer_of(rank, a, p < a ? p : p + 1);
+    // Pipeline: the transfer of chunk c (stream xs) overlaps the unpack of
+    // chunk c-1 and the pack of chunk c+1 (handle stream).  Two staging
+    // slots; chunk c+1's pack reuses the slot of chunk c-1, whose transfer
+    // the handle stream waited for before unpacking it.
+    CUDA_TRY(cudaEventRecord(sv->ev_start, st));
+    CUDA_TRY(cudaStreamWaitEvent(sv->xs, sv->ev_start, 0));
+    auto pack = [&](uint64_t c) -> lq_status {
+        k_pack_parts<<<dim3(grid_for(ch), np), 256, 0, st>>>(sv->shards[0], out[c & 1], ps, a, c * ch, ch);
+        LQ_TRY(check_launch("k_pack_parts"));
+        CUDA_TRY(cudaEventRecord(sv->ev_packed[c & 1], st));
+        return LQ_OK;
+    };
+    LQ_TRY(pack(0));
+    for (uint64_t c = 0; c < nch; c++) {
+        if (c + 1 < nch) LQ_TRY(pack(c + 1));
+        CUDA_TRY(cudaStreamWaitEvent(sv->xs, sv->ev_packed[c & 1], 0));
         NCCL_TRY(nccl().GroupStart());
-        NCCL_TRY(nccl().Send(out, 2 * cnt, ncclFloat64, peer, sv->comm->c, st));
-        NCCL_TRY(nccl().Recv(in, 2 * cnt, ncclFloat64, peer, sv->comm->c, st));
+        for (uint32_t p = 0; p < np; p++) {
+            NCCL_TRY(nccl().Send(out[c & 1] + p * ch, 2 * ch, ncclFloat64, peers[p], sv->comm->c, sv->xs));
+            NCCL_TRY(nccl().Recv(in[c & 1] + p * ch, 2 * ch, ncclFloat64, peers[p], sv->comm->c, sv->xs));
+        }
         NCCL_TRY(nccl().GroupEnd());
-        k_unpack_half<<<grid_for(cnt), 256, 0, st>>>(sv->shards[0], in, l, v, off, cnt);
-        LQ_TRY(check_launch("k_unpack_half"));
+        CUDA_TRY(cudaEventRecord(sv->ev_moved[c & 1], sv->xs));
+        CUDA_TRY(cudaStreamWaitEvent(st, sv->ev_moved[c & 1], 0));
+        k_unpack_parts<<<dim3(grid_for(ch), np), 256, 0, st>>>(sv->shards[0], in[c & 1], ps, a, c * ch, ch);
+        LQ_TRY(check_launch("k_unpack_parts"));
     }
     return LQ_OK;
 }
@@ -871,7 +1008,7 @@ lq_status sh_run(lq_sv *sv, Schedule &sc, const double *theta, size_t n_theta, d
     for (size_t i = 0; i < sc.steps.size(); i++) {
         const DStep &stp = sc.steps[i];
         if (stp.kind == 1) {
-            LQ_TRY(sh_swap(sv, stp.g, stp.l, stp.xmask));
+            LQ_TRY(sh_swap(sv, stp));
             continue;
         }
         DevPlan dp;
@@ -962,9 +1099,10 @@ lq_status sh_gather(lq_sv *sv, const uint64_t *idx, uint64_t offset, uint64_t co
         LQ_TRY(sv->stage_buf.reserve(count * sizeof(double2), st));
         double *d = sv->stage_buf.at<double>(0);
         CUDA_TRY(cudaMemcpyAsync(d, res.data(), count * sizeof(double2), cudaMemcpyHostToDevice, st));
+        LQ_TRY(comm_check(sv->comm));
         NCCL_TRY(nccl().AllReduce(d, d, 2 * count, ncclFloat64, ncclSum, sv->comm->c, st));
         CUDA_TRY(cudaMemcpyAsync(res.data(), d, count * sizeof(double2), cudaMemcpyDeviceToHost, st));
-        LQ_TRY(sync(st));
+        LQ_TRY(comm_sync(sv->comm, st));
     }
     memcpy(host_out, res.data(), count * sizeof(double2));
     return LQ_OK;
@@ -1051,6 +1189,14 @@ lq_status lq_set_option(int option, int64_t value) {
         return LQ_OK;
     case LQ_OPT_FIRST_PASS_FREE: g_opt_first_free = value ? 1 : 0; return LQ_OK;
     case LQ_OPT_POISON_ALLOC: g_opt_poison = value ? 1 : 0; return LQ_OK;
+    case LQ_OPT_COMM_TIMEOUT_MS:
+        if (value < 0) return fail(LQ_ERR_ARG, "timeout must be >= 0 (0 = wait forever)");
+        g_opt_comm_timeout = value;
+        return LQ_OK;
+    case LQ_OPT_SWAP_QUBITS:
+        if (value < 1 || value > 4) return fail(LQ_ERR_ARG, "qubits per exchange must be 1..4");
+        g_opt_swap_k = value;
+        return LQ_OK;
     default: return fail(LQ_ERR_ARG, "unknown option");
     }
 }
@@ -1066,6 +1212,8 @@ int64_t lq_get_option(int option) {
     case LQ_OPT_PASS_BUDGET: return g_opt_budget.load();
     case LQ_OPT_FIRST_PASS_FREE: return g_opt_first_free.load();
     case LQ_OPT_POISON_ALLOC: return g_opt_poison.load();
+    case LQ_OPT_COMM_TIMEOUT_MS: return g_opt_comm_timeout.load();
+    case LQ_OPT_SWAP_QUBITS: return g_opt_swap_k.load();
     default: return -1;
     }
 }
@@ -1138,6 +1286,34 @@ lq_status lq_comm_init(const void *unique_id, size_t len, int rank, int world, l
         return fail(LQ_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
     }
     *out = c;
+    return LQ_OK;
+}
+
+lq_status lq_comm_init_local(int rank, int world, lq_comm **out) {
+    if (!out) return fail(LQ_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return fail(LQ_ERR_ARG, "bad rank/world");
+    lq_comm *c = new lq_comm();
+    c->rank = rank;
+    c->world = world;
+    c->local = true;
+    *out = c;
+    return LQ_OK;
+}
+
+lq_status lq_comm_info(const lq_comm *c, int *rank, int *world, int *has_transport) {
+    if (!c) return fail(LQ_ERR_ARG, "comm is NULL");
+    if (c->dead) return fail(LQ_ERR_STATE, "communicator aborted after an earlier failure: " + c->why);
+    if (rank) *rank = c->rank;
+    if (world) *world = c->world;
+    if (has_transport) *has_transport = c->c != nullptr;
+    return LQ_OK;
+}
+
+lq_status lq_sv_exchange_stats(const lq_sv *sv, uint64_t *n_exchanges, uint64_t *bytes_sent_per_rank) {
+    if (!sv) return fail(LQ_ERR_ARG, "invalid state handle");
+    if (n_exchanges) *n_exchanges = sv->stat_exchanges;
+    if (bytes_sent_per_rank) *bytes_sent_per_rank = sv->stat_bytes_sent;   // every rank sends the same amount
     return LQ_OK;
 }
 
@@ -1215,6 +1391,7 @@ lq_status lq_dist_schedule_json(int n_qubits, int log2_world, const lq_gate *gat
     sc.n = n_qubits;
     sc.m = log2_world;
     sc.nl = n_qubits - log2_world;
+    sc.max_k = (int)g_opt_swap_k.load();
     int32_t qm[64];
     for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
     uint32_t xm = 0;
@@ -1244,6 +1421,12 @@ lq_status lq_sv_free(lq_sv *sv) {
     sv->part_buf.release(sv->stream);
     sv->stage_buf.release(sv->stream);
     sv->ctab_buf.release(sv->stream);
+    if (sv->xs) {
+        cudaStreamSynchronize(sv->stream);
+        cudaStreamDestroy(sv->xs);
+        for (cudaEvent_t ev : {sv->ev_start, sv->ev_packed[0], sv->ev_packed[1], sv->ev_moved[0], sv->ev_moved[1]})
+            if (ev) cudaEventDestroy(ev);
+    }
     cudaError_t e = cudaSuccess;
     if (!sv->shards.empty()) {
         cudaStreamSynchronize(sv->stream);
@@ -1281,7 +1464,7 @@ lq_status lq_sv_qubit_map(const lq_sv *sv, int32_t *map_out) {
     return LQ_OK;
 }
 
-lq_status lq_sv_init_basis(lq_sv *sv, uint64_t k) {
+static lq_status sv_init_basis_body(lq_sv *sv, uint64_t k) {
     LQ_TRY(check_sv(sv));
     if (k >= (1ull << sv->n)) return fail(LQ_ERR_ARG, "basis index out of range");
     sv->reset_map();
@@ -1300,7 +1483,7 @@ lq_status lq_sv_init_basis(lq_sv *sv, uint64_t k) {
     return check_launch("k_fill_basis");
 }
 
-lq_status lq_sv_init_random(lq_sv *sv, uint64_t seed) {
+static lq_status sv_init_random_body(lq_sv *sv, uint64_t seed) {
     LQ_TRY(check_sv(sv));
     sv->reset_map();
     if (sv->m) {   // norm over all shards (sh_sum), then each shard writes its range
@@ -1334,7 +1517,7 @@ lq_status lq_sv_init_random(lq_sv *sv, uint64_t seed) {
     return check_launch("k_random_write");
 }
 
-lq_status lq_sv_norm2(lq_sv *sv, double *out) {
+static lq_status sv_norm2_body(lq_sv *sv, double *out) {
     LQ_TRY(check_sv(sv));
     if (!out) return fail(LQ_ERR_ARG, "out is NULL");
     if (sv->m) {
@@ -1382,7 +1565,7 @@ static lq_status read_impl(lq_sv *sv, const uint64_t *idx, uint64_t offset, uint
     return LQ_OK;
 }
 
-lq_status lq_sv_read(lq_sv *sv, uint64_t offset, uint64_t count, double *host_out) {
+static lq_status sv_read_body(lq_sv *sv, uint64_t offset, uint64_t count, double *host_out) {
     LQ_TRY(check_sv(sv));
     if (!host_out && count) return fail(LQ_ERR_ARG, "host_out is NULL");
     uint64_t N = 1ull << sv->n;
@@ -1392,7 +1575,7 @@ lq_status lq_sv_read(lq_sv *sv, uint64_t offset, uint64_t count, double *host_ou
     return read_impl(sv, nullptr, offset, count, host_out);
 }
 
-lq_status lq_sv_gather(lq_sv *sv, const uint64_t *idx, size_t count, double *host_out) {
+static lq_status sv_gather_body(lq_sv *sv, const uint64_t *idx, size_t count, double *host_out) {
     LQ_TRY(check_sv(sv));
     if (count && (!idx || !host_out)) return fail(LQ_ERR_ARG, "NULL buffer");
     uint64_t N = 1ull << sv->n;
@@ -1403,7 +1586,7 @@ lq_status lq_sv_gather(lq_sv *sv, const uint64_t *idx, size_t count, double *hos
     return read_impl(sv, idx, 0, count, host_out);
 }
 
-lq_status lq_sv_write(lq_sv *sv, uint64_t offset, uint64_t count, const double *host_in) {
+static lq_status sv_write_body(lq_sv *sv, uint64_t offset, uint64_t count, const double *host_in) {
     LQ_TRY(check_sv(sv));
     if (sv->m) return fail(LQ_ERR_ARG, "lq_sv_write is not supported on sharded states");
     if (!host_in && count) return fail(LQ_ERR_ARG, "host_in is NULL");
@@ -1425,7 +1608,7 @@ lq_status lq_sv_write(lq_sv *sv, uint64_t offset, uint64_t count, const double *
     return LQ_OK;
 }
 
-lq_status lq_sv_canonicalize(lq_sv *sv) {
+static lq_status sv_canonicalize_body(lq_sv *sv) {
     LQ_TRY(check_sv(sv));
     if (sv->m) return fail(LQ_ERR_ARG, "lq_sv_canonicalize is not supported on sharded states (reads resolve the layout)");
     return canonicalize(sv);
@@ -1442,6 +1625,7 @@ lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const doub
         sc.n = sv->n;
         sc.m = sv->m;
         sc.nl = sv->nl;
+        sc.max_k = (int)g_opt_swap_k.load();
         int32_t qm[64];
         memcpy(qm, sv->qmap, sizeof(qm));
         uint32_t xm = sv->xmask;
@@ -1473,13 +1657,13 @@ lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const doub
 
 extern "C" {
 
-lq_status lq_apply_circuit(lq_sv *sv, const lq_gate *gates, size_t n_gates, const double *theta, size_t n_theta) {
+static lq_status apply_circuit_body(lq_sv *sv, const lq_gate *gates, size_t n_gates, const double *theta, size_t n_theta) {
     LQ_TRY(check_sv(sv));
     LQ_TRY(validate_gates(sv->n, gates, n_gates, theta, n_theta, true, nullptr));
     return apply_impl(sv, gates, n_gates, theta, n_theta);
 }
 
-lq_status lq_qft(lq_sv *sv, int inverse) {
+static lq_status qft_body(lq_sv *sv, int inverse) {
     LQ_TRY(check_sv(sv));
     int32_t qm[64];
     memcpy(qm, sv->qmap, sizeof(qm));
@@ -1513,7 +1697,7 @@ lq_status lq_qft(lq_sv *sv, int inverse) {
     return LQ_OK;
 }
 
-lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_terms, double *out_energy) {
+static lq_status expval_pauli_sum_body(lq_sv *sv, const lq_pauli_term *terms, size_t n_terms, double *out_energy) {
     LQ_TRY(check_sv(sv));
     if (!out_energy) return fail(LQ_ERR_ARG, "out_energy is NULL");
     LQ_TRY(validate_terms(sv->n, terms, n_terms));
@@ -1522,6 +1706,7 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
         sc.n = sv->n;
         sc.m = sv->m;
         sc.nl = sv->nl;
+        sc.max_k = (int)g_opt_swap_k.load();
         int32_t qm[64];
         memcpy(qm, sv->qmap, sizeof(qm));
         uint32_t xm = sv->xmask;
@@ -1581,7 +1766,7 @@ lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_te
 // to 8 steps share one cached plan whatever h(t) is, and the planner fuses
 // across step boundaries.  E(t) = E_int - h(t) M with E_int = <-sum J PP>
 // and M = <sum Z_i> (two cached expectation plans).
-lq_status lq_trotter_xyz(lq_sv *sv, const lq_xyz_model *mdl, double t0, double dt, int n_steps, int record_every,
+static lq_status trotter_xyz_body(lq_sv *sv, const lq_xyz_model *mdl, double t0, double dt, int n_steps, int record_every,
                          double *energy_out) {
     LQ_TRY(check_sv(sv));
     if (!mdl) return fail(LQ_ERR_ARG, "model is NULL");
@@ -1683,6 +1868,10 @@ struct lq_psr {
     int n = 0;
     size_t n_params = 0;
     int rank = 0, world = 1;
+    lq_comm *comm = nullptr;   // NCCL: the gradient and E are all-reduced inside lq_psr_run
+    bool dead = false;         // poisoned by an asynchronous failure
+    std::string why;
+    DevBuf red;                // n_params + 1 doubles: this rank's share, then the sum
     cudaStream_t stream = nullptr;
     Plan plan;
     MatBuilder mb;
@@ -1703,12 +1892,12 @@ struct lq_psr {
 extern "C" {
 
 lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, size_t n_params,
-                        const lq_pauli_term *terms, size_t n_terms, int shard_rank, int shard_world,
-                        void *cuda_stream, lq_psr **out) {
+                        const lq_pauli_term *terms, size_t n_terms, lq_comm *comm, void *cuda_stream, lq_psr **out) {
     if (!out) return fail(LQ_ERR_ARG, "out is NULL");
     *out = nullptr;
     if (n_qubits < 1 || n_qubits > 36) return fail(LQ_ERR_ARG, "n_qubits must be in [1, 36]");
-    if (shard_world < 1 || shard_rank < 0 || shard_rank >= shard_world) return fail(LQ_ERR_ARG, "bad shard rank/world");
+    if (comm && comm->dead) return fail(LQ_ERR_STATE, "communicator aborted after an earlier failure: " + comm->why);
+    const int shard_rank = comm ? comm->rank : 0, shard_world = comm ? comm->world : 1;
     std::vector<int> uses(n_params, 0);
     LQ_TRY(validate_gates(n_qubits, ansatz, n_gates, nullptr, n_params, false, &uses));
     LQ_TRY(validate_terms(n_qubits, terms, n_terms));
@@ -1718,6 +1907,7 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     P->n_params = n_params;
     P->rank = shard_rank;
     P->world = shard_world;
+    P->comm = comm;
     P->stream = (cudaStream_t)cuda_stream;
     int32_t qm[64];
     for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
@@ -1788,6 +1978,7 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     if (s == LQ_OK) s = P->mats.reserve((size_t)B * std::max<uint32_t>(P->mb.mat_size, 1) * sizeof(double2), st);
     if (s == LQ_OK) s = P->partials.reserve((size_t)B * P->dset.stride() * sizeof(double), st);
     if (s == LQ_OK) s = P->E.reserve(sizeof(double) * std::max(n_circ, 1), st);
+    if (s == LQ_OK) s = P->red.reserve(sizeof(double) * (n_params + 1), st);
     if (s == LQ_OK && P->plan.ctab_total) s = P->ctab.reserve((size_t)P->plan.ctab_total * sizeof(double2), st);
     if (s != LQ_OK) {
         std::string keep = g_err;
@@ -1814,9 +2005,23 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     return LQ_OK;
 }
 
+static lq_status psr_run_body(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev);
+
 lq_status lq_psr_run(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev) {
     if (!P) return fail(LQ_ERR_ARG, "invalid plan");
+    if (P->dead) return fail(LQ_ERR_STATE, "gradient plan unusable after an earlier asynchronous failure: " + P->why);
+    if (P->comm && P->comm->dead)
+        return fail(LQ_ERR_STATE, "communicator aborted after an earlier failure: " + P->comm->why);
     if ((!theta_dev && P->n_params) || (!grad_dev && P->n_params)) return fail(LQ_ERR_ARG, "NULL device pointer");
+    const lq_status s = psr_run_body(P, theta_dev, grad_dev, energy_dev);
+    if (s == LQ_ERR_CUDA || s == LQ_ERR_NCCL) {
+        P->dead = true;
+        P->why = g_err;
+    }
+    return s;
+}
+
+static lq_status psr_run_body(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev) {
     const uint64_t N = 1ull << P->n;
     const int n_circ = (int)P->shifts.size();
     cudaStream_t st = P->stream;
@@ -1840,9 +2045,28 @@ lq_status lq_psr_run(lq_psr *P, const double *theta_dev, double *grad_dev, doubl
         LQ_TRY(launch_passes(P->plan, P->dp, states, N, nb, mats, ms, st, true, part, ss, P->dset.ds.empty()));
         LQ_TRY(finish_expv(P->plan, P->dset, P->d_terms, states, N, nb, part, ss, E + c0, st));
     }
-    k_psr_combine<<<1, 256, 0, st>>>(E, P->d_pairs, (int)P->pairs.size(), P->base_idx, grad_dev, (int)P->n_params,
-                                     energy_dev);
-    LQ_TRY(check_launch("k_psr_combine"));
+    if (!P->comm || !P->comm->c) {
+        k_psr_combine<<<1, 256, 0, st>>>(E, P->d_pairs, (int)P->pairs.size(), P->base_idx, grad_dev,
+                                         (int)P->n_params, energy_dev);
+        LQ_TRY(check_launch("k_psr_combine"));
+    } else {
+        // Each component (and E, on rank 0) comes from exactly one rank and is
+        // 0 elsewhere, so one sum over ranks returns the 1-GPU result exactly,
+        // on every rank.
+        double *red = P->red.at<double>(0);
+        k_psr_combine<<<1, 256, 0, st>>>(E, P->d_pairs, (int)P->pairs.size(), P->base_idx, red, (int)P->n_params,
+                                         red + P->n_params);
+        LQ_TRY(check_launch("k_psr_combine"));
+        LQ_TRY(comm_check(P->comm));
+        {
+            NvtxRange nr_("lq gradient all-reduce");
+            NCCL_TRY(nccl().AllReduce(red, red, P->n_params + 1, ncclFloat64, ncclSum, P->comm->c, st));
+        }
+        if (P->n_params)
+            CUDA_TRY(cudaMemcpyAsync(grad_dev, red, P->n_params * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        if (energy_dev)
+            CUDA_TRY(cudaMemcpyAsync(energy_dev, red + P->n_params, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
     P->launches_per_run = g_launches.load() - l0;
     return LQ_OK;
 }
@@ -1865,7 +2089,7 @@ lq_status lq_vqe_adam(int n_qubits, const lq_gate *ansatz, size_t n_gates, doubl
     for (size_t p = 0; p < n_params; p++)
         if (!std::isfinite(theta[p])) return fail(LQ_ERR_NONFINITE, "non-finite theta[" + std::to_string(p) + "]");
     lq_psr *P = nullptr;
-    LQ_TRY(lq_psr_create(n_qubits, ansatz, n_gates, n_params, terms, n_terms, 0, 1, cuda_stream, &P));
+    LQ_TRY(lq_psr_create(n_qubits, ansatz, n_gates, n_params, terms, n_terms, nullptr, cuda_stream, &P));
     cudaStream_t st = (cudaStream_t)cuda_stream;
     DevBuf buf;
     const size_t np = std::max<size_t>(n_params, 1);
@@ -1990,6 +2214,7 @@ lq_status lq_psr_free(lq_psr *P) {
     P->partials.release(P->stream);
     P->E.release(P->stream);
     P->ctab.release(P->stream);
+    P->red.release(P->stream);
     delete P;
     return LQ_OK;
 }
@@ -2009,11 +2234,12 @@ std::mutex g_psr_mu;
 std::vector<CachedPsr *> g_psr_cache;   // most recent last
 constexpr size_t PSR_CACHE_MAX = 2;
 
-std::string psr_key(int n, const lq_gate *g, size_t ng, size_t np, const lq_pauli_term *t, size_t nt, int rank,
-                    int world, void *stream) {
+std::string psr_key(int n, const lq_gate *g, size_t ng, size_t np, const lq_pauli_term *t, size_t nt,
+                    const lq_comm *comm, void *stream) {
     std::string k;
     auto put = [&](const void *p, size_t b) { k.append(static_cast<const char *>(p), b); };
-    int64_t hdr[8] = {n, (int64_t)ng, (int64_t)np, (int64_t)nt, rank, world, (int64_t)(intptr_t)stream, 0};
+    int64_t hdr[8] = {n, (int64_t)ng, (int64_t)np, (int64_t)nt, (int64_t)(intptr_t)comm,
+                      comm ? comm->rank : 0, (int64_t)(intptr_t)stream, comm ? comm->world : 1};
     put(hdr, sizeof(hdr));
     int64_t opt[7] = {g_opt_fusion.load(), g_opt_K.load(), g_opt_coalesce.load(), g_opt_regbits.load(),
                       g_opt_jit.load(), g_opt_budget.load(), g_opt_first_free.load()};
@@ -2043,8 +2269,9 @@ lq_status lq_psr_cache_clear(void) {
 }
 
 lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gates, const double *theta,
-                              size_t n_params, const lq_pauli_term *terms, size_t n_terms, int shard_rank,
-                              int shard_world, void *cuda_stream, double *grad_out, double *energy_out) {
+                              size_t n_params, const lq_pauli_term *terms, size_t n_terms, lq_comm *comm,
+                              void *cuda_stream, double *grad_out, double *energy_out) {
+    if (comm && comm->dead) return fail(LQ_ERR_STATE, "communicator aborted after an earlier failure: " + comm->why);
     if (n_params && (!theta || !grad_out)) return fail(LQ_ERR_ARG, "theta/grad_out is NULL");
     for (size_t p = 0; p < n_params; p++)
         if (!std::isfinite(theta[p])) return fail(LQ_ERR_NONFINITE, "non-finite theta[" + std::to_string(p) + "]");
@@ -2055,7 +2282,7 @@ lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gate
             return fail(LQ_ERR_ARG, "gate " + std::to_string(i) + ": matrix is NULL");
     std::lock_guard<std::mutex> lk(g_psr_mu);
     const std::string key =
-        psr_key(n_qubits, ansatz, n_gates, n_params, terms, n_terms, shard_rank, shard_world, cuda_stream);
+        psr_key(n_qubits, ansatz, n_gates, n_params, terms, n_terms, comm, cuda_stream);
     CachedPsr *C = nullptr;
     for (size_t i = 0; i < g_psr_cache.size(); i++)
         if (g_psr_cache[i]->key == key) {
@@ -2065,8 +2292,7 @@ lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gate
         }
     if (!C) {
         lq_psr *P = nullptr;
-        LQ_TRY(lq_psr_create(n_qubits, ansatz, n_gates, n_params, terms, n_terms, shard_rank, shard_world,
-                             cuda_stream, &P));
+        LQ_TRY(lq_psr_create(n_qubits, ansatz, n_gates, n_params, terms, n_terms, comm, cuda_stream, &P));
         C = new CachedPsr();
         C->key = key;
         C->P = P;
@@ -2104,7 +2330,14 @@ lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gate
         cudaError_t e = cudaMemcpyAsync(energy_out, d_e, sizeof(double), cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, cudaGetErrorString(e));
     }
-    if (s == LQ_OK) s = sync(st);
+    if (s == LQ_OK) s = comm_sync(comm && comm->c ? comm : nullptr, st);
+    if (s == LQ_ERR_CUDA || s == LQ_ERR_NCCL || P->dead) {   // never reuse a plan an asynchronous failure touched
+        g_psr_cache.pop_back();
+        cudaStreamSynchronize(st);
+        C->io.release(st);
+        lq_psr_free(P);
+        delete C;
+    }
     return s;
 }
 
@@ -2174,6 +2407,68 @@ lq_status lq_plan_describe(int n_qubits, const lq_gate *gates, size_t n_gates, u
         buf[k] = 0;
     }
     return LQ_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- state-handle entry points
+// Every call on a state handle: refuse a poisoned handle, run, and poison the
+// handle if an asynchronous CUDA / NCCL failure surfaced (seal()).
+extern "C" {
+
+lq_status lq_sv_init_basis(lq_sv *sv, uint64_t k) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, sv_init_basis_body(sv, k));
+}
+
+lq_status lq_sv_init_random(lq_sv *sv, uint64_t seed) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, sv_init_random_body(sv, seed));
+}
+
+lq_status lq_sv_norm2(lq_sv *sv, double *out) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, sv_norm2_body(sv, out));
+}
+
+lq_status lq_sv_read(lq_sv *sv, uint64_t offset, uint64_t count, double *host_out) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, sv_read_body(sv, offset, count, host_out));
+}
+
+lq_status lq_sv_gather(lq_sv *sv, const uint64_t *idx, size_t count, double *host_out) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, sv_gather_body(sv, idx, count, host_out));
+}
+
+lq_status lq_sv_write(lq_sv *sv, uint64_t offset, uint64_t count, const double *host_in) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, sv_write_body(sv, offset, count, host_in));
+}
+
+lq_status lq_sv_canonicalize(lq_sv *sv) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, sv_canonicalize_body(sv));
+}
+
+lq_status lq_apply_circuit(lq_sv *sv, const lq_gate *gates, size_t n_gates, const double *theta, size_t n_theta) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, apply_circuit_body(sv, gates, n_gates, theta, n_theta));
+}
+
+lq_status lq_qft(lq_sv *sv, int inverse) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, qft_body(sv, inverse));
+}
+
+lq_status lq_expval_pauli_sum(lq_sv *sv, const lq_pauli_term *terms, size_t n_terms, double *out_energy) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, expval_pauli_sum_body(sv, terms, n_terms, out_energy));
+}
+
+lq_status lq_trotter_xyz(lq_sv *sv, const lq_xyz_model *mdl, double t0, double dt, int n_steps, int record_every, double *energy_out) {
+    LQ_TRY(check_sv(sv));
+    return seal(sv, trotter_xyz_body(sv, mdl, t0, dt, n_steps, record_every, energy_out));
 }
 
 }  // extern "C"

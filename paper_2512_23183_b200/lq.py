@@ -36,8 +36,9 @@ KIND_NAMES = ["H", "X", "Y", "Z", "S", "SDG", "T", "TDG", "RX", "RY", "RZ", "CNO
               "SWAP", "U1", "U2", "CRY", "CCX", "RXX", "RYY", "RZZ"]
 KINDS = {k: i for i, k in enumerate(KIND_NAMES)}
 LQ_OPT_FUSION, LQ_OPT_TILE_BITS, LQ_OPT_COALESCE_BITS, LQ_OPT_REG_BITS, LQ_OPT_KERNEL_TIMING, LQ_OPT_JIT, \
-    LQ_OPT_PASS_BUDGET, LQ_OPT_FIRST_PASS_FREE, LQ_OPT_POISON_ALLOC = 0, 1, 2, 3, 4, 5, 6, 7, 8
-KC_TILE, KC_PAIR, KC_DIAG, KC_PAULI, KC_OTHER = 0, 1, 2, 3, 4
+    LQ_OPT_PASS_BUDGET, LQ_OPT_FIRST_PASS_FREE, LQ_OPT_POISON_ALLOC, LQ_OPT_COMM_TIMEOUT_MS, \
+    LQ_OPT_SWAP_QUBITS = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
+KC_TILE, KC_PAIR, KC_DIAG, KC_PAULI, KC_OTHER, KC_SWAP = 0, 1, 2, 3, 4, 5
 
 
 class lq_gate(ctypes.Structure):
@@ -94,8 +95,8 @@ _SIGS = {
     "lq_apply_circuit": ([_P, _GP, _sz, _DP, _sz], _i32),
     "lq_qft": ([_P, _i32], _i32),
     "lq_expval_pauli_sum": ([_P, _TP, _sz, _DP], _i32),
-    "lq_param_shift_grad": ([_i32, _GP, _sz, _DP, _sz, _TP, _sz, _i32, _i32, _P, _DP, _DP], _i32),
-    "lq_psr_create": ([_i32, _GP, _sz, _sz, _TP, _sz, _i32, _i32, _P, ctypes.POINTER(_P)], _i32),
+    "lq_param_shift_grad": ([_i32, _GP, _sz, _DP, _sz, _TP, _sz, _P, _P, _DP, _DP], _i32),
+    "lq_psr_create": ([_i32, _GP, _sz, _sz, _TP, _sz, _P, _P, ctypes.POINTER(_P)], _i32),
     "lq_psr_run": ([_P, _P, _P, _P], _i32),
     "lq_psr_free": ([_P], _i32),
     "lq_psr_stats": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_u64),
@@ -111,6 +112,9 @@ _SIGS = {
     "lq_comm_unique_id": ([_P, _sz], _i32),
     "lq_comm_init": ([_P, _sz, _i32, _i32, ctypes.POINTER(_P)], _i32),
     "lq_comm_free": ([_P], _i32),
+    "lq_comm_init_local": ([_i32, _i32, ctypes.POINTER(_P)], _i32),
+    "lq_comm_info": ([_P, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)], _i32),
+    "lq_sv_exchange_stats": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i32),
     "lq_sv_alloc_sharded": ([_i32, _P, _P, ctypes.POINTER(_P)], _i32),
     "lq_sv_alloc_group": ([_i32, _i32, _P, ctypes.POINTER(_P)], _i32),
     "lq_sv_shard_info": ([_P, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
@@ -321,15 +325,17 @@ def lq_expval_pauli_sum(h, terms) -> float:
     return out.value
 
 
-def lq_param_shift_grad(n_qubits: int, ansatz, theta, terms, shard_rank: int = 0, shard_world: int = 1,
-                        stream=None, with_energy: bool = True) -> Tuple[np.ndarray, Optional[float]]:
+def lq_param_shift_grad(n_qubits: int, ansatz, theta, terms, comm=None, stream=None,
+                        with_energy: bool = True) -> Tuple[np.ndarray, Optional[float]]:
+    """comm: None (one GPU), an NCCL lq_comm (collective; full gradient and E
+    on every rank) or lq_comm_init_local(rank, world) (this rank's share)."""
     ga = ansatz if isinstance(ansatz, GateArray) else GateArray(ansatz)
     ta = terms if isinstance(terms, TermArray) else TermArray(terms)
     th = np.ascontiguousarray(theta, np.float64)
     grad = np.zeros(th.size, np.float64)
     e = ctypes.c_double()
-    _chk(_lib.lq_param_shift_grad(n_qubits, ga.ptr, ga.n, _dptr(th), th.size, ta.ptr, ta.n, shard_rank,
-                                  shard_world, _stream_ptr(stream), _dptr(grad),
+    _chk(_lib.lq_param_shift_grad(n_qubits, ga.ptr, ga.n, _dptr(th), th.size, ta.ptr, ta.n, comm,
+                                  _stream_ptr(stream), _dptr(grad),
                                   ctypes.byref(e) if with_energy else None))
     return grad, (e.value if with_energy else None)
 
@@ -360,12 +366,11 @@ def lq_vqe_adam(n_qubits: int, ansatz, theta0, terms, lr: float = 1e-2, beta1: f
     return th, trace[: it.value + 1].copy(), it.value
 
 
-def lq_psr_create(n_qubits: int, ansatz, n_params: int, terms, shard_rank: int = 0, shard_world: int = 1,
-                  stream=None):
+def lq_psr_create(n_qubits: int, ansatz, n_params: int, terms, comm=None, stream=None):
     ga = ansatz if isinstance(ansatz, GateArray) else GateArray(ansatz)
     ta = terms if isinstance(terms, TermArray) else TermArray(terms)
     h = _P()
-    _chk(_lib.lq_psr_create(n_qubits, ga.ptr, ga.n, n_params, ta.ptr, ta.n, shard_rank, shard_world,
+    _chk(_lib.lq_psr_create(n_qubits, ga.ptr, ga.n, n_params, ta.ptr, ta.n, comm,
                             _stream_ptr(stream), ctypes.byref(h)))
     return h
 
@@ -477,6 +482,26 @@ def lq_comm_init(unique_id: bytes, rank: int, world: int):
 
 def lq_comm_free(h):
     _chk(_lib.lq_comm_free(h))
+
+
+def lq_comm_init_local(rank: int, world: int):
+    """A transport-less communicator: partitioned work returns this rank's share."""
+    h = _P()
+    _chk(_lib.lq_comm_init_local(rank, world, ctypes.byref(h)))
+    return h
+
+
+def lq_comm_info(h) -> Tuple[int, int, bool]:
+    r, w, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _chk(_lib.lq_comm_info(h, ctypes.byref(r), ctypes.byref(w), ctypes.byref(t)))
+    return r.value, w.value, bool(t.value)
+
+
+def lq_sv_exchange_stats(h) -> Tuple[int, int]:
+    """(global-qubit exchanges so far, bytes each rank sent in them)"""
+    n, b = _u64(), _u64()
+    _chk(_lib.lq_sv_exchange_stats(h, ctypes.byref(n), ctypes.byref(b)))
+    return n.value, b.value
 
 
 def comm_from_torch(group=None):

@@ -107,13 +107,16 @@ def _gloo_worker(rank, world, port, n, m, seed, q):
     nl = sched["nl"]
     psi = oracle.init_random(n, w.seed)[rank << nl:(rank + 1) << nl].copy()
 
-    def exchange(send, peer):
-        t_send = torch.from_numpy(send.view(np.float64).copy())
-        t_recv = torch.empty_like(t_send)
-        reqs = [dist.isend(t_send, peer), dist.irecv(t_recv, peer)]
+    def exchange(sends):
+        reqs, recvs = [], {}
+        for peer, send in sorted(sends.items()):
+            t_send = torch.from_numpy(send.view(np.float64).copy())
+            t_recv = torch.empty_like(t_send)
+            reqs += [dist.isend(t_send, peer), dist.irecv(t_recv, peer)]
+            recvs[peer] = t_recv
         for r in reqs:
             r.wait()
-        return t_recv.numpy().view(np.complex128)
+        return {p: t.numpy().view(np.complex128) for p, t in recvs.items()}
 
     E = 0.0
     for st in sched["steps"]:
@@ -128,11 +131,13 @@ def _gloo_worker(rank, world, port, n, m, seed, q):
     dist.destroy_process_group()
 
 
-def test_gloo_two_ranks_config5_twin_qft_expval(oracle):
-    """world_size 2 over gloo: each process runs its shard; swaps are real
-    point-to-point exchanges; the energy is an all-reduce."""
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_ranks_config5_twin_qft_expval(oracle, world):
+    """world_size 2 and 4 over gloo: each process runs its shard; exchanges
+    are real point-to-point messages (world 4: 2-qubit all-to-alls among the
+    4 ranks); the energy is an all-reduce."""
     import torch.multiprocessing as mp
-    n, m, world = 9, 1, 2
+    n, m = 9, world.bit_length() - 1
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -148,6 +153,10 @@ def test_gloo_two_ranks_config5_twin_qft_expval(oracle):
     oracle.apply_circuit(ref, w.gates)
     oracle.qft(ref)
     assert np.abs(full - ref).max() <= TOL
+    if world == 4:
+        from paper_2512_23183_b200 import lq
+        sched = lq.lq_dist_schedule_json(n, m, w.gates, qft=1)
+        assert any(len(st["g"]) == 2 for st in sched["steps"] if st["kind"] == "swap")
     eo = oracle.expval(ref, W.xyz_terms(n))
     assert abs(E - eo) <= 1e-10 * max(1.0, abs(eo))
 
@@ -195,3 +204,59 @@ def test_shards_smaller_than_three_qubits_rejected(lq):
     for n, m in [(3, 1), (4, 2), (2, 1)]:
         with pytest.raises(LQError):
             lq.lq_dist_schedule_json(n, m, [])
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_exchange_group_size_option(lq, oracle, k):
+    """LQ_OPT_SWAP_QUBITS caps the qubits per exchange (1 = pairwise swaps);
+    every cap gives the same state, and the distributed QFT on 2^3 ranks
+    needs exactly two 3-qubit all-to-alls when the cap allows them (SURVEY
+    §8(e): stages 0..m-1, then n-m..n-1; the SWAP layer is a relabel)."""
+    n, m = 10, 3
+    w = W.config5(n, m, 200)
+    lq.lq_set_option(lq.LQ_OPT_SWAP_QUBITS, k)
+    try:
+        sched = lq.lq_dist_schedule_json(n, m, w.gates, qft=1)
+        qft_only = lq.lq_dist_schedule_json(n, m, [], qft=1)
+    finally:
+        lq.lq_set_option(lq.LQ_OPT_SWAP_QUBITS, 4)
+    assert all(len(st["g"]) <= k for st in sched["steps"] if st["kind"] == "swap")
+    if k == 3:
+        sw = [st for st in qft_only["steps"] if st["kind"] == "swap"]
+        assert len(sw) == 2 and all(len(st["g"]) == 3 for st in sw)
+        assert abs(qft_only["shard_fraction_sent"] - 2 * 7 / 8) < 1e-12
+    # exchanges avoid the coalescing bits 0..2 when they can
+    assert all(min(st["l"]) >= 3 for st in sched["steps"] if st["kind"] == "swap")
+    got, _ = DE.run_group(sched, oracle.init_random(n, w.seed))
+    ref = oracle.init_random(n, w.seed)
+    oracle.apply_circuit(ref, w.gates)
+    oracle.qft(ref)
+    assert np.abs(got - ref).max() <= TOL
+
+
+def test_comm_local_partition_handles(lq):
+    """lq_comm_init_local: rank/world without transport (no device needed)."""
+    c = lq.lq_comm_init_local(2, 4)
+    assert lq.lq_comm_info(c) == (2, 4, False)
+    lq.lq_comm_free(c)
+    from paper_2512_23183_b200.lq import LQError
+    with pytest.raises(LQError):
+        lq.lq_comm_init_local(4, 4)
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """bench.py --gpus 2 on a box with fewer GPUs fails loudly (exit 2)
+    instead of measuring one rank and reporting n_gpus: 1."""
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("this box has >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2 and "visible GPUs" in r.stderr
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, env={**env, "WORLD_SIZE": "1", "RANK": "0"}, timeout=300)
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr

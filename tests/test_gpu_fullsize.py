@@ -112,7 +112,8 @@ def _roundtrip(lq, sv, w, n, n_samples, rng):
     ratio = a0 / raw
     c = float(np.median(ratio.real))
     assert np.abs(ratio - c).max() <= 1e-12 * c
-    assert abs(c * c * (1 << n) - 1.0) <= 1e-3    # S ~ 2^n (sum of 2^n Exp(1)-ish terms, relative spread 2^-n/2)
+    # S = sum of 2^n terms |a_i|^2 = -2 ln u0 with mean 2: S ~ 2^(n+1), relative spread ~2^-(n/2)
+    assert abs(c * c * (1 << (n + 1)) - 1.0) <= 1e-3
     assert abs(sv.norm2() - 1.0) <= 1e-12
     sv.apply(w.gates).qft()
     assert abs(sv.norm2() - 1.0) <= 1e-11
@@ -133,10 +134,12 @@ def test_config5_n33_one_gpu_roundtrip(lq):
     n = 33
     w = W.config5(n=n, m=1)
     sv = lq.StateVector(n)
-    _roundtrip(lq, sv, w, n, 1 << 20, np.random.default_rng(533))
-    sv.free()
-    del sv
-    _free_cache()
+    try:
+        _roundtrip(lq, sv, w, n, 1 << 20, np.random.default_rng(533))
+    finally:
+        sv.free()
+        del sv
+        _free_cache()
 
 
 @pytest.mark.parametrize("G", [2, 4])
@@ -149,10 +152,12 @@ def test_config5_n32_group_roundtrip(lq, G):
     m = G.bit_length() - 1
     w = W.config5(n=n, m=m)
     sv = lq.ShardedState(n, group_world=G)
-    _roundtrip(lq, sv, w, n, 1 << 20, np.random.default_rng(532 + G))
-    sv.free()
-    del sv
-    _free_cache()
+    try:
+        _roundtrip(lq, sv, w, n, 1 << 20, np.random.default_rng(532 + G))
+    finally:
+        sv.free()
+        del sv
+        _free_cache()
 
 
 @pytest.mark.parametrize("G", [2, 4, 8])

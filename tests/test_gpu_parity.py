@@ -388,12 +388,31 @@ def test_psr_shards_partition_components(lq, oracle, world):
     full, e0 = lq.lq_param_shift_grad(w.n, w.gates, w.theta, w.terms)
     acc = np.zeros_like(full)
     for r in range(world):
-        g, e = lq.lq_param_shift_grad(w.n, w.gates, w.theta, w.terms, shard_rank=r, shard_world=world)
+        c = lq.lq_comm_init_local(r, world)
+        assert lq.lq_comm_info(c) == (r, world, False)
+        g, e = lq.lq_param_shift_grad(w.n, w.gates, w.theta, w.terms, comm=c)
+        lq.lq_comm_free(c)
         owned = np.arange(full.size) % world == r
         assert np.all(g[~owned] == 0.0)
         acc += g
         assert e == (e0 if r == 0 else 0.0)
     np.testing.assert_array_equal(acc, full)   # bit-identical
+
+
+def test_psr_nccl_world1_allreduce_path(lq, oracle):
+    """lq_param_shift_grad / lq_psr_run with an NCCL communicator (world 1
+    on this GPU): the combine writes this rank's share into the reduction
+    buffer, one ncclAllReduce over n_params + 1 doubles, copies out -- the
+    same gradient and E as the 1-GPU call, bit for bit."""
+    w = W.config3()
+    g0, e0 = lq.lq_param_shift_grad(w.n, w.gates, w.theta, w.terms)
+    c = lq.lq_comm_init(lq.lq_comm_unique_id(), 0, 1)
+    assert lq.lq_comm_info(c) == (0, 1, True)
+    g1, e1 = lq.lq_param_shift_grad(w.n, w.gates, w.theta, w.terms, comm=c)
+    lq.lq_psr_cache_clear()
+    lq.lq_comm_free(c)
+    np.testing.assert_array_equal(g1, g0)
+    assert e1 == e0
 
 
 @pytest.mark.parametrize("rb", [3, 4])

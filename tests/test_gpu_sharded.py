@@ -181,3 +181,54 @@ def test_sharded_n32_single_qubit_layer_monomial_tail(lq):
         want[i] = a
     assert np.abs(got - want).max() <= 1e-12
     sv.free()
+
+
+# ---------------------------------------------------------------- k-qubit exchanges (all-to-all)
+
+@pytest.mark.parametrize("n,G", [(12, 4), (18, 8), (20, 8)])
+def test_group_alltoall_matches_pairwise_and_oracle(lq, oracle, n, G):
+    """The config-5 generator + QFT on G shards with k-qubit all-to-all
+    exchanges (LQ_OPT_SWAP_QUBITS = 4: the distributed QFT takes two
+    exchanges) and with pairwise swaps only (= 1): both equal the oracle;
+    exchange statistics count (2^k - 1) / 2^k of a shard per exchange."""
+    m = G.bit_length() - 1
+    w = W.config5(n, m, 400)
+    ref = oracle.init_random(n, w.seed)
+    oracle.apply_circuit(ref, w.gates)
+    oracle.qft(ref)
+    stats = {}
+    for k in (1, 4):
+        lq.lq_set_option(lq.LQ_OPT_SWAP_QUBITS, k)
+        try:
+            sv = lq.ShardedState(n, group_world=G)
+            sv.init_random(w.seed).apply(w.gates).qft()
+            assert np.abs(sv.read() - ref).max() <= AMP_TOL
+            stats[k] = lq.lq_sv_exchange_stats(sv.h)
+            sv.free()
+        finally:
+            lq.lq_set_option(lq.LQ_OPT_SWAP_QUBITS, 4)
+    sched1 = None
+    lq.lq_set_option(lq.LQ_OPT_SWAP_QUBITS, 1)
+    try:
+        sched1 = lq.lq_dist_schedule_json(n, m, w.gates, qft=1)
+    finally:
+        lq.lq_set_option(lq.LQ_OPT_SWAP_QUBITS, 4)
+    sched4 = lq.lq_dist_schedule_json(n, m, w.gates, qft=1)
+    shard_bytes = 16 << (n - m)
+    for k, sc in ((1, sched1), (4, sched4)):
+        assert stats[k][0] == sc["n_swaps"]
+        assert abs(stats[k][1] - sc["shard_fraction_sent"] * shard_bytes) <= 1
+    if G > 2:
+        assert sched4["n_swaps"] < sched1["n_swaps"] and stats[4][1] <= stats[1][1]
+
+
+def test_nccl_world1_exchange_free_path(lq):
+    """A world-1 NCCL communicator: the sharded allocation degenerates to an
+    ordinary state (no exchange), lq_sv_exchange_stats reports none."""
+    c = lq.lq_comm_init(lq.lq_comm_unique_id(), 0, 1)
+    sv = lq.ShardedState(10, comm=c)
+    sv.init_random(3).apply(W.config5(10, 1, 50).gates).qft()
+    assert abs(sv.norm2() - 1.0) <= 1e-12
+    assert lq.lq_sv_exchange_stats(sv.h) == (0, 0)
+    sv.free()
+    lq.lq_comm_free(c)
