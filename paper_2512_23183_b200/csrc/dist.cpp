@@ -148,6 +148,21 @@ bool schedule_gates(Schedule &sc, const lq_gate *gates, size_t ng, int32_t *qmap
             if (lx != ly) return ly;
             return x.first > y.first;
         });
+        if (G.kind == LQK_QFT_STAGE && sc.qft_pass_stages > 0) {
+            // pass-aligned victims: qubits never needed again first, then,
+            // among those not needed in the next P stages, the ones needed
+            // soonest (the rest in Belady order)
+            const size_t horizon = i + (size_t)sc.qft_pass_stages;
+            std::vector<std::pair<size_t, int>> late, rest;
+            for (auto &v : vict) (v.first >= horizon && v.second >= COALESCE_BITS ? late : rest).push_back(v);
+            std::stable_sort(late.begin(), late.end(), [](const std::pair<size_t, int> &x, const std::pair<size_t, int> &y) {
+                const bool nx = x.first == (size_t)SIZE_MAX, ny = y.first == (size_t)SIZE_MAX;
+                if (nx != ny) return nx;
+                return x.first < y.first;
+            });
+            late.insert(late.end(), rest.begin(), rest.end());
+            vict.swap(late);
+        }
         if (vict.size() < glob.size()) return false;
         std::vector<int> want(glob);
         // other global qubits needed before the local qubit they would displace

@@ -26,8 +26,12 @@
 // before the next use of the local qubit it would displace (the Belady rule
 // applied to the whole exchange), up to max_k qubits per exchange: one
 // all-to-all instead of several pairwise swaps (the distributed QFT needs
-// two: Alg. 3's stages 0..m-1 and n-m..n-1).  The schedule is a pure
-// function of its inputs: every rank computes the same.
+// two).  For a QFT stage (qft_pass_stages = P > 0) the victims are instead
+// the qubits needed first AFTER the next P stages: the local run then ends
+// exactly at a tile-pass boundary and the second exchange brings them back,
+// so the sharded QFT makes as many local passes as the unsharded one
+// (ceil(n / P)) plus two exchanges.  The schedule is a pure function of its
+// inputs: every rank computes the same.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -52,6 +56,7 @@ struct DStep {
 struct Schedule {
     int n = 0, m = 0, nl = 0;
     int max_k = MAX_SWAP_K;       // qubits per exchange (1: pairwise swaps only)
+    int qft_pass_stages = 0;      // QFT stages one local tile pass holds (0: plain Belady victims)
     std::vector<DStep> steps;
     MatBuilder mb;
     size_t n_swaps = 0, n_relabels = 0;

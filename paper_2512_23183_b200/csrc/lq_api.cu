@@ -142,6 +142,15 @@ lq_status have_device() {
     return LQ_OK;
 }
 
+// QFT stages one local tile pass of a sharded state holds (dist.h): the
+// tile bits the planner takes for a run of stages (12 unless forced) minus
+// the coalescing bits; 0 (plain Belady) for small shards.
+int qft_pass_stages(int nl) {
+    const int K = g_opt_K.load() > 0 ? (int)g_opt_K.load() : 12;
+    if (getenv("LQ_QFT_BELADY") || nl <= K) return 0;   // A/B experiments
+    return std::max(1, K - (int)g_opt_coalesce.load());
+}
+
 PlanOptions options() {
     PlanOptions o;
     o.K = (int)g_opt_K.load();
@@ -967,14 +976,77 @@ lq_status sh_swap(lq_sv *sv, const DStep &stp) {
 
 // Run a schedule on the shards; E (nullable) receives the Pauli sum of the
 // schedule's expectation step.
-lq_status sh_run(lq_sv *sv, Schedule &sc, const double *theta, size_t n_theta, double *E) {
-    cudaStream_t st = sv->stream;
+// Schedules of sharded calls for repeated use (the bench step, a VQE or
+// Trotter loop): an LRU keyed like PlanCache plus the rank relabel and the
+// exchange cap.  A hit skips scheduling, planning and JIT source generation.
+struct CachedSchedule {
+    Schedule sc;
+    int32_t qmap_after[64];
+    uint32_t xmask_after = 0;
+};
+struct ScheduleCache {
+    std::mutex mu;
+    std::list<std::pair<std::string, std::shared_ptr<CachedSchedule>>> lru;
+    static constexpr size_t CAP = 16;
+    std::shared_ptr<CachedSchedule> get(const std::string &k) {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto it = lru.begin(); it != lru.end(); ++it)
+            if (it->first == k) {
+                lru.splice(lru.begin(), lru, it);
+                return it->second;
+            }
+        return nullptr;
+    }
+    void put(const std::string &k, std::shared_ptr<CachedSchedule> p) {
+        std::lock_guard<std::mutex> lk(mu);
+        lru.emplace_front(k, std::move(p));
+        if (lru.size() > CAP) lru.pop_back();
+    }
+    void clear() {
+        std::lock_guard<std::mutex> lk(mu);
+        lru.clear();
+    }
+};
+ScheduleCache g_sched_cache;
+
+// The schedule of gates (terms == nullptr) or of a Pauli sum on sv's current
+// layout, planned and JIT-prepared; cached.
+lq_status sharded_schedule(lq_sv *sv, const std::string &key, const lq_gate *gates, size_t ng,
+                           const lq_pauli_term *terms, size_t nt, std::shared_ptr<CachedSchedule> &out) {
+    int64_t extra[3] = {sv->m, (int64_t)sv->xmask, g_opt_swap_k.load()};
+    std::string k = key;
+    k.append(reinterpret_cast<const char *>(extra), sizeof(extra));
+    out = g_sched_cache.get(k);
+    if (out) return LQ_OK;
+    auto cs = std::make_shared<CachedSchedule>();
+    Schedule &sc = cs->sc;
+    sc.n = sv->n;
+    sc.m = sv->m;
+    sc.nl = sv->nl;
+    sc.max_k = (int)g_opt_swap_k.load();
+    sc.qft_pass_stages = qft_pass_stages(sc.nl);
+    memcpy(cs->qmap_after, sv->qmap, sizeof(cs->qmap_after));
+    cs->xmask_after = sv->xmask;
+    if (terms || nt) {
+        if (!schedule_expval(sc, terms, nt, cs->qmap_after, cs->xmask_after))
+            return fail(LQ_ERR_ARG, "a Pauli term acts with X/Y on more qubits than a shard holds");
+    } else if (!schedule_gates(sc, gates, ng, cs->qmap_after, cs->xmask_after)) {
+        return fail(LQ_ERR_ARG, "shard too small for a gate");
+    }
     plan_steps(sc, options());
     for (auto &stp : sc.steps)
         if (stp.kind == 0) {
-            stp.plan.stream_tag = (uint64_t)(uintptr_t)st;
+            stp.plan.stream_tag = (uint64_t)(uintptr_t)sv->stream;
             LQ_TRY(prepare(stp.plan));
+            stp.plan.prepared = true;
         }
+    g_sched_cache.put(k, cs);
+    out = cs;
+    return LQ_OK;
+}
+
+lq_status sh_run(lq_sv *sv, const Schedule &sc, const double *theta, size_t n_theta, double *E) {
+    cudaStream_t st = sv->stream;
     Blob blob;
     struct Off { size_t sub, kop, perm, pt, et, dt, cd; };
     std::vector<Off> offs(sc.steps.size());
@@ -1392,6 +1464,7 @@ lq_status lq_dist_schedule_json(int n_qubits, int log2_world, const lq_gate *gat
     sc.m = log2_world;
     sc.nl = n_qubits - log2_world;
     sc.max_k = (int)g_opt_swap_k.load();
+    sc.qft_pass_stages = qft_pass_stages(sc.nl);
     int32_t qm[64];
     for (int q = 0; q < n_qubits; q++) qm[q] = n_qubits - 1 - q;
     uint32_t xm = 0;
@@ -1621,18 +1694,12 @@ namespace {
 lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const double *theta, size_t n_theta) {
     if (!n_gates) return LQ_OK;
     if (sv->m) {
-        Schedule sc;
-        sc.n = sv->n;
-        sc.m = sv->m;
-        sc.nl = sv->nl;
-        sc.max_k = (int)g_opt_swap_k.load();
-        int32_t qm[64];
-        memcpy(qm, sv->qmap, sizeof(qm));
-        uint32_t xm = sv->xmask;
-        if (!schedule_gates(sc, gates, n_gates, qm, xm)) return fail(LQ_ERR_ARG, "shard too small for a gate");
-        LQ_TRY(sh_run(sv, sc, theta, n_theta, nullptr));
-        memcpy(sv->qmap, qm, sizeof(qm));
-        sv->xmask = xm;
+        std::shared_ptr<CachedSchedule> cs;
+        LQ_TRY(sharded_schedule(sv, gates_key(sv->n, sv->qmap, gates, n_gates, sv->stream), gates, n_gates, nullptr,
+                                0, cs));
+        LQ_TRY(sh_run(sv, cs->sc, theta, n_theta, nullptr));
+        memcpy(sv->qmap, cs->qmap_after, sizeof(sv->qmap));
+        sv->xmask = cs->xmask_after;
         return LQ_OK;
     }
     const std::string key = gates_key(sv->n, sv->qmap, gates, n_gates, sv->stream);
@@ -1702,19 +1769,13 @@ static lq_status expval_pauli_sum_body(lq_sv *sv, const lq_pauli_term *terms, si
     if (!out_energy) return fail(LQ_ERR_ARG, "out_energy is NULL");
     LQ_TRY(validate_terms(sv->n, terms, n_terms));
     if (sv->m) {
-        Schedule sc;
-        sc.n = sv->n;
-        sc.m = sv->m;
-        sc.nl = sv->nl;
-        sc.max_k = (int)g_opt_swap_k.load();
-        int32_t qm[64];
-        memcpy(qm, sv->qmap, sizeof(qm));
-        uint32_t xm = sv->xmask;
-        if (!schedule_expval(sc, terms, n_terms, qm, xm))
-            return fail(LQ_ERR_ARG, "a Pauli term acts with X/Y on more qubits than a shard holds");
-        LQ_TRY(sh_run(sv, sc, nullptr, 0, out_energy));
-        memcpy(sv->qmap, qm, sizeof(qm));
-        sv->xmask = xm;
+        std::shared_ptr<CachedSchedule> cs;
+        static const lq_pauli_term none{};
+        LQ_TRY(sharded_schedule(sv, plan_key('e', sv->n, sv->qmap, terms, sizeof(lq_pauli_term) * n_terms, sv->stream),
+                                nullptr, 0, n_terms ? terms : &none, n_terms, cs));
+        LQ_TRY(sh_run(sv, cs->sc, nullptr, 0, out_energy));
+        memcpy(sv->qmap, cs->qmap_after, sizeof(sv->qmap));
+        sv->xmask = cs->xmask_after;
         return LQ_OK;
     }
     const std::string key = plan_key('e', sv->n, sv->qmap, terms, sizeof(lq_pauli_term) * n_terms, sv->stream);
@@ -2265,6 +2326,7 @@ lq_status lq_psr_cache_clear(void) {
     }
     g_psr_cache.clear();
     g_plan_cache.clear();
+    g_sched_cache.clear();
     return LQ_OK;
 }
 

@@ -801,6 +801,24 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
     for (auto &sp : mb.specs) mat_off.push_back(sp.out);
     const int nl = opt.n_local > 0 ? std::min(opt.n_local, n) : n;   // tile bits come from [0, nl)
     int K = opt.K > 0 ? std::min(opt.K, nl) : auto_tile_bits(nl);
+    // a run of QFT stages only (Alg. 3 on a permuted or sharded layout):
+    // stages pack strictly in order, as plan_qft's; 12 tile bits when that
+    // saves a whole pass, and no FP64 budget (plan_qft has none either)
+    bool all_qft = !ops.empty();
+    for (const POp &o : ops) all_qft &= o.type == K_QFT;
+    if (all_qft && opt.K <= 0 && nl > 12) {
+        auto count_q = [&](int Kc) {
+            const int cc = std::max(0, std::min(opt.coalesce, Kc - 2));
+            const uint64_t m0 = (1ull << cc) - 1;
+            int np = 0;
+            for (size_t s0 = 0; s0 < ops.size(); np++) {
+                uint64_t Tm = m0;
+                while (s0 < ops.size() && popc(Tm | ops[s0].full()) <= Kc) Tm |= ops[s0++].full();
+            }
+            return np;
+        };
+        if (count_q(12) < count_q(K)) K = 12;
+    }
     if (K > 12) K = 12;   // two 2^K buffers must fit in shared memory
     if (nl <= K) K = nl;
     int Rr = std::min(std::max(1, std::min(opt.reg_bits, R)), K);
@@ -845,7 +863,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
         if (!skip[i]) rem.push_back((int)i);
     // the FP64 budget trades an extra HBM round trip for less arithmetic per
     // pass; a state that is one tile has no HBM round trip to trade
-    const int budget_all = nl > K ? opt.budget : 0;
+    const int budget_all = (nl > K && !all_qft) ? opt.budget : 0;
     // zero-first plans (PlanOptions::first_free): the support U = union of the
     // tiles planned so far (lq_api.cu prepare() runs a pass only over the
     // tiles inside U).  A pass with |U| <= free_upto is exempt from the
@@ -855,8 +873,16 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
     uint64_t U = 0;
     bool track = opt.first_free;
     const int free_upto = getenv("LQ_FREE_UPTO") ? atoi(getenv("LQ_FREE_UPTO")) : 0;   // A/B experiments
+    // support-aware budget (zero-first plans): a pass whose support U misses
+    // some bits reads only 2^|U| amplitudes, so its HBM time is about
+    // (2^(|U|-nl) + 1) / 2 of a full pass and so is the arithmetic it can hide
+    const bool sup_budget = getenv("LQ_SUPPORT_BUDGET") != nullptr;   // A/B experiments
     while (!rem.empty()) {
-        const int budget = (track && popc(U) <= free_upto) ? 0 : budget_all;
+        int budget = (track && popc(U) <= free_upto) ? 0 : budget_all;
+        if (track && sup_budget && budget && popc(U) < nl) {
+            const double f = 0.5 * (std::ldexp(1.0, popc(U) - nl) + 1.0);
+            budget = std::max(1, (int)(budget * f));
+        }
         uint64_t Tm = mand;
         std::vector<int> absorbed, absorbed_w;
         first_fit(ops, rem, K, Tm, absorbed, budget);
@@ -938,7 +964,7 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
             // contiguous runs for coalescing)
             for (int b = 0; b < nl && popc(Tm) < K; b++) Tm |= bit(b);
             emit_tile(n, nl, K, Rr, Tm, ops, absorbed, mat_off, plan, mb);
-            U |= Tm;
+            if (!(plan.passes.back().kp.flags & PF_NO_STORE)) U |= Tm;   // a read-only pass leaves U as it was
         }
         // remove absorbed from rem (absorbed is a subsequence of rem)
         std::vector<int> left;

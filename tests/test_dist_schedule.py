@@ -260,3 +260,19 @@ def test_bench_refuses_more_gpus_than_visible():
     r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
                        capture_output=True, text=True, env={**env, "WORLD_SIZE": "1", "RANK": "0"}, timeout=300)
     assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr
+
+
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_sharded_qft_schedule_is_pass_aligned(lq, m):
+    """The distributed QFT at n = 30 on 2^m ranks (host schedule only): two
+    exchanges (stages 0..m-1 need the global qubits; the qubits swapped out
+    are the ones needed right after the first 12-bit tile pass, and the
+    second exchange trades them back for finished qubits), and the same three
+    local tile passes as the unsharded QFT (9 + 9 + 12 stages; PAPER.md
+    Alg. 3)."""
+    s = lq.lq_dist_schedule_json(30, m, [], qft=1)
+    kinds = [st["kind"] for st in s["steps"]]
+    assert kinds == ["swap", "local", "swap", "local"]
+    assert all(len(st["g"]) == m for st in s["steps"] if st["kind"] == "swap")
+    passes = [p for st in s["steps"] if st["kind"] == "local" for p in st["plan"]["passes"]]
+    assert len(passes) == 3 and all(p["K"] == 12 for p in passes)
