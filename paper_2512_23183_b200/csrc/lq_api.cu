@@ -143,10 +143,10 @@ lq_status have_device() {
 }
 
 // QFT stages one local tile pass of a sharded state holds (dist.h): the
-// tile bits the planner takes for a run of stages (12 unless forced) minus
-// the coalescing bits; 0 (plain Belady) for small shards.
+// tile bits the planner takes for a run of stages minus the coalescing
+// bits; 0 (plain Belady) for small shards.
 int qft_pass_stages(int nl) {
-    const int K = g_opt_K.load() > 0 ? (int)g_opt_K.load() : 12;
+    const int K = g_opt_K.load() > 0 ? (int)g_opt_K.load() : auto_tile_bits(nl);
     if (getenv("LQ_QFT_BELADY") || nl <= K) return 0;   // A/B experiments
     return std::max(1, K - (int)g_opt_coalesce.load());
 }

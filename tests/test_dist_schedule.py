@@ -265,14 +265,14 @@ def test_bench_refuses_more_gpus_than_visible():
 @pytest.mark.parametrize("m", [1, 2, 3])
 def test_sharded_qft_schedule_is_pass_aligned(lq, m):
     """The distributed QFT at n = 30 on 2^m ranks (host schedule only): two
-    exchanges (stages 0..m-1 need the global qubits; the qubits swapped out
-    are the ones needed right after the first 12-bit tile pass, and the
-    second exchange trades them back for finished qubits), and the same three
-    local tile passes as the unsharded QFT (9 + 9 + 12 stages; PAPER.md
-    Alg. 3)."""
+    exchanges -- stages 0..m-1 need the global qubits; the qubits swapped
+    out are those needed right after the first tile pass (8 stages with
+    11-bit tiles), and the second exchange trades them back for finished
+    qubits -- and ceil(30 / 8) = 4 local tile passes, the first exactly one
+    pass long (Alg. 3)."""
     s = lq.lq_dist_schedule_json(30, m, [], qft=1)
     kinds = [st["kind"] for st in s["steps"]]
     assert kinds == ["swap", "local", "swap", "local"]
     assert all(len(st["g"]) == m for st in s["steps"] if st["kind"] == "swap")
-    passes = [p for st in s["steps"] if st["kind"] == "local" for p in st["plan"]["passes"]]
-    assert len(passes) == 3 and all(p["K"] == 12 for p in passes)
+    local = [st["plan"]["passes"] for st in s["steps"] if st["kind"] == "local"]
+    assert len(local[0]) == 1 and sum(len(p) for p in local) == 4
