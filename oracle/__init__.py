@@ -66,6 +66,8 @@ def lib():
         _lib.or_splitmix64.argtypes = [u64]
         _lib.or_splitmix64.restype = u64
         _lib.or_random_gaussian_at.argtypes = [u64, P, u64, P]
+        _lib.or_u53.argtypes = [u64]
+        _lib.or_u53.restype = dbl
         _lib.or_norm2.argtypes = [P, i32]
         _lib.or_norm2.restype = dbl
     return _lib
@@ -149,6 +151,11 @@ def init_random(n: int, seed: int) -> np.ndarray:
 
 def splitmix64(x: int) -> int:
     return int(lib().or_splitmix64(int(x) & (2**64 - 1)))
+
+
+def u53(x: int) -> float:
+    """init_random's uniform deviate ((x >> 11) + 0.5) 2^-53 (c.1 step 2)."""
+    return float(lib().or_u53(int(x) & (2**64 - 1)))
 
 
 def random_gaussian_at(seed: int, idx) -> np.ndarray:

@@ -86,12 +86,19 @@ uint64_t or_splitmix64(uint64_t x)
  * a_i = r (cos 2 pi u1 + i sin 2 pi u1), r = sqrt(-2 ln u0) (Box-Muller),
  * u_j = ((x_j >> 11) + 0.5) 2^-53, x0 = splitmix64(seed ^ 2i),
  * x1 = splitmix64(seed ^ (2i+1)). */
+/* u = ((x >> 11) + 0.5) 2^-53: the midpoint of one of 2^53 equal cells of
+ * (0, 1), never 0 (log u0 stays finite) and never 1. */
+double or_u53(uint64_t x)
+{
+    return ((double)(x >> 11) + 0.5) * 0x1.0p-53;
+}
+
 static void gauss_at(uint64_t seed, uint64_t i, double *re, double *im)
 {
     uint64_t x0 = or_splitmix64(seed ^ (2 * i));
     uint64_t x1 = or_splitmix64(seed ^ (2 * i + 1));
-    double u0 = ((double)(x0 >> 11) + 0.5) * 0x1.0p-53;
-    double u1 = ((double)(x1 >> 11) + 0.5) * 0x1.0p-53;
+    double u0 = or_u53(x0);
+    double u1 = or_u53(x1);
     double r = sqrt(-2.0 * log(u0));
     *re = r * cos(2.0 * OR_PI * u1);
     *im = r * sin(2.0 * OR_PI * u1);

@@ -516,6 +516,11 @@ struct DevPlan {
     const double2 *cst = nullptr;
 };
 
+std::mutex &ctab_mutex(const void *bank) {
+    static std::mutex mu[64];
+    return mu[((uintptr_t)bank >> 8) % 64];
+}
+
 lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uint64_t state_stride, int n_circ,
                         const double2 *mats, uint64_t mat_stride, cudaStream_t st, bool zero_first,
                         double *partials = nullptr, uint64_t slot_stride = 0, bool no_final_store = false,
@@ -540,7 +545,13 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
     for (size_t i = 0; i < plan.passes.size(); i++) {
         const PlanPass &p = plan.passes[i];
         if (p.kind == PASS_TILE) {
+            // A JIT module's constant bank is shared by every plan whose pass
+            // has the same source on the same stream: hold its lock from the
+            // bank refill to the launch, so two host threads issuing on one
+            // stream cannot interleave (stream order = enqueue order).
+            std::unique_lock<std::mutex> bank_lock;
             if (i < plan.jit_ctab.size() && plan.jit_ctab[i]) {
+                bank_lock = std::unique_lock<std::mutex>(ctab_mutex(plan.jit_ctab[i]));
                 const CtabDesc &D = plan.ctab_desc[ci++];
                 CUDA_TRY(cudaMemcpyAsync(plan.jit_ctab[i], dp.ctab_stage + D.out,
                                          (size_t)n_circ * D.smat * sizeof(double2), cudaMemcpyDeviceToDevice, st));

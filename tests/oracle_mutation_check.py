@@ -30,6 +30,13 @@ muts = [
  ("py", 'gates += [(name, i, i + 1, -1, -2.0 * J * dt) for i in range(n - 1)]', 'gates += [(name, i, i + 1, -1, 2.0 * J * dt) for i in range(n - 1)]'),
  ("py", 'gates += [("RZ", i, -1, -1, -2.0 * h(tj) * dt) for i in range(n)]', 'gates += [("RZ", i, -1, -1, -2.0 * h(tj + dt) * dt) for i in range(n)]'),
  ("py", "terms += [(-jx, m, 0), (-jy, m, m), (-jz, 0, m)]", "terms += [(-jx, m, 0), (-jy, m, 0), (-jz, 0, m)]"),
+ # init_random (c.1 step 2): seed convention, u mapping, hash, and the |Im| / NaN rejection
+ ("c", "uint64_t x0 = or_splitmix64(seed ^ (2 * i));", "uint64_t x0 = or_splitmix64(seed ^ i);"),
+ ("c", "return ((double)(x >> 11) + 0.5) * 0x1.0p-53;", "return ((double)(x >> 11) + 0.0) * 0x1.0p-53;"),
+ ("c", "double r = sqrt(-2.0 * log(u0));", "double r = sqrt(-2.0 * log(u1));"),
+ ("c", "double u1 = or_u53(x1);", "double u1 = or_u53(x0);"),
+ ("c", "return z ^ (z >> 31);", "return z ^ (z >> 30);"),
+ ("c", "if (!(fabs(cimag(v)) <= 1e-10) || !isfinite(creal(v))) {", "if (fabs(cimag(v)) > 1e-10) {"),
 ]
 for which, a, b in muts:
     assert a in orig[which], a

@@ -471,6 +471,16 @@ def test_splitmix64_published_vector(oracle):
     assert got == want
 
 
+def test_uniform_deviate_endpoints(oracle):
+    """u = ((x >> 11) + 0.5) 2^-53 (c.1 step 2) at the ends of its range: the
+    cell midpoints 2^-54 and 1 - 2^-54 (u is never 0, so ln u0 is finite),
+    and 1/2 + 2^-54 at x = 2^63."""
+    assert oracle.u53(0) == 2.0 ** -54
+    assert oracle.u53(2**64 - 1) == 1.0 - 2.0 ** -54
+    assert oracle.u53(2**63) == 0.5 + 2.0 ** -54
+    assert oracle.u53(2**11 - 1) == 2.0 ** -54     # the low 11 bits are dropped
+
+
 def test_init_random_hand_computed_amplitudes(oracle):
     """init_random(n, seed)[i] = a_i / sqrt(sum_j |a_j|^2) with
     a_i = sqrt(-2 ln u0) e^{2 pi i u1}, u = ((x >> 11) + 0.5) 2^-53,
