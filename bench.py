@@ -412,6 +412,33 @@ def run_cfg4(args, lq, rank, local, world, dev, comm):
             "clocks_instrumented_region": clk_inst,
             "traffic_source": (tr or {}).get("source")}
 
+    # access-pattern ceiling: each pass's tile set swept without arithmetic
+    # (lq_tile_sweep) over one launch's circuits; a pass that moves fewer
+    # bytes (support tracking, read-only) is scaled by its byte fraction
+    masks = lq.lq_psr_pass_tiles(plan)
+    pbytes = lq.lq_psr_pass_bytes(plan)
+    batches = tile_cnt / max(1, args.steps * tile_passes)
+    B = max(1, round(n_circ / batches)) if batches else 1
+    nb = n + max(0, (B - 1).bit_length())
+    buf = torch.empty(1 << nb, dtype=torch.complex128, device=dev)
+    sweep_cache, ceil_ms_batch = {}, 0.0
+    for m, (kind, byts) in zip(masks, pbytes):
+        if kind != 0 or m == 0:
+            continue
+        if m not in sweep_cache:
+            sweep_cache[m] = lq.lq_tile_sweep(buf.data_ptr(), buf.numel() * 16, nb, m, 3, stream)
+        ceil_ms_batch += sweep_cache[m] * byts / (32.0 * (1 << n))
+    del buf
+    torch.cuda.empty_cache()
+    ceil_ms_step = ceil_ms_batch * batches
+    roof["access_pattern_ceiling"] = {
+        "tile_ms_per_step": ceil_ms_step, "tile_ms_per_step_measured": tile_ms / args.steps,
+        "frac": ceil_ms_step / (tile_ms / args.steps) if tile_ms > 0 else None,
+        "ceiling_GBps": (alg_bytes / args.steps) / (ceil_ms_step / 1e3) / 1e9 if ceil_ms_step else None,
+        "source": "lq_tile_sweep: each pass's tile bit set swept in place (16 B read + 16 B write per amplitude, "
+                  "no arithmetic) over one launch's circuits, x its algorithmic byte fraction; HBM3e serves "
+                  "128-byte runs at large strides below the copy rate (DESIGN.md §5)"}
+
     # ---- e2e: host buffers through the public API (collective with N ranks) -----------------
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
     th_pin = torch.tensor(w.theta, dtype=torch.float64).pin_memory()

@@ -365,6 +365,23 @@ lq_status lq_psr_traffic(const lq_psr *plan, uint64_t *tile_bytes_per_circuit, u
 lq_status lq_psr_pass_bytes(const lq_psr *plan, uint64_t *bytes_out, int32_t *kind_out, uint64_t *support_amps_out,
                             uint32_t *ops_out, size_t cap, size_t *n_passes);
 
+/* The tile bit set of each launched pass of the plan (bit b set = physical
+ * bit b is in the pass's tile; 0 for pair / diagonal passes), in launch
+ * order; fills min(cap, *n_passes) entries. */
+lq_status lq_psr_pass_tiles(const lq_psr *plan, uint64_t *tile_masks_out, size_t cap, size_t *n_passes);
+
+/* Measurement: the access-pattern ceiling of a tile pass.  Sweeps the
+ * 2^n_bits complex128 amplitudes of dev_buf (bytes >= 16 * 2^n_bits; the
+ * contents are scrambled) in place, tile by tile -- a tile = the amplitudes
+ * whose bits outside tile_mask (4..12 bits) are fixed -- with the tile
+ * kernel's access pattern and no arithmetic (read 16 B + write 16 B per
+ * amplitude); *ms_per_sweep = mean time of `reps` sweeps after a warm-up
+ * (CUDA events on cuda_stream; syncs).  HBM3e serves short runs at large
+ * strides below its copy rate: this is the bandwidth a pass with that tile
+ * set can reach. */
+lq_status lq_tile_sweep(void *dev_buf, size_t bytes, int n_bits, uint64_t tile_mask, int reps, void *cuda_stream,
+                        double *ms_per_sweep);
+
 /* ---- execution options (testing / measurement) -------------------------- */
 typedef enum {
     LQ_OPT_FUSION = 0,     /* 1 (default): tile-fused passes; 0: one pass per gate (pair/diag kernels) */

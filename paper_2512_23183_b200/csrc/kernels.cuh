@@ -370,6 +370,40 @@ __global__ void __launch_bounds__(256) k_fill_basis(uint64_t N, uint64_t k, doub
         psi[i] = make_double2(i == k ? 1.0 : 0.0, 0.0);
 }
 
+// ---------------------------------------------------------------- access-pattern ceiling (measurement)
+// The memory traffic of a tile pass without its arithmetic: every tile (the
+// 2^K amplitudes whose bits outside the tile set are fixed) is read and
+// written back in place (re and im swapped), 16 amplitudes per thread, loads
+// first, tiles in the order of their free bits over a persistent grid, as in
+// the tile kernel.  Its time is the ceiling an HBM-bound pass with that tile
+// set can reach (bench.py roofline.access_pattern_ceiling).
+struct SweepSpec {
+    int K, nfree;
+    uint8_t tpos[16];   // tile bit positions, ascending
+    uint8_t fpos[48];   // free bit positions, ascending
+};
+__device__ __forceinline__ uint64_t deposit_bits(uint64_t v, const uint8_t *pos, int cnt) {
+    uint64_t a = 0;
+    for (int i = 0; i < cnt; i++) a |= ((v >> i) & 1ull) << pos[i];
+    return a;
+}
+__global__ void __launch_bounds__(256) k_tile_sweep(double2 *__restrict__ s, uint64_t n_tiles, SweepSpec P) {
+    constexpr int U = 16;
+    const uint32_t per = (1u << P.K) / U;   // threads per tile
+    const uint32_t lane = threadIdx.x % per, slot = threadIdx.x / per, tpc = blockDim.x / per;
+    uint64_t off[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) off[u] = deposit_bits(lane + u * per, P.tpos, P.K);
+    for (uint64_t t = (uint64_t)blockIdx.x * tpc + slot; t < n_tiles; t += (uint64_t)gridDim.x * tpc) {
+        const uint64_t base = deposit_bits(t, P.fpos, P.nfree);
+        double2 a[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) a[u] = s[base | off[u]];
+#pragma unroll
+        for (int u = 0; u < U; u++) s[base | off[u]] = make_double2(a[u].y, a[u].x);
+    }
+}
+
 __global__ void __launch_bounds__(256) k_norm2(uint64_t N, const double2 *__restrict__ psi, double *partial) {
     double acc = 0.0;
     for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < N; i += (uint64_t)gridDim.x * 256) {

@@ -2258,6 +2258,60 @@ lq_status lq_psr_traffic(const lq_psr *P, uint64_t *tile_bytes_per_circuit, uint
     return LQ_OK;
 }
 
+lq_status lq_psr_pass_tiles(const lq_psr *P, uint64_t *tile_masks_out, size_t cap, size_t *n_passes) {
+    if (!P) return fail(LQ_ERR_ARG, "invalid plan");
+    const size_t np = P->plan.passes.size();
+    if (n_passes) *n_passes = np;
+    if (cap && !tile_masks_out) return fail(LQ_ERR_ARG, "output array is NULL");
+    for (size_t i = 0; i < np && i < cap; i++) {
+        const PlanPass &p = P->plan.passes[i];
+        uint64_t m = 0;
+        if (p.kind == PASS_TILE)
+            for (int b = 0; b < p.kp.K; b++) m |= 1ull << p.kp.T[b];
+        tile_masks_out[i] = m;
+    }
+    return LQ_OK;
+}
+
+lq_status lq_tile_sweep(void *dev_buf, size_t bytes, int n_bits, uint64_t tile_mask, int reps, void *cuda_stream,
+                        double *ms_per_sweep) {
+    if (!dev_buf || !ms_per_sweep || reps < 1) return fail(LQ_ERR_ARG, "NULL buffer / output or reps < 1");
+    if (n_bits < 8 || n_bits > 40 || bytes < ((size_t)16 << n_bits)) return fail(LQ_ERR_DIM, "buffer smaller than 16 * 2^n_bits");
+    const int K = __builtin_popcountll(tile_mask);
+    if (tile_mask >> n_bits || K < 4 || K > 12) return fail(LQ_ERR_ARG, "tile mask must have 4..12 bits below n_bits");
+    LQ_TRY(have_device());
+    SweepSpec P;
+    memset(&P, 0, sizeof(P));
+    for (int b = 0; b < n_bits; b++) {
+        if (tile_mask >> b & 1) P.tpos[P.K++] = (uint8_t)b;
+        else P.fpos[P.nfree++] = (uint8_t)b;
+    }
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const uint64_t n_tiles = 1ull << P.nfree;
+    const int threads = std::max(128, (1 << K) / 16);
+    int dev = 0, sms = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)sms * 16 * 128 / threads, n_tiles);
+    double2 *s = (double2 *)dev_buf;
+    cudaEvent_t a = nullptr, b = nullptr;
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    k_tile_sweep<<<grid, threads, 0, st>>>(s, n_tiles, P);   // warm-up
+    cudaEventRecord(a, st);
+    for (int r = 0; r < reps; r++) k_tile_sweep<<<grid, threads, 0, st>>>(s, n_tiles, P);
+    cudaEventRecord(b, st);
+    cudaError_t e = cudaEventSynchronize(b);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (e != cudaSuccess) return fail(LQ_ERR_CUDA, std::string("tile sweep: ") + cudaGetErrorString(e));
+    LQ_TRY(check_launch("k_tile_sweep"));
+    *ms_per_sweep = ms / reps;
+    return LQ_OK;
+}
+
 lq_status lq_psr_pass_bytes(const lq_psr *P, uint64_t *bytes_out, int32_t *kind_out, uint64_t *support_amps_out,
                             uint32_t *ops_out, size_t cap, size_t *n_passes) {
     if (!P) return fail(LQ_ERR_ARG, "invalid plan");

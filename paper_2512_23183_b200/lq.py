@@ -113,6 +113,8 @@ _SIGS = {
     "lq_comm_init": ([_P, _sz, _i32, _i32, ctypes.POINTER(_P)], _i32),
     "lq_comm_free": ([_P], _i32),
     "lq_comm_init_local": ([_i32, _i32, ctypes.POINTER(_P)], _i32),
+    "lq_psr_pass_tiles": ([_P, ctypes.POINTER(_u64), _sz, ctypes.POINTER(_sz)], _i32),
+    "lq_tile_sweep": ([_P, _sz, _i32, _u64, _i32, _P, ctypes.POINTER(_dbl)], _i32),
     "lq_comm_info": ([_P, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)], _i32),
     "lq_sv_exchange_stats": ([_P, ctypes.POINTER(_u64), ctypes.POINTER(_u64)], _i32),
     "lq_sv_alloc_sharded": ([_i32, _P, _P, ctypes.POINTER(_P)], _i32),
@@ -413,6 +415,21 @@ def lq_psr_pass_bytes(plan, with_support: bool = False):
     if with_support:
         return [(k[i], b[i], a[i], o[i]) for i in range(n.value)]
     return [(k[i], b[i]) for i in range(n.value)]
+
+
+def lq_psr_pass_tiles(plan) -> List[int]:
+    n = ctypes.c_size_t()
+    _chk(_lib.lq_psr_pass_tiles(plan, None, 0, ctypes.byref(n)))
+    out = (_u64 * max(n.value, 1))()
+    _chk(_lib.lq_psr_pass_tiles(plan, out, n.value, ctypes.byref(n)))
+    return [int(out[i]) for i in range(n.value)]
+
+
+def lq_tile_sweep(dev_ptr: int, nbytes: int, n_bits: int, tile_mask: int, reps: int = 3, stream=None) -> float:
+    """ms per in-place sweep of 2^n_bits amplitudes with tile_mask's access pattern."""
+    ms = ctypes.c_double()
+    _chk(_lib.lq_tile_sweep(dev_ptr, nbytes, n_bits, tile_mask, reps, _stream_ptr(stream), ctypes.byref(ms)))
+    return ms.value
 
 
 def lq_kernel_timing(kernel_class: int) -> Tuple[float, int]:

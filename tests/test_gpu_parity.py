@@ -761,3 +761,20 @@ def test_degenerate_sizes_and_empty_inputs(lq, oracle, jit):
         grad_close(g, go)
     finally:
         lq.lq_set_option(lq.LQ_OPT_JIT, 1)
+
+
+@pytest.mark.parametrize("mask", [0xff0007, 0x8003ff, 0xfff, 0x3fe00007 >> 8])
+def test_tile_sweep_touches_every_amplitude_once(lq, mask):
+    """lq_tile_sweep (the access-pattern ceiling of bench.py's roofline)
+    swaps re and im of every amplitude once per sweep: after the warm-up plus
+    one timed sweep the buffer is unchanged, after the warm-up plus two it is
+    swapped everywhere -- every tile is visited exactly once."""
+    import torch
+    nb = 24
+    x = torch.randn(1 << nb, dtype=torch.complex128, device="cuda")
+    x0 = x.clone()
+    ms = lq.lq_tile_sweep(x.data_ptr(), x.numel() * 16, nb, mask, 1)
+    assert ms > 0 and torch.equal(x, x0)
+    lq.lq_tile_sweep(x.data_ptr(), x.numel() * 16, nb, mask, 2)
+    assert torch.equal(torch.view_as_real(x)[:, 0], torch.view_as_real(x0)[:, 1])
+    assert torch.equal(torch.view_as_real(x)[:, 1], torch.view_as_real(x0)[:, 0])
