@@ -107,7 +107,9 @@ struct KOp {
     uint8_t qj;          // QFT: logical bit j of the stage
     uint8_t tdep;        // QFT: 0x80 | register positions whose logical bit is below j (the
                          // only ones the register twiddle depends on); 0: unknown
-    uint8_t pad[6];
+    uint8_t qi;          // QFT: register position of logical bit j - 1 when it is in tdep (its
+                         // twiddle factor is exactly +-i), else NOREG
+    uint8_t pad[5];
 };
 static_assert(sizeof(KOp) == 32, "KOp layout");
 

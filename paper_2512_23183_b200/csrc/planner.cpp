@@ -648,9 +648,11 @@ static void lower_qft_stages(Plan &plan, const KSub &sb, const LocalMap &L, int 
         }
         op.mat = (uint32_t)mb.add_const(tab, NREG);
         op.tdep = 0x80;
+        op.qi = NOREG;
         for (int i = 0; i < Rr; i++) {
             const int p = L.T[sb.S[i]];
             if (lp[p] < 64 && lp[p] < j) op.tdep |= (uint8_t)(1u << i);
+            if (lp[p] < 64 && (int)lp[p] == j - 1) op.qi = (uint8_t)i;
         }
         op.b1 = (uint8_t)jmax;
         if (head) op.flags |= QF_HEAD;
@@ -1088,9 +1090,11 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
                 }
                 k.mat = (uint32_t)mb.add_const(tab, NREG);
                 k.tdep = 0x80;
+                k.qi = NOREG;
                 for (int i = 0; i < Rr; i++) {
                     const int p = L.T[sb.S[i]], l = layout_rev ? n - 1 - p : p;
                     if (l < j) k.tdep |= (uint8_t)(1u << i);
+                    if (l == j - 1) k.qi = (uint8_t)i;
                 }
                 if (b == a) k.flags |= QF_HEAD;
                 int jmax = 0;

@@ -361,7 +361,9 @@ struct TState {
     bool hph;          // ph != 1
     double eacc;       // Pauli-group contributions of this thread
     double2 tsc, ph;
-    double2 ttmax;     // QFT twiddle state of the current sub-block
+    double2 ttmax;     // QFT twiddle state of the current sub-block (at its largest j)
+    double2 ttcur;     // ... and at the last stage applied, j = tj
+    int tj;
     uint64_t lg;
     const uint8_t *lpos;   // physical -> logical bit map of the pass (QF_GENERAL stages)
     uint32_t cbase;        // this circuit's offset in the pass's constant op-table bank (JIT, D::CTAB)
@@ -371,7 +373,8 @@ struct TState {
         eacc = 0.0;
         tsc = make_double2(1.0, 0.0);
         ph = make_double2(1.0, 0.0);
-        ttmax = make_double2(1.0, 0.0);
+        ttmax = ttcur = make_double2(1.0, 0.0);
+        tj = -1;
         lg = 0;
     }
 };
@@ -404,18 +407,27 @@ __device__ __forceinline__ void materialize(double2 (&a)[1 << RR], TState &ts, b
 // positions in tdep (logical bits below j), so with tdep known at compile
 // time (JIT) the 8 butterflies share 2^|tdep| distinct twiddles and pairs
 // with no such bit set use tt itself (W = 1 exactly there).
+//
+// qi = the register position of logical bit j - 1 when it is in tdep: its
+// share of the twiddle is e^{+-i pi 2^(j-1) / 2^j} = +-i exactly, so a pair
+// with that bit takes +-i times its partner pattern's twiddle (a swap and a
+// sign) instead of another complex multiply: half of the stage's twiddle
+// products are free (radix-4 structure of adjacent stages).
 template <int RR, int P>
 __device__ __forceinline__ void ap_qft(double2 (&a)[1 << RR], double2 tt, const double2 *__restrict__ W,
-                                       bool inverse, uint32_t tdep) {
+                                       bool inverse, uint32_t tdep, uint32_t qi) {
 #pragma unroll
     for (int v = 0; v < (1 << RR); v++) {
         if (v & (1 << P)) continue;
         const int w = v | (1 << P);
         const bool known = tdep & 0x80u;
         const int lo = (int)(w & tdep & 0x7Fu);
+        const int qb = (known && qi < 8u) ? (lo & (1 << qi)) : 0;
+        const int lo2 = lo & ~qb;
         double2 tw;
-        if (known && lo == 0) tw = tt;
-        else tw = cmul(tt, W[known ? (lo | (1 << P)) : w]);
+        if (known && lo2 == 0) tw = tt;
+        else tw = cmul(tt, W[known ? (lo2 | (1 << P)) : w]);
+        if (qb) tw = inverse ? make_double2(tw.y, -tw.x) : make_double2(-tw.y, tw.x);
         if (!inverse) {
             double2 u = a[v], x = a[w];
             a[v] = cadd(u, x);
@@ -439,9 +451,14 @@ __device__ __forceinline__ void ap_qft(double2 (&a)[1 << RR], double2 tt, const 
 
 // QFT thread twiddle exp(+-i pi Lt / 2^j), Lt = logical(gbase) mod 2^j: one
 // sincospi per sub-block (at its largest j), then the exact recurrence
-// tt_{k-1} = tt_k^2 (-1)^{bit k-1 of Lt}.
-__device__ __forceinline__ double2 qft_thread_twiddle(const KOp &op, uint64_t gbase, int n, double2 &ttmax,
-                                                      uint64_t &lg, const uint8_t *lpos) {
+// tt_{k-1} = tt_k^2 (-1)^{bit k-1 of Lt}.  Stages of a forward QFT come in
+// descending j, so each continues the recurrence from the previous stage's
+// value (one squaring per stage, the same operations in the same order as
+// restarting from the head); the inverse's ascending stages restart.
+__device__ __forceinline__ double2 qft_thread_twiddle(const KOp &op, uint64_t gbase, int n, TState &ts,
+                                                      const uint8_t *lpos) {
+    double2 &ttmax = ts.ttmax;
+    uint64_t &lg = ts.lg;
     const bool inv = op.flags & QF_INVERSE;
     if (op.flags & QF_HEAD) {
         const int jm = op.b1;
@@ -458,12 +475,17 @@ __device__ __forceinline__ double2 qft_thread_twiddle(const KOp &op, uint64_t gb
         double s, c;
         sincospi(ldexp((double)Lt, -jm), &s, &c);
         ttmax = make_double2(c, inv ? -s : s);
+        ts.ttcur = ttmax;
+        ts.tj = jm;
     }
-    double2 tt = ttmax;
-    for (int k = op.b1; k > op.qj; k--) {
+    const bool cont = ts.tj >= (int)op.qj && ts.tj <= (int)op.b1;
+    double2 tt = cont ? ts.ttcur : ttmax;
+    for (int k = cont ? ts.tj : op.b1; k > op.qj; k--) {
         tt = cmul(tt, tt);
         if ((lg >> (k - 1)) & 1) tt = make_double2(-tt.x, -tt.y);
     }
+    ts.ttcur = tt;
+    ts.tj = op.qj;
     return tt;
 }
 
@@ -763,8 +785,8 @@ __device__ __forceinline__ void exec_op(double2 (&a)[1 << RR], const KOp &op, co
         constexpr int P = CODE - C_QFT;
         if constexpr (RR > P) {
             flush_flips<RR>(a, ts.fb);
-            const double2 tt = qft_thread_twiddle(op, gbase, n, ts.ttmax, ts.lg, ts.lpos);
-            ap_qft<RR, P>(a, tt, M, op.flags & QF_INVERSE, op.tdep);
+            const double2 tt = qft_thread_twiddle(op, gbase, n, ts, ts.lpos);
+            ap_qft<RR, P>(a, tt, M, op.flags & QF_INVERSE, op.tdep, op.qi);
             if (op.flags & QF_SCALE) ts.tsc = cscale(ts.tsc, 0.70710678118654752440);
         }
     } else if constexpr (CODE == C_DT) {
@@ -813,7 +835,8 @@ struct InterpProg {
     __device__ __forceinline__ static void run(uint32_t /*sub*/, const KSub &sb, uint32_t op0, double2 (&a)[1 << RR],
                                                const KOp *ops, uint64_t gbase, int n, const double2 *tab,
                                                TState &ts, const ETerm *et) {
-        ts.ttmax = make_double2(1.0, 0.0);
+        ts.ttmax = ts.ttcur = make_double2(1.0, 0.0);
+        ts.tj = -1;
         ts.lg = 0;
         for (uint32_t oi = sb.op_begin - op0; oi < sb.op_end - op0; oi++) {
             const KOp op = ops[oi];
