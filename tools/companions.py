@@ -88,6 +88,6 @@ t_loc = timed(lambda: sh.apply([("H", loc_q(), -1, -1, 0.0)]))
 t_glob = timed(lambda: sh.apply([("H", glob_q(), -1, -1, 0.0)]))
 row("sharded G=2: H on a local qubit (one pass)", 32, t_loc)
 row("sharded G=2: global-local swap (H on the global qubit minus H on a local one)", 16, t_glob - t_loc,
-    "k_swap_halves: each shard exchanges the half of its amplitudes whose local bit differs from its rank bit, in place: "
+    "k_swap_parts (k = 1): each shard exchanges the half of its amplitudes whose local bit differs from its rank bit, in place: "
     "16 B read + 16 B write per moved amplitude = 16 B per amplitude of the state")
 print("JSON " + json.dumps(out))
