@@ -276,3 +276,23 @@ def test_sharded_qft_schedule_is_pass_aligned(lq, m):
     assert all(len(st["g"]) == m for st in s["steps"] if st["kind"] == "swap")
     local = [st["plan"]["passes"] for st in s["steps"] if st["kind"] == "local"]
     assert len(local[0]) == 1 and sum(len(p) for p in local) == 4
+
+
+def test_bench_gpus2_relaunches_under_torchrun_reference_arm():
+    """bench.py --gpus 2 without a launcher re-executes itself under
+    torch.distributed.run with two ranks (127.0.0.1 rendezvous); on the
+    reference arm (the oracle; no GPU needed) rank 0 alone prints the line
+    and the other rank exits 0."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
