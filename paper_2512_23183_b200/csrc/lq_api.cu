@@ -146,7 +146,8 @@ lq_status have_device() {
 // tile bits the planner takes for a run of stages minus the coalescing
 // bits; 0 (plain Belady) for small shards.
 int qft_pass_stages(int nl) {
-    const int K = g_opt_K.load() > 0 ? (int)g_opt_K.load() : auto_tile_bits(nl);
+    // plan_circuit gives a run of QFT stages 12 tile bits when that saves a pass
+    const int K = g_opt_K.load() > 0 ? (int)g_opt_K.load() : (getenv("LQ_QFT_K11") ? auto_tile_bits(nl) : 12);
     if (getenv("LQ_QFT_BELADY") || nl <= K) return 0;   // A/B experiments
     return std::max(1, K - (int)g_opt_coalesce.load());
 }

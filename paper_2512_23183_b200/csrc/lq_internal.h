@@ -87,7 +87,9 @@ enum KOpFlags : uint8_t {
     QF_REVERSED = 2,  // layout is bit-reversed (logical index = brev(physical))
     QF_HEAD = 4,      // first QFT op of its sub-block: compute the thread twiddle for j = b1
     QF_GENERAL = 8,   // any layout: logical index from the pass's physical->logical map (KPass::lpos)
-    QF_SCALE = 16     // the stage carries its own 1/sqrt(2) (deferred into the tile scalar)
+    QF_SCALE = 16,    // the stage carries its own 1/sqrt(2) (deferred into the tile scalar)
+    QF_LGSET = 32     // QF_GENERAL head: the caller (JIT program) already put the thread's logical
+                      // index into TState::lg with the pass's compile-time bit map
 };
 
 // One op inside a sub-block.  Controls on register bits are the register

@@ -804,12 +804,25 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
     const int nl = opt.n_local > 0 ? std::min(opt.n_local, n) : n;   // tile bits come from [0, nl)
     int K = opt.K > 0 ? std::min(opt.K, nl) : auto_tile_bits(nl);
     // a run of QFT stages only (Alg. 3 on a permuted or sharded layout)
-    // packs strictly in order with no FP64 budget, as plan_qft's.  (12 tile
-    // bits to save a pass measured 57 ms vs 40 ms for the n = 30 QFT on 2
-    // shards: the generic stage op at one CTA per SM is slower than the
-    // specialised plan_qft pass.)
+    // packs strictly in order with no FP64 budget, as plan_qft's, and takes
+    // 12 tile bits when that saves a pass (n = 30 QFT on 2 shards: 31 ms vs
+    // 37 ms; before the JIT computed the stages' logical index with
+    // straight-line code it was 57 ms)
     bool all_qft = !ops.empty();
     for (const POp &o : ops) all_qft &= o.type == K_QFT;
+    if (all_qft && opt.K <= 0 && nl > 12 && !getenv("LQ_QFT_K11")) {   // (A/B switch)
+        auto count_q = [&](int Kc) {
+            const int cc = std::max(0, std::min(opt.coalesce, Kc - 2));
+            const uint64_t m0 = (1ull << cc) - 1;
+            int np = 0;
+            for (size_t s0 = 0; s0 < ops.size(); np++) {
+                uint64_t Tm = m0;
+                while (s0 < ops.size() && popc(Tm | ops[s0].full()) <= Kc) Tm |= ops[s0++].full();
+            }
+            return np;
+        };
+        if (count_q(12) < count_q(K)) K = 12;
+    }
     if (K > 12) K = 12;   // two 2^K buffers must fit in shared memory
     if (nl <= K) K = nl;
     int Rr = std::min(std::max(1, std::min(opt.reg_bits, R)), K);

@@ -462,7 +462,9 @@ __device__ __forceinline__ double2 qft_thread_twiddle(const KOp &op, uint64_t gb
     const bool inv = op.flags & QF_INVERSE;
     if (op.flags & QF_HEAD) {
         const int jm = op.b1;
-        if (op.flags & QF_GENERAL) {   // logical bits of this thread's base index
+        if (op.flags & QF_LGSET) {
+            // lg set by the JIT program (straight-line bit map, no table reads)
+        } else if (op.flags & QF_GENERAL) {   // logical bits of this thread's base index
             lg = 0;
             for (uint64_t g = gbase; g; g &= g - 1) {
                 const uint32_t l = lpos[__ffsll((long long)g) - 1];

@@ -266,16 +266,17 @@ def test_bench_refuses_more_gpus_than_visible():
 def test_sharded_qft_schedule_is_pass_aligned(lq, m):
     """The distributed QFT at n = 30 on 2^m ranks (host schedule only): two
     exchanges -- stages 0..m-1 need the global qubits; the qubits swapped
-    out are those needed right after the first tile pass (8 stages with
-    11-bit tiles), and the second exchange trades them back for finished
-    qubits -- and ceil(30 / 8) = 4 local tile passes, the first exactly one
-    pass long (Alg. 3)."""
+    out are those needed right after the first tile pass (9 stages with
+    12-bit tiles), and the second exchange trades them back for finished
+    qubits -- and the same three 12-bit local passes as the unsharded QFT
+    (9 + 9 + 12 stages; Alg. 3)."""
     s = lq.lq_dist_schedule_json(30, m, [], qft=1)
     kinds = [st["kind"] for st in s["steps"]]
     assert kinds == ["swap", "local", "swap", "local"]
     assert all(len(st["g"]) == m for st in s["steps"] if st["kind"] == "swap")
     local = [st["plan"]["passes"] for st in s["steps"] if st["kind"] == "local"]
-    assert len(local[0]) == 1 and sum(len(p) for p in local) == 4
+    assert len(local[0]) == 1 and sum(len(p) for p in local) == 3
+    assert all(p["K"] == 12 for ps in local for p in ps)
 
 
 def test_bench_gpus2_relaunches_under_torchrun_reference_arm():
