@@ -393,8 +393,8 @@ typedef enum {
                                  sm_100a (cached per process) instead of the op-list interpreter kernel;
                                  both execute the same device op templates (tile.cuh).  0: off;
                                  1 (default): auto -- PSR plans and states with n >= 26; 2: always. */
-    LQ_OPT_PASS_BUDGET = 6,   /* planner: estimated FP64 instructions per amplitude (x10) a tile pass may
-                                 absorb before it stops (default 400; 0 = no limit, absorb greedily) */
+    LQ_OPT_PASS_BUDGET = 6,   /* planner, parameter-shift plans: estimated FP64 instructions per amplitude
+                                 (x10) a tile pass may absorb before it stops (default 400; 0 = no limit) */
     LQ_OPT_FIRST_PASS_FREE = 7, /* PSR plans: 1 (default) exempts the first pass -- it synthesises |0...0>,
                                  so every tile but one is stored as zeros without arithmetic -- from
                                  the pass budget; 0: budget it like the others */
@@ -405,8 +405,10 @@ typedef enum {
                                  ncclCommGetAsyncError; after this many ms (default 600000; 0 = forever)
                                  or on an asynchronous NCCL error the communicator is aborted and the
                                  call returns LQ_ERR_NCCL (later calls on its handles: LQ_ERR_STATE) */
-    LQ_OPT_SWAP_QUBITS = 10   /* sharded states: most global qubits one exchange may move (1..4, default
+    LQ_OPT_SWAP_QUBITS = 10,  /* sharded states: most global qubits one exchange may move (1..4, default
                                  4; 1 = pairwise half-shard swaps only, k > 1 = all-to-all among 2^k ranks) */
+    LQ_OPT_STATE_PASS_BUDGET = 11 /* the same budget for every other plan (circuits, QFT, expectations,
+                                 Trotter, sharded steps; default 800) */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);

@@ -49,7 +49,12 @@ std::atomic<int64_t> g_opt_first_free{1};   // PSR plans: the |0...0> pass is ex
 std::atomic<int64_t> g_opt_poison{0};   // LQ_OPT_POISON_ALLOC
 std::atomic<int64_t> g_opt_comm_timeout{600000};   // LQ_OPT_COMM_TIMEOUT_MS
 std::atomic<int64_t> g_opt_swap_k{4};   // LQ_OPT_SWAP_QUBITS: qubits per global exchange (dist.h)
-std::atomic<int64_t> g_opt_budget{400};   // keeps passes from turning compute-bound (swept; 350 gains 0.4 % on config 4 but costs 5-12 % on Trotter / random circuits)
+// FP64 pass budgets, swept on B200: PSR plans (config 4:
+// 2.540 s at 400 vs 2.555 / 2.559 s at 600 / 800) and single-state or
+// sharded plans (n = 30: 8 Trotter steps 371 -> 279 ms, the config-5
+// circuit 186 -> 151 ms, 200 random gates 40.5 -> 35.9 ms at 800 vs 400)
+std::atomic<int64_t> g_opt_budget{400};         // LQ_OPT_PASS_BUDGET (PSR plans)
+std::atomic<int64_t> g_opt_state_budget{800};   // LQ_OPT_STATE_PASS_BUDGET (every other plan)
 const double PI = 3.14159265358979323846264338327950288;
 
 lq_status fail(lq_status s, const std::string &msg) {
@@ -158,7 +163,7 @@ PlanOptions options() {
     o.coalesce = (int)g_opt_coalesce.load();
     o.fusion = g_opt_fusion.load() != 0;
     o.reg_bits = (int)g_opt_regbits.load();
-    o.budget = (int)g_opt_budget.load();
+    o.budget = (int)g_opt_state_budget.load();   // lq_psr_create overrides with g_opt_budget
     return o;
 }
 
@@ -288,7 +293,7 @@ PlanCache g_plan_cache;
 std::string plan_key(char kind, int n, const int32_t *qmap, const void *payload, size_t bytes, const void *stream) {
     std::string k(1, kind);
     int64_t o[8] = {n, g_opt_K.load(), g_opt_coalesce.load(), g_opt_fusion.load(), g_opt_regbits.load(),
-                    g_opt_jit.load(), g_opt_budget.load(), (int64_t)(intptr_t)stream};
+                    g_opt_jit.load(), g_opt_state_budget.load(), (int64_t)(intptr_t)stream};
     k.append(reinterpret_cast<const char *>(o), sizeof(o));
     k.append(reinterpret_cast<const char *>(qmap), sizeof(int32_t) * (size_t)n);
     if (bytes) k.append(reinterpret_cast<const char *>(payload), bytes);
@@ -1273,6 +1278,10 @@ lq_status lq_set_option(int option, int64_t value) {
         return LQ_OK;
     case LQ_OPT_FIRST_PASS_FREE: g_opt_first_free = value ? 1 : 0; return LQ_OK;
     case LQ_OPT_POISON_ALLOC: g_opt_poison = value ? 1 : 0; return LQ_OK;
+    case LQ_OPT_STATE_PASS_BUDGET:
+        if (value < 0 || value > 100000) return fail(LQ_ERR_ARG, "pass budget must be 0..100000");
+        g_opt_state_budget = value;
+        return LQ_OK;
     case LQ_OPT_COMM_TIMEOUT_MS:
         if (value < 0) return fail(LQ_ERR_ARG, "timeout must be >= 0 (0 = wait forever)");
         g_opt_comm_timeout = value;
@@ -1297,6 +1306,7 @@ int64_t lq_get_option(int option) {
     case LQ_OPT_FIRST_PASS_FREE: return g_opt_first_free.load();
     case LQ_OPT_POISON_ALLOC: return g_opt_poison.load();
     case LQ_OPT_COMM_TIMEOUT_MS: return g_opt_comm_timeout.load();
+    case LQ_OPT_STATE_PASS_BUDGET: return g_opt_state_budget.load();
     case LQ_OPT_SWAP_QUBITS: return g_opt_swap_k.load();
     default: return -1;
     }
@@ -1990,6 +2000,7 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     // last gate that touches their qubits)
     lower_pauli(n_qubits, qm, terms, n_terms, ops, P->plan);
     PlanOptions po = options();
+    po.budget = (int)g_opt_budget.load();
     po.first_free = g_opt_first_free.load() != 0;
     plan_circuit(n_qubits, ops, po, P->mb, P->plan);
     P->plan.zero_first = true;   // lq_psr_run launches the first pass with PF_LOAD_ZERO
