@@ -34,13 +34,16 @@ def tm(fn, init):
     return statistics.median(ts)
 
 
+K = int(os.environ.get("LQ_BUDGET_K", 0))   # tile bits (0 = automatic)
+lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
 for b in [int(x) for x in sys.argv[1:]]:
     lq.lq_set_option(lq.LQ_OPT_STATE_PASS_BUDGET, b)
     lq.lq_psr_cache_clear()
-    out = {"budget": b, "n": n}
+    out = {"budget": b, "n": n, "K": K}
     out["trotter_8_steps_ms"] = tm(lambda: sv.trotter_xyz(1.0, 0.7, 0.4, 2.0, 1.0, 0.0, 0.01, 8, 8),
                                    lambda: sv.init_basis((1 << n) - 1))
     out["random200_ms"] = tm(lambda: sv.apply(rand), lambda: sv.init_random(3))
     out["cfg5_1000_ms"] = tm(lambda: sv.apply(cfg5), lambda: sv.init_random(3))
     print(json.dumps(out), flush=True)
 lq.lq_set_option(lq.LQ_OPT_STATE_PASS_BUDGET, 800)
+lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 0)
