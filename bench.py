@@ -547,7 +547,10 @@ def run_cfg5(args, lq, rank, local, world, dev, comm):
             "avg_launch_ms": tile_ms / max(tile_cnt, 1), "peak_source": peak_src,
             "frac_of_nominal_8tbs": (achieved / 8000.0) if achieved else None,
             "kernel_share_of_step": tile_ms / ms_inst if ms_inst > 0 else None,
-            "clocks_instrumented_region": clk_inst}
+            "clocks_instrumented_region": clk_inst,
+            "note": "single-state plans take the 800 FP64 pass budget (LQ_OPT_STATE_PASS_BUDGET): fewer, "
+                    "arithmetic-heavier passes; the update rate rises (1.84 -> 1.65 s per step at n=33) while "
+                    "the pass's HBM fraction falls (0.72 -> 0.51), DESIGN.md §5"}
     exchanges = (ex1[0] - ex0[0]) // 2          # two timed regions
     sent = (ex1[1] - ex0[1]) // 2
     nvl = None
