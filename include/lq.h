@@ -407,8 +407,11 @@ typedef enum {
                                  call returns LQ_ERR_NCCL (later calls on its handles: LQ_ERR_STATE) */
     LQ_OPT_SWAP_QUBITS = 10,  /* sharded states: most global qubits one exchange may move (1..4, default
                                  4; 1 = pairwise half-shard swaps only, k > 1 = all-to-all among 2^k ranks) */
-    LQ_OPT_STATE_PASS_BUDGET = 11 /* the same budget for every other plan (circuits, QFT, expectations,
+    LQ_OPT_STATE_PASS_BUDGET = 11, /* the same budget for every other plan (circuits, QFT, expectations,
                                  Trotter, sharded steps; default 800) */
+    LQ_OPT_GROUP_STAGED = 12  /* testing: 1 runs group-mode exchanges (lq_sv_alloc_group) through the
+                                 NCCL path's pack / unpack kernels and peer map, device copies standing
+                                 in for the send / receive (default 0: in-place k_swap_parts) */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);

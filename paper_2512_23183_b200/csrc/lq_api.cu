@@ -49,6 +49,7 @@ std::atomic<int64_t> g_opt_first_free{1};   // PSR plans: the |0...0> pass is ex
 std::atomic<int64_t> g_opt_poison{0};   // LQ_OPT_POISON_ALLOC
 std::atomic<int64_t> g_opt_comm_timeout{600000};   // LQ_OPT_COMM_TIMEOUT_MS
 std::atomic<int64_t> g_opt_swap_k{4};   // LQ_OPT_SWAP_QUBITS: qubits per global exchange (dist.h)
+std::atomic<int64_t> g_opt_group_staged{0};   // LQ_OPT_GROUP_STAGED: group mode through NCCL mode's pack/unpack
 // FP64 pass budgets, swept on B200: PSR plans (config 4:
 // 2.540 s at 400 vs 2.555 / 2.559 s at 600 / 800) and single-state or
 // sharded plans (n = 30: 8 Trotter steps 371 -> 279 ms, the config-5
@@ -933,6 +934,41 @@ lq_status sh_swap(lq_sv *sv, const DStep &stp) {
     NvtxRange nr_("lq exchange");
     sv->stat_exchanges++;
     sv->stat_bytes_sent += (uint64_t)np * part * sizeof(double2);
+    if (!sv->comm && g_opt_group_staged.load()) {
+        // group mode through NCCL mode's data path: every rank packs its
+        // outgoing parts (k_pack_parts), device copies stand in for the
+        // grouped ncclSend / ncclRecv (rank r's slot p -> the peer's slot for
+        // part value a_r), every rank unpacks (k_unpack_parts) -- the same
+        // kernels, part layout and peer map as sh_swap's NCCL branch
+        const int G = (int)sv->shards.size();
+        const uint64_t ch = std::min(part, (uint64_t)1 << 20), nch = part / ch;
+        const size_t slot_bytes = (size_t)ch * sizeof(double2);
+        LQ_TRY(sv->stage_buf.reserve(2 * (size_t)G * np * slot_bytes, st));
+        double2 *outs = sv->stage_buf.at<double2>(0), *ins = outs + (size_t)G * np * ch;
+        for (uint64_t c = 0; c < nch; c++) {
+            for (int r = 0; r < G; r++) {
+                k_pack_parts<<<dim3(grid_for(ch), np), 256, 0, st>>>(sv->shards[r], outs + (size_t)r * np * ch, ps,
+                                                                     gval(r), c * ch, ch);
+                LQ_TRY(check_launch("k_pack_parts"));
+            }
+            for (int r = 0; r < G; r++) {
+                const uint32_t ar = gval(r);
+                for (uint32_t p = 0; p < np; p++) {
+                    const uint32_t bv = p < ar ? p : p + 1;
+                    const int s2 = peer_of(r, ar, bv);
+                    const uint32_t as = gval(s2), q = ar < as ? ar : ar - 1;   // the peer's slot for part a_r
+                    CUDA_TRY(cudaMemcpyAsync(ins + ((size_t)s2 * np + q) * ch, outs + ((size_t)r * np + p) * ch,
+                                             slot_bytes, cudaMemcpyDeviceToDevice, st));
+                }
+            }
+            for (int r = 0; r < G; r++) {
+                k_unpack_parts<<<dim3(grid_for(ch), np), 256, 0, st>>>(sv->shards[r], ins + (size_t)r * np * ch, ps,
+                                                                       gval(r), c * ch, ch);
+                LQ_TRY(check_launch("k_unpack_parts"));
+            }
+        }
+        return LQ_OK;
+    }
     if (!sv->comm) {   // group mode: every rank of the group lives in this process
         const int G = (int)sv->shards.size();
         for (int r = 0; r < G; r++) {
@@ -1278,6 +1314,7 @@ lq_status lq_set_option(int option, int64_t value) {
         return LQ_OK;
     case LQ_OPT_FIRST_PASS_FREE: g_opt_first_free = value ? 1 : 0; return LQ_OK;
     case LQ_OPT_POISON_ALLOC: g_opt_poison = value ? 1 : 0; return LQ_OK;
+    case LQ_OPT_GROUP_STAGED: g_opt_group_staged = value ? 1 : 0; return LQ_OK;
     case LQ_OPT_STATE_PASS_BUDGET:
         if (value < 0 || value > 100000) return fail(LQ_ERR_ARG, "pass budget must be 0..100000");
         g_opt_state_budget = value;
@@ -1307,6 +1344,7 @@ int64_t lq_get_option(int option) {
     case LQ_OPT_POISON_ALLOC: return g_opt_poison.load();
     case LQ_OPT_COMM_TIMEOUT_MS: return g_opt_comm_timeout.load();
     case LQ_OPT_STATE_PASS_BUDGET: return g_opt_state_budget.load();
+    case LQ_OPT_GROUP_STAGED: return g_opt_group_staged.load();
     case LQ_OPT_SWAP_QUBITS: return g_opt_swap_k.load();
     default: return -1;
     }
