@@ -1,7 +1,8 @@
 """Same-box A/B of config-4 gradient time under environment variants.
 
 Each argument is a variant: "name" or "name:VAR=val,VAR2=val" (empty env =
-the default build).  Every variant runs in its own child process (the
+the default build; AB_TILE_BITS / AB_COALESCE_BITS / AB_REG_BITS /
+AB_PASS_BUDGET / AB_FIRST_PASS_FREE set the library options).  Every variant runs in its own child process (the
 planner reads its experiment switches at plan time); variants are
 interleaved over R rounds so clock drift hits all of them alike.
 Prints one JSON object per variant: median / min gradient ms, passes, E."""
@@ -19,6 +20,9 @@ sys.path.insert(0, %r)
 import torch
 import workloads as W
 from paper_2512_23183_b200 import lq
+for name in ("TILE_BITS", "COALESCE_BITS", "REG_BITS", "PASS_BUDGET", "FIRST_PASS_FREE"):
+    if os.environ.get("AB_" + name):
+        lq.lq_set_option(getattr(lq, "LQ_OPT_" + name), int(os.environ["AB_" + name]))
 w = W.config4()
 npar = len(w.theta)
 th = torch.tensor(w.theta, device="cuda"); g = torch.zeros(npar, dtype=torch.float64, device="cuda")
