@@ -411,7 +411,8 @@ typedef enum {
                                  Trotter, sharded steps; default 800) */
     LQ_OPT_GROUP_STAGED = 12  /* testing: 1 runs group-mode exchanges (lq_sv_alloc_group) through the
                                  NCCL path's pack / unpack kernels and peer map, device copies standing
-                                 in for the send / receive (default 0: in-place k_swap_parts) */
+                                 in for the send / receive (default 0: in-place k_swap_parts); staging
+                                 2 * G * (2^k - 1) * 16 MiB of device memory */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);
