@@ -16,7 +16,7 @@ import pytest
 
 import workloads as W
 from closed_forms import circuit_inverse
-from twin_samples import TWIN_N, twin_indices, twin_weights
+from twin_samples import TWIN_NS, twin_indices, twin_weights
 
 pytestmark = pytest.mark.gpu
 
@@ -72,26 +72,27 @@ def _check_twin(gd, got_idx, read_all):
     assert np.abs(got_idx - want).max() <= AMP_TOL
     full = read_all()
     assert abs(float(np.sum(np.abs(full) ** 2)) - gd["norm2"]) <= 1e-12
-    for wr, pr, pi in zip(twin_weights(TWIN_N), gd["proj_re"], gd["proj_im"]):
+    for wr, pr, pi in zip(twin_weights(gd["n"]), gd["proj_re"], gd["proj_im"]):
         p = complex(np.sum(wr * full))
         assert abs(p - complex(pr, pi)) <= AMP_TOL, (p, pr, pi)
 
 
+@pytest.mark.parametrize("n", TWIN_NS)
 @pytest.mark.parametrize("m", [1, 2, 3])
 @pytest.mark.parametrize("sharded", [False, True])
-def test_config5_twin_n24_vs_oracle(lq, m, sharded):
+def test_config5_twin_vs_oracle(lq, n, m, sharded):
     """SURVEY c.4 (iv): the config-5 generator with the configured m at
-    n = 24 (init_random, 1000 gates with 30 % on the m global qubits, QFT),
-    unsharded and on G = 2^m shards (group mode: the same schedule, swaps and
-    local plans as the NCCL path), against the oracle's amplitudes at 4096
-    seeded indices, its norm, and three +-1 projections over every amplitude
-    (tests/golden/cfg5_twin_n24_m*.json)."""
-    gd = _gold(f"cfg5_twin_n{TWIN_N}_m{m}.json")
-    w = W.config5(n=TWIN_N, m=m)
-    assert gd["seed"] == w.seed and gd["n_gates"] == len(w.gates)
-    sv = lq.ShardedState(TWIN_N, group_world=1 << m) if sharded else lq.StateVector(TWIN_N)
+    the reduced sizes n = 24 and 26 (init_random, 1000 gates with 30 % on the
+    m global qubits, QFT), unsharded and on G = 2^m shards (group mode: the
+    same schedule, exchanges and local plans as the NCCL path), against the
+    oracle's amplitudes at 4096 seeded indices, its norm, and three +-1
+    projections over every amplitude (tests/golden/cfg5_twin_n*_m*.json)."""
+    gd = _gold(f"cfg5_twin_n{n}_m{m}.json")
+    w = W.config5(n=n, m=m)
+    assert gd["seed"] == w.seed and gd["n_gates"] == len(w.gates) and gd["n"] == n
+    sv = lq.ShardedState(n, group_world=1 << m) if sharded else lq.StateVector(n)
     sv.init_random(w.seed).apply(w.gates).qft()
-    idx = twin_indices(TWIN_N, m)
+    idx = twin_indices(n, m)
     assert list(idx) == gd["idx"]
     _check_twin(gd, sv.gather(idx.astype(np.uint64)), sv.read)
     sv.free()

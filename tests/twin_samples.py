@@ -7,6 +7,7 @@ from __future__ import annotations
 import numpy as np
 
 TWIN_N = 24
+TWIN_NS = (24, 26)          # reduced twins of config 5 with golden oracle files
 TWIN_SAMPLES = 4096
 _SEED = 251223183 + 50
 

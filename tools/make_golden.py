@@ -10,8 +10,8 @@ once here instead of on the GPU box.
        and the 8 seeded components of
       ``W.config4().meta['oracle_params']`` by the parameter-shift rule
       (PAPER.md:374-377, 501-539): 17 circuits of 720 gates on 2^24 amplitudes.
-  tests/golden/cfg5_twin_n24_m{1,2,3}.json   the config-5 generator at the
-      reduced size n=24 with the configured m:
+  tests/golden/cfg5_twin_n{24,26}_m{1,2,3}.json   the config-5 generator at
+      the reduced sizes n=24 and 26 with the configured m:
       init_random(seed), the 1000-gate circuit
       (reading A13), then the QFT (Alg. 3).  Stored: the
       amplitudes at 4096 seeded indices and three seeded full-state
@@ -19,7 +19,8 @@ once here instead of on the GPU box.
       ``twin_weights`` (a plain counter hash, no arithmetic of the method),
       so every amplitude enters the comparison.
 
-Run:  python tools/make_golden.py [cfg4] [cfg5]   (about 5 min on 8 cores)
+Run:  python tools/make_golden.py [cfg4] [cfg5] [cfg5n26]   (about 5 min on 8 cores;
+      the n = 26 twins about 8 min more)
 """
 from __future__ import annotations
 
@@ -38,7 +39,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import oracle  # noqa: E402
 import workloads as W  # noqa: E402
-from twin_samples import TWIN_N, TWIN_SAMPLES, twin_indices, twin_weights  # noqa: E402
+from twin_samples import TWIN_N, TWIN_NS, TWIN_SAMPLES, twin_indices, twin_weights  # noqa: E402
 
 GOLD = os.path.join(ROOT, "tests", "golden")
 
@@ -64,8 +65,7 @@ def cfg4(threads: int):
     print("cfg4", out["energy"], out["grad"], out["oracle_seconds"], "s")
 
 
-def twin(m: int):
-    n = TWIN_N
+def twin(m: int, n: int = TWIN_N):
     w = W.config5(n=n, m=m)
     t0 = time.time()
     psi = oracle.init_random(n, w.seed)
@@ -96,6 +96,8 @@ def main():
         futs = []
         if "cfg5" in what:
             futs += [ex.submit(twin, m) for m in (1, 2, 3)]
+        if "cfg5n26" in what:
+            futs += [ex.submit(twin, m, 26) for m in (1, 2, 3)]
         if "cfg4" in what:
             futs.append(ex.submit(cfg4, max(1, threads - 3)))
         for f in futs:
