@@ -162,7 +162,9 @@ lq_status lq_sv_canonicalize(lq_sv *sv);
  * global qubit is a rank relabel.  Every call on a sharded handle is
  * COLLECTIVE: all ranks make the same calls with the same arguments, in the
  * same order; host results (norm, expectation, read/gather) are returned on
- * every rank.  lq_sv_write and lq_sv_canonicalize reject sharded handles. */
+ * every rank.  lq_sv_write on a sharded handle writes the logical range on
+ * the ranks that own it (every rank passes the same host data: checkpoint
+ * restore); lq_sv_canonicalize rejects sharded handles. */
 typedef struct lq_comm lq_comm;   /* NCCL communicator (one process per GPU) */
 
 /* ncclUniqueId for lq_comm_init (len >= 128): call on rank 0 and broadcast

@@ -458,11 +458,12 @@ __global__ void k_gather(int n, QMap m, const double2 *__restrict__ psi, const u
     }
 }
 
-__global__ void k_scatter(int n, QMap m, double2 *__restrict__ psi, uint64_t offset, uint64_t count,
-                          const double2 *__restrict__ in) {
+// idx (nullable): explicit indices instead of offset + i (sharded writes)
+__global__ void k_scatter(int n, QMap m, double2 *__restrict__ psi, const uint64_t *__restrict__ idx, uint64_t offset,
+                          uint64_t count, const double2 *__restrict__ in) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
          i += (uint64_t)gridDim.x * blockDim.x)
-        psi[logical_to_phys(offset + i, n, m)] = in[i];
+        psi[logical_to_phys(idx ? idx[i] : offset + i, n, m)] = in[i];
 }
 
 // ---------------------------------------------------------------- Pauli expectation (a7)

@@ -1721,12 +1721,40 @@ static lq_status sv_gather_body(lq_sv *sv, const uint64_t *idx, size_t count, do
 
 static lq_status sv_write_body(lq_sv *sv, uint64_t offset, uint64_t count, const double *host_in) {
     LQ_TRY(check_sv(sv));
-    if (sv->m) return fail(LQ_ERR_ARG, "lq_sv_write is not supported on sharded states");
     if (!host_in && count) return fail(LQ_ERR_ARG, "host_in is NULL");
     uint64_t N = 1ull << sv->n;
     if (offset > N || count > N - offset) return fail(LQ_ERR_DIM, "write range out of bounds");
     for (uint64_t i = 0; i < 2 * count; i++)
         if (!std::isfinite(host_in[i])) return fail(LQ_ERR_NONFINITE, "non-finite amplitude");
+    if (sv->m) {   // sharded: every rank writes the amplitudes it owns (collective, same host data)
+        const size_t nk = sv->shards.size();
+        std::vector<std::vector<uint64_t>> li(nk);
+        std::vector<std::vector<double2>> val(nk);
+        for (uint64_t i = 0; i < count; i++) {
+            int k;
+            uint64_t l;
+            sh_locate(sv, offset + i, &k, &l);
+            if (k < 0) continue;
+            li[k].push_back(l);
+            val[k].push_back(make_double2(host_in[2 * i], host_in[2 * i + 1]));
+        }
+        QMap ident;
+        memset(&ident, 0, sizeof(ident));
+        for (int q = 0; q < sv->nl; q++) ident.q[q] = (int8_t)(sv->nl - 1 - q);
+        for (size_t k = 0; k < nk; k++) {
+            const uint64_t c = li[k].size();
+            if (!c) continue;
+            LQ_TRY(sv->work_buf.reserve(c * (sizeof(double2) + sizeof(uint64_t)), sv->stream));
+            double2 *tmp = sv->work_buf.at<double2>(0);
+            uint64_t *didx = reinterpret_cast<uint64_t *>(tmp + c);
+            CUDA_TRY(cudaMemcpyAsync(tmp, val[k].data(), c * sizeof(double2), cudaMemcpyHostToDevice, sv->stream));
+            CUDA_TRY(cudaMemcpyAsync(didx, li[k].data(), c * sizeof(uint64_t), cudaMemcpyHostToDevice, sv->stream));
+            k_scatter<<<grid_for(c), 256, 0, sv->stream>>>(sv->nl, ident, sv->shards[k], didx, 0, c, tmp);
+            LQ_TRY(check_launch("k_scatter"));
+            LQ_TRY(sync(sv->stream));
+        }
+        return LQ_OK;
+    }
     const uint64_t CH = 1ull << 22;
     LQ_TRY(sv->work_buf.reserve((size_t)std::min(count, CH) * sizeof(double2) + 16, sv->stream));
     QMap m = to_qmap(sv->n, sv->qmap);
@@ -1734,7 +1762,7 @@ static lq_status sv_write_body(lq_sv *sv, uint64_t offset, uint64_t count, const
         uint64_t cnt = std::min(CH, count - c0);
         double2 *tmp = sv->work_buf.at<double2>(0);
         CUDA_TRY(cudaMemcpyAsync(tmp, host_in + 2 * c0, cnt * sizeof(double2), cudaMemcpyHostToDevice, sv->stream));
-        k_scatter<<<grid_for(cnt), 256, 0, sv->stream>>>(sv->n, m, sv->d, offset + c0, cnt, tmp);
+        k_scatter<<<grid_for(cnt), 256, 0, sv->stream>>>(sv->n, m, sv->d, nullptr, offset + c0, cnt, tmp);
         LQ_TRY(check_launch("k_scatter"));
         LQ_TRY(sync(sv->stream));
     }
