@@ -120,7 +120,7 @@ def test_init_basis_norm_gather_write(lq):
 
 # ---------------------------------------------------------------- circuits
 
-@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 10, 13, 14, 17, 20])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 10, 12, 13, 14, 17, 20])
 def test_rich_random_circuit(lq, oracle, n):
     rng = np.random.default_rng(1000 + n)
     gates = rich_circuit(n, 160, rng)
@@ -379,6 +379,33 @@ def test_config3_gradient(lq, oracle):
     go = oracle.param_shift_grad(w.n, w.gates, w.theta, w.terms)
     eo = oracle.energy(w.n, w.gates, w.theta, w.terms)
     grad_close(g, go)
+    assert abs(e - eo) <= 1e-10 * max(abs(eo), 1)
+
+
+PARAM_KINDS = ("RX", "RY", "RZ", "CP", "CRY", "RXX", "RYY", "RZZ")
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 6, 9, 12])
+def test_psr_every_kind(lq, oracle, n):
+    """Parameter-shift gradients of circuits with every gate kind, one
+    parameter per rotation (reading A7) plus two no gate uses
+    (CRY four-term rule, reading A8), and Pauli sums with
+    X / Y / Z factors, vs the oracle."""
+    rng = np.random.default_rng(4200 + n)
+    gates, n_par = [], 0
+    for g in rich_circuit(n, 60, rng):
+        if g[0] in PARAM_KINDS:
+            g = (g[0], g[1], g[2], n_par, 0.0)
+            n_par += 1
+        gates.append(g)
+    n_par += 2                                   # two parameters no gate uses: g = 0
+    theta = rng.uniform(0, 2 * np.pi, n_par)
+    terms = W.random_pauli_sum(n, min(12, 4 ** n), rng)
+    g, e = lq.lq_param_shift_grad(n, gates, theta, terms)
+    go = oracle.param_shift_grad(n, gates, theta, terms, threads=8)
+    grad_close(g, go)
+    assert g[-1] == 0.0 and g[-2] == 0.0
+    eo = oracle.energy(n, gates, theta, terms)
     assert abs(e - eo) <= 1e-10 * max(abs(eo), 1)
 
 
