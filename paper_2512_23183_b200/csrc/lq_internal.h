@@ -177,7 +177,11 @@ struct KPermTerm {
 enum PassFlags : uint32_t {
     PF_LOAD_ZERO = 1,    // synthesise |0...0> instead of loading (fused init_basis(0))
     PF_EXPV = 2,         // the pass evaluates Pauli groups: write one partial sum per tile
-    PF_NO_STORE = 4      // the state after the pass is not needed (read-only pass / final PSR pass)
+    PF_NO_STORE = 4,     // the state after the pass is not needed (read-only pass / final PSR pass)
+    PF_RELABEL = 8       // store without the store exchange: register i of the last mapping goes to the
+                         // i-th register bit of Sstore and its other bits, in order, to Sstore's other
+                         // bits -- a permutation of the tile's local bits the plan absorbs into the
+                         // qubit map (plan_qft's last pass)
 };
 
 // Tile pass descriptor, passed by value to the kernel.

@@ -475,7 +475,11 @@ __device__ __forceinline__ double2 qft_thread_twiddle(const KOp &op, uint64_t gb
         }
         const uint64_t Lt = (jm == 0) ? 0ull : (lg & ((1ull << jm) - 1));
         double s, c;
+#ifdef LQ_EXP_NOSINCOS   // timing experiment only: wrong twiddles
+        s = ldexp((double)Lt, -jm); c = 1.0 - s;
+#else
         sincospi(ldexp((double)Lt, -jm), &s, &c);
+#endif
         ttmax = make_double2(c, inv ? -s : s);
         ts.ttcur = ttmax;
         ts.tj = jm;
@@ -1079,9 +1083,12 @@ __device__ __forceinline__ void tile_body(const KPass &P, const KSub *__restrict
         }
         materialize<RR>(a, ts, true);
         const uint32_t ms = smask<RR>(P.Sstore);
-        // a non-zero flip mask would scatter the lanes of each store: go
-        // through shared memory (collective decision: the exchange syncs)
-        if (__syncthreads_or(ms != cur_m || ts.fb != 0 || P.store_perm >= 0)) {
+        if (P.flags & PF_RELABEL) {   // no exchange: registers to the Sstore mapping's positions
+            flush_flips<RR>(a, ts.fb);
+            cur.make(t, P.Sstore, s_dlo, s_dhi, tb);
+        } else if (__syncthreads_or(ms != cur_m || ts.fb != 0 || P.store_perm >= 0)) {
+            // a non-zero flip mask would scatter the lanes of each store: go
+            // through shared memory (collective decision: the exchange syncs)
             const uint32_t adj = cur.soff_dyn(ts.fb);
             Unroll<RR>::run([&](auto V) { b[cur.template sidx<decltype(V)::value>() ^ adj] = a[decltype(V)::value]; });
             ts.fb = 0;
@@ -1341,9 +1348,13 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
                 return;
             }
             materialize<RR>(a, ts, true);
-            constexpr bool need_x = D::SSTORE != D::SM[LAST] || D::STORE_PERM >= 0;
+            // RELABEL (PF_RELABEL): no store exchange -- the registers go to
+            // the SSTORE mapping's positions, a local-bit permutation the
+            // plan absorbed into the qubit map
+            constexpr bool need_x = !D::RELABEL && (D::SSTORE != D::SM[LAST] || D::STORE_PERM >= 0);
             bool ex = need_x;
-            if constexpr (!need_x) ex = __syncthreads_or(ts.fb != 0);
+            if constexpr (D::RELABEL) flush_flips<RR>(a, ts.fb);
+            else if constexpr (!need_x) ex = __syncthreads_or(ts.fb != 0);
             if (ex) {
                 if constexpr (need_x && !D::WSAFE[LAST]) __syncthreads();
                 xwrite_c<RR, D, D::SM[LAST], D::ADD_S>(b, a, t, ts.fb);

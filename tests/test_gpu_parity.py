@@ -247,6 +247,33 @@ def test_qft_small_tiles(lq, oracle, K, rb):
     assert np.abs(run_gpu(lq, n, 5, [], qft="forward") - ref).max() <= AMP_TOL
 
 
+@pytest.mark.parametrize("jit", [0, 2])
+@pytest.mark.parametrize("n", [13, 15, 20])
+def test_qft_relabel_store_chains(lq, oracle, n, jit):
+    """plan_qft's last pass stores without a store exchange and relabels the
+    qubits (PF_RELABEL): the forward QFT ends in a layout that is neither
+    natural nor reversed, so a following QFT / inverse QFT takes the
+    permuted-layout path.  Every link vs the oracle, interpreter and JIT."""
+    lq.lq_set_option(lq.LQ_OPT_JIT, jit)
+    psi = oracle.init_random(n, 40 + n)
+    sv = lq.StateVector(n).init_random(40 + n)
+    oracle.qft(psi)
+    sv.qft()
+    qm = sv.qubit_map()
+    assert sorted(qm) == list(range(n))
+    assert qm != list(range(n)) and qm != [n - 1 - q for q in range(n)]
+    assert np.abs(sv.read() - psi).max() <= AMP_TOL
+    oracle.qft(psi)
+    sv.qft()
+    assert np.abs(sv.read() - psi).max() <= AMP_TOL
+    oracle.qft(psi, inverse=True)
+    oracle.qft(psi, inverse=True)
+    sv.qft(inverse=True).qft(inverse=True)
+    assert np.abs(sv.read() - psi).max() <= AMP_TOL
+    np.testing.assert_allclose(sv.read(), oracle.init_random(n, 40 + n), rtol=0, atol=AMP_TOL)
+    sv.free()
+
+
 def test_qft_then_gates_then_canonicalize(lq, oracle):
     """Gates after a QFT act through the qubit map; canonicalize
     materialises natural order."""
