@@ -411,10 +411,19 @@ typedef enum {
                                  4; 1 = pairwise half-shard swaps only, k > 1 = all-to-all among 2^k ranks) */
     LQ_OPT_STATE_PASS_BUDGET = 11, /* the same budget for every other plan (circuits, QFT, expectations,
                                  Trotter, sharded steps; default 800) */
-    LQ_OPT_GROUP_STAGED = 12  /* testing: 1 runs group-mode exchanges (lq_sv_alloc_group) through the
+    LQ_OPT_GROUP_STAGED = 12, /* testing: 1 runs group-mode exchanges (lq_sv_alloc_group) through the
                                  NCCL path's pack / unpack kernels and peer map, device copies standing
                                  in for the send / receive (default 0: in-place k_swap_parts); staging
                                  2 * G * (2^k - 1) * 16 MiB of device memory */
+    LQ_OPT_RELABEL_STORES = 13, /* parameter-shift plans (JIT): 0 (default) = every tile pass updates the
+                                 state in place; 3..5 = relabelling out-of-place stores -- each tile
+                                 pass writes the state to a second buffer in the frame where the next
+                                 pass's tile bits are the contiguous low bits (contiguous reads), its
+                                 lowest `value` lane bits held by that tile (128..512-byte write runs);
+                                 doubles the batch's state memory.  Same results; on config 4 it
+                                 measured 2 % slower than in place */
+    LQ_OPT_EXPORT_PSR = 14    /* testing: 1 makes lq_plan_export_json plan like lq_psr_create (pass
+                                 budget, first-pass exemption, relabelling stores) */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);

@@ -56,6 +56,8 @@ std::atomic<int64_t> g_opt_group_staged{0};   // LQ_OPT_GROUP_STAGED: group mode
 // circuit 186 -> 151 ms, 200 random gates 40.5 -> 35.9 ms at 800 vs 400)
 std::atomic<int64_t> g_opt_budget{400};         // LQ_OPT_PASS_BUDGET (PSR plans)
 std::atomic<int64_t> g_opt_state_budget{800};   // LQ_OPT_STATE_PASS_BUDGET (every other plan)
+std::atomic<int64_t> g_opt_relabel{0};          // LQ_OPT_RELABEL_STORES (PSR plans; measured, off)
+std::atomic<int64_t> g_opt_export_psr{0};       // LQ_OPT_EXPORT_PSR (testing)
 const double PI = 3.14159265358979323846264338327950288;
 
 lq_status fail(lq_status s, const std::string &msg) {
@@ -168,6 +170,18 @@ PlanOptions options() {
     return o;
 }
 
+// Planner options of lq_plan_describe / lq_plan_export_json: the generic
+// ones, or (LQ_OPT_EXPORT_PSR) those of the parameter-shift planner.
+PlanOptions export_options() {
+    PlanOptions po = options();
+    if (g_opt_export_psr.load()) {
+        po.budget = (int)g_opt_budget.load();
+        po.first_free = g_opt_first_free.load() != 0;
+        po.oop = (int)g_opt_relabel.load();
+    }
+    return po;
+}
+
 // JIT-specialise the plan's tile passes (LQ_OPT_JIT).  Auto mode (1)
 // compiles plans that will stream enough amplitudes to amortise NVRTC
 // (~1-5 s per pass): every PSR plan (it runs 2P+1 circuits) and single
@@ -206,6 +220,7 @@ lq_status prepare(Plan &plan, bool reused = false) {
             if (p.kind != PASS_TILE) { ok = false; break; }
             if (p.kp.flags & PF_NO_STORE) continue;
             for (int b = 0; b < p.kp.K; b++) U |= 1ull << p.kp.T[b];
+            U = p.map_store(U);   // a relabelling store moves the support into the next frame
         }
         if (U != all && !plan.wide_groups.empty()) ok = false;
         U = 0;
@@ -218,7 +233,7 @@ lq_status prepare(Plan &plan, bool reused = false) {
                 p.sup_free = U & ~tm & all;
                 p.tiles_log2 = __builtin_popcountll(p.sup_free);
             }
-            if (!(p.kp.flags & PF_NO_STORE)) U |= tm;
+            if (!(p.kp.flags & PF_NO_STORE)) U = p.map_store(U | tm);
         }
     }
     plan.ctab = getenv("LQ_JIT_NO_CTAB") == nullptr;   // constant-bank op tables (A/B switch for experiments)
@@ -443,7 +458,8 @@ template <int RR>
 lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
                          const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                          uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride,
-                         int n_circ, double *partials, uint64_t slot_stride, cudaStream_t st, int tl2) {
+                         int n_circ, double *partials, uint64_t slot_stride, cudaStream_t st, int tl2,
+                         double2 *state_out) {
     static bool attr = false;
     static int n_sm = 0;
     const size_t smem = ((size_t)32 << kp.K) + (size_t)kp.smat * sizeof(double2) +
@@ -480,22 +496,24 @@ lq_status launch_tile_rr(const void *jk, const KPass &kp, const KSub *subs, cons
         void *args[] = {(void *)&kp,      (void *)&subs,   (void *)&kops,       (void *)&perms, (void *)&pterms,
                         (void *)&eterms,  (void *)&mats,   (void *)&mat_stride, (void *)&cst,   (void *)&state,
                         (void *)&state_stride, (void *)&tiles_log2, (void *)&tot32, (void *)&partials,
-                        (void *)&slot_stride};
+                        (void *)&slot_stride, (void *)&state_out};
         CUDA_TRY(cudaLaunchKernel(jk, dim3(grid), dim3(1u << (kp.K - RR)), args, smem, st));
         return check_launch("k_tile (jit)");
     }
     k_tile<RR><<<grid, 1u << (kp.K - RR), smem, st>>>(kp, subs, kops, perms, pterms, eterms, mats, mat_stride, cst,
                                                       state, state_stride, tiles_log2, (uint32_t)total, partials,
-                                                      slot_stride);
+                                                      slot_stride, state);
     return check_launch("k_tile");
 }
 
 lq_status launch_tile(int Rr, const void *jk, const KPass &kp, const KSub *subs, const KOp *kops, const KPerm *perms,
                       const KPermTerm *pterms, uint32_t n_pterms, const ETerm *eterms, const double2 *mats,
                       uint64_t mat_stride, const double2 *cst, double2 *state, uint64_t state_stride, int n_circ,
-                      double *partials, uint64_t slot_stride, cudaStream_t st, int tl2 = -1) {
+                      double *partials, uint64_t slot_stride, cudaStream_t st, int tl2 = -1,
+                      double2 *state_out = nullptr) {
+    if (!state_out) state_out = state;
 #define LT(RRV) launch_tile_rr<RRV>(jk, kp, subs, kops, perms, pterms, n_pterms, eterms, mats, mat_stride, cst, state, \
-                                    state_stride, n_circ, partials, slot_stride, st, tl2)
+                                    state_stride, n_circ, partials, slot_stride, st, tl2, state_out)
     switch (Rr) {
     case 1: return LT(1);
     case 2: return LT(2);
@@ -528,11 +546,17 @@ std::mutex &ctab_mutex(const void *bank) {
     return mu[((uintptr_t)bank >> 8) % 64];
 }
 
+// alt (plans with relabelling stores, Plan::has_oop): the second buffer of
+// the ping-pong pair, as large as `state`; *final_out: the buffer that holds
+// the state after the plan.
 lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uint64_t state_stride, int n_circ,
                         const double2 *mats, uint64_t mat_stride, cudaStream_t st, bool zero_first,
                         double *partials = nullptr, uint64_t slot_stride = 0, bool no_final_store = false,
-                        uint64_t gofs = 0) {
+                        uint64_t gofs = 0, double2 *alt = nullptr, double2 **final_out = nullptr) {
     const int n = plan.nl;   // local index bits
+    if (final_out) *final_out = state;
+    if (plan.has_oop && !alt) return fail(LQ_ERR_STATE, "relabelling plan without a second state buffer (internal)");
+    double2 *const alt_base = state;
     if (zero_first && (plan.passes.empty() || plan.passes[0].kind != PASS_TILE)) {
         dim3 grid(grid_for(1ull << n), n_circ);
         k_fill_basis<<<grid, 256, 0, st>>>(1ull << n, 0, state, state_stride);
@@ -576,8 +600,14 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
             if ((p.tiles_log2 >= 0 || p.support != ~0ull) && jk && !zero_first)
                 return fail(LQ_ERR_STATE, "restricted tile range outside a zero-first run (internal)");
             const int tl2 = jk ? p.tiles_log2 : -1;
+            // a relabelling pass stores into the other buffer (JIT programs only)
+            const bool oop = p.oop && !(kp.flags & PF_NO_STORE);
+            if (p.oop && !jk) return fail(LQ_ERR_STATE, "relabelling pass without its JIT program (internal)");
+            double2 *out = oop ? (state == alt ? alt_base : alt) : state;
             LQ_TRY(launch_tile(plan.Rr, jk, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, dp.eterms, mats, mat_stride,
-                               dp.cst, state, state_stride, n_circ, partials, slot_stride, st, tl2));
+                               dp.cst, state, state_stride, n_circ, partials, slot_stride, st, tl2, out));
+            state = out;
+            if (final_out) *final_out = state;
         } else if (p.kind == PASS_PAIR) {
             const KOp op = plan.kops[p.op_begin];
             uint64_t work = (op.type == K_U1 || op.type == K_X) ? (1ull << (n - 1)) : (1ull << (n - 2));
@@ -1327,6 +1357,11 @@ lq_status lq_set_option(int option, int64_t value) {
         if (value < 1 || value > 4) return fail(LQ_ERR_ARG, "qubits per exchange must be 1..4");
         g_opt_swap_k = value;
         return LQ_OK;
+    case LQ_OPT_RELABEL_STORES:
+        if (value != 0 && (value < 3 || value > 5)) return fail(LQ_ERR_ARG, "relabel stores must be 0 or 3..5");
+        g_opt_relabel = value;
+        return LQ_OK;
+    case LQ_OPT_EXPORT_PSR: g_opt_export_psr = value ? 1 : 0; return LQ_OK;
     default: return fail(LQ_ERR_ARG, "unknown option");
     }
 }
@@ -1343,6 +1378,8 @@ int64_t lq_get_option(int option) {
     case LQ_OPT_FIRST_PASS_FREE: return g_opt_first_free.load();
     case LQ_OPT_POISON_ALLOC: return g_opt_poison.load();
     case LQ_OPT_COMM_TIMEOUT_MS: return g_opt_comm_timeout.load();
+    case LQ_OPT_RELABEL_STORES: return g_opt_relabel.load();
+    case LQ_OPT_EXPORT_PSR: return g_opt_export_psr.load();
     case LQ_OPT_STATE_PASS_BUDGET: return g_opt_state_budget.load();
     case LQ_OPT_GROUP_STAGED: return g_opt_group_staged.load();
     case LQ_OPT_SWAP_QUBITS: return g_opt_swap_k.load();
@@ -1999,7 +2036,10 @@ lq_status lq_plan_export_json(int n_qubits, const lq_gate *gates, size_t n_gates
     Plan plan;
     lower_gates(n_qubits, gates, n_gates, qm, ops, mb);
     if (n_terms) lower_pauli(n_qubits, qm, terms, n_terms, ops, plan);
-    plan_circuit(n_qubits, ops, options(), mb, plan);
+    plan_circuit(n_qubits, ops, export_options(), mb, plan);
+    if (plan.has_oop) {   // the layout after the plan: qubit q ends at frame[qm[q]]
+        for (int q = 0; q < n_qubits; q++) qm[q] = plan.frame[qm[q]];
+    }
     std::string j = export_json(plan, mb, qm);
     if (needed) *needed = j.size() + 1;
     if (buf && buf_len) {
@@ -2068,6 +2108,8 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     PlanOptions po = options();
     po.budget = (int)g_opt_budget.load();
     po.first_free = g_opt_first_free.load() != 0;
+    // relabelling stores need the JIT tile programs (the interpreter stores in place)
+    po.oop = g_opt_jit.load() != 0 ? (int)g_opt_relabel.load() : 0;
     plan_circuit(n_qubits, ops, po, P->mb, P->plan);
     P->plan.zero_first = true;   // lq_psr_run launches the first pass with PF_LOAD_ZERO
     P->dset.build(P->plan);
@@ -2124,7 +2166,8 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
            o_cd = blob.add(P->plan.ctab_desc);
     P->blob_bytes = blob.h.size();
     lq_status s = blob.upload(P->blob_buf, st);
-    if (s == LQ_OK) s = P->states.reserve((size_t)B * N * sizeof(double2), st);
+    // relabelling plans ping-pong between two batches of states
+    if (s == LQ_OK) s = P->states.reserve((size_t)B * N * sizeof(double2) * (P->plan.has_oop ? 2 : 1), st);
     if (s == LQ_OK) s = P->mats.reserve((size_t)B * std::max<uint32_t>(P->mb.mat_size, 1) * sizeof(double2), st);
     if (s == LQ_OK) s = P->partials.reserve((size_t)B * P->dset.stride() * sizeof(double), st);
     if (s == LQ_OK) s = P->E.reserve(sizeof(double) * std::max(n_circ, 1), st);
@@ -2192,8 +2235,10 @@ static lq_status psr_run_body(lq_psr *P, const double *theta_dev, double *grad_d
         const uint32_t ss = P->dset.stride();
         // the state after the last pass is only read by the Pauli groups of
         // that pass: no store (unless a wide group still has to read it)
-        LQ_TRY(launch_passes(P->plan, P->dp, states, N, nb, mats, ms, st, true, part, ss, P->dset.ds.empty()));
-        LQ_TRY(finish_expv(P->plan, P->dset, P->d_terms, states, N, nb, part, ss, E + c0, st));
+        double2 *fin = states;
+        LQ_TRY(launch_passes(P->plan, P->dp, states, N, nb, mats, ms, st, true, part, ss, P->dset.ds.empty(), 0,
+                             P->plan.has_oop ? states + (uint64_t)P->B * N : nullptr, &fin));
+        LQ_TRY(finish_expv(P->plan, P->dset, P->d_terms, fin, N, nb, part, ss, E + c0, st));
     }
     if (!P->comm || !P->comm->c) {
         k_psr_combine<<<1, 256, 0, st>>>(E, P->d_pairs, (int)P->pairs.size(), P->base_idx, grad_dev,
@@ -2561,7 +2606,8 @@ lq_status lq_jit_compile_check(int n_qubits, const lq_gate *gates, size_t n_gate
     Plan plan;
     lower_gates(n_qubits, gates, n_gates, qm, ops, mb);
     if (n_terms) lower_pauli(n_qubits, qm, terms, n_terms, ops, plan);
-    plan_circuit(n_qubits, ops, options(), mb, plan);
+    plan_circuit(n_qubits, ops, export_options(), mb, plan);
+    plan.zero_first = g_opt_export_psr.load() != 0;
     plan.ctab = getenv("LQ_JIT_NO_CTAB") == nullptr;   // as prepare() would
     plan.ctab_circ = 4;
     size_t nk = 0;
@@ -2602,7 +2648,7 @@ lq_status lq_plan_describe(int n_qubits, const lq_gate *gates, size_t n_gates, u
     MatBuilder mb;
     lower_gates(n_qubits, gates, n_gates, qm, ops, mb);
     Plan plan;
-    plan_circuit(n_qubits, ops, options(), mb, plan);
+    plan_circuit(n_qubits, ops, export_options(), mb, plan);
     if (n_passes) *n_passes = plan.passes.size();
     if (n_tile) *n_tile = plan.n_tile;
     if (buf && buf_len) {

@@ -689,7 +689,7 @@ static int32_t build_perm(const std::vector<POp> &ops, const std::vector<int> &g
 // permutations being folded into the exchange that starts the sub-block.
 static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vector<POp> &ops,
                       const std::vector<int> &absorbed, const std::vector<uint32_t> &mat_off,
-                      Plan &plan, MatBuilder &mb) {
+                      Plan &plan, MatBuilder &mb, bool oop = false) {
     LocalMap L(Tm);
     int lowrun = (nl > K) ? lowrun_of(L) : 0;
     PlanPass pp;
@@ -757,7 +757,9 @@ static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vect
     uint32_t top = 0;
     for (int b = K - 1; b >= 0 && popc(top) < Rr; b--) top |= 1u << b;
     uint32_t Ss = segs.back().Sm;
-    if (Ss & lane_forbid) Ss = top;
+    // in place, the store's lanes must be the coalescing bits; a relabelling
+    // store (oop) puts whatever its lanes hold at the new frame's low bits
+    if ((Ss & lane_forbid) && !oop) Ss = top;
     mask_to_S(segs.front().Sm, pp.kp.Sload);
     mask_to_S(Ss, pp.kp.Sstore);
     for (auto &sg : segs) {
@@ -793,12 +795,63 @@ static void emit_tile(int n, int nl, int K, int Rr, uint64_t Tm, const std::vect
 
 }  // namespace
 
+
+// Relabelling out-of-place stores (PlanOptions::oop).
+// The lane bits of a tile pass's store: the lowest local bits outside its
+// store register set, as physical bits in the pass's frame (lane order).
+static std::vector<int> store_lanes(const PlanPass &pp, int Rr) {
+    uint32_t sm = 0;
+    for (int i = 0; i < Rr; i++) sm |= 1u << pp.kp.Sstore[i];
+    std::vector<int> l;
+    for (int b = 0; b < pp.kp.K && l.size() < 5; b++)
+        if (!(sm >> b & 1)) l.push_back(pp.kp.T[b]);
+    return l;
+}
+
+// The next frame: the store's lane bits that the next tile holds, in lane
+// order, go to bits 0, 1, ... (each warp store is then one contiguous run);
+// the next tile's other bits follow up to bit K-1; every other bit keeps its
+// relative order above.
+static void next_frame(int nl, const std::vector<int> &lanes, uint64_t Tn, uint8_t *spos) {
+    int nxt = 0;
+    uint64_t placed = 0;
+    for (int b : lanes) {
+        if (!(Tn >> b & 1)) break;
+        spos[b] = (uint8_t)nxt++;
+        placed |= bit(b);
+    }
+    for (int b = 0; b < nl; b++)
+        if ((Tn >> b & 1) && !(placed >> b & 1)) { spos[b] = (uint8_t)nxt++; placed |= bit(b); }
+    for (int b = 0; b < nl; b++)
+        if (!(placed >> b & 1)) spos[b] = (uint8_t)nxt++;
+    for (int b = nl; b < 64; b++) spos[b] = (uint8_t)b;   // global (shard) bits never move
+}
+
+static uint64_t map_bits(uint64_t m, const uint8_t *spos) {
+    uint64_t r = 0;
+    while (m) { int b = __builtin_ctzll(m); r |= bit(spos[b]); m &= m - 1; }
+    return r;
+}
+
+static void remap_op(POp &o, const uint8_t *spos) {
+    if (o.t0 >= 0) o.t0 = spos[o.t0];
+    if (o.t1 >= 0) o.t1 = spos[o.t1];
+    o.ctrl = map_bits(o.ctrl, spos);
+    o.xm = map_bits(o.xm, spos);
+    o.zm = map_bits(o.zm, spos);
+    o.rd = map_bits(o.rd, spos);
+    o.gx = map_bits(o.gx, spos);
+    o.gz = map_bits(o.gz, spos);
+}
+
 // op types the strided pair kernel (k_pair) executes; everything else
 // (QFT stages, ...) runs in a tile pass even when alone
 static bool pair_kernel_op(uint8_t t) { return t == K_U1 || t == K_X || t == K_G || t == K_U2 || t == K_SWAP; }
 
-void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, MatBuilder &mb,
+void plan_circuit(int n, const std::vector<POp> &ops_in, const PlanOptions &opt, MatBuilder &mb,
                   Plan &plan) {
+    std::vector<POp> ops(ops_in);   // relabelling stores (opt.oop) move later ops into new frames
+    for (int b = 0; b < 64; b++) plan.frame[b] = (uint8_t)b;
     std::vector<uint32_t> mat_off;
     for (auto &sp : mb.specs) mat_off.push_back(sp.out);
     const int nl = opt.n_local > 0 ? std::min(opt.n_local, n) : n;   // tile bits come from [0, nl)
@@ -881,14 +934,26 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
     // some bits reads only 2^|U| amplitudes, so its HBM time is about
     // (2^(|U|-nl) + 1) / 2 of a full pass and so is the arithmetic it can hide
     const bool sup_budget = getenv("LQ_SUPPORT_BUDGET") != nullptr;   // A/B experiments
-    while (!rem.empty()) {
+    // relabelling out-of-place stores (PlanOptions::oop): after each storing
+    // tile pass the next tile is chosen at once -- it must hold the store's
+    // lowest opt.oop lane bits -- and the pass writes the state in the frame
+    // where that tile is bits 0..K-1 (contiguous reads)
+    bool any_qft = false;
+    for (const POp &o : ops) any_qft |= o.type == K_QFT;
+    const bool oop = opt.oop > 0 && nl > K && !any_qft && nl <= 48;
+    // tile selection for the ops in `rem`: Tm starts from `mand0`; the result
+    // is filled to K bits with the bits of `prefer` first, then the lowest
+    auto select = [&](uint64_t mand0, const std::vector<int> &prefer, uint64_t &Tm,
+                      std::vector<int> &absorbed) {
+        const uint64_t mand = mand0;
         int budget = (track && popc(U) <= free_upto) ? 0 : budget_all;
         if (track && sup_budget && budget && popc(U) < nl) {
             const double f = 0.5 * (std::ldexp(1.0, popc(U) - nl) + 1.0);
             budget = std::max(1, (int)(budget * f));
         }
-        uint64_t Tm = mand;
-        std::vector<int> absorbed, absorbed_w;
+        Tm = mand;
+        absorbed.clear();
+        std::vector<int> absorbed_w;
         first_fit(ops, rem, K, Tm, absorbed, budget);
         // local search works on a window of the next ops (bounded cost)
         std::vector<int> window(rem.begin(), rem.begin() + std::min<size_t>(rem.size(), 384));
@@ -933,6 +998,26 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
         }
         if (absorbed.empty()) absorbed.push_back(rem[0]);   // progress guarantee
         if (absorbed.size() > (size_t)MAX_PASS_OPS) absorbed.resize(MAX_PASS_OPS);   // a valid prefix
+        for (int b : prefer)
+            if (popc(Tm) < K && b < nl) Tm |= bit(b);
+        for (int b = 0; b < nl && popc(Tm) < K; b++) Tm |= bit(b);
+    };
+    bool have_pend = false;
+    uint64_t pend_T = 0;
+    std::vector<int> pend_abs;
+    // the first pass of a zero-first plan reads nothing: no coalescing run
+    uint64_t mand_next = (oop && opt.first_free) ? 0 : mand;
+    while (!rem.empty()) {
+        uint64_t Tm = 0;
+        std::vector<int> absorbed;
+        if (have_pend) {
+            Tm = pend_T;
+            absorbed.swap(pend_abs);
+            have_pend = false;
+        } else {
+            select(mand_next, std::vector<int>(), Tm, absorbed);
+        }
+        mand_next = mand;
         int n_full = 0;
         bool has_expv = false;
         for (int i : absorbed) {
@@ -964,10 +1049,9 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
             plan.n_pair++;
             track = false;
         } else {
-            // fill the tile to exactly K bits, lowest free bits first (longer
-            // contiguous runs for coalescing)
-            for (int b = 0; b < nl && popc(Tm) < K; b++) Tm |= bit(b);
-            emit_tile(n, nl, K, Rr, Tm, ops, absorbed, mat_off, plan, mb);
+            // (select() filled the tile to exactly K bits, lowest free bits
+            // first: longer contiguous runs for coalescing)
+            emit_tile(n, nl, K, Rr, Tm, ops, absorbed, mat_off, plan, mb, oop);
             if (!(plan.passes.back().kp.flags & PF_NO_STORE)) U |= Tm;   // a read-only pass leaves U as it was
         }
         // remove absorbed from rem (absorbed is a subsequence of rem)
@@ -978,6 +1062,33 @@ void plan_circuit(int n, const std::vector<POp> &ops, const PlanOptions &opt, Ma
             left.push_back(i);
         }
         rem.swap(left);
+        PlanPass &pp = plan.passes.back();
+        if (oop && pp.kind == PASS_TILE && !(pp.kp.flags & PF_NO_STORE)) {
+            const std::vector<int> lanes = store_lanes(pp, Rr);
+            uint64_t mn = 0;
+            for (size_t k = 0; k < lanes.size() && (int)k < opt.oop; k++) mn |= bit(lanes[k]);
+            uint64_t Tn = mn;
+            if (!rem.empty()) {
+                std::vector<int> prefer(lanes);
+                for (int l = 0; l < pp.kp.K; l++) prefer.push_back(pp.kp.T[l]);
+                select(mn, prefer, Tn, pend_abs);
+                have_pend = true;
+            }
+            next_frame(nl, lanes, Tn, pp.spos);
+            pp.oop = true;
+            plan.has_oop = true;
+            for (POp &o : ops) {
+                remap_op(o, pp.spos);
+                if (o.type == K_EXPV && o.group >= 0) {
+                    PGroup &G = plan.groups[(size_t)o.group];
+                    G.x = map_bits(G.x, pp.spos);
+                    for (auto &t : G.terms) t.z = map_bits(t.z, pp.spos);
+                }
+            }
+            U = map_bits(U, pp.spos);
+            for (int b = 0; b < 64; b++) plan.frame[b] = pp.spos[plan.frame[b]];
+            pend_T = map_bits(Tn, pp.spos);
+        }
     }
 }
 
@@ -1178,7 +1289,13 @@ std::string describe(const Plan &plan) {
         if (p.kind == PASS_TILE) {
             os << "  [" << i << "] TILE ops=" << p.n_ops << " subs=" << (p.kp.sub_end - p.kp.sub_begin) << " T={";
             for (int k = 0; k < p.kp.K; k++) os << (int)p.kp.T[k] << (k + 1 < p.kp.K ? "," : "");
-            os << "}\n";
+            os << "}";
+            if (p.oop) {   // relabelling store: where the tile's bits go in the next frame
+                os << " -> {";
+                for (int k = 0; k < p.kp.K; k++) os << (int)p.spos[p.kp.T[k]] << (k + 1 < p.kp.K ? "," : "");
+                os << "}";
+            }
+            os << (p.kp.flags & PF_NO_STORE ? " ro" : "") << "\n";
         } else {
             os << "  [" << i << "] " << (p.kind == PASS_PAIR ? "PAIR" : "DIAG") << " ops=" << p.n_ops << "\n";
         }
@@ -1210,7 +1327,9 @@ std::string export_json(const Plan &plan, const MatBuilder &mb, const int32_t *q
         o << "],\"T\":[";
         for (int b = 0; b < (p.kind == PASS_TILE ? k.K : 0); b++) o << (b ? "," : "") << (int)k.T[b];
         o << "],\"Sstore\":[" << (int)k.Sstore[0] << "," << (int)k.Sstore[1] << "," << (int)k.Sstore[2] << ","
-          << (int)k.Sstore[3] << "]}";
+          << (int)k.Sstore[3] << "],\"oop\":" << (p.oop ? 1 : 0) << ",\"spos\":[";
+        for (int b = 0; b < (p.oop ? plan.nl : 0); b++) o << (b ? "," : "") << (int)p.spos[b];
+        o << "]}";
     });
     o << ",";
     arr("subs", plan.subs.size(), [&](size_t i) {

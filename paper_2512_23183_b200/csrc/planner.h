@@ -63,6 +63,19 @@ struct PlanPass {
     uint64_t support = ~0ull;
     uint64_t sup_free = ~0ull;
     int tiles_log2 = -1;      // popcount(sup_free) when restricted, else -1 (nl - K)
+    // Relabelling out-of-place store (PlanOptions::oop, TILE passes): the pass
+    // reads the state in its own frame and writes it to the other buffer of a
+    // ping-pong pair with physical bit b moved to bit spos[b] -- the frame of
+    // the next pass, whose tile bits are there the contiguous bits 0..K-1
+    // (DESIGN.md §7).  The plan's ops after this pass are in the new frame.
+    bool oop = false;
+    uint8_t spos[64];
+    uint64_t map_store(uint64_t m) const {   // a physical bit mask in the store frame
+        if (!oop) return m;
+        uint64_t r = 0;
+        while (m) { int b = __builtin_ctzll(m); r |= 1ull << spos[b]; m &= m - 1; }
+        return r;
+    }
 };
 
 struct Plan {
@@ -89,6 +102,8 @@ struct Plan {
     std::vector<void *> jit_ctab;     // per pass: device address of its lqj_ctab, or nullptr (smem tables)
     std::vector<CtabDesc> ctab_desc;  // the passes with jit_ctab, in pass order (staging layout)
     uint32_t ctab_total = 0;          // staging buffer size (double2) for ctab_circ circuits
+    bool has_oop = false;             // some pass stores out of place (the state needs a ping-pong buffer)
+    uint8_t frame[64];                // frame[b]: physical bit, after the plan, of the plan's input bit b
     uint64_t stream_tag = 0;          // the stream the plan runs on: constant banks are per module, so
                                       // JIT modules with constant tables are private to one stream
 };
@@ -111,6 +126,8 @@ struct PlanOptions {
     int n_local = 0;         // sharded state: only bits [0, n_local) are local (0 = all n bits)
     int budget = 0;          // FP64 budget of a tile pass in tenths of an instruction per amplitude (0: none)
     bool first_free = false; // the first pass starts from |0...0> (PSR plans): exempt from the budget
+    int oop = 0;             // > 0: relabelling out-of-place stores (PlanPass::oop); the next tile must hold
+                             // the `oop` lowest lane bits of each store (128 B runs at 3)
 };
 
 // Estimated FP64 instructions per amplitude (x10) an op costs in a tile pass.

@@ -911,7 +911,10 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
         const lq::KPerm *__restrict__ perms, const lq::KPermTerm *__restrict__ pterms,                      \
         const lq::ETerm *__restrict__ eterms, const double2 *__restrict__ mats, uint64_t mat_stride,        \
         const double2 *__restrict__ cst, double2 *__restrict__ state, uint64_t state_stride,                 \
-        uint32_t tiles_log2, uint32_t total_tiles, double *__restrict__ partials, uint64_t slot_stride
+        uint32_t tiles_log2, uint32_t total_tiles, double *__restrict__ partials, uint64_t slot_stride,       \
+        double2 *__restrict__ state_out
+// state_out: where a relabelling out-of-place pass (JIT Desc::OOP, PlanPass::oop) stores the state in the
+// next frame; every other pass updates `state` in place and ignores it
 #define LQ_TILE_ARGS \
     P, subs, ops, perms, pterms, eterms, mats, mat_stride, cst, state, state_stride, tiles_log2, total_tiles, partials, slot_stride
 
@@ -1241,9 +1244,14 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
                                                  uint64_t mat_stride, const double2 *__restrict__ cst,
                                                  double2 *__restrict__ state, uint64_t state_stride,
                                                  uint32_t tiles_log2, uint32_t total_tiles,
-                                                 double *__restrict__ partials, uint64_t slot_stride) {
+                                                 double *__restrict__ partials, uint64_t slot_stride,
+                                                 double2 *__restrict__ state_out) {
     extern __shared__ double2 sm[];
     constexpr int K = D::K;
+    // the store frame (D::OOP: the next pass's frame in the other buffer,
+    // D::sdep / D::stbase = the pass's bit permutation applied to dep / tbase;
+    // otherwise the same addresses in place)
+    double2 *const store_base = D::OOP ? state_out : state;
     constexpr int NV = 1 << RR;
     constexpr uint32_t TS = 1u << K;
     constexpr uint32_t NT = 1u << (K - RR);
@@ -1316,10 +1324,10 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
             // every other tile is zero before and after the pass -- store
             // zeros, skip the arithmetic (CTA-uniform branch)
             if (!(P.flags & PF_NO_STORE)) {
-                double2 *psi = state + (uint64_t)circ * state_stride;
-                const uint64_t gst = tb | D::dep(ins_zeros<D::SSTORE, K>(t));
+                double2 *psi = store_base + (uint64_t)circ * state_stride;
+                const uint64_t gst = D::stbase(g & tmask) | D::sdep(ins_zeros<D::SSTORE, K>(t));
                 Unroll<RR>::run([&](auto V) {
-                    constexpr uint64_t go = D::dep(loff_c<D::SSTORE>(decltype(V)::value));
+                    constexpr uint64_t go = D::sdep(loff_c<D::SSTORE>(decltype(V)::value));
                     psi[gst + go] = make_double2(0.0, 0.0);
                 });
             }
@@ -1339,7 +1347,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
             ts.lpos = P.lpos;
             ts.cbase = CIRC >= 0 ? (uint32_t)CIRC * D::SMAT : (uint32_t)circ * D::SMAT;
             run_subs_c<RR, D, Prog, 0>(a, b, ts, tb, P.gofs, t, s_tab, s_et, P.n, zero);
-            double2 *psi = state + (uint64_t)circ * state_stride;
+            double2 *psi = store_base + (uint64_t)circ * state_stride;
             if (P.flags & PF_EXPV)     // deterministic partials: one per warp of the tile
                 expv_partial(ts.eacc, reinterpret_cast<double *>(b), partials + (uint64_t)circ * slot_stride + P.eslot,
                              g & tmask);
@@ -1361,9 +1369,9 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
                 __syncthreads();
                 xread_c<RR, D, D::SSTORE, D::STORE_PERM, false, D::ADD_S>(b, a, t, tb, P.gofs);
             }
-            const uint64_t gst = tb | D::dep(ins_zeros<D::SSTORE, K>(t));
+            const uint64_t gst = (D::OOP ? D::stbase(g & tmask) : tb) | D::sdep(ins_zeros<D::SSTORE, K>(t));
             Unroll<RR>::run([&](auto V) {
-                constexpr uint64_t go = D::dep(loff_c<D::SSTORE>(decltype(V)::value));
+                constexpr uint64_t go = D::sdep(loff_c<D::SSTORE>(decltype(V)::value));
                 psi[gst + go] = a[decltype(V)::value];
             });
             if constexpr (!LATE) __syncthreads();   // buffer b is refilled by the next iteration's prefetch
@@ -1381,7 +1389,7 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
 
 template <int RR>
 __global__ void __launch_bounds__(RR >= 4 ? 256 : 512, 1) k_tile(LQ_TILE_PARAMS) {
-    tile_body<RR, InterpProg>(LQ_TILE_ARGS);
+    tile_body<RR, InterpProg>(LQ_TILE_ARGS);   // in place only (the planner's oop passes are JIT-only)
 }
 
 }  // namespace lq

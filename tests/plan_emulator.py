@@ -265,6 +265,10 @@ def run(plan, psi, theta=None, shift=None, gofs=0):
         free = [b for b in range(n) if not (tmask >> b) & 1]
         L = np.arange(1 << Kp, dtype=np.int64)
         dep = _deposit(L, T)
+        # relabelling out-of-place store: the pass writes a new array in the
+        # next frame (physical bit b -> spos[b])
+        oop = bool(p.get("oop", 0)) and not (p["flags"] & PF_NO_STORE)
+        out = np.empty_like(psi) if oop else psi
         for tile in range(1 << (n - Kp)):
             tb = 0
             for i, b in enumerate(free):
@@ -292,7 +296,15 @@ def run(plan, psi, theta=None, shift=None, gofs=0):
             if p["store_perm"] >= 0:
                 x = apply_perm(x, p["store_perm"])
             if not (p["flags"] & PF_NO_STORE):
-                psi[g] = x
+                if oop:
+                    gs = np.zeros_like(g)
+                    for b, sb in enumerate(p["spos"]):
+                        gs |= ((g >> b) & 1) << sb
+                    out[gs] = x
+                else:
+                    psi[g] = x
+        if oop:
+            psi[:] = out
     # wide groups (direct kernel)
     j = np.arange(psi.size, dtype=np.int64)
     for gi in plan["wide_groups"]:

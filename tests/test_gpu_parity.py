@@ -36,6 +36,7 @@ def _restore_options(lq):
     lq.lq_set_option(lq.LQ_OPT_JIT, 1)
     lq.lq_set_option(lq.LQ_OPT_FIRST_PASS_FREE, 1)
     lq.lq_set_option(lq.LQ_OPT_POISON_ALLOC, 0)
+    lq.lq_set_option(lq.LQ_OPT_RELABEL_STORES, 0)
 
 
 def grad_close(g, go):
@@ -534,6 +535,49 @@ def test_psr_zero_first_support_restriction(lq, oracle, first_free, monkeypatch)
     which = [0, n, 2 * n + 5, npar - 1]
     go = oracle.param_shift_grad(n, gates, theta, terms, which=which, threads=8)
     scale = float(np.abs(g1).max())
+    for p, v in zip(which, go):
+        assert abs(g1[p] - v) <= 1e-10 * max(abs(v), scale), (p, g1[p], v)
+    assert abs(e1 - oracle.energy(n, gates, theta, terms)) <= 1e-10 * max(abs(e1), 1)
+
+
+@pytest.mark.parametrize("relabel", [0, 3, 4, 5])
+def test_psr_relabel_stores(lq, oracle, relabel):
+    """Relabelling out-of-place stores (LQ_OPT_RELABEL_STORES):
+    each tile pass writes the state into the other buffer of a ping-pong pair,
+    in the frame where the next pass's tile is the contiguous low bits, under
+    support tracking and with poisoned (NaN) work buffers.  Energy and sampled
+    gradient components equal the oracle's; every mode agrees with the
+    in-place plan to rounding; repeated runs are bit-identical."""
+    import torch
+    n = 18
+    lq.lq_set_option(lq.LQ_OPT_POISON_ALLOC, 1)
+    lq.lq_set_option(lq.LQ_OPT_RELABEL_STORES, relabel)
+    gates = W.hea_ansatz(n, 4, "ring")
+    npar = 8 * n
+    theta = np.random.default_rng(180 + relabel).uniform(0, 2 * np.pi, npar)
+    terms = W.xyz_terms(n) + [(0.3, 0b101 << 4, 1 << 17), (-0.2, 0, (1 << 17) | 1)]
+    st = torch.cuda.current_stream()
+    th = torch.tensor(theta, device="cuda")
+
+    def run():
+        lq.lq_psr_cache_clear()
+        P = lq.lq_psr_create(n, gates, npar, terms, stream=st)
+        g = torch.zeros(npar, dtype=torch.float64, device="cuda")
+        e = torch.zeros(1, dtype=torch.float64, device="cuda")
+        lq.lq_psr_run(P, th.data_ptr(), g.data_ptr(), e.data_ptr())
+        torch.cuda.synchronize()
+        lq.lq_psr_free(P)
+        return g.cpu().numpy(), e.item()
+
+    g1, e1 = run()
+    g2, e2 = run()
+    assert np.array_equal(g1, g2) and e1 == e2
+    lq.lq_set_option(lq.LQ_OPT_RELABEL_STORES, 0)
+    g0, e0 = run()
+    scale = float(np.abs(g0).max())
+    assert np.abs(g1 - g0).max() <= 1e-12 * max(scale, 1.0) and abs(e1 - e0) <= 1e-12 * max(abs(e0), 1)
+    which = [0, 5, n + 3, 3 * n + 7, npar - 1]
+    go = oracle.param_shift_grad(n, gates, theta, terms, which=which, threads=8)
     for p, v in zip(which, go):
         assert abs(g1[p] - v) <= 1e-10 * max(abs(v), scale), (p, g1[p], v)
     assert abs(e1 - oracle.energy(n, gates, theta, terms)) <= 1e-10 * max(abs(e1), 1)

@@ -60,3 +60,40 @@ def test_emulated_expval_only(lq, oracle, n):
     psi0 = oracle.init_random(n, 9)
     _, E, plan = emulate(lq, n, [], psi0, None, terms)
     assert E == pytest.approx(oracle.expval(psi0, terms), abs=1e-10)
+
+
+@pytest.mark.parametrize("relabel", [3, 4, 5])
+@pytest.mark.parametrize("n", [12, 14])
+def test_emulated_psr_relabel_stores(lq, oracle, n, relabel):
+    """The parameter-shift planner with relabelling out-of-place stores
+    (LQ_OPT_RELABEL_STORES): every storing tile pass writes the
+    state in the next pass's frame.  The plan's energy and final state (in the
+    exported final layout) match the oracle; every pass after the first reads
+    its tile as the contiguous low bits, and every store's lowest `relabel`
+    lane bits land on the new frame's lowest bits."""
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 7 if n == 12 else 0)
+    lq.lq_set_option(lq.LQ_OPT_EXPORT_PSR, 1)
+    lq.lq_set_option(lq.LQ_OPT_RELABEL_STORES, relabel)
+    try:
+        gates = W.hea_ansatz(n, 3, "ring")
+        theta = np.random.default_rng(n).uniform(0, 2 * np.pi, 6 * n)
+        terms = W.xyz_terms(n)
+        psi0 = oracle.zeros(n)
+        got, E, plan = emulate(lq, n, gates, psi0, theta, terms)
+        assert E == pytest.approx(oracle.energy(n, gates, theta, terms), abs=1e-10)
+        tiles = [p for p in plan["passes"] if p["kind"] == EM.PASS_TILE]
+        assert all(p["oop"] for p in tiles if not (p["flags"] & EM.PF_NO_STORE))
+        K = plan["K"]
+        for a, b in zip(tiles, tiles[1:]):
+            if a["oop"]:
+                assert sorted(b["T"]) == list(range(K))       # contiguous reads
+                sm = set(a["Sstore"][:plan["Rr"]])
+                lanes = [a["T"][l] for l in range(K) if l not in sm][:relabel]
+                assert [a["spos"][x] for x in lanes] == list(range(len(lanes)))
+        # the final state, read through the exported final layout
+        ref = oracle.apply_circuit(oracle.zeros(n), gates, theta)
+        if not (tiles[-1]["flags"] & EM.PF_NO_STORE):
+            assert np.abs(got - ref).max() <= 1e-10
+    finally:
+        lq.lq_set_option(lq.LQ_OPT_EXPORT_PSR, 0)
+        lq.lq_set_option(lq.LQ_OPT_RELABEL_STORES, 0)

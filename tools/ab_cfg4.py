@@ -20,7 +20,7 @@ sys.path.insert(0, %r)
 import torch
 import workloads as W
 from paper_2512_23183_b200 import lq
-for name in ("TILE_BITS", "COALESCE_BITS", "REG_BITS", "PASS_BUDGET", "FIRST_PASS_FREE"):
+for name in ("TILE_BITS", "COALESCE_BITS", "REG_BITS", "PASS_BUDGET", "FIRST_PASS_FREE", "RELABEL_STORES"):
     if os.environ.get("AB_" + name):
         lq.lq_set_option(getattr(lq, "LQ_OPT_" + name), int(os.environ["AB_" + name]))
 w = W.config4()
