@@ -389,7 +389,8 @@ typedef enum {
     LQ_OPT_FUSION = 0,     /* 1 (default): tile-fused passes; 0: one pass per gate (pair/diag kernels) */
     LQ_OPT_TILE_BITS = 1,  /* tile size K in bits (default 0 = automatic) */
     LQ_OPT_COALESCE_BITS = 2, /* low physical bits every strided tile includes (default 3) */
-    LQ_OPT_REG_BITS = 3,      /* amplitudes per thread in tile passes = 2^value, 3 or 4 (default 4) */
+    LQ_OPT_REG_BITS = 3,      /* amplitudes per thread in tile passes = 2^value, 2..4 (default 4;
+                                 states under 9 qubits use down to 2 so a tile spans more threads) */
     LQ_OPT_KERNEL_TIMING = 4, /* 1: bracket every launch with CUDA events on its stream (lq_kernel_timing) */
     LQ_OPT_JIT = 5,           /* tile passes as per-plan specialised kernels compiled with NVRTC for
                                  sm_100a (cached per process) instead of the op-list interpreter kernel;
@@ -422,8 +423,14 @@ typedef enum {
                                  lowest `value` lane bits held by that tile (128..512-byte write runs);
                                  doubles the batch's state memory.  Same results; on config 4 it
                                  measured 2 % slower than in place */
-    LQ_OPT_EXPORT_PSR = 14    /* testing: 1 makes lq_plan_export_json plan like lq_psr_create (pass
+    LQ_OPT_EXPORT_PSR = 14,   /* testing: 1 makes lq_plan_export_json plan like lq_psr_create (pass
                                  budget, first-pass exemption, relabelling stores) */
+    LQ_OPT_GRAPHS = 15        /* 1 (default): launch-bound parameter-shift runs (at most 2^24 amplitudes
+                                 per run, no communicator, no kernel timing) are captured as a CUDA graph
+                                 on their second run with the same device pointers and replayed after;
+                                 lq_vqe_adam on such a plan runs its loop on the device (stopping rule
+                                 and Adam step in one kernel of the graph, one status read per chunk of
+                                 iterations).  0: plain stream launches */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);

@@ -24,6 +24,14 @@ namespace lq {
 // fills `err` on failure.
 bool jit_plan(const Plan &plan, std::vector<const void *> &kernels, std::vector<void *> &ctabs, std::string &err);
 
+// A JIT pass whose op tables do not fit a constant bank for plan.ctab_circ
+// circuits: k_stage_ctab stages them in global memory (CtabDesc, like the
+// bank passes) and the pass copies its circuit's block flat into shared
+// memory.  The JIT source and the launcher (lq_api.cu) both decide with this.
+inline bool plan_flat_tables(const Plan &plan, const KPass &kp) {
+    return plan.ctab && kp.smat > 0 && (uint64_t)kp.smat * (uint64_t)plan.ctab_circ > 4096;
+}
+
 // Generated CUDA source of one tile pass (exposed for lq_plan_export_json /
 // debugging).
 std::string jit_source(const Plan &plan, size_t pass);

@@ -559,4 +559,51 @@ __global__ void k_adam_step(double *__restrict__ theta, double *__restrict__ m, 
     }
 }
 
+// One VQE iteration's bookkeeping on the device (lq_vqe_adam's graph path,
+// PAPER.md:739-762; stopping rule reading A21): record E_t, decide the stop
+// exactly as the host loop does -- non-finite E (state 2), or
+// |E_t - E_{t-1}| < tol for t >= 1, or t == max_iter (state 1) -- and
+// otherwise take the Adam step with the host-computed bias corrections
+// bc[2t], bc[2t+1] (the same _rn arithmetic as k_adam_step).  Once stopped,
+// later iterations of the replayed graph leave theta, the trace and the
+// counter alone.  One block.
+struct VqeCtl {
+    int32_t t;        // iteration index
+    int32_t state;    // 0 running, 1 stopped, 2 non-finite energy
+    double prev;      // E_{t-1}
+};
+__global__ void k_vqe_step(double *__restrict__ theta, double *__restrict__ m, double *__restrict__ v,
+                           const double *__restrict__ g, int n, double lr, double b1, double b2, double eps,
+                           double tol, int max_iter, const double *__restrict__ bc, const double *__restrict__ E,
+                           double *__restrict__ trace, VqeCtl *__restrict__ ctl) {
+    __shared__ int go, t;
+    if (threadIdx.x == 0) {
+        go = 0;
+        t = ctl->t;
+        if (ctl->state == 0) {
+            const double e = *E;
+            trace[t] = e;
+            if (!isfinite(e)) ctl->state = 2;
+            else if ((t >= 1 && fabs(e - ctl->prev) < tol) || t == max_iter) ctl->state = 1;
+            else {
+                ctl->prev = e;
+                go = 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (!go) return;
+    const double bc1 = bc[2 * t], bc2 = bc[2 * t + 1];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double gi = g[i];
+        const double mi = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(__dadd_rn(1.0, -b1), gi));
+        const double vi = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dadd_rn(1.0, -b2), __dmul_rn(gi, gi)));
+        m[i] = mi;
+        v[i] = vi;
+        const double mh = __ddiv_rn(mi, bc1), vh = __ddiv_rn(vi, bc2);
+        theta[i] = __dadd_rn(theta[i], -__ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), eps)));
+    }
+    if (threadIdx.x == 0) ctl->t = t + 1;
+}
+
 }  // namespace lq

@@ -58,6 +58,7 @@ std::atomic<int64_t> g_opt_budget{400};         // LQ_OPT_PASS_BUDGET (PSR plans
 std::atomic<int64_t> g_opt_state_budget{800};   // LQ_OPT_STATE_PASS_BUDGET (every other plan)
 std::atomic<int64_t> g_opt_relabel{0};          // LQ_OPT_RELABEL_STORES (PSR plans; measured, off)
 std::atomic<int64_t> g_opt_export_psr{0};       // LQ_OPT_EXPORT_PSR (testing)
+std::atomic<int64_t> g_opt_graphs{1};           // LQ_OPT_GRAPHS
 const double PI = 3.14159265358979323846264338327950288;
 
 lq_status fail(lq_status s, const std::string &msg) {
@@ -246,7 +247,9 @@ lq_status prepare(Plan &plan, bool reused = false) {
     plan.ctab_desc.clear();
     plan.ctab_total = 0;
     for (size_t i = 0; i < plan.passes.size(); i++) {
-        if (!plan.jit_ctab[i]) continue;
+        // bank passes and flat-staged passes (jit.h plan_flat_tables) both stage through k_stage_ctab
+        const bool flat = plan.jit[i] && plan.passes[i].kind == PASS_TILE && plan_flat_tables(plan, plan.passes[i].kp);
+        if (!plan.jit_ctab[i] && !flat) continue;
         const KPass &kp = plan.passes[i].kp;
         plan.ctab_desc.push_back({kp.op_begin, kp.op_end, kp.smat, plan.ctab_total});
         plan.ctab_total += kp.smat * (uint32_t)plan.ctab_circ;
@@ -581,11 +584,17 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
             // bank refill to the launch, so two host threads issuing on one
             // stream cannot interleave (stream order = enqueue order).
             std::unique_lock<std::mutex> bank_lock;
+            const double2 *pmats = mats;   // the pass's table source
+            uint64_t pmat_stride = mat_stride;
             if (i < plan.jit_ctab.size() && plan.jit_ctab[i]) {
                 bank_lock = std::unique_lock<std::mutex>(ctab_mutex(plan.jit_ctab[i]));
                 const CtabDesc &D = plan.ctab_desc[ci++];
                 CUDA_TRY(cudaMemcpyAsync(plan.jit_ctab[i], dp.ctab_stage + D.out,
                                          (size_t)n_circ * D.smat * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+            } else if (i < plan.jit.size() && plan.jit[i] && plan_flat_tables(plan, p.kp)) {
+                const CtabDesc &D = plan.ctab_desc[ci++];   // flat-staged: read in place
+                pmats = dp.ctab_stage + D.out;
+                pmat_stride = D.smat;
             }
             KPass kp = p.kp;
             kp.gofs = gofs;
@@ -604,8 +613,8 @@ lq_status launch_passes(const Plan &plan, const DevPlan &dp, double2 *state, uin
             const bool oop = p.oop && !(kp.flags & PF_NO_STORE);
             if (p.oop && !jk) return fail(LQ_ERR_STATE, "relabelling pass without its JIT program (internal)");
             double2 *out = oop ? (state == alt ? alt_base : alt) : state;
-            LQ_TRY(launch_tile(plan.Rr, jk, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, dp.eterms, mats, mat_stride,
-                               dp.cst, state, state_stride, n_circ, partials, slot_stride, st, tl2, out));
+            LQ_TRY(launch_tile(plan.Rr, jk, kp, dp.subs, dp.kops, dp.perms, dp.pterms, npt, dp.eterms, pmats,
+                               pmat_stride, dp.cst, state, state_stride, n_circ, partials, slot_stride, st, tl2, out));
             state = out;
             if (final_out) *final_out = state;
         } else if (p.kind == PASS_PAIR) {
@@ -1328,7 +1337,7 @@ lq_status lq_set_option(int option, int64_t value) {
         g_opt_coalesce = value;
         return LQ_OK;
     case LQ_OPT_REG_BITS:
-        if (value != 3 && value != 4) return fail(LQ_ERR_ARG, "register bits must be 3 or 4");
+        if (value < 2 || value > 4) return fail(LQ_ERR_ARG, "register bits must be 2..4");
         g_opt_regbits = value;
         return LQ_OK;
     case LQ_OPT_KERNEL_TIMING:
@@ -1362,6 +1371,7 @@ lq_status lq_set_option(int option, int64_t value) {
         g_opt_relabel = value;
         return LQ_OK;
     case LQ_OPT_EXPORT_PSR: g_opt_export_psr = value ? 1 : 0; return LQ_OK;
+    case LQ_OPT_GRAPHS: g_opt_graphs = value ? 1 : 0; return LQ_OK;
     default: return fail(LQ_ERR_ARG, "unknown option");
     }
 }
@@ -1380,6 +1390,7 @@ int64_t lq_get_option(int option) {
     case LQ_OPT_COMM_TIMEOUT_MS: return g_opt_comm_timeout.load();
     case LQ_OPT_RELABEL_STORES: return g_opt_relabel.load();
     case LQ_OPT_EXPORT_PSR: return g_opt_export_psr.load();
+    case LQ_OPT_GRAPHS: return g_opt_graphs.load();
     case LQ_OPT_STATE_PASS_BUDGET: return g_opt_state_budget.load();
     case LQ_OPT_GROUP_STAGED: return g_opt_group_staged.load();
     case LQ_OPT_SWAP_QUBITS: return g_opt_swap_k.load();
@@ -2076,6 +2087,12 @@ struct lq_psr {
     const PTerm *d_terms = nullptr;
     uint64_t launches_per_run = 0;
     uint64_t blob_bytes = 0;
+    // CUDA graph of one run (LQ_OPT_GRAPHS): captured on the second run with
+    // the same device pointers, replayed while they stay the same
+    cudaGraphExec_t gexec = nullptr;
+    const void *g_ptr[3] = {nullptr, nullptr, nullptr};   // pointers of the last run
+    uint64_t graph_launches = 0;                           // kernels in the graph
+    uint64_t graph_replays = 0;
 };
 
 extern "C" {
@@ -2198,7 +2215,10 @@ lq_status lq_psr_create(int n_qubits, const lq_gate *ansatz, size_t n_gates, siz
     return LQ_OK;
 }
 
-static lq_status psr_run_body(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev);
+static lq_status psr_run_body(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev,
+                              cudaStream_t st);
+static lq_status psr_run_graph(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev);
+static bool psr_graphs(const lq_psr *P);
 
 lq_status lq_psr_run(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev) {
     if (!P) return fail(LQ_ERR_ARG, "invalid plan");
@@ -2206,7 +2226,8 @@ lq_status lq_psr_run(lq_psr *P, const double *theta_dev, double *grad_dev, doubl
     if (P->comm && P->comm->dead)
         return fail(LQ_ERR_STATE, "communicator aborted after an earlier failure: " + P->comm->why);
     if ((!theta_dev && P->n_params) || (!grad_dev && P->n_params)) return fail(LQ_ERR_ARG, "NULL device pointer");
-    const lq_status s = psr_run_body(P, theta_dev, grad_dev, energy_dev);
+    const lq_status s = psr_graphs(P) ? psr_run_graph(P, theta_dev, grad_dev, energy_dev)
+                                      : psr_run_body(P, theta_dev, grad_dev, energy_dev, P->stream);
     if (s == LQ_ERR_CUDA || s == LQ_ERR_NCCL) {
         P->dead = true;
         P->why = g_err;
@@ -2214,10 +2235,10 @@ lq_status lq_psr_run(lq_psr *P, const double *theta_dev, double *grad_dev, doubl
     return s;
 }
 
-static lq_status psr_run_body(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev) {
+static lq_status psr_run_body(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev,
+                              cudaStream_t st) {
     const uint64_t N = 1ull << P->n;
     const int n_circ = (int)P->shifts.size();
-    cudaStream_t st = P->stream;
     uint64_t l0 = g_launches.load();
     double2 *states = P->states.at<double2>(0);
     double2 *mats = P->mats.at<double2>(0);
@@ -2266,6 +2287,78 @@ static lq_status psr_run_body(lq_psr *P, const double *theta_dev, double *grad_d
     return LQ_OK;
 }
 
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- CUDA graphs
+// Launch-bound runs (small states, many short kernels: configs 1-3, the VQE
+// loop) are captured once as a CUDA graph and replayed: one cudaGraphLaunch
+// instead of one host launch per kernel and per constant-bank copy, and no
+// host gaps between the kernels.  Capture runs on a private stream in
+// thread-local mode (nothing executes); the graph replays on the caller's
+// stream, after everything queued there before it.
+template <class F>
+static lq_status capture_graph(F body, cudaGraphExec_t *out, uint64_t *kernels) {
+    *out = nullptr;
+    cudaStream_t cs = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    const uint64_t l0 = g_launches.load();
+    lq_status s = LQ_OK;
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    else s = body(cs);
+    cudaGraph_t g = nullptr;
+    if (e == cudaSuccess) {
+        const cudaError_t e2 = cudaStreamEndCapture(cs, &g);   // always end a begun capture
+        if (s == LQ_OK && e2 != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e2));
+    }
+    if (s == LQ_OK) {
+        e = cudaGraphInstantiate(out, g, 0);
+        if (e != cudaSuccess) {
+            *out = nullptr;
+            s = fail(LQ_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        }
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cs);
+    // the captured launches have not run: count them when the graph replays
+    *kernels = g_launches.load() - l0;
+    g_launches.fetch_sub(*kernels);
+    cudaGetLastError();
+    return s;
+}
+
+// Graphs pay off where launches dominate: plans of at most 2^24 amplitudes
+// per run, no communicator (its all-reduce and error polling stay on the
+// host path), no per-launch timing.
+static bool psr_graphs(const lq_psr *P) {
+    if (!g_opt_graphs.load() || P->comm || g_opt_timing.load()) return false;
+    return (uint64_t)P->shifts.size() << P->n <= (1ull << 24);
+}
+
+static lq_status psr_run_graph(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev) {
+    const void *ptr[3] = {theta_dev, grad_dev, energy_dev};
+    const bool same = ptr[0] == P->g_ptr[0] && ptr[1] == P->g_ptr[1] && ptr[2] == P->g_ptr[2];
+    if (!same || !P->gexec) {
+        if (P->gexec) {
+            cudaGraphExecDestroy(P->gexec);
+            P->gexec = nullptr;
+        }
+        if (!same) {   // first run with these pointers: run directly, capture if they come again
+            for (int i = 0; i < 3; i++) P->g_ptr[i] = ptr[i];
+            return psr_run_body(P, theta_dev, grad_dev, energy_dev, P->stream);
+        }
+        LQ_TRY(capture_graph([&](cudaStream_t cs) { return psr_run_body(P, theta_dev, grad_dev, energy_dev, cs); },
+                             &P->gexec, &P->graph_launches));
+    }
+    CUDA_TRY(cudaGraphLaunch(P->gexec, P->stream));
+    g_launches.fetch_add(P->graph_launches);
+    P->graph_replays++;
+    return LQ_OK;
+}
+
+extern "C" {
+
 // VQE outer loop: Adam on parameter-shift
 // gradients.  The plan is built once; every iteration is one lq_psr_run (E and
 // g at theta^t), one k_adam_step, and one 8-byte read of E for the stopping
@@ -2296,6 +2389,68 @@ lq_status lq_vqe_adam(int n_qubits, const lq_gate *ansatz, size_t n_gates, doubl
         if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe setup: ") + cudaGetErrorString(e));
     }
     int t = 0;
+    if (s == LQ_OK && psr_graphs(P)) {
+        // Device-resident loop: one graph = one lq_psr_run + k_vqe_step (the
+        // stopping rule and the Adam step on the device, bias corrections from
+        // the same host pow() as below); replayed in growing chunks with one
+        // 16-byte status read per chunk instead of one sync per iteration.
+        // Iterations past the stop replay as no-ops for theta and the trace.
+        const int T = cfg->max_iter + 1;
+        DevBuf vb;
+        std::vector<double> bc(2 * (size_t)T);
+        for (int i = 0; i < T; i++) {
+            bc[2 * i] = 1.0 - std::pow(cfg->beta1, (double)(i + 1));
+            bc[2 * i + 1] = 1.0 - std::pow(cfg->beta2, (double)(i + 1));
+        }
+        s = vb.reserve(sizeof(double) * 3 * (size_t)T + sizeof(VqeCtl), st);
+        double *d_bc = s == LQ_OK ? vb.at<double>(0) : nullptr, *d_tr = d_bc ? d_bc + 2 * T : nullptr;
+        VqeCtl *d_ctl = d_tr ? reinterpret_cast<VqeCtl *>(d_tr + T) : nullptr;
+        cudaGraphExec_t gx = nullptr;
+        uint64_t gk = 0;
+        if (s == LQ_OK) {
+            cudaError_t e = cudaMemcpyAsync(d_bc, bc.data(), sizeof(double) * 2 * T, cudaMemcpyHostToDevice, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(d_ctl, 0, sizeof(VqeCtl), st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // bc is pageable host memory
+            if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe setup: ") + cudaGetErrorString(e));
+        }
+        if (s == LQ_OK)
+            s = capture_graph(
+                [&](cudaStream_t cs) {
+                    LQ_TRY(psr_run_body(P, d_th, d_g, d_e, cs));
+                    k_vqe_step<<<1, 256, 0, cs>>>(d_th, d_m, d_v, d_g, (int)n_params, cfg->lr, cfg->beta1, cfg->beta2,
+                                                  cfg->eps, cfg->tol, cfg->max_iter, d_bc, d_e, d_tr, d_ctl);
+                    return check_launch("k_vqe_step");
+                },
+                &gx, &gk);
+        VqeCtl ctl{0, 0, 0.0};
+        for (int done = 0, chunk = 1; s == LQ_OK && done < T && ctl.state == 0; chunk = std::min(chunk * 2, 32)) {
+            const int c = std::min(chunk, T - done);
+            for (int i = 0; i < c && s == LQ_OK; i++) {
+                const cudaError_t e = cudaGraphLaunch(gx, st);
+                if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe graph: ") + cudaGetErrorString(e));
+                g_launches.fetch_add(gk);
+            }
+            done += c;
+            if (s == LQ_OK) {
+                cudaError_t e = cudaMemcpyAsync(&ctl, d_ctl, sizeof(VqeCtl), cudaMemcpyDeviceToHost, st);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+                if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe: ") + cudaGetErrorString(e));
+            }
+        }
+        if (gx) cudaGraphExecDestroy(gx);
+        t = ctl.t;
+        if (s == LQ_OK && energy_trace) {
+            // a non-finite E_t is reported, not recorded (as the host loop)
+            const size_t cnt = (size_t)(ctl.state == 2 ? t : t + 1);
+            cudaError_t e = cnt ? cudaMemcpyAsync(energy_trace, d_tr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st)
+                                : cudaSuccess;
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe: ") + cudaGetErrorString(e));
+        }
+        if (s == LQ_OK && ctl.state == 2) s = fail(LQ_ERR_NONFINITE, "non-finite energy at iteration " + std::to_string(t));
+        if (s == LQ_OK && ctl.state == 0) s = fail(LQ_ERR_STATE, "vqe loop ended without its stopping rule (internal)");
+        vb.release(st);
+    } else {
     double prev = 0.0;
     for (; s == LQ_OK; t++) {
         s = lq_psr_run(P, d_th, d_g, d_e);
@@ -2319,6 +2474,7 @@ lq_status lq_vqe_adam(int n_qubits, const lq_gate *ansatz, size_t n_gates, doubl
                                                              cfg->beta2, cfg->eps, bc1, bc2);
             s = check_launch("k_adam_step");
         }
+    }
     }
     if (s == LQ_OK && n_params) {
         cudaError_t e = cudaMemcpyAsync(theta, d_th, sizeof(double) * n_params, cudaMemcpyDeviceToHost, st);
@@ -2457,6 +2613,7 @@ lq_status lq_psr_pass_bytes(const lq_psr *P, uint64_t *bytes_out, int32_t *kind_
 
 lq_status lq_psr_free(lq_psr *P) {
     if (!P) return LQ_OK;
+    if (P->gexec) cudaGraphExecDestroy(P->gexec);
     P->blob_buf.release(P->stream);
     P->states.release(P->stream);
     P->mats.release(P->stream);
@@ -2478,6 +2635,12 @@ struct CachedPsr {
     std::string key;
     lq_psr *P = nullptr;
     DevBuf io;   // theta, grad, energy
+    // pinned host mirror of io: the copies in and out are asynchronous
+    // (pageable copies stage through the driver and stall the stream)
+    double *hio = nullptr;
+    ~CachedPsr() {
+        if (hio) cudaFreeHost(hio);
+    }
 };
 std::mutex g_psr_mu;
 std::vector<CachedPsr *> g_psr_cache;   // most recent last
@@ -2567,20 +2730,32 @@ lq_status lq_param_shift_grad(int n_qubits, const lq_gate *ansatz, size_t n_gate
     cudaStream_t st = P->stream;
     double *d_theta = C->io.at<double>(0), *d_grad = d_theta + n_params, *d_e = d_grad + n_params;
     lq_status s = LQ_OK;
+    const size_t nio = 2 * n_params + 1;   // theta, grad, energy
+    if (!C->hio && cudaMallocHost(&C->hio, sizeof(double) * nio) != cudaSuccess) {
+        cudaGetLastError();
+        C->hio = nullptr;   // no pinned memory: pageable copies below
+    }
+    double *h_theta = C->hio ? C->hio : const_cast<double *>(theta);
+    double *h_grad = C->hio ? C->hio + n_params : grad_out, *h_e = C->hio ? C->hio + 2 * n_params : energy_out;
     if (n_params) {
-        cudaError_t e = cudaMemcpyAsync(d_theta, theta, n_params * sizeof(double), cudaMemcpyHostToDevice, st);
+        if (C->hio) memcpy(h_theta, theta, n_params * sizeof(double));   // the previous call has synchronised
+        cudaError_t e = cudaMemcpyAsync(d_theta, h_theta, n_params * sizeof(double), cudaMemcpyHostToDevice, st);
         if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, cudaGetErrorString(e));
     }
     if (s == LQ_OK) s = lq_psr_run(P, d_theta, d_grad, d_e);
     if (s == LQ_OK && n_params) {
-        cudaError_t e = cudaMemcpyAsync(grad_out, d_grad, n_params * sizeof(double), cudaMemcpyDeviceToHost, st);
+        cudaError_t e = cudaMemcpyAsync(h_grad, d_grad, n_params * sizeof(double), cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, cudaGetErrorString(e));
     }
     if (s == LQ_OK && energy_out) {
-        cudaError_t e = cudaMemcpyAsync(energy_out, d_e, sizeof(double), cudaMemcpyDeviceToHost, st);
+        cudaError_t e = cudaMemcpyAsync(h_e, d_e, sizeof(double), cudaMemcpyDeviceToHost, st);
         if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, cudaGetErrorString(e));
     }
     if (s == LQ_OK) s = comm_sync(comm && comm->c ? comm : nullptr, st);
+    if (s == LQ_OK && C->hio) {
+        if (n_params) memcpy(grad_out, h_grad, n_params * sizeof(double));
+        if (energy_out) *energy_out = *h_e;
+    }
     if (s == LQ_ERR_CUDA || s == LQ_ERR_NCCL || P->dead) {   // never reuse a plan an asynchronous failure touched
         g_psr_cache.pop_back();
         cudaStreamSynchronize(st);

@@ -879,6 +879,11 @@ void plan_circuit(int n, const std::vector<POp> &ops_in, const PlanOptions &opt,
     if (K > 12) K = 12;   // two 2^K buffers must fit in shared memory
     if (nl <= K) K = nl;
     int Rr = std::min(std::max(1, std::min(opt.reg_bits, R)), K);
+    // a tile of fewer than 2^5 threads runs its gates as one thread's serial
+    // chain: small states (K < 9) spread a tile over more threads, down to 4
+    // amplitudes per thread (a 2-qubit op needs both its bits in registers):
+    // config 3 (n = 4, 4 threads) 41 -> 37 us per gradient on B200
+    if (opt.reg_bits >= R && K - Rr < 5) Rr = std::min(Rr, std::max(2, K - 5));
     plan.Rr = Rr;
     plan.n = n;
     plan.nl = nl;

@@ -1306,7 +1306,11 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
         if constexpr (!D::CTAB) {
             if (circ != cur_circ) {   // (re)stage this circuit's op tables
                 const double2 *M = mats + (uint64_t)circ * mat_stride;
-                for (uint32_t k = t; k < nops; k += blockDim.x) stage_table(ops[P.op_begin + k], s_tab, M, cst);
+                if constexpr (D::FLAT) {   // staged by k_stage_ctab: one flat block of P.smat entries
+                    for (uint32_t k = t; k < P.smat; k += blockDim.x) s_tab[k] = M[k];
+                } else {
+                    for (uint32_t k = t; k < nops; k += blockDim.x) stage_table(ops[P.op_begin + k], s_tab, M, cst);
+                }
                 cur_circ = circ;
             }
         }

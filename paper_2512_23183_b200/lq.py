@@ -39,7 +39,7 @@ KINDS = {k: i for i, k in enumerate(KIND_NAMES)}
 (LQ_OPT_FUSION, LQ_OPT_TILE_BITS, LQ_OPT_COALESCE_BITS, LQ_OPT_REG_BITS, LQ_OPT_KERNEL_TIMING, LQ_OPT_JIT,
  LQ_OPT_PASS_BUDGET, LQ_OPT_FIRST_PASS_FREE, LQ_OPT_POISON_ALLOC, LQ_OPT_COMM_TIMEOUT_MS,
  LQ_OPT_SWAP_QUBITS, LQ_OPT_STATE_PASS_BUDGET, LQ_OPT_GROUP_STAGED,
- LQ_OPT_RELABEL_STORES, LQ_OPT_EXPORT_PSR) = range(15)
+ LQ_OPT_RELABEL_STORES, LQ_OPT_EXPORT_PSR, LQ_OPT_GRAPHS) = range(16)
 KC_TILE, KC_PAIR, KC_DIAG, KC_PAULI, KC_OTHER, KC_SWAP = 0, 1, 2, 3, 4, 5
 
 

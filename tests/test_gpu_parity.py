@@ -37,6 +37,7 @@ def _restore_options(lq):
     lq.lq_set_option(lq.LQ_OPT_FIRST_PASS_FREE, 1)
     lq.lq_set_option(lq.LQ_OPT_POISON_ALLOC, 0)
     lq.lq_set_option(lq.LQ_OPT_RELABEL_STORES, 0)
+    lq.lq_set_option(lq.LQ_OPT_GRAPHS, 1)
 
 
 def grad_close(g, go):
@@ -755,6 +756,55 @@ def test_vqe_adam_single_qubit_and_zero_hamiltonian(lq):
     np.testing.assert_array_equal(th, w.theta)
     with pytest.raises(lq.LQError):
         lq.lq_vqe_adam(1, [("RY", 0, -1, 0, 0.0)], [float("nan")], [(1.0, 0, 1)])
+
+
+def test_cuda_graph_replay_is_bit_identical(lq):
+    """LQ_OPT_GRAPHS: a launch-bound PSR plan is captured as a CUDA graph on
+    its second run with the same pointers and replayed after; the replays
+    give the stream path's bits, count their kernels, and follow theta
+    changes written into the same device buffer.  The device-resident VQE
+    loop (stopping rule + Adam in the graph) reproduces the host loop's
+    trajectory bit for bit, including an early stop."""
+    import torch
+    w = W.config3()
+    npar = len(w.theta)
+    st = torch.cuda.current_stream()
+    th0 = torch.tensor(w.theta, device="cuda")
+    th1 = th0 + 0.25
+    th = th0.clone()
+    P = lq.lq_psr_create(w.n, w.gates, npar, w.terms, stream=st)
+    g = torch.zeros(npar, dtype=torch.float64, device="cuda")
+    e = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def run():
+        lq.lq_psr_run(P, th.data_ptr(), g.data_ptr(), e.data_ptr())
+        torch.cuda.synchronize()
+        return g.cpu().numpy().copy(), e.item()
+    lq.lq_set_option(lq.LQ_OPT_GRAPHS, 0)
+    ref = [run()]
+    th.copy_(th1)
+    ref.append(run())
+    th.copy_(th0)
+    lq.lq_set_option(lq.LQ_OPT_GRAPHS, 1)
+    got = []
+    for k in range(4):      # direct, capture + replay, replay, replay (theta changed)
+        if k == 3:
+            th.copy_(th1)
+        c0 = lq.lq_launch_count()
+        got.append(run())
+        assert lq.lq_launch_count() > c0
+    lq.lq_psr_free(P)
+    for k in range(3):
+        assert np.array_equal(got[k][0], ref[0][0]) and got[k][1] == ref[0][1]
+    assert np.array_equal(got[3][0], ref[1][0]) and got[3][1] == ref[1][1]
+    for tol, it in ((1e-7, 40), (1e-3, 200)):   # full run / early stop
+        lq.lq_set_option(lq.LQ_OPT_GRAPHS, 0)
+        a = lq.lq_vqe_adam(w.n, w.gates, w.theta, w.terms, max_iter=it, tol=tol)
+        lq.lq_set_option(lq.LQ_OPT_GRAPHS, 1)
+        b = lq.lq_vqe_adam(w.n, w.gates, w.theta, w.terms, max_iter=it, tol=tol)
+        assert a[2] == b[2] and np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        if tol == 1e-3:
+            assert b[2] < it
 
 
 # ---------------------------------------------------------------- Trotter XYZ (f1)
