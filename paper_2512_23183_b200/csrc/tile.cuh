@@ -898,6 +898,32 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// Bulk (TMA) copies of whole contiguous tiles (JIT Desc::BULK): one thread
+// arms the buffer's mbarrier with the tile's byte count and issues one
+// cp.async.bulk; the others wait on the barrier's phase.  Frees the LSU of
+// 2^K per-thread LDGSTS per tile (the 12-bit contiguous QFT pass).
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    // order this CTA's earlier generic-proxy accesses of dst before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done)
+                     : "r"(smem_addr(bar)), "r"(parity)
+                     : "memory");
+}
+
 // Persistent tile kernel.  One CTA per SM walks the
 // tiles of all circuits of the launch (tile g = circuit * tiles_per_circ +
 // tile).  While it computes tile i out of shared buffer i&1 it streams tile
@@ -1266,7 +1292,24 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
     const uint64_t dep_t = D::dep(t);
     const uint32_t sw_t = D::swz(t);
     const uint32_t tmask = (1u << tiles_log2) - 1u;
+    // BULK: a contiguous tile (bits 0..K-1) filled in the identity layout is
+    // one 2^K * 16-byte block of HBM -- one TMA bulk copy per tile
+    __shared__ __align__(8) uint64_t s_bar[2];
+    if constexpr (D::BULK) {
+        if (t == 0) {
+            mbar_init(&s_bar[0], 1);
+            mbar_init(&s_bar[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+    }
     auto issue = [&](uint32_t g, double2 *buf) {
+        if constexpr (D::BULK) {
+            if (t == 0)
+                bulk_load(buf, state + (uint64_t)(g >> tiles_log2) * state_stride + D::tbase(g & tmask), TS * 16u,
+                          &s_bar[buf == sm ? 0 : 1]);
+            return;
+        }
         const uint64_t tbg = D::tbase(g & tmask);
         const double2 *psi = state + (uint64_t)(g >> tiles_log2) * state_stride + tbg + dep_t;
         // UMASK (zero-first plans, lq_api.cu prepare()): the state is zero at
@@ -1314,8 +1357,13 @@ __device__ __forceinline__ void tile_body_static(const KPass &P, const KOp *__re
                 cur_circ = circ;
             }
         }
-        if constexpr (LATE) cp_async_wait0();
-        else cp_async_wait1();
+        if constexpr (D::BULK) {
+            if (!zero) mbar_wait(&s_bar[i & 1], (i >> 1) & 1u);   // fill i>>1 of buffer i&1
+        } else if constexpr (LATE) {
+            cp_async_wait0();
+        } else {
+            cp_async_wait1();
+        }
         __syncthreads();
         if constexpr (LATE) {
             if (gn < total_tiles && !zero) issue(gn, sm + ((i + 1) & 1) * TS);
