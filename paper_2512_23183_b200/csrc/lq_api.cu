@@ -2333,7 +2333,8 @@ static lq_status capture_graph(F body, cudaGraphExec_t *out, uint64_t *kernels) 
 // host path), no per-launch timing.
 static bool psr_graphs(const lq_psr *P) {
     if (!g_opt_graphs.load() || P->comm || g_opt_timing.load()) return false;
-    return (uint64_t)P->shifts.size() << P->n <= (1ull << 24);
+    static const bool any = getenv("LQ_GRAPH_ANY") != nullptr;   // A/B experiments: every plan size
+    return any || (uint64_t)P->shifts.size() << P->n <= (1ull << 24);
 }
 
 static lq_status psr_run_graph(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev) {
