@@ -425,12 +425,12 @@ typedef enum {
                                  measured 2 % slower than in place */
     LQ_OPT_EXPORT_PSR = 14,   /* testing: 1 makes lq_plan_export_json plan like lq_psr_create (pass
                                  budget, first-pass exemption, relabelling stores) */
-    LQ_OPT_GRAPHS = 15        /* 1 (default): launch-bound parameter-shift runs (at most 2^24 amplitudes
-                                 per run, no communicator, no kernel timing) are captured as a CUDA graph
-                                 on their second run with the same device pointers and replayed after;
-                                 lq_vqe_adam on such a plan runs its loop on the device (stopping rule
-                                 and Adam step in one kernel of the graph, one status read per chunk of
-                                 iterations).  0: plain stream launches */
+    LQ_OPT_GRAPHS = 15        /* 1 (default): parameter-shift runs (no communicator, no kernel timing)
+                                 are captured as a CUDA graph on their second run with the same device
+                                 pointers and replayed after; lq_vqe_adam runs its loop on the device
+                                 (stopping rule and Adam step in one kernel of the graph; runs of at most
+                                 2^24 amplitudes read the status once per chunk of up to 32 iterations,
+                                 larger ones after every iteration).  0: plain stream launches */
 } lq_option;
 lq_status lq_set_option(int option, int64_t value);
 int64_t lq_get_option(int option);

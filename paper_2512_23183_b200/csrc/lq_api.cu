@@ -2328,14 +2328,17 @@ static lq_status capture_graph(F body, cudaGraphExec_t *out, uint64_t *kernels) 
     return s;
 }
 
-// Graphs pay off where launches dominate: plans of at most 2^24 amplitudes
-// per run, no communicator (its all-reduce and error polling stay on the
-// host path), no per-launch timing.
+// Graphs pay off most where launches dominate (config 3: 47 -> 37 us per
+// gradient), and still trim the launch gaps of a config-4 gradient (6748
+// tile launches: 2.600 -> 2.578 s, same box).  Not with a communicator (its
+// all-reduce and error polling stay on the host path) or per-launch timing.
 static bool psr_graphs(const lq_psr *P) {
-    if (!g_opt_graphs.load() || P->comm || g_opt_timing.load()) return false;
-    static const bool any = getenv("LQ_GRAPH_ANY") != nullptr;   // A/B experiments: every plan size
-    return any || (uint64_t)P->shifts.size() << P->n <= (1ull << 24);
+    return g_opt_graphs.load() && !P->comm && !g_opt_timing.load();
 }
+// runs short enough that the device VQE loop may replay iterations past the
+// stop (at most 2^24 amplitudes per run; a config-4 run, 2.6 s, reads the
+// status after every iteration instead)
+static bool psr_small(const lq_psr *P) { return (uint64_t)P->shifts.size() << P->n <= (1ull << 24); }
 
 static lq_status psr_run_graph(lq_psr *P, const double *theta_dev, double *grad_dev, double *energy_dev) {
     const void *ptr[3] = {theta_dev, grad_dev, energy_dev};
@@ -2424,7 +2427,8 @@ lq_status lq_vqe_adam(int n_qubits, const lq_gate *ansatz, size_t n_gates, doubl
                 },
                 &gx, &gk);
         VqeCtl ctl{0, 0, 0.0};
-        for (int done = 0, chunk = 1; s == LQ_OK && done < T && ctl.state == 0; chunk = std::min(chunk * 2, 32)) {
+        const int max_chunk = psr_small(P) ? 32 : 1;
+        for (int done = 0, chunk = 1; s == LQ_OK && done < T && ctl.state == 0; chunk = std::min(chunk * 2, max_chunk)) {
             const int c = std::min(chunk, T - done);
             for (int i = 0; i < c && s == LQ_OK; i++) {
                 const cudaError_t e = cudaGraphLaunch(gx, st);
