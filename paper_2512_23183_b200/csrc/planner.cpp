@@ -880,10 +880,15 @@ void plan_circuit(int n, const std::vector<POp> &ops_in, const PlanOptions &opt,
     if (nl <= K) K = nl;
     int Rr = std::min(std::max(1, std::min(opt.reg_bits, R)), K);
     // a tile of fewer than 2^5 threads runs its gates as one thread's serial
-    // chain: small states (K < 9) spread a tile over more threads, down to 4
-    // amplitudes per thread (a 2-qubit op needs both its bits in registers):
-    // config 3 (n = 4, 4 threads) 41 -> 37 us per gradient on B200
-    if (opt.reg_bits >= R && K - Rr < 5) Rr = std::min(Rr, std::max(2, K - 5));
+    // chain, and a state that is one tile runs on one CTA: such plans spread
+    // the tile over more threads, down to 4 amplitudes per thread (a 2-qubit
+    // op needs both its bits in registers) -- config 3 (n = 4, 4 threads)
+    // 41 -> 37 us per gradient, config 1 (n = 10, 256 threads) 156 -> 124 us
+    // per run on B200 (tools/cfg3_rb.py, tools/cfg1_variants.py)
+    if (opt.reg_bits >= R) {
+        if (nl <= K) Rr = std::min(Rr, std::max(2, K - 8));
+        else if (K - Rr < 5) Rr = std::min(Rr, std::max(2, K - 5));
+    }
     plan.Rr = Rr;
     plan.n = n;
     plan.nl = nl;
