@@ -59,6 +59,8 @@ std::atomic<int64_t> g_opt_state_budget{800};   // LQ_OPT_STATE_PASS_BUDGET (eve
 std::atomic<int64_t> g_opt_relabel{0};          // LQ_OPT_RELABEL_STORES (PSR plans; measured, off)
 std::atomic<int64_t> g_opt_export_psr{0};       // LQ_OPT_EXPORT_PSR (testing)
 std::atomic<int64_t> g_opt_graphs{1};           // LQ_OPT_GRAPHS
+std::atomic<uint64_t> g_plan_uid{1};            // Plan::uid of cached plans
+uint64_t next_plan_uid() { return g_plan_uid.fetch_add(1); }
 const double PI = 3.14159265358979323846264338327950288;
 
 lq_status fail(lq_status s, const std::string &msg) {
@@ -282,6 +284,7 @@ lq_status promote(CachedPlan &cp) {
     cp.plan.prepared = false;
     lq_status s = prepare(cp.plan, true);
     cp.plan.prepared = true;
+    cp.plan.uid = next_plan_uid();   // its tables changed (constant-bank descriptors)
     return s;
 }
 struct PlanCache {
@@ -380,6 +383,7 @@ struct Blob {
         return LQ_OK;
     }
 };
+
 
 bool is_rotation(int k) {
     return k == LQ_RX || k == LQ_RY || k == LQ_RZ || k == LQ_CP || k == LQ_CRY || k == LQ_RXX || k == LQ_RYY ||
@@ -728,6 +732,8 @@ struct lq_sv {
     cudaStream_t stream = nullptr;
     int32_t qmap[64];
     DevBuf plan_buf, work_buf;
+    uint64_t blob_uid = 0;           // Plan::uid whose tables plan_buf holds (0: none / per-call data)
+    size_t blob_bytes = 0;
     // ---- sharded states (dist.h): m > 0
     int m = 0, nl = 0;               // log2 G; local index bits
     lq_comm *comm = nullptr;         // NCCL mode: one shard per process
@@ -770,6 +776,18 @@ lq_status seal(lq_sv *sv, lq_status s) {
 }
 
 // Run a circuit-level plan on one state (apply_circuit / canonicalize / qft).
+// A cached plan's tables (uid != 0, no per-call data) stay in the state's
+// plan buffer between calls: a repeated call (config 2's QFTs, a VQE or
+// Trotter loop on one state) skips the host -> device copy of its blob.
+lq_status upload_tables(lq_sv *sv, const Blob &blob, uint64_t uid) {
+    if (uid && sv->blob_uid == uid && sv->blob_bytes == blob.h.size() && sv->plan_buf.p) return LQ_OK;
+    sv->blob_uid = 0;
+    LQ_TRY(const_cast<Blob &>(blob).upload(sv->plan_buf, sv->stream));
+    sv->blob_uid = uid;
+    sv->blob_bytes = blob.h.size();
+    return LQ_OK;
+}
+
 lq_status run_single(lq_sv *sv, Plan &plan, const MatBuilder &mb, const double *theta, size_t n_theta) {
     if (plan.passes.empty()) return LQ_OK;
     if (!plan.prepared) plan.stream_tag = (uint64_t)(uintptr_t)sv->stream;
@@ -780,7 +798,7 @@ lq_status run_single(lq_sv *sv, Plan &plan, const MatBuilder &mb, const double *
            o_pt = blob.add(plan.perm_terms);
     size_t o_th = blob.add(theta, theta ? n_theta * sizeof(double) : 0);
     size_t o_cd = blob.add(plan.ctab_desc);
-    LQ_TRY(blob.upload(sv->plan_buf, sv->stream));
+    LQ_TRY(upload_tables(sv, blob, theta ? 0 : plan.uid));
     DevPlan dp;
     if (plan.ctab_total) {
         LQ_TRY(sv->ctab_buf.reserve((size_t)plan.ctab_total * sizeof(double2), sv->stream));
@@ -1157,6 +1175,7 @@ lq_status sh_run(lq_sv *sv, const Schedule &sc, const double *theta, size_t n_th
     size_t o_spec = blob.add(sc.mb.specs), o_fac = blob.add(sc.mb.factors), o_cst = blob.add(sc.mb.cst);
     size_t o_th = blob.add(theta, theta ? n_theta * sizeof(double) : 0);
     LQ_TRY(blob.upload(sv->plan_buf, st));
+    sv->blob_uid = 0;
     double2 *mats = nullptr;
     if (sc.mb.mat_size) {
         LQ_TRY(sv->mats_buf.reserve((size_t)sc.mb.mat_size * sizeof(double2), st));
@@ -1597,6 +1616,7 @@ lq_status lq_dist_schedule_json(int n_qubits, int log2_world, const lq_gate *gat
 lq_status lq_sv_free(lq_sv *sv) {
     if (!sv) return LQ_OK;
     sv->plan_buf.release(sv->stream);
+    sv->blob_uid = 0;
     sv->work_buf.release(sv->stream);
     sv->mats_buf.release(sv->stream);
     sv->part_buf.release(sv->stream);
@@ -1849,6 +1869,7 @@ lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const doub
         cp->plan.stream_tag = (uint64_t)(uintptr_t)sv->stream;
         if (!cp->plan.passes.empty()) LQ_TRY(prepare(cp->plan));
         cp->plan.prepared = true;
+        cp->plan.uid = next_plan_uid();
         g_plan_cache.put(key, cp);
     }
     LQ_TRY(promote(*cp));
@@ -1892,6 +1913,7 @@ static lq_status qft_body(lq_sv *sv, int inverse) {
         cp->plan.stream_tag = (uint64_t)(uintptr_t)sv->stream;
         LQ_TRY(prepare(cp->plan));
         cp->plan.prepared = true;
+        cp->plan.uid = next_plan_uid();
         g_plan_cache.put(key, cp);
     }
     LQ_TRY(promote(*cp));
@@ -1924,6 +1946,7 @@ static lq_status expval_pauli_sum_body(lq_sv *sv, const lq_pauli_term *terms, si
         cp->plan.stream_tag = (uint64_t)(uintptr_t)sv->stream;
         LQ_TRY(prepare(cp->plan));
         cp->plan.prepared = true;
+        cp->plan.uid = next_plan_uid();
         g_plan_cache.put(key, cp);
     }
     LQ_TRY(promote(*cp));
@@ -1934,7 +1957,7 @@ static lq_status expval_pauli_sum_body(lq_sv *sv, const lq_pauli_term *terms, si
     size_t o_sub = blob.add(plan.subs), o_kop = blob.add(plan.kops), o_perm = blob.add(plan.perms),
            o_pt = blob.add(plan.perm_terms), o_et = blob.add(plan.eterms), o_dt = blob.add(dset.terms),
            o_cd = blob.add(plan.ctab_desc);
-    LQ_TRY(blob.upload(sv->plan_buf, sv->stream));
+    LQ_TRY(upload_tables(sv, blob, plan.uid));
     DevPlan dp;
     if (plan.ctab_total) {
         LQ_TRY(sv->ctab_buf.reserve((size_t)plan.ctab_total * sizeof(double2), sv->stream));

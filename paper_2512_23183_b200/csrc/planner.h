@@ -102,6 +102,8 @@ struct Plan {
     std::vector<void *> jit_ctab;     // per pass: device address of its lqj_ctab, or nullptr (smem tables)
     std::vector<CtabDesc> ctab_desc;  // the passes with jit_ctab, in pass order (staging layout)
     uint32_t ctab_total = 0;          // staging buffer size (double2) for ctab_circ circuits
+    uint64_t uid = 0;                 // nonzero: identity of a cached plan's device tables (lq_api.cu
+                                      // re-uploads them to a state only when it changes)
     bool has_oop = false;             // some pass stores out of place (the state needs a ping-pong buffer)
     uint8_t frame[64];                // frame[b]: physical bit, after the plan, of the plan's input bit b
     uint64_t stream_tag = 0;          // the stream the plan runs on: constant banks are per module, so
