@@ -10,6 +10,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <thread>
@@ -143,6 +144,37 @@ lq_status check_launch(const char *what) {
     return LQ_OK;
 }
 
+template <class F>
+static lq_status capture_graph(F body, cudaGraphExec_t *out, uint64_t *kernels) {
+    *out = nullptr;
+    cudaStream_t cs = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    const uint64_t l0 = g_launches.load();
+    lq_status s = LQ_OK;
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    else s = body(cs);
+    cudaGraph_t g = nullptr;
+    if (e == cudaSuccess) {
+        const cudaError_t e2 = cudaStreamEndCapture(cs, &g);   // always end a begun capture
+        if (s == LQ_OK && e2 != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e2));
+    }
+    if (s == LQ_OK) {
+        e = cudaGraphInstantiate(out, g, 0);
+        if (e != cudaSuccess) {
+            *out = nullptr;
+            s = fail(LQ_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+        }
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cs);
+    // the captured launches have not run: count them when the graph replays
+    *kernels = g_launches.load() - l0;
+    g_launches.fetch_sub(*kernels);
+    cudaGetLastError();
+    return s;
+}
+
 lq_status have_device() {
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
@@ -272,6 +304,15 @@ struct CachedPlan {
     int32_t qmap_after[64];
     int uses = 0;
     bool promoted = false;
+    // CUDA graph of this plan's launches on one state (LQ_OPT_GRAPHS; run_single):
+    // captured on the second run with the same buffers, replayed after
+    std::mutex gmu;
+    cudaGraphExec_t gexec = nullptr;
+    uint64_t gkernels = 0;
+    std::array<const void *, 6> gkey{}, gseen{};
+    ~CachedPlan() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+    }
 };
 
 // Compile on second use: in auto JIT mode small single-state plans start on
@@ -788,7 +829,8 @@ lq_status upload_tables(lq_sv *sv, const Blob &blob, uint64_t uid) {
     return LQ_OK;
 }
 
-lq_status run_single(lq_sv *sv, Plan &plan, const MatBuilder &mb, const double *theta, size_t n_theta) {
+lq_status run_single(lq_sv *sv, Plan &plan, const MatBuilder &mb, const double *theta, size_t n_theta,
+                     CachedPlan *cp = nullptr) {
     if (plan.passes.empty()) return LQ_OK;
     if (!plan.prepared) plan.stream_tag = (uint64_t)(uintptr_t)sv->stream;
     LQ_TRY(prepare(plan));
@@ -816,12 +858,40 @@ lq_status run_single(lq_sv *sv, Plan &plan, const MatBuilder &mb, const double *
     if (mb.mat_size) {
         LQ_TRY(sv->work_buf.reserve((size_t)mb.mat_size * sizeof(double2), sv->stream));
         mats = sv->work_buf.at<double2>(0);
-        k_build_mats<<<grid_for(mb.specs.size()), 256, 0, sv->stream>>>(
-            dp.specs, (int)mb.specs.size(), dp.factors, theta ? sv->plan_buf.at<double>(o_th) : nullptr, nullptr,
-            dp.cst, mats, mb.mat_size, 1);
-        LQ_TRY(check_launch("k_build_mats"));
     }
-    return launch_passes(plan, dp, sv->d, 0, 1, mats, 0, sv->stream, false);
+    auto body = [&](cudaStream_t st) -> lq_status {
+        if (mb.mat_size) {
+            k_build_mats<<<grid_for(mb.specs.size()), 256, 0, st>>>(
+                dp.specs, (int)mb.specs.size(), dp.factors, theta ? sv->plan_buf.at<double>(o_th) : nullptr, nullptr,
+                dp.cst, mats, mb.mat_size, 1);
+            LQ_TRY(check_launch("k_build_mats"));
+        }
+        return launch_passes(plan, dp, sv->d, 0, 1, mats, 0, st, false);
+    };
+    // a cached plan without per-call data: replay its CUDA graph when the
+    // state's buffers are the ones it was captured with (host launch cost of
+    // one graph instead of one per kernel and constant-bank copy)
+    if (cp && !theta && plan.uid && g_opt_graphs.load() && !g_opt_timing.load()) {
+        std::lock_guard<std::mutex> lk(cp->gmu);
+        const std::array<const void *, 6> key{sv->d, sv->plan_buf.p, sv->work_buf.p, sv->ctab_buf.p,
+                                              (const void *)sv->stream, (const void *)(uintptr_t)plan.uid};
+        if (!(cp->gexec && cp->gkey == key)) {
+            if (cp->gseen != key) {   // first run with these buffers: direct
+                cp->gseen = key;
+                return body(sv->stream);
+            }
+            if (cp->gexec) {
+                cudaGraphExecDestroy(cp->gexec);
+                cp->gexec = nullptr;
+            }
+            LQ_TRY(capture_graph(body, &cp->gexec, &cp->gkernels));
+            cp->gkey = key;
+        }
+        CUDA_TRY(cudaGraphLaunch(cp->gexec, sv->stream));
+        g_launches.fetch_add(cp->gkernels);
+        return LQ_OK;
+    }
+    return body(sv->stream);
 }
 
 lq_status canonicalize(lq_sv *sv) {
@@ -1873,7 +1943,7 @@ lq_status apply_impl(lq_sv *sv, const lq_gate *gates, size_t n_gates, const doub
         g_plan_cache.put(key, cp);
     }
     LQ_TRY(promote(*cp));
-    LQ_TRY(run_single(sv, cp->plan, cp->mb, theta, n_theta));
+    LQ_TRY(run_single(sv, cp->plan, cp->mb, theta, n_theta, cp.get()));
     memcpy(sv->qmap, cp->qmap_after, sizeof(sv->qmap));
     return LQ_OK;
 }
@@ -1917,7 +1987,7 @@ static lq_status qft_body(lq_sv *sv, int inverse) {
         g_plan_cache.put(key, cp);
     }
     LQ_TRY(promote(*cp));
-    LQ_TRY(run_single(sv, cp->plan, cp->mb, nullptr, 0));
+    LQ_TRY(run_single(sv, cp->plan, cp->mb, nullptr, 0, cp.get()));
     memcpy(sv->qmap, cp->qmap_after, sizeof(sv->qmap));
     return LQ_OK;
 }
@@ -2320,37 +2390,6 @@ static lq_status psr_run_body(lq_psr *P, const double *theta_dev, double *grad_d
 // host gaps between the kernels.  Capture runs on a private stream in
 // thread-local mode (nothing executes); the graph replays on the caller's
 // stream, after everything queued there before it.
-template <class F>
-static lq_status capture_graph(F body, cudaGraphExec_t *out, uint64_t *kernels) {
-    *out = nullptr;
-    cudaStream_t cs = nullptr;
-    CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    const uint64_t l0 = g_launches.load();
-    lq_status s = LQ_OK;
-    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-    if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-    else s = body(cs);
-    cudaGraph_t g = nullptr;
-    if (e == cudaSuccess) {
-        const cudaError_t e2 = cudaStreamEndCapture(cs, &g);   // always end a begun capture
-        if (s == LQ_OK && e2 != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e2));
-    }
-    if (s == LQ_OK) {
-        e = cudaGraphInstantiate(out, g, 0);
-        if (e != cudaSuccess) {
-            *out = nullptr;
-            s = fail(LQ_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-        }
-    }
-    if (g) cudaGraphDestroy(g);
-    cudaStreamDestroy(cs);
-    // the captured launches have not run: count them when the graph replays
-    *kernels = g_launches.load() - l0;
-    g_launches.fetch_sub(*kernels);
-    cudaGetLastError();
-    return s;
-}
-
 // Graphs pay off most where launches dominate (config 3: 47 -> 37 us per
 // gradient), and still trim the launch gaps of a config-4 gradient (6748
 // tile launches: 2.600 -> 2.578 s, same box).  Not with a communicator (its

@@ -807,6 +807,29 @@ def test_cuda_graph_replay_is_bit_identical(lq):
             assert b[2] < it
 
 
+def test_cuda_graph_single_state_replay(lq):
+    """Cached single-state plans (a circuit without parameters, the QFT) are
+    captured as CUDA graphs on their second run on the same state buffers
+    and replayed after: bit-identical to the stream path, across a state that
+    is re-initialised between runs and a second state (new buffers)."""
+    rng = np.random.default_rng(77)
+    n = 14
+    gates = rich_circuit(n, 60, rng)
+    outs = {}
+    for graphs in (0, 1):
+        lq.lq_set_option(lq.LQ_OPT_GRAPHS, graphs)
+        res = []
+        for k in range(2):
+            sv = lq.StateVector(n)
+            for r in range(4):     # direct, capture + replay, replay, replay
+                sv.init_random(100 + r).apply(gates).qft()
+                res.append(sv.read())
+            sv.free()
+        outs[graphs] = res
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+
+
 # ---------------------------------------------------------------- Trotter XYZ (f1)
 
 def test_trotter_xyz_vs_oracle(lq, oracle):
