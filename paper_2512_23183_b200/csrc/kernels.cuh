@@ -280,11 +280,80 @@ __global__ void __launch_bounds__(256) k_random_norm(uint64_t N, uint64_t off, u
     if (threadIdx.x == 0) partial[blockIdx.x] = r;
 }
 
+// The write sweep evaluates the same formula as gauss_amp with table-driven
+// log and sincospi (the libdevice FP64 routines cost ~100 FP64 instructions
+// per amplitude and made this sweep FP64-bound at a quarter of the write
+// roofline):
+//   log u0 = e ln2 + log c_j + log1p(r), u0 = 2^e m, m in [1, 2),
+//            c_j = 1 + j/64 (top 6 bits of m), r = (m - c_j) / c_j, |r| < 1/64,
+//            log1p by its Taylor series to r^10 (remainder < 2^-66);
+//   (cos, sin)(pi x), x = 2 u1 in (0, 2): x = j/128 + t, t in [0, 1/128),
+//            rotate the tabulated (cos, sin)(pi j/128) by (cos, sin)(pi t)
+//            from their Taylor series (degree 8 / 9, remainder < 2^-70).
+// m - c_j and x - j/128 are exact; the tables are computed per block with
+// the libdevice routines.  Relative error ~1e-16 (lq.h lq_sv_init_random
+// promises the formula to 1e-12; tests compare with the oracle to 1e-10).
+__device__ __forceinline__ double2 gauss_amp_tab(uint64_t seed, uint64_t i, const double2 *__restrict__ lt,
+                                                 const double2 *__restrict__ sc) {
+    const uint64_t x0 = splitmix64(seed ^ (2 * i)), x1 = splitmix64(seed ^ (2 * i + 1));
+    const double u0 = ((double)(x0 >> 11) + 0.5) * 0x1.0p-53;
+    const double u1 = ((double)(x1 >> 11) + 0.5) * 0x1.0p-53;
+    // log u0
+    const uint64_t b = (uint64_t)__double_as_longlong(u0);
+    const int e = (int)((b >> 52) & 0x7FF) - 1023;   // u0 >= 2^-54: normal
+    const uint32_t j = (uint32_t)((b >> 46) & 63u);
+    const double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+    const double2 L = lt[j];                          // (1 / c_j, log c_j)
+    const double r = (m - (1.0 + (double)j * 0.015625)) * L.x;
+    double p = -1.0 / 10.0;
+    p = fma(p, r, 1.0 / 9.0);
+    p = fma(p, r, -1.0 / 8.0);
+    p = fma(p, r, 1.0 / 7.0);
+    p = fma(p, r, -1.0 / 6.0);
+    p = fma(p, r, 1.0 / 5.0);
+    p = fma(p, r, -1.0 / 4.0);
+    p = fma(p, r, 1.0 / 3.0);
+    p = fma(p, r, -0.5);
+    p = p * r * r + r;                                 // log1p(r)
+    const double lg = fma((double)e, 0.69314718055994530942, L.y + p);
+    const double rad = sqrt(-2.0 * lg);
+    // (cos, sin)(2 pi u1)
+    const double x = 2.0 * u1;
+    const uint32_t k = (uint32_t)(x * 128.0);         // 0..255
+    const double t = (x - (double)k * 0.0078125) * 3.14159265358979323846;
+    const double t2 = t * t;
+    double cs = 1.0 / 40320.0;
+    cs = fma(cs, t2, -1.0 / 720.0);
+    cs = fma(cs, t2, 1.0 / 24.0);
+    cs = fma(cs, t2, -0.5);
+    cs = fma(cs, t2, 1.0);
+    double sn = 1.0 / 362880.0;
+    sn = fma(sn, t2, -1.0 / 5040.0);
+    sn = fma(sn, t2, 1.0 / 120.0);
+    sn = fma(sn, t2, -1.0 / 6.0);
+    sn = fma(sn * t2, t, t);
+    const double2 T = sc[k];                          // (cos, sin)(pi k / 128)
+    const double c = fma(T.x, cs, -T.y * sn), s = fma(T.y, cs, T.x * sn);
+    return make_double2(rad * c, rad * s);
+}
+
 __global__ void __launch_bounds__(256) k_random_write(uint64_t N, uint64_t off, uint64_t seed, const double *norm2,
                                                       double2 *__restrict__ psi) {
+    __shared__ double2 lt[64], sc[256];
+    {
+        const uint32_t q = threadIdx.x;   // blockDim = 256
+        double s, c;
+        sincospi((double)q / 128.0, &s, &c);
+        sc[q] = make_double2(c, s);
+        if (q < 64) {
+            const double cj = 1.0 + (double)q / 64.0;
+            lt[q] = make_double2(1.0 / cj, log(cj));
+        }
+    }
+    __syncthreads();
     const double inv = 1.0 / sqrt(*norm2);
     for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < N; i += (uint64_t)gridDim.x * 256)
-        psi[i] = cscale(gauss_amp(seed, off + i), inv);
+        psi[i] = cscale(gauss_amp_tab(seed, off + i, lt, sc), inv);
 }
 
 // ---------------------------------------------------------------- global-qubit exchange (a9)
