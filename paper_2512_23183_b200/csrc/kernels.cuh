@@ -291,8 +291,8 @@ __global__ void __launch_bounds__(256) k_random_norm(uint64_t N, uint64_t off, u
 //            rotate the tabulated (cos, sin)(pi j/128) by (cos, sin)(pi t)
 //            from their Taylor series (degree 8 / 9, remainder < 2^-70).
 // m - c_j and x - j/128 are exact; the tables are computed per block with
-// the libdevice routines.  Relative error ~1e-16 (lq.h lq_sv_init_random
-// promises the formula to 1e-12; tests compare with the oracle to 1e-10).
+// the libdevice routines.  Relative error ~1e-16 (lq.h lq_sv_init_random;
+// the GPU tests compare with the oracle to 1e-13 absolute).
 __device__ __forceinline__ double2 gauss_amp_tab(uint64_t seed, uint64_t i, const double2 *__restrict__ lt,
                                                  const double2 *__restrict__ sc) {
     const uint64_t x0 = splitmix64(seed ^ (2 * i)), x1 = splitmix64(seed ^ (2 * i + 1));
