@@ -310,6 +310,7 @@ struct CachedPlan {
     cudaGraphExec_t gexec = nullptr;
     uint64_t gkernels = 0;
     std::array<const void *, 6> gkey{}, gseen{};
+    bool gdisabled = false;   // a capture failed: stream launches only
     ~CachedPlan() {
         if (gexec) cudaGraphExecDestroy(gexec);
     }
@@ -871,7 +872,7 @@ lq_status run_single(lq_sv *sv, Plan &plan, const MatBuilder &mb, const double *
     // a cached plan without per-call data: replay its CUDA graph when the
     // state's buffers are the ones it was captured with (host launch cost of
     // one graph instead of one per kernel and constant-bank copy)
-    if (cp && !theta && plan.uid && g_opt_graphs.load() && !g_opt_timing.load()) {
+    if (cp && !cp->gdisabled && !theta && plan.uid && g_opt_graphs.load() && !g_opt_timing.load()) {
         std::lock_guard<std::mutex> lk(cp->gmu);
         const std::array<const void *, 6> key{sv->d, sv->plan_buf.p, sv->work_buf.p, sv->ctab_buf.p,
                                               (const void *)sv->stream, (const void *)(uintptr_t)plan.uid};
@@ -884,7 +885,11 @@ lq_status run_single(lq_sv *sv, Plan &plan, const MatBuilder &mb, const double *
                 cudaGraphExecDestroy(cp->gexec);
                 cp->gexec = nullptr;
             }
-            LQ_TRY(capture_graph(body, &cp->gexec, &cp->gkernels));
+            if (capture_graph(body, &cp->gexec, &cp->gkernels) != LQ_OK) {
+                // a capture failure is not a fault of the state: run on the stream from now on
+                cp->gdisabled = true;
+                return body(sv->stream);
+            }
             cp->gkey = key;
         }
         CUDA_TRY(cudaGraphLaunch(cp->gexec, sv->stream));
@@ -2186,6 +2191,7 @@ struct lq_psr {
     const void *g_ptr[3] = {nullptr, nullptr, nullptr};   // pointers of the last run
     uint64_t graph_launches = 0;                           // kernels in the graph
     uint64_t graph_replays = 0;
+    bool gdisabled = false;                                // a capture failed: stream launches only
 };
 
 extern "C" {
@@ -2395,7 +2401,7 @@ static lq_status psr_run_body(lq_psr *P, const double *theta_dev, double *grad_d
 // tile launches: 2.600 -> 2.578 s, same box).  Not with a communicator (its
 // all-reduce and error polling stay on the host path) or per-launch timing.
 static bool psr_graphs(const lq_psr *P) {
-    return g_opt_graphs.load() && !P->comm && !g_opt_timing.load();
+    return g_opt_graphs.load() && !P->comm && !g_opt_timing.load() && !P->gdisabled;
 }
 // runs short enough that the device VQE loop may replay iterations past the
 // stop (at most 2^24 amplitudes per run; a config-4 run, 2.6 s, reads the
@@ -2414,8 +2420,11 @@ static lq_status psr_run_graph(lq_psr *P, const double *theta_dev, double *grad_
             for (int i = 0; i < 3; i++) P->g_ptr[i] = ptr[i];
             return psr_run_body(P, theta_dev, grad_dev, energy_dev, P->stream);
         }
-        LQ_TRY(capture_graph([&](cudaStream_t cs) { return psr_run_body(P, theta_dev, grad_dev, energy_dev, cs); },
-                             &P->gexec, &P->graph_launches));
+        if (capture_graph([&](cudaStream_t cs) { return psr_run_body(P, theta_dev, grad_dev, energy_dev, cs); },
+                          &P->gexec, &P->graph_launches) != LQ_OK) {
+            P->gdisabled = true;   // not a fault of the plan: stream launches from now on
+            return psr_run_body(P, theta_dev, grad_dev, energy_dev, P->stream);
+        }
     }
     CUDA_TRY(cudaGraphLaunch(P->gexec, P->stream));
     g_launches.fetch_add(P->graph_launches);
@@ -2455,7 +2464,8 @@ lq_status lq_vqe_adam(int n_qubits, const lq_gate *ansatz, size_t n_gates, doubl
         if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe setup: ") + cudaGetErrorString(e));
     }
     int t = 0;
-    if (s == LQ_OK && psr_graphs(P)) {
+    bool graph_loop = s == LQ_OK && psr_graphs(P);
+    if (graph_loop) {
         // Device-resident loop: one graph = one lq_psr_run + k_vqe_step (the
         // stopping rule and the Adam step on the device, bias corrections from
         // the same host pow() as below); replayed in growing chunks with one
@@ -2479,18 +2489,22 @@ lq_status lq_vqe_adam(int n_qubits, const lq_gate *ansatz, size_t n_gates, doubl
             if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // bc is pageable host memory
             if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe setup: ") + cudaGetErrorString(e));
         }
-        if (s == LQ_OK)
-            s = capture_graph(
+        if (s == LQ_OK &&
+            capture_graph(
                 [&](cudaStream_t cs) {
                     LQ_TRY(psr_run_body(P, d_th, d_g, d_e, cs));
                     k_vqe_step<<<1, 256, 0, cs>>>(d_th, d_m, d_v, d_g, (int)n_params, cfg->lr, cfg->beta1, cfg->beta2,
                                                   cfg->eps, cfg->tol, cfg->max_iter, d_bc, d_e, d_tr, d_ctl);
                     return check_launch("k_vqe_step");
                 },
-                &gx, &gk);
+                &gx, &gk) != LQ_OK) {
+            graph_loop = false;   // capture failed (not a fault): the host loop below
+            P->gdisabled = true;
+        }
         VqeCtl ctl{0, 0, 0.0};
         const int max_chunk = psr_small(P) ? 32 : 1;
-        for (int done = 0, chunk = 1; s == LQ_OK && done < T && ctl.state == 0; chunk = std::min(chunk * 2, max_chunk)) {
+        for (int done = 0, chunk = 1; graph_loop && s == LQ_OK && done < T && ctl.state == 0;
+             chunk = std::min(chunk * 2, max_chunk)) {
             const int c = std::min(chunk, T - done);
             for (int i = 0; i < c && s == LQ_OK; i++) {
                 const cudaError_t e = cudaGraphLaunch(gx, st);
@@ -2505,8 +2519,8 @@ lq_status lq_vqe_adam(int n_qubits, const lq_gate *ansatz, size_t n_gates, doubl
             }
         }
         if (gx) cudaGraphExecDestroy(gx);
-        t = ctl.t;
-        if (s == LQ_OK && energy_trace) {
+        if (graph_loop) t = ctl.t;
+        if (graph_loop && s == LQ_OK && energy_trace) {
             // a non-finite E_t is reported, not recorded (as the host loop)
             const size_t cnt = (size_t)(ctl.state == 2 ? t : t + 1);
             cudaError_t e = cnt ? cudaMemcpyAsync(energy_trace, d_tr, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st)
@@ -2514,10 +2528,13 @@ lq_status lq_vqe_adam(int n_qubits, const lq_gate *ansatz, size_t n_gates, doubl
             if (e == cudaSuccess) e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) s = fail(LQ_ERR_CUDA, std::string("vqe: ") + cudaGetErrorString(e));
         }
-        if (s == LQ_OK && ctl.state == 2) s = fail(LQ_ERR_NONFINITE, "non-finite energy at iteration " + std::to_string(t));
-        if (s == LQ_OK && ctl.state == 0) s = fail(LQ_ERR_STATE, "vqe loop ended without its stopping rule (internal)");
+        if (graph_loop && s == LQ_OK && ctl.state == 2)
+            s = fail(LQ_ERR_NONFINITE, "non-finite energy at iteration " + std::to_string(t));
+        if (graph_loop && s == LQ_OK && ctl.state == 0)
+            s = fail(LQ_ERR_STATE, "vqe loop ended without its stopping rule (internal)");
         vb.release(st);
-    } else {
+    }
+    if (!graph_loop) {
     double prev = 0.0;
     for (; s == LQ_OK; t++) {
         s = lq_psr_run(P, d_th, d_g, d_e);
