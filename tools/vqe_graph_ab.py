@@ -1,3 +1,6 @@
+"""Config-3 VQE loop (200 Adam iterations) and one-shot gradient device time
+with CUDA graphs off / on (LQ_OPT_GRAPHS), interleaved A/B
+(profiles/r02/graphs_config3.jsonl)."""
 import json, os, sys
 sys.path.insert(0, os.getcwd())
 import torch, numpy as np
