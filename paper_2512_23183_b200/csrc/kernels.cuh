@@ -284,15 +284,22 @@ __global__ void __launch_bounds__(256) k_random_norm(uint64_t N, uint64_t off, u
 // log and sincospi (the libdevice FP64 routines cost ~100 FP64 instructions
 // per amplitude and made this sweep FP64-bound at a quarter of the write
 // roofline):
-//   log u0 = e ln2 + log c_j + log1p(r), u0 = 2^e m, m in [1, 2),
-//            c_j = 1 + j/64 (top 6 bits of m), r = (m - c_j) / c_j, |r| < 1/64,
-//            log1p by its Taylor series to r^10 (remainder < 2^-66);
+//   log u0 = e ln2 + log c + log1p(r), u0 = 2^e m, m in [0.75, 1.5)
+//            (m in [1.5, 2) is halved and e incremented), c = the nearest
+//            node of spacing 1/128 above 1 and 1/256 below it (130 nodes),
+//            r = (m - c) / c, |r| <= 1/256, log1p by its Taylor series to
+//            r^8 (remainder < 2^-75 relative).  Reducing to m around 1 keeps the
+//            relative error at a few ulp where log u0 -> 0 (u0 -> 1): there
+//            c = 1, log c = 0 and log u0 = log1p(r) with r exact; a fixed
+//            m in [1, 2) would cancel -ln2 against log c ~ ln2 (4e-9 relative
+//            at u0 = 1 - 1e-6);
 //   (cos, sin)(pi x), x = 2 u1 in (0, 2): x = j/128 + t, t in [0, 1/128),
 //            rotate the tabulated (cos, sin)(pi j/128) by (cos, sin)(pi t)
 //            from their Taylor series (degree 8 / 9, remainder < 2^-70).
-// m - c_j and x - j/128 are exact; the tables are computed per block with
-// the libdevice routines.  Relative error ~1e-16 (lq.h lq_sv_init_random;
-// the GPU tests compare with the oracle to 1e-13 absolute).
+// m - c and x - j/128 are exact; the tables are computed per block with
+// the libdevice routines.  Relative error of the amplitude a few 1e-16
+// everywhere (lq.h lq_sv_init_random; test_gpu_fullsize checks the ratio to
+// the oracle's unnormalised amplitudes to 1e-12 relative at n = 33).
 __device__ __forceinline__ double2 gauss_amp_tab(uint64_t seed, uint64_t i, const double2 *__restrict__ lt,
                                                  const double2 *__restrict__ sc) {
     const uint64_t x0 = splitmix64(seed ^ (2 * i)), x1 = splitmix64(seed ^ (2 * i + 1));
@@ -300,14 +307,24 @@ __device__ __forceinline__ double2 gauss_amp_tab(uint64_t seed, uint64_t i, cons
     const double u1 = ((double)(x1 >> 11) + 0.5) * 0x1.0p-53;
     // log u0
     const uint64_t b = (uint64_t)__double_as_longlong(u0);
-    const int e = (int)((b >> 52) & 0x7FF) - 1023;   // u0 >= 2^-54: normal
-    const uint32_t j = (uint32_t)((b >> 46) & 63u);
-    const double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
-    const double2 L = lt[j];                          // (1 / c_j, log c_j)
-    const double r = (m - (1.0 + (double)j * 0.015625)) * L.x;
-    double p = -1.0 / 10.0;
-    p = fma(p, r, 1.0 / 9.0);
-    p = fma(p, r, -1.0 / 8.0);
+    int e = (int)((b >> 52) & 0x7FF) - 1023;         // u0 >= 2^-54: normal
+    const uint32_t mt = (uint32_t)((b >> 44) & 255u); // top 8 mantissa bits
+    const uint32_t kk = (mt + 1) >> 1;                // nearest 1/128 step: 0..128
+    double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+    double cn;
+    uint32_t j;
+    if (mt >= 128) {                                   // m in [1.5, 2): m/2 in [0.75, 1)
+        m *= 0.5;
+        e += 1;
+        cn = 0.5 + (double)kk * 0.00390625;           // kk in 64..128: c in [0.75, 1]
+        j = kk + 1;
+    } else {
+        cn = 1.0 + (double)kk * 0.0078125;            // kk in 0..64: c in [1, 1.5]
+        j = kk;
+    }
+    const double2 L = lt[j];                          // (1 / c, log c)
+    const double r = (m - cn) * L.x;                  // m - c exact (Sterbenz)
+    double p = -1.0 / 8.0;
     p = fma(p, r, 1.0 / 7.0);
     p = fma(p, r, -1.0 / 6.0);
     p = fma(p, r, 1.0 / 5.0);
@@ -339,14 +356,14 @@ __device__ __forceinline__ double2 gauss_amp_tab(uint64_t seed, uint64_t i, cons
 
 __global__ void __launch_bounds__(256) k_random_write(uint64_t N, uint64_t off, uint64_t seed, const double *norm2,
                                                       double2 *__restrict__ psi) {
-    __shared__ double2 lt[64], sc[256];
+    __shared__ double2 lt[130], sc[256];
     {
         const uint32_t q = threadIdx.x;   // blockDim = 256
         double s, c;
         sincospi((double)q / 128.0, &s, &c);
         sc[q] = make_double2(c, s);
-        if (q < 64) {
-            const double cj = 1.0 + (double)q / 64.0;
+        if (q < 130) {   // nodes of gauss_amp_tab: 1 + q/128 (q <= 64), 0.5 + (q - 1)/256 (q >= 65)
+            const double cj = q <= 64 ? 1.0 + (double)q * 0.0078125 : 0.5 + (double)(q - 1) * 0.00390625;
             lt[q] = make_double2(1.0 / cj, log(cj));
         }
     }
