@@ -112,3 +112,14 @@ def test_planner_validation_errors(lq):
         with pytest.raises(lq.LQError) as ei:
             lq.lq_plan_describe(5, gates)
         assert ei.value.status == status, gates
+
+
+def test_jit_programs_compile_without_device(lq):
+    """The JIT pass programs (tile.cuh + the generated op programs) compile
+    for sm_100a through NVRTC on a host without a GPU: the QFT at n = 30 both
+    ways (three 12-bit passes) and the
+    config-1 circuit + QFT plan at n = 10."""
+    assert lq.lq_qft_jit_compile_check(30, False) == 3
+    assert lq.lq_qft_jit_compile_check(30, True) >= 3
+    w = W.config1()
+    assert lq.lq_jit_compile_check(w.n, w.gates) >= 1
