@@ -105,6 +105,26 @@ def test_init_random_matches_oracle(lq, oracle):
         np.testing.assert_allclose(got, oracle.init_random(n, 1234 + n), rtol=0, atol=1e-13)
 
 
+def test_init_random_relative_accuracy_at_small_amplitudes(lq, oracle):
+    """|a_i|^2 = -2 ln u0 -> 0 as u0 -> 1: the device's log must stay
+    relatively exact there, not only to 1e-13 absolute (a table-driven log
+    that added -ln2 to log c ~ ln2 lost ~1e-10 relative on the smallest
+    amplitudes of n = 22).  On the 64 smallest unnormalised amplitudes of the
+    oracle's formula (c.1) and 4096 seeded others, state_i / a_i is one real
+    constant 1/sqrt(S) to 1e-13 relative."""
+    n, seed = 22, 4242
+    raw = oracle.random_gaussian_at(seed, np.arange(1 << n, dtype=np.uint64))
+    small = np.argsort(np.abs(raw))[:64]
+    other = np.random.default_rng(5).choice(1 << n, 4096, replace=False)
+    idx = np.unique(np.concatenate([small, other])).astype(np.uint64)
+    sv = lq.StateVector(n)
+    sv.init_random(seed)
+    ratio = sv.gather(idx) / raw[idx.astype(np.int64)]
+    sv.free()
+    c = float(np.median(ratio.real))
+    assert np.abs(ratio - c).max() <= 1e-13 * c, np.abs(ratio - c).max() / c
+
+
 def test_init_basis_norm_gather_write(lq):
     n = 12
     sv = lq.StateVector(n)
