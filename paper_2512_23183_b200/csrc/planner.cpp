@@ -1159,10 +1159,37 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
     size_t s = 0;
     uint32_t relabel_from = 0, relabel_to = 0;   // PF_RELABEL of the last pass: register masks
     LocalMap relabel_L(0);
+    // Balanced stage packing: the pass over the low (contiguous) bits takes K
+    // stages, and the strided passes share the other n - K stages evenly, so
+    // the tile bits they leave unused extend the coalescing run (the fill
+    // below adds low bits): n = 31 (K = 11) packs 7+7+6+11 stages with 256-,
+    // 256- and 512-byte runs instead of 8+8+8+7 with 128-byte runs, n = 28
+    // (K = 12) packs 8+8+12 with 256-byte runs instead of 9+9+10, n = 33
+    // (K = 11) 8+7+7+11 instead of 8+8+8+9.  B200, same box: QFT(28) 5.68 ->
+    // 4.92 ms, QFT(31) 59.0 -> 48.9 ms, QFT(33) 240.9 -> 223.1 ms; the pass
+    // count is the greedy one and n = 30 (9+9+12) is unchanged
+    // (profiles/r02/ab_qft_balance.jsonl).
+    std::vector<size_t> cap;
+    size_t qpass = 0;
+    if (n > K && !getenv("LQ_QFT_GREEDY")) {   // (A/B switch)
+        const int np = count_passes(K), ns = np - 1;
+        // (fewer stages in the contiguous pass and 256-byte instead of 512-byte
+        // runs in the strided ones measured the same: n = 31, 7+7+7+10 vs
+        // 7+7+6+11 at K = 11, 48.9 vs 48.7 ms, profiles/r02/ab_qft_balance.jsonl)
+        const int Lc = K, S = n - Lc;
+        const bool low_first = phys(js.front()) < phys(js.back());
+        if (ns > 0 && S > 0 && (S + ns - 1) / ns <= K - c) {
+            for (int p = 0; p < ns; p++) cap.push_back((size_t)(S / ns + (p < S % ns ? 1 : 0)));
+            if (low_first) cap.insert(cap.begin(), (size_t)Lc);
+            else cap.push_back((size_t)Lc);
+        }
+    }
     while (s < js.size()) {
         uint64_t Tm = mand;
         std::vector<int> st;
-        while (s < js.size() && popc(Tm | bit(phys(js[s]))) <= K) {
+        const size_t cap_p = qpass < cap.size() ? cap[qpass] : (size_t)K;
+        qpass++;
+        while (s < js.size() && st.size() < cap_p && popc(Tm | bit(phys(js[s]))) <= K) {
             Tm |= bit(phys(js[s]));
             st.push_back(js[s]);
             s++;

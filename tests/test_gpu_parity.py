@@ -889,7 +889,7 @@ def test_trotter_diagonal_chain_closed_form_n20(lq):
 
 def test_max_size_n33_monomial_qft_closed_form(lq):
     """Largest single-GPU state (n = 33, 128 GiB): a 400-gate monomial
-    circuit from a basis state, then the full QFT (3 tile passes of 12 bits,
+    circuit from a basis state, then the full QFT (4 tile passes of 12 bits,
     bit reversal as a relabel); 2^18 sampled amplitudes against the closed
     form e^{i phi} N^-1/2 e^{2 pi i j k' / N} (SURVEY c.4 (i)); norm."""
     import torch
@@ -904,6 +904,33 @@ def test_max_size_n33_monomial_qft_closed_form(lq):
     sv.init_basis(k).apply(gates).qft()
     idx = np.unique(rng.integers(0, 1 << n, size=1 << 18, dtype=np.uint64))
     assert np.abs(sv.gather(idx) - ph * qft_of_basis(n, kp, idx)).max() <= 1e-12
+    assert abs(sv.norm2() - 1.0) <= 1e-11
+    sv.free()
+    del sv
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n", [25, 28, 29, 31])
+def test_qft_balanced_stage_packing_closed_form(lq, n):
+    """plan_qft's balanced packing (planner.cpp): the strided passes share
+    n - K stages evenly and their spare tile bits lengthen the coalescing run
+    (n = 28: 8+8+12 stages with 256-byte runs, n = 31: 7+6+6+12 with 512-byte
+    runs).  QFT of a basis state against the closed form on sampled
+    amplitudes, then QFT^-1 back to the basis state."""
+    import torch
+    from closed_forms import qft_of_basis
+    torch.cuda.empty_cache()
+    rng = np.random.default_rng(2800 + n)
+    k = int(rng.integers(0, 1 << n))
+    sv = lq.StateVector(n).init_basis(k).qft()
+    idx = np.unique(np.concatenate([rng.integers(0, 1 << n, size=1 << 16, dtype=np.uint64),
+                                    np.array([0, 1, (1 << n) - 1, k], dtype=np.uint64)]))
+    assert np.abs(sv.gather(idx) - qft_of_basis(n, k, idx)).max() <= 1e-12
+    assert abs(sv.norm2() - 1.0) <= 1e-11
+    sv.qft(inverse=True)
+    got = sv.gather(idx)
+    want = (idx == np.uint64(k)).astype(np.complex128)
+    assert np.abs(got - want).max() <= 1e-12
     assert abs(sv.norm2() - 1.0) <= 1e-11
     sv.free()
     del sv

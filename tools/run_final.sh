@@ -10,5 +10,5 @@ ncu -i /tmp/lqj_batch.ncu-rep --page raw --csv > gpurun_out/cfg4_batch.raw.csv 2
 ncu -i /tmp/lqj_batch.ncu-rep --page source --csv --print-source sass -k regex:lqj --launch-skip 2 --launch-count 1 > gpurun_out/cfg4_p2_sass.csv 2>/dev/null
 timeout 900 python tools/companions.py > gpurun_out/companions.log 2>&1; echo comp=$?
 timeout 900 python tools/next_rows.py > gpurun_out/next_rows.jsonl 2> gpurun_out/next_rows.err; echo next=$?
-GS=1,2,4,8 timeout 900 python tools/cfg5_probe.py > gpurun_out/cfg5_n30.jsonl 2> gpurun_out/cfg5.err; echo cfg5=$?
+timeout 900 python tools/cfg5_group.py > gpurun_out/cfg5_group_n30.jsonl 2> gpurun_out/cfg5_group.err; echo cfg5g=$?
 du -sh gpurun_out

@@ -35,7 +35,8 @@ __device__ __forceinline__ uint64_t deposit(uint64_t v, const uint8_t *pos, int 
 // block around it (cp.async.bulk.prefetch.L2) -- runs of the neighbouring
 // tiles, which other CTAs load at about the same time.  pf = -B: the same
 // for the NEXT tile this CTA will process.
-__global__ void __launch_bounds__(256) sweep(double2 *__restrict__ s, uint64_t n_tiles, Pattern P, int pf) {
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) sweep(double2 *__restrict__ s, uint64_t n_tiles, Pattern P, int pf) {
     const uint32_t T = 1u << P.K, per = T / U;   // threads per tile
     const uint32_t lane = threadIdx.x % per, slot = threadIdx.x / per, tiles_per_cta = blockDim.x / per;
     uint64_t off[U];
@@ -82,10 +83,16 @@ static double run(double2 *s, int n, uint64_t mask, int occ, int sms, float *ms_
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    sweep<<<grid, threads>>>(s, n_tiles, P, pf);
+    // 13-bit tiles (512 threads) get their own instantiation, so the 256-thread
+    // code the earlier measurements used is unchanged
+    auto launch = [&]() {
+        if (threads <= 256) sweep<256><<<grid, threads>>>(s, n_tiles, P, pf);
+        else sweep<512><<<grid, threads>>>(s, n_tiles, P, pf);
+    };
+    launch();
     cudaEventRecord(a);
     const int R = 5;
-    for (int r = 0; r < R; r++) sweep<<<grid, threads>>>(s, n_tiles, P, pf);
+    for (int r = 0; r < R; r++) launch();
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms = 0;
