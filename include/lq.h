@@ -460,6 +460,19 @@ lq_status lq_jit_compile_check(int n_qubits, const lq_gate *gates, size_t n_gate
  * QFT^-1) on n qubits in the identity layout. */
 lq_status lq_qft_jit_compile_check(int n_qubits, int inverse, uint64_t *n_kernels);
 
+/* Host-only: the tile-pass plan of the QFT (inverse != 0: QFT^-1) on n
+ * qubits, PAPER.md:597-641 (Alg. 2/3), as JSON in the format of
+ * lq_plan_export_json, with the qubit map the plan leaves behind (the bit
+ * reversal and the last pass's store relabel are relabels, not data moves).
+ * reversed_layout != 0 plans for the layout a forward QFT leaves (qubit q on
+ * physical bit q) instead of the identity layout (qubit q on bit n-1-q); the
+ * JSON's "qmap_in" is that input layout.  Same buffer protocol as
+ * lq_plan_export_json (LQ_ERR_ARG for n outside [1, 40]).  No device needed:
+ * the CPU tests execute these plans with tests/plan_emulator.py against the
+ * oracle. */
+lq_status lq_qft_plan_export_json(int n_qubits, int inverse, int reversed_layout, char *buf, size_t buf_len,
+                                  size_t *needed);
+
 /* Accumulated device time of launches made while LQ_OPT_KERNEL_TIMING was
  * on, per kernel class: 0 tile pass, 1 pair pass, 2 diagonal pass,
  * 3 Pauli expectation, 4 other, 5 global-qubit exchange of a sharded state

@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -2890,6 +2891,29 @@ lq_status lq_qft_jit_compile_check(int n_qubits, int inverse, uint64_t *n_kernel
     std::string err;
     if (!jit_check(plan, &nk, err)) return fail(LQ_ERR_CUDA, err);
     if (n_kernels) *n_kernels = nk;
+    return LQ_OK;
+}
+
+lq_status lq_qft_plan_export_json(int n_qubits, int inverse, int reversed_layout, char *buf, size_t buf_len,
+                                  size_t *needed) {
+    if (n_qubits < 1 || n_qubits > 40) return fail(LQ_ERR_ARG, "n_qubits must be in [1, 40]");
+    int32_t qm[64], qin[64];
+    for (int q = 0; q < n_qubits; q++) qin[q] = qm[q] = reversed_layout ? q : n_qubits - 1 - q;
+    MatBuilder mb;
+    Plan plan;
+    if (!plan_qft(n_qubits, qm, inverse != 0, options(), plan, mb)) return fail(LQ_ERR_STATE, "qft planning failed");
+    std::string j = export_json(plan, mb, qm);
+    std::ostringstream o;
+    o << "{\"qmap_in\":[";
+    for (int q = 0; q < n_qubits; q++) o << (q ? "," : "") << qin[q];
+    o << "]," << j.substr(1);
+    j = o.str();
+    if (needed) *needed = j.size() + 1;
+    if (buf && buf_len) {
+        size_t k = std::min(buf_len - 1, j.size());
+        memcpy(buf, j.data(), k);
+        buf[k] = 0;
+    }
     return LQ_OK;
 }
 

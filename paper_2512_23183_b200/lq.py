@@ -132,6 +132,7 @@ _SIGS = {
     "lq_jit_stats": ([ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_dbl)], _i32),
     "lq_jit_compile_check": ([_i32, _GP, _sz, _TP, _sz, ctypes.POINTER(_u64)], _i32),
     "lq_qft_jit_compile_check": ([_i32, _i32, ctypes.POINTER(_u64)], _i32),
+    "lq_qft_plan_export_json": ([_i32, _i32, _i32, ctypes.c_char_p, _sz, ctypes.POINTER(ctypes.c_size_t)], _i32),
     "lq_trotter_xyz": ([_P, _P, _dbl, _dbl, _i32, _i32, _DP], _i32),
     "lq_vqe_adam": ([_i32, _GP, _sz, _DP, _sz, _TP, _sz, _P, _P, _DP, ctypes.POINTER(ctypes.c_int32)], _i32),
 }
@@ -483,6 +484,17 @@ def lq_qft_jit_compile_check(n_qubits: int, inverse: bool = False) -> int:
     nk = _u64()
     _chk(_lib.lq_qft_jit_compile_check(n_qubits, int(bool(inverse)), ctypes.byref(nk)))
     return nk.value
+
+
+def lq_qft_plan_export_json(n_qubits: int, inverse: bool = False, reversed_layout: bool = False) -> dict:
+    import json
+    need = ctypes.c_size_t()
+    _chk(_lib.lq_qft_plan_export_json(n_qubits, int(bool(inverse)), int(bool(reversed_layout)), None, 0,
+                                      ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _chk(_lib.lq_qft_plan_export_json(n_qubits, int(bool(inverse)), int(bool(reversed_layout)), buf, len(buf),
+                                      ctypes.byref(need)))
+    return json.loads(buf.value.decode())
 
 
 # ---- sharded states (a9) ---------------------------------------------------

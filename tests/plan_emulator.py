@@ -20,7 +20,7 @@ GK_REAL, GK_IMAG, GK_HAD = range(3)
 FK_YDIAG = 100
 PASS_TILE, PASS_PAIR, PASS_DIAG = 0, 1, 2
 MF_U2x2, MF_DIAG2, MF_U4x4, MF_DIAG4, MF_G = range(5)
-PF_EXPV, PF_NO_STORE = 2, 4
+PF_EXPV, PF_NO_STORE, PF_RELABEL = 2, 4, 8
 QF_INVERSE, QF_REVERSED, QF_GENERAL, QF_SCALE = 1, 2, 8, 16
 # lq_kind numbering
 (LQ_H, LQ_X, LQ_Y, LQ_Z, LQ_S, LQ_SDG, LQ_T, LQ_TDG, LQ_RX, LQ_RY, LQ_RZ, LQ_CNOT, LQ_CZ, LQ_CP,
@@ -295,6 +295,24 @@ def run(plan, psi, theta=None, shift=None, gofs=0):
                                    p.get("lpos"))
             if p["store_perm"] >= 0:
                 x = apply_perm(x, p["store_perm"])
+            if p["flags"] & PF_RELABEL:
+                # no store exchange (lq_internal.h PassFlags): the thread that
+                # holds local index l under the last sub-block's register
+                # mapping stores it where the Sstore mapping puts the same
+                # (thread, register) pair: register bit i moves from local bit
+                # S_last[i] to Sstore[i], thread bit k from the k-th other bit
+                # of one mapping to the k-th other bit of the other
+                Rr = plan["Rr"]
+                S_last = subs[p["sub_end"] - 1]["S"][:Rr]
+                S_st = p["Sstore"][:Rr]
+                o_last = [b for b in range(Kp) if b not in S_last]
+                o_st = [b for b in range(Kp) if b not in S_st]
+                dst = np.zeros_like(L)
+                for a, b in list(zip(S_last, S_st)) + list(zip(o_last, o_st)):
+                    dst |= ((L >> a) & 1) << b
+                y = np.empty_like(x)
+                y[dst] = x
+                x = y
             if not (p["flags"] & PF_NO_STORE):
                 if oop:
                     gs = np.zeros_like(g)

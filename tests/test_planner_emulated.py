@@ -97,3 +97,67 @@ def test_emulated_psr_relabel_stores(lq, oracle, n, relabel):
     finally:
         lq.lq_set_option(lq.LQ_OPT_EXPORT_PSR, 0)
         lq.lq_set_option(lq.LQ_OPT_RELABEL_STORES, 0)
+
+
+@pytest.mark.parametrize("K,rb", [(0, 4), (6, 4), (5, 3), (7, 2)])
+@pytest.mark.parametrize("n", [4, 9, 10, 13, 14])
+def test_emulated_qft_plans(lq, oracle, n, K, rb):
+    """plan_qft (the single-state QFT planner: balanced stage packing, register
+    twiddle tables, per-pass scale, bit reversal and the last pass's store
+    relabel folded into the qubit map) executed by the plan emulator against
+    the oracle's QFT, forward and inverse, from the identity
+    layout and from the layout a forward QFT leaves."""
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
+    lq.lq_set_option(lq.LQ_OPT_REG_BITS, rb)
+    psi_log = oracle.init_random(n, 77 + n)
+    x = np.arange(psi_log.size, dtype=np.int64)
+    for inverse in (False, True):
+        ref = psi_log.copy()
+        oracle.qft(ref, inverse=inverse)
+        for rev in (False, True):
+            plan = lq.lq_qft_plan_export_json(n, inverse, rev)
+            stages = [sum(1 for k in plan["kops"][sb["op_begin"]:sb["op_end"]] if k["type"] == EM.K_QFT)
+                      for ps in plan["passes"] for sb in plan["subs"][ps["sub_begin"]:ps["sub_end"]]]
+            assert sum(stages) == n
+            # physical-layout input: logical bit n-1-q sits on physical bit qmap_in[q]
+            g = np.zeros_like(x)
+            for q in range(n):
+                g |= ((x >> (n - 1 - q)) & 1) << plan["qmap_in"][q]
+            psi = np.empty_like(psi_log)
+            psi[g] = psi_log
+            EM.run(plan, psi)
+            got = EM.logical_state(plan["qmap"], psi)
+            assert np.abs(got - ref).max() <= 1e-12
+
+
+def test_qft_plan_balanced_stage_packing(lq):
+    """The strided passes share n - K stages evenly and fill their spare tile
+    bits with low bits (longer coalescing runs); the contiguous pass takes K
+    stages; the pass count is the greedy packing's."""
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 0)
+    lq.lq_set_option(lq.LQ_OPT_REG_BITS, 4)
+
+    def shape(n, inverse=False, rev=False):
+        plan = lq.lq_qft_plan_export_json(n, inverse, rev)
+        out = []
+        for ps in plan["passes"]:
+            ns = sum(1 for sb in plan["subs"][ps["sub_begin"]:ps["sub_end"]]
+                     for k in plan["kops"][sb["op_begin"]:sb["op_end"]] if k["type"] == EM.K_QFT)
+            run = 0
+            while run in ps["T"]:
+                run += 1
+            out.append((ns, run, len(ps["T"])))
+        return out
+
+    assert [s[0] for s in shape(30)] == [9, 9, 12]
+    assert [s[0] for s in shape(28)] == [8, 8, 12]
+    assert [s[1] for s in shape(28)] == [4, 4, 12]          # 256-byte runs
+    # QFT^-1 of the layout a forward QFT leaves starts with the contiguous pass
+    assert [s[0] for s in shape(28, True, True)] == [12, 8, 8]
+    assert [s[1] for s in shape(28, True, True)] == [12, 4, 4]
+    s31 = shape(31)
+    assert [s[0] for s in s31] == [7, 7, 6, 11] and [s[1] for s in s31] == [4, 4, 5, 11]
+    for n in range(13, 41):
+        sh = shape(n)
+        assert sum(s[0] for s in sh) == n and all(s[2] == sh[0][2] for s in sh)
+        assert all(s[1] >= 3 for s in sh)
