@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 constexpr int U = 16;
 
@@ -66,6 +68,33 @@ __global__ void __launch_bounds__(MAXT) sweep(double2 *__restrict__ s, uint64_t 
     }
 }
 
+// TPBW_PAIR = 1 / 2: clusters of two CTAs sweep adjacent tiles (t, t + 1: the
+// 128-byte runs of one are the neighbours of the other's) in lockstep -- a
+// cluster barrier before each tile's loads (1) and also before its stores
+// (2) -- to see whether HBM serves two 128-byte halves of a 256-byte segment
+// that arrive from two SMs at about the same time like one 256-byte run.
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) sweep_pair(double2 *__restrict__ s, uint64_t n_tiles, Pattern P, int mode) {
+    cg::cluster_group cl = cg::this_cluster();
+    const uint32_t T = 1u << P.K, per = T / U;
+    const uint32_t lane = threadIdx.x % per, slot = threadIdx.x / per, tiles_per_cta = blockDim.x / per;
+    uint64_t off[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) off[u] = deposit(lane + u * per, P.tpos, P.K);
+    const uint64_t step = (uint64_t)gridDim.x * tiles_per_cta;
+    // (trip counts agree inside a cluster: n_tiles and the grid are even)
+    for (uint64_t t = (uint64_t)blockIdx.x * tiles_per_cta + slot; t < n_tiles; t += step) {
+        const uint64_t base = deposit(t, P.fpos, P.nfree);
+        cl.sync();
+        double2 a[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) a[u] = s[base | off[u]];
+        if (mode >= 2) cl.sync();
+#pragma unroll
+        for (int u = 0; u < U; u++) s[base | off[u]] = make_double2(a[u].y, a[u].x);
+    }
+}
+
 static Pattern make(int n, uint64_t mask) {
     Pattern P{};
     for (int b = 0; b < n; b++) {
@@ -85,8 +114,21 @@ static double run(double2 *s, int n, uint64_t mask, int occ, int sms, float *ms_
     cudaEventCreate(&b);
     // 13-bit tiles (512 threads) get their own instantiation, so the 256-thread
     // code the earlier measurements used is unchanged
+    const int pair = getenv("TPBW_PAIR") ? atoi(getenv("TPBW_PAIR")) : 0;
     auto launch = [&]() {
-        if (threads <= 256) sweep<256><<<grid, threads>>>(s, n_tiles, P, pf);
+        if (pair && threads <= 256 && threads == (1 << P.K) / U) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid & ~1);
+            cfg.blockDim = dim3(threads);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, sweep_pair<256>, s, n_tiles, P, pair);
+        } else if (threads <= 256) sweep<256><<<grid, threads>>>(s, n_tiles, P, pf);
         else sweep<512><<<grid, threads>>>(s, n_tiles, P, pf);
     };
     launch();
