@@ -928,6 +928,38 @@ void plan_circuit(int n, const std::vector<POp> &ops_in, const PlanOptions &opt,
     std::vector<int> rem;
     for (size_t i = 0; i < ops.size(); i++)
         if (!skip[i]) rem.push_back((int)i);
+    // Balanced stage packing of a run of QFT stages (as plan_qft's): the pass
+    // count is the greedy one, but a pass whose stages cover the coalescing
+    // bits (its tile needs no extra low bits) takes K stages and the others
+    // share the rest evenly, so their spare tile bits lengthen the coalescing
+    // run.  Caps are upper bounds on the stages per pass: any prefix of the
+    // run is a valid pass.
+    std::vector<size_t> qcap;
+    size_t qpass = 0;
+    if (all_qft && nl > K && opt.fusion && !getenv("LQ_QFT_GREEDY")) {   // (A/B switch)
+        const int m = (int)ops.size();
+        int np = 0;
+        for (size_t s0 = 0; s0 < ops.size(); np++) {
+            uint64_t Tq = mand;
+            const size_t b0 = s0;
+            while (s0 < ops.size() && popc(Tq | ops[s0].full()) <= K) Tq |= ops[s0++].full();
+            if (s0 == b0) { np = 0; break; }
+        }
+        auto covers = [&](int from, int to) {   // stages [from, to): distinct single bits that include mand
+            uint64_t u = 0;
+            for (int i = from; i < to; i++) u |= ops[i].full();
+            return (u & mand) == mand && popc(u) == to - from;
+        };
+        const int Lc = std::min(K, m);
+        const bool last_free = covers(m - Lc, m), head_free = !last_free && covers(0, Lc);
+        const int ns = (last_free || head_free) ? np - 1 : np;
+        const int S = (last_free || head_free) ? m - Lc : m;
+        if (np > 1 && ns > 0 && S > 0 && (S + ns - 1) / ns <= K - c) {
+            for (int p = 0; p < ns; p++) qcap.push_back((size_t)(S / ns + (p < S % ns ? 1 : 0)));
+            if (head_free) qcap.insert(qcap.begin(), (size_t)Lc);
+            else if (last_free) qcap.push_back((size_t)Lc);
+        }
+    }
     // the FP64 budget trades an extra HBM round trip for less arithmetic per
     // pass; a state that is one tile has no HBM round trip to trade
     const int budget_all = (nl > K && !all_qft) ? opt.budget : 0;
@@ -1027,6 +1059,13 @@ void plan_circuit(int n, const std::vector<POp> &ops_in, const PlanOptions &opt,
         } else {
             select(mand_next, std::vector<int>(), Tm, absorbed);
         }
+        if (qpass < qcap.size() && absorbed.size() > qcap[qpass]) {
+            absorbed.resize(qcap[qpass]);
+            Tm = mand;
+            for (int i : absorbed) Tm |= ops[i].full();
+            for (int b = 0; b < nl && popc(Tm) < K; b++) Tm |= bit(b);
+        }
+        qpass++;
         mand_next = mand;
         int n_full = 0;
         bool has_expv = false;

@@ -279,6 +279,59 @@ def test_sharded_qft_schedule_is_pass_aligned(lq, m):
     assert all(p["K"] == 12 for ps in local for p in ps)
 
 
+def _qft_pass_shapes(sched):
+    """(stages, low contiguous tile bits, tile bits) of every local tile pass."""
+    out = []
+    for st in sched["steps"]:
+        if st["kind"] != "local":
+            continue
+        pl = st["plan"]
+        for ps in pl["passes"]:
+            ns = sum(1 for sb in pl["subs"][ps["sub_begin"]:ps["sub_end"]]
+                     for k in pl["kops"][sb["op_begin"]:sb["op_end"]] if k["type"] == 6)   # K_QFT
+            run = 0
+            while run in ps["T"]:
+                run += 1
+            out.append((ns, run, len(ps["T"])))
+    return out
+
+
+@pytest.mark.parametrize("K,n,m", [(4, 12, 1), (6, 10, 2), (6, 14, 3), (5, 13, 2)])
+def test_group_qft_only_balanced_runs_emulated(lq, oracle, K, n, m):
+    """QFT-only schedules with tiles small enough that the balanced caps of
+    the local runs bite, executed by the emulator against the oracle, forward
+    and inverse."""
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, K)
+    try:
+        for qft in (1, -1):
+            sched = lq.lq_dist_schedule_json(n, m, [], qft=qft)
+            got, _ = DE.run_group(sched, oracle.init_random(n, 21 + n))
+            ref = oracle.init_random(n, 21 + n)
+            oracle.qft(ref, inverse=qft < 0)
+            assert np.abs(got - ref).max() <= TOL
+    finally:
+        lq.lq_set_option(lq.LQ_OPT_TILE_BITS, 0)
+
+
+def test_sharded_qft_local_runs_pack_balanced(lq):
+    """The local QFT runs of a sharded state pack like plan_qft: same pass
+    count as the greedy packing, the pass over the low bits takes K stages
+    and the strided passes share the rest, their spare tile bits going to the
+    coalescing run (config 5 at n = 34 on 2 ranks: 9 | 7 + 7 + 11 with 256-byte
+    runs instead of 9 | 8 + 8 + 9 with 128-byte runs).  n = 30 and n = 36
+    fill their tiles exactly and are unchanged."""
+    assert _qft_pass_shapes(lq.lq_dist_schedule_json(34, 1, [], qft=1)) == \
+        [(9, 3, 12), (7, 4, 11), (7, 4, 11), (11, 11, 11)]
+    assert _qft_pass_shapes(lq.lq_dist_schedule_json(36, 3, [], qft=1)) == \
+        [(9, 3, 12), (8, 3, 11), (8, 3, 11), (11, 11, 11)]
+    assert _qft_pass_shapes(lq.lq_dist_schedule_json(30, 3, [], qft=1)) == \
+        [(9, 3, 12), (9, 3, 12), (12, 12, 12)]
+    for n, m in ((29, 1), (31, 3), (32, 2), (33, 3), (35, 2)):
+        sh = _qft_pass_shapes(lq.lq_dist_schedule_json(n, m, [], qft=-1))
+        assert sum(s[0] for s in sh) == n and all(s[1] >= 3 for s in sh)
+        assert sh[-1][0] == sh[-1][2]          # the last pass is all stages
+
+
 def test_bench_gpus2_relaunches_under_torchrun_reference_arm():
     """bench.py --gpus 2 without a launcher re-executes itself under
     torch.distributed.run with two ranks (127.0.0.1 rendezvous); on the
