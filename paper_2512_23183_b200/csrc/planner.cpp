@@ -1186,6 +1186,19 @@ bool plan_qft(int n, int32_t *qmap, bool inverse, const PlanOptions &opt, Plan &
     // pass -- at n = 30 four passes of 11 bits take 29.2 ms, three of 12 take
     // 25.0 ms (B200)
     if (opt.K <= 0 && n > 12 && count_passes(12) < count_passes(K)) K = 12;
+    // ... or, at the same pass count, when the balanced packing below would
+    // leave a strided pass of the smaller tile without a spare bit (128-byte
+    // runs) and 12 bits give every strided pass one: QFT(27) 2.555 -> 2.418
+    // ms, QFT(33) 219.8 -> 210.2 ms; the sizes the rule leaves alone are
+    // faster with the smaller tile at 3 CTAs/SM (n = 24, 25, 31, 32: +2 ..
+    // +11 % with 12 bits; profiles/r02/ab_qft_k12.jsonl)
+    // (HBM-resident sizes only, n >= 26: measured there)
+    if (opt.K <= 0 && n >= 26 && K < 12 && !getenv("LQ_QFT_GREEDY") && !getenv("LQ_QFT_K11")) {   // (A/B switches)
+        const int np = count_passes(K), ns = np - 1;
+        const int cK = std::max(0, std::min(opt.coalesce, K - 1)), c12 = std::max(0, std::min(opt.coalesce, 11));
+        if (np == count_passes(12) && ns > 0 && (n - K + ns - 1) / ns == K - cK && (n - 12 + ns - 1) / ns < 12 - c12)
+            K = 12;
+    }
     if (K > 12) K = 12;
     if (n <= K) K = n;
     int Rr = std::min(std::max(1, std::min(opt.reg_bits, R)), K);

@@ -157,6 +157,11 @@ def test_qft_plan_balanced_stage_packing(lq):
     assert [s[1] for s in shape(28, True, True)] == [12, 4, 4]
     s31 = shape(31)
     assert [s[0] for s in s31] == [7, 7, 6, 11] and [s[1] for s in s31] == [4, 4, 5, 11]
+    # at equal pass counts the automatic tile size takes 12 bits when 11 would
+    # leave a strided pass on 128-byte runs (n = 27, 33), else 11 (n = 25, 31, 32)
+    assert [s[0] for s in shape(33)] == [7, 7, 7, 12] and [s[1] for s in shape(33)] == [5, 5, 5, 12]
+    assert [s[0] for s in shape(27)] == [8, 7, 12]
+    assert [s[2] for s in shape(25)] == [11] * 3 and [s[2] for s in shape(32)] == [11] * 4
     for n in range(13, 41):
         sh = shape(n)
         assert sum(s[0] for s in sh) == n and all(s[2] == sh[0][2] for s in sh)

@@ -21,6 +21,8 @@ sys.path.insert(0, %r)
 import numpy as np, torch
 from paper_2512_23183_b200 import lq
 n = int(os.environ.get("AB_N", "30"))
+if os.environ.get("AB_TILE_BITS"):   # LQ_OPT_TILE_BITS for this variant (0 = automatic)
+    lq.lq_set_option(lq.LQ_OPT_TILE_BITS, int(os.environ["AB_TILE_BITS"]))
 st = torch.cuda.current_stream()
 sv = lq.StateVector(n, stream=st)
 ts = []
